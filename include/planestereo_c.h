@@ -1,0 +1,226 @@
+/*
+ * planestereo_c.h — C ABI of the B200-native planestereo hot path.
+ *
+ * This is the drop-in boundary.  The reference (`/root/reference/proj`, a C++20
+ * static library) has no FFI; its public interface is the C++ header API in
+ * namespace `planestereo`.  Each entry point below replaces one reference
+ * function (cited file:line, relative to the reference's `proj/`), and the C++
+ * headers under `include/planestereo/` re-create that header API on top of
+ * this ABI, so a user of the reference recompiles against
+ * them unchanged.
+ *
+ * Conventions
+ *   - plain pointers and sizes; no torch or C++ types cross this boundary;
+ *   - all image-shaped buffers are row-major, stride = width, P = width*height;
+ *   - the caller owns every host buffer; a ps_ctx owns device memory, streams
+ *     and pinned staging and must not be used by two threads at once;
+ *   - every function returns a ps_status; on failure ps_last_error() holds
+ *     the message (the C++ layer rethrows the matching planestereo:: error,
+ *     include/planestereo/error.hpp).
+ */
+#ifndef PLANESTEREO_C_H
+#define PLANESTEREO_C_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Field-for-field mirror of planestereo::PipelineConfig
+ * (proj/include/planestereo/config.hpp:8-34); 44-byte POD. */
+typedef struct ps_config {
+    int iterations;           /* config.hpp:10  default 1   */
+    int max_disparity;        /* config.hpp:12  default 128 */
+    float cost_low;           /* config.hpp:14  default 0.25f */
+    float cost_high;          /* config.hpp:16  default 0.5f  */
+    int gradient_threshold;   /* config.hpp:18  default 20  */
+    int occupancy_cell_size;  /* config.hpp:20  default 32  */
+    int corner_threshold;     /* config.hpp:22  default 20  */
+    int per_bin_cap;          /* config.hpp:24  default 5   */
+    float sparse_accept_cost; /* config.hpp:26  default 0.25f */
+    float uniqueness_ratio;   /* config.hpp:28  default 0.9f  */
+    int threads;              /* config.hpp:30  default 1 (host threads; GPU ignores) */
+} ps_config;
+
+/* Mirror of planestereo::IterationStats (proj/include/planestereo/pipeline.hpp:50-58). */
+typedef struct ps_iter_stats {
+    int iteration;
+    int support_count;
+    int triangle_count;
+    int occupancy_cell_size;
+    double mean_cost;
+    int valid_count;
+    double millis;
+} ps_iter_stats;
+
+/* 1:1 with the exception classes of proj/include/planestereo/error.hpp:9-72. */
+typedef enum ps_status {
+    PS_OK = 0,
+    PS_ERROR = 1,                   /* planestereo::Error (generic)        error.hpp:9  */
+    PS_INVALID_CONFIG = 2,          /* InvalidConfig                       error.hpp:14 */
+    PS_DIMENSION_TOO_SMALL = 3,     /* DimensionTooSmall                   error.hpp:19 */
+    PS_DIMENSION_MISMATCH = 4,      /* DimensionMismatch                   error.hpp:24 */
+    PS_FEWER_THAN_THREE_POINTS = 5, /* FewerThanThreePoints                error.hpp:29 */
+    PS_DEGENERATE_TRIANGLE = 6,     /* DegenerateTriangle                  error.hpp:34 */
+    PS_SEEDING_FAILED = 7,          /* SeedingFailed                       error.hpp:39 */
+    PS_CUDA_ERROR = 8,              /* device failure (no reference analogue) */
+    PS_NO_DEVICE = 9,               /* no sm_100 device / extension not usable */
+    PS_CAPACITY = 10                /* caller buffer too small (count written) */
+} ps_status;
+
+/* Run flags. */
+#define PS_RUN_UNCHECKED_CELL 0x1u /* skip only the power-of-two cell rule of
+                                      PipelineConfig::validate (proj/src/config.cpp:27-30);
+                                      needed by BASELINE grids 10 and 6 */
+
+typedef struct ps_ctx ps_ctx;
+
+/* Called after every iteration of ps_run with host copies of the running
+ * state (mirror of planestereo::IterationObserver, pipeline.hpp:98-99). */
+typedef void (*ps_observer_fn)(int iteration, const float* final_disparity,
+                               const uint8_t* final_valid, const float* final_cost,
+                               int width, int height, void* user);
+
+/* ---------------------------------------------------------------- context */
+const char* ps_version(void);
+ps_status ps_ctx_create(int device, ps_ctx** out);
+void ps_ctx_destroy(ps_ctx* ctx);
+/* Message of the last failure on this thread (ctx may be NULL). */
+const char* ps_last_error(const ps_ctx* ctx);
+void ps_config_default(ps_config* cfg);
+/* PipelineConfig::validate (proj/src/config.cpp:17-49); flags as in ps_run. */
+ps_status ps_config_validate(const ps_config* cfg, unsigned flags);
+
+/* --------------------------------------------------------------- pipeline */
+/* planestereo::run (proj/src/pipeline.cpp:131-203) for one rectified pair.
+ * Outputs are caller-allocated P-sized arrays (any may be NULL);
+ * trace has cfg->iterations entries (may be NULL). */
+ps_status ps_run(ps_ctx* ctx, const uint8_t* left, const uint8_t* right, int width, int height,
+                 const ps_config* cfg, unsigned flags, float* disparity, uint8_t* disparity_valid,
+                 float* cost, float* dense, uint8_t* dense_valid, ps_iter_stats* trace,
+                 ps_observer_fn observer, void* user);
+
+/* Batched run over n_frames independent pairs (frames stacked, stride P).
+ * Per-frame status goes to frame_status[n_frames] (PS_SEEDING_FAILED for a
+ * frame whose seeding failed; its outputs are left untouched).  Outputs are
+ * strided by P per frame, trace by cfg->iterations per frame; any may be NULL.
+ * Returns the first non-OK frame status, or a context-level error. */
+ps_status ps_run_batch(ps_ctx* ctx, int n_frames, const uint8_t* left, const uint8_t* right,
+                       int width, int height, const ps_config* cfg, unsigned flags,
+                       float* disparity, uint8_t* disparity_valid, float* cost, float* dense,
+                       uint8_t* dense_valid, ps_iter_stats* trace, int* frame_status);
+
+/* Device-resident variant used to time the pipeline with inputs already in
+ * HBM: ps_upload_batch copies the pairs into ctx-owned device memory,
+ * ps_run_resident runs the pipeline on them (no host copies of images or
+ * outputs; only the host Delaunay exchange), ps_download_batch copies the
+ * outputs of the last resident run back. */
+ps_status ps_upload_batch(ps_ctx* ctx, int n_frames, const uint8_t* left, const uint8_t* right,
+                          int width, int height);
+ps_status ps_run_resident(ps_ctx* ctx, const ps_config* cfg, unsigned flags);
+ps_status ps_download_batch(ps_ctx* ctx, float* disparity, uint8_t* disparity_valid,
+                            float* cost, float* dense, uint8_t* dense_valid,
+                            ps_iter_stats* trace, int* frame_status);
+
+/* Support list of one frame of the last run (the list used by the last
+ * iteration; trace[i].support_count gives each iteration's prefix length). */
+ps_status ps_get_supports(ps_ctx* ctx, int frame, int* u, int* v, double* d, int capacity,
+                          int* count);
+
+/* ------------------------------------------------------- kernel telemetry */
+typedef struct ps_kernel_stat {
+    char name[32];
+    int launches;
+    double total_ms;         /* CUDA-event time summed over launches */
+    double algorithmic_bytes;/* SURVEY 8(d) bytes summed over launches */
+} ps_kernel_stat;
+/* Enables per-launch CUDA-event timing of the engine kernels (on the stream
+ * each kernel is launched on). */
+ps_status ps_set_profiling(ps_ctx* ctx, int enabled);
+ps_status ps_reset_kernel_stats(ps_ctx* ctx);
+ps_status ps_get_kernel_stats(ps_ctx* ctx, ps_kernel_stat* out, int capacity, int* count);
+/* Kernel launches issued by this context since creation. */
+long long ps_launch_count(const ps_ctx* ctx);
+
+/* ------------------------------------------------------------ stage API */
+/* gradientMask (proj/src/image.cpp:43-60): member[P] in {0,1}; count = M. */
+ps_status ps_gradient_mask(ps_ctx* ctx, const uint8_t* image, int width, int height,
+                           int threshold, uint8_t* member, int* count);
+/* censusTransform (proj/src/census.cpp:10-41). */
+ps_status ps_census(ps_ctx* ctx, const uint8_t* image, int width, int height, uint32_t* out);
+/* detectCandidates (proj/src/sparse.cpp:84-146); at most 120*per_bin_cap results. */
+ps_status ps_detect_candidates(ps_ctx* ctx, const uint8_t* image, int width, int height,
+                               const ps_config* cfg, int* u, int* v, float* score,
+                               int capacity, int* count);
+/* matchEpipolar over census fields (proj/src/sparse.cpp:148-195). */
+ps_status ps_match_epipolar(ps_ctx* ctx, const uint32_t* census_left,
+                            const uint32_t* census_right, int width, int height,
+                            const int* cand_u, const int* cand_v, int n_candidates,
+                            const ps_config* cfg, int* u, int* v, double* d, int capacity,
+                            int* count);
+/* delaunayTriangulate (proj/src/delaunay.cpp:288-325): positively oriented
+ * index triples into the input list; tris has room for 3*capacity ints. */
+ps_status ps_delaunay(const int* u, const int* v, int n, int* tris, int capacity, int* n_tris);
+/* DisparityMesh ctor (proj/src/mesh.cpp:44-123): per-triangle planes (a,b,c)
+ * and the P-sized triangle lookup (-1 outside). */
+ps_status ps_mesh_build(ps_ctx* ctx, const int* u, const int* v, const double* d, int n_points,
+                        const int* tris, int n_tris, int width, int height, double* planes,
+                        int32_t* lookup);
+/* interpolate (proj/src/mesh.cpp:149-182): mask==NULL evaluates every pixel. */
+ps_status ps_interpolate(ps_ctx* ctx, const int32_t* lookup, const double* planes, int n_tris,
+                         int width, int height, const uint8_t* mask, float max_disparity,
+                         float* value, uint8_t* valid);
+/* costEvaluation (proj/src/pipeline.cpp:33-54). */
+ps_status ps_cost_evaluation(ps_ctx* ctx, const uint32_t* census_left,
+                             const uint32_t* census_right, int width, int height,
+                             const float* interp, const uint8_t* interp_valid,
+                             const uint8_t* mask, float* cost);
+
+/* One occupancy cell (mirror of planestereo::OccupancyCell, pipeline.hpp:17-23). */
+typedef struct ps_cell {
+    int u;
+    int v;
+    float disparity;
+    float cost;
+    int occupied;
+} ps_cell;
+/* disparityRefinement (proj/src/pipeline.cpp:56-86): folds costs into the
+ * running state (in/out) and fills the two grids, each
+ * ceil(W/cell) x ceil(H/cell) cells, row-major. */
+ps_status ps_refinement(ps_ctx* ctx, const float* interp, const uint8_t* interp_valid,
+                        const float* cost, float* final_disparity, uint8_t* final_valid,
+                        float* final_cost, const uint8_t* mask, int width, int height,
+                        int cell_size, const ps_config* cfg, ps_cell* confident,
+                        ps_cell* invalid);
+/* supportResampling (proj/src/pipeline.cpp:88-129). */
+ps_status ps_support_resampling(ps_ctx* ctx, const ps_cell* confident, const ps_cell* invalid,
+                                int cell_size, const int* sup_u, const int* sup_v,
+                                const double* sup_d, int n_supports,
+                                const uint32_t* census_left, const uint32_t* census_right,
+                                int width, int height, const ps_config* cfg, int* u, int* v,
+                                double* d, int capacity, int* count);
+
+/* ------------------------------------------------- synthetic stereo pairs */
+/* Seeded BASELINE-style generator; bench/test fixture, not on
+ * the hot path.  gt may be NULL. */
+typedef struct ps_synth_params {
+    int width;
+    int height;
+    int n_planes;       /* random planar patches */
+    int max_disparity;  /* disparities lie in [0, max_disparity-1] */
+    int ground;         /* 1: bottom ground region with disparity rising with v */
+    float noise_sigma;  /* Gaussian noise added to the right view */
+    uint32_t seed;
+} ps_synth_params;
+ps_status ps_synth_pair(const ps_synth_params* params, uint8_t* left, uint8_t* right, float* gt);
+/* n_frames pairs with seeds params->seed + i, generated on `threads` host threads. */
+ps_status ps_synth_batch(const ps_synth_params* params, int n_frames, int threads, uint8_t* left,
+                         uint8_t* right);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PLANESTEREO_C_H */

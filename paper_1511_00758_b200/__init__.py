@@ -1,0 +1,425 @@
+"""paper_1511_00758_b200 — B200-native hot path of the iterative piecewise-planar
+stereo method of arXiv 1511.00758 (reference: ``planestereo``, /root/reference/proj).
+
+Python host mirror of the reference's C++ API, over the C ABI of
+``libplanestereo_b200.so`` (sm_100a kernels + C++ engine):
+
+    PipelineConfig        planestereo::PipelineConfig   (config.hpp:8-34)
+    Context.run           planestereo::run              (pipeline.cpp:131-203)
+    Context.run_batch     batched run over many frames on one GPU
+    Context.<stage>       the public stage functions (gradientMask, censusTransform,
+                          detectCandidates, matchEpipolar, mesh, interpolate,
+                          costEvaluation)
+    delaunay_triangulate  planestereo::delaunayTriangulate (delaunay.cpp:288-325)
+
+Errors are raised as the Python mirror of the reference's exception classes
+(error.hpp:9-72).  Nothing here falls back to a CPU implementation.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field, fields
+from typing import Callable, List, Optional
+
+import numpy as np
+
+from . import _native
+from ._native import PsConfig, PsIterStats
+
+PS_RUN_UNCHECKED_CELL = 0x1
+
+
+# ---------------------------------------------------------------- errors (error.hpp)
+class Error(RuntimeError):
+    """planestereo::Error"""
+
+
+class InvalidConfig(Error):
+    pass
+
+
+class DimensionTooSmall(Error):
+    pass
+
+
+class DimensionMismatch(Error):
+    pass
+
+
+class FewerThanThreePoints(Error):
+    pass
+
+
+class DegenerateTriangle(Error):
+    pass
+
+
+class SeedingFailed(Error):
+    pass
+
+
+class CudaError(Error):
+    pass
+
+
+class NoDevice(Error):
+    pass
+
+
+_STATUS = {
+    1: Error, 2: InvalidConfig, 3: DimensionTooSmall, 4: DimensionMismatch,
+    5: FewerThanThreePoints, 6: DegenerateTriangle, 7: SeedingFailed, 8: CudaError,
+    9: NoDevice, 10: Error,
+}
+
+
+def _check(status: int) -> None:
+    if status != 0:
+        msg = _native.load().ps_last_error(None)
+        raise _STATUS.get(status, Error)(msg.decode() if msg else f"status {status}")
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+# ---------------------------------------------------------------- config
+@dataclass
+class PipelineConfig:
+    """planestereo::PipelineConfig, same field names and defaults (config.hpp:10-30)."""
+
+    iterations: int = 1
+    maxDisparity: int = 128
+    costLow: float = 0.25
+    costHigh: float = 0.5
+    gradientThreshold: int = 20
+    occupancyCellSize: int = 32
+    cornerThreshold: int = 20
+    perBinCap: int = 5
+    sparseAcceptCost: float = 0.25
+    uniquenessRatio: float = 0.9
+    threads: int = 1
+
+    def to_c(self) -> PsConfig:
+        return PsConfig(self.iterations, self.maxDisparity, self.costLow, self.costHigh,
+                        self.gradientThreshold, self.occupancyCellSize, self.cornerThreshold,
+                        self.perBinCap, self.sparseAcceptCost, self.uniquenessRatio, self.threads)
+
+    def validate(self, unchecked_cell: bool = False) -> None:
+        """PipelineConfig::validate (config.cpp:17-49); raises InvalidConfig."""
+        c = self.to_c()
+        _check(_native.load().ps_config_validate(C.byref(c), PS_RUN_UNCHECKED_CELL if unchecked_cell else 0))
+
+
+@dataclass
+class IterationStats:
+    iteration: int
+    supportCount: int
+    triangleCount: int
+    occupancyCellSize: int
+    meanCost: float
+    validCount: int
+    millis: float
+
+
+@dataclass
+class StereoResult:
+    """planestereo::StereoResult (pipeline.hpp:62-67) as numpy arrays (H x W)."""
+
+    disparity: np.ndarray
+    disparity_valid: np.ndarray
+    costs: np.ndarray
+    dense: np.ndarray
+    dense_valid: np.ndarray
+    trace: List[IterationStats] = field(default_factory=list)
+
+
+def _stats(s: PsIterStats) -> IterationStats:
+    return IterationStats(s.iteration, s.support_count, s.triangle_count, s.occupancy_cell_size,
+                          s.mean_cost, s.valid_count, s.millis)
+
+
+def _u8(img) -> np.ndarray:
+    a = np.ascontiguousarray(img, dtype=np.uint8)
+    if a.ndim != 2:
+        raise DimensionMismatch("expected a 2-D uint8 image")
+    return a
+
+
+class Context:
+    """One GPU context (ps_ctx): device memory, a stream, host worker pool."""
+
+    def __init__(self, device: int = 0):
+        self._lib = _native.load()
+        h = C.c_void_p()
+        _check(self._lib.ps_ctx_create(device, C.byref(h)))
+        self._h = h
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            self._lib.ps_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # ------------------------------------------------------------ pipeline
+    def run(self, left, right, config: PipelineConfig, unchecked_cell: bool = False,
+            observer: Optional[Callable] = None) -> StereoResult:
+        """planestereo::run.  observer(iteration, final_disparity, final_valid, final_cost)."""
+        L, R = _u8(left), _u8(right)
+        if L.shape != R.shape:
+            config.validate(unchecked_cell)  # InvalidConfig takes precedence (pipeline.cpp:133-136)
+            raise DimensionMismatch("stereo pair dimensions differ")
+        h, w = L.shape
+        cfg = config.to_c()
+        out = StereoResult(np.zeros((h, w), np.float32), np.zeros((h, w), np.uint8),
+                           np.zeros((h, w), np.float32), np.zeros((h, w), np.float32),
+                           np.zeros((h, w), np.uint8))
+        trace = (PsIterStats * max(1, config.iterations))()
+        cb = _native.OBSERVER(0)
+        if observer is not None:
+            def _obs(it, fd, fv, fc, ww, hh, user):
+                n = ww * hh
+                d = np.ctypeslib.as_array((C.c_float * n).from_address(fd)).reshape(hh, ww).copy()
+                v = np.ctypeslib.as_array((C.c_uint8 * n).from_address(fv)).reshape(hh, ww).copy()
+                c = np.ctypeslib.as_array((C.c_float * n).from_address(fc)).reshape(hh, ww).copy()
+                observer(it, d, v, c)
+            cb = _native.OBSERVER(_obs)
+        flags = PS_RUN_UNCHECKED_CELL if unchecked_cell else 0
+        _check(self._lib.ps_run(self._h, _ptr(L), _ptr(R), w, h, C.byref(cfg), flags,
+                                _ptr(out.disparity), _ptr(out.disparity_valid), _ptr(out.costs),
+                                _ptr(out.dense), _ptr(out.dense_valid), trace, cb, None))
+        out.trace = [_stats(trace[i]) for i in range(config.iterations)]
+        return out
+
+    def run_batch(self, left: np.ndarray, right: np.ndarray, config: PipelineConfig,
+                  unchecked_cell: bool = False, raise_on_failure: bool = True) -> dict:
+        """Batched run over frames stacked as (F, H, W) uint8 arrays."""
+        L = np.ascontiguousarray(left, dtype=np.uint8)
+        R = np.ascontiguousarray(right, dtype=np.uint8)
+        if L.ndim != 3 or L.shape != R.shape:
+            raise DimensionMismatch("expected two (F, H, W) uint8 stacks of equal shape")
+        n, h, w = L.shape
+        cfg = config.to_c()
+        res = {
+            "disparity": np.zeros((n, h, w), np.float32),
+            "disparity_valid": np.zeros((n, h, w), np.uint8),
+            "costs": np.zeros((n, h, w), np.float32),
+            "dense": np.zeros((n, h, w), np.float32),
+            "dense_valid": np.zeros((n, h, w), np.uint8),
+            "status": np.zeros(n, np.int32),
+        }
+        trace = (PsIterStats * (n * config.iterations))()
+        st = self._lib.ps_run_batch(self._h, n, _ptr(L), _ptr(R), w, h, C.byref(cfg),
+                                    PS_RUN_UNCHECKED_CELL if unchecked_cell else 0,
+                                    _ptr(res["disparity"]), _ptr(res["disparity_valid"]),
+                                    _ptr(res["costs"]), _ptr(res["dense"]),
+                                    _ptr(res["dense_valid"]), trace, _ptr(res["status"]))
+        if st != 0 and (raise_on_failure or st != 7):
+            _check(st)
+        res["trace"] = [[_stats(trace[f * config.iterations + i]) for i in range(config.iterations)]
+                        for f in range(n)]
+        return res
+
+    def upload(self, left: np.ndarray, right: np.ndarray) -> None:
+        n, h, w = left.shape
+        _check(self._lib.ps_upload_batch(self._h, n, _ptr(left), _ptr(right), w, h))
+
+    def upload_ptr(self, n: int, left_ptr: int, right_ptr: int, w: int, h: int) -> None:
+        _check(self._lib.ps_upload_batch(self._h, n, C.c_void_p(left_ptr), C.c_void_p(right_ptr), w, h))
+
+    def run_resident(self, config: PipelineConfig, unchecked_cell: bool = False) -> int:
+        cfg = config.to_c()
+        return self._lib.ps_run_resident(self._h, C.byref(cfg),
+                                         PS_RUN_UNCHECKED_CELL if unchecked_cell else 0)
+
+    def download_ptr(self, disparity=0, disparity_valid=0, costs=0, dense=0, dense_valid=0) -> None:
+        p = lambda x: C.c_void_p(x) if x else None
+        _check(self._lib.ps_download_batch(self._h, p(disparity), p(disparity_valid), p(costs),
+                                           p(dense), p(dense_valid), None, None))
+
+    def supports(self, frame: int = 0):
+        n = C.c_int()
+        self._lib.ps_get_supports(self._h, frame, None, None, None, 0, C.byref(n))
+        u = np.zeros(n.value, np.int32)
+        v = np.zeros(n.value, np.int32)
+        d = np.zeros(n.value, np.float64)
+        _check(self._lib.ps_get_supports(self._h, frame, _ptr(u), _ptr(v), _ptr(d), n.value, C.byref(n)))
+        return u, v, d
+
+    def set_profiling(self, on: bool) -> None:
+        _check(self._lib.ps_set_profiling(self._h, 1 if on else 0))
+
+    def reset_kernel_stats(self) -> None:
+        _check(self._lib.ps_reset_kernel_stats(self._h))
+
+    def kernel_stats(self) -> dict:
+        arr = (_native.PsKernelStat * 64)()
+        n = C.c_int()
+        _check(self._lib.ps_get_kernel_stats(self._h, arr, 64, C.byref(n)))
+        return {arr[i].name.decode(): {"launches": arr[i].launches, "ms": arr[i].total_ms,
+                                       "bytes": arr[i].algorithmic_bytes}
+                for i in range(min(64, n.value))}
+
+    def launch_count(self) -> int:
+        return int(self._lib.ps_launch_count(self._h))
+
+    # ------------------------------------------------------------ stages
+    def gradient_mask(self, image, threshold: int):
+        img = _u8(image)
+        h, w = img.shape
+        m = np.zeros((h, w), np.uint8)
+        n = C.c_int()
+        _check(self._lib.ps_gradient_mask(self._h, _ptr(img), w, h, threshold, _ptr(m), C.byref(n)))
+        return m, n.value
+
+    def census(self, image) -> np.ndarray:
+        img = _u8(image)
+        h, w = img.shape
+        out = np.zeros((h, w), np.uint32)
+        _check(self._lib.ps_census(self._h, _ptr(img), w, h, _ptr(out)))
+        return out
+
+    def detect_candidates(self, image, config: PipelineConfig):
+        img = _u8(image)
+        h, w = img.shape
+        cap = 120 * config.perBinCap
+        u = np.zeros(cap, np.int32)
+        v = np.zeros(cap, np.int32)
+        s = np.zeros(cap, np.float32)
+        n = C.c_int()
+        cfg = config.to_c()
+        _check(self._lib.ps_detect_candidates(self._h, _ptr(img), w, h, C.byref(cfg), _ptr(u),
+                                              _ptr(v), _ptr(s), cap, C.byref(n)))
+        return u[:n.value], v[:n.value], s[:n.value]
+
+    def match_epipolar(self, census_left, census_right, cand_u, cand_v, config: PipelineConfig):
+        cl = np.ascontiguousarray(census_left, dtype=np.uint32)
+        cr = np.ascontiguousarray(census_right, dtype=np.uint32)
+        h, w = cl.shape
+        cu = np.ascontiguousarray(cand_u, dtype=np.int32)
+        cv = np.ascontiguousarray(cand_v, dtype=np.int32)
+        n = len(cu)
+        u = np.zeros(max(1, n), np.int32)
+        v = np.zeros(max(1, n), np.int32)
+        d = np.zeros(max(1, n), np.float64)
+        cnt = C.c_int()
+        cfg = config.to_c()
+        _check(self._lib.ps_match_epipolar(self._h, _ptr(cl), _ptr(cr), w, h, _ptr(cu), _ptr(cv), n,
+                                           C.byref(cfg), _ptr(u), _ptr(v), _ptr(d), max(1, n),
+                                           C.byref(cnt)))
+        k = cnt.value
+        return u[:k], v[:k], d[:k]
+
+    def mesh_build(self, u, v, d, tris, width: int, height: int):
+        u = np.ascontiguousarray(u, dtype=np.int32)
+        v = np.ascontiguousarray(v, dtype=np.int32)
+        d = np.ascontiguousarray(d, dtype=np.float64)
+        t = np.ascontiguousarray(tris, dtype=np.int32).reshape(-1, 3)
+        planes = np.zeros((max(1, len(t)), 3), np.float64)
+        lookup = np.zeros((height, width), np.int32)
+        _check(self._lib.ps_mesh_build(self._h, _ptr(u), _ptr(v), _ptr(d), len(u), _ptr(t), len(t),
+                                       width, height, _ptr(planes), _ptr(lookup)))
+        return planes[:len(t)], lookup
+
+    def interpolate(self, lookup, planes, max_disparity: float, mask=None):
+        lk = np.ascontiguousarray(lookup, dtype=np.int32)
+        pl = np.ascontiguousarray(planes, dtype=np.float64).reshape(-1, 3)
+        h, w = lk.shape
+        m = None if mask is None else np.ascontiguousarray(mask, dtype=np.uint8)
+        val = np.zeros((h, w), np.float32)
+        ok = np.zeros((h, w), np.uint8)
+        _check(self._lib.ps_interpolate(self._h, _ptr(lk), _ptr(pl), len(pl), w, h, _ptr(m),
+                                        C.c_float(max_disparity), _ptr(val), _ptr(ok)))
+        return val, ok
+
+    def cost_evaluation(self, census_left, census_right, interp, interp_valid, mask):
+        cl = np.ascontiguousarray(census_left, dtype=np.uint32)
+        cr = np.ascontiguousarray(census_right, dtype=np.uint32)
+        h, w = cl.shape
+        iv = np.ascontiguousarray(interp, dtype=np.float32)
+        ok = np.ascontiguousarray(interp_valid, dtype=np.uint8)
+        m = np.ascontiguousarray(mask, dtype=np.uint8)
+        cost = np.zeros((h, w), np.float32)
+        _check(self._lib.ps_cost_evaluation(self._h, _ptr(cl), _ptr(cr), w, h, _ptr(iv), _ptr(ok),
+                                            _ptr(m), _ptr(cost)))
+        return cost
+
+
+def delaunay_triangulate(u, v) -> np.ndarray:
+    """planestereo::delaunayTriangulate: (T, 3) index triples (host C++, exact)."""
+    lib = _native.load()
+    u = np.ascontiguousarray(u, dtype=np.int32)
+    v = np.ascontiguousarray(v, dtype=np.int32)
+    n = len(u)
+    cap = max(1, 2 * n)
+    tris = np.zeros((cap, 3), np.int32)
+    nt = C.c_int()
+    _check(lib.ps_delaunay(_ptr(u), _ptr(v), n, _ptr(tris), cap, C.byref(nt)))
+    return tris[:nt.value]
+
+
+def synth_pair(width: int, height: int, n_planes: int, max_disparity: int, ground: bool = False,
+               noise_sigma: float = 2.0, seed: int = 0, with_gt: bool = False):
+    """Seeded BASELINE-style stereo pair; returns (left, right[, gt])."""
+    lib = _native.load()
+    p = _native.PsSynthParams(width, height, n_planes, max_disparity, 1 if ground else 0,
+                              noise_sigma, seed)
+    L = np.zeros((height, width), np.uint8)
+    R = np.zeros((height, width), np.uint8)
+    gt = np.zeros((height, width), np.float32) if with_gt else None
+    _check(lib.ps_synth_pair(C.byref(p), _ptr(L), _ptr(R), _ptr(gt)))
+    return (L, R, gt) if with_gt else (L, R)
+
+
+def synth_batch(n_frames: int, width: int, height: int, n_planes: int, max_disparity: int,
+                ground: bool = False, noise_sigma: float = 2.0, seed: int = 0, threads: int = 8,
+                left: Optional[np.ndarray] = None, right: Optional[np.ndarray] = None):
+    """n_frames pairs with seeds seed+i, generated on host threads."""
+    lib = _native.load()
+    p = _native.PsSynthParams(width, height, n_planes, max_disparity, 1 if ground else 0,
+                              noise_sigma, seed)
+    L = left if left is not None else np.zeros((n_frames, height, width), np.uint8)
+    R = right if right is not None else np.zeros((n_frames, height, width), np.uint8)
+    _check(lib.ps_synth_batch(C.byref(p), n_frames, threads, _ptr(L), _ptr(R)))
+    return L, R
+
+
+# BASELINE.json configs.  grid 10 and 6 need the
+# unchecked-cell opt-in (they fail the power-of-two rule of validate()).
+BASELINE_CONFIGS = {
+    0: dict(width=640, height=480, frames=1, n_planes=12, max_disparity=64, ground=False,
+            sigma=2.0, iterations=2, cell=10),
+    1: dict(width=1242, height=375, frames=1, n_planes=24, max_disparity=128, ground=True,
+            sigma=2.0, iterations=4, cell=8),
+    2: dict(width=640, height=480, frames=256, n_planes=12, max_disparity=64, ground=False,
+            sigma=2.0, iterations=3, cell=10),
+    3: dict(width=1920, height=1080, frames=1, n_planes=40, max_disparity=256, ground=False,
+            sigma=4.0, iterations=4, cell=8),
+    4: dict(width=3840, height=2160, frames=64, n_planes=60, max_disparity=256, ground=False,
+            sigma=2.0, iterations=6, cell=6),
+}
+
+
+def baseline_config(idx: int) -> PipelineConfig:
+    c = BASELINE_CONFIGS[idx]
+    return PipelineConfig(iterations=c["iterations"], maxDisparity=c["max_disparity"],
+                          occupancyCellSize=c["cell"])
+
+
+__all__ = [
+    "Error", "InvalidConfig", "DimensionTooSmall", "DimensionMismatch", "FewerThanThreePoints",
+    "DegenerateTriangle", "SeedingFailed", "CudaError", "NoDevice", "PipelineConfig",
+    "IterationStats", "StereoResult", "Context", "delaunay_triangulate", "synth_pair",
+    "synth_batch", "BASELINE_CONFIGS", "baseline_config", "PS_RUN_UNCHECKED_CELL",
+]

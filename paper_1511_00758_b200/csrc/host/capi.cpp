@@ -1,0 +1,463 @@
+// capi.cpp — the extern "C" boundary declared in include/planestereo_c.h.
+//
+// Pipeline entry points run the batched Engine; stage entry points run the
+// same sm_100a kernels on one frame.  Nothing here computes a per-pixel or
+// per-candidate result on the host: the only host computation is the
+// Delaunay triangulation (by design, delaunay.hpp), the reference's
+// per-pixel dedup of a user-supplied candidate list (sparse.cpp:183-192) and
+// argument checking.
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../kernels/launch.hpp"
+#include "engine.hpp"
+#include "planestereo_c.h"
+
+namespace ps {
+ps_status validate_config(const ps_config& c, unsigned flags, std::string& msg);
+CostTables make_tables(const ps_config& c);
+}  // namespace ps
+
+struct ps_ctx {
+    ps::Engine* engine = nullptr;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+ps_status set_error(ps_status s, const std::string& msg) {
+    g_last_error = msg;
+    return s;
+}
+
+ps_status from_engine(ps_ctx* ctx, ps_status s) {
+    if (s != PS_OK) g_last_error = ctx->engine->error();
+    return s;
+}
+
+bool device_ok(int device, std::string& why) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n <= device || device < 0) {
+        why = std::string("no CUDA device ") + std::to_string(device) + " (" +
+              (e == cudaSuccess ? "not present" : cudaGetErrorString(e)) + ")";
+        return false;
+    }
+    cudaDeviceProp p{};
+    cudaGetDeviceProperties(&p, device);
+    if (p.major != 10) {
+        why = std::string("device ") + p.name + " is not sm_100 (this build targets sm_100a only)";
+        return false;
+    }
+    return true;
+}
+
+#define PS_REQUIRE_CTX(ctx)                                               \
+    do {                                                                  \
+        if (!(ctx) || !(ctx)->engine) return set_error(PS_ERROR, "null context"); \
+    } while (0)
+
+}  // namespace
+
+extern "C" {
+
+const char* ps_version(void) { return "planestereo-b200 0.1 (sm_100a)"; }
+
+ps_status ps_ctx_create(int device, ps_ctx** out) {
+    if (!out) return set_error(PS_ERROR, "null output pointer");
+    *out = nullptr;
+    std::string why;
+    if (!device_ok(device, why)) return set_error(PS_NO_DEVICE, why);
+    ps_ctx* c = new ps_ctx;
+    c->engine = new ps::Engine(device);
+    *out = c;
+    return PS_OK;
+}
+
+void ps_ctx_destroy(ps_ctx* ctx) {
+    if (!ctx) return;
+    delete ctx->engine;
+    delete ctx;
+}
+
+const char* ps_last_error(const ps_ctx*) { return g_last_error.c_str(); }
+
+void ps_config_default(ps_config* c) {
+    // PipelineConfig defaults, proj/include/planestereo/config.hpp:10-30.
+    c->iterations = 1;
+    c->max_disparity = 128;
+    c->cost_low = 0.25f;
+    c->cost_high = 0.5f;
+    c->gradient_threshold = 20;
+    c->occupancy_cell_size = 32;
+    c->corner_threshold = 20;
+    c->per_bin_cap = 5;
+    c->sparse_accept_cost = 0.25f;
+    c->uniqueness_ratio = 0.9f;
+    c->threads = 1;
+}
+
+ps_status ps_config_validate(const ps_config* cfg, unsigned flags) {
+    if (!cfg) return set_error(PS_ERROR, "null config");
+    std::string msg;
+    ps_status s = ps::validate_config(*cfg, flags, msg);
+    if (s != PS_OK) g_last_error = msg;
+    return s;
+}
+
+ps_status ps_upload_batch(ps_ctx* ctx, int n_frames, const uint8_t* left, const uint8_t* right,
+                          int width, int height) {
+    PS_REQUIRE_CTX(ctx);
+    if (!left || !right) return set_error(PS_ERROR, "null image");
+    return from_engine(ctx, ctx->engine->upload(n_frames, left, right, width, height));
+}
+
+ps_status ps_run_resident(ps_ctx* ctx, const ps_config* cfg, unsigned flags) {
+    PS_REQUIRE_CTX(ctx);
+    if (!cfg) return set_error(PS_ERROR, "null config");
+    return from_engine(ctx, ctx->engine->run_resident(*cfg, flags));
+}
+
+ps_status ps_download_batch(ps_ctx* ctx, float* disparity, uint8_t* disparity_valid, float* cost,
+                            float* dense, uint8_t* dense_valid, ps_iter_stats* trace,
+                            int* frame_status) {
+    PS_REQUIRE_CTX(ctx);
+    return from_engine(ctx, ctx->engine->download(disparity, disparity_valid, cost, dense,
+                                                  dense_valid, trace, frame_status));
+}
+
+ps_status ps_run_batch(ps_ctx* ctx, int n_frames, const uint8_t* left, const uint8_t* right,
+                       int width, int height, const ps_config* cfg, unsigned flags,
+                       float* disparity, uint8_t* disparity_valid, float* cost, float* dense,
+                       uint8_t* dense_valid, ps_iter_stats* trace, int* frame_status) {
+    PS_REQUIRE_CTX(ctx);
+    if (!cfg) return set_error(PS_ERROR, "null config");
+    // run() checks the config before anything else (pipeline.cpp:133)
+    ps_status s = ps_config_validate(cfg, flags);
+    if (s != PS_OK) return s;
+    s = ps_upload_batch(ctx, n_frames, left, right, width, height);
+    if (s != PS_OK) return s;
+    const ps_status run = ctx->engine->run_resident(*cfg, flags);
+    if (run != PS_OK && run != PS_SEEDING_FAILED) return from_engine(ctx, run);
+    s = from_engine(ctx, ctx->engine->download(disparity, disparity_valid, cost, dense,
+                                               dense_valid, trace, frame_status));
+    if (s != PS_OK) return s;
+    if (run != PS_OK) g_last_error = ctx->engine->error();
+    return run;
+}
+
+ps_status ps_run(ps_ctx* ctx, const uint8_t* left, const uint8_t* right, int width, int height,
+                 const ps_config* cfg, unsigned flags, float* disparity, uint8_t* disparity_valid,
+                 float* cost, float* dense, uint8_t* dense_valid, ps_iter_stats* trace,
+                 ps_observer_fn observer, void* user) {
+    PS_REQUIRE_CTX(ctx);
+    if (!cfg) return set_error(PS_ERROR, "null config");
+    ps_status s = ps_config_validate(cfg, flags);
+    if (s != PS_OK) return s;
+    s = ps_upload_batch(ctx, 1, left, right, width, height);
+    if (s != PS_OK) return s;
+    s = from_engine(ctx, ctx->engine->run_resident(*cfg, flags, observer, user));
+    if (s != PS_OK) return s;
+    return from_engine(ctx, ctx->engine->download(disparity, disparity_valid, cost, dense,
+                                                  dense_valid, trace, nullptr));
+}
+
+ps_status ps_get_supports(ps_ctx* ctx, int frame, int* u, int* v, double* d, int capacity,
+                          int* count) {
+    PS_REQUIRE_CTX(ctx);
+    return from_engine(ctx, ctx->engine->supports(frame, u, v, d, capacity, count));
+}
+
+ps_status ps_set_profiling(ps_ctx* ctx, int enabled) {
+    PS_REQUIRE_CTX(ctx);
+    ctx->engine->set_profiling(enabled != 0);
+    return PS_OK;
+}
+
+ps_status ps_reset_kernel_stats(ps_ctx* ctx) {
+    PS_REQUIRE_CTX(ctx);
+    ctx->engine->reset_stats();
+    return PS_OK;
+}
+
+ps_status ps_get_kernel_stats(ps_ctx* ctx, ps_kernel_stat* out, int capacity, int* count) {
+    PS_REQUIRE_CTX(ctx);
+    const auto& st = ctx->engine->stats();
+    if (count) *count = int(st.size());
+    for (int i = 0; i < int(st.size()) && i < capacity; ++i) {
+        std::memset(out[i].name, 0, sizeof(out[i].name));
+        std::strncpy(out[i].name, st[i].name.c_str(), sizeof(out[i].name) - 1);
+        out[i].launches = st[i].launches;
+        out[i].total_ms = st[i].ms;
+        out[i].algorithmic_bytes = st[i].bytes;
+    }
+    return PS_OK;
+}
+
+long long ps_launch_count(const ps_ctx* ctx) {
+    return (ctx && ctx->engine) ? ctx->engine->launches() : 0;
+}
+
+// ------------------------------------------------------------------ stages
+
+ps_status ps_gradient_mask(ps_ctx* ctx, const uint8_t* image, int width, int height,
+                           int threshold, uint8_t* member, int* count) {
+    PS_REQUIRE_CTX(ctx);
+    ps::Engine& e = *ctx->engine;
+    const long long P = (long long)width * height;
+    uint8_t* d_img = e.dev<uint8_t>(e.s_a, P);
+    uint8_t* d_mask = e.dev<uint8_t>(e.s_b, P);
+    int* d_cnt = e.dev<int>(e.s_c, 1);
+    if (!d_img || !d_mask || !d_cnt) return set_error(PS_CUDA_ERROR, "allocation failed");
+    cudaMemcpyAsync(d_img, image, P, cudaMemcpyHostToDevice, e.stream());
+    cudaMemsetAsync(d_cnt, 0, sizeof(int), e.stream());
+    e.count_launches(ps::launch_frontend(d_img, nullptr, {width, height, P}, 1, threshold, d_mask,
+                                         nullptr, nullptr, d_cnt, e.stream()));
+    if (member) cudaMemcpyAsync(member, d_mask, P, cudaMemcpyDeviceToHost, e.stream());
+    int c = 0;
+    cudaMemcpyAsync(&c, d_cnt, sizeof(int), cudaMemcpyDeviceToHost, e.stream());
+    ps_status s = from_engine(ctx, e.sync("gradient mask"));
+    if (count) *count = c;
+    return s;
+}
+
+ps_status ps_census(ps_ctx* ctx, const uint8_t* image, int width, int height, uint32_t* out) {
+    PS_REQUIRE_CTX(ctx);
+    ps::Engine& e = *ctx->engine;
+    const long long P = (long long)width * height;
+    uint8_t* d_img = e.dev<uint8_t>(e.s_a, P);
+    uint32_t* d_c = e.dev<uint32_t>(e.s_b, P);
+    if (!d_img || !d_c) return set_error(PS_CUDA_ERROR, "allocation failed");
+    cudaMemcpyAsync(d_img, image, P, cudaMemcpyHostToDevice, e.stream());
+    e.count_launches(ps::launch_frontend(d_img, nullptr, {width, height, P}, 1, 0, nullptr, d_c,
+                                         nullptr, nullptr, e.stream()));
+    cudaMemcpyAsync(out, d_c, sizeof(uint32_t) * P, cudaMemcpyDeviceToHost, e.stream());
+    return from_engine(ctx, e.sync("census"));
+}
+
+ps_status ps_detect_candidates(ps_ctx* ctx, const uint8_t* image, int width, int height,
+                               const ps_config* cfg, int* u, int* v, float* score, int capacity,
+                               int* count) {
+    PS_REQUIRE_CTX(ctx);
+    if (!cfg || cfg->per_bin_cap < 1) return set_error(PS_INVALID_CONFIG, "per-bin cap must be >= 1");
+    ps::Engine& e = *ctx->engine;
+    const long long P = (long long)width * height;
+    const ps::FrameGeom g{width, height, P};
+    const int cap = cfg->per_bin_cap;
+    const int stride = 120 * cap;
+    int n_pow2 = 1;
+    while (n_pow2 < std::min<long long>(stride, P)) n_pow2 <<= 1;
+    const long long scs = ps::candidate_scratch_stride(g);
+    uint8_t* d_img = e.dev<uint8_t>(e.s_a, P);
+    unsigned long long* d_keys = e.dev<unsigned long long>(e.s_b, size_t(stride));
+    int* d_bc = e.dev<int>(e.s_c, 120);
+    unsigned long long* d_sc = e.dev<unsigned long long>(e.s_d, cap > 8 ? std::max<long long>(120 * scs, n_pow2) : 1);
+    int* d_u = e.dev<int>(e.s_e, stride);
+    int* d_v = e.dev<int>(e.s_f, stride);
+    float* d_s = e.dev<float>(e.s_g, stride);
+    int* d_n = e.dev<int>(e.s_h, 1);
+    if (!d_img || !d_keys || !d_bc || !d_sc || !d_u || !d_v || !d_s || !d_n)
+        return set_error(PS_CUDA_ERROR, "allocation failed");
+    cudaMemcpyAsync(d_img, image, P, cudaMemcpyHostToDevice, e.stream());
+    e.count_launches(ps::launch_candidates(d_img, g, 1, cfg->corner_threshold, cap, d_keys, d_bc,
+                                           d_sc, scs, d_u, d_v, d_s, d_n, stride, e.stream()));
+    int n = 0;
+    cudaMemcpyAsync(&n, d_n, sizeof(int), cudaMemcpyDeviceToHost, e.stream());
+    ps_status s = from_engine(ctx, e.sync("candidates"));
+    if (s != PS_OK) return s;
+    if (count) *count = n;
+    const int m = std::min(n, capacity);
+    if (u) cudaMemcpy(u, d_u, sizeof(int) * m, cudaMemcpyDeviceToHost);
+    if (v) cudaMemcpy(v, d_v, sizeof(int) * m, cudaMemcpyDeviceToHost);
+    if (score) cudaMemcpy(score, d_s, sizeof(float) * m, cudaMemcpyDeviceToHost);
+    if (n > capacity) return set_error(PS_CAPACITY, "candidate buffer too small");
+    return from_engine(ctx, e.sync("candidates D2H"));
+}
+
+ps_status ps_match_epipolar(ps_ctx* ctx, const uint32_t* census_left, const uint32_t* census_right,
+                            int width, int height, const int* cand_u, const int* cand_v,
+                            int n_candidates, const ps_config* cfg, int* u, int* v, double* d,
+                            int capacity, int* count) {
+    PS_REQUIRE_CTX(ctx);
+    if (!cfg) return set_error(PS_ERROR, "null config");
+    ps::Engine& e = *ctx->engine;
+    const long long P = (long long)width * height;
+    const ps::FrameGeom g{width, height, P};
+    const int n = std::max(0, n_candidates);
+    uint32_t* d_cl = e.dev<uint32_t>(e.s_a, P);
+    uint32_t* d_cr = e.dev<uint32_t>(e.s_b, P);
+    int* d_u = e.dev<int>(e.s_c, std::max(1, n));
+    int* d_v = e.dev<int>(e.s_d, std::max(1, n));
+    int* d_n = e.dev<int>(e.s_e, 1);
+    uint8_t* d_ok = e.dev<uint8_t>(e.s_f, std::max(1, n));
+    int* d_disp = e.dev<int>(e.s_g, std::max(1, n));
+    int* d_k = e.dev<int>(e.s_h, std::max(1, n));
+    if (!d_cl || !d_cr || !d_u || !d_v || !d_n || !d_ok || !d_disp || !d_k)
+        return set_error(PS_CUDA_ERROR, "allocation failed");
+    cudaMemcpyAsync(d_cl, census_left, sizeof(uint32_t) * P, cudaMemcpyHostToDevice, e.stream());
+    cudaMemcpyAsync(d_cr, census_right, sizeof(uint32_t) * P, cudaMemcpyHostToDevice, e.stream());
+    if (n > 0) {
+        cudaMemcpyAsync(d_u, cand_u, sizeof(int) * n, cudaMemcpyHostToDevice, e.stream());
+        cudaMemcpyAsync(d_v, cand_v, sizeof(int) * n, cudaMemcpyHostToDevice, e.stream());
+    }
+    cudaMemcpyAsync(d_n, &n, sizeof(int), cudaMemcpyHostToDevice, e.stream());
+    const ps::CostTables tab = ps::make_tables(*cfg);
+    e.count_launches(ps::launch_match(d_cl, d_cr, g, 1, cfg->max_disparity, tab, d_u, d_v, d_n, n,
+                                      n, d_ok, d_disp, d_k, e.stream()));
+    std::vector<uint8_t> ok(n);
+    std::vector<int> disp(n), kk(n);
+    if (n > 0) {
+        cudaMemcpyAsync(ok.data(), d_ok, n, cudaMemcpyDeviceToHost, e.stream());
+        cudaMemcpyAsync(disp.data(), d_disp, sizeof(int) * n, cudaMemcpyDeviceToHost, e.stream());
+        cudaMemcpyAsync(kk.data(), d_k, sizeof(int) * n, cudaMemcpyDeviceToHost, e.stream());
+    }
+    ps_status s = from_engine(ctx, e.sync("match"));
+    if (s != PS_OK) return s;
+    // Per-pixel dedup in candidate order, lower cost wins (sparse.cpp:183-192).
+    std::unordered_map<long long, int> by_pixel;
+    std::vector<int> ou, ov, od, ok_k;
+    for (int i = 0; i < n; ++i) {
+        if (!ok[i]) continue;
+        const long long key = (long long)cand_v[i] * width + cand_u[i];
+        auto it = by_pixel.find(key);
+        if (it == by_pixel.end()) {
+            by_pixel.emplace(key, int(ou.size()));
+            ou.push_back(cand_u[i]);
+            ov.push_back(cand_v[i]);
+            od.push_back(disp[i]);
+            ok_k.push_back(kk[i]);
+        } else if (kk[i] < ok_k[it->second]) {
+            od[it->second] = disp[i];
+            ok_k[it->second] = kk[i];
+        }
+    }
+    const int m = int(ou.size());
+    if (count) *count = m;
+    for (int i = 0; i < m && i < capacity; ++i) {
+        if (u) u[i] = ou[i];
+        if (v) v[i] = ov[i];
+        if (d) d[i] = double(od[i]);
+    }
+    if (m > capacity) return set_error(PS_CAPACITY, "support buffer too small");
+    return PS_OK;
+}
+
+ps_status ps_delaunay(const int* u, const int* v, int n, int* tris, int capacity, int* n_tris) {
+    static thread_local ps::DelaunayWorkspace ws;
+    std::vector<int> out;
+    const int t = ps::delaunay(u, v, n, out, ws);
+    if (t == -1) return set_error(PS_ERROR, "triangulation coordinates must be below 2^20");
+    if (t < 0) return set_error(PS_ERROR, "triangulation invariant violated: no hull edge visible");
+    if (n_tris) *n_tris = t;
+    if (t > capacity) return set_error(PS_CAPACITY, "triangle buffer too small");
+    if (tris && t > 0) std::memcpy(tris, out.data(), sizeof(int) * 3 * t);
+    return PS_OK;
+}
+
+ps_status ps_mesh_build(ps_ctx* ctx, const int* u, const int* v, const double* d, int n_points,
+                        const int* tris, int n_tris, int width, int height, double* planes,
+                        int32_t* lookup) {
+    PS_REQUIRE_CTX(ctx);
+    ps::Engine& e = *ctx->engine;
+    const long long P = (long long)width * height;
+    const ps::FrameGeom g{width, height, P};
+    const int np = std::max(1, n_points), nt = std::max(0, n_tris);
+    int* d_u = e.dev<int>(e.s_a, np);
+    int* d_v = e.dev<int>(e.s_b, np);
+    double* d_d = e.dev<double>(e.s_c, np);
+    int* d_t = e.dev<int>(e.s_d, 3 * std::max(1, nt));
+    int off[2] = {0, nt};
+    int* d_off = e.dev<int>(e.s_e, 2);
+    double* d_pl = e.dev<double>(e.s_f, 3 * std::max(1, nt));
+    int32_t* d_lk = e.dev<int32_t>(e.s_g, P);
+    int* d_err = e.dev<int>(e.s_h, 1);
+    if (!d_u || !d_v || !d_d || !d_t || !d_off || !d_pl || !d_lk || !d_err)
+        return set_error(PS_CUDA_ERROR, "allocation failed");
+    cudaStream_t st = e.stream();
+    if (n_points > 0) {
+        cudaMemcpyAsync(d_u, u, sizeof(int) * n_points, cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(d_v, v, sizeof(int) * n_points, cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(d_d, d, sizeof(double) * n_points, cudaMemcpyHostToDevice, st);
+    }
+    if (nt > 0) cudaMemcpyAsync(d_t, tris, sizeof(int) * 3 * nt, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_off, off, sizeof(off), cudaMemcpyHostToDevice, st);
+    cudaMemsetAsync(d_lk, 0xff, sizeof(int32_t) * P, st);
+    cudaMemsetAsync(d_err, 0, sizeof(int), st);
+    e.count_launches(ps::launch_mesh(d_t, d_off, 1, nt, d_u, d_v, d_d, np, g, d_pl, d_lk, d_err, st));
+    int err = 0;
+    cudaMemcpyAsync(&err, d_err, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (planes && nt > 0) cudaMemcpyAsync(planes, d_pl, sizeof(double) * 3 * nt, cudaMemcpyDeviceToHost, st);
+    if (lookup) cudaMemcpyAsync(lookup, d_lk, sizeof(int32_t) * P, cudaMemcpyDeviceToHost, st);
+    ps_status s = from_engine(ctx, e.sync("mesh"));
+    if (s != PS_OK) return s;
+    if (err) return set_error(PS_DEGENERATE_TRIANGLE, "collinear vertices in a triangle");
+    return PS_OK;
+}
+
+ps_status ps_interpolate(ps_ctx* ctx, const int32_t* lookup, const double* planes, int n_tris,
+                         int width, int height, const uint8_t* mask, float max_disparity,
+                         float* value, uint8_t* valid) {
+    PS_REQUIRE_CTX(ctx);
+    ps::Engine& e = *ctx->engine;
+    const long long P = (long long)width * height;
+    const int nt = std::max(1, n_tris);
+    int32_t* d_lk = e.dev<int32_t>(e.s_a, P);
+    double* d_pl = e.dev<double>(e.s_b, 3 * nt);
+    uint8_t* d_m = mask ? e.dev<uint8_t>(e.s_c, P) : nullptr;
+    float* d_val = e.dev<float>(e.s_d, P);
+    uint8_t* d_ok = e.dev<uint8_t>(e.s_e, P);
+    if (!d_lk || !d_pl || (mask && !d_m) || !d_val || !d_ok) return set_error(PS_CUDA_ERROR, "allocation failed");
+    cudaStream_t st = e.stream();
+    cudaMemcpyAsync(d_lk, lookup, sizeof(int32_t) * P, cudaMemcpyHostToDevice, st);
+    if (n_tris > 0) cudaMemcpyAsync(d_pl, planes, sizeof(double) * 3 * n_tris, cudaMemcpyHostToDevice, st);
+    if (mask) cudaMemcpyAsync(d_m, mask, P, cudaMemcpyHostToDevice, st);
+    e.count_launches(ps::launch_interpolate(d_lk, d_pl, {width, height, P}, d_m, max_disparity, d_val, d_ok, st));
+    cudaMemcpyAsync(value, d_val, sizeof(float) * P, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(valid, d_ok, P, cudaMemcpyDeviceToHost, st);
+    return from_engine(ctx, e.sync("interpolate"));
+}
+
+ps_status ps_cost_evaluation(ps_ctx* ctx, const uint32_t* census_left, const uint32_t* census_right,
+                             int width, int height, const float* interp, const uint8_t* interp_valid,
+                             const uint8_t* mask, float* cost) {
+    PS_REQUIRE_CTX(ctx);
+    ps::Engine& e = *ctx->engine;
+    const long long P = (long long)width * height;
+    uint32_t* d_cl = e.dev<uint32_t>(e.s_a, P);
+    uint32_t* d_cr = e.dev<uint32_t>(e.s_b, P);
+    float* d_val = e.dev<float>(e.s_c, P);
+    uint8_t* d_ok = e.dev<uint8_t>(e.s_d, P);
+    uint8_t* d_m = e.dev<uint8_t>(e.s_e, P);
+    float* d_cost = e.dev<float>(e.s_f, P);
+    if (!d_cl || !d_cr || !d_val || !d_ok || !d_m || !d_cost) return set_error(PS_CUDA_ERROR, "allocation failed");
+    cudaStream_t st = e.stream();
+    cudaMemcpyAsync(d_cl, census_left, 4 * P, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_cr, census_right, 4 * P, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_val, interp, 4 * P, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_ok, interp_valid, P, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_m, mask, P, cudaMemcpyHostToDevice, st);
+    ps_config dc;
+    ps_config_default(&dc);
+    const ps::CostTables tab = ps::make_tables(dc);
+    e.count_launches(ps::launch_cost_eval(d_cl, d_cr, {width, height, P}, d_val, d_ok, d_m, tab, d_cost, st));
+    cudaMemcpyAsync(cost, d_cost, 4 * P, cudaMemcpyDeviceToHost, st);
+    return from_engine(ctx, e.sync("cost evaluation"));
+}
+
+ps_status ps_refinement(ps_ctx*, const float*, const uint8_t*, const float*, float*, uint8_t*,
+                        float*, const uint8_t*, int, int, int, const ps_config*, ps_cell*,
+                        ps_cell*) {
+    return set_error(PS_ERROR, "ps_refinement: stage entry point not built in this round");
+}
+
+ps_status ps_support_resampling(ps_ctx*, const ps_cell*, const ps_cell*, int, const int*,
+                                const int*, const double*, int, const uint32_t*, const uint32_t*,
+                                int, int, const ps_config*, int*, int*, double*, int, int*) {
+    return set_error(PS_ERROR, "ps_support_resampling: stage entry point not built in this round");
+}
+
+}  // extern "C"

@@ -1,0 +1,34 @@
+// delaunay.hpp — exact Delaunay triangulation of integer pixel coordinates.
+//
+// Replaces planestereo::delaunayTriangulate (proj/src/delaunay.cpp:288-325).
+// Contract: the output TRIANGLE SET equals the reference's;
+// triangle order and per-triangle rotation are not contractual.  The set is
+// the unique Delaunay subdivision with every cocircular cell triangulated so
+// that each interior diagonal avoids the lexicographically largest vertex of
+// its quad — what a lexicographic insertion with strict in-circle flips
+// produces, because the newly inserted point is always the lexicographic
+// maximum of every quad it tests.
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+namespace ps {
+
+struct DelaunayWorkspace {
+    std::vector<uint64_t> key, key_tmp;
+    std::vector<int> ord, ord_tmp;
+    std::vector<int> kept;
+    std::vector<int> px, py;
+    std::vector<int> tv, tn;  // triangle vertices / neighbour half-edges
+    std::vector<int> hnext, hprev, hedge;
+    std::vector<int> stack;
+};
+
+// Returns the number of triangles (index triples into the input written to
+// `tris`, 3 ints each, positively oriented: orient2d > 0), 0 for fewer than
+// three distinct points or a collinear set, -1 if a coordinate has
+// |c| >= 2^20 (the reference's exactness bound, delaunay.cpp:289-294).
+int delaunay(const int* u, const int* v, int n, std::vector<int>& tris, DelaunayWorkspace& ws);
+
+}  // namespace ps

@@ -1,0 +1,662 @@
+// engine.cpp — batched B200 pipeline (see engine.hpp).
+//
+// Stage order per batch mirrors planestereo::run (proj/src/pipeline.cpp:131-203):
+//   K1 frontend -> K2 candidates -> K3 seed match -> seed compaction
+//   for it in 1..iterations:
+//       supports delta D2H -> host Delaunay per frame (thread pool) -> triangles H2D
+//       K5/K6 mesh (planes + lookup) -> K7 refine (+K9 dense on the last iteration)
+//       if not last: K8 resample (confident append, invalid cells -> K3 re-match -> append)
+//   trace reduction D2H.
+// Every device stage is one launch over all frames of the batch.
+#include "engine.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <thread>
+
+#include "../kernels/launch.hpp"
+
+namespace ps {
+
+namespace {
+
+int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+bool is_pow2(int x) { return x > 0 && (x & (x - 1)) == 0; }
+
+double now_ms() {
+    return std::chrono::duration<double, std::milli>(
+               std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+}
+
+}  // namespace
+
+// PipelineConfig::validate (proj/src/config.cpp:17-49); messages match.
+ps_status validate_config(const ps_config& c, unsigned flags, std::string& msg) {
+    if (c.iterations < 1) {
+        msg = "iterations must be >= 1, got " + std::to_string(c.iterations);
+        return PS_INVALID_CONFIG;
+    }
+    if (c.max_disparity < 1) {
+        msg = "max disparity must be >= 1, got " + std::to_string(c.max_disparity);
+        return PS_INVALID_CONFIG;
+    }
+    if (!(c.cost_low > 0.0f && c.cost_low < c.cost_high && c.cost_high <= 1.0f)) {
+        msg = "cost thresholds must satisfy 0 < low < high <= 1";
+        return PS_INVALID_CONFIG;
+    }
+    const bool cell_ok = (flags & PS_RUN_UNCHECKED_CELL) ? c.occupancy_cell_size >= 1
+                                                          : is_pow2(c.occupancy_cell_size);
+    if (!cell_ok) {
+        msg = "occupancy cell size must be a power of two, got " +
+              std::to_string(c.occupancy_cell_size);
+        return PS_INVALID_CONFIG;
+    }
+    if (c.gradient_threshold < 0) {
+        msg = "gradient threshold must be non-negative";
+        return PS_INVALID_CONFIG;
+    }
+    if (c.corner_threshold < 0) {
+        msg = "corner threshold must be non-negative";
+        return PS_INVALID_CONFIG;
+    }
+    if (c.per_bin_cap < 1) {
+        msg = "per-bin cap must be >= 1";
+        return PS_INVALID_CONFIG;
+    }
+    if (!(c.sparse_accept_cost > 0.0f && c.sparse_accept_cost <= 1.0f)) {
+        msg = "sparse accept cost must lie in (0, 1]";
+        return PS_INVALID_CONFIG;
+    }
+    if (!(c.uniqueness_ratio > 0.0f && c.uniqueness_ratio <= 1.0f)) {
+        msg = "uniqueness ratio must lie in (0, 1]";
+        return PS_INVALID_CONFIG;
+    }
+    if (c.threads < 1) {
+        msg = "threads must be >= 1";
+        return PS_INVALID_CONFIG;
+    }
+    return PS_OK;
+}
+
+// Host-evaluated binary32 decision tables (this file is built with
+// -ffp-contract=off; x86-64 SSE evaluates float in binary32 exactly as the
+// reference does).
+CostTables make_tables(const ps_config& c) {
+    CostTables t{};
+    volatile float ratio = c.uniqueness_ratio;
+    for (int k = 0; k <= kCensusBits; ++k) t.cost[k] = float(k) / float(kCensusBits);
+    for (int k = 0; k <= kCensusBits; ++k) {
+        if (t.cost[k] < c.cost_low) t.low_mask |= 1u << k;
+        if (t.cost[k] > c.cost_high) t.high_mask |= 1u << k;
+        if (!(t.cost[k] > c.sparse_accept_cost)) t.accept_mask |= 1u << k;
+        for (int k2 = 0; k2 <= kCensusBits; ++k2) {
+            volatile float prod = ratio * t.cost[k2];
+            if (t.cost[k] > prod) t.uniq_reject[k] |= 1u << k2;
+        }
+    }
+    for (int k = 0; k <= kCensusBits; ++k)
+        t.fixed[k] = (unsigned long long)std::ldexp(double(t.cost[k]), 36);
+    t.fixed[kCensusBits + 1] = (unsigned long long)std::ldexp(double(c.cost_high), 36);
+    t.cost_high = c.cost_high;
+    return t;
+}
+
+// C_f values are k/24 floats or costHigh; their 2^-36 fixed-point sum is exact
+// iff costHigh * 2^36 is an integer (true for costHigh >= 2^-12 with a short
+// mantissa, e.g. every decimal-looking default).
+bool trace_fixed_exact(float cost_high) {
+    const double x = std::ldexp(double(cost_high), 36);
+    return x == std::floor(x);
+}
+
+struct Engine::Timer {};
+
+Engine::Engine(int device) : device_(device) {
+    cudaSetDevice(device_);
+    cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking);
+    const int hw = std::max(1u, std::thread::hardware_concurrency());
+    pool_ = new ThreadPool(hw);
+    ws_.resize(pool_->size());
+}
+
+Engine::~Engine() {
+    cudaSetDevice(device_);
+    if (st_) cudaStreamSynchronize(st_);
+    DevBuf* bufs[] = {&dL_, &dR_, &dMask_, &dMaskCount_, &dCL_, &dCR_, &dDf_, &dDv_, &dCf_,
+                      &dDense_, &dDenseV_, &dLookup_, &dSu_, &dSv_, &dSd_, &dS_, &dSnext_,
+                      &dSprev_, &dTaken_, &dTri_, &dTriOff_, &dPlanes_, &dCg_, &dCb_, &dBinKeys_,
+                      &dBinCount_, &dScratch_, &dCandU_, &dCandV_, &dCandCount_, &dOk_, &dDisp_,
+                      &dRemU_, &dRemV_, &dRemCount_, &dConf_, &dChunk_, &dTraceSum_,
+                      &dTraceValid_, &dErr_, &dPack_, &dPackOff_, &s_a, &s_b, &s_c, &s_d, &s_e,
+                      &s_f, &s_g, &s_h, &s_i, &s_j};
+    for (DevBuf* b : bufs)
+        if (b->p) cudaFree(b->p);
+    HostBuf* hbufs[] = {&hS_, &hSprev_, &hPackOff_, &hPack_, &hTri_, &hTriOff_, &hTraceSum_,
+                        &hTraceValid_, &hMaskCount_, &hL_, &hR_};
+    for (HostBuf* b : hbufs)
+        if (b->p) cudaFreeHost(b->p);
+    for (auto& p : pending_) {
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
+    for (cudaEvent_t e : event_pool_) cudaEventDestroy(e);
+    if (st_) cudaStreamDestroy(st_);
+    delete pool_;
+}
+
+template <class T>
+T* Engine::dev(DevBuf& b, size_t count) {
+    const size_t need = std::max<size_t>(count * sizeof(T), 256);
+    if (b.bytes < need) {
+        if (b.p) {
+            cudaStreamSynchronize(st_);
+            cudaFree(b.p);
+        }
+        b.p = nullptr;
+        b.bytes = 0;
+        if (cudaMalloc(&b.p, need) != cudaSuccess) {
+            b.p = nullptr;
+            return nullptr;
+        }
+        b.bytes = need;
+    }
+    return static_cast<T*>(b.p);
+}
+
+template <class T>
+T* Engine::host(HostBuf& b, size_t count) {
+    const size_t need = std::max<size_t>(count * sizeof(T), 256);
+    if (b.bytes < need) {
+        if (b.p) {
+            cudaStreamSynchronize(st_);
+            cudaFreeHost(b.p);
+        }
+        b.p = nullptr;
+        b.bytes = 0;
+        if (cudaHostAlloc(&b.p, need, cudaHostAllocDefault) != cudaSuccess) {
+            b.p = nullptr;
+            return nullptr;
+        }
+        b.bytes = need;
+    }
+    return static_cast<T*>(b.p);
+}
+
+template uint8_t* Engine::dev<uint8_t>(DevBuf&, size_t);
+template int* Engine::dev<int>(DevBuf&, size_t);
+template uint32_t* Engine::dev<uint32_t>(DevBuf&, size_t);
+template float* Engine::dev<float>(DevBuf&, size_t);
+template double* Engine::dev<double>(DevBuf&, size_t);
+template unsigned long long* Engine::dev<unsigned long long>(DevBuf&, size_t);
+template int2* Engine::dev<int2>(DevBuf&, size_t);
+template int* Engine::host<int>(HostBuf&, size_t);
+template uint8_t* Engine::host<uint8_t>(HostBuf&, size_t);
+
+ps_status Engine::check(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return PS_OK;
+    return fail(PS_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+ps_status Engine::sync(const char* what) {
+    cudaError_t e = cudaStreamSynchronize(st_);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    return check(e, what);
+}
+
+void Engine::begin_kernel(const char* name, double bytes) {
+    if (!profiling_) return;
+    int idx = -1;
+    for (size_t i = 0; i < stats_.size(); ++i)
+        if (stats_[i].name == name) idx = int(i);
+    if (idx < 0) {
+        stats_.push_back({name, 0, 0.0, 0.0});
+        idx = int(stats_.size()) - 1;
+    }
+    stats_[idx].bytes += bytes;
+    stats_[idx].launches += 1;
+    cudaEvent_t a;
+    if (!event_pool_.empty()) {
+        a = event_pool_.back();
+        event_pool_.pop_back();
+    } else {
+        cudaEventCreate(&a);
+    }
+    cudaEventRecord(a, st_);
+    pending_stat_ = idx;
+    pending_start_ = a;
+}
+
+void Engine::end_kernel() {
+    if (!profiling_ || pending_stat_ < 0) return;
+    cudaEvent_t b;
+    if (!event_pool_.empty()) {
+        b = event_pool_.back();
+        event_pool_.pop_back();
+    } else {
+        cudaEventCreate(&b);
+    }
+    cudaEventRecord(b, st_);
+    pending_.push_back({pending_stat_, pending_start_, b});
+    pending_stat_ = -1;
+}
+
+void Engine::resolve_timers() {
+    for (auto& p : pending_) {
+        float ms = 0.0f;
+        if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) stats_[p.stat].ms += ms;
+        event_pool_.push_back(p.a);
+        event_pool_.push_back(p.b);
+    }
+    pending_.clear();
+}
+
+ps_status Engine::upload(int frames, const uint8_t* left, const uint8_t* right, int width,
+                         int height) {
+    if (width < 16 || height < 16)
+        return fail(PS_DIMENSION_TOO_SMALL, "image must be at least 16x16, got " +
+                                                std::to_string(width) + "x" +
+                                                std::to_string(height));
+    if (frames < 1) return fail(PS_ERROR, "batch needs at least one frame");
+    cudaSetDevice(device_);
+    F_ = frames;
+    W_ = width;
+    H_ = height;
+    P_ = (long long)width * height;
+    const size_t n = size_t(F_) * P_;
+    uint8_t* dl = dev<uint8_t>(dL_, n);
+    uint8_t* dr = dev<uint8_t>(dR_, n);
+    if (!dl || !dr) return fail(PS_CUDA_ERROR, "device allocation failed (images)");
+    ps_status s = check(cudaMemcpyAsync(dl, left, n, cudaMemcpyHostToDevice, st_), "H2D left");
+    if (s != PS_OK) return s;
+    s = check(cudaMemcpyAsync(dr, right, n, cudaMemcpyHostToDevice, st_), "H2D right");
+    if (s != PS_OK) return s;
+    have_inputs_ = true;
+    have_outputs_ = false;
+    return PS_OK;
+}
+
+ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer_fn observer,
+                               void* user) {
+    if (!have_inputs_) return fail(PS_ERROR, "no batch uploaded");
+    ps_status st = validate_config(cfg, flags, err_);
+    if (st != PS_OK) return st;
+    cudaSetDevice(device_);
+    const int F = F_, W = W_, H = H_;
+    const long long P = P_;
+    const FrameGeom g{W, H, P};
+    const CostTables tab = make_tables(cfg);
+    const int iters = cfg.iterations;
+    iters_ = iters;
+    cost_high_ = cfg.cost_high;
+    const bool fixed_trace = trace_fixed_exact(cfg.cost_high);
+
+    // cell schedule s_i (pipeline.cpp:147,171) and capacities
+    std::vector<int> cell_of(iters);
+    long long bound = 120ll * cfg.per_bin_cap;
+    int cells_max = 1;
+    for (int it = 0, s = cfg.occupancy_cell_size; it < iters; ++it) {
+        cell_of[it] = s;
+        const int cells = ceil_div(W, s) * ceil_div(H, s);
+        cells_max = std::max(cells_max, cells);
+        if (it + 1 < iters) bound += 2ll * cells;
+        s = std::max(1, s / 2);
+    }
+    scap_ = int(std::min<long long>(P, bound));
+    const int cand_stride = 120 * cfg.per_bin_cap;
+    const int mstride = std::max(cand_stride, cells_max);
+    const int chunks = ceil_div(mstride, 1024);
+    const long long words = (P + 31) / 32;
+    int n_pow2 = 1;
+    while (n_pow2 < std::min<long long>(cand_stride, P)) n_pow2 <<= 1;
+    const long long sc_stride = candidate_scratch_stride(g);
+    const size_t scratch_keys =
+        cfg.per_bin_cap > 8 ? size_t(F) * std::max<long long>(120 * sc_stride, n_pow2) : 1;
+
+    uint8_t* dMask = dev<uint8_t>(dMask_, size_t(F) * P);
+    int* dMaskCount = dev<int>(dMaskCount_, F);
+    uint32_t* dCL = dev<uint32_t>(dCL_, size_t(F) * P);
+    uint32_t* dCR = dev<uint32_t>(dCR_, size_t(F) * P);
+    float* dDf = dev<float>(dDf_, size_t(F) * P);
+    uint8_t* dDv = dev<uint8_t>(dDv_, size_t(F) * P);
+    float* dCf = dev<float>(dCf_, size_t(F) * P);
+    float* dDense = dev<float>(dDense_, size_t(F) * P);
+    uint8_t* dDenseV = dev<uint8_t>(dDenseV_, size_t(F) * P);
+    int32_t* dLookup = dev<int32_t>(dLookup_, size_t(F) * P);
+    int* dSu = dev<int>(dSu_, size_t(F) * scap_);
+    int* dSv = dev<int>(dSv_, size_t(F) * scap_);
+    double* dSd = dev<double>(dSd_, size_t(F) * scap_);
+    dev<int>(dS_, F);
+    dev<int>(dSnext_, F);
+    int* dSprev = dev<int>(dSprev_, F);
+    uint32_t* dTaken = dev<uint32_t>(dTaken_, size_t(F) * words);
+    int* dTriOff = dev<int>(dTriOff_, F + 1);
+    unsigned long long* dCg = dev<unsigned long long>(dCg_, size_t(F) * cells_max);
+    unsigned long long* dCb = dev<unsigned long long>(dCb_, size_t(F) * cells_max);
+    unsigned long long* dBinKeys = dev<unsigned long long>(dBinKeys_, size_t(F) * 120 * cfg.per_bin_cap);
+    int* dBinCount = dev<int>(dBinCount_, size_t(F) * 120);
+    unsigned long long* dScratch = dev<unsigned long long>(dScratch_, scratch_keys);
+    int* dCandU = dev<int>(dCandU_, size_t(F) * cand_stride);
+    int* dCandV = dev<int>(dCandV_, size_t(F) * cand_stride);
+    int* dCandCount = dev<int>(dCandCount_, F);
+    uint8_t* dOk = dev<uint8_t>(dOk_, size_t(F) * mstride);
+    int* dDisp = dev<int>(dDisp_, size_t(F) * mstride);
+    int* dRemU = dev<int>(dRemU_, size_t(F) * cells_max);
+    int* dRemV = dev<int>(dRemV_, size_t(F) * cells_max);
+    int* dRemCount = dev<int>(dRemCount_, F);
+    int* dConf = dev<int>(dConf_, F);
+    int* dChunk = dev<int>(dChunk_, size_t(F) * chunks + 1);
+    unsigned long long* dTraceSum = dev<unsigned long long>(dTraceSum_, size_t(F) * iters);
+    unsigned* dTraceValid = reinterpret_cast<unsigned*>(dev<uint32_t>(dTraceValid_, size_t(F) * iters));
+    int* dErr = dev<int>(dErr_, 1);
+    int* dPackOff = dev<int>(dPackOff_, F);
+    int* hS = host<int>(hS_, F);
+    int* hSprev = host<int>(hSprev_, F);
+    int* hPackOff = host<int>(hPackOff_, F);
+    int* hTriOff = host<int>(hTriOff_, F + 1);
+    int* hMaskCount = host<int>(hMaskCount_, F);
+    unsigned long long* hTraceSum =
+        reinterpret_cast<unsigned long long*>(host<uint8_t>(hTraceSum_, size_t(F) * iters * 8));
+    unsigned* hTraceValid = reinterpret_cast<unsigned*>(host<uint8_t>(hTraceValid_, size_t(F) * iters * 4));
+    void* must[] = {dMask, dMaskCount, dCL, dCR, dDf, dDv, dCf, dDense, dDenseV, dLookup, dSu, dSv,
+                    dSd, dS_.p, dSnext_.p, dSprev, dTaken, dTriOff, dCg, dCb, dBinKeys, dBinCount,
+                    dScratch, dCandU, dCandV, dCandCount, dOk, dDisp, dRemU, dRemV, dRemCount,
+                    dConf, dChunk, dTraceSum, dTraceValid, dErr, dPackOff, hS, hSprev, hPackOff,
+                    hTriOff, hMaskCount, hTraceSum, hTraceValid};
+    for (void* p : must)
+        if (!p) return fail(PS_CUDA_ERROR, "allocation failed for a batch of " + std::to_string(F) +
+                                               " frames of " + std::to_string(W) + "x" +
+                                               std::to_string(H));
+
+    const uint8_t* dL = static_cast<const uint8_t*>(dL_.p);
+    const uint8_t* dR = static_cast<const uint8_t*>(dR_.p);
+    // ---- state init (pipeline.cpp:145-146: D_f invalid, C_f = costHigh everywhere)
+    cudaMemsetAsync(dMaskCount, 0, sizeof(int) * F, st_);
+    cudaMemsetAsync(dTaken, 0, sizeof(uint32_t) * F * words, st_);
+    cudaMemsetAsync(dTraceSum, 0, sizeof(unsigned long long) * F * iters, st_);
+    cudaMemsetAsync(dTraceValid, 0, sizeof(unsigned) * F * iters, st_);
+    cudaMemsetAsync(dDf, 0, sizeof(float) * F * P, st_);
+    cudaMemsetAsync(dDv, 0, size_t(F) * P, st_);
+    cudaMemsetAsync(dErr, 0, sizeof(int), st_);
+    launches_ += launch_fill_f32(dCf, (long long)F * P, cfg.cost_high, st_);
+
+    // ---- K1 frontend (image.cpp:43-60, census.cpp:10-41)
+    begin_kernel("frontend", 11.0 * double(P) * F);
+    launches_ += launch_frontend(dL, dR, g, F, cfg.gradient_threshold, dMask, dCL, dCR, dMaskCount, st_);
+    end_kernel();
+    // ---- K2 candidates (sparse.cpp:84-146)
+    begin_kernel("candidates", double(P) * F);
+    launches_ += launch_candidates(dL, g, F, cfg.corner_threshold, cfg.per_bin_cap, dBinKeys,
+                                   dBinCount, dScratch, sc_stride, dCandU, dCandV, nullptr,
+                                   dCandCount, cand_stride, st_);
+    end_kernel();
+    // ---- K3 seed match (sparse.cpp:148-195) + ordered compaction
+    begin_kernel("match_seed", 0.0);
+    launches_ += launch_match(dCL, dCR, g, F, cfg.max_disparity, tab, dCandU, dCandV, dCandCount,
+                              cand_stride, cand_stride, dOk, dDisp, nullptr, st_);
+    end_kernel();
+    begin_kernel("compact", 0.0);
+    launches_ += launch_emit_matches(dCandU, dCandV, dCandCount, cand_stride, cand_stride, dOk,
+                                     dDisp, g, F, dTaken, dSu, dSv, dSd, scap_, nullptr, nullptr,
+                                     static_cast<int*>(dS_.p), dChunk, st_);
+    end_kernel();
+    ps_status s = check(cudaMemcpyAsync(hS, dS_.p, sizeof(int) * F, cudaMemcpyDeviceToHost, st_), "D2H S");
+    if (s == PS_OK)
+        s = check(cudaMemcpyAsync(hMaskCount, dMaskCount, sizeof(int) * F, cudaMemcpyDeviceToHost, st_),
+                  "D2H M");
+    if (s == PS_OK) s = sync("seeding");
+    if (s != PS_OK) return s;
+
+    status_.assign(F, PS_OK);
+    hu_.resize(F);
+    hv_.resize(F);
+    htri_.resize(F);
+    for (int f = 0; f < F; ++f) {
+        hu_[f].clear();
+        hv_[f].clear();
+        hSprev[f] = 0;
+        if (hS[f] < 3) status_[f] = PS_SEEDING_FAILED;  // pipeline.cpp:151-154
+    }
+    trace_.assign(size_t(F) * iters, ps_iter_stats{});
+
+    for (int it = 1; it <= iters; ++it) {
+        const double tic = now_ms();
+        const bool last = it == iters;
+        const int cell = cell_of[it - 1];
+        if (it > 1) {
+            s = check(cudaMemcpyAsync(hS, dS_.p, sizeof(int) * F, cudaMemcpyDeviceToHost, st_), "D2H S");
+            if (s == PS_OK) s = sync("support count");
+            if (s != PS_OK) return s;
+        }
+        // ---- supports delta to the host
+        long long total_new = 0;
+        int max_new = 0;
+        for (int f = 0; f < F; ++f) {
+            hPackOff[f] = int(total_new);
+            const int n = hS[f] - hSprev[f];
+            total_new += n;
+            max_new = std::max(max_new, n);
+        }
+        int2* dPack = dev<int2>(dPack_, size_t(std::max<long long>(total_new, 1)));
+        int2* hPack = reinterpret_cast<int2*>(host<uint8_t>(hPack_, size_t(std::max<long long>(total_new, 1)) * 8));
+        if (!dPack || !hPack) return fail(PS_CUDA_ERROR, "allocation failed (support staging)");
+        s = check(cudaMemcpyAsync(dSprev, hSprev, sizeof(int) * F, cudaMemcpyHostToDevice, st_), "H2D Sprev");
+        if (s == PS_OK)
+            s = check(cudaMemcpyAsync(dPackOff, hPackOff, sizeof(int) * F, cudaMemcpyHostToDevice, st_),
+                      "H2D pack offsets");
+        if (s != PS_OK) return s;
+        launches_ += launch_pack_new_supports(dSu, dSv, scap_, dSprev, static_cast<int*>(dS_.p),
+                                              dPackOff, F, max_new, dPack, st_);
+        if (total_new > 0)
+            s = check(cudaMemcpyAsync(hPack, dPack, sizeof(int2) * total_new, cudaMemcpyDeviceToHost, st_),
+                      "D2H supports");
+        if (s == PS_OK) s = sync("support delta");
+        if (s != PS_OK) return s;
+
+        // ---- host Delaunay per frame (delaunay.cpp:288-325 contract)
+        std::vector<int> ntri(F, 0);
+        pool_->parallel_for(F, [&](int f, int worker) {
+            const int n = hS[f] - hSprev[f];
+            for (int i = 0; i < n; ++i) {
+                hu_[f].push_back(hPack[hPackOff[f] + i].x);
+                hv_[f].push_back(hPack[hPackOff[f] + i].y);
+            }
+            if (status_[f] != PS_OK) {
+                htri_[f].clear();
+                return;
+            }
+            const int t = delaunay(hu_[f].data(), hv_[f].data(), int(hu_[f].size()), htri_[f],
+                                   ws_[worker]);
+            if (t < 0) {
+                status_[f] = PS_ERROR;
+                htri_[f].clear();
+                return;
+            }
+            ntri[f] = t;
+        });
+        long long total_tri = 0;
+        for (int f = 0; f < F; ++f) {
+            hTriOff[f] = int(total_tri);
+            total_tri += ntri[f];
+        }
+        hTriOff[F] = int(total_tri);
+        int* hTri = host<int>(hTri_, size_t(std::max<long long>(total_tri, 1)) * 3);
+        int* dTri = dev<int>(dTri_, size_t(std::max<long long>(total_tri, 1)) * 3);
+        double* dPlanes = dev<double>(dPlanes_, size_t(std::max<long long>(total_tri, 1)) * 3);
+        if (!hTri || !dTri || !dPlanes) return fail(PS_CUDA_ERROR, "allocation failed (triangles)");
+        pool_->parallel_for(F, [&](int f, int) {
+            if (ntri[f] > 0)
+                std::memcpy(hTri + 3ll * hTriOff[f], htri_[f].data(), sizeof(int) * 3 * ntri[f]);
+        });
+        if (total_tri > 0)
+            s = check(cudaMemcpyAsync(dTri, hTri, sizeof(int) * 3 * total_tri, cudaMemcpyHostToDevice, st_),
+                      "H2D triangles");
+        if (s == PS_OK)
+            s = check(cudaMemcpyAsync(dTriOff, hTriOff, sizeof(int) * (F + 1), cudaMemcpyHostToDevice, st_),
+                      "H2D triangle offsets");
+        if (s != PS_OK) return s;
+        for (int f = 0; f < F; ++f) {
+            ps_iter_stats& ts = trace_[size_t(f) * iters + (it - 1)];
+            ts.iteration = it;
+            ts.support_count = hS[f];  // mesh.vertices().size() (pipeline.cpp:180)
+            ts.triangle_count = ntri[f];
+            ts.occupancy_cell_size = cell;
+            hSprev[f] = hS[f];
+        }
+
+        // ---- K5/K6 mesh (mesh.cpp:44-123)
+        cudaMemsetAsync(dLookup, 0xff, sizeof(int32_t) * F * P, st_);
+        begin_kernel("mesh", 4.0 * double(P) * F + 60.0 * double(total_tri));
+        launches_ += launch_mesh(dTri, dTriOff, F, total_tri, dSu, dSv, dSd, scap_, g, dPlanes,
+                                 dLookup, dErr, st_);
+        end_kernel();
+
+        // ---- K7 (+K9) refine (mesh.cpp:149-182, pipeline.cpp:33-86)
+        const int cols = ceil_div(W, cell);
+        const int cells = cols * ceil_div(H, cell);
+        cudaMemsetAsync(dCg, 0xff, sizeof(unsigned long long) * F * cells, st_);
+        cudaMemsetAsync(dCb, 0xff, sizeof(unsigned long long) * F * cells, st_);
+        RefineArgs ra{g,       F,   dMask,    dLookup, dPlanes,           dCL,
+                      dCR,     float(cfg.max_disparity), cell, cols, cells, dDf,
+                      dDv,     dCf, dCg,      dCb,     dTraceSum + (it - 1),
+                      dTraceValid + (it - 1), iters, dDense, dDenseV};
+        double mbytes = 0.0;
+        for (int f = 0; f < F; ++f) mbytes += double(hMaskCount[f]);
+        const double kbytes = double(P) * F + 29.0 * mbytes + (last ? 9.0 * double(P) * F - 4.0 * mbytes : 0.0);
+        begin_kernel("refine", kbytes);
+        launches_ += launch_refine(ra, tab, last, st_);
+        end_kernel();
+
+        if (!last) {
+            // ---- K8 resampling (pipeline.cpp:88-129)
+            begin_kernel("resample", 0.0);
+            launches_ += launch_resample_confident(dCg, cells, g, F, dLookup, dPlanes, dTaken, dSu,
+                                                   dSv, dSd, scap_, static_cast<int*>(dS_.p),
+                                                   dConf, dChunk, st_);
+            launches_ += launch_resample_invalid(dCb, cells, g, F, dRemU, dRemV, cells_max,
+                                                 dRemCount, dChunk, st_);
+            end_kernel();
+            begin_kernel("match_resample", 0.0);
+            launches_ += launch_match(dCL, dCR, g, F, cfg.max_disparity, tab, dRemU, dRemV,
+                                      dRemCount, cells_max, cells, dOk, dDisp, nullptr, st_);
+            end_kernel();
+            begin_kernel("compact", 0.0);
+            launches_ += launch_emit_matches(dRemU, dRemV, dRemCount, cells_max, cells, dOk, dDisp,
+                                             g, F, dTaken, dSu, dSv, dSd, scap_,
+                                             static_cast<int*>(dS_.p), dConf,
+                                             static_cast<int*>(dSnext_.p), dChunk, st_);
+            end_kernel();
+            std::swap(dS_, dSnext_);
+        }
+        if (observer && F == 1) {
+            std::vector<float> fd(P), fc(P);
+            std::vector<uint8_t> fv(P);
+            s = check(cudaMemcpyAsync(fd.data(), dDf, sizeof(float) * P, cudaMemcpyDeviceToHost, st_), "D2H");
+            if (s == PS_OK) s = check(cudaMemcpyAsync(fv.data(), dDv, P, cudaMemcpyDeviceToHost, st_), "D2H");
+            if (s == PS_OK) s = check(cudaMemcpyAsync(fc.data(), dCf, sizeof(float) * P, cudaMemcpyDeviceToHost, st_), "D2H");
+            if (s == PS_OK) s = sync("observer");
+            if (s != PS_OK) return s;
+            observer(it, fd.data(), fv.data(), fc.data(), W, H, user);
+        }
+        const double toc = now_ms();
+        for (int f = 0; f < F; ++f) trace_[size_t(f) * iters + (it - 1)].millis = toc - tic;
+    }
+
+    // ---- trace (pipeline.cpp:183-191)
+    int herr = 0;
+    s = check(cudaMemcpyAsync(hTraceSum, dTraceSum, sizeof(unsigned long long) * F * iters,
+                              cudaMemcpyDeviceToHost, st_), "D2H trace");
+    if (s == PS_OK)
+        s = check(cudaMemcpyAsync(hTraceValid, dTraceValid, sizeof(unsigned) * F * iters,
+                                  cudaMemcpyDeviceToHost, st_), "D2H trace");
+    if (s == PS_OK) s = check(cudaMemcpyAsync(&herr, dErr, sizeof(int), cudaMemcpyDeviceToHost, st_), "D2H err");
+    if (s == PS_OK) s = sync("pipeline");
+    if (s != PS_OK) return s;
+    resolve_timers();
+    if (herr) return fail(PS_DEGENERATE_TRIANGLE, "collinear vertices in a triangle");
+    for (int f = 0; f < F; ++f) {
+        for (int it = 0; it < iters; ++it) {
+            ps_iter_stats& ts = trace_[size_t(f) * iters + it];
+            const int M = hMaskCount[f];
+            // The fixed-point sum is exact (see trace_fixed_exact); the double
+            // conversion rounds once, exactly like the reference's exact
+            // running double sum.
+            const double sum = std::ldexp(double(hTraceSum[size_t(f) * iters + it]), -36);
+            ts.mean_cost = M > 0 ? sum / M : 0.0;
+            ts.valid_count = int(hTraceValid[size_t(f) * iters + it]);
+        }
+    }
+    if (!fixed_trace) {
+        // costHigh with a mantissa too long for the 2^-36 grid: recompute the
+        // last iteration's mean from the final costs (earlier ones stay approximate).
+        std::vector<float> fc(P);
+        std::vector<uint8_t> mk(P);
+        for (int f = 0; f < F; ++f) {
+            cudaMemcpy(fc.data(), dCf + size_t(f) * P, sizeof(float) * P, cudaMemcpyDeviceToHost);
+            cudaMemcpy(mk.data(), dMask + size_t(f) * P, P, cudaMemcpyDeviceToHost);
+            double sum = 0.0;
+            for (long long i = 0; i < P; ++i)
+                if (mk[i]) sum += fc[i];
+            const int M = hMaskCount[f];
+            trace_[size_t(f) * iters + iters - 1].mean_cost = M > 0 ? sum / M : 0.0;
+        }
+    }
+    have_outputs_ = true;
+    for (int f = 0; f < F; ++f)
+        if (status_[f] != PS_OK) return fail(ps_status(status_[f]),
+                                            "only " + std::to_string(hS[f]) +
+                                                " seed matches survived; need at least 3");
+    return PS_OK;
+}
+
+ps_status Engine::download(float* disparity, uint8_t* disparity_valid, float* cost, float* dense,
+                           uint8_t* dense_valid, ps_iter_stats* trace, int* frame_status) {
+    if (!have_outputs_) return fail(PS_ERROR, "no completed run to download");
+    cudaSetDevice(device_);
+    const size_t n = size_t(F_) * P_;
+    ps_status s = PS_OK;
+    if (disparity && s == PS_OK)
+        s = check(cudaMemcpyAsync(disparity, dDf_.p, n * 4, cudaMemcpyDeviceToHost, st_), "D2H disparity");
+    if (disparity_valid && s == PS_OK)
+        s = check(cudaMemcpyAsync(disparity_valid, dDv_.p, n, cudaMemcpyDeviceToHost, st_), "D2H validity");
+    if (cost && s == PS_OK)
+        s = check(cudaMemcpyAsync(cost, dCf_.p, n * 4, cudaMemcpyDeviceToHost, st_), "D2H cost");
+    if (dense && s == PS_OK)
+        s = check(cudaMemcpyAsync(dense, dDense_.p, n * 4, cudaMemcpyDeviceToHost, st_), "D2H dense");
+    if (dense_valid && s == PS_OK)
+        s = check(cudaMemcpyAsync(dense_valid, dDenseV_.p, n, cudaMemcpyDeviceToHost, st_), "D2H dense validity");
+    if (s == PS_OK) s = sync("download");
+    if (s != PS_OK) return s;
+    for (int f = 0; f < F_; ++f) {
+        if (frame_status) frame_status[f] = status_[f];
+        if (status_[f] == PS_OK) continue;
+        // A frame whose seeding failed has no result (run() throws SeedingFailed).
+        const size_t b = size_t(f) * P_;
+        if (disparity) std::fill(disparity + b, disparity + b + P_, 0.0f);
+        if (disparity_valid) std::fill(disparity_valid + b, disparity_valid + b + P_, uint8_t(0));
+        if (cost) std::fill(cost + b, cost + b + P_, cost_high_);
+        if (dense) std::fill(dense + b, dense + b + P_, 0.0f);
+        if (dense_valid) std::fill(dense_valid + b, dense_valid + b + P_, uint8_t(0));
+    }
+    if (trace) std::copy(trace_.begin(), trace_.end(), trace);
+    return PS_OK;
+}
+
+ps_status Engine::supports(int frame, int* u, int* v, double* d, int capacity, int* count) {
+    if (!have_outputs_ || frame < 0 || frame >= F_) return fail(PS_ERROR, "no such frame");
+    // The last iteration's list: trace support_count of the last iteration.
+    const int n = trace_[size_t(frame) * iters_ + iters_ - 1].support_count;
+    if (count) *count = n;
+    if (n > capacity) return fail(PS_CAPACITY, "support buffer too small");
+    const size_t b = size_t(frame) * scap_;
+    ps_status s = PS_OK;
+    if (u) s = check(cudaMemcpy(u, static_cast<int*>(dSu_.p) + b, sizeof(int) * n, cudaMemcpyDeviceToHost), "D2H");
+    if (v && s == PS_OK) s = check(cudaMemcpy(v, static_cast<int*>(dSv_.p) + b, sizeof(int) * n, cudaMemcpyDeviceToHost), "D2H");
+    if (d && s == PS_OK) s = check(cudaMemcpy(d, static_cast<double*>(dSd_.p) + b, sizeof(double) * n, cudaMemcpyDeviceToHost), "D2H");
+    return s;
+}
+
+}  // namespace ps

@@ -1,0 +1,68 @@
+// common.cuh — shared device-side definitions for the sm_100a kernels.
+//
+// Parity-critical arithmetic lives here:
+//   * census cost k/24 is carried as the integer k (0..24); every float
+//     comparison the reference makes on costs is pre-evaluated on the host in
+//     binary32 into the tables of CostTables, so no device float rounding can
+//     differ from the reference;
+//   * plane evaluation is ((a*u)+(b*v))+c in binary64 with explicit _rn
+//     intrinsics (no FMA contraction, mesh.hpp:19 as compiled without
+//     -march), then rounded to binary32 with __double2float_rn.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ps {
+
+constexpr int kCensusBits = 24;
+constexpr int kNoKey = 25;  // "no second-best" marker (BestMatch init 2.0f, sparse.cpp:38-42)
+constexpr unsigned long long kEmptyCell = ~0ull;
+
+// Host-built lookup tables derived from the PipelineConfig floats.
+struct CostTables {
+    float cost[kCensusBits + 1];        // float(k)/24.0f, census.hpp:45-47
+    unsigned low_mask;                  // bit k: cost[k] <  costLow   (pipeline.cpp:73)
+    unsigned high_mask;                 // bit k: cost[k] >  costHigh  (pipeline.cpp:78)
+    unsigned accept_mask;               // bit k: !(cost[k] > sparseAcceptCost)   (sparse.cpp:169)
+    unsigned uniq_reject[kCensusBits + 1];  // bit k2 of [k1]: cost[k1] > ratio*cost[k2] (sparse.cpp:172)
+    unsigned long long fixed[kCensusBits + 2];  // cost*2^36 for k=0..24, [25] = costHigh
+    float cost_high;
+};
+
+// Launch parameters shared by the per-frame kernels of one batch.
+struct FrameGeom {
+    int width;
+    int height;
+    long long pixels;  // P = width*height, frame stride of image-shaped buffers
+};
+
+#ifdef __CUDACC__
+__device__ __forceinline__ float plane_eval(const double* __restrict__ pl, int u, int v) {
+    // DisparityPlane::at (mesh.hpp:19) evaluated as the reference binary does:
+    // mulsd, mulsd, addsd, addsd, cvtsd2ss.
+    const double a = __ldg(pl), b = __ldg(pl + 1), c = __ldg(pl + 2);
+    const double s = __dadd_rn(__dmul_rn(a, double(u)), __dmul_rn(b, double(v)));
+    return __double2float_rn(__dadd_rn(s, c));
+}
+
+__device__ __forceinline__ int lround_away(float x) {
+    // std::lround(float): half away from zero (pipeline.cpp:44, App. A.3).
+    return int(roundf(x));
+}
+
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long y = __shfl_xor_sync(0xffffffffu, x, o);
+        x = y < x ? y : x;
+    }
+    return x;
+}
+
+__device__ __forceinline__ unsigned warp_min_u32(unsigned x) {
+    return __reduce_min_sync(0xffffffffu, x);
+}
+#endif  // __CUDACC__
+
+}  // namespace ps

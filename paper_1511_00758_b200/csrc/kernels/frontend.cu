@@ -1,0 +1,387 @@
+// frontend.cu — K1 (gradient mask + both census fields) and K2 (segment-test
+// corners, per-bin top-k, global candidate sort).
+//
+// K1 replaces gradientMask (proj/src/image.cpp:43-60) and censusTransform
+// (proj/src/census.cpp:10-41).  One 256-thread block stages a 128x8 tile of L
+// and R plus a 2-px halo in shared memory (coalesced byte rows), each thread
+// produces 4 horizontally adjacent pixels and writes them as one uint4 census
+// word group and one uchar4 mask group when the row segment is 16-B aligned.
+// HBM traffic is the algorithmic 11 B/px.
+//
+// K2 replaces detectCandidates (proj/src/sparse.cpp:84-146).  One block per
+// (bin, frame): every thread keeps a sorted register top-k of packed keys
+//   key = (4095 - score) << 40 | v << 20 | u
+// (ascending key = score desc, v asc, u asc = byScoreThenRowMajor, :130-134),
+// then the block merges the per-thread lists by repeated block-min.  A second
+// kernel sorts the <= 120*cap survivors of each frame with a shared-memory
+// bitonic sort.
+#include <cuda_runtime.h>
+
+#include "launch.hpp"
+
+namespace ps {
+
+namespace {
+
+constexpr int kTileW = 128;  // 32 threads x 4 px
+constexpr int kTileH = 8;
+constexpr int kHalo = 2;
+constexpr int kSmW = kTileW + 2 * kHalo;
+constexpr int kSmH = kTileH + 2 * kHalo;
+
+__device__ __forceinline__ uint32_t census_at(const uint8_t (*s)[kSmW], int x, int y) {
+    // Bit k = k-th neighbour of the 5x5 window in row-major order, centre
+    // skipped, set when strictly darker than the centre (census.cpp:22-35).
+    const uint8_t c = s[y][x];
+    uint32_t desc = 0;
+    int bit = 0;
+#pragma unroll
+    for (int dv = -2; dv <= 2; ++dv) {
+#pragma unroll
+        for (int du = -2; du <= 2; ++du) {
+            if (dv == 0 && du == 0) continue;
+            desc |= uint32_t(s[y + dv][x + du] < c) << bit;
+            ++bit;
+        }
+    }
+    return desc;
+}
+
+__global__ void __launch_bounds__(256) k_frontend(const uint8_t* __restrict__ left,
+                                                  const uint8_t* __restrict__ right, FrameGeom g,
+                                                  int thr, uint8_t* __restrict__ mask,
+                                                  uint32_t* __restrict__ cl,
+                                                  uint32_t* __restrict__ cr,
+                                                  int* __restrict__ mask_count) {
+    __shared__ uint8_t sl[kSmH][kSmW];
+    __shared__ uint8_t sr[kSmH][kSmW];
+    __shared__ int warp_cnt[8];
+    const int f = blockIdx.z;
+    const int W = g.width, H = g.height;
+    const int u0 = blockIdx.x * kTileW - kHalo;
+    const int v0 = blockIdx.y * kTileH - kHalo;
+    const uint8_t* L = left + f * g.pixels;
+    const uint8_t* R = right ? right + f * g.pixels : nullptr;
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+    for (int i = tid; i < kSmH * kSmW; i += 256) {
+        const int y = i / kSmW, x = i % kSmW;
+        const int gu = u0 + x, gv = v0 + y;
+        const bool in = gu >= 0 && gu < W && gv >= 0 && gv < H;
+        sl[y][x] = in ? __ldg(L + (long long)gv * W + gu) : 0;
+        if (R) sr[y][x] = in ? __ldg(R + (long long)gv * W + gu) : 0;
+    }
+    __syncthreads();
+
+    const int v = blockIdx.y * kTileH + threadIdx.y;
+    const int ub = blockIdx.x * kTileW + threadIdx.x * 4;
+    int cnt = 0;
+    if (v < H) {
+        uint32_t dl[4], dr[4];
+        uint8_t mk[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int u = ub + j;
+            const int x = threadIdx.x * 4 + j + kHalo, y = threadIdx.y + kHalo;
+            const bool interior = u >= 2 && u < W - 2 && v >= 2 && v < H - 2;
+            dl[j] = interior ? census_at(sl, x, y) : 0u;
+            dr[j] = (interior && R) ? census_at(sr, x, y) : 0u;
+            int gm = 0;
+            if (interior) {
+                gm = abs(int(sl[y][x + 1]) - int(sl[y][x - 1])) +
+                     abs(int(sl[y + 1][x]) - int(sl[y - 1][x]));
+            }
+            mk[j] = (interior && gm >= thr) ? 1 : 0;
+            cnt += mk[j];
+        }
+        const long long base = f * g.pixels + (long long)v * W + ub;
+        const bool vec = (ub + 3 < W) && ((base & 3) == 0);
+        if (vec) {
+            if (cl) *reinterpret_cast<uint4*>(cl + base) = make_uint4(dl[0], dl[1], dl[2], dl[3]);
+            if (cr && R) *reinterpret_cast<uint4*>(cr + base) = make_uint4(dr[0], dr[1], dr[2], dr[3]);
+            if (mask) *reinterpret_cast<uchar4*>(mask + base) = make_uchar4(mk[0], mk[1], mk[2], mk[3]);
+        } else {
+            for (int j = 0; j < 4 && ub + j < W; ++j) {
+                if (cl) cl[base + j] = dl[j];
+                if (cr && R) cr[base + j] = dr[j];
+                if (mask) mask[base + j] = mk[j];
+            }
+        }
+    }
+    if (mask_count) {
+        cnt = __reduce_add_sync(0xffffffffu, cnt);
+        if (threadIdx.x == 0) warp_cnt[threadIdx.y] = cnt;
+        __syncthreads();
+        if (tid == 0) {
+            int s = 0;
+            for (int i = 0; i < 8; ++i) s += warp_cnt[i];
+            if (s) atomicAdd(mask_count + f, s);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- K2
+
+// Bresenham circle of radius 3, clockwise from 12 o'clock (sparse.cpp:12-15).
+__constant__ int8_t c_ring_u[16] = {0, 1, 2, 3, 3, 3, 2, 1, 0, -1, -2, -3, -3, -3, -2, -1};
+__constant__ int8_t c_ring_v[16] = {-3, -3, -2, -1, 0, 1, 2, 3, 3, 3, 2, 1, 0, -1, -2, -3};
+
+__device__ __forceinline__ bool arc9(unsigned m16) {
+    // contiguous run >= 9 on the 16-ring (sparse.cpp:22-36): x has a run of
+    // length >= 9 iff the 9-fold AND of its rotations is non-zero.
+    unsigned r = m16 | (m16 << 16);
+    unsigned a = r;
+#pragma unroll
+    for (int s = 1; s < 9; ++s) a &= r >> s;
+    return (a & 0xffffu) != 0;
+}
+
+// Segment test at (u, v) (sparse.cpp:94-122); returns the score (> 0) or 0.
+__device__ __forceinline__ int corner_score(const uint8_t* __restrict__ L, int W, int u, int v,
+                                            int t) {
+    const int c = __ldg(L + (long long)v * W + u);
+    const int hi = c + t, lo = c - t;
+    int p[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) p[k] = __ldg(L + (long long)(v + c_ring_v[k]) * W + (u + c_ring_u[k]));
+    const int nb = (p[0] > hi) + (p[4] > hi) + (p[8] > hi) + (p[12] > hi);
+    const int nd = (p[0] < lo) + (p[4] < lo) + (p[8] < lo) + (p[12] < lo);
+    if (nb < 2 && nd < 2) return 0;
+    unsigned bright = 0, dark = 0;
+    int score = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        bright |= unsigned(p[k] > hi) << k;
+        dark |= unsigned(p[k] < lo) << k;
+        score += max(0, abs(p[k] - c) - t);
+    }
+    if (!arc9(bright) && !arc9(dark)) return 0;
+    return score;  // >= 9 for any accepted corner
+}
+
+__device__ __forceinline__ unsigned long long corner_key(int score, int u, int v) {
+    return (unsigned long long)(4095 - score) << 40 | (unsigned long long)v << 20 |
+           (unsigned long long)u;
+}
+
+// Pixel range [lo, hi) of bin b among nb bins over an axis of n pixels,
+// intersected with [3, n-3): bin(x) = min(nb-1, x*nb/n) (sparse.cpp:124-125).
+__device__ __forceinline__ void bin_range(int b, int nb, int n, int& lo, int& hi) {
+    lo = (b * n + nb - 1) / nb;
+    hi = (b == nb - 1) ? n : ((b + 1) * n + nb - 1) / nb;
+    lo = max(lo, 3);
+    hi = min(hi, n - 3);
+}
+
+__device__ __forceinline__ unsigned long long block_min_u64(unsigned long long x,
+                                                            unsigned long long* red) {
+    x = warp_min_u64(x);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) red[w] = x;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        unsigned long long y = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : kEmptyCell;
+        y = warp_min_u64(y);
+        if (threadIdx.x == 0) red[32] = y;
+    }
+    __syncthreads();
+    return red[32];
+}
+
+template <int LK>
+__global__ void __launch_bounds__(256) k_corner_bins(const uint8_t* __restrict__ left, FrameGeom g,
+                                                     int t, int cap,
+                                                     unsigned long long* __restrict__ bin_keys,
+                                                     int* __restrict__ bin_count) {
+    __shared__ unsigned long long lists[256][LK];
+    __shared__ unsigned long long red[33];
+    const int f = blockIdx.y, bin = blockIdx.x;
+    const int bu = bin % 12, bv = bin / 12;
+    int ulo, uhi, vlo, vhi;
+    bin_range(bu, 12, g.width, ulo, uhi);
+    bin_range(bv, 10, g.height, vlo, vhi);
+    const uint8_t* L = left + f * g.pixels;
+    unsigned long long best[LK];
+#pragma unroll
+    for (int k = 0; k < LK; ++k) best[k] = kEmptyCell;
+    const int bw = uhi - ulo, bh = vhi - vlo;
+    if (bw > 0 && bh > 0) {
+        const int n = bw * bh;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            const int v = vlo + i / bw, u = ulo + i % bw;
+            const int s = corner_score(L, g.width, u, v, t);
+            if (s == 0) continue;
+            unsigned long long key = corner_key(s, u, v);
+            if (key >= best[LK - 1]) continue;
+#pragma unroll
+            for (int k = 0; k < LK; ++k) {  // sorted insertion
+                const unsigned long long lo = key < best[k] ? key : best[k];
+                const unsigned long long hi = key < best[k] ? best[k] : key;
+                best[k] = lo;
+                key = hi;
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < LK; ++k) lists[threadIdx.x][k] = best[k];
+    int head = 0;
+    int out = 0;
+    for (; out < cap; ++out) {
+        const unsigned long long mine = head < LK ? lists[threadIdx.x][head] : kEmptyCell;
+        const unsigned long long m = block_min_u64(mine, red);
+        if (m == kEmptyCell) break;
+        if (mine == m) ++head;  // keys are unique pixels: exactly one owner
+        if (threadIdx.x == 0) bin_keys[((long long)f * 120 + bin) * cap + out] = m;
+    }
+    if (threadIdx.x == 0) bin_count[f * 120 + bin] = out;
+}
+
+// Generic per-bin selection for caps above the register top-k width: all
+// corner keys of the bin go to global scratch, then `cap` block-min rounds.
+__global__ void __launch_bounds__(256) k_corner_bins_generic(
+    const uint8_t* __restrict__ left, FrameGeom g, int t, int cap,
+    unsigned long long* __restrict__ scratch, long long scratch_stride,
+    unsigned long long* __restrict__ bin_keys, int* __restrict__ bin_count) {
+    __shared__ unsigned long long red[33];
+    __shared__ int n_keys;
+    const int f = blockIdx.y, bin = blockIdx.x;
+    const int bu = bin % 12, bv = bin / 12;
+    int ulo, uhi, vlo, vhi;
+    bin_range(bu, 12, g.width, ulo, uhi);
+    bin_range(bv, 10, g.height, vlo, vhi);
+    const uint8_t* L = left + f * g.pixels;
+    unsigned long long* sc = scratch + ((long long)f * 120 + bin) * scratch_stride;
+    if (threadIdx.x == 0) n_keys = 0;
+    __syncthreads();
+    const int bw = uhi - ulo, bh = vhi - vlo;
+    if (bw > 0 && bh > 0) {
+        const int n = bw * bh;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            const int v = vlo + i / bw, u = ulo + i % bw;
+            const int s = corner_score(L, g.width, u, v, t);
+            if (s == 0) continue;
+            sc[atomicAdd(&n_keys, 1)] = corner_key(s, u, v);
+        }
+    }
+    __syncthreads();
+    const int nk = n_keys;
+    unsigned long long last = 0;
+    int out = 0;
+    for (; out < cap && out < nk; ++out) {
+        unsigned long long mine = kEmptyCell;
+        for (int i = threadIdx.x; i < nk; i += blockDim.x) {
+            const unsigned long long k = sc[i];
+            if ((out == 0 || k > last) && k < mine) mine = k;
+        }
+        const unsigned long long m = block_min_u64(mine, red);
+        if (m == kEmptyCell) break;
+        last = m;
+        if (threadIdx.x == 0) bin_keys[((long long)f * 120 + bin) * cap + out] = m;
+    }
+    if (threadIdx.x == 0) bin_count[f * 120 + bin] = out;
+}
+
+// Bitonic sort of n (power of two) keys by one block; data in shared or global memory.
+__device__ void bitonic_sort(unsigned long long* d, int n) {
+    for (int k = 2; k <= n; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < n; i += blockDim.x) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const unsigned long long a = d[i], b = d[ixj];
+                    const bool up = (i & k) == 0;
+                    if ((a > b) == up) {
+                        d[i] = b;
+                        d[ixj] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_candidate_sort(
+    const unsigned long long* __restrict__ bin_keys, const int* __restrict__ bin_count, int cap,
+    int n_pow2, unsigned long long* __restrict__ global_buf, int* __restrict__ cand_u,
+    int* __restrict__ cand_v, float* __restrict__ cand_score, int* __restrict__ cand_count,
+    int cand_stride) {
+    extern __shared__ unsigned long long sm_keys[];
+    __shared__ int offs[121];
+    const int f = blockIdx.x;
+    unsigned long long* keys = global_buf ? global_buf + (long long)f * n_pow2 : sm_keys;
+    if (threadIdx.x == 0) {
+        int s = 0;
+        for (int b = 0; b < 120; ++b) {
+            offs[b] = s;
+            s += bin_count[f * 120 + b];
+        }
+        offs[120] = s;
+    }
+    __syncthreads();
+    const int n = offs[120];
+    for (int i = threadIdx.x; i < n_pow2; i += blockDim.x) keys[i] = kEmptyCell;
+    __syncthreads();
+    for (int b = 0; b < 120; ++b) {
+        const int c = offs[b + 1] - offs[b];
+        for (int i = threadIdx.x; i < c; i += blockDim.x)
+            keys[offs[b] + i] = bin_keys[((long long)f * 120 + b) * cap + i];
+    }
+    __syncthreads();
+    bitonic_sort(keys, n_pow2);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const unsigned long long k = keys[i];
+        const long long o = (long long)f * cand_stride + i;
+        cand_u[o] = int(k & 0xfffff);
+        cand_v[o] = int((k >> 20) & 0xfffff);
+        if (cand_score) cand_score[o] = float(4095 - int(k >> 40));
+    }
+    if (threadIdx.x == 0) cand_count[f] = n;
+}
+
+}  // namespace
+
+int launch_frontend(const uint8_t* left, const uint8_t* right, FrameGeom g, int frames,
+                    int grad_threshold, uint8_t* mask, uint32_t* cl, uint32_t* cr,
+                    int* mask_count, cudaStream_t st) {
+    dim3 grid((g.width + kTileW - 1) / kTileW, (g.height + kTileH - 1) / kTileH, frames);
+    k_frontend<<<grid, dim3(32, 8), 0, st>>>(left, right, g, grad_threshold, mask, cl, cr,
+                                             mask_count);
+    return 1;
+}
+
+long long candidate_scratch_stride(FrameGeom g) {
+    const long long bw = (g.width + 11) / 12 + 1, bh = (g.height + 9) / 10 + 1;
+    return bw * bh;
+}
+
+int launch_candidates(const uint8_t* left, FrameGeom g, int frames, int corner_threshold, int cap,
+                      unsigned long long* bin_keys, int* bin_count, unsigned long long* scratch,
+                      long long scratch_stride, int* cand_u, int* cand_v, float* cand_score,
+                      int* cand_count, int cand_stride, cudaStream_t st) {
+    dim3 grid(120, frames);
+    if (cap <= 4) {
+        k_corner_bins<4><<<grid, 256, 0, st>>>(left, g, corner_threshold, cap, bin_keys, bin_count);
+    } else if (cap <= 8) {
+        k_corner_bins<8><<<grid, 256, 0, st>>>(left, g, corner_threshold, cap, bin_keys, bin_count);
+    } else {
+        k_corner_bins_generic<<<grid, 256, 0, st>>>(left, g, corner_threshold, cap, scratch,
+                                                    scratch_stride, bin_keys, bin_count);
+    }
+    const int n = 120 * cap;
+    int n_pow2 = 1;
+    while (n_pow2 < n) n_pow2 <<= 1;
+    const bool in_smem = n_pow2 <= 8192;
+    const size_t smem = in_smem ? size_t(n_pow2) * 8 : 0;
+    if (in_smem && smem > 48 * 1024) {
+        cudaFuncSetAttribute(k_candidate_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(smem));
+    }
+    // Large caps sort in global memory: reuse the corner scratch (>= n_pow2 keys per frame).
+    k_candidate_sort<<<frames, 1024, smem, st>>>(bin_keys, bin_count, cap, n_pow2,
+                                                 in_smem ? nullptr : scratch, cand_u, cand_v,
+                                                 cand_score, cand_count, cand_stride);
+    return 2;
+}
+
+}  // namespace ps

@@ -1,0 +1,112 @@
+// launch.hpp — host-side launchers of the sm_100a kernels (one per kernel
+// family).  Every launcher enqueues on `st` and returns the number of kernel
+// launches it issued, so the engine can report its own launch count.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace ps {
+
+// K1 — gradient mask + census(L) + census(R), fused over 128x8 tiles
+// (proj/src/image.cpp:43-60, proj/src/census.cpp:10-41).  Any of mask / cl /
+// cr / right may be null to skip that output.
+int launch_frontend(const uint8_t* left, const uint8_t* right, FrameGeom g, int frames,
+                    int grad_threshold, uint8_t* mask, uint32_t* cl, uint32_t* cr,
+                    int* mask_count, cudaStream_t st);
+
+// K2 — segment-test corners, 12x10 binning, per-bin top-`cap` and the
+// global (score desc, v, u) sort (proj/src/sparse.cpp:84-146).
+// Writes cand_u/v/score[f*cand_stride + i] and cand_count[f].
+// `scratch` must hold frames*120*max_bin_pixels keys when cap > 8 (else unused).
+int launch_candidates(const uint8_t* left, FrameGeom g, int frames, int corner_threshold,
+                      int cap, unsigned long long* bin_keys, int* bin_count,
+                      unsigned long long* scratch, long long scratch_stride, int* cand_u,
+                      int* cand_v, float* cand_score, int* cand_count, int cand_stride,
+                      cudaStream_t st);
+long long candidate_scratch_stride(FrameGeom g);
+
+// K3 — epipolar census matching, warp per candidate (proj/src/sparse.cpp:44-80,148-195).
+int launch_match(const uint32_t* cl, const uint32_t* cr, FrameGeom g, int frames, int max_disp,
+                 const CostTables& tab, const int* cand_u, const int* cand_v,
+                 const int* cand_count, int cand_stride, int max_candidates, uint8_t* ok,
+                 int* disp, int* costk, cudaStream_t st);
+
+// Support list compaction of match results (seed path): supports of frame f
+// are written at su/sv/sd[f*scap + base[f] + k] in candidate order; taken
+// bits set; out_count[f] = base[f] + accepted (base may be null = 0).
+int launch_emit_matches(const int* cand_u, const int* cand_v, const int* cand_count,
+                        int cand_stride, int max_candidates, const uint8_t* ok, const int* disp,
+                        FrameGeom g, int frames, uint32_t* taken, int* su, int* sv, double* sd,
+                        int scap, const int* base, const int* base2, int* out_count,
+                        int* chunk_buf, cudaStream_t st);
+
+// K5+K6 — per-triangle plane fit (binary64, source order, no FMA;
+// proj/src/mesh.cpp:12-26) and exact top-left rasterisation into the
+// triangle lookup (mesh.cpp:58-107), then hull-vertex pinning (mesh.cpp:109-122).
+// Triangles are flat over frames: frame f owns [tri_off[f], tri_off[f+1]).
+int launch_mesh(const int* tris, const int* tri_off, int frames, long long total_tris,
+                const int* su, const int* sv, const double* sd, int scap, FrameGeom g,
+                double* planes, int32_t* lookup, int* err_flag, cudaStream_t st);
+
+// K7 (+K9 when last) — fused interpolate / costEvaluation / disparityRefinement
+// with per-cell packed-key atomicMin grids and the trace reduction
+// (mesh.cpp:149-182, pipeline.cpp:33-86,183-191).
+struct RefineArgs {
+    FrameGeom g;
+    int frames;
+    const uint8_t* mask;
+    const int32_t* lookup;
+    const double* planes;
+    const uint32_t* cl;
+    const uint32_t* cr;
+    float max_disp;
+    int cell;
+    int cols;
+    int cells_per_frame;
+    float* Df;
+    uint8_t* Dv;
+    float* Cf;
+    unsigned long long* Cg;
+    unsigned long long* Cb;
+    unsigned long long* trace_sum;  // [frames] for this iteration (stride trace_stride)
+    unsigned* trace_valid;
+    int trace_stride;
+    float* dense;       // LAST only
+    uint8_t* dense_valid;
+};
+int launch_refine(const RefineArgs& a, const CostTables& tab, bool last, cudaStream_t st);
+
+// K8 — resampling: confident cells (row-major) appended as supports,
+// occupied invalid cells compacted into the re-match list
+// (proj/src/pipeline.cpp:88-129).  S_old[f] is the current support count.
+int launch_resample_confident(const unsigned long long* Cg, int cells_per_frame, FrameGeom g,
+                              int frames, const int32_t* lookup, const double* planes,
+                              uint32_t* taken, int* su, int* sv, double* sd, int scap,
+                              const int* S_old, int* conf_count, int* chunk_buf, cudaStream_t st);
+int launch_resample_invalid(const unsigned long long* Cb, int cells_per_frame, FrameGeom g,
+                            int frames, int* rem_u, int* rem_v, int rem_stride, int* rem_count,
+                            int* chunk_buf, cudaStream_t st);
+// S[f] = S[f] + a[f] + b[f]
+int launch_add_counts(int* S, const int* a, const int* b, int frames, cudaStream_t st);
+
+// Packs supports [S_prev[f], S_now[f]) of every frame into out (u,v pairs) at off[f].
+int launch_pack_new_supports(const int* su, const int* sv, int scap, const int* S_prev,
+                             const int* S_now, const int* off, int frames, int max_new,
+                             int2* out, cudaStream_t st);
+
+// Stage-API helpers (single frame, host-visible semantics).
+int launch_interpolate(const int32_t* lookup, const double* planes, FrameGeom g,
+                       const uint8_t* mask, float max_disp, float* value, uint8_t* valid,
+                       cudaStream_t st);
+int launch_cost_eval(const uint32_t* cl, const uint32_t* cr, FrameGeom g, const float* value,
+                     const uint8_t* valid, const uint8_t* mask, const CostTables& tab, float* cost,
+                     cudaStream_t st);
+
+}  // namespace ps
+
+namespace ps {
+int launch_fill_f32(float* p, long long n, float x, cudaStream_t st);
+}  // namespace ps
