@@ -380,6 +380,34 @@ int ref_run_batch(int n, const uint8_t* left, const uint8_t* right, int w, int h
     return 0;
 }
 
+// renderScene (proj/src/synth.cpp:148-227) for the fixture generator:
+// kind 0 = flat(p0), 1 = slanted(p0, p1, p2), 2 = steps(p0, p1).
+int ref_render_scene(int kind, double p0, double p1, double p2, int w, int h, uint32_t seed,
+                     float max_disparity, uint8_t* left, uint8_t* right, float* gt,
+                     uint8_t* gt_valid) {
+    try {
+        PlanarScene s = kind == 0   ? PlanarScene::flat(p0, w, h, seed)
+                        : kind == 1 ? PlanarScene::slanted(p0, p1, p2, w, h, seed)
+                                    : PlanarScene::steps(p0, p1, w, h, seed);
+        s.maxDisparity = max_disparity;
+        RenderedScene r = renderScene(s);
+        std::memcpy(left, r.left.data().data(), std::size_t(w) * h);
+        std::memcpy(right, r.right.data().data(), std::size_t(w) * h);
+        copyMap(r.groundTruth, gt, gt_valid);
+        return PS_OK;
+    } catch (const std::exception& e) {
+        return statusOf(e);
+    }
+}
+
+// wtaOracle (proj/src/synth.cpp:229-256): exhaustive census WTA lower bound.
+void ref_wta(const uint8_t* left, const uint8_t* right, int w, int h, const uint8_t* mask,
+             int max_disparity, float* disp, uint8_t* valid, float* cost) {
+    auto r = wtaOracle(toImage(left, w, h), toImage(right, w, h), toMask(mask, w, h), max_disparity);
+    copyMap(r.first, disp, valid);
+    std::memcpy(cost, r.second.values().data(), sizeof(float) * std::size_t(w) * h);
+}
+
 // The reference's own timing harness (proj/src/eval.cpp:144-177): pinned
 // core, one warm-up, sorted samples; returns the median ms of `repeats` runs.
 double ref_benchmark_run(const uint8_t* left, const uint8_t* right, int w, int h,
