@@ -21,6 +21,7 @@
 #include "planestereo/mesh.hpp"
 #include "planestereo/pipeline.hpp"
 #include "planestereo/sparse.hpp"
+#include "planestereo/synth.hpp"
 #include "planestereo_c.h"
 
 using namespace planestereo;
