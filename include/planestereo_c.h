@@ -143,6 +143,9 @@ ps_status ps_reset_kernel_stats(ps_ctx* ctx);
 ps_status ps_get_kernel_stats(ps_ctx* ctx, ps_kernel_stat* out, int capacity, int* count);
 /* Kernel launches issued by this context since creation. */
 long long ps_launch_count(const ps_ctx* ctx);
+/* The context's CUDA stream (a cudaStream_t), so callers can bracket a
+ * pipeline run with their own CUDA events on the stream it runs on. */
+void* ps_ctx_stream(const ps_ctx* ctx);
 
 /* ------------------------------------------------------------ stage API */
 /* gradientMask (proj/src/image.cpp:43-60): member[P] in {0,1}; count = M. */

@@ -274,6 +274,10 @@ class Context:
     def launch_count(self) -> int:
         return int(self._lib.ps_launch_count(self._h))
 
+    def stream_handle(self) -> int:
+        """cudaStream_t of this context (for torch.cuda.ExternalStream)."""
+        return int(self._lib.ps_ctx_stream(self._h) or 0)
+
     # ------------------------------------------------------------ stages
     def gradient_mask(self, image, threshold: int):
         img = _u8(image)

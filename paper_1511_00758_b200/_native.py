@@ -101,6 +101,7 @@ SIGNATURES = {
     "ps_reset_kernel_stats": (I, [P]),
     "ps_get_kernel_stats": (I, [P, P, I, P]),
     "ps_launch_count": (C.c_longlong, [P]),
+    "ps_ctx_stream": (C.c_void_p, [P]),
     "ps_gradient_mask": (I, [P, P, I, I, I, P, P]),
     "ps_census": (I, [P, P, I, I, P]),
     "ps_detect_candidates": (I, [P, P, I, I, P, P, P, P, I, P]),

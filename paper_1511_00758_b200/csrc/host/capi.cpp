@@ -202,6 +202,10 @@ long long ps_launch_count(const ps_ctx* ctx) {
     return (ctx && ctx->engine) ? ctx->engine->launches() : 0;
 }
 
+void* ps_ctx_stream(const ps_ctx* ctx) {
+    return (ctx && ctx->engine) ? static_cast<void*>(ctx->engine->stream()) : nullptr;
+}
+
 // ------------------------------------------------------------------ stages
 
 ps_status ps_gradient_mask(ps_ctx* ctx, const uint8_t* image, int width, int height,

@@ -25,12 +25,15 @@ namespace {
 
 constexpr int kWarpsPerBlock = 8;
 
-__device__ __forceinline__ long long floor_div(long long a, long long b) {
-    long long q = a / b;
+// floorDiv / ceilDiv of mesh.cpp:30-40, for 32- or 64-bit operands.
+template <class T>
+__device__ __forceinline__ T floor_div(T a, T b) {
+    T q = a / b;
     if ((a % b != 0) && ((a < 0) != (b < 0))) --q;
     return q;
 }
-__device__ __forceinline__ long long ceil_div(long long a, long long b) { return -floor_div(-a, b); }
+template <class T>
+__device__ __forceinline__ T ceil_div(T a, T b) { return -floor_div<T>(-a, b); }
 
 __device__ __forceinline__ int frame_of(const int* __restrict__ tri_off, int frames, long long t) {
     int lo = 0, hi = frames - 1;  // largest f with tri_off[f] <= t
@@ -41,6 +44,9 @@ __device__ __forceinline__ int frame_of(const int* __restrict__ tri_off, int fra
     return lo;
 }
 
+// Int = int when every edge-function value fits in 32 bits (W, H < 2^14),
+// long long otherwise; the results are identical, 32-bit division is faster.
+template <class Int>
 __global__ void __launch_bounds__(256) k_raster(const int* __restrict__ tris,
                                                 const int* __restrict__ tri_off, int frames,
                                                 long long total, const int* __restrict__ su,
@@ -86,7 +92,7 @@ __global__ void __launch_bounds__(256) k_raster(const int* __restrict__ tris,
     const int W = g.width, H = g.height;
     const int vmin = max(0, min(y[0], min(y[1], y[2])));
     const int vmax = min(H - 1, max(y[0], max(y[1], y[2])));
-    long long A[3], bias[3];
+    Int A[3], bias[3];
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
         const int j = (i + 1) % 3;
@@ -94,13 +100,17 @@ __global__ void __launch_bounds__(256) k_raster(const int* __restrict__ tris,
         bias[i] = ((y[j] < y[i]) || (y[j] == y[i] && x[j] > x[i])) ? 0 : 1;
     }
     int32_t* lk = lookup + f * g.pixels;
-    for (int v = vmin; v <= vmax; ++v) {
-        long long lo = 0, hi = W - 1;
-        bool empty = false;
+    // 32 rows at a time: lane r computes the exact span of row r0 + r
+    // (mesh.cpp:84-103), then the warp fills each non-empty row with
+    // coalesced stores.
+    for (int r0 = vmin; r0 <= vmax; r0 += 32) {
+        const int v = r0 + lane;
+        Int lo = 0, hi = W - 1;
+        bool empty = v > vmax;
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
             const int j = (i + 1) % 3;
-            const long long K = (long long)(x[j] - x[i]) * (v - y[i]) + (long long)(y[j] - y[i]) * x[i];
+            const Int K = Int(x[j] - x[i]) * Int(v - y[i]) + Int(y[j] - y[i]) * Int(x[i]);
             if (A[i] > 0) {
                 lo = max(lo, ceil_div(bias[i] - K, A[i]));
             } else if (A[i] < 0) {
@@ -109,9 +119,16 @@ __global__ void __launch_bounds__(256) k_raster(const int* __restrict__ tris,
                 empty = true;
             }
         }
-        if (empty || lo > hi) continue;
-        int32_t* row = lk + (long long)v * W;
-        for (long long u = lo + lane; u <= hi; u += 32) row[u] = int32_t(t);
+        unsigned rows = __ballot_sync(0xffffffffu, !empty && lo <= hi);
+        const int lo32 = int(lo), hi32 = int(hi);
+        while (rows) {
+            const int r = __ffs(rows) - 1;
+            rows &= rows - 1;
+            const int l = __shfl_sync(0xffffffffu, lo32, r);
+            const int h = __shfl_sync(0xffffffffu, hi32, r);
+            int32_t* row = lk + (long long)(r0 + r) * W;
+            for (int u = l + lane; u <= h; u += 32) row[u] = int32_t(t);
+        }
     }
 }
 
@@ -141,9 +158,13 @@ int launch_mesh(const int* tris, const int* tri_off, int frames, long long total
                 double* planes, int32_t* lookup, int* err_flag, cudaStream_t st) {
     if (total_tris <= 0) return 0;
     const long long blocks = (total_tris + kWarpsPerBlock - 1) / kWarpsPerBlock;
-    k_raster<<<unsigned(blocks), 32 * kWarpsPerBlock, 0, st>>>(tris, tri_off, frames, total_tris,
-                                                               su, sv, sd, scap, g, planes, lookup,
-                                                               err_flag);
+    if (g.width < (1 << 14) && g.height < (1 << 14)) {
+        k_raster<int><<<unsigned(blocks), 32 * kWarpsPerBlock, 0, st>>>(
+            tris, tri_off, frames, total_tris, su, sv, sd, scap, g, planes, lookup, err_flag);
+    } else {
+        k_raster<long long><<<unsigned(blocks), 32 * kWarpsPerBlock, 0, st>>>(
+            tris, tri_off, frames, total_tris, su, sv, sd, scap, g, planes, lookup, err_flag);
+    }
     const long long corners = 3 * total_tris;
     const unsigned pb = unsigned((corners + 255) / 256);
     k_pin<<<pb, 256, 0, st>>>(tris, tri_off, frames, total_tris, su, sv, scap, g, lookup, 0);

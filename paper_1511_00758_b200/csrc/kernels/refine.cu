@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(256) k_refine(RefineArgs a, CostTables tab) {
     const int f = blockIdx.y;
     const long long P = a.g.pixels;
     const int W = a.g.width;
-    const long long i0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    const int i0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;  // per-frame index (P < 2^31)
     unsigned long long tsum = 0;
     unsigned tvalid = 0;
     if (i0 < P) {
@@ -73,8 +73,8 @@ __global__ void __launch_bounds__(256) k_refine(RefineArgs a, CostTables tab) {
                 for (int j = 0; j < 4; ++j) lk[j] = (i0 + j < P) ? a.lookup[fb + i0 + j] : -1;
             }
         }
-        int v = int(i0 / W);
-        int u = int(i0 - (long long)v * W);
+        const int v = i0 / W;
+        const int u = i0 - v * W;
         float dit[4];
         bool ok[4];
 #pragma unroll
