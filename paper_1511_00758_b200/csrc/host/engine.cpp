@@ -1,13 +1,14 @@
 // engine.cpp — batched B200 pipeline (see engine.hpp).
 //
 // Stage order per batch mirrors planestereo::run (proj/src/pipeline.cpp:131-203):
-//   K1 frontend -> K2 candidates -> K3 seed match -> seed compaction
-//   for it in 1..iterations:
+//   K1 frontend -> K2 candidates -> K3 seed match -> seed compaction     (all frames)
+//   for it in 1..iterations:  for each frame group g (own stream):
 //       supports delta D2H -> host Delaunay per frame (thread pool) -> triangles H2D
 //       K5/K6 mesh (planes + lookup) -> K7 refine (+K9 dense on the last iteration)
 //       if not last: K8 resample (confident append, invalid cells -> K3 re-match -> append)
 //   trace reduction D2H.
-// Every device stage is one launch over all frames of the batch.
+// The device stages of group g are enqueued asynchronously, so they run while
+// the host triangulates group g+1 (a software pipeline over groups).
 #include "engine.hpp"
 
 #include <algorithm>
@@ -79,6 +80,10 @@ ps_status validate_config(const ps_config& c, unsigned flags, std::string& msg) 
         msg = "threads must be >= 1";
         return PS_INVALID_CONFIG;
     }
+    if (c.max_disparity > 65535) {  // packed (k << 16 | d) warp keys in K3
+        msg = "max disparity above 65535 is not supported by this build";
+        return PS_INVALID_CONFIG;
+    }
     return PS_OK;
 }
 
@@ -113,11 +118,10 @@ bool trace_fixed_exact(float cost_high) {
     return x == std::floor(x);
 }
 
-struct Engine::Timer {};
-
 Engine::Engine(int device) : device_(device) {
     cudaSetDevice(device_);
     cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking);
+    for (FrameGroup& g : groups_) cudaStreamCreateWithFlags(&g.st, cudaStreamNonBlocking);
     const int hw = std::max(1u, std::thread::hardware_concurrency());
     pool_ = new ThreadPool(hw);
     ws_.resize(pool_->size());
@@ -125,20 +129,25 @@ Engine::Engine(int device) : device_(device) {
 
 Engine::~Engine() {
     cudaSetDevice(device_);
-    if (st_) cudaStreamSynchronize(st_);
+    cudaDeviceSynchronize();
     DevBuf* bufs[] = {&dL_, &dR_, &dMask_, &dMaskCount_, &dCL_, &dCR_, &dDf_, &dDv_, &dCf_,
                       &dDense_, &dDenseV_, &dLookup_, &dSu_, &dSv_, &dSd_, &dS_, &dSnext_,
-                      &dSprev_, &dTaken_, &dTri_, &dTriOff_, &dPlanes_, &dCg_, &dCb_, &dBinKeys_,
-                      &dBinCount_, &dScratch_, &dCandU_, &dCandV_, &dCandCount_, &dOk_, &dDisp_,
-                      &dRemU_, &dRemV_, &dRemCount_, &dConf_, &dChunk_, &dTraceSum_,
-                      &dTraceValid_, &dErr_, &dPack_, &dPackOff_, &s_a, &s_b, &s_c, &s_d, &s_e,
-                      &s_f, &s_g, &s_h, &s_i, &s_j};
+                      &dTaken_, &dCg_, &dCb_, &dBinKeys_, &dBinCount_, &dScratch_, &dCandU_,
+                      &dCandV_, &dCandCount_, &dOk_, &dDisp_, &dRemU_, &dRemV_, &dRemCount_,
+                      &dConf_, &dChunk_, &dTraceSum_, &dTraceValid_, &dErr_, &s_a, &s_b, &s_c,
+                      &s_d, &s_e, &s_f, &s_g, &s_h, &s_i, &s_j};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
-    HostBuf* hbufs[] = {&hS_, &hSprev_, &hPackOff_, &hPack_, &hTri_, &hTriOff_, &hTraceSum_,
-                        &hTraceValid_, &hMaskCount_, &hL_, &hR_};
+    HostBuf* hbufs[] = {&hS_, &hTraceSum_, &hTraceValid_, &hMaskCount_};
     for (HostBuf* b : hbufs)
         if (b->p) cudaFreeHost(b->p);
+    for (FrameGroup& g : groups_) {
+        for (DevBuf* b : {&g.dTri, &g.dTriOff, &g.dPlanes, &g.dPack, &g.dPackOff, &g.dSprev, &g.dChunk})
+            if (b->p) cudaFree(b->p);
+        for (HostBuf* b : {&g.hS, &g.hSprev, &g.hPackOff, &g.hPack, &g.hTri, &g.hTriOff})
+            if (b->p) cudaFreeHost(b->p);
+        if (g.st) cudaStreamDestroy(g.st);
+    }
     for (auto& p : pending_) {
         cudaEventDestroy(p.a);
         cudaEventDestroy(p.b);
@@ -153,7 +162,7 @@ T* Engine::dev(DevBuf& b, size_t count) {
     const size_t need = std::max<size_t>(count * sizeof(T), 256);
     if (b.bytes < need) {
         if (b.p) {
-            cudaStreamSynchronize(st_);
+            cudaDeviceSynchronize();
             cudaFree(b.p);
         }
         b.p = nullptr;
@@ -172,7 +181,7 @@ T* Engine::host(HostBuf& b, size_t count) {
     const size_t need = std::max<size_t>(count * sizeof(T), 256);
     if (b.bytes < need) {
         if (b.p) {
-            cudaStreamSynchronize(st_);
+            cudaDeviceSynchronize();
             cudaFreeHost(b.p);
         }
         b.p = nullptr;
@@ -201,13 +210,26 @@ ps_status Engine::check(cudaError_t e, const char* what) {
     return fail(PS_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-ps_status Engine::sync(const char* what) {
-    cudaError_t e = cudaStreamSynchronize(st_);
+ps_status Engine::sync(const char* what) { return sync(st_, what); }
+
+ps_status Engine::sync(cudaStream_t s, const char* what) {
+    cudaError_t e = cudaStreamSynchronize(s);
     if (e == cudaSuccess) e = cudaGetLastError();
     return check(e, what);
 }
 
-void Engine::begin_kernel(const char* name, double bytes) {
+cudaEvent_t Engine::take_event() {
+    cudaEvent_t e;
+    if (!event_pool_.empty()) {
+        e = event_pool_.back();
+        event_pool_.pop_back();
+    } else {
+        cudaEventCreate(&e);
+    }
+    return e;
+}
+
+void Engine::begin_kernel(const char* name, double bytes, cudaStream_t s) {
     if (!profiling_) return;
     int idx = -1;
     for (size_t i = 0; i < stats_.size(); ++i)
@@ -218,28 +240,16 @@ void Engine::begin_kernel(const char* name, double bytes) {
     }
     stats_[idx].bytes += bytes;
     stats_[idx].launches += 1;
-    cudaEvent_t a;
-    if (!event_pool_.empty()) {
-        a = event_pool_.back();
-        event_pool_.pop_back();
-    } else {
-        cudaEventCreate(&a);
-    }
-    cudaEventRecord(a, st_);
+    cudaEvent_t a = take_event();
+    cudaEventRecord(a, s);
     pending_stat_ = idx;
     pending_start_ = a;
 }
 
-void Engine::end_kernel() {
+void Engine::end_kernel(cudaStream_t s) {
     if (!profiling_ || pending_stat_ < 0) return;
-    cudaEvent_t b;
-    if (!event_pool_.empty()) {
-        b = event_pool_.back();
-        event_pool_.pop_back();
-    } else {
-        cudaEventCreate(&b);
-    }
-    cudaEventRecord(b, st_);
+    cudaEvent_t b = take_event();
+    cudaEventRecord(b, s);
     pending_.push_back({pending_stat_, pending_start_, b});
     pending_stat_ = -1;
 }
@@ -325,15 +335,13 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     float* dCf = dev<float>(dCf_, size_t(F) * P);
     float* dDense = dev<float>(dDense_, size_t(F) * P);
     uint8_t* dDenseV = dev<uint8_t>(dDenseV_, size_t(F) * P);
-    int32_t* dLookup = dev<int32_t>(dLookup_, size_t(F) * P);
+    int32_t* dLookup = reinterpret_cast<int32_t*>(dev<int>(dLookup_, size_t(F) * P));
     int* dSu = dev<int>(dSu_, size_t(F) * scap_);
     int* dSv = dev<int>(dSv_, size_t(F) * scap_);
     double* dSd = dev<double>(dSd_, size_t(F) * scap_);
-    dev<int>(dS_, F);
-    dev<int>(dSnext_, F);
-    int* dSprev = dev<int>(dSprev_, F);
+    int* dS = dev<int>(dS_, F);
+    int* dSnext = dev<int>(dSnext_, F);
     uint32_t* dTaken = dev<uint32_t>(dTaken_, size_t(F) * words);
-    int* dTriOff = dev<int>(dTriOff_, F + 1);
     unsigned long long* dCg = dev<unsigned long long>(dCg_, size_t(F) * cells_max);
     unsigned long long* dCb = dev<unsigned long long>(dCb_, size_t(F) * cells_max);
     unsigned long long* dBinKeys = dev<unsigned long long>(dBinKeys_, size_t(F) * 120 * cfg.per_bin_cap);
@@ -350,23 +358,19 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     int* dConf = dev<int>(dConf_, F);
     int* dChunk = dev<int>(dChunk_, size_t(F) * chunks + 1);
     unsigned long long* dTraceSum = dev<unsigned long long>(dTraceSum_, size_t(F) * iters);
-    unsigned* dTraceValid = reinterpret_cast<unsigned*>(dev<uint32_t>(dTraceValid_, size_t(F) * iters));
+    unsigned* dTraceValid = dev<uint32_t>(dTraceValid_, size_t(F) * iters);
     int* dErr = dev<int>(dErr_, 1);
-    int* dPackOff = dev<int>(dPackOff_, F);
     int* hS = host<int>(hS_, F);
-    int* hSprev = host<int>(hSprev_, F);
-    int* hPackOff = host<int>(hPackOff_, F);
-    int* hTriOff = host<int>(hTriOff_, F + 1);
     int* hMaskCount = host<int>(hMaskCount_, F);
     unsigned long long* hTraceSum =
         reinterpret_cast<unsigned long long*>(host<uint8_t>(hTraceSum_, size_t(F) * iters * 8));
     unsigned* hTraceValid = reinterpret_cast<unsigned*>(host<uint8_t>(hTraceValid_, size_t(F) * iters * 4));
-    void* must[] = {dMask, dMaskCount, dCL, dCR, dDf, dDv, dCf, dDense, dDenseV, dLookup, dSu, dSv,
-                    dSd, dS_.p, dSnext_.p, dSprev, dTaken, dTriOff, dCg, dCb, dBinKeys, dBinCount,
-                    dScratch, dCandU, dCandV, dCandCount, dOk, dDisp, dRemU, dRemV, dRemCount,
-                    dConf, dChunk, dTraceSum, dTraceValid, dErr, dPackOff, hS, hSprev, hPackOff,
-                    hTriOff, hMaskCount, hTraceSum, hTraceValid};
-    for (void* p : must)
+    const void* must[] = {dMask, dMaskCount, dCL, dCR, dDf, dDv, dCf, dDense, dDenseV, dLookup,
+                          dSu, dSv, dSd, dS, dSnext, dTaken, dCg, dCb, dBinKeys, dBinCount,
+                          dScratch, dCandU, dCandV, dCandCount, dOk, dDisp, dRemU, dRemV,
+                          dRemCount, dConf, dChunk, dTraceSum, dTraceValid, dErr, hS, hMaskCount,
+                          hTraceSum, hTraceValid};
+    for (const void* p : must)
         if (!p) return fail(PS_CUDA_ERROR, "allocation failed for a batch of " + std::to_string(F) +
                                                " frames of " + std::to_string(W) + "x" +
                                                std::to_string(H));
@@ -384,26 +388,26 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     launches_ += launch_fill_f32(dCf, (long long)F * P, cfg.cost_high, st_);
 
     // ---- K1 frontend (image.cpp:43-60, census.cpp:10-41)
-    begin_kernel("frontend", 11.0 * double(P) * F);
+    begin_kernel("frontend", 11.0 * double(P) * F, st_);
     launches_ += launch_frontend(dL, dR, g, F, cfg.gradient_threshold, dMask, dCL, dCR, dMaskCount, st_);
-    end_kernel();
+    end_kernel(st_);
     // ---- K2 candidates (sparse.cpp:84-146)
-    begin_kernel("candidates", double(P) * F);
+    begin_kernel("candidates", double(P) * F, st_);
     launches_ += launch_candidates(dL, g, F, cfg.corner_threshold, cfg.per_bin_cap, dBinKeys,
                                    dBinCount, dScratch, sc_stride, dCandU, dCandV, nullptr,
                                    dCandCount, cand_stride, st_);
-    end_kernel();
+    end_kernel(st_);
     // ---- K3 seed match (sparse.cpp:148-195) + ordered compaction
-    begin_kernel("match_seed", 0.0);
+    begin_kernel("match_seed", 0.0, st_);
     launches_ += launch_match(dCL, dCR, g, F, cfg.max_disparity, tab, dCandU, dCandV, dCandCount,
                               cand_stride, cand_stride, dOk, dDisp, nullptr, st_);
-    end_kernel();
-    begin_kernel("compact", 0.0);
+    end_kernel(st_);
+    begin_kernel("compact", 0.0, st_);
     launches_ += launch_emit_matches(dCandU, dCandV, dCandCount, cand_stride, cand_stride, dOk,
                                      dDisp, g, F, dTaken, dSu, dSv, dSd, scap_, nullptr, nullptr,
-                                     static_cast<int*>(dS_.p), dChunk, st_);
-    end_kernel();
-    ps_status s = check(cudaMemcpyAsync(hS, dS_.p, sizeof(int) * F, cudaMemcpyDeviceToHost, st_), "D2H S");
+                                     dS, dChunk, st_);
+    end_kernel(st_);
+    ps_status s = check(cudaMemcpyAsync(hS, dS, sizeof(int) * F, cudaMemcpyDeviceToHost, st_), "D2H S");
     if (s == PS_OK)
         s = check(cudaMemcpyAsync(hMaskCount, dMaskCount, sizeof(int) * F, cudaMemcpyDeviceToHost, st_),
                   "D2H M");
@@ -411,161 +415,236 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     if (s != PS_OK) return s;
 
     status_.assign(F, PS_OK);
+    final_count_.assign(F, 0);
     hu_.resize(F);
     hv_.resize(F);
     htri_.resize(F);
     for (int f = 0; f < F; ++f) {
         hu_[f].clear();
         hv_[f].clear();
-        hSprev[f] = 0;
         if (hS[f] < 3) status_[f] = PS_SEEDING_FAILED;  // pipeline.cpp:151-154
     }
     trace_.assign(size_t(F) * iters, ps_iter_stats{});
 
+    // ---- frame groups (software pipeline over streams)
+    const int G = std::max(1, std::min(kMaxGroups, (F + 31) / 32));
+    for (int gi = 0; gi < G; ++gi) {
+        FrameGroup& grp = groups_[gi];
+        grp.f0 = int((long long)F * gi / G);
+        grp.n = int((long long)F * (gi + 1) / G) - grp.f0;
+        grp.S = dS + grp.f0;
+        grp.Snext = dSnext + grp.f0;
+        grp.ntri.assign(grp.n, 0);
+        int* hs = host<int>(grp.hS, grp.n);
+        int* hsp = host<int>(grp.hSprev, grp.n);
+        if (!host<int>(grp.hPackOff, grp.n) || !host<int>(grp.hTriOff, grp.n + 1) ||
+            !dev<int>(grp.dTriOff, grp.n + 1) || !dev<int>(grp.dPackOff, grp.n) ||
+            !dev<int>(grp.dSprev, grp.n) || !dev<int>(grp.dChunk, size_t(grp.n) * chunks + 1) || !hs ||
+            !hsp)
+            return fail(PS_CUDA_ERROR, "allocation failed (group staging)");
+        for (int i = 0; i < grp.n; ++i) {
+            hs[i] = hS[grp.f0 + i];
+            hsp[i] = 0;
+        }
+    }
+
     for (int it = 1; it <= iters; ++it) {
-        const double tic = now_ms();
         const bool last = it == iters;
         const int cell = cell_of[it - 1];
-        if (it > 1) {
-            s = check(cudaMemcpyAsync(hS, dS_.p, sizeof(int) * F, cudaMemcpyDeviceToHost, st_), "D2H S");
-            if (s == PS_OK) s = sync("support count");
-            if (s != PS_OK) return s;
-        }
-        // ---- supports delta to the host
-        long long total_new = 0;
-        int max_new = 0;
-        for (int f = 0; f < F; ++f) {
-            hPackOff[f] = int(total_new);
-            const int n = hS[f] - hSprev[f];
-            total_new += n;
-            max_new = std::max(max_new, n);
-        }
-        int2* dPack = dev<int2>(dPack_, size_t(std::max<long long>(total_new, 1)));
-        int2* hPack = reinterpret_cast<int2*>(host<uint8_t>(hPack_, size_t(std::max<long long>(total_new, 1)) * 8));
-        if (!dPack || !hPack) return fail(PS_CUDA_ERROR, "allocation failed (support staging)");
-        s = check(cudaMemcpyAsync(dSprev, hSprev, sizeof(int) * F, cudaMemcpyHostToDevice, st_), "H2D Sprev");
-        if (s == PS_OK)
-            s = check(cudaMemcpyAsync(dPackOff, hPackOff, sizeof(int) * F, cudaMemcpyHostToDevice, st_),
-                      "H2D pack offsets");
-        if (s != PS_OK) return s;
-        launches_ += launch_pack_new_supports(dSu, dSv, scap_, dSprev, static_cast<int*>(dS_.p),
-                                              dPackOff, F, max_new, dPack, st_);
-        if (total_new > 0)
-            s = check(cudaMemcpyAsync(hPack, dPack, sizeof(int2) * total_new, cudaMemcpyDeviceToHost, st_),
-                      "D2H supports");
-        if (s == PS_OK) s = sync("support delta");
-        if (s != PS_OK) return s;
-
-        // ---- host Delaunay per frame (delaunay.cpp:288-325 contract)
-        std::vector<int> ntri(F, 0);
-        pool_->parallel_for(F, [&](int f, int worker) {
-            const int n = hS[f] - hSprev[f];
-            for (int i = 0; i < n; ++i) {
-                hu_[f].push_back(hPack[hPackOff[f] + i].x);
-                hv_[f].push_back(hPack[hPackOff[f] + i].y);
-            }
-            if (status_[f] != PS_OK) {
-                htri_[f].clear();
-                return;
-            }
-            const int t = delaunay(hu_[f].data(), hv_[f].data(), int(hu_[f].size()), htri_[f],
-                                   ws_[worker]);
-            if (t < 0) {
-                status_[f] = PS_ERROR;
-                htri_[f].clear();
-                return;
-            }
-            ntri[f] = t;
-        });
-        long long total_tri = 0;
-        for (int f = 0; f < F; ++f) {
-            hTriOff[f] = int(total_tri);
-            total_tri += ntri[f];
-        }
-        hTriOff[F] = int(total_tri);
-        int* hTri = host<int>(hTri_, size_t(std::max<long long>(total_tri, 1)) * 3);
-        int* dTri = dev<int>(dTri_, size_t(std::max<long long>(total_tri, 1)) * 3);
-        double* dPlanes = dev<double>(dPlanes_, size_t(std::max<long long>(total_tri, 1)) * 3);
-        if (!hTri || !dTri || !dPlanes) return fail(PS_CUDA_ERROR, "allocation failed (triangles)");
-        pool_->parallel_for(F, [&](int f, int) {
-            if (ntri[f] > 0)
-                std::memcpy(hTri + 3ll * hTriOff[f], htri_[f].data(), sizeof(int) * 3 * ntri[f]);
-        });
-        if (total_tri > 0)
-            s = check(cudaMemcpyAsync(dTri, hTri, sizeof(int) * 3 * total_tri, cudaMemcpyHostToDevice, st_),
-                      "H2D triangles");
-        if (s == PS_OK)
-            s = check(cudaMemcpyAsync(dTriOff, hTriOff, sizeof(int) * (F + 1), cudaMemcpyHostToDevice, st_),
-                      "H2D triangle offsets");
-        if (s != PS_OK) return s;
-        for (int f = 0; f < F; ++f) {
-            ps_iter_stats& ts = trace_[size_t(f) * iters + (it - 1)];
-            ts.iteration = it;
-            ts.support_count = hS[f];  // mesh.vertices().size() (pipeline.cpp:180)
-            ts.triangle_count = ntri[f];
-            ts.occupancy_cell_size = cell;
-            hSprev[f] = hS[f];
-        }
-
-        // ---- K5/K6 mesh (mesh.cpp:44-123)
-        cudaMemsetAsync(dLookup, 0xff, sizeof(int32_t) * F * P, st_);
-        begin_kernel("mesh", 4.0 * double(P) * F + 60.0 * double(total_tri));
-        launches_ += launch_mesh(dTri, dTriOff, F, total_tri, dSu, dSv, dSd, scap_, g, dPlanes,
-                                 dLookup, dErr, st_);
-        end_kernel();
-
-        // ---- K7 (+K9) refine (mesh.cpp:149-182, pipeline.cpp:33-86)
         const int cols = ceil_div(W, cell);
         const int cells = cols * ceil_div(H, cell);
-        cudaMemsetAsync(dCg, 0xff, sizeof(unsigned long long) * F * cells, st_);
-        cudaMemsetAsync(dCb, 0xff, sizeof(unsigned long long) * F * cells, st_);
-        RefineArgs ra{g,       F,   dMask,    dLookup, dPlanes,           dCL,
-                      dCR,     float(cfg.max_disparity), cell, cols, cells, dDf,
-                      dDv,     dCf, dCg,      dCb,     dTraceSum + (it - 1),
-                      dTraceValid + (it - 1), iters, dDense, dDenseV};
-        double mbytes = 0.0;
-        for (int f = 0; f < F; ++f) mbytes += double(hMaskCount[f]);
-        const double kbytes = double(P) * F + 29.0 * mbytes + (last ? 9.0 * double(P) * F - 4.0 * mbytes : 0.0);
-        begin_kernel("refine", kbytes);
-        launches_ += launch_refine(ra, tab, last, st_);
-        end_kernel();
-
-        if (!last) {
-            // ---- K8 resampling (pipeline.cpp:88-129)
-            begin_kernel("resample", 0.0);
-            launches_ += launch_resample_confident(dCg, cells, g, F, dLookup, dPlanes, dTaken, dSu,
-                                                   dSv, dSd, scap_, static_cast<int*>(dS_.p),
-                                                   dConf, dChunk, st_);
-            launches_ += launch_resample_invalid(dCb, cells, g, F, dRemU, dRemV, cells_max,
-                                                 dRemCount, dChunk, st_);
-            end_kernel();
-            begin_kernel("match_resample", 0.0);
-            launches_ += launch_match(dCL, dCR, g, F, cfg.max_disparity, tab, dRemU, dRemV,
-                                      dRemCount, cells_max, cells, dOk, dDisp, nullptr, st_);
-            end_kernel();
-            begin_kernel("compact", 0.0);
-            launches_ += launch_emit_matches(dRemU, dRemV, dRemCount, cells_max, cells, dOk, dDisp,
-                                             g, F, dTaken, dSu, dSv, dSd, scap_,
-                                             static_cast<int*>(dS_.p), dConf,
-                                             static_cast<int*>(dSnext_.p), dChunk, st_);
-            end_kernel();
-            std::swap(dS_, dSnext_);
-        }
-        if (observer && F == 1) {
-            std::vector<float> fd(P), fc(P);
-            std::vector<uint8_t> fv(P);
-            s = check(cudaMemcpyAsync(fd.data(), dDf, sizeof(float) * P, cudaMemcpyDeviceToHost, st_), "D2H");
-            if (s == PS_OK) s = check(cudaMemcpyAsync(fv.data(), dDv, P, cudaMemcpyDeviceToHost, st_), "D2H");
-            if (s == PS_OK) s = check(cudaMemcpyAsync(fc.data(), dCf, sizeof(float) * P, cudaMemcpyDeviceToHost, st_), "D2H");
-            if (s == PS_OK) s = sync("observer");
+        for (int gi = 0; gi < G; ++gi) {
+            FrameGroup& grp = groups_[gi];
+            const double tic = now_ms();
+            const int f0 = grp.f0, n = grp.n;
+            cudaStream_t gs = grp.st;
+            int* hs = static_cast<int*>(grp.hS.p);
+            int* hsp = static_cast<int*>(grp.hSprev.p);
+            int* hoff = static_cast<int*>(grp.hPackOff.p);
+            if (it > 1) {
+                s = check(cudaMemcpyAsync(hs, grp.S, sizeof(int) * n, cudaMemcpyDeviceToHost, gs), "D2H S");
+                if (s == PS_OK) s = sync(gs, "support count");
+                if (s != PS_OK) return s;
+            }
+            // ---- supports delta to the host
+            long long total_new = 0;
+            int max_new = 0;
+            for (int i = 0; i < n; ++i) {
+                hoff[i] = int(total_new);
+                const int k = hs[i] - hsp[i];
+                total_new += k;
+                max_new = std::max(max_new, k);
+            }
+            int2* dPack = dev<int2>(grp.dPack, size_t(std::max<long long>(total_new, 1)));
+            int2* hPack = reinterpret_cast<int2*>(host<uint8_t>(grp.hPack, size_t(std::max<long long>(total_new, 1)) * 8));
+            if (!dPack || !hPack) return fail(PS_CUDA_ERROR, "allocation failed (support staging)");
+            int* dSprev = static_cast<int*>(grp.dSprev.p);
+            int* dPackOff = static_cast<int*>(grp.dPackOff.p);
+            s = check(cudaMemcpyAsync(dSprev, hsp, sizeof(int) * n, cudaMemcpyHostToDevice, gs), "H2D Sprev");
+            if (s == PS_OK)
+                s = check(cudaMemcpyAsync(dPackOff, hoff, sizeof(int) * n, cudaMemcpyHostToDevice, gs),
+                          "H2D pack offsets");
             if (s != PS_OK) return s;
-            observer(it, fd.data(), fv.data(), fc.data(), W, H, user);
+            launches_ += launch_pack_new_supports(dSu + size_t(f0) * scap_, dSv + size_t(f0) * scap_,
+                                                  scap_, dSprev, grp.S, dPackOff, n, max_new, dPack, gs);
+            if (total_new > 0)
+                s = check(cudaMemcpyAsync(hPack, dPack, sizeof(int2) * total_new, cudaMemcpyDeviceToHost, gs),
+                          "D2H supports");
+            if (s == PS_OK) s = sync(gs, "support delta");
+            if (s != PS_OK) return s;
+
+            // ---- host Delaunay per frame (delaunay.cpp:288-325 contract)
+            pool_->parallel_for(n, [&](int i, int worker) {
+                const int f = f0 + i;
+                const int k = hs[i] - hsp[i];
+                for (int j = 0; j < k; ++j) {
+                    hu_[f].push_back(hPack[hoff[i] + j].x);
+                    hv_[f].push_back(hPack[hoff[i] + j].y);
+                }
+                grp.ntri[i] = 0;
+                if (status_[f] != PS_OK) {
+                    htri_[f].clear();
+                    return;
+                }
+                const int t = delaunay(hu_[f].data(), hv_[f].data(), int(hu_[f].size()), htri_[f],
+                                       ws_[worker]);
+                if (t < 0) {
+                    status_[f] = PS_ERROR;
+                    htri_[f].clear();
+                    return;
+                }
+                grp.ntri[i] = t;
+            });
+            int* hTriOff = static_cast<int*>(grp.hTriOff.p);
+            long long total_tri = 0;
+            for (int i = 0; i < n; ++i) {
+                hTriOff[i] = int(total_tri);
+                total_tri += grp.ntri[i];
+            }
+            hTriOff[n] = int(total_tri);
+            int* hTri = host<int>(grp.hTri, size_t(std::max<long long>(total_tri, 1)) * 3);
+            int* dTri = dev<int>(grp.dTri, size_t(std::max<long long>(total_tri, 1)) * 3);
+            double* dPlanes = dev<double>(grp.dPlanes, size_t(std::max<long long>(total_tri, 1)) * 3);
+            int* dTriOff = static_cast<int*>(grp.dTriOff.p);
+            if (!hTri || !dTri || !dPlanes) return fail(PS_CUDA_ERROR, "allocation failed (triangles)");
+            pool_->parallel_for(n, [&](int i, int) {
+                if (grp.ntri[i] > 0)
+                    std::memcpy(hTri + 3ll * hTriOff[i], htri_[f0 + i].data(), sizeof(int) * 3 * grp.ntri[i]);
+            });
+            if (total_tri > 0)
+                s = check(cudaMemcpyAsync(dTri, hTri, sizeof(int) * 3 * total_tri, cudaMemcpyHostToDevice, gs),
+                          "H2D triangles");
+            if (s == PS_OK)
+                s = check(cudaMemcpyAsync(dTriOff, hTriOff, sizeof(int) * (n + 1), cudaMemcpyHostToDevice, gs),
+                          "H2D triangle offsets");
+            if (s != PS_OK) return s;
+            for (int i = 0; i < n; ++i) {
+                ps_iter_stats& ts = trace_[size_t(f0 + i) * iters + (it - 1)];
+                ts.iteration = it;
+                ts.support_count = hs[i];  // mesh.vertices().size() (pipeline.cpp:180)
+                ts.triangle_count = grp.ntri[i];
+                ts.occupancy_cell_size = cell;
+                hsp[i] = hs[i];
+                final_count_[f0 + i] = hs[i];
+            }
+
+            // ---- K5/K6 mesh (mesh.cpp:44-123)
+            int32_t* lk = dLookup + size_t(f0) * P;
+            cudaMemsetAsync(lk, 0xff, sizeof(int32_t) * n * P, gs);
+            begin_kernel("mesh", 4.0 * double(P) * n + 60.0 * double(total_tri), gs);
+            launches_ += launch_mesh(dTri, dTriOff, n, total_tri, dSu + size_t(f0) * scap_,
+                                     dSv + size_t(f0) * scap_, dSd + size_t(f0) * scap_, scap_, g,
+                                     dPlanes, lk, dErr, gs);
+            end_kernel(gs);
+
+            // ---- K7 (+K9) refine (mesh.cpp:149-182, pipeline.cpp:33-86)
+            unsigned long long* cg = dCg + size_t(f0) * cells_max;
+            unsigned long long* cb = dCb + size_t(f0) * cells_max;
+            cudaMemset2DAsync(cg, sizeof(unsigned long long) * cells_max, 0xff,
+                              sizeof(unsigned long long) * cells, n, gs);
+            cudaMemset2DAsync(cb, sizeof(unsigned long long) * cells_max, 0xff,
+                              sizeof(unsigned long long) * cells, n, gs);
+            const size_t fp = size_t(f0) * P;
+            RefineArgs ra{};
+            ra.g = g;
+            ra.frames = n;
+            ra.mask = dMask + fp;
+            ra.lookup = lk;
+            ra.planes = dPlanes;
+            ra.cl = dCL + fp;
+            ra.cr = dCR + fp;
+            ra.max_disp = float(cfg.max_disparity);
+            ra.cell = cell;
+            ra.cols = cols;
+            ra.cells_per_frame = cells;
+            ra.cell_stride = cells_max;
+            ra.Df = dDf + fp;
+            ra.Dv = dDv + fp;
+            ra.Cf = dCf + fp;
+            ra.Cg = cg;
+            ra.Cb = cb;
+            ra.trace_sum = dTraceSum + size_t(f0) * iters + (it - 1);
+            ra.trace_valid = dTraceValid + size_t(f0) * iters + (it - 1);
+            ra.trace_stride = iters;
+            ra.dense = dDense + fp;
+            ra.dense_valid = dDenseV + fp;
+            double mbytes = 0.0;
+            for (int i = 0; i < n; ++i) mbytes += double(hMaskCount[f0 + i]);
+            const double kbytes = double(P) * n + 29.0 * mbytes + (last ? 9.0 * double(P) * n - 4.0 * mbytes : 0.0);
+            begin_kernel("refine", kbytes, gs);
+            launches_ += launch_refine(ra, tab, last, gs);
+            end_kernel(gs);
+
+            if (!last) {
+                // ---- K8 resampling (pipeline.cpp:88-129)
+                int* su = dSu + size_t(f0) * scap_;
+                int* sv = dSv + size_t(f0) * scap_;
+                double* sd = dSd + size_t(f0) * scap_;
+                uint32_t* tk = dTaken + size_t(f0) * words;
+                int* chunk = static_cast<int*>(grp.dChunk.p);
+                begin_kernel("resample", 0.0, gs);
+                launches_ += launch_resample_confident(cg, cells, cells_max, g, n, lk, dPlanes, tk,
+                                                       su, sv, sd, scap_, grp.S, dConf + f0, chunk, gs);
+                launches_ += launch_resample_invalid(cb, cells, cells_max, g, n,
+                                                     dRemU + size_t(f0) * cells_max,
+                                                     dRemV + size_t(f0) * cells_max, cells_max,
+                                                     dRemCount + f0, chunk, gs);
+                end_kernel(gs);
+                uint8_t* ok = dOk + size_t(f0) * mstride;
+                int* disp = dDisp + size_t(f0) * mstride;
+                begin_kernel("match_resample", 0.0, gs);
+                launches_ += launch_match(dCL + fp, dCR + fp, g, n, cfg.max_disparity, tab,
+                                          dRemU + size_t(f0) * cells_max, dRemV + size_t(f0) * cells_max,
+                                          dRemCount + f0, cells_max, cells, ok, disp, nullptr, gs);
+                end_kernel(gs);
+                begin_kernel("compact", 0.0, gs);
+                launches_ += launch_emit_matches(dRemU + size_t(f0) * cells_max,
+                                                 dRemV + size_t(f0) * cells_max, dRemCount + f0,
+                                                 cells_max, cells, ok, disp, g, n, tk, su, sv, sd,
+                                                 scap_, grp.S, dConf + f0, grp.Snext, chunk, gs);
+                end_kernel(gs);
+                std::swap(grp.S, grp.Snext);
+            }
+            if (observer && F == 1) {
+                std::vector<float> fd(P), fc(P);
+                std::vector<uint8_t> fv(P);
+                s = check(cudaMemcpyAsync(fd.data(), dDf, sizeof(float) * P, cudaMemcpyDeviceToHost, gs), "D2H");
+                if (s == PS_OK) s = check(cudaMemcpyAsync(fv.data(), dDv, P, cudaMemcpyDeviceToHost, gs), "D2H");
+                if (s == PS_OK) s = check(cudaMemcpyAsync(fc.data(), dCf, sizeof(float) * P, cudaMemcpyDeviceToHost, gs), "D2H");
+                if (s == PS_OK) s = sync(gs, "observer");
+                if (s != PS_OK) return s;
+                observer(it, fd.data(), fv.data(), fc.data(), W, H, user);
+            }
+            grp.millis = now_ms() - tic;
+            for (int i = 0; i < n; ++i) trace_[size_t(f0 + i) * iters + (it - 1)].millis = grp.millis;
         }
-        const double toc = now_ms();
-        for (int f = 0; f < F; ++f) trace_[size_t(f) * iters + (it - 1)].millis = toc - tic;
     }
 
     // ---- trace (pipeline.cpp:183-191)
+    for (int gi = 0; gi < G; ++gi) {
+        s = sync(groups_[gi].st, "pipeline");
+        if (s != PS_OK) return s;
+    }
     int herr = 0;
     s = check(cudaMemcpyAsync(hTraceSum, dTraceSum, sizeof(unsigned long long) * F * iters,
                               cudaMemcpyDeviceToHost, st_), "D2H trace");
@@ -606,9 +685,9 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     }
     have_outputs_ = true;
     for (int f = 0; f < F; ++f)
-        if (status_[f] != PS_OK) return fail(ps_status(status_[f]),
-                                            "only " + std::to_string(hS[f]) +
-                                                " seed matches survived; need at least 3");
+        if (status_[f] != PS_OK)
+            return fail(ps_status(status_[f]), "only " + std::to_string(hS[f]) +
+                                                   " seed matches survived; need at least 3");
     return PS_OK;
 }
 
@@ -647,8 +726,8 @@ ps_status Engine::download(float* disparity, uint8_t* disparity_valid, float* co
 
 ps_status Engine::supports(int frame, int* u, int* v, double* d, int capacity, int* count) {
     if (!have_outputs_ || frame < 0 || frame >= F_) return fail(PS_ERROR, "no such frame");
-    // The last iteration's list: trace support_count of the last iteration.
-    const int n = trace_[size_t(frame) * iters_ + iters_ - 1].support_count;
+    // The last iteration's list (its length is the last trace support_count).
+    const int n = final_count_[frame];
     if (count) *count = n;
     if (n > capacity) return fail(PS_CAPACITY, "support buffer too small");
     const size_t b = size_t(frame) * scap_;

@@ -1,11 +1,12 @@
 // engine.hpp — the batched B200 pipeline behind the C ABI.
 //
-// One Engine per ps_ctx: a device, one CUDA stream, grow-only device/pinned
-// buffers and a host worker pool for the per-frame Delaunay step.  A batch of
-// F frames of one shape runs planestereo::run (proj/src/pipeline.cpp:131-203)
-// for every frame at once: each stage is one launch over all frames
-// (frame = grid.y / grid.z), the host triangulates every frame in parallel
-// between the device stages of an iteration.
+// One Engine per ps_ctx: a device, grow-only device/pinned buffers, a host
+// worker pool for the per-frame Delaunay step, and up to kMaxGroups CUDA
+// streams.  A batch of F frames of one shape runs planestereo::run
+// (proj/src/pipeline.cpp:131-203) for every frame at once: the front end and
+// seeding are one launch per stage over all frames; the iterations run as a
+// software pipeline over frame groups, each on its own stream, so that the
+// device stages of group g overlap the host Delaunay of group g+1.
 #pragma once
 
 #include <cstdint>
@@ -38,8 +39,23 @@ struct KernelStat {
     double bytes = 0.0;
 };
 
+// A contiguous range of frames with its own stream and per-iteration staging.
+struct FrameGroup {
+    int f0 = 0;
+    int n = 0;
+    cudaStream_t st = nullptr;
+    int* S = nullptr;      // device support counts of the group's frames (current)
+    int* Snext = nullptr;  // device support counts (next)
+    DevBuf dTri, dTriOff, dPlanes, dPack, dPackOff, dSprev, dChunk;
+    HostBuf hS, hSprev, hPackOff, hPack, hTri, hTriOff;
+    std::vector<int> ntri;
+    double millis = 0.0;
+};
+
 class Engine {
 public:
+    static constexpr int kMaxGroups = 8;
+
     explicit Engine(int device);
     ~Engine();
 
@@ -66,6 +82,7 @@ public:
     T* host(HostBuf& b, size_t count);
     ps_status check(cudaError_t e, const char* what);
     ps_status sync(const char* what);
+    ps_status sync(cudaStream_t s, const char* what);
     void count_launches(int n) { launches_ += n; }
     ThreadPool& pool() { return *pool_; }
     DelaunayWorkspace& workspace(int worker) { return ws_[worker]; }
@@ -74,10 +91,10 @@ public:
     DevBuf s_a, s_b, s_c, s_d, s_e, s_f, s_g, s_h, s_i, s_j;
 
 private:
-    struct Timer;
-    void begin_kernel(const char* name, double bytes);
-    void end_kernel();
+    void begin_kernel(const char* name, double bytes, cudaStream_t s);
+    void end_kernel(cudaStream_t s);
     void resolve_timers();
+    cudaEvent_t take_event();
     ps_status fail(ps_status s, const std::string& msg) {
         err_ = msg;
         return s;
@@ -99,6 +116,7 @@ private:
     std::vector<cudaEvent_t> event_pool_;
     int pending_stat_ = -1;
     cudaEvent_t pending_start_ = nullptr;
+    FrameGroup groups_[kMaxGroups];
 
     // batch shape
     int F_ = 0, W_ = 0, H_ = 0;
@@ -108,18 +126,16 @@ private:
     int iters_ = 0;
     float cost_high_ = 0.5f;
 
-    // device buffers
+    // device buffers (frame-strided)
     DevBuf dL_, dR_, dMask_, dMaskCount_, dCL_, dCR_, dDf_, dDv_, dCf_, dDense_, dDenseV_,
-        dLookup_, dSu_, dSv_, dSd_, dS_, dSnext_, dSprev_, dTaken_, dTri_, dTriOff_, dPlanes_,
-        dCg_, dCb_, dBinKeys_, dBinCount_, dScratch_, dCandU_, dCandV_, dCandCount_, dOk_,
-        dDisp_, dRemU_, dRemV_, dRemCount_, dConf_, dChunk_, dTraceSum_, dTraceValid_, dErr_,
-        dPack_, dPackOff_;
+        dLookup_, dSu_, dSv_, dSd_, dS_, dSnext_, dTaken_, dCg_, dCb_, dBinKeys_, dBinCount_,
+        dScratch_, dCandU_, dCandV_, dCandCount_, dOk_, dDisp_, dRemU_, dRemV_, dRemCount_,
+        dConf_, dChunk_, dTraceSum_, dTraceValid_, dErr_;
     // pinned host staging
-    HostBuf hS_, hSprev_, hPackOff_, hPack_, hTri_, hTriOff_, hTraceSum_, hTraceValid_,
-        hMaskCount_, hL_, hR_;
+    HostBuf hS_, hTraceSum_, hTraceValid_, hMaskCount_;
     int scap_ = 0;
     std::vector<std::vector<int>> hu_, hv_, htri_;
-    std::vector<int> status_;
+    std::vector<int> status_, final_count_;
     std::vector<ps_iter_stats> trace_;
 };
 

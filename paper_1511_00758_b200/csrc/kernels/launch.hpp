@@ -65,7 +65,8 @@ struct RefineArgs {
     float max_disp;
     int cell;
     int cols;
-    int cells_per_frame;
+    int cells_per_frame;  // cells of this iteration
+    int cell_stride;      // per-frame stride of the grid arrays (>= cells_per_frame)
     float* Df;
     uint8_t* Dv;
     float* Cf;
@@ -82,13 +83,14 @@ int launch_refine(const RefineArgs& a, const CostTables& tab, bool last, cudaStr
 // K8 — resampling: confident cells (row-major) appended as supports,
 // occupied invalid cells compacted into the re-match list
 // (proj/src/pipeline.cpp:88-129).  S_old[f] is the current support count.
-int launch_resample_confident(const unsigned long long* Cg, int cells_per_frame, FrameGeom g,
-                              int frames, const int32_t* lookup, const double* planes,
-                              uint32_t* taken, int* su, int* sv, double* sd, int scap,
-                              const int* S_old, int* conf_count, int* chunk_buf, cudaStream_t st);
-int launch_resample_invalid(const unsigned long long* Cb, int cells_per_frame, FrameGeom g,
-                            int frames, int* rem_u, int* rem_v, int rem_stride, int* rem_count,
-                            int* chunk_buf, cudaStream_t st);
+int launch_resample_confident(const unsigned long long* Cg, int cells_per_frame, int cell_stride,
+                              FrameGeom g, int frames, const int32_t* lookup,
+                              const double* planes, uint32_t* taken, int* su, int* sv, double* sd,
+                              int scap, const int* S_old, int* conf_count, int* chunk_buf,
+                              cudaStream_t st);
+int launch_resample_invalid(const unsigned long long* Cb, int cells_per_frame, int cell_stride,
+                            FrameGeom g, int frames, int* rem_u, int* rem_v, int rem_stride,
+                            int* rem_count, int* chunk_buf, cudaStream_t st);
 // S[f] = S[f] + a[f] + b[f]
 int launch_add_counts(int* S, const int* a, const int* b, int frames, cudaStream_t st);
 

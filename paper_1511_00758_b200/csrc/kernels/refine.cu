@@ -153,17 +153,17 @@ __global__ void __launch_bounds__(256) k_refine(RefineArgs a, CostTables tab) {
                 const int cell = (vj / a.cell) * a.cols + (uu / a.cell);
                 const unsigned long long idx = (unsigned long long)vj * W + uu;
                 if ((tab.low_mask >> k) & 1u) {
-                    acc_push(accg, a.Cg + (long long)f * a.cells_per_frame, cell,
+                    acc_push(accg, a.Cg + (long long)f * a.cell_stride, cell,
                              (unsigned long long)k << 32 | idx);
                 } else if ((tab.high_mask >> k) & 1u) {
-                    acc_push(accb, a.Cb + (long long)f * a.cells_per_frame, cell,
+                    acc_push(accb, a.Cb + (long long)f * a.cell_stride, cell,
                              (unsigned long long)(kCensusBits - k) << 32 | idx);
                 }
                 tsum += __double2ull_rn(__dmul_rn(double(cf[j]), 68719476736.0));  // * 2^36
                 tvalid += cf[j] < tab.cost_high ? 1u : 0u;
             }
-            if (accg.cell >= 0) atomicMin(a.Cg + (long long)f * a.cells_per_frame + accg.cell, accg.key);
-            if (accb.cell >= 0) atomicMin(a.Cb + (long long)f * a.cells_per_frame + accb.cell, accb.key);
+            if (accg.cell >= 0) atomicMin(a.Cg + (long long)f * a.cell_stride + accg.cell, accg.key);
+            if (accb.cell >= 0) atomicMin(a.Cb + (long long)f * a.cell_stride + accb.cell, accb.key);
             const bool any_upd = upd[0] | upd[1] | upd[2] | upd[3];
             if (any_upd) {
                 if (VEC && upd[0] && upd[1] && upd[2] && upd[3]) {

@@ -24,6 +24,7 @@ namespace {
 struct ConfidentOp {
     const unsigned long long* Cg;
     int cells;
+    int stride;
     FrameGeom g;
     const int32_t* lookup;
     const double* planes;
@@ -35,7 +36,7 @@ struct ConfidentOp {
 
     __device__ int items(int) const { return cells; }
     __device__ bool winner(int f, int c, int& u, int& v, float& d) const {
-        const unsigned long long key = Cg[(long long)f * cells + c];
+        const unsigned long long key = Cg[(long long)f * stride + c];
         if (key == kEmptyCell) return false;  // !cell.occupied
         const long long idx = (long long)(key & 0xffffffffull);
         v = int(idx / g.width);
@@ -71,15 +72,16 @@ struct ConfidentOp {
 struct InvalidOp {
     const unsigned long long* Cb;
     int cells;
+    int stride;
     FrameGeom g;
     int* ru;
     int* rv;
     int rstride;
 
     __device__ int items(int) const { return cells; }
-    __device__ bool test(int f, int c) const { return Cb[(long long)f * cells + c] != kEmptyCell; }
+    __device__ bool test(int f, int c) const { return Cb[(long long)f * stride + c] != kEmptyCell; }
     __device__ void emit(int f, int c, int pos) const {
-        const long long idx = (long long)(Cb[(long long)f * cells + c] & 0xffffffffull);
+        const long long idx = (long long)(Cb[(long long)f * stride + c] & 0xffffffffull);
         const int v = int(idx / g.width);
         ru[(long long)f * rstride + pos] = int(idx - (long long)v * g.width);
         rv[(long long)f * rstride + pos] = v;
@@ -104,19 +106,20 @@ __global__ void k_pack_new(const int* __restrict__ su, const int* __restrict__ s
 
 }  // namespace
 
-int launch_resample_confident(const unsigned long long* Cg, int cells_per_frame, FrameGeom g,
-                              int frames, const int32_t* lookup, const double* planes,
-                              uint32_t* taken, int* su, int* sv, double* sd, int scap,
-                              const int* S_old, int* conf_count, int* chunk_buf, cudaStream_t st) {
-    ConfidentOp op{Cg, cells_per_frame, g, lookup, planes, taken, su, sv, sd, scap};
+int launch_resample_confident(const unsigned long long* Cg, int cells_per_frame, int cell_stride,
+                              FrameGeom g, int frames, const int32_t* lookup,
+                              const double* planes, uint32_t* taken, int* su, int* sv, double* sd,
+                              int scap, const int* S_old, int* conf_count, int* chunk_buf,
+                              cudaStream_t st) {
+    ConfidentOp op{Cg, cells_per_frame, cell_stride, g, lookup, planes, taken, su, sv, sd, scap};
     return run_compaction(op, frames, cells_per_frame, chunk_buf, conf_count, S_old, nullptr,
                           nullptr, st);
 }
 
-int launch_resample_invalid(const unsigned long long* Cb, int cells_per_frame, FrameGeom g,
-                            int frames, int* rem_u, int* rem_v, int rem_stride, int* rem_count,
-                            int* chunk_buf, cudaStream_t st) {
-    InvalidOp op{Cb, cells_per_frame, g, rem_u, rem_v, rem_stride};
+int launch_resample_invalid(const unsigned long long* Cb, int cells_per_frame, int cell_stride,
+                            FrameGeom g, int frames, int* rem_u, int* rem_v, int rem_stride,
+                            int* rem_count, int* chunk_buf, cudaStream_t st) {
+    InvalidOp op{Cb, cells_per_frame, cell_stride, g, rem_u, rem_v, rem_stride};
     return run_compaction(op, frames, cells_per_frame, chunk_buf, rem_count, nullptr, nullptr,
                           nullptr, st);
 }
