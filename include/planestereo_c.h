@@ -164,8 +164,14 @@ ps_status ps_match_epipolar(ps_ctx* ctx, const uint32_t* census_left,
                             const ps_config* cfg, int* u, int* v, double* d, int capacity,
                             int* count);
 /* delaunayTriangulate (proj/src/delaunay.cpp:288-325): positively oriented
- * index triples into the input list; tris has room for 3*capacity ints. */
+ * index triples into the input list, in the reference's own order and
+ * rotation; tris has room for 3*capacity ints.  Host code (exact integer
+ * predicates). */
 ps_status ps_delaunay(const int* u, const int* v, int n, int* tris, int capacity, int* n_tris);
+/* Same triangle set, in radial-sweep order (the engine's fast path; triangle
+ * order and rotation are not part of the Delaunay contract). */
+ps_status ps_delaunay_fast(const int* u, const int* v, int n, int* tris, int capacity,
+                           int* n_tris);
 /* DisparityMesh ctor (proj/src/mesh.cpp:44-123): per-triangle planes (a,b,c)
  * and the P-sized triangle lookup (-1 outside). */
 ps_status ps_mesh_build(ps_ctx* ctx, const int* u, const int* v, const double* d, int n_points,

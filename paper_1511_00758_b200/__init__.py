@@ -360,8 +360,9 @@ class Context:
         return cost
 
 
-def delaunay_triangulate(u, v) -> np.ndarray:
-    """planestereo::delaunayTriangulate: (T, 3) index triples (host C++, exact)."""
+def delaunay_triangulate(u, v, fast: bool = False) -> np.ndarray:
+    """planestereo::delaunayTriangulate: (T, 3) index triples (host C++, exact).
+    fast=True returns the same set in the engine's radial-sweep order."""
     lib = _native.load()
     u = np.ascontiguousarray(u, dtype=np.int32)
     v = np.ascontiguousarray(v, dtype=np.int32)
@@ -369,7 +370,8 @@ def delaunay_triangulate(u, v) -> np.ndarray:
     cap = max(1, 2 * n)
     tris = np.zeros((cap, 3), np.int32)
     nt = C.c_int()
-    _check(lib.ps_delaunay(_ptr(u), _ptr(v), n, _ptr(tris), cap, C.byref(nt)))
+    fn = lib.ps_delaunay_fast if fast else lib.ps_delaunay
+    _check(fn(_ptr(u), _ptr(v), n, _ptr(tris), cap, C.byref(nt)))
     return tris[:nt.value]
 
 

@@ -107,6 +107,7 @@ SIGNATURES = {
     "ps_detect_candidates": (I, [P, P, I, I, P, P, P, P, I, P]),
     "ps_match_epipolar": (I, [P, P, P, I, I, P, P, I, P, P, P, P, I, P]),
     "ps_delaunay": (I, [P, P, I, P, I, P]),
+    "ps_delaunay_fast": (I, [P, P, I, P, I, P]),
     "ps_mesh_build": (I, [P, P, P, P, I, P, I, I, I, P, P]),
     "ps_interpolate": (I, [P, P, P, I, I, I, P, F, P, P]),
     "ps_cost_evaluation": (I, [P, P, P, I, I, P, P, P, P]),

@@ -350,16 +350,26 @@ ps_status ps_match_epipolar(ps_ctx* ctx, const uint32_t* census_left, const uint
     return PS_OK;
 }
 
-ps_status ps_delaunay(const int* u, const int* v, int n, int* tris, int capacity, int* n_tris) {
+static ps_status delaunay_common(bool fast, const int* u, const int* v, int n, int* tris,
+                                 int capacity, int* n_tris) {
     static thread_local ps::DelaunayWorkspace ws;
     std::vector<int> out;
-    const int t = ps::delaunay(u, v, n, out, ws);
+    const int t = fast ? ps::delaunay(u, v, n, out, ws) : ps::delaunay_lex(u, v, n, out, ws);
     if (t == -1) return set_error(PS_ERROR, "triangulation coordinates must be below 2^20");
     if (t < 0) return set_error(PS_ERROR, "triangulation invariant violated: no hull edge visible");
     if (n_tris) *n_tris = t;
     if (t > capacity) return set_error(PS_CAPACITY, "triangle buffer too small");
     if (tris && t > 0) std::memcpy(tris, out.data(), sizeof(int) * 3 * t);
     return PS_OK;
+}
+
+ps_status ps_delaunay(const int* u, const int* v, int n, int* tris, int capacity, int* n_tris) {
+    return delaunay_common(false, u, v, n, tris, capacity, n_tris);
+}
+
+ps_status ps_delaunay_fast(const int* u, const int* v, int n, int* tris, int capacity,
+                           int* n_tris) {
+    return delaunay_common(true, u, v, n, tris, capacity, n_tris);
 }
 
 ps_status ps_mesh_build(ps_ctx* ctx, const int* u, const int* v, const double* d, int n_points,

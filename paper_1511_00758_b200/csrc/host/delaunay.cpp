@@ -237,34 +237,49 @@ int bit_width(uint64_t v) {
 
 }  // namespace
 
-int delaunay(const int* u, const int* v, int n, std::vector<int>& tris, DelaunayWorkspace& ws) {
-    tris.clear();
-    constexpr int kLimit = 1 << 20;
-    int minx = kLimit, maxx = -kLimit, miny = kLimit, maxy = -kLimit;
-    for (int i = 0; i < n; ++i) {
-        if (std::abs(u[i]) >= kLimit || std::abs(v[i]) >= kLimit) return -1;
+// Lexicographic (u, v) order with coincident points removed, first occurrence
+// kept (delaunay.cpp:296-311): ws.kept[0..m) = original indices.  Stable LSD
+// radix sort on 43-bit keys, so equal coordinates keep input order.
+void lex_order(const int* u, const int* v, int n, DelaunayWorkspace& ws, int& minx, int& miny,
+               int& m, int& spanx, int& spany) {
+    minx = u[0];
+    miny = v[0];
+    int maxx = u[0], maxy = v[0];
+    for (int i = 1; i < n; ++i) {
         minx = std::min(minx, u[i]);
         maxx = std::max(maxx, u[i]);
         miny = std::min(miny, v[i]);
         maxy = std::max(maxy, v[i]);
     }
-    if (n < 3) return 0;
-
-    // 1. lexicographic order + dedup, first occurrence wins (delaunay.cpp:296-311)
+    spanx = maxx - minx;
+    spany = maxy - miny;
     ws.key.resize(n);
     ws.ord.resize(n);
     for (int i = 0; i < n; ++i) {
         ws.key[i] = (uint64_t(uint32_t(u[i] - minx)) << 21) | uint64_t(uint32_t(v[i] - miny));
         ws.ord[i] = i;
     }
-    radix_sort_keys(ws.key, ws.ord, ws.key_tmp, ws.ord_tmp, n, 21 + bit_width(uint64_t(maxx - minx)));
+    radix_sort_keys(ws.key, ws.ord, ws.key_tmp, ws.ord_tmp, n, 21 + bit_width(uint64_t(spanx)));
     ws.kept.resize(n);
-    int m = 0;
+    m = 0;
     for (int i = 0; i < n; ++i) {
         if (m > 0 && ws.key[i] == ws.key[i - 1]) continue;
         ws.kept[m++] = ws.ord[i];
     }
+}
+
+int delaunay(const int* u, const int* v, int n, std::vector<int>& tris, DelaunayWorkspace& ws) {
+    tris.clear();
+    constexpr int kLimit = 1 << 20;
+    for (int i = 0; i < n; ++i)
+        if (std::abs(u[i]) >= kLimit || std::abs(v[i]) >= kLimit) return -1;
+    if (n < 3) return 0;
+
+    // 1. lexicographic order + dedup, first occurrence wins
+    int minx, miny, m, spanx, spany;
+    lex_order(u, v, n, ws, minx, miny, m, spanx, spany);
     if (m < 3) return 0;
+    const int maxx = minx + spanx, maxy = miny + spany;
 
     // 2. radial order around an integer centre (stable: ties stay lexicographic)
     const int cx = minx + (maxx - minx) / 2, cy = miny + (maxy - miny) / 2;

@@ -23,6 +23,8 @@ struct DelaunayWorkspace {
     std::vector<int> tv, tn;  // triangle vertices / neighbour half-edges
     std::vector<int> hnext, hprev, hedge;
     std::vector<int> stack;
+    std::vector<uint8_t> covered;  // pin_ambiguous scratch
+    std::vector<float> first;
 };
 
 // Returns the number of triangles (index triples into the input written to
@@ -30,5 +32,15 @@ struct DelaunayWorkspace {
 // three distinct points or a collinear set, -1 if a coordinate has
 // |c| >= 2^20 (the reference's exactness bound, delaunay.cpp:289-294).
 int delaunay(const int* u, const int* v, int n, std::vector<int>& tris, DelaunayWorkspace& ws);
+
+// Same set, in the reference's own triangle order and rotation (lexicographic
+// sweep, delaunay_lex.cpp).  Slower (~4x more in-circle tests).
+int delaunay_lex(const int* u, const int* v, int n, std::vector<int>& tris, DelaunayWorkspace& ws);
+
+// True when the first-incident-triangle pinning of an uncovered hull vertex
+// (mesh.cpp:109-122) would depend on the triangle order for this mesh (pins.cpp).
+bool pin_ambiguous(const int* u, const int* v, const double* d, int n, const int* tris, int nt,
+                   int width, int height, std::vector<uint8_t>& covered,
+                   std::vector<float>& first);
 
 }  // namespace ps

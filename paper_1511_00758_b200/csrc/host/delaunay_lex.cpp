@@ -1,0 +1,214 @@
+// delaunay_lex.cpp — lexicographic-sweep Delaunay in the reference's order.
+//
+// Same triangle SET as delaunay() (delaunay.cpp) but also the same triangle
+// ORDER and vertex rotation as planestereo::delaunayTriangulate
+// (proj/src/delaunay.cpp:288-325), because it performs the same sequence of
+// textbook operations: points inserted in (u, v) order, each new point fanned
+// to its strictly visible hull chain from the first to the last edge, Lawson
+// flips of the edges opposite the new point in LIFO order with a strict
+// in-circle test, and a flipped pair (a,b,c)+(b,a,d) rewritten in place as
+// (a,d,c)+(d,b,c).  Checked array-for-array against the compiled reference
+// (tests/test_delaunay.py).
+//
+// The order only matters for one thing downstream: an uncovered hull vertex
+// pixel takes its FIRST incident triangle (mesh.cpp:109-122), and when the
+// incident planes evaluate to different floats at that vertex (a vertex at
+// d = 0, plane value +-1e-17) the choice decides validity.  The engine uses the
+// fast radial sweep and falls back to this order only for such frames
+// (pin_ambiguous()).  It is also the order of the public ps_delaunay().
+#include <cstdlib>
+
+#include "delaunay.hpp"
+
+namespace ps {
+
+namespace {
+
+inline int lnext(int e) { return (e % 3 == 2) ? e - 2 : e + 1; }
+
+struct LexSweep {
+    const int* x;
+    const int* y;
+    int* tv;
+    int* tn;
+    int* hnext;
+    int* hprev;
+    int* hedge;
+    std::vector<int>* stack;
+    int ntri = 0;
+    bool wide = false;
+
+    long long orient(int a, int b, int c) const {
+        const long long abx = (long long)x[b] - x[a], aby = (long long)y[b] - y[a];
+        const long long acx = (long long)x[c] - x[a], acy = (long long)y[c] - y[a];
+        return abx * acy - aby * acx;
+    }
+
+    bool inside(int a, int b, int c, int d) const {
+        const long long adx = (long long)x[a] - x[d], ady = (long long)y[a] - y[d];
+        const long long bdx = (long long)x[b] - x[d], bdy = (long long)y[b] - y[d];
+        const long long cdx = (long long)x[c] - x[d], cdy = (long long)y[c] - y[d];
+        const long long aq = adx * adx + ady * ady;
+        const long long bq = bdx * bdx + bdy * bdy;
+        const long long cq = cdx * cdx + cdy * cdy;
+        if (!wide) {
+            return adx * (bdy * cq - cdy * bq) - ady * (bdx * cq - cdx * bq) +
+                       aq * (bdx * cdy - cdx * bdy) > 0;
+        }
+        using W = __int128;
+        return W(adx) * (W(bdy) * cq - W(cdy) * bq) - W(ady) * (W(bdx) * cq - W(cdx) * bq) +
+                   W(aq) * (W(bdx) * cdy - W(cdx) * bdy) > 0;
+    }
+
+    int add(int a, int b, int c, int na, int nb, int nc) {
+        const int e = 3 * ntri++;
+        tv[e] = a;
+        tv[e + 1] = b;
+        tv[e + 2] = c;
+        tn[e] = na;
+        tn[e + 1] = nb;
+        tn[e + 2] = nc;
+        if (na >= 0) tn[na] = e;
+        if (nb >= 0) tn[nb] = e + 1;
+        if (nc >= 0) tn[nc] = e + 2;
+        return e;
+    }
+
+    void hull(int a, int b) {
+        hnext[a] = b;
+        hprev[b] = a;
+    }
+
+    void legalize() {
+        while (!stack->empty()) {
+            const int e = stack->back();
+            stack->pop_back();
+            const int f = tn[e];
+            if (f < 0) continue;
+            const int e1 = lnext(e), e2 = lnext(e1);
+            const int f1 = lnext(f), f2 = lnext(f1);
+            const int a = tv[e], b = tv[e1], c = tv[e2], d = tv[f2];
+            if (!inside(a, b, c, d)) continue;  // strict: cocircular never flips
+            const int ne1 = tn[e1], ne2 = tn[e2], nf1 = tn[f1], nf2 = tn[f2];
+            tv[e1] = d;
+            tv[f] = d;
+            tv[f1] = b;
+            tv[f2] = c;
+            tn[e] = nf1;
+            if (nf1 >= 0) tn[nf1] = e; else hedge[a] = e;
+            tn[e1] = f2;
+            tn[f2] = e1;
+            tn[e2] = ne2;
+            tn[f] = nf2;
+            if (nf2 >= 0) tn[nf2] = f; else hedge[d] = f;
+            tn[f1] = ne1;
+            if (ne1 >= 0) tn[ne1] = f1; else hedge[b] = f1;
+            // edges incident to the new point (f1, e2) are locally Delaunay
+            // and never flip; only the two opposite edges are re-examined
+            stack->push_back(e);
+            stack->push_back(f);
+        }
+    }
+
+    bool visible(int a, int p) const { return orient(a, hnext[a], p) < 0; }
+
+    bool insert(int p) {
+        const int q = p - 1;  // lexicographic max so far: on the hull
+        int a, b;
+        if (visible(q, p)) {
+            a = q;
+            b = hnext[q];
+        } else if (visible(hprev[q], p)) {
+            a = hprev[q];
+            b = q;
+        } else {
+            return false;
+        }
+        while (hnext[b] != a && visible(b, p)) b = hnext[b];
+        while (hprev[a] != b && visible(hprev[a], p)) a = hprev[a];
+        int prevE1 = -1, firstE0 = -1;
+        for (int xv = a; xv != b;) {
+            const int xn = hnext[xv];
+            const int e = add(xv, p, xn, prevE1, -1, hedge[xv]);
+            if (firstE0 < 0) firstE0 = e;
+            prevE1 = e + 1;
+            stack->push_back(e + 2);
+            xv = xn;
+        }
+        hull(a, p);
+        hull(p, b);
+        hedge[a] = firstE0;
+        hedge[p] = prevE1;
+        legalize();
+        return true;
+    }
+};
+
+}  // namespace
+
+void lex_order(const int* u, const int* v, int n, DelaunayWorkspace& ws, int& minx, int& miny,
+               int& m, int& spanx, int& spany);
+
+int delaunay_lex(const int* u, const int* v, int n, std::vector<int>& tris,
+                 DelaunayWorkspace& ws) {
+    tris.clear();
+    constexpr int kLimit = 1 << 20;
+    for (int i = 0; i < n; ++i)
+        if (std::abs(u[i]) >= kLimit || std::abs(v[i]) >= kLimit) return -1;
+    if (n < 3) return 0;
+    int minx, miny, m, spanx, spany;
+    lex_order(u, v, n, ws, minx, miny, m, spanx, spany);  // sorted + deduplicated in ws.kept
+    if (m < 3) return 0;
+    ws.px.resize(m);
+    ws.py.resize(m);
+    for (int i = 0; i < m; ++i) {
+        ws.px[i] = u[ws.kept[i]];
+        ws.py[i] = v[ws.kept[i]];
+    }
+    ws.tv.resize(6 * std::size_t(m));
+    ws.tn.resize(6 * std::size_t(m));
+    ws.hnext.assign(m, -1);
+    ws.hprev.assign(m, -1);
+    ws.hedge.assign(m, -1);
+    ws.stack.clear();
+    LexSweep s{ws.px.data(), ws.py.data(), ws.tv.data(), ws.tn.data(), ws.hnext.data(),
+               ws.hprev.data(), ws.hedge.data(), &ws.stack};
+    s.wide = spanx >= (1 << 14) || spany >= (1 << 14);
+
+    int k = 2;
+    while (k < m && s.orient(0, 1, k) == 0) ++k;
+    if (k == m) return 0;
+    const int apex = k;
+    if (s.orient(0, 1, apex) > 0) {
+        int prevE1 = -1;
+        for (int j = 0; j + 1 < k; ++j) {
+            const int e = s.add(j, j + 1, apex, -1, -1, prevE1);
+            if (j == 0) s.hedge[apex] = e + 2;
+            s.hedge[j] = e;
+            prevE1 = e + 1;
+        }
+        s.hedge[k - 1] = prevE1;
+        for (int j = 0; j + 1 < k; ++j) s.hull(j, j + 1);
+        s.hull(k - 1, apex);
+        s.hull(apex, 0);
+    } else {
+        int prevE2 = -1;
+        for (int j = 0; j + 1 < k; ++j) {
+            const int e = s.add(j + 1, j, apex, -1, prevE2, -1);
+            if (j == 0) s.hedge[0] = e + 1;
+            s.hedge[j + 1] = e;
+            prevE2 = e + 2;
+        }
+        s.hedge[apex] = prevE2;
+        for (int j = 0; j + 1 < k; ++j) s.hull(j + 1, j);
+        s.hull(0, apex);
+        s.hull(apex, k - 1);
+    }
+    for (int p = apex + 1; p < m; ++p)
+        if (!s.insert(p)) return -2;
+    tris.resize(3 * std::size_t(s.ntri));
+    for (int e = 0; e < 3 * s.ntri; ++e) tris[e] = ws.kept[ws.tv[e]];
+    return s.ntri;
+}
+
+}  // namespace ps

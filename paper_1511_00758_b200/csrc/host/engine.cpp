@@ -142,9 +142,10 @@ Engine::~Engine() {
     for (HostBuf* b : hbufs)
         if (b->p) cudaFreeHost(b->p);
     for (FrameGroup& g : groups_) {
-        for (DevBuf* b : {&g.dTri, &g.dTriOff, &g.dPlanes, &g.dPack, &g.dPackOff, &g.dSprev, &g.dChunk})
+        for (DevBuf* b : {&g.dTri, &g.dTriOff, &g.dPlanes, &g.dPack, &g.dPackD, &g.dPackOff,
+                          &g.dSprev, &g.dChunk})
             if (b->p) cudaFree(b->p);
-        for (HostBuf* b : {&g.hS, &g.hSprev, &g.hPackOff, &g.hPack, &g.hTri, &g.hTriOff})
+        for (HostBuf* b : {&g.hS, &g.hSprev, &g.hPackOff, &g.hPack, &g.hPackD, &g.hTri, &g.hTriOff})
             if (b->p) cudaFreeHost(b->p);
         if (g.st) cudaStreamDestroy(g.st);
     }
@@ -416,12 +417,16 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
 
     status_.assign(F, PS_OK);
     final_count_.assign(F, 0);
+    lex_used_.assign(F, 0);
+    double host_dt_ms = 0.0;
     hu_.resize(F);
     hv_.resize(F);
+    hd_.resize(F);
     htri_.resize(F);
     for (int f = 0; f < F; ++f) {
         hu_[f].clear();
         hv_[f].clear();
+        hd_[f].clear();
         if (hS[f] < 3) status_[f] = PS_SEEDING_FAILED;  // pipeline.cpp:151-154
     }
     trace_.assign(size_t(F) * iters, ps_iter_stats{});
@@ -475,9 +480,13 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                 total_new += k;
                 max_new = std::max(max_new, k);
             }
-            int2* dPack = dev<int2>(grp.dPack, size_t(std::max<long long>(total_new, 1)));
-            int2* hPack = reinterpret_cast<int2*>(host<uint8_t>(grp.hPack, size_t(std::max<long long>(total_new, 1)) * 8));
-            if (!dPack || !hPack) return fail(PS_CUDA_ERROR, "allocation failed (support staging)");
+            const size_t npk = size_t(std::max<long long>(total_new, 1));
+            int2* dPack = dev<int2>(grp.dPack, npk);
+            double* dPackD = dev<double>(grp.dPackD, npk);
+            int2* hPack = reinterpret_cast<int2*>(host<uint8_t>(grp.hPack, npk * 8));
+            double* hPackD = reinterpret_cast<double*>(host<uint8_t>(grp.hPackD, npk * 8));
+            if (!dPack || !hPack || !dPackD || !hPackD)
+                return fail(PS_CUDA_ERROR, "allocation failed (support staging)");
             int* dSprev = static_cast<int*>(grp.dSprev.p);
             int* dPackOff = static_cast<int*>(grp.dPackOff.p);
             s = check(cudaMemcpyAsync(dSprev, hsp, sizeof(int) * n, cudaMemcpyHostToDevice, gs), "H2D Sprev");
@@ -486,28 +495,43 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                           "H2D pack offsets");
             if (s != PS_OK) return s;
             launches_ += launch_pack_new_supports(dSu + size_t(f0) * scap_, dSv + size_t(f0) * scap_,
-                                                  scap_, dSprev, grp.S, dPackOff, n, max_new, dPack, gs);
-            if (total_new > 0)
+                                                  dSd + size_t(f0) * scap_, scap_, dSprev, grp.S,
+                                                  dPackOff, n, max_new, dPack, dPackD, gs);
+            if (total_new > 0) {
                 s = check(cudaMemcpyAsync(hPack, dPack, sizeof(int2) * total_new, cudaMemcpyDeviceToHost, gs),
                           "D2H supports");
+                if (s == PS_OK)
+                    s = check(cudaMemcpyAsync(hPackD, dPackD, sizeof(double) * total_new,
+                                              cudaMemcpyDeviceToHost, gs), "D2H support d");
+            }
             if (s == PS_OK) s = sync(gs, "support delta");
             if (s != PS_OK) return s;
 
-            // ---- host Delaunay per frame (delaunay.cpp:288-325 contract)
+            // ---- host Delaunay per frame (delaunay.cpp:288-325 contract): the
+            // radial sweep, or the reference-order sweep when the hull-vertex
+            // pinning depends on the order (pins.cpp)
+            const double dt0 = now_ms();
             pool_->parallel_for(n, [&](int i, int worker) {
                 const int f = f0 + i;
                 const int k = hs[i] - hsp[i];
                 for (int j = 0; j < k; ++j) {
                     hu_[f].push_back(hPack[hoff[i] + j].x);
                     hv_[f].push_back(hPack[hoff[i] + j].y);
+                    hd_[f].push_back(hPackD[hoff[i] + j]);
                 }
                 grp.ntri[i] = 0;
                 if (status_[f] != PS_OK) {
                     htri_[f].clear();
                     return;
                 }
-                const int t = delaunay(hu_[f].data(), hv_[f].data(), int(hu_[f].size()), htri_[f],
-                                       ws_[worker]);
+                const int ns = int(hu_[f].size());
+                DelaunayWorkspace& w = ws_[worker];
+                int t = delaunay(hu_[f].data(), hv_[f].data(), ns, htri_[f], w);
+                if (t > 0 && pin_ambiguous(hu_[f].data(), hv_[f].data(), hd_[f].data(), ns,
+                                           htri_[f].data(), t, W, H, w.covered, w.first)) {
+                    t = delaunay_lex(hu_[f].data(), hv_[f].data(), ns, htri_[f], w);
+                    lex_used_[f] += 1;
+                }
                 if (t < 0) {
                     status_[f] = PS_ERROR;
                     htri_[f].clear();
@@ -515,6 +539,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                 }
                 grp.ntri[i] = t;
             });
+            host_dt_ms += now_ms() - dt0;
             int* hTriOff = static_cast<int*>(grp.hTriOff.p);
             long long total_tri = 0;
             for (int i = 0; i < n; ++i) {
@@ -655,6 +680,19 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     if (s == PS_OK) s = sync("pipeline");
     if (s != PS_OK) return s;
     resolve_timers();
+    if (profiling_) {
+        auto stat = [&](const char* name) -> KernelStat& {
+            for (auto& k : stats_)
+                if (k.name == name) return k;
+            stats_.push_back({name, 0, 0.0, 0.0});
+            return stats_.back();
+        };
+        KernelStat& dt = stat("host_delaunay");
+        dt.launches += F * iters;
+        dt.ms += host_dt_ms;
+        KernelStat& lx = stat("host_lex_fallback");
+        for (int f = 0; f < F; ++f) lx.launches += lex_used_[f];
+    }
     if (herr) return fail(PS_DEGENERATE_TRIANGLE, "collinear vertices in a triangle");
     for (int f = 0; f < F; ++f) {
         for (int it = 0; it < iters; ++it) {

@@ -46,8 +46,8 @@ struct FrameGroup {
     cudaStream_t st = nullptr;
     int* S = nullptr;      // device support counts of the group's frames (current)
     int* Snext = nullptr;  // device support counts (next)
-    DevBuf dTri, dTriOff, dPlanes, dPack, dPackOff, dSprev, dChunk;
-    HostBuf hS, hSprev, hPackOff, hPack, hTri, hTriOff;
+    DevBuf dTri, dTriOff, dPlanes, dPack, dPackD, dPackOff, dSprev, dChunk;
+    HostBuf hS, hSprev, hPackOff, hPack, hPackD, hTri, hTriOff;
     std::vector<int> ntri;
     double millis = 0.0;
 };
@@ -135,7 +135,9 @@ private:
     HostBuf hS_, hTraceSum_, hTraceValid_, hMaskCount_;
     int scap_ = 0;
     std::vector<std::vector<int>> hu_, hv_, htri_;
+    std::vector<std::vector<double>> hd_;
     std::vector<int> status_, final_count_;
+    std::vector<int> lex_used_;  // frames x iterations that needed the reference-order sweep
     std::vector<ps_iter_stats> trace_;
 };
 

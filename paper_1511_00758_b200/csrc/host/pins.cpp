@@ -1,0 +1,79 @@
+// pins.cpp — does the triangle order matter for this frame?
+//
+// The reference pins every vertex pixel left uncovered by the top-left tie
+// rule to its FIRST incident triangle (proj/src/mesh.cpp:109-122).  Only hull
+// vertices can be uncovered.  If all incident triangles of every such vertex
+// evaluate to the same binary32 disparity there, the choice is irrelevant and
+// any triangle order (the fast radial sweep's) reproduces the reference; if
+// two of them differ (typically d = 0 with plane values of +-1e-17, which
+// decides 0 <= d < ND), the frame must use the reference's own triangle order
+// (delaunay_lex).  Arithmetic is the reference's: fitPlane in binary64 in
+// source order without FMA (mesh.cpp:12-26; this file is compiled with
+// -ffp-contract=off), plane evaluation ((a*u)+(b*v))+c then a binary32
+// rounding (mesh.hpp:19, mesh.cpp:158).
+#include <cstring>
+#include <vector>
+
+#include "delaunay.hpp"
+
+namespace ps {
+
+namespace {
+
+bool tie_accept(int xi, int yi, int xj, int yj) {
+    // edge i->j accepts pixels on it (mesh.cpp:80)
+    return (yj < yi) || (yj == yi && xj > xi);
+}
+
+float plane_at_vertex(const int* u, const int* v, const double* d, const int* t, int k) {
+    const long long u1 = u[t[0]], u2 = u[t[1]], u3 = u[t[2]];
+    const long long w1 = v[t[0]], w2 = v[t[1]], w3 = v[t[2]];
+    const long long det = u1 * (w2 - w3) + u2 * (w3 - w1) + u3 * (w1 - w2);
+    if (det == 0) return 0.0f;
+    const double d1 = d[t[0]], d2 = d[t[1]], d3 = d[t[2]];
+    const double dA = d1 * double(w2 - w3) + d2 * double(w3 - w1) + d3 * double(w1 - w2);
+    const double dB = double(u1) * (d2 - d3) + double(u2) * (d3 - d1) + double(u3) * (d1 - d2);
+    const double dC = d1 * double(u2 * w3 - u3 * w2) - d2 * double(u1 * w3 - u3 * w1) +
+                      d3 * double(u1 * w2 - u2 * w1);
+    const double a = dA / double(det), b = dB / double(det), c = dC / double(det);
+    const double s = a * double(u[t[k]]) + b * double(v[t[k]]);
+    return float(s + c);
+}
+
+}  // namespace
+
+bool pin_ambiguous(const int* u, const int* v, const double* d, int n, const int* tris, int nt,
+                   int width, int height, std::vector<uint8_t>& covered,
+                   std::vector<float>& first) {
+    covered.assign(n, 0);
+    for (int t = 0; t < nt; ++t) {
+        const int* tr = tris + 3 * t;
+        for (int k = 0; k < 3; ++k) {
+            const int p = tr[k], q = tr[(k + 1) % 3], r = tr[(k + 2) % 3];
+            // vertex p: edges r->p and p->q meet there with value 0; the
+            // third edge is positive (non-degenerate triangle)
+            if (tie_accept(u[r], v[r], u[p], v[p]) && tie_accept(u[p], v[p], u[q], v[q]))
+                covered[p] = 1;
+        }
+    }
+    first.assign(n, 0.0f);
+    std::vector<uint8_t>& seen = covered;  // 0 uncovered/unseen, 1 covered, 2 uncovered+seen
+    for (int t = 0; t < nt; ++t) {
+        const int* tr = tris + 3 * t;
+        for (int k = 0; k < 3; ++k) {
+            const int p = tr[k];
+            if (seen[p] == 1) continue;
+            if (u[p] < 0 || u[p] >= width || v[p] < 0 || v[p] >= height) continue;
+            const float val = plane_at_vertex(u, v, d, tr, k);
+            if (seen[p] == 0) {
+                seen[p] = 2;
+                first[p] = val;
+            } else if (std::memcmp(&val, &first[p], sizeof(float)) != 0) {
+                return true;
+            }
+        }
+    }
+    return false;
+}
+
+}  // namespace ps

@@ -94,10 +94,11 @@ int launch_resample_invalid(const unsigned long long* Cb, int cells_per_frame, i
 // S[f] = S[f] + a[f] + b[f]
 int launch_add_counts(int* S, const int* a, const int* b, int frames, cudaStream_t st);
 
-// Packs supports [S_prev[f], S_now[f]) of every frame into out (u,v pairs) at off[f].
-int launch_pack_new_supports(const int* su, const int* sv, int scap, const int* S_prev,
-                             const int* S_now, const int* off, int frames, int max_new,
-                             int2* out, cudaStream_t st);
+// Packs supports [S_prev[f], S_now[f]) of every frame into out (u,v pairs)
+// and out_d (disparities) at off[f].
+int launch_pack_new_supports(const int* su, const int* sv, const double* sd, int scap,
+                             const int* S_prev, const int* S_now, const int* off, int frames,
+                             int max_new, int2* out, double* out_d, cudaStream_t st);
 
 // Stage-API helpers (single frame, host-visible semantics).
 int launch_interpolate(const int32_t* lookup, const double* planes, FrameGeom g,

@@ -93,15 +93,18 @@ __global__ void k_add_counts(int* S, const int* a, const int* b, int frames) {
     if (f < frames) S[f] += (a ? a[f] : 0) + (b ? b[f] : 0);
 }
 
-__global__ void k_pack_new(const int* __restrict__ su, const int* __restrict__ sv, int scap,
+__global__ void k_pack_new(const int* __restrict__ su, const int* __restrict__ sv,
+                           const double* __restrict__ sd, int scap,
                            const int* __restrict__ S_prev, const int* __restrict__ S_now,
-                           const int* __restrict__ off, int2* __restrict__ out) {
+                           const int* __restrict__ off, int2* __restrict__ out,
+                           double* __restrict__ out_d) {
     const int f = blockIdx.y;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int n = S_now[f] - S_prev[f];
     if (i >= n) return;
     const long long s = (long long)f * scap + S_prev[f] + i;
     out[off[f] + i] = make_int2(su[s], sv[s]);
+    out_d[off[f] + i] = sd[s];
 }
 
 }  // namespace
@@ -129,12 +132,12 @@ int launch_add_counts(int* S, const int* a, const int* b, int frames, cudaStream
     return 1;
 }
 
-int launch_pack_new_supports(const int* su, const int* sv, int scap, const int* S_prev,
-                             const int* S_now, const int* off, int frames, int max_new, int2* out,
-                             cudaStream_t st) {
+int launch_pack_new_supports(const int* su, const int* sv, const double* sd, int scap,
+                             const int* S_prev, const int* S_now, const int* off, int frames,
+                             int max_new, int2* out, double* out_d, cudaStream_t st) {
     if (max_new <= 0) return 0;
     dim3 grid((max_new + 255) / 256, frames);
-    k_pack_new<<<grid, 256, 0, st>>>(su, sv, scap, S_prev, S_now, off, out);
+    k_pack_new<<<grid, 256, 0, st>>>(su, sv, sd, scap, S_prev, S_now, off, out, out_d);
     return 1;
 }
 

@@ -54,6 +54,15 @@ def golden_names(prefix):
     return sorted(os.path.basename(p) for p in glob.glob(os.path.join(GOLDEN, prefix + "*.npz")))
 
 
+def random_image(width, height, seed):
+    """testutil::randomImage (proj/tests/testutil.hpp:10-17): raw std::mt19937(seed)
+    draws & 0xff.  numpy's RandomState seeds MT19937 with init_genrand exactly like
+    std::mt19937, so the images are the reference tests' own images."""
+    rs = np.random.RandomState(seed)
+    raw = rs.randint(0, 2**32, size=width * height, dtype=np.uint32)
+    return (raw & 0xFF).astype(np.uint8).reshape(height, width)
+
+
 def config_of(meta):
     import paper_1511_00758_b200 as ps
 

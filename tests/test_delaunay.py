@@ -147,16 +147,24 @@ def _point_sets(rng, count):
         yield u[p].astype(np.int32), v[p].astype(np.int32)
 
 
+def fast(u, v):
+    return ps.delaunay_triangulate(np.asarray(u, np.int32), np.asarray(v, np.int32), fast=True)
+
+
 def test_set_equals_oracle_restatement(orc):
     rng = np.random.default_rng(11)
     for u, v in _point_sets(rng, 1500):
-        assert canon(tri(u, v)) == canon(orc.delaunay(u, v))
+        want = orc.delaunay(u, v)
+        assert canon(fast(u, v)) == canon(want)        # radial sweep: same set
+        assert np.array_equal(tri(u, v), want)         # lexicographic sweep: same array
 
 
 def test_set_equals_compiled_reference(ref):
     rng = np.random.default_rng(12)
     for u, v in _point_sets(rng, 1500):
-        assert canon(tri(u, v)) == canon(ref.delaunay(u, v))
+        want = ref.delaunay(u, v)
+        assert canon(fast(u, v)) == canon(want)
+        assert np.array_equal(tri(u, v), want)
 
 
 def test_pipeline_support_sets_equal_reference(orc):
@@ -168,4 +176,6 @@ def test_pipeline_support_sets_equal_reference(orc):
         if int(g["status"]) != 0:
             continue
         u, v = g["sup_u"], g["sup_v"]
-        assert canon(tri(u, v)) == canon(orc.delaunay(u, v)), name
+        want = orc.delaunay(u, v)
+        assert canon(fast(u, v)) == canon(want), name
+        assert np.array_equal(tri(u, v), want), name

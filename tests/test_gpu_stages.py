@@ -5,13 +5,13 @@ import numpy as np
 import pytest
 
 import paper_1511_00758_b200 as ps
-from conftest import load_golden
+from conftest import load_golden, random_image
 
 pytestmark = pytest.mark.gpu
 
 
 def rand_img(w, h, seed):
-    return np.random.default_rng(seed).integers(0, 256, (h, w), dtype=np.uint8)
+    return random_image(w, h, seed)  # the reference tests' own images (testutil.hpp:10-17)
 
 
 # ------------------------------------------------------------- K1 census / mask
@@ -99,7 +99,7 @@ def test_checkerboard_cap(ctx):
 
 
 # ------------------------------------------------------------- K3 matching
-def test_matching_known_answers(ctx):
+def test_matching_known_answers(ctx, orc):
     cfg = ps.PipelineConfig()
     img = rand_img(80, 64, 12)
     c = ctx.census(img)
@@ -113,7 +113,13 @@ def test_matching_known_answers(ctx):
         cl, cr = ctx.census(left), ctx.census(right)
         u, v, s = ctx.detect_candidates(left, cfg)
         su, sv, sd = ctx.match_epipolar(cl, cr, u, v, cfg)
-        assert len(su) > 0 and (sd == 7.0).all()
+        # The reference test claims d == 7 at EVERY accepted point; the
+        # reference code itself accepts a few points near the left border
+        # with d < 7 on these very images (oracle/_ref, same mt19937 bytes),
+        # so parity with the reference is the check, plus the bulk property.
+        ou, ov, od = orc.match_epipolar(cl, cr, u, v, cfg)
+        assert np.array_equal(su, ou) and np.array_equal(sd, od)
+        assert len(su) > 0 and np.mean(sd == 7.0) > 0.9
     left = rand_img(64, 48, 5)  # :107-117
     right = rand_img(64, 48, 77)
     right[:, : 64 - 9] = left[:, 9:]
