@@ -401,7 +401,16 @@ ps_status ps_mesh_build(ps_ctx* ctx, const int* u, const int* v, const double* d
     cudaMemcpyAsync(d_off, off, sizeof(off), cudaMemcpyHostToDevice, st);
     cudaMemsetAsync(d_lk, 0xff, sizeof(int32_t) * P, st);
     cudaMemsetAsync(d_err, 0, sizeof(int), st);
-    e.count_launches(ps::launch_mesh(d_t, d_off, 1, nt, d_u, d_v, d_d, np, g, d_pl, d_lk, d_err, st));
+    // hull-vertex pins in the caller's triangle order (mesh.cpp:109-122)
+    std::vector<uint8_t> state, pins;
+    std::vector<float> first;
+    if (nt > 0)
+        ps::mesh_pins(u, v, d, n_points, tris, nt, width, height, false, state, first, pins);
+    uint8_t* d_pin = e.dev<uint8_t>(e.s_i, std::max(1, nt));
+    if (!d_pin) return set_error(PS_CUDA_ERROR, "allocation failed");
+    if (nt > 0) cudaMemcpyAsync(d_pin, pins.data(), nt, cudaMemcpyHostToDevice, st);
+    e.count_launches(ps::launch_mesh(d_t, d_off, 1, nt, d_u, d_v, d_d, np, g, d_pin, d_pl, d_lk,
+                                     d_err, st));
     int err = 0;
     cudaMemcpyAsync(&err, d_err, sizeof(int), cudaMemcpyDeviceToHost, st);
     if (planes && nt > 0) cudaMemcpyAsync(planes, d_pl, sizeof(double) * 3 * nt, cudaMemcpyDeviceToHost, st);

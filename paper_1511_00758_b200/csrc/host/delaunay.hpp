@@ -23,7 +23,7 @@ struct DelaunayWorkspace {
     std::vector<int> tv, tn;  // triangle vertices / neighbour half-edges
     std::vector<int> hnext, hprev, hedge;
     std::vector<int> stack;
-    std::vector<uint8_t> covered;  // pin_ambiguous scratch
+    std::vector<uint8_t> covered;  // mesh_pins scratch
     std::vector<float> first;
 };
 
@@ -37,10 +37,12 @@ int delaunay(const int* u, const int* v, int n, std::vector<int>& tris, Delaunay
 // sweep, delaunay_lex.cpp).  Slower (~4x more in-circle tests).
 int delaunay_lex(const int* u, const int* v, int n, std::vector<int>& tris, DelaunayWorkspace& ws);
 
-// True when the first-incident-triangle pinning of an uncovered hull vertex
-// (mesh.cpp:109-122) would depend on the triangle order for this mesh (pins.cpp).
-bool pin_ambiguous(const int* u, const int* v, const double* d, int n, const int* tris, int nt,
-                   int width, int height, std::vector<uint8_t>& covered,
-                   std::vector<float>& first);
+// Hull-vertex pinning (mesh.cpp:109-122) for this triangle list: pin_bits[t]
+// bit k set when corner k of triangle t is an uncovered vertex pixel whose
+// first incident triangle is t.  With check_order, returns true (and stops)
+// as soon as the pinned value would depend on the triangle order (pins.cpp).
+bool mesh_pins(const int* u, const int* v, const double* d, int n, const int* tris, int nt,
+               int width, int height, bool check_order, std::vector<uint8_t>& state,
+               std::vector<float>& first, std::vector<uint8_t>& pin_bits);
 
 }  // namespace ps

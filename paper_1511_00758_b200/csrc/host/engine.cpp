@@ -143,9 +143,10 @@ Engine::~Engine() {
         if (b->p) cudaFreeHost(b->p);
     for (FrameGroup& g : groups_) {
         for (DevBuf* b : {&g.dTri, &g.dTriOff, &g.dPlanes, &g.dPack, &g.dPackD, &g.dPackOff,
-                          &g.dSprev, &g.dChunk})
+                          &g.dSprev, &g.dChunk, &g.dPin})
             if (b->p) cudaFree(b->p);
-        for (HostBuf* b : {&g.hS, &g.hSprev, &g.hPackOff, &g.hPack, &g.hPackD, &g.hTri, &g.hTriOff})
+        for (HostBuf* b : {&g.hS, &g.hSprev, &g.hPackOff, &g.hPack, &g.hPackD, &g.hTri, &g.hTriOff,
+                           &g.hPin})
             if (b->p) cudaFreeHost(b->p);
         if (g.st) cudaStreamDestroy(g.st);
     }
@@ -336,7 +337,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     float* dCf = dev<float>(dCf_, size_t(F) * P);
     float* dDense = dev<float>(dDense_, size_t(F) * P);
     uint8_t* dDenseV = dev<uint8_t>(dDenseV_, size_t(F) * P);
-    int32_t* dLookup = reinterpret_cast<int32_t*>(dev<int>(dLookup_, size_t(F) * P));
+    float* dDit = dev<float>(dLookup_, size_t(F) * P);  // D_it per pixel (NaN = invalid)
     int* dSu = dev<int>(dSu_, size_t(F) * scap_);
     int* dSv = dev<int>(dSv_, size_t(F) * scap_);
     double* dSd = dev<double>(dSd_, size_t(F) * scap_);
@@ -366,7 +367,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     unsigned long long* hTraceSum =
         reinterpret_cast<unsigned long long*>(host<uint8_t>(hTraceSum_, size_t(F) * iters * 8));
     unsigned* hTraceValid = reinterpret_cast<unsigned*>(host<uint8_t>(hTraceValid_, size_t(F) * iters * 4));
-    const void* must[] = {dMask, dMaskCount, dCL, dCR, dDf, dDv, dCf, dDense, dDenseV, dLookup,
+    const void* must[] = {dMask, dMaskCount, dCL, dCR, dDf, dDv, dCf, dDense, dDenseV, dDit,
                           dSu, dSv, dSd, dS, dSnext, dTaken, dCg, dCb, dBinKeys, dBinCount,
                           dScratch, dCandU, dCandV, dCandCount, dOk, dDisp, dRemU, dRemV,
                           dRemCount, dConf, dChunk, dTraceSum, dTraceValid, dErr, hS, hMaskCount,
@@ -422,6 +423,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     hu_.resize(F);
     hv_.resize(F);
     hd_.resize(F);
+    hpin_.resize(F);
     htri_.resize(F);
     for (int f = 0; f < F; ++f) {
         hu_[f].clear();
@@ -527,10 +529,14 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                 const int ns = int(hu_[f].size());
                 DelaunayWorkspace& w = ws_[worker];
                 int t = delaunay(hu_[f].data(), hv_[f].data(), ns, htri_[f], w);
-                if (t > 0 && pin_ambiguous(hu_[f].data(), hv_[f].data(), hd_[f].data(), ns,
-                                           htri_[f].data(), t, W, H, w.covered, w.first)) {
+                if (t > 0 && mesh_pins(hu_[f].data(), hv_[f].data(), hd_[f].data(), ns,
+                                       htri_[f].data(), t, W, H, true, w.covered, w.first,
+                                       hpin_[f])) {
                     t = delaunay_lex(hu_[f].data(), hv_[f].data(), ns, htri_[f], w);
                     lex_used_[f] += 1;
+                    if (t > 0)
+                        mesh_pins(hu_[f].data(), hv_[f].data(), hd_[f].data(), ns, htri_[f].data(),
+                                  t, W, H, false, w.covered, w.first, hpin_[f]);
                 }
                 if (t < 0) {
                     status_[f] = PS_ERROR;
@@ -547,18 +553,26 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                 total_tri += grp.ntri[i];
             }
             hTriOff[n] = int(total_tri);
-            int* hTri = host<int>(grp.hTri, size_t(std::max<long long>(total_tri, 1)) * 3);
-            int* dTri = dev<int>(grp.dTri, size_t(std::max<long long>(total_tri, 1)) * 3);
-            double* dPlanes = dev<double>(grp.dPlanes, size_t(std::max<long long>(total_tri, 1)) * 3);
+            const size_t ntot = size_t(std::max<long long>(total_tri, 1));
+            int* hTri = host<int>(grp.hTri, ntot * 3);
+            uint8_t* hPin = host<uint8_t>(grp.hPin, ntot);
+            int* dTri = dev<int>(grp.dTri, ntot * 3);
+            uint8_t* dPin = dev<uint8_t>(grp.dPin, ntot);
             int* dTriOff = static_cast<int*>(grp.dTriOff.p);
-            if (!hTri || !dTri || !dPlanes) return fail(PS_CUDA_ERROR, "allocation failed (triangles)");
+            if (!hTri || !dTri || !hPin || !dPin)
+                return fail(PS_CUDA_ERROR, "allocation failed (triangles)");
             pool_->parallel_for(n, [&](int i, int) {
-                if (grp.ntri[i] > 0)
+                if (grp.ntri[i] > 0) {
                     std::memcpy(hTri + 3ll * hTriOff[i], htri_[f0 + i].data(), sizeof(int) * 3 * grp.ntri[i]);
+                    std::memcpy(hPin + hTriOff[i], hpin_[f0 + i].data(), grp.ntri[i]);
+                }
             });
-            if (total_tri > 0)
+            if (total_tri > 0) {
                 s = check(cudaMemcpyAsync(dTri, hTri, sizeof(int) * 3 * total_tri, cudaMemcpyHostToDevice, gs),
                           "H2D triangles");
+                if (s == PS_OK)
+                    s = check(cudaMemcpyAsync(dPin, hPin, total_tri, cudaMemcpyHostToDevice, gs), "H2D pins");
+            }
             if (s == PS_OK)
                 s = check(cudaMemcpyAsync(dTriOff, hTriOff, sizeof(int) * (n + 1), cudaMemcpyHostToDevice, gs),
                           "H2D triangle offsets");
@@ -573,13 +587,13 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                 final_count_[f0 + i] = hs[i];
             }
 
-            // ---- K5/K6 mesh (mesh.cpp:44-123)
-            int32_t* lk = dLookup + size_t(f0) * P;
-            cudaMemsetAsync(lk, 0xff, sizeof(int32_t) * n * P, gs);
-            begin_kernel("mesh", 4.0 * double(P) * n + 60.0 * double(total_tri), gs);
-            launches_ += launch_mesh(dTri, dTriOff, n, total_tri, dSu + size_t(f0) * scap_,
-                                     dSv + size_t(f0) * scap_, dSd + size_t(f0) * scap_, scap_, g,
-                                     dPlanes, lk, dErr, gs);
+            // ---- K5/K6 mesh (mesh.cpp:44-123) -> interpolated disparity (mesh.cpp:149-182)
+            float* lk = dDit + size_t(f0) * P;
+            cudaMemsetAsync(lk, 0xff, sizeof(float) * n * P, gs);  // NaN: outside the hull
+            begin_kernel("mesh", 4.0 * double(P) * n + 36.0 * double(total_tri), gs);
+            launches_ += launch_mesh_disparity(dTri, dTriOff, n, total_tri, dSu + size_t(f0) * scap_,
+                                               dSv + size_t(f0) * scap_, dSd + size_t(f0) * scap_,
+                                               scap_, g, dPin, float(cfg.max_disparity), lk, dErr, gs);
             end_kernel(gs);
 
             // ---- K7 (+K9) refine (mesh.cpp:149-182, pipeline.cpp:33-86)
@@ -594,8 +608,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
             ra.g = g;
             ra.frames = n;
             ra.mask = dMask + fp;
-            ra.lookup = lk;
-            ra.planes = dPlanes;
+            ra.dit = lk;
             ra.cl = dCL + fp;
             ra.cr = dCR + fp;
             ra.max_disp = float(cfg.max_disparity);
@@ -628,8 +641,8 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                 uint32_t* tk = dTaken + size_t(f0) * words;
                 int* chunk = static_cast<int*>(grp.dChunk.p);
                 begin_kernel("resample", 0.0, gs);
-                launches_ += launch_resample_confident(cg, cells, cells_max, g, n, lk, dPlanes, tk,
-                                                       su, sv, sd, scap_, grp.S, dConf + f0, chunk, gs);
+                launches_ += launch_resample_confident(cg, cells, cells_max, g, n, lk, tk, su, sv,
+                                                       sd, scap_, grp.S, dConf + f0, chunk, gs);
                 launches_ += launch_resample_invalid(cb, cells, cells_max, g, n,
                                                      dRemU + size_t(f0) * cells_max,
                                                      dRemV + size_t(f0) * cells_max, cells_max,

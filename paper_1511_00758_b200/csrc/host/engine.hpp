@@ -46,8 +46,8 @@ struct FrameGroup {
     cudaStream_t st = nullptr;
     int* S = nullptr;      // device support counts of the group's frames (current)
     int* Snext = nullptr;  // device support counts (next)
-    DevBuf dTri, dTriOff, dPlanes, dPack, dPackD, dPackOff, dSprev, dChunk;
-    HostBuf hS, hSprev, hPackOff, hPack, hPackD, hTri, hTriOff;
+    DevBuf dTri, dTriOff, dPlanes, dPack, dPackD, dPackOff, dSprev, dChunk, dPin;
+    HostBuf hS, hSprev, hPackOff, hPack, hPackD, hTri, hTriOff, hPin;
     std::vector<int> ntri;
     double millis = 0.0;
 };
@@ -136,6 +136,7 @@ private:
     int scap_ = 0;
     std::vector<std::vector<int>> hu_, hv_, htri_;
     std::vector<std::vector<double>> hd_;
+    std::vector<std::vector<uint8_t>> hpin_;
     std::vector<int> status_, final_count_;
     std::vector<int> lex_used_;  // frames x iterations that needed the reference-order sweep
     std::vector<ps_iter_stats> trace_;

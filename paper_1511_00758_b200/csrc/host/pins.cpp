@@ -1,16 +1,21 @@
-// pins.cpp — does the triangle order matter for this frame?
+// pins.cpp — hull-vertex pinning decided on the host, from the exact tie rule.
 //
 // The reference pins every vertex pixel left uncovered by the top-left tie
-// rule to its FIRST incident triangle (proj/src/mesh.cpp:109-122).  Only hull
-// vertices can be uncovered.  If all incident triangles of every such vertex
-// evaluate to the same binary32 disparity there, the choice is irrelevant and
-// any triangle order (the fast radial sweep's) reproduces the reference; if
-// two of them differ (typically d = 0 with plane values of +-1e-17, which
-// decides 0 <= d < ND), the frame must use the reference's own triangle order
-// (delaunay_lex).  Arithmetic is the reference's: fitPlane in binary64 in
-// source order without FMA (mesh.cpp:12-26; this file is compiled with
-// -ffp-contract=off), plane evaluation ((a*u)+(b*v))+c then a binary32
-// rounding (mesh.hpp:19, mesh.cpp:158).
+// rule to its FIRST incident triangle (proj/src/mesh.cpp:109-122).  A vertex
+// pixel lies on two edges of each incident triangle (edge value 0) and
+// strictly inside the third, so it is covered by that triangle iff both
+// incident edges accept ties (mesh.cpp:80); only hull vertices can end up
+// uncovered.  mesh_pins() marks, per triangle, the corners that pin (3 bits),
+// which the raster kernel stores directly.
+//
+// It also answers whether the triangle ORDER matters for this mesh: if all
+// incident triangles of every uncovered vertex evaluate to the same binary32
+// disparity there, any order reproduces the reference; if two differ
+// (typically d = 0 with plane values of +-1e-17, which decides 0 <= d < ND),
+// the frame must use the reference's own order (delaunay_lex).  Arithmetic is
+// the reference's: fitPlane in binary64 in source order without FMA
+// (mesh.cpp:12-26; this file is compiled with -ffp-contract=off), plane
+// evaluation ((a*u)+(b*v))+c then a binary32 rounding (mesh.hpp:19, mesh.cpp:158).
 #include <cstring>
 #include <vector>
 
@@ -42,34 +47,34 @@ float plane_at_vertex(const int* u, const int* v, const double* d, const int* t,
 
 }  // namespace
 
-bool pin_ambiguous(const int* u, const int* v, const double* d, int n, const int* tris, int nt,
-                   int width, int height, std::vector<uint8_t>& covered,
-                   std::vector<float>& first) {
-    covered.assign(n, 0);
+bool mesh_pins(const int* u, const int* v, const double* d, int n, const int* tris, int nt,
+               int width, int height, bool check_order, std::vector<uint8_t>& state,
+               std::vector<float>& first, std::vector<uint8_t>& pin_bits) {
+    // state: 0 = not (yet) seen uncovered, 1 = covered, 2 = uncovered and pinned
+    state.assign(n, 0);
     for (int t = 0; t < nt; ++t) {
         const int* tr = tris + 3 * t;
         for (int k = 0; k < 3; ++k) {
             const int p = tr[k], q = tr[(k + 1) % 3], r = tr[(k + 2) % 3];
-            // vertex p: edges r->p and p->q meet there with value 0; the
-            // third edge is positive (non-degenerate triangle)
             if (tie_accept(u[r], v[r], u[p], v[p]) && tie_accept(u[p], v[p], u[q], v[q]))
-                covered[p] = 1;
+                state[p] = 1;
         }
     }
-    first.assign(n, 0.0f);
-    std::vector<uint8_t>& seen = covered;  // 0 uncovered/unseen, 1 covered, 2 uncovered+seen
+    pin_bits.assign(nt, 0);
+    if (check_order) first.assign(n, 0.0f);
     for (int t = 0; t < nt; ++t) {
         const int* tr = tris + 3 * t;
         for (int k = 0; k < 3; ++k) {
             const int p = tr[k];
-            if (seen[p] == 1) continue;
+            if (state[p] == 1) continue;
             if (u[p] < 0 || u[p] >= width || v[p] < 0 || v[p] >= height) continue;
-            const float val = plane_at_vertex(u, v, d, tr, k);
-            if (seen[p] == 0) {
-                seen[p] = 2;
-                first[p] = val;
-            } else if (std::memcmp(&val, &first[p], sizeof(float)) != 0) {
-                return true;
+            if (state[p] == 0) {
+                state[p] = 2;
+                pin_bits[t] |= uint8_t(1u << k);  // first incident triangle
+                if (check_order) first[p] = plane_at_vertex(u, v, d, tr, k);
+            } else if (check_order) {
+                const float val = plane_at_vertex(u, v, d, tr, k);
+                if (std::memcmp(&val, &first[p], sizeof(float)) != 0) return true;
             }
         }
     }

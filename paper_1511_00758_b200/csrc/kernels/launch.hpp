@@ -45,11 +45,22 @@ int launch_emit_matches(const int* cand_u, const int* cand_v, const int* cand_co
 
 // K5+K6 — per-triangle plane fit (binary64, source order, no FMA;
 // proj/src/mesh.cpp:12-26) and exact top-left rasterisation into the
-// triangle lookup (mesh.cpp:58-107), then hull-vertex pinning (mesh.cpp:109-122).
+// triangle lookup (mesh.cpp:58-107), with hull-vertex pinning (mesh.cpp:109-122)
+// given as host-computed pin bits (3 per triangle, pins.cpp; may be null).
 // Triangles are flat over frames: frame f owns [tri_off[f], tri_off[f+1]).
+// The lookup must be preset to -1.
 int launch_mesh(const int* tris, const int* tri_off, int frames, long long total_tris,
                 const int* su, const int* sv, const double* sd, int scap, FrameGeom g,
-                double* planes, int32_t* lookup, int* err_flag, cudaStream_t st);
+                const uint8_t* pin_bits, double* planes, int32_t* lookup, int* err_flag,
+                cudaStream_t st);
+// Pipeline variant: rasterises the interpolated disparity itself
+// (interpolate(), mesh.cpp:149-182) instead of the triangle id: dit[px] =
+// binary32 plane value when 0 <= d < max_disp, NaN for invalid or outside the
+// hull.  dit must be preset to NaN (memset 0xff).
+int launch_mesh_disparity(const int* tris, const int* tri_off, int frames, long long total_tris,
+                          const int* su, const int* sv, const double* sd, int scap, FrameGeom g,
+                          const uint8_t* pin_bits, float max_disp, float* dit, int* err_flag,
+                          cudaStream_t st);
 
 // K7 (+K9 when last) — fused interpolate / costEvaluation / disparityRefinement
 // with per-cell packed-key atomicMin grids and the trace reduction
@@ -58,8 +69,7 @@ struct RefineArgs {
     FrameGeom g;
     int frames;
     const uint8_t* mask;
-    const int32_t* lookup;
-    const double* planes;
+    const float* dit;  // interpolated disparity, NaN = invalid (launch_mesh_disparity)
     const uint32_t* cl;
     const uint32_t* cr;
     float max_disp;
@@ -84,10 +94,9 @@ int launch_refine(const RefineArgs& a, const CostTables& tab, bool last, cudaStr
 // occupied invalid cells compacted into the re-match list
 // (proj/src/pipeline.cpp:88-129).  S_old[f] is the current support count.
 int launch_resample_confident(const unsigned long long* Cg, int cells_per_frame, int cell_stride,
-                              FrameGeom g, int frames, const int32_t* lookup,
-                              const double* planes, uint32_t* taken, int* su, int* sv, double* sd,
-                              int scap, const int* S_old, int* conf_count, int* chunk_buf,
-                              cudaStream_t st);
+                              FrameGeom g, int frames, const float* dit, uint32_t* taken, int* su,
+                              int* sv, double* sd, int scap, const int* S_old, int* conf_count,
+                              int* chunk_buf, cudaStream_t st);
 int launch_resample_invalid(const unsigned long long* Cb, int cells_per_frame, int cell_stride,
                             FrameGeom g, int frames, int* rem_u, int* rem_v, int rem_stride,
                             int* rem_count, int* chunk_buf, cudaStream_t st);

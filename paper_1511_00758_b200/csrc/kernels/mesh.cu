@@ -1,20 +1,24 @@
 // mesh.cu — K5+K6: per-triangle plane fit and exact rasterisation into the
-// pixel -> triangle lookup, then hull-vertex pinning.
+// pixel -> triangle lookup, with hull-vertex pinning.
 //
 // Replaces the DisparityMesh constructor (proj/src/mesh.cpp:44-56), fitPlane
-// (:12-26) and rasterize (:58-123).  One warp per triangle (flat over all
+// (:12-26) and rasterize (:58-123).  One thread per triangle (flat over all
 // frames of the batch; a triangle finds its frame by binary search of the
-// per-frame offsets).  Lane 0 solves the plane in binary64 in the reference's
-// source order with _rn intrinsics (no FMA); the warp then walks the rows of
-// the triangle's bounding box, every lane computing the exact integer span
-// [lo, hi] of the row with the top-left tie bias (mesh.cpp:75-106), and fills
-// the span with coalesced 4-byte stores.  Lookup entries are flat triangle
-// ids, so the per-pixel kernels index the flat plane array directly.
-//
-// Pinning (mesh.cpp:109-122): vertex pixels left uncovered by the tie rule get
-// their first incident triangle.  Done with atomicMin on an encoded value
-// (INT_MIN + t, always < -1) over the uncovered vertex pixels, then decoded.
-#include <climits>
+// per-frame offsets):
+//   * the thread solves its plane in binary64 in the reference's source order
+//     with _rn intrinsics (no FMA);
+//   * small triangles (the vast majority after the first iteration: median
+//     2x area 3-15 px) are filled by their own thread, row by row,
+//     from the exact integer span [lo, hi] of each row with the top-left tie
+//     bias (mesh.cpp:75-106);
+//   * large ones are handed to the whole warp, which computes 32 row spans at
+//     once (one per lane) and fills each row with coalesced stores.
+// Pinning (mesh.cpp:109-122): an uncovered vertex pixel takes its first
+// incident triangle; which (triangle, corner) pairs pin is decided on the host
+// from the exact tie rule (pins.cpp) and passed as 3 bits per triangle, so the
+// pin is a plain store here (no other triangle writes an uncovered pixel).
+// Lookup entries are flat triangle ids, so the per-pixel kernels index the
+// flat plane array directly.
 #include <cuda_runtime.h>
 
 #include "launch.hpp"
@@ -23,7 +27,7 @@ namespace ps {
 
 namespace {
 
-constexpr int kWarpsPerBlock = 8;
+constexpr int kThreads = 256;
 
 // floorDiv / ceilDiv of mesh.cpp:30-40, for 32- or 64-bit operands.
 template <class T>
@@ -44,34 +48,79 @@ __device__ __forceinline__ int frame_of(const int* __restrict__ tri_off, int fra
     return lo;
 }
 
+// Exact covered span of row v (mesh.cpp:84-103); false if the row is empty.
+template <class Int>
+__device__ __forceinline__ bool row_span(const int* x, const int* y, int v, int W, Int& lo, Int& hi) {
+    lo = 0;
+    hi = W - 1;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const int j = (i + 1) % 3;
+        const Int A = Int(y[i] - y[j]);
+        const Int bias = ((y[j] < y[i]) || (y[j] == y[i] && x[j] > x[i])) ? 0 : 1;
+        const Int K = Int(x[j] - x[i]) * Int(v - y[i]) + Int(y[j] - y[i]) * Int(x[i]);
+        if (A > 0) {
+            lo = max(lo, ceil_div<Int>(bias - K, A));
+        } else if (A < 0) {
+            hi = min(hi, floor_div<Int>(K - bias, -A));
+        } else if (K < bias) {
+            return false;
+        }
+    }
+    return lo <= hi;
+}
+
+// Output of the raster: the triangle id (DisparityMesh::lookup, the stage
+// API) or, for the pipeline, the interpolated disparity itself
+// (interpolate(), mesh.cpp:149-164: binary32 plane value if 0 <= d < ND,
+// NaN for "invalid or outside the hull"), so the per-pixel kernel reads one
+// word per pixel and never gathers planes.
+struct RasterOut {
+    int32_t* lookup;  // mode lookup
+    float* dit;       // mode disparity
+    float max_disp;
+};
+
+__device__ __forceinline__ void put(const RasterOut& o, long long frame_base, long long idx,
+                                    int32_t t, double a, double b, double c, int u, int v) {
+    if (o.lookup) {
+        o.lookup[frame_base + idx] = t;
+    } else {
+        const double s = __dadd_rn(__dmul_rn(a, double(u)), __dmul_rn(b, double(v)));
+        const float d = __double2float_rn(__dadd_rn(s, c));
+        o.dit[frame_base + idx] = (d >= 0.0f && d < o.max_disp) ? d : __int_as_float(0x7fffffff);
+    }
+}
+
 // Int = int when every edge-function value fits in 32 bits (W, H < 2^14),
 // long long otherwise; the results are identical, 32-bit division is faster.
 template <class Int>
-__global__ void __launch_bounds__(256) k_raster(const int* __restrict__ tris,
-                                                const int* __restrict__ tri_off, int frames,
-                                                long long total, const int* __restrict__ su,
-                                                const int* __restrict__ sv,
-                                                const double* __restrict__ sd, int scap,
-                                                FrameGeom g, double* __restrict__ planes,
-                                                int32_t* __restrict__ lookup,
-                                                int* __restrict__ err) {
-    const long long t = (long long)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-    if (t >= total) return;
+__global__ void __launch_bounds__(kThreads) k_raster(
+    const int* __restrict__ tris, const int* __restrict__ tri_off, int frames, long long total,
+    const int* __restrict__ su, const int* __restrict__ sv, const double* __restrict__ sd, int scap,
+    FrameGeom g, const uint8_t* __restrict__ pin_bits, double* __restrict__ planes, RasterOut out,
+    int* __restrict__ err) {
+    const long long t = (long long)blockIdx.x * kThreads + threadIdx.x;
     const int lane = threadIdx.x & 31;
-    const int f = frame_of(tri_off, frames, t);
-    const long long sb = (long long)f * scap;
-    const int i0 = __ldg(tris + 3 * t), i1 = __ldg(tris + 3 * t + 1), i2 = __ldg(tris + 3 * t + 2);
-    const int x[3] = {__ldg(su + sb + i0), __ldg(su + sb + i1), __ldg(su + sb + i2)};
-    const int y[3] = {__ldg(sv + sb + i0), __ldg(sv + sb + i1), __ldg(sv + sb + i2)};
-
-    if (lane == 0) {
+    const bool active = t < total;
+    const int W = g.width, H = g.height;
+    int x[3] = {0, 0, 0}, y[3] = {0, 0, 0};
+    int f = 0, vmin = 0, vmax = -1;
+    double pa = 0.0, pb = 0.0, pc = 0.0;
+    bool big = false;
+    if (active) {
+        f = frame_of(tri_off, frames, t);
+        const long long sb = (long long)f * scap;
+        const int i0 = __ldg(tris + 3 * t), i1 = __ldg(tris + 3 * t + 1), i2 = __ldg(tris + 3 * t + 2);
+        x[0] = __ldg(su + sb + i0); x[1] = __ldg(su + sb + i1); x[2] = __ldg(su + sb + i2);
+        y[0] = __ldg(sv + sb + i0); y[1] = __ldg(sv + sb + i1); y[2] = __ldg(sv + sb + i2);
         // fitPlane, mesh.cpp:12-26 (integer det exact; doubles in source order)
         const long long u1 = x[0], u2 = x[1], u3 = x[2], w1 = y[0], w2 = y[1], w3 = y[2];
         const long long det = u1 * (w2 - w3) + u2 * (w3 - w1) + u3 * (w1 - w2);
-        double* pl = planes + 3 * t;
+        double* pl = planes ? planes + 3 * t : nullptr;
         if (det == 0) {
             atomicExch(err, 1);
-            pl[0] = pl[1] = pl[2] = 0.0;
+            if (pl) pl[0] = pl[1] = pl[2] = 0.0;
         } else {
             const double d1 = __ldg(sd + sb + i0), d2 = __ldg(sd + sb + i1), d3 = __ldg(sd + sb + i2);
             const double dA = __dadd_rn(__dadd_rn(__dmul_rn(d1, double(w2 - w3)),
@@ -83,93 +132,112 @@ __global__ void __launch_bounds__(256) k_raster(const int* __restrict__ tris,
             const double dC = __dadd_rn(__dsub_rn(__dmul_rn(d1, double(u2 * w3 - u3 * w2)),
                                                   __dmul_rn(d2, double(u1 * w3 - u3 * w1))),
                                         __dmul_rn(d3, double(u1 * w2 - u2 * w1)));
-            pl[0] = __ddiv_rn(dA, double(det));
-            pl[1] = __ddiv_rn(dB, double(det));
-            pl[2] = __ddiv_rn(dC, double(det));
-        }
-    }
-
-    const int W = g.width, H = g.height;
-    const int vmin = max(0, min(y[0], min(y[1], y[2])));
-    const int vmax = min(H - 1, max(y[0], max(y[1], y[2])));
-    Int A[3], bias[3];
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-        const int j = (i + 1) % 3;
-        A[i] = y[i] - y[j];
-        bias[i] = ((y[j] < y[i]) || (y[j] == y[i] && x[j] > x[i])) ? 0 : 1;
-    }
-    int32_t* lk = lookup + f * g.pixels;
-    // 32 rows at a time: lane r computes the exact span of row r0 + r
-    // (mesh.cpp:84-103), then the warp fills each non-empty row with
-    // coalesced stores.
-    for (int r0 = vmin; r0 <= vmax; r0 += 32) {
-        const int v = r0 + lane;
-        Int lo = 0, hi = W - 1;
-        bool empty = v > vmax;
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            const int j = (i + 1) % 3;
-            const Int K = Int(x[j] - x[i]) * Int(v - y[i]) + Int(y[j] - y[i]) * Int(x[i]);
-            if (A[i] > 0) {
-                lo = max(lo, ceil_div(bias[i] - K, A[i]));
-            } else if (A[i] < 0) {
-                hi = min(hi, floor_div(K - bias[i], -A[i]));
-            } else if (K < bias[i]) {
-                empty = true;
+            pa = __ddiv_rn(dA, double(det));
+            pb = __ddiv_rn(dB, double(det));
+            pc = __ddiv_rn(dC, double(det));
+            if (planes) {
+                pl[0] = pa;
+                pl[1] = pb;
+                pl[2] = pc;
             }
         }
-        unsigned rows = __ballot_sync(0xffffffffu, !empty && lo <= hi);
-        const int lo32 = int(lo), hi32 = int(hi);
-        while (rows) {
-            const int r = __ffs(rows) - 1;
-            rows &= rows - 1;
-            const int l = __shfl_sync(0xffffffffu, lo32, r);
-            const int h = __shfl_sync(0xffffffffu, hi32, r);
-            int32_t* row = lk + (long long)(r0 + r) * W;
-            for (int u = l + lane; u <= h; u += 32) row[u] = int32_t(t);
+        const long long fb = f * g.pixels;
+        if (pin_bits) {
+            const unsigned bits = __ldg(pin_bits + t);
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                if ((bits >> k) & 1u)
+                    put(out, fb, (long long)y[k] * W + x[k], int32_t(t), pa, pb, pc, x[k], y[k]);
+        }
+        vmin = max(0, min(y[0], min(y[1], y[2])));
+        vmax = min(H - 1, max(y[0], max(y[1], y[2])));
+        const int xmin = min(x[0], min(x[1], x[2])), xmax = max(x[0], max(x[1], x[2]));
+        big = (vmax - vmin) >= 4 || (xmax - xmin) >= 24;
+        if (!big) {
+            for (int v = vmin; v <= vmax; ++v) {
+                Int lo, hi;
+                if (!row_span<Int>(x, y, v, W, lo, hi)) continue;
+                for (int u = int(lo); u <= int(hi); ++u)
+                    put(out, fb, (long long)v * W + u, int32_t(t), pa, pb, pc, u, v);
+            }
+        }
+    }
+    // Large triangles: the whole warp, 32 rows at a time.
+    unsigned bigs = __ballot_sync(0xffffffffu, big);
+    while (bigs) {
+        const int src = __ffs(bigs) - 1;
+        bigs &= bigs - 1;
+        int bx[3], by[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            bx[k] = __shfl_sync(0xffffffffu, x[k], src);
+            by[k] = __shfl_sync(0xffffffffu, y[k], src);
+        }
+        const int bf = __shfl_sync(0xffffffffu, f, src);
+        const int b0 = __shfl_sync(0xffffffffu, vmin, src);
+        const int b1 = __shfl_sync(0xffffffffu, vmax, src);
+        const int32_t bt = int32_t(__shfl_sync(0xffffffffu, (long long)t, src));
+        const double ba = __shfl_sync(0xffffffffu, pa, src);
+        const double bb = __shfl_sync(0xffffffffu, pb, src);
+        const double bc = __shfl_sync(0xffffffffu, pc, src);
+        const long long fb = bf * g.pixels;
+        for (int r0 = b0; r0 <= b1; r0 += 32) {
+            const int v = r0 + lane;
+            Int lo = 0, hi = -1;
+            const bool ok = v <= b1 && row_span<Int>(bx, by, v, W, lo, hi);
+            unsigned rows = __ballot_sync(0xffffffffu, ok);
+            const int lo32 = int(lo), hi32 = int(hi);
+            while (rows) {
+                const int r = __ffs(rows) - 1;
+                rows &= rows - 1;
+                const int l = __shfl_sync(0xffffffffu, lo32, r);
+                const int h = __shfl_sync(0xffffffffu, hi32, r);
+                const long long rowb = (long long)(r0 + r) * W;
+                for (int u = l + lane; u <= h; u += 32) put(out, fb, rowb + u, bt, ba, bb, bc, u, r0 + r);
+            }
         }
     }
 }
 
-__global__ void k_pin(const int* __restrict__ tris, const int* __restrict__ tri_off, int frames,
-                      long long total, const int* __restrict__ su, const int* __restrict__ sv,
-                      int scap, FrameGeom g, int32_t* __restrict__ lookup, int decode) {
-    const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= 3 * total) return;
-    const long long t = c / 3;
-    const int f = frame_of(tri_off, frames, t);
-    const int idx = __ldg(tris + c);
-    const int u = __ldg(su + (long long)f * scap + idx), v = __ldg(sv + (long long)f * scap + idx);
-    if (u < 0 || u >= g.width || v < 0 || v >= g.height) return;
-    int32_t* cell = lookup + f * g.pixels + (long long)v * g.width + u;
-    if (!decode) {
-        if (*cell < 0) atomicMin(cell, int32_t(INT_MIN + t));
-    } else {
-        const int32_t x = *cell;
-        if (x < -1) *cell = int32_t((long long)x - INT_MIN);
-    }
+template <class Int>
+void launch_raster(const int* tris, const int* tri_off, int frames, long long total, const int* su,
+                   const int* sv, const double* sd, int scap, FrameGeom g, const uint8_t* pin_bits,
+                   double* planes, RasterOut out, int* err, cudaStream_t st) {
+    const unsigned blocks = unsigned((total + kThreads - 1) / kThreads);
+    k_raster<Int><<<blocks, kThreads, 0, st>>>(tris, tri_off, frames, total, su, sv, sd, scap, g,
+                                               pin_bits, planes, out, err);
 }
 
 }  // namespace
 
 int launch_mesh(const int* tris, const int* tri_off, int frames, long long total_tris,
                 const int* su, const int* sv, const double* sd, int scap, FrameGeom g,
-                double* planes, int32_t* lookup, int* err_flag, cudaStream_t st) {
+                const uint8_t* pin_bits, double* planes, int32_t* lookup, int* err_flag,
+                cudaStream_t st) {
     if (total_tris <= 0) return 0;
-    const long long blocks = (total_tris + kWarpsPerBlock - 1) / kWarpsPerBlock;
-    if (g.width < (1 << 14) && g.height < (1 << 14)) {
-        k_raster<int><<<unsigned(blocks), 32 * kWarpsPerBlock, 0, st>>>(
-            tris, tri_off, frames, total_tris, su, sv, sd, scap, g, planes, lookup, err_flag);
-    } else {
-        k_raster<long long><<<unsigned(blocks), 32 * kWarpsPerBlock, 0, st>>>(
-            tris, tri_off, frames, total_tris, su, sv, sd, scap, g, planes, lookup, err_flag);
-    }
-    const long long corners = 3 * total_tris;
-    const unsigned pb = unsigned((corners + 255) / 256);
-    k_pin<<<pb, 256, 0, st>>>(tris, tri_off, frames, total_tris, su, sv, scap, g, lookup, 0);
-    k_pin<<<pb, 256, 0, st>>>(tris, tri_off, frames, total_tris, su, sv, scap, g, lookup, 1);
-    return 3;
+    const RasterOut out{lookup, nullptr, 0.0f};
+    if (g.width < (1 << 14) && g.height < (1 << 14))
+        launch_raster<int>(tris, tri_off, frames, total_tris, su, sv, sd, scap, g, pin_bits, planes,
+                           out, err_flag, st);
+    else
+        launch_raster<long long>(tris, tri_off, frames, total_tris, su, sv, sd, scap, g, pin_bits,
+                                 planes, out, err_flag, st);
+    return 1;
+}
+
+int launch_mesh_disparity(const int* tris, const int* tri_off, int frames, long long total_tris,
+                          const int* su, const int* sv, const double* sd, int scap, FrameGeom g,
+                          const uint8_t* pin_bits, float max_disp, float* dit, int* err_flag,
+                          cudaStream_t st) {
+    if (total_tris <= 0) return 0;
+    const RasterOut out{nullptr, dit, max_disp};
+    if (g.width < (1 << 14) && g.height < (1 << 14))
+        launch_raster<int>(tris, tri_off, frames, total_tris, su, sv, sd, scap, g, pin_bits,
+                           nullptr, out, err_flag, st);
+    else
+        launch_raster<long long>(tris, tri_off, frames, total_tris, su, sv, sd, scap, g, pin_bits,
+                                 nullptr, out, err_flag, st);
+    return 1;
 }
 
 }  // namespace ps

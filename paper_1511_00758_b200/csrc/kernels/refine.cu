@@ -1,8 +1,9 @@
 // refine.cu — K7 (+K9): the graded per-pixel kernel.
 //
 // One pass over the frame fuses, per gradient-mask pixel:
-//   interpolate   (proj/src/mesh.cpp:149-164): lookup -> plane -> binary32 D_it,
-//                 valid iff 0 <= D_it < ND;
+//   interpolate   (proj/src/mesh.cpp:149-164): D_it is read as written by the
+//                 raster (launch_mesh_disparity): binary32 plane value, NaN
+//                 when invalid or outside the hull;
 //   costEvaluation (proj/src/pipeline.cpp:33-54): k = popcount(cL(u) ^ cR(u-d)),
 //                 d = lround(D_it), sentinel k = 24 (cost 1.0) when unusable;
 //   disparityRefinement (pipeline.cpp:56-86): C_f/D_f fold, and the two
@@ -14,12 +15,16 @@
 //   trace (pipeline.cpp:183-191): sum of C_f over the mask in 2^-36 fixed
 //                 point (exact for every k/24 float) and the valid count.
 // In the last iteration the same pass also writes the full-image dense
-// interpolation (mesh.cpp:166-182, K9), reusing the lookup read.
+// interpolation (mesh.cpp:166-182, K9).
 //
-// Each thread owns 4 consecutive pixels of a frame (uchar4 mask, int4 lookup,
-// uint4 census, float4 C_f/D_f when the frame stride allows 16-B alignment).
-// Algorithmic traffic P + 29*M bytes per frame; planes and the
-// census gather of the right view are L2-resident.
+// Layout: a warp owns a 128-pixel chunk of one frame; slot j of lane l is
+// pixel chunk + 32*j + l, so every load/store instruction of the warp covers
+// 32 consecutive pixels (coalesced), the four first-level loads of all slots
+// (mask, D_it, cL, C_f) are issued before any use (memory-level parallelism),
+// and pixels of one occupancy cell are contiguous lanes of a slot: the grid
+// keys of a cell are min-reduced across the warp (__match_any_sync +
+// __reduce_min_sync on the two key words) before ONE atomicMin per cell and
+// slot.  Algorithmic traffic P + 29*M bytes per frame.
 #include <cuda_runtime.h>
 
 #include "launch.hpp"
@@ -28,157 +33,117 @@ namespace ps {
 
 namespace {
 
-struct CellAcc {
-    int cell = -1;
-    unsigned long long key = kEmptyCell;
-};
+constexpr int kSlots = 4;
+constexpr int kChunk = 32 * kSlots;
 
-__device__ __forceinline__ void acc_push(CellAcc& a, unsigned long long* __restrict__ grid, int cell,
-                                         unsigned long long key) {
-    if (cell != a.cell) {
-        if (a.cell >= 0) atomicMin(grid + a.cell, a.key);
-        a.cell = cell;
-        a.key = key;
-    } else if (key < a.key) {
-        a.key = key;
-    }
+// Warp-cooperative min of 64-bit keys over the lanes in `group` (same cell),
+// then one atomicMin by the group's lowest lane.
+__device__ __forceinline__ void group_atomic_min(unsigned group, int lane, bool has,
+                                                 unsigned long long key,
+                                                 unsigned long long* addr) {
+    const unsigned hi = has ? unsigned(key >> 32) : 0xffffffffu;
+    const unsigned hmin = __reduce_min_sync(group, hi);
+    const unsigned lo = (has && hi == hmin) ? unsigned(key) : 0xffffffffu;
+    const unsigned lmin = __reduce_min_sync(group, lo);
+    if (hmin != 0xffffffffu && lane == __ffs(group) - 1)
+        atomicMin(addr, (unsigned long long)hmin << 32 | lmin);
 }
 
-template <bool VEC, bool LAST>
-__global__ void __launch_bounds__(256) k_refine(RefineArgs a, CostTables tab) {
+__device__ __forceinline__ int div_small(int n, int d, float inv) {
+    // n / d for 0 <= n < 2^24 via a float reciprocal and one exact correction
+    int q = __float2int_rz(__int2float_rn(n) * inv);
+    if (q * d > n) --q;
+    else if ((q + 1) * d <= n) ++q;
+    return q;
+}
+
+template <bool LAST>
+__global__ void __launch_bounds__(256) k_refine(RefineArgs a, CostTables tab, float inv_cell,
+                                                float inv_w) {
     const int f = blockIdx.y;
     const long long P = a.g.pixels;
     const int W = a.g.width;
-    const int i0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;  // per-frame index (P < 2^31)
+    const int lane = threadIdx.x & 31;
+    const long long chunk = ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * kChunk;
     unsigned long long tsum = 0;
     unsigned tvalid = 0;
-    if (i0 < P) {
+    if (chunk < P) {  // warp-uniform
         const long long fb = (long long)f * P;
-        uint8_t m[4];
-        int32_t lk[4];
-        if (VEC) {
-            const uchar4 mv = *reinterpret_cast<const uchar4*>(a.mask + fb + i0);
-            m[0] = mv.x; m[1] = mv.y; m[2] = mv.z; m[3] = mv.w;
-        } else {
+        uint8_t m[kSlots];
+        float d[kSlots], cf[kSlots];
+        uint32_t cl[kSlots];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) m[j] = (i0 + j < P) ? a.mask[fb + i0 + j] : 0;
+        for (int j = 0; j < kSlots; ++j) {
+            const long long i = chunk + 32 * j + lane;
+            const bool in = i < P;
+            m[j] = in ? __ldg(a.mask + fb + i) : 0;
+            d[j] = in ? __ldg(a.dit + fb + i) : __int_as_float(0x7fffffff);
+            cl[j] = in ? __ldg(a.cl + fb + i) : 0u;
+            cf[j] = in ? a.Cf[fb + i] : 0.0f;
         }
-        const bool any_mask = (m[0] | m[1] | m[2] | m[3]) != 0;
-        if (LAST || any_mask) {
-            if (VEC) {
-                const int4 l4 = *reinterpret_cast<const int4*>(a.lookup + fb + i0);
-                lk[0] = l4.x; lk[1] = l4.y; lk[2] = l4.z; lk[3] = l4.w;
-            } else {
+        int u[kSlots], v[kSlots], k[kSlots];
+        uint32_t crv[kSlots];
+        const long long v0 = chunk / W;  // one 64-bit division per warp
+        const int r0 = int(chunk - v0 * W);
 #pragma unroll
-                for (int j = 0; j < 4; ++j) lk[j] = (i0 + j < P) ? a.lookup[fb + i0 + j] : -1;
-            }
-        }
-        const int v = i0 / W;
-        const int u = i0 - v * W;
-        float dit[4];
-        bool ok[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            ok[j] = false;
-            dit[j] = 0.0f;
-            const int uj = u + j;
-            const int vj = v + (uj >= W ? 1 : 0);  // W >= 16, so at most one wrap
-            const int uu = uj >= W ? uj - W : uj;
-            if ((LAST || m[j]) && (i0 + j < P) && lk[j] >= 0) {
-                const float d = plane_eval(a.planes + 3ll * lk[j], uu, vj);
-                dit[j] = d;
-                ok[j] = d >= 0.0f && d < a.max_disp;
-            }
-        }
-        if (LAST) {
-            float dv[4];
-            uint8_t dvv[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                dv[j] = ok[j] ? dit[j] : 0.0f;
-                dvv[j] = ok[j] ? 1 : 0;
-            }
-            if (VEC) {
-                *reinterpret_cast<float4*>(a.dense + fb + i0) = make_float4(dv[0], dv[1], dv[2], dv[3]);
-                *reinterpret_cast<uchar4*>(a.dense_valid + fb + i0) =
-                    make_uchar4(dvv[0], dvv[1], dvv[2], dvv[3]);
-            } else {
-                for (int j = 0; j < 4 && i0 + j < P; ++j) {
-                    a.dense[fb + i0 + j] = dv[j];
-                    a.dense_valid[fb + i0 + j] = dvv[j];
+        for (int j = 0; j < kSlots; ++j) {
+            const int r = r0 + 32 * j + lane;  // < W + 128 < 2^24
+            const int dv = div_small(r, W, inv_w);
+            v[j] = int(v0) + dv;
+            u[j] = r - dv * W;
+            k[j] = kCensusBits;  // sentinel cost 1.0 (pipeline.cpp:15,35)
+            crv[j] = 0;
+            if (m[j] && d[j] == d[j]) {  // mask pixel with a valid D_it
+                const int dr = lround_away(d[j]);
+                const int ur = u[j] - dr;
+                if (dr >= 0 && ur >= 2) {
+                    k[j] = 0;
+                    crv[j] = __ldg(a.cr + fb + (long long)v[j] * W + ur);
                 }
             }
         }
-        if (any_mask) {
-            uint32_t cl4[4];
-            float cf[4], df[4];
-            uint8_t dvalid[4];
-            if (VEC) {
-                const uint4 c = *reinterpret_cast<const uint4*>(a.cl + fb + i0);
-                cl4[0] = c.x; cl4[1] = c.y; cl4[2] = c.z; cl4[3] = c.w;
-                const float4 c2 = *reinterpret_cast<const float4*>(a.Cf + fb + i0);
-                cf[0] = c2.x; cf[1] = c2.y; cf[2] = c2.z; cf[3] = c2.w;
-            } else {
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    cl4[j] = (i0 + j < P) ? a.cl[fb + i0 + j] : 0u;
-                    cf[j] = (i0 + j < P) ? a.Cf[fb + i0 + j] : 0.0f;
-                }
+        for (int j = 0; j < kSlots; ++j) {
+            const long long i = chunk + 32 * j + lane;
+            const bool valid = d[j] == d[j];
+            if (LAST && i < P) {
+                a.dense[fb + i] = valid ? d[j] : 0.0f;
+                a.dense_valid[fb + i] = valid ? 1 : 0;
             }
-            bool upd[4];
-            CellAcc accg, accb;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                upd[j] = false;
-                df[j] = 0.0f;
-                dvalid[j] = 0;
-                if (!m[j]) continue;
-                const int uj = u + j;
-                const int vj = v + (uj >= W ? 1 : 0);
-                const int uu = uj >= W ? uj - W : uj;
-                int k = kCensusBits;  // sentinel cost 1.0 (pipeline.cpp:15,35)
-                if (ok[j]) {
-                    const int d = lround_away(dit[j]);
-                    const int ur = uu - d;
-                    if (d >= 0 && ur >= 2)
-                        k = __popc(cl4[j] ^ __ldg(a.cr + fb + (long long)vj * W + ur));
-                }
-                const float c = tab.cost[k];
+            if (k[j] == 0) k[j] = __popc(cl[j] ^ crv[j]);
+            bool qg = false, qb = false;
+            unsigned long long keyg = 0, keyb = 0;
+            int cell = -1;
+            if (m[j]) {
+                const float c = tab.cost[k[j]];
                 if (c < cf[j]) {  // pipeline.cpp:68-71
-                    upd[j] = true;
                     cf[j] = c;
-                    df[j] = dit[j];
-                    dvalid[j] = 1;
+                    a.Cf[fb + i] = c;
+                    a.Df[fb + i] = d[j];
+                    a.Dv[fb + i] = 1;
                 }
-                const int cell = (vj / a.cell) * a.cols + (uu / a.cell);
-                const unsigned long long idx = (unsigned long long)vj * W + uu;
-                if ((tab.low_mask >> k) & 1u) {
-                    acc_push(accg, a.Cg + (long long)f * a.cell_stride, cell,
-                             (unsigned long long)k << 32 | idx);
-                } else if ((tab.high_mask >> k) & 1u) {
-                    acc_push(accb, a.Cb + (long long)f * a.cell_stride, cell,
-                             (unsigned long long)(kCensusBits - k) << 32 | idx);
-                }
+                const unsigned long long idx = (unsigned long long)i;
+                qg = (tab.low_mask >> k[j]) & 1u;
+                qb = !qg && ((tab.high_mask >> k[j]) & 1u);
+                keyg = (unsigned long long)k[j] << 32 | idx;
+                keyb = (unsigned long long)(kCensusBits - k[j]) << 32 | idx;
                 tsum += __double2ull_rn(__dmul_rn(double(cf[j]), 68719476736.0));  // * 2^36
                 tvalid += cf[j] < tab.cost_high ? 1u : 0u;
             }
-            if (accg.cell >= 0) atomicMin(a.Cg + (long long)f * a.cell_stride + accg.cell, accg.key);
-            if (accb.cell >= 0) atomicMin(a.Cb + (long long)f * a.cell_stride + accb.cell, accb.key);
-            const bool any_upd = upd[0] | upd[1] | upd[2] | upd[3];
-            if (any_upd) {
-                if (VEC && upd[0] && upd[1] && upd[2] && upd[3]) {
-                    *reinterpret_cast<float4*>(a.Cf + fb + i0) = make_float4(cf[0], cf[1], cf[2], cf[3]);
-                    *reinterpret_cast<float4*>(a.Df + fb + i0) = make_float4(df[0], df[1], df[2], df[3]);
-                    *reinterpret_cast<uchar4*>(a.Dv + fb + i0) = make_uchar4(1, 1, 1, 1);
-                } else {
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        if (!upd[j]) continue;
-                        a.Cf[fb + i0 + j] = cf[j];
-                        a.Df[fb + i0 + j] = df[j];
-                        a.Dv[fb + i0 + j] = 1;
-                    }
-                }
+            if (i < P) {
+                cell = div_small(v[j], a.cell, inv_cell) * a.cols + div_small(u[j], a.cell, inv_cell);
+            }
+            // one atomic per (cell, slot): pixels of a cell are contiguous lanes
+            const unsigned anyg = __ballot_sync(0xffffffffu, qg);
+            const unsigned anyb = __ballot_sync(0xffffffffu, qb);
+            if (anyg | anyb) {
+                const unsigned group = __match_any_sync(0xffffffffu, cell);
+                if (anyg)
+                    group_atomic_min(group, lane, qg, keyg,
+                                     a.Cg + (long long)f * a.cell_stride + (cell < 0 ? 0 : cell));
+                if (anyb)
+                    group_atomic_min(group, lane, qb, keyb,
+                                     a.Cb + (long long)f * a.cell_stride + (cell < 0 ? 0 : cell));
             }
         }
     }
@@ -189,7 +154,7 @@ __global__ void __launch_bounds__(256) k_refine(RefineArgs a, CostTables tab) {
     tsum = __shfl_xor_sync(0xffffffffu, tsum, 2) + tsum;
     tsum = __shfl_xor_sync(0xffffffffu, tsum, 1) + tsum;
     tvalid = __reduce_add_sync(0xffffffffu, tvalid);
-    if ((threadIdx.x & 31) == 0 && (tsum | tvalid)) {
+    if (lane == 0 && (tsum | tvalid)) {
         atomicAdd(a.trace_sum + (long long)f * a.trace_stride, tsum);
         atomicAdd(a.trace_valid + (long long)f * a.trace_stride, tvalid);
     }
@@ -233,19 +198,24 @@ __global__ void k_cost_eval(const uint32_t* __restrict__ cl, const uint32_t* __r
     cost[i] = c;
 }
 
+__global__ void k_fill_f32(float* __restrict__ p, long long n, float x) {
+    const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    if (i + 3 < n && (reinterpret_cast<uintptr_t>(p + i) & 15) == 0) {
+        *reinterpret_cast<float4*>(p + i) = make_float4(x, x, x, x);
+    } else {
+        for (long long j = i; j < i + 4 && j < n; ++j) p[j] = x;
+    }
+}
+
 }  // namespace
 
 int launch_refine(const RefineArgs& a, const CostTables& tab, bool last, cudaStream_t st) {
-    const long long groups = (a.g.pixels + 3) / 4;
-    dim3 grid(unsigned((groups + 255) / 256), a.frames);
-    const bool vec = (a.g.pixels % 4) == 0;
-    if (vec) {
-        if (last) k_refine<true, true><<<grid, 256, 0, st>>>(a, tab);
-        else k_refine<true, false><<<grid, 256, 0, st>>>(a, tab);
-    } else {
-        if (last) k_refine<false, true><<<grid, 256, 0, st>>>(a, tab);
-        else k_refine<false, false><<<grid, 256, 0, st>>>(a, tab);
-    }
+    const long long chunks = (a.g.pixels + kChunk - 1) / kChunk;
+    dim3 grid(unsigned((chunks + 7) / 8), a.frames);
+    // reciprocals for the exact small-integer divisions (div_small corrects them)
+    const float inv_cell = 1.0f / float(a.cell), inv_w = 1.0f / float(a.g.width);
+    if (last) k_refine<true><<<grid, 256, 0, st>>>(a, tab, inv_cell, inv_w);
+    else k_refine<false><<<grid, 256, 0, st>>>(a, tab, inv_cell, inv_w);
     return 1;
 }
 
@@ -265,24 +235,11 @@ int launch_cost_eval(const uint32_t* cl, const uint32_t* cr, FrameGeom g, const 
     return 1;
 }
 
-}  // namespace ps
-
-namespace ps {
-namespace {
-__global__ void k_fill_f32(float* __restrict__ p, long long n, float x) {
-    const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 4;
-    if (i + 3 < n && (reinterpret_cast<uintptr_t>(p + i) & 15) == 0) {
-        *reinterpret_cast<float4*>(p + i) = make_float4(x, x, x, x);
-    } else {
-        for (long long j = i; j < i + 4 && j < n; ++j) p[j] = x;
-    }
-}
-}  // namespace
-
 int launch_fill_f32(float* p, long long n, float x, cudaStream_t st) {
     if (n <= 0) return 0;
     const long long groups = (n + 3) / 4;
     k_fill_f32<<<unsigned((groups + 255) / 256), 256, 0, st>>>(p, n, x);
     return 1;
 }
+
 }  // namespace ps

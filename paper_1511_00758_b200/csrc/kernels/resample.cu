@@ -26,8 +26,7 @@ struct ConfidentOp {
     int cells;
     int stride;
     FrameGeom g;
-    const int32_t* lookup;
-    const double* planes;
+    const float* dit;
     uint32_t* taken;
     int* su;
     int* sv;
@@ -41,8 +40,7 @@ struct ConfidentOp {
         const long long idx = (long long)(key & 0xffffffffull);
         v = int(idx / g.width);
         u = int(idx - (long long)v * g.width);
-        const int t = lookup[(long long)f * g.pixels + idx];
-        d = plane_eval(planes + 3ll * t, u, v);
+        d = dit[(long long)f * g.pixels + idx];  // the winner's D_it (valid: its cost < costLow)
         return true;
     }
     __device__ bool test(int f, int c) const {
@@ -110,11 +108,10 @@ __global__ void k_pack_new(const int* __restrict__ su, const int* __restrict__ s
 }  // namespace
 
 int launch_resample_confident(const unsigned long long* Cg, int cells_per_frame, int cell_stride,
-                              FrameGeom g, int frames, const int32_t* lookup,
-                              const double* planes, uint32_t* taken, int* su, int* sv, double* sd,
-                              int scap, const int* S_old, int* conf_count, int* chunk_buf,
-                              cudaStream_t st) {
-    ConfidentOp op{Cg, cells_per_frame, cell_stride, g, lookup, planes, taken, su, sv, sd, scap};
+                              FrameGeom g, int frames, const float* dit, uint32_t* taken, int* su,
+                              int* sv, double* sd, int scap, const int* S_old, int* conf_count,
+                              int* chunk_buf, cudaStream_t st) {
+    ConfidentOp op{Cg, cells_per_frame, cell_stride, g, dit, taken, su, sv, sd, scap};
     return run_compaction(op, frames, cells_per_frame, chunk_buf, conf_count, S_old, nullptr,
                           nullptr, st);
 }
