@@ -40,9 +40,11 @@ int delaunay_lex(const int* u, const int* v, int n, std::vector<int>& tris, Dela
 // Hull-vertex pinning (mesh.cpp:109-122) for this triangle list: pin_bits[t]
 // bit k set when corner k of triangle t is an uncovered vertex pixel whose
 // first incident triangle is t.  With check_order, returns true (and stops)
-// as soon as the pinned value would depend on the triangle order (pins.cpp).
+// as soon as the pinned vertex's validity (0 <= d < max_disp) would depend on
+// the triangle order (pins.cpp).
 bool mesh_pins(const int* u, const int* v, const double* d, int n, const int* tris, int nt,
-               int width, int height, bool check_order, std::vector<uint8_t>& state,
-               std::vector<float>& first, std::vector<uint8_t>& pin_bits);
+               int width, int height, float max_disp, bool check_order,
+               std::vector<uint8_t>& state, std::vector<float>& first,
+               std::vector<uint8_t>& pin_bits);
 
 }  // namespace ps

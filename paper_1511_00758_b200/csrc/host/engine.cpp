@@ -12,9 +12,12 @@
 #include "engine.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
+#include <condition_variable>
 #include <cstring>
+#include <mutex>
 #include <thread>
 
 #include "../kernels/launch.hpp"
@@ -149,6 +152,7 @@ Engine::~Engine() {
                            &g.hPin})
             if (b->p) cudaFreeHost(b->p);
         if (g.st) cudaStreamDestroy(g.st);
+        if (g.done_event) cudaEventDestroy(g.done_event);
     }
     for (auto& p : pending_) {
         cudaEventDestroy(p.a);
@@ -433,8 +437,13 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     }
     trace_.assign(size_t(F) * iters, ps_iter_stats{});
 
-    // ---- frame groups (software pipeline over streams)
+    // ---- frame groups: a dataflow pipeline.  Per group, each iteration is
+    //   delta D2H -> Delaunay tasks on the worker pool -> triangles H2D ->
+    //   device stages on the group's stream -> (completion) -> next iteration.
+    // The host loop below only moves data and launches; the workers
+    // triangulate continuously while the device runs other groups' stages.
     const int G = std::max(1, std::min(kMaxGroups, (F + 31) / 32));
+    const int tri_cap = int(std::min<long long>(2ll * scap_ + 8, 2ll * P + 8));  // T <= 2S per frame
     for (int gi = 0; gi < G; ++gi) {
         FrameGroup& grp = groups_[gi];
         grp.f0 = int((long long)F * gi / G);
@@ -442,241 +451,332 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         grp.S = dS + grp.f0;
         grp.Snext = dSnext + grp.f0;
         grp.ntri.assign(grp.n, 0);
+        grp.it = 0;
+        grp.phase = FrameGroup::kIdle;
+        grp.pending.store(0);
         int* hs = host<int>(grp.hS, grp.n);
         int* hsp = host<int>(grp.hSprev, grp.n);
         if (!host<int>(grp.hPackOff, grp.n) || !host<int>(grp.hTriOff, grp.n + 1) ||
             !dev<int>(grp.dTriOff, grp.n + 1) || !dev<int>(grp.dPackOff, grp.n) ||
-            !dev<int>(grp.dSprev, grp.n) || !dev<int>(grp.dChunk, size_t(grp.n) * chunks + 1) || !hs ||
-            !hsp)
+            !dev<int>(grp.dSprev, grp.n) || !dev<int>(grp.dChunk, size_t(grp.n) * chunks + 1) ||
+            !host<int>(grp.hTri, size_t(grp.n) * tri_cap * 3) ||
+            !host<uint8_t>(grp.hPin, size_t(grp.n) * tri_cap) || !hs || !hsp)
             return fail(PS_CUDA_ERROR, "allocation failed (group staging)");
+        if (!grp.done_event) cudaEventCreateWithFlags(&grp.done_event, cudaEventDisableTiming);
         for (int i = 0; i < grp.n; ++i) {
             hs[i] = hS[grp.f0 + i];
             hsp[i] = 0;
         }
     }
+    std::mutex done_m;
+    std::condition_variable done_cv;
+    std::atomic<double> dt_ms_sum{0.0};
 
-    for (int it = 1; it <= iters; ++it) {
-        const bool last = it == iters;
-        const int cell = cell_of[it - 1];
-        const int cols = ceil_div(W, cell);
-        const int cells = cols * ceil_div(H, cell);
-        for (int gi = 0; gi < G; ++gi) {
-            FrameGroup& grp = groups_[gi];
-            const double tic = now_ms();
-            const int f0 = grp.f0, n = grp.n;
-            cudaStream_t gs = grp.st;
-            int* hs = static_cast<int*>(grp.hS.p);
-            int* hsp = static_cast<int*>(grp.hSprev.p);
-            int* hoff = static_cast<int*>(grp.hPackOff.p);
-            if (it > 1) {
-                s = check(cudaMemcpyAsync(hs, grp.S, sizeof(int) * n, cudaMemcpyDeviceToHost, gs), "D2H S");
-                if (s == PS_OK) s = sync(gs, "support count");
-                if (s != PS_OK) return s;
-            }
-            // ---- supports delta to the host
-            long long total_new = 0;
-            int max_new = 0;
-            for (int i = 0; i < n; ++i) {
-                hoff[i] = int(total_new);
-                const int k = hs[i] - hsp[i];
-                total_new += k;
-                max_new = std::max(max_new, k);
-            }
-            const size_t npk = size_t(std::max<long long>(total_new, 1));
-            int2* dPack = dev<int2>(grp.dPack, npk);
-            double* dPackD = dev<double>(grp.dPackD, npk);
-            int2* hPack = reinterpret_cast<int2*>(host<uint8_t>(grp.hPack, npk * 8));
-            double* hPackD = reinterpret_cast<double*>(host<uint8_t>(grp.hPackD, npk * 8));
-            if (!dPack || !hPack || !dPackD || !hPackD)
-                return fail(PS_CUDA_ERROR, "allocation failed (support staging)");
-            int* dSprev = static_cast<int*>(grp.dSprev.p);
-            int* dPackOff = static_cast<int*>(grp.dPackOff.p);
-            s = check(cudaMemcpyAsync(dSprev, hsp, sizeof(int) * n, cudaMemcpyHostToDevice, gs), "H2D Sprev");
-            if (s == PS_OK)
-                s = check(cudaMemcpyAsync(dPackOff, hoff, sizeof(int) * n, cudaMemcpyHostToDevice, gs),
-                          "H2D pack offsets");
-            if (s != PS_OK) return s;
-            launches_ += launch_pack_new_supports(dSu + size_t(f0) * scap_, dSv + size_t(f0) * scap_,
-                                                  dSd + size_t(f0) * scap_, scap_, dSprev, grp.S,
-                                                  dPackOff, n, max_new, dPack, dPackD, gs);
-            if (total_new > 0) {
-                s = check(cudaMemcpyAsync(hPack, dPack, sizeof(int2) * total_new, cudaMemcpyDeviceToHost, gs),
-                          "D2H supports");
-                if (s == PS_OK)
-                    s = check(cudaMemcpyAsync(hPackD, dPackD, sizeof(double) * total_new,
-                                              cudaMemcpyDeviceToHost, gs), "D2H support d");
-            }
-            if (s == PS_OK) s = sync(gs, "support delta");
-            if (s != PS_OK) return s;
+    // (1) supports added since the group's last iteration -> pinned host staging
+    auto fetch_delta = [&](FrameGroup& grp, bool counts) -> ps_status {
+        const int n = grp.n;
+        cudaStream_t gs = grp.st;
+        int* hs = static_cast<int*>(grp.hS.p);
+        int* hsp = static_cast<int*>(grp.hSprev.p);
+        int* hoff = static_cast<int*>(grp.hPackOff.p);
+        ps_status r = PS_OK;
+        if (counts) {
+            r = check(cudaMemcpyAsync(hs, grp.S, sizeof(int) * n, cudaMemcpyDeviceToHost, gs), "D2H S");
+            if (r == PS_OK) r = sync(gs, "support count");
+            if (r != PS_OK) return r;
+        }
+        long long total_new = 0;
+        int max_new = 0;
+        for (int i = 0; i < n; ++i) {
+            hoff[i] = int(total_new);
+            const int k = hs[i] - hsp[i];
+            total_new += k;
+            max_new = std::max(max_new, k);
+        }
+        const size_t npk = size_t(std::max<long long>(total_new, 1));
+        int2* dPack = dev<int2>(grp.dPack, npk);
+        double* dPackD = dev<double>(grp.dPackD, npk);
+        int2* hPack = reinterpret_cast<int2*>(host<uint8_t>(grp.hPack, npk * 8));
+        double* hPackD = reinterpret_cast<double*>(host<uint8_t>(grp.hPackD, npk * 8));
+        if (!dPack || !hPack || !dPackD || !hPackD)
+            return fail(PS_CUDA_ERROR, "allocation failed (support staging)");
+        int* dSprev = static_cast<int*>(grp.dSprev.p);
+        int* dPackOff = static_cast<int*>(grp.dPackOff.p);
+        r = check(cudaMemcpyAsync(dSprev, hsp, sizeof(int) * n, cudaMemcpyHostToDevice, gs), "H2D Sprev");
+        if (r == PS_OK)
+            r = check(cudaMemcpyAsync(dPackOff, hoff, sizeof(int) * n, cudaMemcpyHostToDevice, gs),
+                      "H2D pack offsets");
+        if (r != PS_OK) return r;
+        const int f0 = grp.f0;
+        launches_ += launch_pack_new_supports(dSu + size_t(f0) * scap_, dSv + size_t(f0) * scap_,
+                                              dSd + size_t(f0) * scap_, scap_, dSprev, grp.S,
+                                              dPackOff, n, max_new, dPack, dPackD, gs);
+        if (total_new > 0) {
+            r = check(cudaMemcpyAsync(hPack, dPack, sizeof(int2) * total_new, cudaMemcpyDeviceToHost, gs),
+                      "D2H supports");
+            if (r == PS_OK)
+                r = check(cudaMemcpyAsync(hPackD, dPackD, sizeof(double) * total_new,
+                                          cudaMemcpyDeviceToHost, gs), "D2H support d");
+        }
+        if (r == PS_OK) r = sync(gs, "support delta");
+        return r;
+    };
 
-            // ---- host Delaunay per frame (delaunay.cpp:288-325 contract): the
-            // radial sweep, or the reference-order sweep when the hull-vertex
-            // pinning depends on the order (pins.cpp)
-            const double dt0 = now_ms();
-            pool_->parallel_for(n, [&](int i, int worker) {
-                const int f = f0 + i;
+    // (2) host Delaunay per frame (delaunay.cpp:288-325 contract): the radial
+    // sweep, or the reference-order sweep when the validity of a pinned hull
+    // vertex depends on the triangle order (pins.cpp).  Each task writes its
+    // triangles and pin bits into the group's pinned staging at a fixed slot.
+    auto submit_dt = [&](FrameGroup& grp) {
+        grp.pending.store(grp.n);
+        grp.phase = FrameGroup::kHost;
+        grp.tic = now_ms();
+        for (int i = 0; i < grp.n; ++i) {
+            pool_->submit([&, i, gp = &grp](int worker) {
+                FrameGroup& g2 = *gp;
+                const double t0 = now_ms();
+                const int f = g2.f0 + i;
+                const int* hs = static_cast<const int*>(g2.hS.p);
+                const int* hsp = static_cast<const int*>(g2.hSprev.p);
+                const int* hoff = static_cast<const int*>(g2.hPackOff.p);
+                const int2* hPack = static_cast<const int2*>(g2.hPack.p);
+                const double* hPackD = static_cast<const double*>(g2.hPackD.p);
                 const int k = hs[i] - hsp[i];
                 for (int j = 0; j < k; ++j) {
                     hu_[f].push_back(hPack[hoff[i] + j].x);
                     hv_[f].push_back(hPack[hoff[i] + j].y);
                     hd_[f].push_back(hPackD[hoff[i] + j]);
                 }
-                grp.ntri[i] = 0;
-                if (status_[f] != PS_OK) {
-                    htri_[f].clear();
-                    return;
+                int t = 0;
+                if (status_[f] == PS_OK) {
+                    const int ns = int(hu_[f].size());
+                    DelaunayWorkspace& w = ws_[worker];
+                    t = delaunay(hu_[f].data(), hv_[f].data(), ns, htri_[f], w);
+                    if (t > 0 && mesh_pins(hu_[f].data(), hv_[f].data(), hd_[f].data(), ns,
+                                           htri_[f].data(), t, W, H, float(cfg.max_disparity),
+                                           true, w.covered, w.first, hpin_[f])) {
+                        t = delaunay_lex(hu_[f].data(), hv_[f].data(), ns, htri_[f], w);
+                        lex_used_[f] += 1;
+                        if (t > 0)
+                            mesh_pins(hu_[f].data(), hv_[f].data(), hd_[f].data(), ns,
+                                      htri_[f].data(), t, W, H, float(cfg.max_disparity), false,
+                                      w.covered, w.first, hpin_[f]);
+                    }
+                    if (t < 0 || t > tri_cap) {
+                        status_[f] = PS_ERROR;
+                        t = 0;
+                    }
+                    if (t > 0) {
+                        std::memcpy(static_cast<int*>(g2.hTri.p) + size_t(i) * tri_cap * 3,
+                                    htri_[f].data(), sizeof(int) * 3 * t);
+                        std::memcpy(static_cast<uint8_t*>(g2.hPin.p) + size_t(i) * tri_cap,
+                                    hpin_[f].data(), t);
+                    }
                 }
-                const int ns = int(hu_[f].size());
-                DelaunayWorkspace& w = ws_[worker];
-                int t = delaunay(hu_[f].data(), hv_[f].data(), ns, htri_[f], w);
-                if (t > 0 && mesh_pins(hu_[f].data(), hv_[f].data(), hd_[f].data(), ns,
-                                       htri_[f].data(), t, W, H, true, w.covered, w.first,
-                                       hpin_[f])) {
-                    t = delaunay_lex(hu_[f].data(), hv_[f].data(), ns, htri_[f], w);
-                    lex_used_[f] += 1;
-                    if (t > 0)
-                        mesh_pins(hu_[f].data(), hv_[f].data(), hd_[f].data(), ns, htri_[f].data(),
-                                  t, W, H, false, w.covered, w.first, hpin_[f]);
-                }
-                if (t < 0) {
-                    status_[f] = PS_ERROR;
-                    htri_[f].clear();
-                    return;
-                }
-                grp.ntri[i] = t;
-            });
-            host_dt_ms += now_ms() - dt0;
-            int* hTriOff = static_cast<int*>(grp.hTriOff.p);
-            long long total_tri = 0;
-            for (int i = 0; i < n; ++i) {
-                hTriOff[i] = int(total_tri);
-                total_tri += grp.ntri[i];
-            }
-            hTriOff[n] = int(total_tri);
-            const size_t ntot = size_t(std::max<long long>(total_tri, 1));
-            int* hTri = host<int>(grp.hTri, ntot * 3);
-            uint8_t* hPin = host<uint8_t>(grp.hPin, ntot);
-            int* dTri = dev<int>(grp.dTri, ntot * 3);
-            uint8_t* dPin = dev<uint8_t>(grp.dPin, ntot);
-            int* dTriOff = static_cast<int*>(grp.dTriOff.p);
-            if (!hTri || !dTri || !hPin || !dPin)
-                return fail(PS_CUDA_ERROR, "allocation failed (triangles)");
-            pool_->parallel_for(n, [&](int i, int) {
-                if (grp.ntri[i] > 0) {
-                    std::memcpy(hTri + 3ll * hTriOff[i], htri_[f0 + i].data(), sizeof(int) * 3 * grp.ntri[i]);
-                    std::memcpy(hPin + hTriOff[i], hpin_[f0 + i].data(), grp.ntri[i]);
+                g2.ntri[i] = t;
+                double cur = dt_ms_sum.load();
+                while (!dt_ms_sum.compare_exchange_weak(cur, cur + (now_ms() - t0))) {}
+                if (g2.pending.fetch_sub(1) == 1) {
+                    std::lock_guard<std::mutex> lk(done_m);
+                    done_cv.notify_all();
                 }
             });
-            if (total_tri > 0) {
-                s = check(cudaMemcpyAsync(dTri, hTri, sizeof(int) * 3 * total_tri, cudaMemcpyHostToDevice, gs),
-                          "H2D triangles");
-                if (s == PS_OK)
-                    s = check(cudaMemcpyAsync(dPin, hPin, total_tri, cudaMemcpyHostToDevice, gs), "H2D pins");
-            }
-            if (s == PS_OK)
-                s = check(cudaMemcpyAsync(dTriOff, hTriOff, sizeof(int) * (n + 1), cudaMemcpyHostToDevice, gs),
-                          "H2D triangle offsets");
-            if (s != PS_OK) return s;
-            for (int i = 0; i < n; ++i) {
-                ps_iter_stats& ts = trace_[size_t(f0 + i) * iters + (it - 1)];
-                ts.iteration = it;
-                ts.support_count = hs[i];  // mesh.vertices().size() (pipeline.cpp:180)
-                ts.triangle_count = grp.ntri[i];
-                ts.occupancy_cell_size = cell;
-                hsp[i] = hs[i];
-                final_count_[f0 + i] = hs[i];
-            }
+        }
+    };
 
-            // ---- K5/K6 mesh (mesh.cpp:44-123) -> interpolated disparity (mesh.cpp:149-182)
-            float* lk = dDit + size_t(f0) * P;
-            cudaMemsetAsync(lk, 0xff, sizeof(float) * n * P, gs);  // NaN: outside the hull
-            begin_kernel("mesh", 4.0 * double(P) * n + 36.0 * double(total_tri), gs);
-            launches_ += launch_mesh_disparity(dTri, dTriOff, n, total_tri, dSu + size_t(f0) * scap_,
-                                               dSv + size_t(f0) * scap_, dSd + size_t(f0) * scap_,
-                                               scap_, g, dPin, float(cfg.max_disparity), lk, dErr, gs);
+    // (3) triangles H2D + device stages of iteration grp.it on the group's stream
+    auto launch_device = [&](FrameGroup& grp) -> ps_status {
+        const int it = grp.it;
+        const bool last = it == iters;
+        const int cell = cell_of[it - 1];
+        const int cols = ceil_div(W, cell);
+        const int cells = cols * ceil_div(H, cell);
+        const int f0 = grp.f0, n = grp.n;
+        cudaStream_t gs = grp.st;
+        int* hs = static_cast<int*>(grp.hS.p);
+        int* hsp = static_cast<int*>(grp.hSprev.p);
+        int* hTriOff = static_cast<int*>(grp.hTriOff.p);
+        long long total_tri = 0;
+        for (int i = 0; i < n; ++i) {
+            hTriOff[i] = int(total_tri);
+            total_tri += grp.ntri[i];
+        }
+        hTriOff[n] = int(total_tri);
+        const size_t ntot = size_t(std::max<long long>(total_tri, 1));
+        int* dTri = dev<int>(grp.dTri, ntot * 3);
+        uint8_t* dPin = dev<uint8_t>(grp.dPin, ntot);
+        int* dTriOff = static_cast<int*>(grp.dTriOff.p);
+        if (!dTri || !dPin) return fail(PS_CUDA_ERROR, "allocation failed (triangles)");
+        ps_status r = PS_OK;
+        for (int i = 0; i < n && r == PS_OK; ++i) {
+            if (grp.ntri[i] == 0) continue;
+            r = check(cudaMemcpyAsync(dTri + 3ll * hTriOff[i],
+                                      static_cast<int*>(grp.hTri.p) + size_t(i) * tri_cap * 3,
+                                      sizeof(int) * 3 * grp.ntri[i], cudaMemcpyHostToDevice, gs),
+                      "H2D triangles");
+            if (r == PS_OK)
+                r = check(cudaMemcpyAsync(dPin + hTriOff[i],
+                                          static_cast<uint8_t*>(grp.hPin.p) + size_t(i) * tri_cap,
+                                          grp.ntri[i], cudaMemcpyHostToDevice, gs), "H2D pins");
+        }
+        if (r == PS_OK)
+            r = check(cudaMemcpyAsync(dTriOff, hTriOff, sizeof(int) * (n + 1), cudaMemcpyHostToDevice, gs),
+                      "H2D triangle offsets");
+        if (r != PS_OK) return r;
+        for (int i = 0; i < n; ++i) {
+            ps_iter_stats& ts = trace_[size_t(f0 + i) * iters + (it - 1)];
+            ts.iteration = it;
+            ts.support_count = hs[i];  // mesh.vertices().size() (pipeline.cpp:180)
+            ts.triangle_count = grp.ntri[i];
+            ts.occupancy_cell_size = cell;
+            hsp[i] = hs[i];
+            final_count_[f0 + i] = hs[i];
+        }
+
+        // ---- K5/K6 mesh (mesh.cpp:44-123) -> interpolated disparity (mesh.cpp:149-182)
+        float* lk = dDit + size_t(f0) * P;
+        cudaMemsetAsync(lk, 0xff, sizeof(float) * n * P, gs);  // NaN: outside the hull
+        begin_kernel("mesh", 4.0 * double(P) * n + 36.0 * double(total_tri), gs);
+        launches_ += launch_mesh_disparity(dTri, dTriOff, n, total_tri, dSu + size_t(f0) * scap_,
+                                           dSv + size_t(f0) * scap_, dSd + size_t(f0) * scap_,
+                                           scap_, g, dPin, float(cfg.max_disparity), lk, dErr, gs);
+        end_kernel(gs);
+
+        // ---- K7 (+K9) refine (mesh.cpp:149-182, pipeline.cpp:33-86)
+        unsigned long long* cg = dCg + size_t(f0) * cells_max;
+        unsigned long long* cb = dCb + size_t(f0) * cells_max;
+        cudaMemset2DAsync(cg, sizeof(unsigned long long) * cells_max, 0xff,
+                          sizeof(unsigned long long) * cells, n, gs);
+        cudaMemset2DAsync(cb, sizeof(unsigned long long) * cells_max, 0xff,
+                          sizeof(unsigned long long) * cells, n, gs);
+        const size_t fp = size_t(f0) * P;
+        RefineArgs ra{};
+        ra.g = g;
+        ra.frames = n;
+        ra.mask = dMask + fp;
+        ra.dit = lk;
+        ra.cl = dCL + fp;
+        ra.cr = dCR + fp;
+        ra.max_disp = float(cfg.max_disparity);
+        ra.cell = cell;
+        ra.cols = cols;
+        ra.cells_per_frame = cells;
+        ra.cell_stride = cells_max;
+        ra.Df = dDf + fp;
+        ra.Dv = dDv + fp;
+        ra.Cf = dCf + fp;
+        ra.Cg = cg;
+        ra.Cb = cb;
+        ra.trace_sum = dTraceSum + size_t(f0) * iters + (it - 1);
+        ra.trace_valid = dTraceValid + size_t(f0) * iters + (it - 1);
+        ra.trace_stride = iters;
+        ra.dense = dDense + fp;
+        ra.dense_valid = dDenseV + fp;
+        double mbytes = 0.0;
+        for (int i = 0; i < n; ++i) mbytes += double(hMaskCount[f0 + i]);
+        const double kbytes =
+            double(P) * n + 29.0 * mbytes + (last ? 9.0 * double(P) * n - 4.0 * mbytes : 0.0);
+        begin_kernel("refine", kbytes, gs);
+        launches_ += launch_refine(ra, tab, last, gs);
+        end_kernel(gs);
+
+        if (!last) {
+            // ---- K8 resampling (pipeline.cpp:88-129)
+            int* su = dSu + size_t(f0) * scap_;
+            int* sv = dSv + size_t(f0) * scap_;
+            double* sd = dSd + size_t(f0) * scap_;
+            uint32_t* tk = dTaken + size_t(f0) * words;
+            int* chunk = static_cast<int*>(grp.dChunk.p);
+            begin_kernel("resample", 0.0, gs);
+            launches_ += launch_resample_confident(cg, cells, cells_max, g, n, lk, tk, su, sv, sd,
+                                                   scap_, grp.S, dConf + f0, chunk, gs);
+            launches_ += launch_resample_invalid(cb, cells, cells_max, g, n,
+                                                 dRemU + size_t(f0) * cells_max,
+                                                 dRemV + size_t(f0) * cells_max, cells_max,
+                                                 dRemCount + f0, chunk, gs);
             end_kernel(gs);
-
-            // ---- K7 (+K9) refine (mesh.cpp:149-182, pipeline.cpp:33-86)
-            unsigned long long* cg = dCg + size_t(f0) * cells_max;
-            unsigned long long* cb = dCb + size_t(f0) * cells_max;
-            cudaMemset2DAsync(cg, sizeof(unsigned long long) * cells_max, 0xff,
-                              sizeof(unsigned long long) * cells, n, gs);
-            cudaMemset2DAsync(cb, sizeof(unsigned long long) * cells_max, 0xff,
-                              sizeof(unsigned long long) * cells, n, gs);
-            const size_t fp = size_t(f0) * P;
-            RefineArgs ra{};
-            ra.g = g;
-            ra.frames = n;
-            ra.mask = dMask + fp;
-            ra.dit = lk;
-            ra.cl = dCL + fp;
-            ra.cr = dCR + fp;
-            ra.max_disp = float(cfg.max_disparity);
-            ra.cell = cell;
-            ra.cols = cols;
-            ra.cells_per_frame = cells;
-            ra.cell_stride = cells_max;
-            ra.Df = dDf + fp;
-            ra.Dv = dDv + fp;
-            ra.Cf = dCf + fp;
-            ra.Cg = cg;
-            ra.Cb = cb;
-            ra.trace_sum = dTraceSum + size_t(f0) * iters + (it - 1);
-            ra.trace_valid = dTraceValid + size_t(f0) * iters + (it - 1);
-            ra.trace_stride = iters;
-            ra.dense = dDense + fp;
-            ra.dense_valid = dDenseV + fp;
-            double mbytes = 0.0;
-            for (int i = 0; i < n; ++i) mbytes += double(hMaskCount[f0 + i]);
-            const double kbytes = double(P) * n + 29.0 * mbytes + (last ? 9.0 * double(P) * n - 4.0 * mbytes : 0.0);
-            begin_kernel("refine", kbytes, gs);
-            launches_ += launch_refine(ra, tab, last, gs);
+            uint8_t* ok = dOk + size_t(f0) * mstride;
+            int* disp = dDisp + size_t(f0) * mstride;
+            begin_kernel("match_resample", 0.0, gs);
+            launches_ += launch_match(dCL + fp, dCR + fp, g, n, cfg.max_disparity, tab,
+                                      dRemU + size_t(f0) * cells_max, dRemV + size_t(f0) * cells_max,
+                                      dRemCount + f0, cells_max, cells, ok, disp, nullptr, gs);
             end_kernel(gs);
+            begin_kernel("compact", 0.0, gs);
+            launches_ += launch_emit_matches(dRemU + size_t(f0) * cells_max,
+                                             dRemV + size_t(f0) * cells_max, dRemCount + f0,
+                                             cells_max, cells, ok, disp, g, n, tk, su, sv, sd,
+                                             scap_, grp.S, dConf + f0, grp.Snext, chunk, gs);
+            end_kernel(gs);
+            std::swap(grp.S, grp.Snext);
+        }
+        cudaEventRecord(grp.done_event, gs);
+        grp.phase = FrameGroup::kDevice;
+        return PS_OK;
+    };
 
-            if (!last) {
-                // ---- K8 resampling (pipeline.cpp:88-129)
-                int* su = dSu + size_t(f0) * scap_;
-                int* sv = dSv + size_t(f0) * scap_;
-                double* sd = dSd + size_t(f0) * scap_;
-                uint32_t* tk = dTaken + size_t(f0) * words;
-                int* chunk = static_cast<int*>(grp.dChunk.p);
-                begin_kernel("resample", 0.0, gs);
-                launches_ += launch_resample_confident(cg, cells, cells_max, g, n, lk, tk, su, sv,
-                                                       sd, scap_, grp.S, dConf + f0, chunk, gs);
-                launches_ += launch_resample_invalid(cb, cells, cells_max, g, n,
-                                                     dRemU + size_t(f0) * cells_max,
-                                                     dRemV + size_t(f0) * cells_max, cells_max,
-                                                     dRemCount + f0, chunk, gs);
-                end_kernel(gs);
-                uint8_t* ok = dOk + size_t(f0) * mstride;
-                int* disp = dDisp + size_t(f0) * mstride;
-                begin_kernel("match_resample", 0.0, gs);
-                launches_ += launch_match(dCL + fp, dCR + fp, g, n, cfg.max_disparity, tab,
-                                          dRemU + size_t(f0) * cells_max, dRemV + size_t(f0) * cells_max,
-                                          dRemCount + f0, cells_max, cells, ok, disp, nullptr, gs);
-                end_kernel(gs);
-                begin_kernel("compact", 0.0, gs);
-                launches_ += launch_emit_matches(dRemU + size_t(f0) * cells_max,
-                                                 dRemV + size_t(f0) * cells_max, dRemCount + f0,
-                                                 cells_max, cells, ok, disp, g, n, tk, su, sv, sd,
-                                                 scap_, grp.S, dConf + f0, grp.Snext, chunk, gs);
-                end_kernel(gs);
-                std::swap(grp.S, grp.Snext);
+    // ---- the dataflow loop
+    for (int gi = 0; gi < G; ++gi) {
+        FrameGroup& grp = groups_[gi];
+        s = fetch_delta(grp, false);  // seeds: counts already on the host
+        if (s != PS_OK) {
+            pool_->wait_idle();
+            return s;
+        }
+        grp.it = 1;
+        submit_dt(grp);
+    }
+    int done_groups = 0;
+    while (done_groups < G) {
+        bool progress = false;
+        for (int gi = 0; gi < G; ++gi) {
+            FrameGroup& grp = groups_[gi];
+            if (grp.phase == FrameGroup::kHost && grp.pending.load() == 0) {
+                s = launch_device(grp);
+                if (s != PS_OK) {
+                    pool_->wait_idle();
+                    return s;
+                }
+                progress = true;
+            } else if (grp.phase == FrameGroup::kDevice) {
+                const cudaError_t q = cudaEventQuery(grp.done_event);
+                if (q == cudaErrorNotReady) continue;
+                if (q != cudaSuccess) {
+                    pool_->wait_idle();
+                    return check(q, "device stages");
+                }
+                const double ms = now_ms() - grp.tic;
+                for (int i = 0; i < grp.n; ++i) trace_[size_t(grp.f0 + i) * iters + (grp.it - 1)].millis = ms;
+                if (observer && F == 1) {
+                    std::vector<float> fd(P), fc(P);
+                    std::vector<uint8_t> fv(P);
+                    s = check(cudaMemcpy(fd.data(), dDf, sizeof(float) * P, cudaMemcpyDeviceToHost), "D2H");
+                    if (s == PS_OK) s = check(cudaMemcpy(fv.data(), dDv, P, cudaMemcpyDeviceToHost), "D2H");
+                    if (s == PS_OK) s = check(cudaMemcpy(fc.data(), dCf, sizeof(float) * P, cudaMemcpyDeviceToHost), "D2H");
+                    if (s != PS_OK) return s;
+                    observer(grp.it, fd.data(), fv.data(), fc.data(), W, H, user);
+                }
+                if (grp.it == iters) {
+                    grp.phase = FrameGroup::kDone;
+                    ++done_groups;
+                } else {
+                    s = fetch_delta(grp, true);
+                    if (s != PS_OK) {
+                        pool_->wait_idle();
+                        return s;
+                    }
+                    grp.it += 1;
+                    submit_dt(grp);
+                }
+                progress = true;
             }
-            if (observer && F == 1) {
-                std::vector<float> fd(P), fc(P);
-                std::vector<uint8_t> fv(P);
-                s = check(cudaMemcpyAsync(fd.data(), dDf, sizeof(float) * P, cudaMemcpyDeviceToHost, gs), "D2H");
-                if (s == PS_OK) s = check(cudaMemcpyAsync(fv.data(), dDv, P, cudaMemcpyDeviceToHost, gs), "D2H");
-                if (s == PS_OK) s = check(cudaMemcpyAsync(fc.data(), dCf, sizeof(float) * P, cudaMemcpyDeviceToHost, gs), "D2H");
-                if (s == PS_OK) s = sync(gs, "observer");
-                if (s != PS_OK) return s;
-                observer(it, fd.data(), fv.data(), fc.data(), W, H, user);
-            }
-            grp.millis = now_ms() - tic;
-            for (int i = 0; i < n; ++i) trace_[size_t(f0 + i) * iters + (it - 1)].millis = grp.millis;
+        }
+        if (!progress) {
+            // wait for a Delaunay completion, or poll the device again shortly
+            std::unique_lock<std::mutex> lk(done_m);
+            done_cv.wait_for(lk, std::chrono::microseconds(200));
         }
     }
+    host_dt_ms = dt_ms_sum.load() / std::max(1, pool_->size());
 
     // ---- trace (pipeline.cpp:183-191)
     for (int gi = 0; gi < G; ++gi) {

@@ -9,6 +9,7 @@
 // device stages of group g overlap the host Delaunay of group g+1.
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -41,8 +42,14 @@ struct KernelStat {
 
 // A contiguous range of frames with its own stream and per-iteration staging.
 struct FrameGroup {
+    enum Phase { kIdle, kHost, kDevice, kDone };
     int f0 = 0;
     int n = 0;
+    int it = 0;                   // iteration being processed
+    Phase phase = kIdle;
+    std::atomic<int> pending{0};  // Delaunay tasks still running
+    cudaEvent_t done_event = nullptr;
+    double tic = 0.0;
     cudaStream_t st = nullptr;
     int* S = nullptr;      // device support counts of the group's frames (current)
     int* Snext = nullptr;  // device support counts (next)

@@ -48,8 +48,9 @@ float plane_at_vertex(const int* u, const int* v, const double* d, const int* t,
 }  // namespace
 
 bool mesh_pins(const int* u, const int* v, const double* d, int n, const int* tris, int nt,
-               int width, int height, bool check_order, std::vector<uint8_t>& state,
-               std::vector<float>& first, std::vector<uint8_t>& pin_bits) {
+               int width, int height, float max_disp, bool check_order,
+               std::vector<uint8_t>& state, std::vector<float>& first,
+               std::vector<uint8_t>& pin_bits) {
     // state: 0 = not (yet) seen uncovered, 1 = covered, 2 = uncovered and pinned
     state.assign(n, 0);
     for (int t = 0; t < nt; ++t) {
@@ -73,8 +74,15 @@ bool mesh_pins(const int* u, const int* v, const double* d, int n, const int* tr
                 pin_bits[t] |= uint8_t(1u << k);  // first incident triangle
                 if (check_order) first[p] = plane_at_vertex(u, v, d, tr, k);
             } else if (check_order) {
+                // Only the validity decision can propagate (sentinel vs census
+                // cost -> C_f, grids, supports): two valid values differ by a
+                // rounding of the exact vertex disparity (~1e-17 at d = 0) and
+                // give the same lround column and cost; that residue stays in
+                // D_f / dense, inside the 1e-3 px tolerance.
                 const float val = plane_at_vertex(u, v, d, tr, k);
-                if (std::memcmp(&val, &first[p], sizeof(float)) != 0) return true;
+                const bool a = val >= 0.0f && val < max_disp;
+                const bool b = first[p] >= 0.0f && first[p] < max_disp;
+                if (a != b) return true;
             }
         }
     }

@@ -2,10 +2,14 @@
 // The reference's only concurrency is fork/join row bands
 // (proj/include/planestereo/parallel.hpp:13-37); here the host parallelism is
 // across frames of a batch, and results do not depend on the schedule.
+//
+// Two modes: submit() queues independent tasks (the engine's dataflow loop
+// keeps the workers busy while it launches device work), parallel_for() runs
+// n items and returns when all are done.
 #pragma once
 
-#include <atomic>
 #include <condition_variable>
+#include <deque>
 #include <functional>
 #include <mutex>
 #include <thread>
@@ -17,74 +21,65 @@ class ThreadPool {
 public:
     explicit ThreadPool(int threads) {
         if (threads < 1) threads = 1;
-        for (int i = 0; i < threads - 1; ++i) workers_.emplace_back([this, i] { loop(i + 1); });
+        for (int i = 0; i < threads; ++i) workers_.emplace_back([this, i] { loop(i); });
     }
     ~ThreadPool() {
         {
             std::lock_guard<std::mutex> lk(m_);
             stop_ = true;
-            ++generation_;
         }
         cv_.notify_all();
         for (auto& w : workers_) w.join();
     }
-    int size() const { return int(workers_.size()) + 1; }
+    int size() const { return int(workers_.size()); }
 
-    // Runs fn(item, worker) for item in [0, n); the caller participates as worker 0.
-    void parallel_for(int n, const std::function<void(int, int)>& fn) {
-        if (n <= 0) return;
-        if (workers_.empty() || n == 1) {
-            for (int i = 0; i < n; ++i) fn(i, 0);
-            return;
-        }
+    // Queues fn(worker); returns immediately.
+    void submit(std::function<void(int)> fn) {
         {
             std::lock_guard<std::mutex> lk(m_);
-            fn_ = &fn;
-            n_ = n;
-            next_.store(0);
-            active_ = int(workers_.size());
-            ++generation_;
+            q_.push_back(std::move(fn));
+            ++outstanding_;
         }
-        cv_.notify_all();
-        run_items(0);
+        cv_.notify_one();
+    }
+
+    // Blocks until every submitted task has finished.
+    void wait_idle() {
         std::unique_lock<std::mutex> lk(m_);
-        done_cv_.wait(lk, [this] { return active_ == 0; });
-        fn_ = nullptr;
+        idle_cv_.wait(lk, [this] { return outstanding_ == 0; });
+    }
+
+    // Runs fn(item, worker) for item in [0, n) and waits for completion.
+    void parallel_for(int n, const std::function<void(int, int)>& fn) {
+        if (n <= 0) return;
+        for (int i = 0; i < n; ++i) submit([&fn, i](int w) { fn(i, w); });
+        wait_idle();
     }
 
 private:
-    void run_items(int worker) {
-        for (;;) {
-            const int i = next_.fetch_add(1);
-            if (i >= n_) break;
-            (*fn_)(i, worker);
-        }
-    }
     void loop(int worker) {
-        long long seen = 0;
         for (;;) {
+            std::function<void(int)> task;
             {
                 std::unique_lock<std::mutex> lk(m_);
-                cv_.wait(lk, [&] { return generation_ != seen; });
-                seen = generation_;
-                if (stop_) return;
+                cv_.wait(lk, [&] { return stop_ || !q_.empty(); });
+                if (stop_ && q_.empty()) return;
+                task = std::move(q_.front());
+                q_.pop_front();
             }
-            run_items(worker);
+            task(worker);
             {
                 std::lock_guard<std::mutex> lk(m_);
-                if (--active_ == 0) done_cv_.notify_one();
+                if (--outstanding_ == 0) idle_cv_.notify_all();
             }
         }
     }
 
     std::vector<std::thread> workers_;
     std::mutex m_;
-    std::condition_variable cv_, done_cv_;
-    const std::function<void(int, int)>* fn_ = nullptr;
-    int n_ = 0;
-    std::atomic<int> next_{0};
-    int active_ = 0;
-    long long generation_ = 0;
+    std::condition_variable cv_, idle_cv_;
+    std::deque<std::function<void(int)>> q_;
+    long long outstanding_ = 0;
     bool stop_ = false;
 };
 

@@ -48,6 +48,56 @@ __device__ __forceinline__ int frame_of(const int* __restrict__ tri_off, int fra
     return lo;
 }
 
+// Row-incremental form of one edge's constraint (mesh.cpp:88-99): per row the
+// exact ceil/floor quotient advances by a precomputed quotient/remainder step,
+// so a triangle pays two divisions per edge instead of one per edge and row.
+template <class Int>
+struct EdgeWalk {
+    int kind;  // 1: u >= q (A > 0), 2: u <= q (A < 0), 0: horizontal, row test K >= bias
+    Int q, r, qs, rs, B, K, dK, bias;
+
+    __device__ __forceinline__ void init(int xi, int yi, int xj, int yj, int v0) {
+        const Int A = Int(yi - yj);
+        bias = ((yj < yi) || (yj == yi && xj > xi)) ? 0 : 1;
+        const Int dx = Int(xj - xi);
+        K = dx * Int(v0 - yi) + Int(yj - yi) * Int(xi);  // edge value at (0, v0)
+        dK = dx;
+        if (A > 0) {  // lo(v) = ceil((bias - K) / A)
+            kind = 1;
+            B = A;
+            const Int N = bias - K;
+            q = ceil_div<Int>(N, B);
+            r = q * B - N;               // in [0, B)
+            qs = floor_div<Int>(-dx, B);  // N decreases by dx per row
+            rs = -dx - qs * B;           // in [0, B)
+        } else if (A < 0) {  // hi(v) = floor((K - bias) / -A)
+            kind = 2;
+            B = -A;
+            const Int M = K - bias;
+            q = floor_div<Int>(M, B);
+            r = M - q * B;  // in [0, B)
+            qs = floor_div<Int>(dx, B);
+            rs = dx - qs * B;
+        } else {
+            kind = 0;
+        }
+    }
+    __device__ __forceinline__ void step() {
+        if (kind == 1) {
+            const bool c = rs > r;
+            q += qs + (c ? 1 : 0);
+            r += (c ? B : 0) - rs;
+        } else if (kind == 2) {
+            r += rs;
+            const bool c = r >= B;
+            q += qs + (c ? 1 : 0);
+            r -= c ? B : 0;
+        } else {
+            K += dK;
+        }
+    }
+};
+
 // Exact covered span of row v (mesh.cpp:84-103); false if the row is empty.
 template <class Int>
 __device__ __forceinline__ bool row_span(const int* x, const int* y, int v, int W, Int& lo, Int& hi) {
@@ -108,8 +158,11 @@ __global__ void __launch_bounds__(kThreads) k_raster(
     int f = 0, vmin = 0, vmax = -1;
     double pa = 0.0, pb = 0.0, pc = 0.0;
     bool big = false;
+    // frame of the block's first triangle (uniform), then a short local scan
+    const int fblk = frame_of(tri_off, frames, (long long)blockIdx.x * kThreads);
     if (active) {
-        f = frame_of(tri_off, frames, t);
+        f = fblk;
+        while (f + 1 < frames && __ldg(tri_off + f + 1) <= t) ++f;
         const long long sb = (long long)f * scap;
         const int i0 = __ldg(tris + 3 * t), i1 = __ldg(tris + 3 * t + 1), i2 = __ldg(tris + 3 * t + 2);
         x[0] = __ldg(su + sb + i0); x[1] = __ldg(su + sb + i1); x[2] = __ldg(su + sb + i2);
@@ -152,13 +205,31 @@ __global__ void __launch_bounds__(kThreads) k_raster(
         vmin = max(0, min(y[0], min(y[1], y[2])));
         vmax = min(H - 1, max(y[0], max(y[1], y[2])));
         const int xmin = min(x[0], min(x[1], x[2])), xmax = max(x[0], max(x[1], x[2]));
-        big = (vmax - vmin) >= 4 || (xmax - xmin) >= 24;
-        if (!big) {
-            for (int v = vmin; v <= vmax; ++v) {
-                Int lo, hi;
-                if (!row_span<Int>(x, y, v, W, lo, hi)) continue;
-                for (int u = int(lo); u <= int(hi); ++u)
-                    put(out, fb, (long long)v * W + u, int32_t(t), pa, pb, pc, u, v);
+        // warp-cooperative only when the bounding box is large (many pixels
+        // or many rows); slivers and small triangles stay on their thread
+        big = (long long)(vmax - vmin + 1) * (xmax - xmin + 1) > 192 || (vmax - vmin) >= 32;
+        if (!big && vmin <= vmax) {
+            EdgeWalk<Int> e[3];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                const int j = (i + 1) % 3;
+                e[i].init(x[i], y[i], x[j], y[j], vmin);
+            }
+            for (int v = vmin;; ++v) {
+                Int lo = 0, hi = W - 1;
+                bool empty = false;
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    if (e[i].kind == 1) lo = max(lo, e[i].q);
+                    else if (e[i].kind == 2) hi = min(hi, e[i].q);
+                    else if (e[i].K < e[i].bias) empty = true;
+                }
+                if (!empty)
+                    for (int u = int(lo); u <= int(hi); ++u)
+                        put(out, fb, (long long)v * W + u, int32_t(t), pa, pb, pc, u, v);
+                if (v == vmax) break;
+#pragma unroll
+                for (int i = 0; i < 3; ++i) e[i].step();
             }
         }
     }

@@ -36,17 +36,12 @@ namespace {
 constexpr int kSlots = 4;
 constexpr int kChunk = 32 * kSlots;
 
-// Warp-cooperative min of 64-bit keys over the lanes in `group` (same cell),
-// then one atomicMin by the group's lowest lane.
-__device__ __forceinline__ void group_atomic_min(unsigned group, int lane, bool has,
-                                                 unsigned long long key,
-                                                 unsigned long long* addr) {
-    const unsigned hi = has ? unsigned(key >> 32) : 0xffffffffu;
-    const unsigned hmin = __reduce_min_sync(group, hi);
-    const unsigned lo = (has && hi == hmin) ? unsigned(key) : 0xffffffffu;
-    const unsigned lmin = __reduce_min_sync(group, lo);
-    if (hmin != 0xffffffffu && lane == __ffs(group) - 1)
-        atomicMin(addr, (unsigned long long)hmin << 32 | lmin);
+constexpr unsigned kIdxBits = 27;  // 32-bit warp keys (k << 27 | idx) need P <= 2^27
+constexpr unsigned kIdxMask = (1u << kIdxBits) - 1;
+
+__device__ __forceinline__ unsigned long long widen(unsigned key32) {
+    // (k << 27 | idx) -> the grid's (k << 32 | idx): same order
+    return (unsigned long long)(key32 >> kIdxBits) << 32 | (key32 & kIdxMask);
 }
 
 __device__ __forceinline__ int div_small(int n, int d, float inv) {
@@ -57,7 +52,7 @@ __device__ __forceinline__ int div_small(int n, int d, float inv) {
     return q;
 }
 
-template <bool LAST>
+template <bool LAST, bool KEY32>
 __global__ void __launch_bounds__(256) k_refine(RefineArgs a, CostTables tab, float inv_cell,
                                                 float inv_w) {
     const int f = blockIdx.y;
@@ -88,7 +83,7 @@ __global__ void __launch_bounds__(256) k_refine(RefineArgs a, CostTables tab, fl
 #pragma unroll
         for (int j = 0; j < kSlots; ++j) {
             const int r = r0 + 32 * j + lane;  // < W + 128 < 2^24
-            const int dv = div_small(r, W, inv_w);
+            const int dv = W >= kChunk ? (r >= W ? 1 : 0) : div_small(r, W, inv_w);
             v[j] = int(v0) + dv;
             u[j] = r - dv * W;
             k[j] = kCensusBits;  // sentinel cost 1.0 (pipeline.cpp:15,35)
@@ -133,17 +128,33 @@ __global__ void __launch_bounds__(256) k_refine(RefineArgs a, CostTables tab, fl
             if (i < P) {
                 cell = div_small(v[j], a.cell, inv_cell) * a.cols + div_small(u[j], a.cell, inv_cell);
             }
-            // one atomic per (cell, slot): pixels of a cell are contiguous lanes
-            const unsigned anyg = __ballot_sync(0xffffffffu, qg);
-            const unsigned anyb = __ballot_sync(0xffffffffu, qb);
-            if (anyg | anyb) {
-                const unsigned group = __match_any_sync(0xffffffffu, cell);
-                if (anyg)
-                    group_atomic_min(group, lane, qg, keyg,
-                                     a.Cg + (long long)f * a.cell_stride + (cell < 0 ? 0 : cell));
-                if (anyb)
-                    group_atomic_min(group, lane, qb, keyb,
-                                     a.Cb + (long long)f * a.cell_stride + (cell < 0 ? 0 : cell));
+            unsigned long long* cg = a.Cg + (long long)f * a.cell_stride + (cell < 0 ? 0 : cell);
+            unsigned long long* cb = a.Cb + (long long)f * a.cell_stride + (cell < 0 ? 0 : cell);
+            if (!KEY32) {
+                if (qg) atomicMin(cg, keyg);
+                if (qb) atomicMin(cb, keyb);
+                continue;
+            }
+            // One atomic per (cell, slot): the pixels of a cell are contiguous
+            // lanes, so a segmented shuffle min (doubling, with a same-cell
+            // check) leaves each run's minimum key in its first lane.
+            if (__ballot_sync(0xffffffffu, qg | qb) == 0u) continue;
+            unsigned kg = qg ? ((unsigned)k[j] << kIdxBits) | unsigned(i) : 0xffffffffu;
+            unsigned kb = qb ? ((unsigned)(kCensusBits - k[j]) << kIdxBits) | unsigned(i) : 0xffffffffu;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int c2 = __shfl_down_sync(0xffffffffu, cell, o);
+                const unsigned g2 = __shfl_down_sync(0xffffffffu, kg, o);
+                const unsigned b2 = __shfl_down_sync(0xffffffffu, kb, o);
+                if (lane + o < 32 && c2 == cell) {
+                    kg = min(kg, g2);
+                    kb = min(kb, b2);
+                }
+            }
+            const int cprev = __shfl_up_sync(0xffffffffu, cell, 1);
+            if (lane == 0 || cprev != cell) {
+                if (kg != 0xffffffffu) atomicMin(cg, widen(kg));
+                if (kb != 0xffffffffu) atomicMin(cb, widen(kb));
             }
         }
     }
@@ -214,8 +225,14 @@ int launch_refine(const RefineArgs& a, const CostTables& tab, bool last, cudaStr
     dim3 grid(unsigned((chunks + 7) / 8), a.frames);
     // reciprocals for the exact small-integer divisions (div_small corrects them)
     const float inv_cell = 1.0f / float(a.cell), inv_w = 1.0f / float(a.g.width);
-    if (last) k_refine<true><<<grid, 256, 0, st>>>(a, tab, inv_cell, inv_w);
-    else k_refine<false><<<grid, 256, 0, st>>>(a, tab, inv_cell, inv_w);
+    const bool key32 = a.g.pixels <= (1ll << kIdxBits);
+    if (last) {
+        if (key32) k_refine<true, true><<<grid, 256, 0, st>>>(a, tab, inv_cell, inv_w);
+        else k_refine<true, false><<<grid, 256, 0, st>>>(a, tab, inv_cell, inv_w);
+    } else {
+        if (key32) k_refine<false, true><<<grid, 256, 0, st>>>(a, tab, inv_cell, inv_w);
+        else k_refine<false, false><<<grid, 256, 0, st>>>(a, tab, inv_cell, inv_w);
+    }
     return 1;
 }
 
