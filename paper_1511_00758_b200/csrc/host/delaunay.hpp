@@ -37,6 +37,11 @@ int delaunay(const int* u, const int* v, int n, std::vector<int>& tris, Delaunay
 // sweep, delaunay_lex.cpp).  Slower (~4x more in-circle tests).
 int delaunay_lex(const int* u, const int* v, int n, std::vector<int>& tris, DelaunayWorkspace& ws);
 
+// True when fitPlane gives bit-identical planes for every vertex rotation of
+// every triangle (all its additions exact), i.e. the radial sweep's rotations
+// reproduce the reference's planes (pins.cpp).
+bool planes_rotation_exact(const int* u, const int* v, const double* d, const int* tris, int nt);
+
 // Hull-vertex pinning (mesh.cpp:109-122) for this triangle list: pin_bits[t]
 // bit k set when corner k of triangle t is an uncovered vertex pixel whose
 // first incident triangle is t.  With check_order, returns true (and stops)

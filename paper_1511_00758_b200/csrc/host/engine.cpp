@@ -551,9 +551,12 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                     const int ns = int(hu_[f].size());
                     DelaunayWorkspace& w = ws_[worker];
                     t = delaunay(hu_[f].data(), hv_[f].data(), ns, htri_[f], w);
-                    if (t > 0 && mesh_pins(hu_[f].data(), hv_[f].data(), hd_[f].data(), ns,
-                                           htri_[f].data(), t, W, H, float(cfg.max_disparity),
-                                           true, w.covered, w.first, hpin_[f])) {
+                    if (t > 0 &&
+                        (!planes_rotation_exact(hu_[f].data(), hv_[f].data(), hd_[f].data(),
+                                                htri_[f].data(), t) ||
+                         mesh_pins(hu_[f].data(), hv_[f].data(), hd_[f].data(), ns,
+                                   htri_[f].data(), t, W, H, float(cfg.max_disparity), true,
+                                   w.covered, w.first, hpin_[f]))) {
                         t = delaunay_lex(hu_[f].data(), hv_[f].data(), ns, htri_[f], w);
                         lex_used_[f] += 1;
                         if (t > 0)

@@ -16,6 +16,8 @@
 // the reference's: fitPlane in binary64 in source order without FMA
 // (mesh.cpp:12-26; this file is compiled with -ffp-contract=off), plane
 // evaluation ((a*u)+(b*v))+c then a binary32 rounding (mesh.hpp:19, mesh.cpp:158).
+#include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <vector>
 
@@ -46,6 +48,40 @@ float plane_at_vertex(const int* u, const int* v, const double* d, const int* t,
 }
 
 }  // namespace
+
+// fitPlane (mesh.cpp:12-26) sums three exact products in source order; the
+// sums, and with them the plane, depend on the vertex rotation only if one of
+// them rounds.  Supports carry float-representable disparities, so every
+// term is a multiple of 2^E (E = lowest mantissa bit over the non-zero d's);
+// if every sum's magnitude bound stays below 2^(E+52), all of fitPlane's
+// additions are exact and every rotation yields bit-identical planes.  Fails
+// only for meshes mixing tiny (~1e-15, d = 0 plane noise) and large
+// disparities in one triangle; those frames take the reference's own order
+// and rotation (delaunay_lex).
+bool planes_rotation_exact(const int* u, const int* v, const double* d, const int* tris, int nt) {
+    for (int t = 0; t < nt; ++t) {
+        const int* tr = tris + 3 * t;
+        int emin = 1 << 20;
+        double dmax = 0.0;
+        for (int k = 0; k < 3; ++k) {
+            const double x = d[tr[k]];
+            if (x == 0.0) continue;
+            const float fx = float(x);
+            emin = std::min(emin, std::ilogb(fx) - 23);
+            dmax = std::max(dmax, std::fabs(x));
+        }
+        if (dmax == 0.0) continue;
+        double umax = 0.0, wmax = 0.0;
+        for (int k = 0; k < 3; ++k) {
+            umax = std::max(umax, std::fabs(double(u[tr[k]])));
+            wmax = std::max(wmax, std::fabs(double(v[tr[k]])));
+        }
+        // |detA| <= 3*dmax*2*wmax, |detB| <= 3*umax*2*dmax, |detC| <= 3*dmax*2*umax*wmax
+        const double bound = 6.0 * dmax * std::max(std::max(umax, wmax), umax * wmax) + 6.0 * dmax;
+        if (bound >= std::ldexp(1.0, emin + 52)) return false;
+    }
+    return true;
+}
 
 bool mesh_pins(const int* u, const int* v, const double* d, int n, const int* tris, int nt,
                int width, int height, float max_disp, bool check_order,
