@@ -403,9 +403,7 @@ ps_status ps_mesh_build(ps_ctx* ctx, const int* u, const int* v, const double* d
     cudaMemsetAsync(d_err, 0, sizeof(int), st);
     // hull-vertex pins in the caller's triangle order (mesh.cpp:109-122)
     std::vector<uint8_t> state, pins;
-    std::vector<float> first;
-    if (nt > 0)
-        ps::mesh_pins(u, v, d, n_points, tris, nt, width, height, 0.0f, false, state, first, pins);
+    if (nt > 0) ps::mesh_pins(u, v, n_points, tris, nt, width, height, state, pins);
     uint8_t* d_pin = e.dev<uint8_t>(e.s_i, std::max(1, nt));
     if (!d_pin) return set_error(PS_CUDA_ERROR, "allocation failed");
     if (nt > 0) cudaMemcpyAsync(d_pin, pins.data(), nt, cudaMemcpyHostToDevice, st);

@@ -34,22 +34,15 @@ struct DelaunayWorkspace {
 int delaunay(const int* u, const int* v, int n, std::vector<int>& tris, DelaunayWorkspace& ws);
 
 // Same set, in the reference's own triangle order and rotation (lexicographic
-// sweep, delaunay_lex.cpp).  Slower (~4x more in-circle tests).
+// sweep, delaunay_lex.cpp): ~4x more in-circle tests than the radial sweep,
+// but cache-friendly, so only ~15% slower; the engine uses it because the
+// order decides hull-vertex pins and the rotation decides fitPlane rounding.
 int delaunay_lex(const int* u, const int* v, int n, std::vector<int>& tris, DelaunayWorkspace& ws);
-
-// True when fitPlane gives bit-identical planes for every vertex rotation of
-// every triangle (all its additions exact), i.e. the radial sweep's rotations
-// reproduce the reference's planes (pins.cpp).
-bool planes_rotation_exact(const int* u, const int* v, const double* d, const int* tris, int nt);
 
 // Hull-vertex pinning (mesh.cpp:109-122) for this triangle list: pin_bits[t]
 // bit k set when corner k of triangle t is an uncovered vertex pixel whose
-// first incident triangle is t.  With check_order, returns true (and stops)
-// as soon as the pinned vertex's validity (0 <= d < max_disp) would depend on
-// the triangle order (pins.cpp).
-bool mesh_pins(const int* u, const int* v, const double* d, int n, const int* tris, int nt,
-               int width, int height, float max_disp, bool check_order,
-               std::vector<uint8_t>& state, std::vector<float>& first,
-               std::vector<uint8_t>& pin_bits);
+// first incident triangle is t (pins.cpp).
+void mesh_pins(const int* u, const int* v, int n, const int* tris, int nt, int width, int height,
+               std::vector<uint8_t>& state, std::vector<uint8_t>& pin_bits);
 
 }  // namespace ps

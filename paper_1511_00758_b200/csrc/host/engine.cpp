@@ -422,7 +422,6 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
 
     status_.assign(F, PS_OK);
     final_count_.assign(F, 0);
-    lex_used_.assign(F, 0);
     double host_dt_ms = 0.0;
     hu_.resize(F);
     hv_.resize(F);
@@ -550,20 +549,12 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                 if (status_[f] == PS_OK) {
                     const int ns = int(hu_[f].size());
                     DelaunayWorkspace& w = ws_[worker];
-                    t = delaunay(hu_[f].data(), hv_[f].data(), ns, htri_[f], w);
-                    if (t > 0 &&
-                        (!planes_rotation_exact(hu_[f].data(), hv_[f].data(), hd_[f].data(),
-                                                htri_[f].data(), t) ||
-                         mesh_pins(hu_[f].data(), hv_[f].data(), hd_[f].data(), ns,
-                                   htri_[f].data(), t, W, H, float(cfg.max_disparity), true,
-                                   w.covered, w.first, hpin_[f]))) {
-                        t = delaunay_lex(hu_[f].data(), hv_[f].data(), ns, htri_[f], w);
-                        lex_used_[f] += 1;
-                        if (t > 0)
-                            mesh_pins(hu_[f].data(), hv_[f].data(), hd_[f].data(), ns,
-                                      htri_[f].data(), t, W, H, float(cfg.max_disparity), false,
-                                      w.covered, w.first, hpin_[f]);
-                    }
+                    // the reference's triangle order and rotation: pins and
+                    // fitPlane rounding then match it bit for bit
+                    t = delaunay_lex(hu_[f].data(), hv_[f].data(), ns, htri_[f], w);
+                    if (t > 0)
+                        mesh_pins(hu_[f].data(), hv_[f].data(), ns, htri_[f].data(), t, W, H,
+                                  w.covered, hpin_[f]);
                     if (t < 0 || t > tri_cap) {
                         status_[f] = PS_ERROR;
                         t = 0;
@@ -803,11 +794,9 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
             stats_.push_back({name, 0, 0.0, 0.0});
             return stats_.back();
         };
-        KernelStat& dt = stat("host_delaunay");
+        KernelStat& dt = stat("host_delaunay");  // ms = per-worker share of the work
         dt.launches += F * iters;
         dt.ms += host_dt_ms;
-        KernelStat& lx = stat("host_lex_fallback");
-        for (int f = 0; f < F; ++f) lx.launches += lex_used_[f];
     }
     if (herr) return fail(PS_DEGENERATE_TRIANGLE, "collinear vertices in a triangle");
     for (int f = 0; f < F; ++f) {

@@ -145,7 +145,6 @@ private:
     std::vector<std::vector<double>> hd_;
     std::vector<std::vector<uint8_t>> hpin_;
     std::vector<int> status_, final_count_;
-    std::vector<int> lex_used_;  // frames x iterations that needed the reference-order sweep
     std::vector<ps_iter_stats> trace_;
 };
 
