@@ -1,0 +1,4 @@
+// census.hpp — drop-in name for the reference header proj/include/planestereo/census.hpp;
+// the whole API is declared in planestereo.hpp.
+#pragma once
+#include "planestereo/planestereo.hpp"

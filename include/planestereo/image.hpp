@@ -1,0 +1,4 @@
+// image.hpp — drop-in name for the reference header proj/include/planestereo/image.hpp;
+// the whole API is declared in planestereo.hpp.
+#pragma once
+#include "planestereo/planestereo.hpp"

@@ -1,0 +1,4 @@
+// mesh.hpp — drop-in name for the reference header proj/include/planestereo/mesh.hpp;
+// the whole API is declared in planestereo.hpp.
+#pragma once
+#include "planestereo/planestereo.hpp"

@@ -469,16 +469,108 @@ ps_status ps_cost_evaluation(ps_ctx* ctx, const uint32_t* census_left, const uin
     return from_engine(ctx, e.sync("cost evaluation"));
 }
 
-ps_status ps_refinement(ps_ctx*, const float*, const uint8_t*, const float*, float*, uint8_t*,
-                        float*, const uint8_t*, int, int, int, const ps_config*, ps_cell*,
-                        ps_cell*) {
-    return set_error(PS_ERROR, "ps_refinement: stage entry point not built in this round");
+ps_status ps_refinement(ps_ctx* ctx, const float* interp, const uint8_t* interp_valid,
+                        const float* cost, float* final_disparity, uint8_t* final_valid,
+                        float* final_cost, const uint8_t* mask, int width, int height,
+                        int cell_size, const ps_config* cfg, ps_cell* confident,
+                        ps_cell* invalid) {
+    PS_REQUIRE_CTX(ctx);
+    if (!cfg || cell_size < 1) return set_error(PS_ERROR, "bad refinement arguments");
+    static_assert(sizeof(ps_cell) == sizeof(ps::StageCell), "ps_cell layout");
+    ps::Engine& e = *ctx->engine;
+    const long long P = (long long)width * height;
+    const int cells = ((width + cell_size - 1) / cell_size) * ((height + cell_size - 1) / cell_size);
+    float* d_iv = e.dev<float>(e.s_a, P);
+    uint8_t* d_ok = e.dev<uint8_t>(e.s_b, P);
+    float* d_c = e.dev<float>(e.s_c, P);
+    uint8_t* d_m = e.dev<uint8_t>(e.s_d, P);
+    float* d_fd = e.dev<float>(e.s_e, P);
+    uint8_t* d_fv = e.dev<uint8_t>(e.s_f, P);
+    float* d_fc = e.dev<float>(e.s_g, P);
+    unsigned long long* d_k = e.dev<unsigned long long>(e.s_h, 2 * size_t(cells));
+    ps::StageCell* d_cells = reinterpret_cast<ps::StageCell*>(
+        e.dev<uint8_t>(e.s_i, 2 * size_t(cells) * sizeof(ps::StageCell)));
+    if (!d_iv || !d_ok || !d_c || !d_m || !d_fd || !d_fv || !d_fc || !d_k || !d_cells)
+        return set_error(PS_CUDA_ERROR, "allocation failed");
+    cudaStream_t st = e.stream();
+    cudaMemcpyAsync(d_iv, interp, 4 * P, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_ok, interp_valid, P, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_c, cost, 4 * P, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_m, mask, P, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_fd, final_disparity, 4 * P, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_fv, final_valid, P, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_fc, final_cost, 4 * P, cudaMemcpyHostToDevice, st);
+    e.count_launches(ps::launch_stage_refine({width, height, P}, d_iv, d_ok, d_c, d_m, d_fd, d_fv,
+                                             d_fc, cell_size, cfg->cost_low, cfg->cost_high, d_k,
+                                             d_k + cells, d_cells, d_cells + cells, st));
+    cudaMemcpyAsync(final_disparity, d_fd, 4 * P, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(final_valid, d_fv, P, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(final_cost, d_fc, 4 * P, cudaMemcpyDeviceToHost, st);
+    if (confident)
+        cudaMemcpyAsync(confident, d_cells, sizeof(ps_cell) * cells, cudaMemcpyDeviceToHost, st);
+    if (invalid)
+        cudaMemcpyAsync(invalid, d_cells + cells, sizeof(ps_cell) * cells, cudaMemcpyDeviceToHost, st);
+    return from_engine(ctx, e.sync("refinement"));
 }
 
-ps_status ps_support_resampling(ps_ctx*, const ps_cell*, const ps_cell*, int, const int*,
-                                const int*, const double*, int, const uint32_t*, const uint32_t*,
-                                int, int, const ps_config*, int*, int*, double*, int, int*) {
-    return set_error(PS_ERROR, "ps_support_resampling: stage entry point not built in this round");
+ps_status ps_support_resampling(ps_ctx* ctx, const ps_cell* confident, const ps_cell* invalid,
+                                int cell_size, const int* sup_u, const int* sup_v,
+                                const double* sup_d, int n_supports,
+                                const uint32_t* census_left, const uint32_t* census_right,
+                                int width, int height, const ps_config* cfg, int* u, int* v,
+                                double* d, int capacity, int* count) {
+    PS_REQUIRE_CTX(ctx);
+    if (!cfg || cell_size < 1) return set_error(PS_ERROR, "bad resampling arguments");
+    // supportResampling (pipeline.cpp:88-129): ordered list assembly with the
+    // reference's taken-set semantics; the epipolar re-match of the invalid
+    // cells runs on the device (ps_match_epipolar).
+    const int cells = ((width + cell_size - 1) / cell_size) * ((height + cell_size - 1) / cell_size);
+    const long long w = width;
+    std::unordered_map<long long, char> taken;
+    taken.reserve(size_t(n_supports) * 2 + 16);
+    std::vector<int> ou(sup_u, sup_u + n_supports), ov(sup_v, sup_v + n_supports);
+    std::vector<double> od(sup_d, sup_d + n_supports);
+    for (int i = 0; i < n_supports; ++i) taken.emplace((long long)sup_v[i] * w + sup_u[i], 1);
+    for (int c = 0; c < cells; ++c) {
+        const ps_cell& cell = confident[c];
+        if (!cell.occupied) continue;
+        const float diff = float(cell.u) - cell.disparity;  // binary32, pipeline.cpp:105
+        if (diff < 2.0f) continue;
+        if (taken.emplace((long long)cell.v * w + cell.u, 1).second) {
+            ou.push_back(cell.u);
+            ov.push_back(cell.v);
+            od.push_back(double(cell.disparity));
+        }
+    }
+    std::vector<int> ru, rv;
+    for (int c = 0; c < cells; ++c) {
+        if (!invalid[c].occupied) continue;
+        ru.push_back(invalid[c].u);
+        rv.push_back(invalid[c].v);
+    }
+    std::vector<int> mu(ru.size() + 1), mv(ru.size() + 1);
+    std::vector<double> md(ru.size() + 1);
+    int nm = 0;
+    const ps_status s = ps_match_epipolar(ctx, census_left, census_right, width, height, ru.data(),
+                                          rv.data(), int(ru.size()), cfg, mu.data(), mv.data(),
+                                          md.data(), int(ru.size()) + 1, &nm);
+    if (s != PS_OK) return s;
+    for (int i = 0; i < nm; ++i) {
+        if (taken.emplace((long long)mv[i] * w + mu[i], 1).second) {
+            ou.push_back(mu[i]);
+            ov.push_back(mv[i]);
+            od.push_back(md[i]);
+        }
+    }
+    const int m = int(ou.size());
+    if (count) *count = m;
+    for (int i = 0; i < m && i < capacity; ++i) {
+        if (u) u[i] = ou[i];
+        if (v) v[i] = ov[i];
+        if (d) d[i] = od[i];
+    }
+    if (m > capacity) return set_error(PS_CAPACITY, "support buffer too small");
+    return PS_OK;
 }
 
 }  // extern "C"

@@ -121,4 +121,20 @@ int launch_cost_eval(const uint32_t* cl, const uint32_t* cr, FrameGeom g, const 
 
 namespace ps {
 int launch_fill_f32(float* p, long long n, float x, cudaStream_t st);
+
+// Layout of ps_cell / planestereo::OccupancyCell marshalling (pipeline.hpp:17-23).
+struct StageCell {
+    int u;
+    int v;
+    float disparity;
+    float cost;
+    int occupied;
+};
+// disparityRefinement over user maps (stage.cu): final state in place, both
+// grids (ceil(W/cell) x ceil(H/cell) cells) written to out_conf / out_inv.
+int launch_stage_refine(FrameGeom g, const float* interp, const uint8_t* interp_valid,
+                        const float* cost, const uint8_t* mask, float* fd, uint8_t* fv, float* fc,
+                        int cell, float cost_low, float cost_high, unsigned long long* kg,
+                        unsigned long long* kb, StageCell* out_conf, StageCell* out_inv,
+                        cudaStream_t st);
 }  // namespace ps
