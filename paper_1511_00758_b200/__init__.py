@@ -347,6 +347,49 @@ class Context:
                                         C.c_float(max_disparity), _ptr(val), _ptr(ok)))
         return val, ok
 
+    def refinement(self, interp, interp_valid, cost, final_disparity, final_valid, final_cost,
+                   mask, cell_size: int, config: PipelineConfig):
+        """disparityRefinement: updates the final_* arrays in place, returns the
+        (confident, invalid) grids as structured arrays (u, v, disparity, cost, occupied)."""
+        h, w = np.asarray(interp).shape
+        cells = (-(-w // cell_size)) * (-(-h // cell_size))
+        dt = np.dtype([("u", np.int32), ("v", np.int32), ("disparity", np.float32),
+                       ("cost", np.float32), ("occupied", np.int32)])
+        conf = np.zeros(cells, dt)
+        inv = np.zeros(cells, dt)
+        cfg = config.to_c()
+        for a, t in ((final_disparity, np.float32), (final_valid, np.uint8), (final_cost, np.float32)):
+            if not (isinstance(a, np.ndarray) and a.dtype == t and a.flags.c_contiguous):
+                raise Error("final_* must be C-contiguous arrays of the reference types")
+        _check(self._lib.ps_refinement(
+            self._h, _ptr(np.ascontiguousarray(interp, np.float32)),
+            _ptr(np.ascontiguousarray(interp_valid, np.uint8)),
+            _ptr(np.ascontiguousarray(cost, np.float32)), _ptr(final_disparity), _ptr(final_valid),
+            _ptr(final_cost), _ptr(np.ascontiguousarray(mask, np.uint8)), w, h, cell_size,
+            C.byref(cfg), _ptr(conf), _ptr(inv)))
+        return conf, inv
+
+    def support_resampling(self, confident, invalid, cell_size: int, sup_u, sup_v, sup_d,
+                           census_left, census_right, config: PipelineConfig):
+        """supportResampling over structured cell arrays (as returned by refinement)."""
+        cl = np.ascontiguousarray(census_left, np.uint32)
+        h, w = cl.shape
+        su = np.ascontiguousarray(sup_u, np.int32)
+        sv = np.ascontiguousarray(sup_v, np.int32)
+        sd = np.ascontiguousarray(sup_d, np.float64)
+        cap = len(su) + 2 * len(confident) + 1
+        u = np.zeros(cap, np.int32)
+        v = np.zeros(cap, np.int32)
+        d = np.zeros(cap, np.float64)
+        n = C.c_int()
+        cfg = config.to_c()
+        _check(self._lib.ps_support_resampling(
+            self._h, _ptr(np.ascontiguousarray(confident)), _ptr(np.ascontiguousarray(invalid)),
+            cell_size, _ptr(su), _ptr(sv), _ptr(sd), len(su), _ptr(cl),
+            _ptr(np.ascontiguousarray(census_right, np.uint32)), w, h, C.byref(cfg), _ptr(u),
+            _ptr(v), _ptr(d), cap, C.byref(n)))
+        return u[:n.value], v[:n.value], d[:n.value]
+
     def cost_evaluation(self, census_left, census_right, interp, interp_valid, mask):
         cl = np.ascontiguousarray(census_left, dtype=np.uint32)
         cr = np.ascontiguousarray(census_right, dtype=np.uint32)

@@ -223,3 +223,35 @@ def test_cost_evaluation_equals_oracle(ctx, orc):
     ok = (rng.random((150, 200)) < 0.9).astype(np.uint8)
     val = np.where(ok == 1, val, np.float32(0))
     assert np.array_equal(ctx.cost_evaluation(cl, cr, val, ok, m), orc.cost_evaluation(cl, cr, val, ok, m))
+
+
+# ------------------------------------------------------------- refinement / resampling stages
+def test_refinement_and_resampling_equal_oracle(ctx, orc):
+    rng = np.random.default_rng(8)
+    w, h = 90, 70
+    img = rng.integers(0, 256, (h, w), dtype=np.uint8)
+    img2 = rng.integers(0, 256, (h, w), dtype=np.uint8)
+    cfg = ps.PipelineConfig()
+    mask = (rng.random((h, w)) < 0.7).astype(np.uint8)
+    ok = (rng.random((h, w)) < 0.9).astype(np.uint8)
+    val = np.where(ok == 1, (rng.random((h, w)) * 30).astype(np.float32), np.float32(0))
+    # arbitrary float costs (not only k/24), including exact ties
+    cost = rng.choice(np.array([0.0, 0.05, 0.1, 0.1, 0.25, 0.3, 0.5, 0.8, 0.9, 1.0], np.float32),
+                      size=(h, w)).astype(np.float32)
+    cl, cr = orc.census(img), orc.census(img2)
+    for cell in (1, 3, 8, 32):
+        fd1 = np.zeros((h, w), np.float32); fv1 = np.zeros((h, w), np.uint8)
+        fc1 = np.full((h, w), 0.5, np.float32)
+        fd2, fv2, fc2 = fd1.copy(), fv1.copy(), fc1.copy()
+        g1 = ctx.refinement(val, ok, cost, fd1, fv1, fc1, mask, cell, cfg)
+        g2 = orc.refinement(val, ok, cost, fd2, fv2, fc2, mask, cell, cfg)
+        assert np.array_equal(fd1, fd2) and np.array_equal(fv1, fv2) and np.array_equal(fc1, fc2)
+        for a, b in zip(g1, g2):
+            assert a.tobytes() == b.tobytes(), cell
+        su = rng.integers(2, w - 2, 20).astype(np.int32)
+        sv = rng.integers(2, h - 2, 20).astype(np.int32)
+        sd = rng.integers(0, 20, 20).astype(np.float64)
+        a = ctx.support_resampling(g1[0], g1[1], cell, su, sv, sd, cl, cr, cfg)
+        b = orc.support_resampling(g2[0], g2[1], cell, su, sv, sd, cl, cr, cfg)
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y), cell
