@@ -131,6 +131,17 @@ def cpu_checker():
     return oracle.load_oracle(), "port"
 
 
+def rank_seed(rank: int, frames: int) -> int:
+    """First generator seed of a rank's batch: ranks get disjoint frame sets
+    (frames never interact, so sharding needs no collective)."""
+    return 1000 + rank * frames
+
+
+def whole_job_value(frames_per_rank: int, world: int, steps: int, max_ms: float) -> float:
+    """Aggregate frames/s over all ranks from the slowest rank's time."""
+    return frames_per_rank * world * steps / (max_ms / 1e3)
+
+
 def make_inputs(ps, cfgd, frames, seed, pinned):
     import numpy as np
 
@@ -216,7 +227,7 @@ def run_ours(args, rank, world, local_rank):
     frames = args.frames or cfgd["frames"]
     H, W = cfgd["height"], cfgd["width"]
     P = W * H
-    L, R, keep = make_inputs(ps, cfgd, frames, 1000 + rank * frames, pinned=True)
+    L, R, keep = make_inputs(ps, cfgd, frames, rank_seed(rank, frames), pinned=True)
     ctx = ps.Context(local_rank)
     stream = torch.cuda.ExternalStream(ctx.stream_handle())
     lib = ps._native.load()
@@ -250,7 +261,7 @@ def run_ours(args, rank, world, local_rank):
     ctx.set_profiling(False)
     status = np.zeros(frames, np.int32)
     lib.ps_download_batch(ctx._h, None, None, None, None, None, None, status.ctypes.data_as(C.c_void_p))
-    value = frames * world * args.steps / (ms / 1e3)
+    value = whole_job_value(frames, world, args.steps, ms)
 
     # ---------------- e2e: public C-ABI call with host buffers (pinned), copies inside
     outs = [torch.empty(frames * P * 4, dtype=torch.uint8, pin_memory=True),
@@ -278,7 +289,7 @@ def run_ours(args, rank, world, local_rank):
     f1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = max_over_ranks(f0.elapsed_time(f1))
-    e2e_value = frames * world * args.steps / (e2e_ms / 1e3)
+    e2e_value = whole_job_value(frames, world, args.steps, e2e_ms)
     h2d = 2 * frames * P
     d2h = frames * P * (4 + 1 + 4 + 4 + 1) + frames * cfg.iterations * C.sizeof(ps._native.PsIterStats)
 
