@@ -171,6 +171,210 @@ __global__ void __launch_bounds__(256) k_refine(RefineArgs a, CostTables tab, fl
     }
 }
 
+// ---------------------------------------------------------------------------
+// Bulk-copy (TMA 1-D) variant: a persistent CTA streams 2048-pixel tiles of
+// mask / D_it / cL / C_f into a 3-stage shared-memory ring with
+// cp.async.bulk + mbarrier complete_tx (one elected thread issues, all wait),
+// so the next two tiles are in flight while the current one is processed and
+// its cR gathers are outstanding.  Same per-pixel logic and cell reduction
+// as k_refine.  Needs 16-B aligned tiles: P % 16 == 0.
+constexpr int kTile = 2048;          // 8 warps x 8 slots x 32 lanes
+constexpr int kTileSlots = 8;
+constexpr int kStages = 3;
+constexpr int kStageBytes = kTile * (1 + 4 + 4 + 4);
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+        :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void bar_wait(unsigned long long* bar, unsigned phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" :: "r"(smem_u32(bar)), "r"(phase) : "memory");
+}
+
+template <bool LAST, bool KEY32>
+__global__ void __launch_bounds__(256) k_refine_bulk(RefineArgs a, CostTables tab, float inv_cell,
+                                                     float inv_w, int tiles_per_frame,
+                                                     long long total_tiles) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) unsigned long long bars[kStages];
+    const long long P = a.g.pixels;
+    const int W = a.g.width;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    auto stage_ptr = [&](int s) { return smem + s * kStageBytes; };
+
+    auto issue = [&](long long tile, int s) {
+        const int f = int(tile / tiles_per_frame);
+        const long long off = (tile - (long long)f * tiles_per_frame) * kTile;
+        const unsigned n = unsigned(min((long long)kTile, P - off));
+        const long long base = (long long)f * P + off;
+        unsigned char* st = stage_ptr(s);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n"
+                     :: "r"(smem_u32(&bars[s])), "r"(n * 13u) : "memory");
+        bulk_g2s(st, a.mask + base, n, &bars[s]);
+        bulk_g2s(st + kTile, a.dit + base, 4 * n, &bars[s]);
+        bulk_g2s(st + 5 * kTile, a.cl + base, 4 * n, &bars[s]);
+        bulk_g2s(st + 9 * kTile, a.Cf + base, 4 * n, &bars[s]);
+    };
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" :: "r"(smem_u32(&bars[s])));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        for (int s = 0; s < kStages; ++s) {
+            const long long tile = blockIdx.x + (long long)s * gridDim.x;
+            if (tile < total_tiles) issue(tile, s);
+        }
+    }
+    __syncthreads();
+
+    unsigned long long tsum = 0;
+    unsigned tvalid = 0;
+    int cur_f = -1;
+    int j = 0;
+    for (long long tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++j) {
+        const int s = j % kStages;
+        bar_wait(&bars[s], unsigned((j / kStages) & 1));
+        const int f = int(tile / tiles_per_frame);
+        if (f != cur_f) {  // frame change: flush the trace partials of the previous frame
+            if (cur_f >= 0) {
+                unsigned long long ts = tsum;
+                ts = __shfl_xor_sync(0xffffffffu, ts, 16) + ts;
+                ts = __shfl_xor_sync(0xffffffffu, ts, 8) + ts;
+                ts = __shfl_xor_sync(0xffffffffu, ts, 4) + ts;
+                ts = __shfl_xor_sync(0xffffffffu, ts, 2) + ts;
+                ts = __shfl_xor_sync(0xffffffffu, ts, 1) + ts;
+                const unsigned tv = __reduce_add_sync(0xffffffffu, tvalid);
+                if (lane == 0 && (ts | tv)) {
+                    atomicAdd(a.trace_sum + (long long)cur_f * a.trace_stride, ts);
+                    atomicAdd(a.trace_valid + (long long)cur_f * a.trace_stride, tv);
+                }
+            }
+            cur_f = f;
+            tsum = 0;
+            tvalid = 0;
+        }
+        const long long off = (tile - (long long)f * tiles_per_frame) * kTile;
+        const long long fb = (long long)f * P;
+        const unsigned char* st = stage_ptr(s);
+        const uint8_t* sm_mask = st;
+        const float* sm_dit = reinterpret_cast<const float*>(st + kTile);
+        const uint32_t* sm_cl = reinterpret_cast<const uint32_t*>(st + 5 * kTile);
+        const float* sm_cf = reinterpret_cast<const float*>(st + 9 * kTile);
+        const long long v0 = off / W;
+        const int r0 = int(off - v0 * W);
+        int u[kTileSlots], v[kTileSlots], k[kTileSlots];
+        uint32_t crv[kTileSlots];
+#pragma unroll
+        for (int q = 0; q < kTileSlots; ++q) {
+            const int p = warp * 256 + q * 32 + lane;
+            const int r = r0 + p;
+            const int dv = div_small(r, W, inv_w);
+            v[q] = int(v0) + dv;
+            u[q] = r - dv * W;
+            k[q] = kCensusBits;
+            crv[q] = 0;
+            if (off + p < P && sm_mask[p]) {
+                const float d = sm_dit[p];
+                if (d == d) {
+                    const int dr = lround_away(d);
+                    const int ur = u[q] - dr;
+                    if (dr >= 0 && ur >= 2) {
+                        k[q] = 0;
+                        crv[q] = __ldg(a.cr + fb + (long long)v[q] * W + ur);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < kTileSlots; ++q) {
+            const int p = warp * 256 + q * 32 + lane;
+            const long long i = off + p;
+            const bool in = i < P;
+            const uint8_t m = in ? sm_mask[p] : 0;
+            const float d = in ? sm_dit[p] : __int_as_float(0x7fffffff);
+            const bool valid = d == d;
+            if (LAST && in) {
+                a.dense[fb + i] = valid ? d : 0.0f;
+                a.dense_valid[fb + i] = valid ? 1 : 0;
+            }
+            if (k[q] == 0) k[q] = __popc(sm_cl[p] ^ crv[q]);
+            bool qg = false, qb = false;
+            int cell = -1;
+            if (m) {
+                float cf = sm_cf[p];
+                const float c = tab.cost[k[q]];
+                if (c < cf) {  // pipeline.cpp:68-71
+                    cf = c;
+                    a.Cf[fb + i] = c;
+                    a.Df[fb + i] = d;
+                    a.Dv[fb + i] = 1;
+                }
+                qg = (tab.low_mask >> k[q]) & 1u;
+                qb = !qg && ((tab.high_mask >> k[q]) & 1u);
+                tsum += __double2ull_rn(__dmul_rn(double(cf), 68719476736.0));  // * 2^36
+                tvalid += cf < tab.cost_high ? 1u : 0u;
+            }
+            if (in) cell = div_small(v[q], a.cell, inv_cell) * a.cols + div_small(u[q], a.cell, inv_cell);
+            unsigned long long* cg = a.Cg + (long long)f * a.cell_stride + (cell < 0 ? 0 : cell);
+            unsigned long long* cb = a.Cb + (long long)f * a.cell_stride + (cell < 0 ? 0 : cell);
+            if (!KEY32) {
+                if (qg) atomicMin(cg, (unsigned long long)k[q] << 32 | (unsigned long long)i);
+                if (qb) atomicMin(cb, (unsigned long long)(kCensusBits - k[q]) << 32 | (unsigned long long)i);
+                continue;
+            }
+            if (__ballot_sync(0xffffffffu, qg | qb) == 0u) continue;
+            unsigned kg = qg ? ((unsigned)k[q] << kIdxBits) | unsigned(i) : 0xffffffffu;
+            unsigned kb = qb ? ((unsigned)(kCensusBits - k[q]) << kIdxBits) | unsigned(i) : 0xffffffffu;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int c2 = __shfl_down_sync(0xffffffffu, cell, o);
+                const unsigned g2 = __shfl_down_sync(0xffffffffu, kg, o);
+                const unsigned b2 = __shfl_down_sync(0xffffffffu, kb, o);
+                if (lane + o < 32 && c2 == cell) {
+                    kg = min(kg, g2);
+                    kb = min(kb, b2);
+                }
+            }
+            const int cprev = __shfl_up_sync(0xffffffffu, cell, 1);
+            if (lane == 0 || cprev != cell) {
+                if (kg != 0xffffffffu) atomicMin(cg, widen(kg));
+                if (kb != 0xffffffffu) atomicMin(cb, widen(kb));
+            }
+        }
+        __syncthreads();  // every thread is done with stage s
+        if (threadIdx.x == 0) {
+            const long long next = tile + (long long)kStages * gridDim.x;
+            if (next < total_tiles) issue(next, s);
+        }
+    }
+    if (cur_f >= 0) {
+        tsum = __shfl_xor_sync(0xffffffffu, tsum, 16) + tsum;
+        tsum = __shfl_xor_sync(0xffffffffu, tsum, 8) + tsum;
+        tsum = __shfl_xor_sync(0xffffffffu, tsum, 4) + tsum;
+        tsum = __shfl_xor_sync(0xffffffffu, tsum, 2) + tsum;
+        tsum = __shfl_xor_sync(0xffffffffu, tsum, 1) + tsum;
+        tvalid = __reduce_add_sync(0xffffffffu, tvalid);
+        if (lane == 0 && (tsum | tvalid)) {
+            atomicAdd(a.trace_sum + (long long)cur_f * a.trace_stride, tsum);
+            atomicAdd(a.trace_valid + (long long)cur_f * a.trace_stride, tvalid);
+        }
+    }
+}
+
 __global__ void k_interpolate(const int32_t* __restrict__ lookup, const double* __restrict__ planes,
                               FrameGeom g, const uint8_t* __restrict__ mask, float max_disp,
                               float* __restrict__ value, uint8_t* __restrict__ valid) {
@@ -226,6 +430,25 @@ int launch_refine(const RefineArgs& a, const CostTables& tab, bool last, cudaStr
     // reciprocals for the exact small-integer divisions (div_small corrects them)
     const float inv_cell = 1.0f / float(a.cell), inv_w = 1.0f / float(a.g.width);
     const bool key32 = a.g.pixels <= (1ll << kIdxBits);
+    if (a.g.pixels % 16 == 0 && key32) {
+        // bulk-copy pipeline: persistent CTAs, 2 per SM
+        static int sms = 0;
+        if (sms == 0) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            const int smem = kStages * kStageBytes;
+            cudaFuncSetAttribute(k_refine_bulk<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            cudaFuncSetAttribute(k_refine_bulk<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        }
+        const int tpf = int((a.g.pixels + kTile - 1) / kTile);
+        const long long total = (long long)tpf * a.frames;
+        const unsigned blocks = unsigned(std::min<long long>(total, 2ll * sms));
+        const size_t smem = size_t(kStages) * kStageBytes;
+        if (last) k_refine_bulk<true, true><<<blocks, 256, smem, st>>>(a, tab, inv_cell, inv_w, tpf, total);
+        else k_refine_bulk<false, true><<<blocks, 256, smem, st>>>(a, tab, inv_cell, inv_w, tpf, total);
+        return 1;
+    }
     if (last) {
         if (key32) k_refine<true, true><<<grid, 256, 0, st>>>(a, tab, inv_cell, inv_w);
         else k_refine<true, false><<<grid, 256, 0, st>>>(a, tab, inv_cell, inv_w);
