@@ -139,6 +139,9 @@ typedef struct ps_kernel_stat {
 /* Enables per-launch CUDA-event timing of the engine kernels (on the stream
  * each kernel is launched on). */
 ps_status ps_set_profiling(ps_ctx* ctx, int enabled);
+/* At most `groups` frame groups (CUDA streams) in flight; default 8.  With 1
+ * the device stages run back to back, so kernel times are isolated. */
+ps_status ps_set_max_groups(ps_ctx* ctx, int groups);
 ps_status ps_reset_kernel_stats(ps_ctx* ctx);
 ps_status ps_get_kernel_stats(ps_ctx* ctx, ps_kernel_stat* out, int capacity, int* count);
 /* Kernel launches issued by this context since creation. */

@@ -260,6 +260,9 @@ class Context:
     def set_profiling(self, on: bool) -> None:
         _check(self._lib.ps_set_profiling(self._h, 1 if on else 0))
 
+    def set_max_groups(self, groups: int) -> None:
+        _check(self._lib.ps_set_max_groups(self._h, groups))
+
     def reset_kernel_stats(self) -> None:
         _check(self._lib.ps_reset_kernel_stats(self._h))
 

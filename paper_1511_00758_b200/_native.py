@@ -98,6 +98,7 @@ SIGNATURES = {
     "ps_download_batch": (I, [P, P, P, P, P, P, P, P]),
     "ps_get_supports": (I, [P, I, P, P, P, I, P]),
     "ps_set_profiling": (I, [P, I]),
+    "ps_set_max_groups": (I, [P, I]),
     "ps_reset_kernel_stats": (I, [P]),
     "ps_get_kernel_stats": (I, [P, P, I, P]),
     "ps_launch_count": (C.c_longlong, [P]),

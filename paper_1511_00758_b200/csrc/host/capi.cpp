@@ -178,6 +178,12 @@ ps_status ps_set_profiling(ps_ctx* ctx, int enabled) {
     return PS_OK;
 }
 
+ps_status ps_set_max_groups(ps_ctx* ctx, int groups) {
+    PS_REQUIRE_CTX(ctx);
+    ctx->engine->set_max_groups(groups);
+    return PS_OK;
+}
+
 ps_status ps_reset_kernel_stats(ps_ctx* ctx) {
     PS_REQUIRE_CTX(ctx);
     ctx->engine->reset_stats();

@@ -441,7 +441,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     //   device stages on the group's stream -> (completion) -> next iteration.
     // The host loop below only moves data and launches; the workers
     // triangulate continuously while the device runs other groups' stages.
-    const int G = std::max(1, std::min(kMaxGroups, (F + 31) / 32));
+    const int G = std::max(1, std::min(std::min(kMaxGroups, max_groups_), (F + 31) / 32));
     const int tri_cap = int(std::min<long long>(2ll * scap_ + 8, 2ll * P + 8));  // T <= 2S per frame
     for (int gi = 0; gi < G; ++gi) {
         FrameGroup& grp = groups_[gi];

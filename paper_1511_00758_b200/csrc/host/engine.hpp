@@ -78,6 +78,9 @@ public:
     ps_status supports(int frame, int* u, int* v, double* d, int capacity, int* count);
 
     void set_profiling(bool on) { profiling_ = on; }
+    // Upper bound on concurrent frame groups (streams); 1 serialises the
+    // device stages, so per-kernel event times are isolated launch durations.
+    void set_max_groups(int g) { max_groups_ = g < 1 ? 1 : g; }
     void reset_stats() { stats_.clear(); }
     const std::vector<KernelStat>& stats() const { return stats_; }
     long long launches() const { return launches_; }
@@ -113,6 +116,7 @@ private:
     ThreadPool* pool_ = nullptr;
     std::vector<DelaunayWorkspace> ws_;
     bool profiling_ = false;
+    int max_groups_ = kMaxGroups;
     long long launches_ = 0;
     std::vector<KernelStat> stats_;
     struct Pending {

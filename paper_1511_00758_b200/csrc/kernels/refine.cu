@@ -183,6 +183,20 @@ constexpr int kTileSlots = 8;
 constexpr int kStages = 3;
 constexpr int kStageBytes = kTile * (1 + 4 + 4 + 4);
 
+// n / d for 0 <= n, d < 2^16 with magic = ceil(2^32 / d) (exact in that range).
+__device__ __forceinline__ int mdiv(int n, unsigned magic, int d) {
+    return d == 1 ? n : int(__umulhi(unsigned(n), magic));
+}
+
+// x * 2^36 for a non-negative float >= 2^-13 (or 0): exact, integer ops only.
+__device__ __forceinline__ unsigned long long fixed36(float x) {
+    const unsigned b = __float_as_uint(x);
+    if (b == 0u) return 0ull;
+    const int sh = int(b >> 23) - 127 + 36 - 23;
+    const unsigned long long m = (b & 0x7fffffu) | 0x800000u;
+    return sh >= 0 ? m << sh : m >> (-sh);
+}
+
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
@@ -206,11 +220,13 @@ __device__ __forceinline__ void bar_wait(unsigned long long* bar, unsigned phase
 }
 
 template <bool LAST, bool KEY32>
-__global__ void __launch_bounds__(256) k_refine_bulk(RefineArgs a, CostTables tab, float inv_cell,
-                                                     float inv_w, int tiles_per_frame,
+__global__ void __launch_bounds__(256) k_refine_bulk(RefineArgs a, CostTables tab, unsigned magic_cell,
+                                                     unsigned magic_w, int tiles_per_frame,
                                                      long long total_tiles) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) unsigned long long bars[kStages];
+    __shared__ float s_cost[32];  // k/24 table in smem: lane-divergent k, no constant-cache serialisation
+    if (threadIdx.x <= kCensusBits) s_cost[threadIdx.x] = tab.cost[threadIdx.x];
     const long long P = a.g.pixels;
     const int W = a.g.width;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -282,7 +298,7 @@ __global__ void __launch_bounds__(256) k_refine_bulk(RefineArgs a, CostTables ta
         for (int q = 0; q < kTileSlots; ++q) {
             const int p = warp * 256 + q * 32 + lane;
             const int r = r0 + p;
-            const int dv = div_small(r, W, inv_w);
+            const int dv = mdiv(r, magic_w, W);
             v[q] = int(v0) + dv;
             u[q] = r - dv * W;
             k[q] = kCensusBits;
@@ -316,7 +332,7 @@ __global__ void __launch_bounds__(256) k_refine_bulk(RefineArgs a, CostTables ta
             int cell = -1;
             if (m) {
                 float cf = sm_cf[p];
-                const float c = tab.cost[k[q]];
+                const float c = s_cost[k[q]];
                 if (c < cf) {  // pipeline.cpp:68-71
                     cf = c;
                     a.Cf[fb + i] = c;
@@ -325,10 +341,10 @@ __global__ void __launch_bounds__(256) k_refine_bulk(RefineArgs a, CostTables ta
                 }
                 qg = (tab.low_mask >> k[q]) & 1u;
                 qb = !qg && ((tab.high_mask >> k[q]) & 1u);
-                tsum += __double2ull_rn(__dmul_rn(double(cf), 68719476736.0));  // * 2^36
+                tsum += fixed36(cf);  // cf * 2^36 (exact, see trace_fixed_exact)
                 tvalid += cf < tab.cost_high ? 1u : 0u;
             }
-            if (in) cell = div_small(v[q], a.cell, inv_cell) * a.cols + div_small(u[q], a.cell, inv_cell);
+            if (in) cell = mdiv(v[q], magic_cell, a.cell) * a.cols + mdiv(u[q], magic_cell, a.cell);
             unsigned long long* cg = a.Cg + (long long)f * a.cell_stride + (cell < 0 ? 0 : cell);
             unsigned long long* cb = a.Cb + (long long)f * a.cell_stride + (cell < 0 ? 0 : cell);
             if (!KEY32) {
@@ -430,7 +446,11 @@ int launch_refine(const RefineArgs& a, const CostTables& tab, bool last, cudaStr
     // reciprocals for the exact small-integer divisions (div_small corrects them)
     const float inv_cell = 1.0f / float(a.cell), inv_w = 1.0f / float(a.g.width);
     const bool key32 = a.g.pixels <= (1ll << kIdxBits);
-    if (a.g.pixels % 16 == 0 && key32) {
+    if (a.g.pixels % 16 == 0 && key32 && a.g.width + kTile < (1 << 16) && a.g.height < (1 << 16) &&
+        a.cell < (1 << 16)) {
+        // exact 16-bit magic reciprocals for the row / cell divisions (mdiv)
+        const unsigned magic_w = unsigned((0x100000000ull + a.g.width - 1) / a.g.width);
+        const unsigned magic_cell = unsigned((0x100000000ull + a.cell - 1) / a.cell);
         // bulk-copy pipeline: persistent CTAs, 2 per SM
         static int sms = 0;
         if (sms == 0) {
@@ -445,8 +465,8 @@ int launch_refine(const RefineArgs& a, const CostTables& tab, bool last, cudaStr
         const long long total = (long long)tpf * a.frames;
         const unsigned blocks = unsigned(std::min<long long>(total, 2ll * sms));
         const size_t smem = size_t(kStages) * kStageBytes;
-        if (last) k_refine_bulk<true, true><<<blocks, 256, smem, st>>>(a, tab, inv_cell, inv_w, tpf, total);
-        else k_refine_bulk<false, true><<<blocks, 256, smem, st>>>(a, tab, inv_cell, inv_w, tpf, total);
+        if (last) k_refine_bulk<true, true><<<blocks, 256, smem, st>>>(a, tab, magic_cell, magic_w, tpf, total);
+        else k_refine_bulk<false, true><<<blocks, 256, smem, st>>>(a, tab, magic_cell, magic_w, tpf, total);
         return 1;
     }
     if (last) {
