@@ -178,8 +178,9 @@ __global__ void __launch_bounds__(256) k_refine(RefineArgs a, CostTables tab, fl
 // so the next two tiles are in flight while the current one is processed and
 // its cR gathers are outstanding.  Same per-pixel logic and cell reduction
 // as k_refine.  Needs 16-B aligned tiles: P % 16 == 0.
-constexpr int kTile = 2048;          // 8 warps x 8 slots x 32 lanes
-constexpr int kTileSlots = 8;
+constexpr int kTileSlots = 4;
+constexpr int kWarpPx = 32 * kTileSlots;
+constexpr int kTile = 8 * kWarpPx;   // 8 warps x 4 slots x 32 lanes = 1024 px
 constexpr int kStages = 3;
 constexpr int kStageBytes = kTile * (1 + 4 + 4 + 4);
 
@@ -222,7 +223,7 @@ __device__ __forceinline__ void bar_wait(unsigned long long* bar, unsigned phase
 template <bool LAST, bool KEY32>
 __global__ void __launch_bounds__(256) k_refine_bulk(RefineArgs a, CostTables tab, unsigned magic_cell,
                                                      unsigned magic_w, int tiles_per_frame,
-                                                     long long total_tiles) {
+                                                     long long total_tiles, int run_span) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) unsigned long long bars[kStages];
     __shared__ float s_cost[32];  // k/24 table in smem: lane-divergent k, no constant-cache serialisation
@@ -296,7 +297,7 @@ __global__ void __launch_bounds__(256) k_refine_bulk(RefineArgs a, CostTables ta
         uint32_t crv[kTileSlots];
 #pragma unroll
         for (int q = 0; q < kTileSlots; ++q) {
-            const int p = warp * 256 + q * 32 + lane;
+            const int p = warp * kWarpPx + q * 32 + lane;
             const int r = r0 + p;
             const int dv = mdiv(r, magic_w, W);
             v[q] = int(v0) + dv;
@@ -317,7 +318,7 @@ __global__ void __launch_bounds__(256) k_refine_bulk(RefineArgs a, CostTables ta
         }
 #pragma unroll
         for (int q = 0; q < kTileSlots; ++q) {
-            const int p = warp * 256 + q * 32 + lane;
+            const int p = warp * kWarpPx + q * 32 + lane;
             const long long i = off + p;
             const bool in = i < P;
             const uint8_t m = in ? sm_mask[p] : 0;
@@ -355,8 +356,8 @@ __global__ void __launch_bounds__(256) k_refine_bulk(RefineArgs a, CostTables ta
             if (__ballot_sync(0xffffffffu, qg | qb) == 0u) continue;
             unsigned kg = qg ? ((unsigned)k[q] << kIdxBits) | unsigned(i) : 0xffffffffu;
             unsigned kb = qb ? ((unsigned)(kCensusBits - k[q]) << kIdxBits) | unsigned(i) : 0xffffffffu;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
+            // a run of equal cells spans at most run_span lanes (power of two)
+            for (int o = 1; o < run_span; o <<= 1) {
                 const int c2 = __shfl_down_sync(0xffffffffu, cell, o);
                 const unsigned g2 = __shfl_down_sync(0xffffffffu, kg, o);
                 const unsigned b2 = __shfl_down_sync(0xffffffffu, kb, o);
@@ -451,22 +452,32 @@ int launch_refine(const RefineArgs& a, const CostTables& tab, bool last, cudaStr
         // exact 16-bit magic reciprocals for the row / cell divisions (mdiv)
         const unsigned magic_w = unsigned((0x100000000ull + a.g.width - 1) / a.g.width);
         const unsigned magic_cell = unsigned((0x100000000ull + a.cell - 1) / a.cell);
-        // bulk-copy pipeline: persistent CTAs, 2 per SM
-        static int sms = 0;
+        // bulk-copy pipeline: persistent CTAs, as many per SM as registers and
+        // shared memory allow (queried once)
+        static int sms = 0, per_sm_last = 0, per_sm = 0;
+        const size_t smem = size_t(kStages) * kStageBytes;
         if (sms == 0) {
             int dev = 0;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            const int smem = kStages * kStageBytes;
-            cudaFuncSetAttribute(k_refine_bulk<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-            cudaFuncSetAttribute(k_refine_bulk<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            cudaFuncSetAttribute(k_refine_bulk<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            cudaFuncSetAttribute(k_refine_bulk<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_last, k_refine_bulk<true, true>, 256, smem);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_refine_bulk<false, true>, 256, smem);
+            per_sm_last = std::max(1, per_sm_last);
+            per_sm = std::max(1, per_sm);
         }
         const int tpf = int((a.g.pixels + kTile - 1) / kTile);
         const long long total = (long long)tpf * a.frames;
-        const unsigned blocks = unsigned(std::min<long long>(total, 2ll * sms));
-        const size_t smem = size_t(kStages) * kStageBytes;
-        if (last) k_refine_bulk<true, true><<<blocks, 256, smem, st>>>(a, tab, magic_cell, magic_w, tpf, total);
-        else k_refine_bulk<false, true><<<blocks, 256, smem, st>>>(a, tab, magic_cell, magic_w, tpf, total);
+        const unsigned blocks =
+            unsigned(std::min<long long>(total, (long long)(last ? per_sm_last : per_sm) * sms));
+        // longest run of equal cells inside a 32-pixel slot, rounded up to 2^n
+        const int cols = (a.g.width + a.cell - 1) / a.cell;
+        int run = cols == 1 ? 32 : std::min(a.cell, 32);
+        int run_span = 1;
+        while (run_span < run) run_span <<= 1;
+        if (last) k_refine_bulk<true, true><<<blocks, 256, smem, st>>>(a, tab, magic_cell, magic_w, tpf, total, run_span);
+        else k_refine_bulk<false, true><<<blocks, 256, smem, st>>>(a, tab, magic_cell, magic_w, tpf, total, run_span);
         return 1;
     }
     if (last) {
