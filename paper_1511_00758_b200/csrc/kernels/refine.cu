@@ -291,86 +291,92 @@ __global__ void __launch_bounds__(256) k_refine_bulk(RefineArgs a, CostTables ta
         const float* sm_dit = reinterpret_cast<const float*>(st + kTile);
         const uint32_t* sm_cl = reinterpret_cast<const uint32_t*>(st + 5 * kTile);
         const float* sm_cf = reinterpret_cast<const float*>(st + 9 * kTile);
+        // per-tile bases: 32-bit pixel offsets from here on
+        const int n_in = int(min((long long)kTile, P - off));
         const long long v0 = off / W;
         const int r0 = int(off - v0 * W);
-        int u[kTileSlots], v[kTileSlots], k[kTileSlots];
+        const int ib = int(off);  // first pixel of the tile within the frame (P <= 2^27)
+        const uint32_t* cr_f = a.cr + fb;
+        float* Cf_f = a.Cf + fb;
+        float* Df_f = a.Df + fb;
+        uint8_t* Dv_f = a.Dv + fb;
+        unsigned long long* Cg_f = a.Cg + (long long)f * a.cell_stride;
+        unsigned long long* Cb_f = a.Cb + (long long)f * a.cell_stride;
+        const int cellsz = a.cell, cols = a.cols;
+        // slot geometry: lane l of slot q is pixel p = warp*128 + q*32 + l; the
+        // slot's first pixel is uniform, each lane adds its lane index (W >= 32:
+        // at most one row wrap inside a slot)
+        int us[kTileSlots], vs[kTileSlots];
         uint32_t crv[kTileSlots];
+        unsigned okm = 0;
 #pragma unroll
         for (int q = 0; q < kTileSlots; ++q) {
-            const int p = warp * kWarpPx + q * 32 + lane;
-            const int r = r0 + p;
+            const int r = r0 + warp * kWarpPx + q * 32;
             const int dv = mdiv(r, magic_w, W);
-            v[q] = int(v0) + dv;
-            u[q] = r - dv * W;
-            k[q] = kCensusBits;
-            crv[q] = 0;
-            if (off + p < P && sm_mask[p]) {
-                const float d = sm_dit[p];
-                if (d == d) {
-                    const int dr = lround_away(d);
-                    const int ur = u[q] - dr;
-                    if (dr >= 0 && ur >= 2) {
-                        k[q] = 0;
-                        crv[q] = __ldg(a.cr + fb + (long long)v[q] * W + ur);
-                    }
-                }
+            int u = r - dv * W + lane;
+            int v = int(v0) + dv;
+            if (u >= W) {
+                u -= W;
+                ++v;
             }
+            us[q] = u;
+            vs[q] = v;
+            const int p = warp * kWarpPx + q * 32 + lane;
+            const float d = sm_dit[p];
+            const int dr = lround_away(d);
+            const int ur = u - dr;
+            const bool ok = p < n_in && sm_mask[p] && d == d && dr >= 0 && ur >= 2;
+            crv[q] = ok ? __ldg(cr_f + v * W + ur) : 0u;
+            okm |= unsigned(ok) << q;
         }
 #pragma unroll
         for (int q = 0; q < kTileSlots; ++q) {
             const int p = warp * kWarpPx + q * 32 + lane;
-            const long long i = off + p;
-            const bool in = i < P;
-            const uint8_t m = in ? sm_mask[p] : 0;
-            const float d = in ? sm_dit[p] : __int_as_float(0x7fffffff);
-            const bool valid = d == d;
+            const int i = ib + p;
+            const bool in = p < n_in;
+            const bool m = in && sm_mask[p];
+            const float d = sm_dit[p];
             if (LAST && in) {
+                const bool valid = d == d;
                 a.dense[fb + i] = valid ? d : 0.0f;
                 a.dense_valid[fb + i] = valid ? 1 : 0;
             }
-            if (k[q] == 0) k[q] = __popc(sm_cl[p] ^ crv[q]);
-            bool qg = false, qb = false;
-            int cell = -1;
-            if (m) {
-                float cf = sm_cf[p];
-                const float c = s_cost[k[q]];
-                if (c < cf) {  // pipeline.cpp:68-71
-                    cf = c;
-                    a.Cf[fb + i] = c;
-                    a.Df[fb + i] = d;
-                    a.Dv[fb + i] = 1;
-                }
-                qg = (tab.low_mask >> k[q]) & 1u;
-                qb = !qg && ((tab.high_mask >> k[q]) & 1u);
-                tsum += fixed36(cf);  // cf * 2^36 (exact, see trace_fixed_exact)
-                tvalid += cf < tab.cost_high ? 1u : 0u;
+            const int k = ((okm >> q) & 1u) ? __popc(sm_cl[p] ^ crv[q]) : kCensusBits;
+            const float c = s_cost[k];
+            float cf = sm_cf[p];
+            const bool upd = m && c < cf;  // pipeline.cpp:68-71
+            if (upd) {
+                Cf_f[i] = c;
+                Df_f[i] = d;
+                Dv_f[i] = 1;
             }
-            if (in) cell = mdiv(v[q], magic_cell, a.cell) * a.cols + mdiv(u[q], magic_cell, a.cell);
-            unsigned long long* cg = a.Cg + (long long)f * a.cell_stride + (cell < 0 ? 0 : cell);
-            unsigned long long* cb = a.Cb + (long long)f * a.cell_stride + (cell < 0 ? 0 : cell);
+            cf = upd ? c : cf;
+            const bool qg = m && ((tab.low_mask >> k) & 1u);
+            const bool qb = m && !qg && ((tab.high_mask >> k) & 1u);
+            tsum += m ? fixed36(cf) : 0ull;  // cf * 2^36 (exact, see trace_fixed_exact)
+            tvalid += (m && cf < tab.cost_high) ? 1u : 0u;
+            const int cell = in ? mdiv(vs[q], magic_cell, cellsz) * cols + mdiv(us[q], magic_cell, cellsz) : -1;
             if (!KEY32) {
-                if (qg) atomicMin(cg, (unsigned long long)k[q] << 32 | (unsigned long long)i);
-                if (qb) atomicMin(cb, (unsigned long long)(kCensusBits - k[q]) << 32 | (unsigned long long)i);
+                if (qg) atomicMin(Cg_f + cell, (unsigned long long)k << 32 | (unsigned long long)i);
+                if (qb) atomicMin(Cb_f + cell, (unsigned long long)(kCensusBits - k) << 32 | (unsigned long long)i);
                 continue;
             }
             if (__ballot_sync(0xffffffffu, qg | qb) == 0u) continue;
-            unsigned kg = qg ? ((unsigned)k[q] << kIdxBits) | unsigned(i) : 0xffffffffu;
-            unsigned kb = qb ? ((unsigned)(kCensusBits - k[q]) << kIdxBits) | unsigned(i) : 0xffffffffu;
+            unsigned kg = qg ? ((unsigned)k << kIdxBits) | unsigned(i) : 0xffffffffu;
+            unsigned kb = qb ? ((unsigned)(kCensusBits - k) << kIdxBits) | unsigned(i) : 0xffffffffu;
             // a run of equal cells spans at most run_span lanes (power of two)
             for (int o = 1; o < run_span; o <<= 1) {
                 const int c2 = __shfl_down_sync(0xffffffffu, cell, o);
                 const unsigned g2 = __shfl_down_sync(0xffffffffu, kg, o);
                 const unsigned b2 = __shfl_down_sync(0xffffffffu, kb, o);
-                if (lane + o < 32 && c2 == cell) {
-                    kg = min(kg, g2);
-                    kb = min(kb, b2);
-                }
+                const bool same = lane + o < 32 && c2 == cell;
+                kg = same ? min(kg, g2) : kg;
+                kb = same ? min(kb, b2) : kb;
             }
             const int cprev = __shfl_up_sync(0xffffffffu, cell, 1);
-            if (lane == 0 || cprev != cell) {
-                if (kg != 0xffffffffu) atomicMin(cg, widen(kg));
-                if (kb != 0xffffffffu) atomicMin(cb, widen(kb));
-            }
+            const bool lead = lane == 0 || cprev != cell;
+            if (lead && kg != 0xffffffffu) atomicMin(Cg_f + cell, widen(kg));
+            if (lead && kb != 0xffffffffu) atomicMin(Cb_f + cell, widen(kb));
         }
         __syncthreads();  // every thread is done with stage s
         if (threadIdx.x == 0) {
@@ -447,8 +453,8 @@ int launch_refine(const RefineArgs& a, const CostTables& tab, bool last, cudaStr
     // reciprocals for the exact small-integer divisions (div_small corrects them)
     const float inv_cell = 1.0f / float(a.cell), inv_w = 1.0f / float(a.g.width);
     const bool key32 = a.g.pixels <= (1ll << kIdxBits);
-    if (a.g.pixels % 16 == 0 && key32 && a.g.width + kTile < (1 << 16) && a.g.height < (1 << 16) &&
-        a.cell < (1 << 16)) {
+    if (a.g.pixels % 16 == 0 && key32 && a.g.width >= 32 && a.g.width + kTile < (1 << 16) &&
+        a.g.height < (1 << 16) && a.cell < (1 << 16)) {
         // exact 16-bit magic reciprocals for the row / cell divisions (mdiv)
         const unsigned magic_w = unsigned((0x100000000ull + a.g.width - 1) / a.g.width);
         const unsigned magic_cell = unsigned((0x100000000ull + a.cell - 1) / a.cell);
