@@ -106,9 +106,11 @@ CostTables make_tables(const ps_config& c) {
             if (t.cost[k] > prod) t.uniq_reject[k] |= 1u << k2;
         }
     }
-    for (int k = 0; k <= kCensusBits; ++k)
+    t.code_high = 0;
+    while (t.code_high <= kCensusBits && t.cost[t.code_high] < c.cost_high) ++t.code_high;
+    for (int k = 0; k < t.code_high; ++k)
         t.fixed[k] = (unsigned long long)std::ldexp(double(t.cost[k]), 36);
-    t.fixed[kCensusBits + 1] = (unsigned long long)std::ldexp(double(c.cost_high), 36);
+    t.fixed[t.code_high] = (unsigned long long)std::ldexp(double(c.cost_high), 36);
     t.cost_high = c.cost_high;
     return t;
 }
@@ -133,7 +135,7 @@ Engine::Engine(int device) : device_(device) {
 Engine::~Engine() {
     cudaSetDevice(device_);
     cudaDeviceSynchronize();
-    DevBuf* bufs[] = {&dL_, &dR_, &dMask_, &dMaskCount_, &dCL_, &dCR_, &dDf_, &dDv_, &dCf_,
+    DevBuf* bufs[] = {&dL_, &dR_, &dMask_, &dMaskCount_, &dCL_, &dCR_, &dDf_, &dDv_, &dCf_, &dCode_,
                       &dDense_, &dDenseV_, &dLookup_, &dSu_, &dSv_, &dSd_, &dS_, &dSnext_,
                       &dTaken_, &dCg_, &dCb_, &dBinKeys_, &dBinCount_, &dScratch_, &dCandU_,
                       &dCandV_, &dCandCount_, &dOk_, &dDisp_, &dRemU_, &dRemV_, &dRemCount_,
@@ -339,6 +341,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     float* dDf = dev<float>(dDf_, size_t(F) * P);
     uint8_t* dDv = dev<uint8_t>(dDv_, size_t(F) * P);
     float* dCf = dev<float>(dCf_, size_t(F) * P);
+    uint8_t* dCode = dev<uint8_t>(dCode_, size_t(F) * P);
     float* dDense = dev<float>(dDense_, size_t(F) * P);
     uint8_t* dDenseV = dev<uint8_t>(dDenseV_, size_t(F) * P);
     float* dDit = dev<float>(dLookup_, size_t(F) * P);  // D_it per pixel (NaN = invalid)
@@ -371,7 +374,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     unsigned long long* hTraceSum =
         reinterpret_cast<unsigned long long*>(host<uint8_t>(hTraceSum_, size_t(F) * iters * 8));
     unsigned* hTraceValid = reinterpret_cast<unsigned*>(host<uint8_t>(hTraceValid_, size_t(F) * iters * 4));
-    const void* must[] = {dMask, dMaskCount, dCL, dCR, dDf, dDv, dCf, dDense, dDenseV, dDit,
+    const void* must[] = {dMask, dMaskCount, dCL, dCR, dDf, dDv, dCf, dCode, dDense, dDenseV, dDit,
                           dSu, dSv, dSd, dS, dSnext, dTaken, dCg, dCb, dBinKeys, dBinCount,
                           dScratch, dCandU, dCandV, dCandCount, dOk, dDisp, dRemU, dRemV,
                           dRemCount, dConf, dChunk, dTraceSum, dTraceValid, dErr, hS, hMaskCount,
@@ -389,13 +392,12 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     cudaMemsetAsync(dTraceSum, 0, sizeof(unsigned long long) * F * iters, st_);
     cudaMemsetAsync(dTraceValid, 0, sizeof(unsigned) * F * iters, st_);
     cudaMemsetAsync(dDf, 0, sizeof(float) * F * P, st_);
-    cudaMemsetAsync(dDv, 0, size_t(F) * P, st_);
     cudaMemsetAsync(dErr, 0, sizeof(int), st_);
-    launches_ += launch_fill_f32(dCf, (long long)F * P, cfg.cost_high, st_);
 
     // ---- K1 frontend (image.cpp:43-60, census.cpp:10-41)
     begin_kernel("frontend", 11.0 * double(P) * F, st_);
-    launches_ += launch_frontend(dL, dR, g, F, cfg.gradient_threshold, dMask, dCL, dCR, dMaskCount, st_);
+    launches_ += launch_frontend(dL, dR, g, F, cfg.gradient_threshold, dMask, dCL, dCR, dMaskCount, st_,
+                                 dCode, tab.code_high);
     end_kernel(st_);
     // ---- K2 candidates (sparse.cpp:84-146)
     begin_kernel("candidates", double(P) * F, st_);
@@ -658,6 +660,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         ra.Df = dDf + fp;
         ra.Dv = dDv + fp;
         ra.Cf = dCf + fp;
+        ra.code = dCode + fp;
         ra.Cg = cg;
         ra.Cb = cb;
         ra.trace_sum = dTraceSum + size_t(f0) * iters + (it - 1);
@@ -742,11 +745,15 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                 for (int i = 0; i < grp.n; ++i) trace_[size_t(grp.f0 + i) * iters + (grp.it - 1)].millis = ms;
                 if (observer && F == 1) {
                     std::vector<float> fd(P), fc(P);
-                    std::vector<uint8_t> fv(P);
+                    std::vector<uint8_t> fv(P), code(P);
                     s = check(cudaMemcpy(fd.data(), dDf, sizeof(float) * P, cudaMemcpyDeviceToHost), "D2H");
-                    if (s == PS_OK) s = check(cudaMemcpy(fv.data(), dDv, P, cudaMemcpyDeviceToHost), "D2H");
-                    if (s == PS_OK) s = check(cudaMemcpy(fc.data(), dCf, sizeof(float) * P, cudaMemcpyDeviceToHost), "D2H");
+                    if (s == PS_OK) s = check(cudaMemcpy(code.data(), dCode, P, cudaMemcpyDeviceToHost), "D2H");
                     if (s != PS_OK) return s;
+                    for (long long i = 0; i < P; ++i) {  // C_f / validity from the byte codes
+                        const bool fin = code[i] < tab.code_high;
+                        fv[i] = fin ? 1 : 0;
+                        fc[i] = fin ? tab.cost[code[i]] : tab.cost_high;
+                    }
                     observer(grp.it, fd.data(), fv.data(), fc.data(), W, H, user);
                 }
                 if (grp.it == iters) {

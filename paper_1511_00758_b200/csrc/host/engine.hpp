@@ -138,7 +138,7 @@ private:
     float cost_high_ = 0.5f;
 
     // device buffers (frame-strided)
-    DevBuf dL_, dR_, dMask_, dMaskCount_, dCL_, dCR_, dDf_, dDv_, dCf_, dDense_, dDenseV_,
+    DevBuf dL_, dR_, dMask_, dMaskCount_, dCL_, dCR_, dDf_, dDv_, dCf_, dCode_, dDense_, dDenseV_,
         dLookup_, dSu_, dSv_, dSd_, dS_, dSnext_, dTaken_, dCg_, dCb_, dBinKeys_, dBinCount_,
         dScratch_, dCandU_, dCandV_, dCandCount_, dOk_, dDisp_, dRemU_, dRemV_, dRemCount_,
         dConf_, dChunk_, dTraceSum_, dTraceValid_, dErr_;

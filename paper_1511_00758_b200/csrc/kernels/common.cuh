@@ -18,6 +18,7 @@ namespace ps {
 constexpr int kCensusBits = 24;
 constexpr int kNoKey = 25;  // "no second-best" marker (BestMatch init 2.0f, sparse.cpp:38-42)
 constexpr unsigned long long kEmptyCell = ~0ull;
+constexpr unsigned char kCodeOff = 0xFF;  // C_f code of a pixel outside the gradient mask
 
 // Host-built lookup tables derived from the PipelineConfig floats.
 struct CostTables {
@@ -26,7 +27,13 @@ struct CostTables {
     unsigned high_mask;                 // bit k: cost[k] >  costHigh  (pipeline.cpp:78)
     unsigned accept_mask;               // bit k: !(cost[k] > sparseAcceptCost)   (sparse.cpp:169)
     unsigned uniq_reject[kCensusBits + 1];  // bit k2 of [k1]: cost[k1] > ratio*cost[k2] (sparse.cpp:172)
-    unsigned long long fixed[kCensusBits + 2];  // cost*2^36 for k=0..24, [25] = costHigh
+    // C_f as a byte code: c < code_high is cost[c], code_high is costHigh
+    // (the initial value), kCodeOff marks a pixel outside the gradient mask.
+    // Every C_f value the reference can hold is one of these: C_f starts at
+    // costHigh and only takes cost[k] < C_f (pipeline.cpp:68-71), so
+    // cost[k] < C_f  <=>  k < code, and C_f < costHigh  <=>  code < code_high.
+    unsigned long long fixed[kCensusBits + 2];  // C_f*2^36 per code (trace)
+    int code_high;                              // #{k : cost[k] < costHigh}
     float cost_high;
 };
 

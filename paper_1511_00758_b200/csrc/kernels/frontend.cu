@@ -52,7 +52,8 @@ __global__ void __launch_bounds__(256) k_frontend(const uint8_t* __restrict__ le
                                                   int thr, uint8_t* __restrict__ mask,
                                                   uint32_t* __restrict__ cl,
                                                   uint32_t* __restrict__ cr,
-                                                  int* __restrict__ mask_count) {
+                                                  int* __restrict__ mask_count,
+                                                  uint8_t* __restrict__ code, uint8_t code_high) {
     __shared__ uint8_t sl[kSmH][kSmW];
     __shared__ uint8_t sr[kSmH][kSmW];
     __shared__ int warp_cnt[8];
@@ -99,11 +100,16 @@ __global__ void __launch_bounds__(256) k_frontend(const uint8_t* __restrict__ le
             if (cl) *reinterpret_cast<uint4*>(cl + base) = make_uint4(dl[0], dl[1], dl[2], dl[3]);
             if (cr && R) *reinterpret_cast<uint4*>(cr + base) = make_uint4(dr[0], dr[1], dr[2], dr[3]);
             if (mask) *reinterpret_cast<uchar4*>(mask + base) = make_uchar4(mk[0], mk[1], mk[2], mk[3]);
+            if (code)
+                *reinterpret_cast<uchar4*>(code + base) =
+                    make_uchar4(mk[0] ? code_high : kCodeOff, mk[1] ? code_high : kCodeOff,
+                                mk[2] ? code_high : kCodeOff, mk[3] ? code_high : kCodeOff);
         } else {
             for (int j = 0; j < 4 && ub + j < W; ++j) {
                 if (cl) cl[base + j] = dl[j];
                 if (cr && R) cr[base + j] = dr[j];
                 if (mask) mask[base + j] = mk[j];
+                if (code) code[base + j] = mk[j] ? code_high : kCodeOff;
             }
         }
     }
@@ -343,10 +349,10 @@ __global__ void __launch_bounds__(1024) k_candidate_sort(
 
 int launch_frontend(const uint8_t* left, const uint8_t* right, FrameGeom g, int frames,
                     int grad_threshold, uint8_t* mask, uint32_t* cl, uint32_t* cr,
-                    int* mask_count, cudaStream_t st) {
+                    int* mask_count, cudaStream_t st, uint8_t* code, int code_high) {
     dim3 grid((g.width + kTileW - 1) / kTileW, (g.height + kTileH - 1) / kTileH, frames);
     k_frontend<<<grid, dim3(32, 8), 0, st>>>(left, right, g, grad_threshold, mask, cl, cr,
-                                             mask_count);
+                                             mask_count, code, uint8_t(code_high));
     return 1;
 }
 

@@ -12,10 +12,13 @@ namespace ps {
 
 // K1 — gradient mask + census(L) + census(R), fused over 128x8 tiles
 // (proj/src/image.cpp:43-60, proj/src/census.cpp:10-41).  Any of mask / cl /
-// cr / right may be null to skip that output.
+// cr / right may be null to skip that output.  `code` (optional) receives the
+// initial per-pixel C_f state of the refinement: code_high on mask pixels
+// (C_f = costHigh, pipeline.cpp:146), kCodeOff elsewhere.
 int launch_frontend(const uint8_t* left, const uint8_t* right, FrameGeom g, int frames,
                     int grad_threshold, uint8_t* mask, uint32_t* cl, uint32_t* cr,
-                    int* mask_count, cudaStream_t st);
+                    int* mask_count, cudaStream_t st, uint8_t* code = nullptr,
+                    int code_high = 0);
 
 // K2 — segment-test corners, 12x10 binning, per-bin top-`cap` and the
 // global (score desc, v, u) sort (proj/src/sparse.cpp:84-146).
@@ -77,9 +80,10 @@ struct RefineArgs {
     int cols;
     int cells_per_frame;  // cells of this iteration
     int cell_stride;      // per-frame stride of the grid arrays (>= cells_per_frame)
+    uint8_t* code;  // C_f per pixel as a byte code (CostTables), updated in place
     float* Df;
-    uint8_t* Dv;
-    float* Cf;
+    uint8_t* Dv;    // LAST only: D_f validity (code < code_high)
+    float* Cf;      // LAST only: C_f as binary32
     unsigned long long* Cg;
     unsigned long long* Cb;
     unsigned long long* trace_sum;  // [frames] for this iteration (stride trace_stride)

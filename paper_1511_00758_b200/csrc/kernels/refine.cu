@@ -64,17 +64,16 @@ __global__ void __launch_bounds__(256) k_refine(RefineArgs a, CostTables tab, fl
     unsigned tvalid = 0;
     if (chunk < P) {  // warp-uniform
         const long long fb = (long long)f * P;
-        uint8_t m[kSlots];
-        float d[kSlots], cf[kSlots];
+        uint8_t cc[kSlots];
+        float d[kSlots];
         uint32_t cl[kSlots];
 #pragma unroll
         for (int j = 0; j < kSlots; ++j) {
             const long long i = chunk + 32 * j + lane;
             const bool in = i < P;
-            m[j] = in ? __ldg(a.mask + fb + i) : 0;
+            cc[j] = in ? a.code[fb + i] : kCodeOff;
             d[j] = in ? __ldg(a.dit + fb + i) : __int_as_float(0x7fffffff);
             cl[j] = in ? __ldg(a.cl + fb + i) : 0u;
-            cf[j] = in ? a.Cf[fb + i] : 0.0f;
         }
         int u[kSlots], v[kSlots], k[kSlots];
         uint32_t crv[kSlots];
@@ -88,7 +87,7 @@ __global__ void __launch_bounds__(256) k_refine(RefineArgs a, CostTables tab, fl
             u[j] = r - dv * W;
             k[j] = kCensusBits;  // sentinel cost 1.0 (pipeline.cpp:15,35)
             crv[j] = 0;
-            if (m[j] && d[j] == d[j]) {  // mask pixel with a valid D_it
+            if (cc[j] != kCodeOff && d[j] == d[j]) {  // mask pixel with a valid D_it
                 const int dr = lround_away(d[j]);
                 const int ur = u[j] - dr;
                 if (dr >= 0 && ur >= 2) {
@@ -101,29 +100,31 @@ __global__ void __launch_bounds__(256) k_refine(RefineArgs a, CostTables tab, fl
         for (int j = 0; j < kSlots; ++j) {
             const long long i = chunk + 32 * j + lane;
             const bool valid = d[j] == d[j];
-            if (LAST && i < P) {
-                a.dense[fb + i] = valid ? d[j] : 0.0f;
-                a.dense_valid[fb + i] = valid ? 1 : 0;
-            }
+            const bool m = cc[j] != kCodeOff;
             if (k[j] == 0) k[j] = __popc(cl[j] ^ crv[j]);
             bool qg = false, qb = false;
             unsigned long long keyg = 0, keyb = 0;
             int cell = -1;
-            if (m[j]) {
-                const float c = tab.cost[k[j]];
-                if (c < cf[j]) {  // pipeline.cpp:68-71
-                    cf[j] = c;
-                    a.Cf[fb + i] = c;
+            if (m) {
+                if (k[j] < cc[j]) {  // cost[k] < C_f (pipeline.cpp:68-71), see CostTables
+                    cc[j] = uint8_t(k[j]);
+                    a.code[fb + i] = cc[j];
                     a.Df[fb + i] = d[j];
-                    a.Dv[fb + i] = 1;
                 }
                 const unsigned long long idx = (unsigned long long)i;
                 qg = (tab.low_mask >> k[j]) & 1u;
                 qb = !qg && ((tab.high_mask >> k[j]) & 1u);
                 keyg = (unsigned long long)k[j] << 32 | idx;
                 keyb = (unsigned long long)(kCensusBits - k[j]) << 32 | idx;
-                tsum += __double2ull_rn(__dmul_rn(double(cf[j]), 68719476736.0));  // * 2^36
-                tvalid += cf[j] < tab.cost_high ? 1u : 0u;
+                tsum += tab.fixed[cc[j]];
+                tvalid += cc[j] < tab.code_high ? 1u : 0u;
+            }
+            if (LAST && i < P) {
+                const bool fin = m && cc[j] < tab.code_high;
+                a.dense[fb + i] = valid ? d[j] : 0.0f;
+                a.dense_valid[fb + i] = valid ? 1 : 0;
+                a.Cf[fb + i] = fin ? tab.cost[cc[j]] : tab.cost_high;
+                a.Dv[fb + i] = fin ? 1 : 0;
             }
             if (i < P) {
                 cell = div_small(v[j], a.cell, inv_cell) * a.cols + div_small(u[j], a.cell, inv_cell);
@@ -182,20 +183,11 @@ constexpr int kTileSlots = 4;
 constexpr int kWarpPx = 32 * kTileSlots;
 constexpr int kTile = 8 * kWarpPx;   // 8 warps x 4 slots x 32 lanes = 1024 px
 constexpr int kStages = 3;
-constexpr int kStageBytes = kTile * (1 + 4 + 4 + 4);
+constexpr int kStageBytes = kTile * (4 + 4 + 1);  // D_it, cL, C_f code
 
 // n / d for 0 <= n, d < 2^16 with magic = ceil(2^32 / d) (exact in that range).
 __device__ __forceinline__ int mdiv(int n, unsigned magic, int d) {
     return d == 1 ? n : int(__umulhi(unsigned(n), magic));
-}
-
-// x * 2^36 for a non-negative float >= 2^-13 (or 0): exact, integer ops only.
-__device__ __forceinline__ unsigned long long fixed36(float x) {
-    const unsigned b = __float_as_uint(x);
-    if (b == 0u) return 0ull;
-    const int sh = int(b >> 23) - 127 + 36 - 23;
-    const unsigned long long m = (b & 0x7fffffu) | 0x800000u;
-    return sh >= 0 ? m << sh : m >> (-sh);
 }
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -220,14 +212,18 @@ __device__ __forceinline__ void bar_wait(unsigned long long* bar, unsigned phase
         "}\n" :: "r"(smem_u32(bar)), "r"(phase) : "memory");
 }
 
-template <bool LAST, bool KEY32>
+template <bool LAST, bool KEY32, int SPAN>
 __global__ void __launch_bounds__(256) k_refine_bulk(RefineArgs a, CostTables tab, unsigned magic_cell,
                                                      unsigned magic_w, int tiles_per_frame,
-                                                     long long total_tiles, int run_span) {
+                                                     long long total_tiles) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) unsigned long long bars[kStages];
-    __shared__ float s_cost[32];  // k/24 table in smem: lane-divergent k, no constant-cache serialisation
+    // lane-divergent table lookups from smem, not the (serialising) constant bank
+    __shared__ float s_cost[32];
+    __shared__ unsigned long long s_fix[32];
     if (threadIdx.x <= kCensusBits) s_cost[threadIdx.x] = tab.cost[threadIdx.x];
+    if (threadIdx.x <= kCensusBits + 1) s_fix[threadIdx.x] = tab.fixed[threadIdx.x];
+    const unsigned code_high = unsigned(tab.code_high);
     const long long P = a.g.pixels;
     const int W = a.g.width;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -240,11 +236,10 @@ __global__ void __launch_bounds__(256) k_refine_bulk(RefineArgs a, CostTables ta
         const long long base = (long long)f * P + off;
         unsigned char* st = stage_ptr(s);
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n"
-                     :: "r"(smem_u32(&bars[s])), "r"(n * 13u) : "memory");
-        bulk_g2s(st, a.mask + base, n, &bars[s]);
-        bulk_g2s(st + kTile, a.dit + base, 4 * n, &bars[s]);
-        bulk_g2s(st + 5 * kTile, a.cl + base, 4 * n, &bars[s]);
-        bulk_g2s(st + 9 * kTile, a.Cf + base, 4 * n, &bars[s]);
+                     :: "r"(smem_u32(&bars[s])), "r"(n * 9u) : "memory");
+        bulk_g2s(st, a.dit + base, 4 * n, &bars[s]);
+        bulk_g2s(st + 4 * kTile, a.cl + base, 4 * n, &bars[s]);
+        bulk_g2s(st + 8 * kTile, a.code + base, n, &bars[s]);
     };
 
     if (threadIdx.x == 0) {
@@ -287,19 +282,17 @@ __global__ void __launch_bounds__(256) k_refine_bulk(RefineArgs a, CostTables ta
         const long long off = (tile - (long long)f * tiles_per_frame) * kTile;
         const long long fb = (long long)f * P;
         const unsigned char* st = stage_ptr(s);
-        const uint8_t* sm_mask = st;
-        const float* sm_dit = reinterpret_cast<const float*>(st + kTile);
-        const uint32_t* sm_cl = reinterpret_cast<const uint32_t*>(st + 5 * kTile);
-        const float* sm_cf = reinterpret_cast<const float*>(st + 9 * kTile);
+        const float* sm_dit = reinterpret_cast<const float*>(st);
+        const uint32_t* sm_cl = reinterpret_cast<const uint32_t*>(st + 4 * kTile);
+        const uint8_t* sm_code = st + 8 * kTile;
         // per-tile bases: 32-bit pixel offsets from here on
         const int n_in = int(min((long long)kTile, P - off));
         const long long v0 = off / W;
         const int r0 = int(off - v0 * W);
         const int ib = int(off);  // first pixel of the tile within the frame (P <= 2^27)
         const uint32_t* cr_f = a.cr + fb;
-        float* Cf_f = a.Cf + fb;
+        uint8_t* code_f = a.code + fb;
         float* Df_f = a.Df + fb;
-        uint8_t* Dv_f = a.Dv + fb;
         unsigned long long* Cg_f = a.Cg + (long long)f * a.cell_stride;
         unsigned long long* Cb_f = a.Cb + (long long)f * a.cell_stride;
         const int cellsz = a.cell, cols = a.cols;
@@ -325,7 +318,7 @@ __global__ void __launch_bounds__(256) k_refine_bulk(RefineArgs a, CostTables ta
             const float d = sm_dit[p];
             const int dr = lround_away(d);
             const int ur = u - dr;
-            const bool ok = p < n_in && sm_mask[p] && d == d && dr >= 0 && ur >= 2;
+            const bool ok = p < n_in && sm_code[p] != kCodeOff && d == d && dr >= 0 && ur >= 2;
             crv[q] = ok ? __ldg(cr_f + v * W + ur) : 0u;
             okm |= unsigned(ok) << q;
         }
@@ -334,27 +327,28 @@ __global__ void __launch_bounds__(256) k_refine_bulk(RefineArgs a, CostTables ta
             const int p = warp * kWarpPx + q * 32 + lane;
             const int i = ib + p;
             const bool in = p < n_in;
-            const bool m = in && sm_mask[p];
+            const unsigned c0 = sm_code[p];
+            const bool m = in && c0 != kCodeOff;
             const float d = sm_dit[p];
+            const int k = ((okm >> q) & 1u) ? __popc(sm_cl[p] ^ crv[q]) : kCensusBits;
+            const bool upd = m && unsigned(k) < c0;  // cost[k] < C_f (pipeline.cpp:68-71)
+            if (upd) {
+                code_f[i] = uint8_t(k);
+                Df_f[i] = d;
+            }
+            const unsigned cc = upd ? unsigned(k) : c0;
             if (LAST && in) {
                 const bool valid = d == d;
+                const bool fin = m && cc < code_high;
                 a.dense[fb + i] = valid ? d : 0.0f;
                 a.dense_valid[fb + i] = valid ? 1 : 0;
+                a.Cf[fb + i] = fin ? s_cost[cc] : tab.cost_high;
+                a.Dv[fb + i] = fin ? 1 : 0;
             }
-            const int k = ((okm >> q) & 1u) ? __popc(sm_cl[p] ^ crv[q]) : kCensusBits;
-            const float c = s_cost[k];
-            float cf = sm_cf[p];
-            const bool upd = m && c < cf;  // pipeline.cpp:68-71
-            if (upd) {
-                Cf_f[i] = c;
-                Df_f[i] = d;
-                Dv_f[i] = 1;
-            }
-            cf = upd ? c : cf;
             const bool qg = m && ((tab.low_mask >> k) & 1u);
             const bool qb = m && !qg && ((tab.high_mask >> k) & 1u);
-            tsum += m ? fixed36(cf) : 0ull;  // cf * 2^36 (exact, see trace_fixed_exact)
-            tvalid += (m && cf < tab.cost_high) ? 1u : 0u;
+            tsum += m ? s_fix[cc] : 0ull;  // C_f * 2^36 (exact, see trace_fixed_exact)
+            tvalid += (m && cc < code_high) ? 1u : 0u;
             const int cell = in ? mdiv(vs[q], magic_cell, cellsz) * cols + mdiv(us[q], magic_cell, cellsz) : -1;
             if (!KEY32) {
                 if (qg) atomicMin(Cg_f + cell, (unsigned long long)k << 32 | (unsigned long long)i);
@@ -364,8 +358,9 @@ __global__ void __launch_bounds__(256) k_refine_bulk(RefineArgs a, CostTables ta
             if (__ballot_sync(0xffffffffu, qg | qb) == 0u) continue;
             unsigned kg = qg ? ((unsigned)k << kIdxBits) | unsigned(i) : 0xffffffffu;
             unsigned kb = qb ? ((unsigned)(kCensusBits - k) << kIdxBits) | unsigned(i) : 0xffffffffu;
-            // a run of equal cells spans at most run_span lanes (power of two)
-            for (int o = 1; o < run_span; o <<= 1) {
+            // a run of equal cells spans at most SPAN lanes (power of two)
+#pragma unroll
+            for (int o = 1; o < SPAN; o <<= 1) {
                 const int c2 = __shfl_down_sync(0xffffffffu, cell, o);
                 const unsigned g2 = __shfl_down_sync(0xffffffffu, kg, o);
                 const unsigned b2 = __shfl_down_sync(0xffffffffu, kb, o);
@@ -447,6 +442,29 @@ __global__ void k_fill_f32(float* __restrict__ p, long long n, float x) {
 
 }  // namespace
 
+namespace {
+// Persistent bulk-copy launch: as many CTAs per SM as registers and shared
+// memory allow (queried once per instantiation).
+template <bool LAST, int SPAN>
+void launch_bulk(const RefineArgs& a, const CostTables& tab, unsigned magic_cell, unsigned magic_w,
+                 int tpf, long long total, cudaStream_t st) {
+    static int sms = 0, per_sm = 0;
+    const size_t smem = size_t(kStages) * kStageBytes;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(k_refine_bulk<LAST, true, SPAN>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_refine_bulk<LAST, true, SPAN>, 256,
+                                                      smem);
+        per_sm = std::max(1, per_sm);
+    }
+    const unsigned blocks = unsigned(std::min<long long>(total, (long long)per_sm * sms));
+    k_refine_bulk<LAST, true, SPAN><<<blocks, 256, smem, st>>>(a, tab, magic_cell, magic_w, tpf, total);
+}
+}  // namespace
+
 int launch_refine(const RefineArgs& a, const CostTables& tab, bool last, cudaStream_t st) {
     const long long chunks = (a.g.pixels + kChunk - 1) / kChunk;
     dim3 grid(unsigned((chunks + 7) / 8), a.frames);
@@ -458,32 +476,27 @@ int launch_refine(const RefineArgs& a, const CostTables& tab, bool last, cudaStr
         // exact 16-bit magic reciprocals for the row / cell divisions (mdiv)
         const unsigned magic_w = unsigned((0x100000000ull + a.g.width - 1) / a.g.width);
         const unsigned magic_cell = unsigned((0x100000000ull + a.cell - 1) / a.cell);
-        // bulk-copy pipeline: persistent CTAs, as many per SM as registers and
-        // shared memory allow (queried once)
-        static int sms = 0, per_sm_last = 0, per_sm = 0;
-        const size_t smem = size_t(kStages) * kStageBytes;
-        if (sms == 0) {
-            int dev = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            cudaFuncSetAttribute(k_refine_bulk<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-            cudaFuncSetAttribute(k_refine_bulk<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_last, k_refine_bulk<true, true>, 256, smem);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_refine_bulk<false, true>, 256, smem);
-            per_sm_last = std::max(1, per_sm_last);
-            per_sm = std::max(1, per_sm);
-        }
         const int tpf = int((a.g.pixels + kTile - 1) / kTile);
         const long long total = (long long)tpf * a.frames;
-        const unsigned blocks =
-            unsigned(std::min<long long>(total, (long long)(last ? per_sm_last : per_sm) * sms));
         // longest run of equal cells inside a 32-pixel slot, rounded up to 2^n
         const int cols = (a.g.width + a.cell - 1) / a.cell;
-        int run = cols == 1 ? 32 : std::min(a.cell, 32);
-        int run_span = 1;
-        while (run_span < run) run_span <<= 1;
-        if (last) k_refine_bulk<true, true><<<blocks, 256, smem, st>>>(a, tab, magic_cell, magic_w, tpf, total, run_span);
-        else k_refine_bulk<false, true><<<blocks, 256, smem, st>>>(a, tab, magic_cell, magic_w, tpf, total, run_span);
+        const int run = cols == 1 ? 32 : std::min(a.cell, 32);
+        int span = 1;
+        while (span < run) span <<= 1;
+        switch (span * 2 + (last ? 1 : 0)) {
+            case 2: launch_bulk<false, 1>(a, tab, magic_cell, magic_w, tpf, total, st); break;
+            case 3: launch_bulk<true, 1>(a, tab, magic_cell, magic_w, tpf, total, st); break;
+            case 4: launch_bulk<false, 2>(a, tab, magic_cell, magic_w, tpf, total, st); break;
+            case 5: launch_bulk<true, 2>(a, tab, magic_cell, magic_w, tpf, total, st); break;
+            case 8: launch_bulk<false, 4>(a, tab, magic_cell, magic_w, tpf, total, st); break;
+            case 9: launch_bulk<true, 4>(a, tab, magic_cell, magic_w, tpf, total, st); break;
+            case 16: launch_bulk<false, 8>(a, tab, magic_cell, magic_w, tpf, total, st); break;
+            case 17: launch_bulk<true, 8>(a, tab, magic_cell, magic_w, tpf, total, st); break;
+            case 32: launch_bulk<false, 16>(a, tab, magic_cell, magic_w, tpf, total, st); break;
+            case 33: launch_bulk<true, 16>(a, tab, magic_cell, magic_w, tpf, total, st); break;
+            case 64: launch_bulk<false, 32>(a, tab, magic_cell, magic_w, tpf, total, st); break;
+            default: launch_bulk<true, 32>(a, tab, magic_cell, magic_w, tpf, total, st); break;
+        }
         return 1;
     }
     if (last) {
