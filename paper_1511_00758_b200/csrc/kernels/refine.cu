@@ -173,21 +173,31 @@ __global__ void __launch_bounds__(256) k_refine(RefineArgs a, CostTables tab, fl
 }
 
 // ---------------------------------------------------------------------------
-// Bulk-copy (TMA 1-D) variant: a persistent CTA streams 2048-pixel tiles of
-// mask / D_it / cL / C_f into a 3-stage shared-memory ring with
-// cp.async.bulk + mbarrier complete_tx (one elected thread issues, all wait),
-// so the next two tiles are in flight while the current one is processed and
-// its cR gathers are outstanding.  Same per-pixel logic and cell reduction
-// as k_refine.  Needs 16-B aligned tiles: P % 16 == 0.
+// Bulk-copy (TMA 1-D) variant, the production path.  A persistent CTA owns a
+// CONTIGUOUS range of 1024-pixel tiles (so frame changes, and with them the
+// trace flushes, are rare) and streams per tile D_it, cL, the C_f code and
+// the tile's cR row span (plus a max_disp halo to the left, for the same-row
+// gather cR(u - d)) into a shared-memory ring with cp.async.bulk + mbarrier
+// complete_tx, under an L2 evict-first policy (every byte is read once).  The
+// cR gather is then a shared-memory load.  Stage release: the last of the 8
+// warps to finish a stage refills it (no CTA-wide barrier).  Needs 16-B
+// aligned tiles (P % 16 == 0) and max_disp <= kMaxHalo.
 constexpr int kTileSlots = 4;
 constexpr int kWarpPx = 32 * kTileSlots;
-constexpr int kTile = 8 * kWarpPx;   // 8 warps x 4 slots x 32 lanes = 1024 px
-constexpr int kStages = 3;
-constexpr int kStageBytes = kTile * (4 + 4 + 1);  // D_it, cL, C_f code
+constexpr int kWarps = 8;
+constexpr int kTile = kWarps * kWarpPx;  // 8 warps x 4 slots x 32 lanes = 1024 px
+constexpr int kStages = 4;
+constexpr int kMaxHalo = 1024;  // cR words staged left of the tile (>= max_disp)
 
 // n / d for 0 <= n, d < 2^16 with magic = ceil(2^32 / d) (exact in that range).
 __device__ __forceinline__ int mdiv(int n, unsigned magic, int d) {
     return d == 1 ? n : int(__umulhi(unsigned(n), magic));
+}
+
+// n / d with magic31 = ceil(2^31 / d): exact whenever n * d < 2^31 (here
+// n < 2^16 and d < 2^15), including d = 1, so no special case.
+__device__ __forceinline__ int mdiv31(int n, unsigned magic31) {
+    return int(__umulhi(unsigned(n) << 1, magic31));
 }
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -195,137 +205,156 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
 }
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
-                                         unsigned long long* bar) {
+                                         unsigned long long* bar, unsigned long long policy) {
     asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
-        :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1], %2, [%3], %4;\n"
+        :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
         : "memory");
 }
 
 __device__ __forceinline__ void bar_wait(unsigned long long* bar, unsigned phase) {
+    // try_wait with a suspend-time hint: the warp sleeps until the phase
+    // completes instead of spinning on the issue slots
     asm volatile(
         "{\n"
         ".reg .pred P1;\n"
         "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, 1000000;\n"
         "@!P1 bra WAIT_%=;\n"
         "}\n" :: "r"(smem_u32(bar)), "r"(phase) : "memory");
 }
 
+struct BulkGeom {
+    int tiles_per_frame;
+    int total_tiles;
+    int halo;         // cR words staged left of a tile: max_disp rounded up to 4
+    int stage_bytes;  // 9 * kTile + 4 * (kTile + halo)
+    int q_tile;       // kTile / W
+    int r_tile;       // kTile % W
+};
+
 template <bool LAST, bool KEY32, int SPAN>
-__global__ void __launch_bounds__(256) k_refine_bulk(RefineArgs a, CostTables tab, unsigned magic_cell,
-                                                     unsigned magic_w, int tiles_per_frame,
-                                                     long long total_tiles) {
+__global__ void __launch_bounds__(256, 4) k_refine_bulk(RefineArgs a, CostTables tab,
+                                                        unsigned magic_cell31, unsigned magic_w,
+                                                        BulkGeom bg) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) unsigned long long bars[kStages];
-    // lane-divergent table lookups from smem, not the (serialising) constant bank
-    __shared__ float s_cost[32];
+    __shared__ unsigned s_done[kStages];  // warps finished with the stage (monotonic)
+    // indexed by code & 31 (kCodeOff -> 31): output C_f, and C_f * 2^36 for
+    // the trace (0 off the mask); smem, not the (serialising) constant bank
+    __shared__ float s_cout[32];
     __shared__ unsigned long long s_fix[32];
-    if (threadIdx.x <= kCensusBits) s_cost[threadIdx.x] = tab.cost[threadIdx.x];
-    if (threadIdx.x <= kCensusBits + 1) s_fix[threadIdx.x] = tab.fixed[threadIdx.x];
     const unsigned code_high = unsigned(tab.code_high);
-    const long long P = a.g.pixels;
+    if (threadIdx.x < 32) {
+        const unsigned c = threadIdx.x;
+        s_cout[c] = c < code_high ? tab.cost[c] : tab.cost_high;
+        s_fix[c] = c <= code_high ? tab.fixed[c] : 0ull;
+    }
+    // frames * P < 2^31 (launch_refine splits larger batches): 32-bit pixel offsets
+    const int P = int(a.g.pixels);
     const int W = a.g.width;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    auto stage_ptr = [&](int s) { return smem + s * kStageBytes; };
+    const int H = bg.halo;
+    const int t_begin = int((long long)bg.total_tiles * blockIdx.x / gridDim.x);
+    const int t_end = int((long long)bg.total_tiles * (blockIdx.x + 1) / gridDim.x);
+    auto stage_ptr = [&](int s) { return smem + s * bg.stage_bytes; };
 
-    auto issue = [&](long long tile, int s) {
-        const int f = int(tile / tiles_per_frame);
-        const long long off = (tile - (long long)f * tiles_per_frame) * kTile;
-        const unsigned n = unsigned(min((long long)kTile, P - off));
-        const long long base = (long long)f * P + off;
+    auto issue = [&](int tile, int s) {
+        unsigned long long policy;
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(policy));
+        const int f = tile / bg.tiles_per_frame;
+        const int off = (tile - f * bg.tiles_per_frame) * kTile;
+        const unsigned n = unsigned(min(kTile, P - off));
+        const int h = min(off, H);  // halo inside this frame (rows never reach back further)
+        const int base = f * P + off;
         unsigned char* st = stage_ptr(s);
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n"
-                     :: "r"(smem_u32(&bars[s])), "r"(n * 9u) : "memory");
-        bulk_g2s(st, a.dit + base, 4 * n, &bars[s]);
-        bulk_g2s(st + 4 * kTile, a.cl + base, 4 * n, &bars[s]);
-        bulk_g2s(st + 8 * kTile, a.code + base, n, &bars[s]);
+                     :: "r"(smem_u32(&bars[s])), "r"(n * 13u + 4u * unsigned(h)) : "memory");
+        bulk_g2s(st, a.dit + base, 4 * n, &bars[s], policy);
+        bulk_g2s(st + 4 * kTile, a.cl + base, 4 * n, &bars[s], policy);
+        bulk_g2s(st + 8 * kTile, a.code + base, n, &bars[s], policy);
+        bulk_g2s(st + 9 * kTile + 4 * (H - h), a.cr + base - h, 4 * (unsigned(h) + n), &bars[s], policy);
     };
 
+    if (threadIdx.x < kStages) s_done[threadIdx.x] = 0;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s)
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" :: "r"(smem_u32(&bars[s])));
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-        for (int s = 0; s < kStages; ++s) {
-            const long long tile = blockIdx.x + (long long)s * gridDim.x;
-            if (tile < total_tiles) issue(tile, s);
-        }
+        for (int s = 0; s < kStages && t_begin + s < t_end; ++s) issue(t_begin + s, s);
     }
     __syncthreads();
 
+    // tile geometry, advanced incrementally (no per-tile divisions)
+    int f = t_begin / bg.tiles_per_frame;
+    int off = (t_begin - f * bg.tiles_per_frame) * kTile;
+    int v0 = off / W;
+    int r0 = off - v0 * W;
     unsigned long long tsum = 0;
     unsigned tvalid = 0;
-    int cur_f = -1;
-    int j = 0;
-    for (long long tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++j) {
+    auto flush = [&](int fr) {  // per-warp trace partials of frame fr
+        unsigned long long ts = tsum;
+        ts = __shfl_xor_sync(0xffffffffu, ts, 16) + ts;
+        ts = __shfl_xor_sync(0xffffffffu, ts, 8) + ts;
+        ts = __shfl_xor_sync(0xffffffffu, ts, 4) + ts;
+        ts = __shfl_xor_sync(0xffffffffu, ts, 2) + ts;
+        ts = __shfl_xor_sync(0xffffffffu, ts, 1) + ts;
+        const unsigned tv = __reduce_add_sync(0xffffffffu, tvalid);
+        if (lane == 0 && (ts | tv)) {
+            atomicAdd(a.trace_sum + (long long)fr * a.trace_stride, ts);
+            atomicAdd(a.trace_valid + (long long)fr * a.trace_stride, tv);
+        }
+        tsum = 0;
+        tvalid = 0;
+    };
+    const int cellsz = a.cell, cols = a.cols;
+    for (int tile = t_begin, j = 0; tile < t_end; ++tile, ++j) {
         const int s = j % kStages;
         bar_wait(&bars[s], unsigned((j / kStages) & 1));
-        const int f = int(tile / tiles_per_frame);
-        if (f != cur_f) {  // frame change: flush the trace partials of the previous frame
-            if (cur_f >= 0) {
-                unsigned long long ts = tsum;
-                ts = __shfl_xor_sync(0xffffffffu, ts, 16) + ts;
-                ts = __shfl_xor_sync(0xffffffffu, ts, 8) + ts;
-                ts = __shfl_xor_sync(0xffffffffu, ts, 4) + ts;
-                ts = __shfl_xor_sync(0xffffffffu, ts, 2) + ts;
-                ts = __shfl_xor_sync(0xffffffffu, ts, 1) + ts;
-                const unsigned tv = __reduce_add_sync(0xffffffffu, tvalid);
-                if (lane == 0 && (ts | tv)) {
-                    atomicAdd(a.trace_sum + (long long)cur_f * a.trace_stride, ts);
-                    atomicAdd(a.trace_valid + (long long)cur_f * a.trace_stride, tv);
-                }
-            }
-            cur_f = f;
-            tsum = 0;
-            tvalid = 0;
-        }
-        const long long off = (tile - (long long)f * tiles_per_frame) * kTile;
-        const long long fb = (long long)f * P;
         const unsigned char* st = stage_ptr(s);
         const float* sm_dit = reinterpret_cast<const float*>(st);
         const uint32_t* sm_cl = reinterpret_cast<const uint32_t*>(st + 4 * kTile);
         const uint8_t* sm_code = st + 8 * kTile;
-        // per-tile bases: 32-bit pixel offsets from here on
-        const int n_in = int(min((long long)kTile, P - off));
-        const long long v0 = off / W;
-        const int r0 = int(off - v0 * W);
-        const int ib = int(off);  // first pixel of the tile within the frame (P <= 2^27)
-        const uint32_t* cr_f = a.cr + fb;
-        uint8_t* code_f = a.code + fb;
-        float* Df_f = a.Df + fb;
+        const uint32_t* sm_cr = reinterpret_cast<const uint32_t*>(st + 9 * kTile) + H;  // [p - dr]
+        const int n_in = min(kTile, P - off);
+        const int ib = off;          // first pixel of the tile within the frame (P <= 2^27)
+        const int tb = f * P + off;  // first pixel of the tile within the batch
         unsigned long long* Cg_f = a.Cg + (long long)f * a.cell_stride;
         unsigned long long* Cb_f = a.Cb + (long long)f * a.cell_stride;
-        const int cellsz = a.cell, cols = a.cols;
         // slot geometry: lane l of slot q is pixel p = warp*128 + q*32 + l; the
-        // slot's first pixel is uniform, each lane adds its lane index (W >= 32:
-        // at most one row wrap inside a slot)
-        int us[kTileSlots], vs[kTileSlots];
+        // slot's first pixel (row vrow, column ucol) is uniform, each lane adds
+        // its lane index (W >= 32: at most one row wrap inside a slot).  The
+        // pixels of one occupancy cell are a run of consecutive lanes: run_end
+        // is the last lane of this lane's run, lead marks its first lane.
+        int cells[kTileSlots], run_end[kTileSlots];
         uint32_t crv[kTileSlots];
-        unsigned okm = 0;
+        unsigned okm = 0, leadm = 0;
 #pragma unroll
         for (int q = 0; q < kTileSlots; ++q) {
             const int r = r0 + warp * kWarpPx + q * 32;
-            const int dv = mdiv(r, magic_w, W);
+            const int dv = int(__umulhi(unsigned(r), magic_w));  // W >= 32
+            const int vrow = v0 + dv;
             int u = r - dv * W + lane;
-            int v = int(v0) + dv;
-            if (u >= W) {
-                u -= W;
-                ++v;
-            }
-            us[q] = u;
-            vs[q] = v;
+            const bool wrap = u >= W;
+            u = wrap ? u - W : u;
+            const int crow0 = mdiv31(vrow, magic_cell31) * cols;
+            const int crow1 = mdiv31(vrow + 1, magic_cell31) * cols;
+            const int ccol = mdiv31(u, magic_cell31);
+            const int ubeg = ccol * cellsz;
+            cells[q] = (wrap ? crow1 : crow0) + ccol;
+            run_end[q] = lane + min(ubeg + cellsz, W) - u - 1;
+            leadm |= unsigned(lane == 0 || u == ubeg) << q;
             const int p = warp * kWarpPx + q * 32 + lane;
             const float d = sm_dit[p];
             const int dr = lround_away(d);
-            const int ur = u - dr;
-            const bool ok = p < n_in && sm_code[p] != kCodeOff && d == d && dr >= 0 && ur >= 2;
-            crv[q] = ok ? __ldg(cr_f + v * W + ur) : 0u;
+            const bool ok = p < n_in && sm_code[p] != kCodeOff && d == d && dr >= 0 && u - dr >= 2;
+            crv[q] = ok ? sm_cr[p - dr] : 0u;  // same-row cR(u - dr), staged
             okm |= unsigned(ok) << q;
         }
 #pragma unroll
         for (int q = 0; q < kTileSlots; ++q) {
             const int p = warp * kWarpPx + q * 32 + lane;
-            const int i = ib + p;
             const bool in = p < n_in;
             const unsigned c0 = sm_code[p];
             const bool m = in && c0 != kCodeOff;
@@ -333,64 +362,75 @@ __global__ void __launch_bounds__(256) k_refine_bulk(RefineArgs a, CostTables ta
             const int k = ((okm >> q) & 1u) ? __popc(sm_cl[p] ^ crv[q]) : kCensusBits;
             const bool upd = m && unsigned(k) < c0;  // cost[k] < C_f (pipeline.cpp:68-71)
             if (upd) {
-                code_f[i] = uint8_t(k);
-                Df_f[i] = d;
+                a.code[tb + p] = uint8_t(k);
+                a.Df[tb + p] = d;
             }
-            const unsigned cc = upd ? unsigned(k) : c0;
+            const unsigned cc = (upd ? unsigned(k) : c0) & 31u;  // kCodeOff -> 31
             if (LAST && in) {
                 const bool valid = d == d;
-                const bool fin = m && cc < code_high;
-                a.dense[fb + i] = valid ? d : 0.0f;
-                a.dense_valid[fb + i] = valid ? 1 : 0;
-                a.Cf[fb + i] = fin ? s_cost[cc] : tab.cost_high;
-                a.Dv[fb + i] = fin ? 1 : 0;
+                a.dense[tb + p] = valid ? d : 0.0f;
+                a.dense_valid[tb + p] = valid ? 1 : 0;
+                a.Cf[tb + p] = s_cout[cc];
+                a.Dv[tb + p] = cc < code_high ? 1 : 0;
             }
             const bool qg = m && ((tab.low_mask >> k) & 1u);
             const bool qb = m && !qg && ((tab.high_mask >> k) & 1u);
-            tsum += m ? s_fix[cc] : 0ull;  // C_f * 2^36 (exact, see trace_fixed_exact)
-            tvalid += (m && cc < code_high) ? 1u : 0u;
-            const int cell = in ? mdiv(vs[q], magic_cell, cellsz) * cols + mdiv(us[q], magic_cell, cellsz) : -1;
+            tsum += in ? s_fix[cc] : 0ull;  // C_f * 2^36 (exact, see trace_fixed_exact); 0 off-mask
+            tvalid += (in && cc < code_high) ? 1u : 0u;
             if (!KEY32) {
-                if (qg) atomicMin(Cg_f + cell, (unsigned long long)k << 32 | (unsigned long long)i);
-                if (qb) atomicMin(Cb_f + cell, (unsigned long long)(kCensusBits - k) << 32 | (unsigned long long)i);
+                const int i = ib + p;
+                if (qg) atomicMin(Cg_f + cells[q], (unsigned long long)k << 32 | (unsigned long long)i);
+                if (qb) atomicMin(Cb_f + cells[q], (unsigned long long)(kCensusBits - k) << 32 | (unsigned long long)i);
                 continue;
             }
             if (__ballot_sync(0xffffffffu, qg | qb) == 0u) continue;
-            unsigned kg = qg ? ((unsigned)k << kIdxBits) | unsigned(i) : 0xffffffffu;
-            unsigned kb = qb ? ((unsigned)(kCensusBits - k) << kIdxBits) | unsigned(i) : 0xffffffffu;
-            // a run of equal cells spans at most SPAN lanes (power of two)
+            // both grid keys of the lane in one word, 16 bits each: (k << 5 | lane)
+            // for the confident grid, ((24 - k) << 5 | lane) for the invalid one;
+            // lanes grow with the pixel index, so the min is the reference's
+            // first-row-major winner.  Segmented min over the run: VIMNMX.U16x2.
+            unsigned key = (qg ? ((unsigned(k) << 5 | unsigned(lane)) << 16) : 0xffff0000u) |
+                           (qb ? (unsigned(kCensusBits - k) << 5 | unsigned(lane)) : 0xffffu);
 #pragma unroll
             for (int o = 1; o < SPAN; o <<= 1) {
-                const int c2 = __shfl_down_sync(0xffffffffu, cell, o);
-                const unsigned g2 = __shfl_down_sync(0xffffffffu, kg, o);
-                const unsigned b2 = __shfl_down_sync(0xffffffffu, kb, o);
-                const bool same = lane + o < 32 && c2 == cell;
-                kg = same ? min(kg, g2) : kg;
-                kb = same ? min(kb, b2) : kb;
+                const unsigned other = __shfl_down_sync(0xffffffffu, key, o);
+                key = lane + o <= run_end[q] ? __vminu2(key, other) : key;
             }
-            const int cprev = __shfl_up_sync(0xffffffffu, cell, 1);
-            const bool lead = lane == 0 || cprev != cell;
-            if (lead && kg != 0xffffffffu) atomicMin(Cg_f + cell, widen(kg));
-            if (lead && kb != 0xffffffffu) atomicMin(Cb_f + cell, widen(kb));
+            if ((leadm >> q) & 1u) {
+                const unsigned i0 = unsigned(ib + warp * kWarpPx + q * 32);  // pixel of lane 0
+                const unsigned g = key >> 16, b = key & 0xffffu;
+                if (g != 0xffffu)
+                    atomicMin(Cg_f + cells[q], (unsigned long long)(g >> 5) << 32 | (i0 + (g & 31u)));
+                if (b != 0xffffu)
+                    atomicMin(Cb_f + cells[q], (unsigned long long)(b >> 5) << 32 | (i0 + (b & 31u)));
+            }
         }
-        __syncthreads();  // every thread is done with stage s
-        if (threadIdx.x == 0) {
-            const long long next = tile + (long long)kStages * gridDim.x;
-            if (next < total_tiles) issue(next, s);
+        // release stage s: the last of the 8 warps to finish it refills it
+        // (no CTA-wide barrier, so fast warps run ahead into the next stages)
+        __syncwarp();
+        if (lane == 0) {
+            const unsigned prev = atomicAdd(&s_done[s], 1u);
+            if (prev % kWarps == kWarps - 1 && tile + kStages < t_end) {
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                issue(tile + kStages, s);
+            }
+        }
+        // next tile
+        off += kTile;
+        r0 += bg.r_tile;
+        v0 += bg.q_tile;
+        if (r0 >= W) {
+            r0 -= W;
+            ++v0;
+        }
+        if (off >= P) {  // frame change (tiles never straddle frames)
+            flush(f);
+            ++f;
+            off = 0;
+            v0 = 0;
+            r0 = 0;
         }
     }
-    if (cur_f >= 0) {
-        tsum = __shfl_xor_sync(0xffffffffu, tsum, 16) + tsum;
-        tsum = __shfl_xor_sync(0xffffffffu, tsum, 8) + tsum;
-        tsum = __shfl_xor_sync(0xffffffffu, tsum, 4) + tsum;
-        tsum = __shfl_xor_sync(0xffffffffu, tsum, 2) + tsum;
-        tsum = __shfl_xor_sync(0xffffffffu, tsum, 1) + tsum;
-        tvalid = __reduce_add_sync(0xffffffffu, tvalid);
-        if (lane == 0 && (tsum | tvalid)) {
-            atomicAdd(a.trace_sum + (long long)cur_f * a.trace_stride, tsum);
-            atomicAdd(a.trace_valid + (long long)cur_f * a.trace_stride, tvalid);
-        }
-    }
+    flush(f);  // partial frame (no-op when nothing accumulated)
 }
 
 __global__ void k_interpolate(const int32_t* __restrict__ lookup, const double* __restrict__ planes,
@@ -446,22 +486,61 @@ namespace {
 // Persistent bulk-copy launch: as many CTAs per SM as registers and shared
 // memory allow (queried once per instantiation).
 template <bool LAST, int SPAN>
-void launch_bulk(const RefineArgs& a, const CostTables& tab, unsigned magic_cell, unsigned magic_w,
-                 int tpf, long long total, cudaStream_t st) {
-    static int sms = 0, per_sm = 0;
-    const size_t smem = size_t(kStages) * kStageBytes;
+int launch_bulk(const RefineArgs& a0, const CostTables& tab, unsigned magic_cell31, unsigned magic_w,
+                cudaStream_t st) {
+    static int sms = 0;
+    static int per_sm[kMaxHalo / 4 + 1] = {};
+    BulkGeom bg{};
+    const long long P = a0.g.pixels;
+    bg.tiles_per_frame = int((P + kTile - 1) / kTile);
+    bg.halo = (int(a0.max_disp) + 3) & ~3;
+    bg.stage_bytes = 9 * kTile + 4 * (kTile + bg.halo);
+    bg.q_tile = kTile / a0.g.width;
+    bg.r_tile = kTile % a0.g.width;
+    const size_t smem = size_t(kStages) * bg.stage_bytes;
     if (sms == 0) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaFuncSetAttribute(k_refine_bulk<LAST, true, SPAN>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_refine_bulk<LAST, true, SPAN>, 256,
-                                                      smem);
-        per_sm = std::max(1, per_sm);
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(size_t(kStages) * (9 * kTile + 4 * (kTile + kMaxHalo))));
     }
-    const unsigned blocks = unsigned(std::min<long long>(total, (long long)per_sm * sms));
-    k_refine_bulk<LAST, true, SPAN><<<blocks, 256, smem, st>>>(a, tab, magic_cell, magic_w, tpf, total);
+    int& occ = per_sm[bg.halo / 4];
+    if (occ == 0) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_refine_bulk<LAST, true, SPAN>, 256, smem);
+        occ = std::max(1, occ);
+    }
+    // the kernel indexes the batch with 32-bit pixel offsets: launch per
+    // chunk of frames holding < 2^31 pixels
+    const int chunk = int(std::max<long long>(1, ((1ll << 31) - 1) / P));
+    int launches = 0;
+    for (int f0 = 0; f0 < a0.frames; f0 += chunk) {
+        RefineArgs a = a0;
+        const long long px = (long long)f0 * P;
+        a.frames = std::min(chunk, a0.frames - f0);
+        a.mask = a0.mask ? a0.mask + px : nullptr;
+        a.dit += px;
+        a.cl += px;
+        a.cr += px;
+        a.code += px;
+        a.Df += px;
+        a.Cg += (long long)f0 * a0.cell_stride;
+        a.Cb += (long long)f0 * a0.cell_stride;
+        a.trace_sum += (long long)f0 * a0.trace_stride;
+        a.trace_valid += (long long)f0 * a0.trace_stride;
+        if (LAST) {
+            a.Dv += px;
+            a.Cf += px;
+            a.dense += px;
+            a.dense_valid += px;
+        }
+        bg.total_tiles = bg.tiles_per_frame * a.frames;
+        const unsigned blocks = unsigned(std::min<long long>(bg.total_tiles, (long long)occ * sms));
+        k_refine_bulk<LAST, true, SPAN><<<blocks, 256, smem, st>>>(a, tab, magic_cell31, magic_w, bg);
+        ++launches;
+    }
+    return launches;
 }
 }  // namespace
 
@@ -472,32 +551,30 @@ int launch_refine(const RefineArgs& a, const CostTables& tab, bool last, cudaStr
     const float inv_cell = 1.0f / float(a.cell), inv_w = 1.0f / float(a.g.width);
     const bool key32 = a.g.pixels <= (1ll << kIdxBits);
     if (a.g.pixels % 16 == 0 && key32 && a.g.width >= 32 && a.g.width + kTile < (1 << 16) &&
-        a.g.height < (1 << 16) && a.cell < (1 << 16)) {
+        a.g.height < (1 << 16) && a.cell < (1 << 15) && a.max_disp >= 0.0f &&
+        a.max_disp <= float(kMaxHalo)) {
         // exact 16-bit magic reciprocals for the row / cell divisions (mdiv)
         const unsigned magic_w = unsigned((0x100000000ull + a.g.width - 1) / a.g.width);
-        const unsigned magic_cell = unsigned((0x100000000ull + a.cell - 1) / a.cell);
-        const int tpf = int((a.g.pixels + kTile - 1) / kTile);
-        const long long total = (long long)tpf * a.frames;
+        const unsigned magic_cell = unsigned((0x80000000ull + a.cell - 1) / a.cell);  // 2^31 / cell
         // longest run of equal cells inside a 32-pixel slot, rounded up to 2^n
         const int cols = (a.g.width + a.cell - 1) / a.cell;
         const int run = cols == 1 ? 32 : std::min(a.cell, 32);
         int span = 1;
         while (span < run) span <<= 1;
         switch (span * 2 + (last ? 1 : 0)) {
-            case 2: launch_bulk<false, 1>(a, tab, magic_cell, magic_w, tpf, total, st); break;
-            case 3: launch_bulk<true, 1>(a, tab, magic_cell, magic_w, tpf, total, st); break;
-            case 4: launch_bulk<false, 2>(a, tab, magic_cell, magic_w, tpf, total, st); break;
-            case 5: launch_bulk<true, 2>(a, tab, magic_cell, magic_w, tpf, total, st); break;
-            case 8: launch_bulk<false, 4>(a, tab, magic_cell, magic_w, tpf, total, st); break;
-            case 9: launch_bulk<true, 4>(a, tab, magic_cell, magic_w, tpf, total, st); break;
-            case 16: launch_bulk<false, 8>(a, tab, magic_cell, magic_w, tpf, total, st); break;
-            case 17: launch_bulk<true, 8>(a, tab, magic_cell, magic_w, tpf, total, st); break;
-            case 32: launch_bulk<false, 16>(a, tab, magic_cell, magic_w, tpf, total, st); break;
-            case 33: launch_bulk<true, 16>(a, tab, magic_cell, magic_w, tpf, total, st); break;
-            case 64: launch_bulk<false, 32>(a, tab, magic_cell, magic_w, tpf, total, st); break;
-            default: launch_bulk<true, 32>(a, tab, magic_cell, magic_w, tpf, total, st); break;
+            case 2: return launch_bulk<false, 1>(a, tab, magic_cell, magic_w, st);
+            case 3: return launch_bulk<true, 1>(a, tab, magic_cell, magic_w, st);
+            case 4: return launch_bulk<false, 2>(a, tab, magic_cell, magic_w, st);
+            case 5: return launch_bulk<true, 2>(a, tab, magic_cell, magic_w, st);
+            case 8: return launch_bulk<false, 4>(a, tab, magic_cell, magic_w, st);
+            case 9: return launch_bulk<true, 4>(a, tab, magic_cell, magic_w, st);
+            case 16: return launch_bulk<false, 8>(a, tab, magic_cell, magic_w, st);
+            case 17: return launch_bulk<true, 8>(a, tab, magic_cell, magic_w, st);
+            case 32: return launch_bulk<false, 16>(a, tab, magic_cell, magic_w, st);
+            case 33: return launch_bulk<true, 16>(a, tab, magic_cell, magic_w, st);
+            case 64: return launch_bulk<false, 32>(a, tab, magic_cell, magic_w, st);
+            default: return launch_bulk<true, 32>(a, tab, magic_cell, magic_w, st);
         }
-        return 1;
     }
     if (last) {
         if (key32) k_refine<true, true><<<grid, 256, 0, st>>>(a, tab, inv_cell, inv_w);
