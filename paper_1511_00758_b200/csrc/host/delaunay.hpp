@@ -15,12 +15,20 @@
 
 namespace ps {
 
+// One triangle slot of the lexicographic sweep (delaunay_lex.cpp).
+struct alignas(32) LexTri {
+    int v[3];
+    int n[3];
+    int pad[2];
+};
+
 struct DelaunayWorkspace {
     std::vector<uint64_t> key, key_tmp;
     std::vector<int> ord, ord_tmp;
     std::vector<int> kept;
     std::vector<int> px, py;
-    std::vector<int> tv, tn;  // triangle vertices / neighbour half-edges
+    std::vector<int> tv, tn;  // triangle vertices / neighbour half-edges (radial sweep)
+    std::vector<LexTri> lex;  // triangle slots (lexicographic sweep)
     std::vector<int> hnext, hprev, hedge;
     std::vector<int> stack;
     std::vector<uint8_t> covered;  // mesh_pins scratch

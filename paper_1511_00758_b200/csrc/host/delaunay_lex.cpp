@@ -10,12 +10,11 @@
 // (a,d,c)+(d,b,c).  Checked array-for-array against the compiled reference
 // (tests/test_delaunay.py).
 //
-// The order only matters for one thing downstream: an uncovered hull vertex
-// pixel takes its FIRST incident triangle (mesh.cpp:109-122), and when the
-// incident planes evaluate to different floats at that vertex (a vertex at
-// d = 0, plane value +-1e-17) the choice decides validity.  The engine uses the
-// fast radial sweep and falls back to this order only for such frames
-// (pin_ambiguous()).  It is also the order of the public ps_delaunay().
+// The order matters downstream in two places: an uncovered hull vertex pixel
+// takes its FIRST incident triangle (mesh.cpp:109-122), and fitPlane's binary64
+// rounding depends on the vertex rotation (the plane offset is anchored at the
+// first vertex).  The engine therefore always triangulates with this sweep;
+// it is also the order of the public ps_delaunay().
 #include <cstdlib>
 
 #include "delaunay.hpp"
@@ -24,19 +23,23 @@ namespace ps {
 
 namespace {
 
-inline int lnext(int e) { return (e % 3 == 2) ? e - 2 : e + 1; }
+// Half-edge e = 4 * slot + k (k = 0..2): one 32-byte record per triangle slot
+// holds its vertices and neighbour half-edges (one cache line per flip side).
+inline int lnext(int e) { return (e & 3) == 2 ? e - 2 : e + 1; }
 
 struct LexSweep {
     const int* x;
     const int* y;
-    int* tv;
-    int* tn;
+    LexTri* T;
     int* hnext;
     int* hprev;
     int* hedge;
     std::vector<int>* stack;
     int ntri = 0;
     bool wide = false;
+
+    int& V(int e) const { return T[e >> 2].v[e & 3]; }
+    int& N(int e) const { return T[e >> 2].n[e & 3]; }
 
     long long orient(int a, int b, int c) const {
         const long long abx = (long long)x[b] - x[a], aby = (long long)y[b] - y[a];
@@ -61,16 +64,17 @@ struct LexSweep {
     }
 
     int add(int a, int b, int c, int na, int nb, int nc) {
-        const int e = 3 * ntri++;
-        tv[e] = a;
-        tv[e + 1] = b;
-        tv[e + 2] = c;
-        tn[e] = na;
-        tn[e + 1] = nb;
-        tn[e + 2] = nc;
-        if (na >= 0) tn[na] = e;
-        if (nb >= 0) tn[nb] = e + 1;
-        if (nc >= 0) tn[nc] = e + 2;
+        const int e = 4 * ntri;
+        LexTri& r = T[ntri++];
+        r.v[0] = a;
+        r.v[1] = b;
+        r.v[2] = c;
+        r.n[0] = na;
+        r.n[1] = nb;
+        r.n[2] = nc;
+        if (na >= 0) N(na) = e;
+        if (nb >= 0) N(nb) = e + 1;
+        if (nc >= 0) N(nc) = e + 2;
         return e;
     }
 
@@ -83,26 +87,25 @@ struct LexSweep {
         while (!stack->empty()) {
             const int e = stack->back();
             stack->pop_back();
-            const int f = tn[e];
+            const int f = N(e);
             if (f < 0) continue;
             const int e1 = lnext(e), e2 = lnext(e1);
             const int f1 = lnext(f), f2 = lnext(f1);
-            const int a = tv[e], b = tv[e1], c = tv[e2], d = tv[f2];
+            const int a = V(e), b = V(e1), c = V(e2), d = V(f2);
             if (!inside(a, b, c, d)) continue;  // strict: cocircular never flips
-            const int ne1 = tn[e1], ne2 = tn[e2], nf1 = tn[f1], nf2 = tn[f2];
-            tv[e1] = d;
-            tv[f] = d;
-            tv[f1] = b;
-            tv[f2] = c;
-            tn[e] = nf1;
-            if (nf1 >= 0) tn[nf1] = e; else hedge[a] = e;
-            tn[e1] = f2;
-            tn[f2] = e1;
-            tn[e2] = ne2;
-            tn[f] = nf2;
-            if (nf2 >= 0) tn[nf2] = f; else hedge[d] = f;
-            tn[f1] = ne1;
-            if (ne1 >= 0) tn[ne1] = f1; else hedge[b] = f1;
+            const int ne1 = N(e1), nf1 = N(f1), nf2 = N(f2);
+            V(e1) = d;
+            V(f) = d;
+            V(f1) = b;
+            V(f2) = c;
+            N(e) = nf1;
+            if (nf1 >= 0) N(nf1) = e; else hedge[a] = e;
+            N(e1) = f2;
+            N(f2) = e1;
+            N(f) = nf2;
+            if (nf2 >= 0) N(nf2) = f; else hedge[d] = f;
+            N(f1) = ne1;
+            if (ne1 >= 0) N(ne1) = f1; else hedge[b] = f1;
             // edges incident to the new point (f1, e2) are locally Delaunay
             // and never flip; only the two opposite edges are re-examined
             stack->push_back(e);
@@ -165,13 +168,12 @@ int delaunay_lex(const int* u, const int* v, int n, std::vector<int>& tris,
         ws.px[i] = u[ws.kept[i]];
         ws.py[i] = v[ws.kept[i]];
     }
-    ws.tv.resize(6 * std::size_t(m));
-    ws.tn.resize(6 * std::size_t(m));
+    ws.lex.resize(2 * std::size_t(m));  // T <= 2m - 5
     ws.hnext.assign(m, -1);
     ws.hprev.assign(m, -1);
     ws.hedge.assign(m, -1);
     ws.stack.clear();
-    LexSweep s{ws.px.data(), ws.py.data(), ws.tv.data(), ws.tn.data(), ws.hnext.data(),
+    LexSweep s{ws.px.data(), ws.py.data(), ws.lex.data(), ws.hnext.data(),
                ws.hprev.data(), ws.hedge.data(), &ws.stack};
     s.wide = spanx >= (1 << 14) || spany >= (1 << 14);
 
@@ -207,7 +209,8 @@ int delaunay_lex(const int* u, const int* v, int n, std::vector<int>& tris,
     for (int p = apex + 1; p < m; ++p)
         if (!s.insert(p)) return -2;
     tris.resize(3 * std::size_t(s.ntri));
-    for (int e = 0; e < 3 * s.ntri; ++e) tris[e] = ws.kept[ws.tv[e]];
+    for (int t = 0; t < s.ntri; ++t)
+        for (int k = 0; k < 3; ++k) tris[3 * t + k] = ws.kept[ws.lex[t].v[k]];
     return s.ntri;
 }
 
