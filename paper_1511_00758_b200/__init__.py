@@ -203,22 +203,31 @@ class Context:
         return out
 
     def run_batch(self, left: np.ndarray, right: np.ndarray, config: PipelineConfig,
-                  unchecked_cell: bool = False, raise_on_failure: bool = True) -> dict:
-        """Batched run over frames stacked as (F, H, W) uint8 arrays."""
+                  unchecked_cell: bool = False, raise_on_failure: bool = True,
+                  out: Optional[dict] = None) -> dict:
+        """Batched run over frames stacked as (F, H, W) uint8 arrays.
+
+        `out` may supply the five output arrays (keys disparity,
+        disparity_valid, costs, dense, dense_valid; C-contiguous, right dtype
+        and shape); page-locked ones are filled group by group during the run
+        (streamed D2H, Engine::set_sink)."""
         L = np.ascontiguousarray(left, dtype=np.uint8)
         R = np.ascontiguousarray(right, dtype=np.uint8)
         if L.ndim != 3 or L.shape != R.shape:
             raise DimensionMismatch("expected two (F, H, W) uint8 stacks of equal shape")
         n, h, w = L.shape
         cfg = config.to_c()
-        res = {
-            "disparity": np.zeros((n, h, w), np.float32),
-            "disparity_valid": np.zeros((n, h, w), np.uint8),
-            "costs": np.zeros((n, h, w), np.float32),
-            "dense": np.zeros((n, h, w), np.float32),
-            "dense_valid": np.zeros((n, h, w), np.uint8),
-            "status": np.zeros(n, np.int32),
-        }
+        spec = {"disparity": np.float32, "disparity_valid": np.uint8, "costs": np.float32,
+                "dense": np.float32, "dense_valid": np.uint8}
+        res = {}
+        for key, dt in spec.items():
+            a = (out or {}).get(key)
+            if a is None:
+                a = np.zeros((n, h, w), dt)
+            elif a.dtype != dt or a.shape != (n, h, w) or not a.flags["C_CONTIGUOUS"]:
+                raise ValueError(f"out[{key!r}] must be a C-contiguous {np.dtype(dt).name} array of shape {(n, h, w)}")
+            res[key] = a
+        res["status"] = np.zeros(n, np.int32)
         trace = (PsIterStats * (n * config.iterations))()
         st = self._lib.ps_run_batch(self._h, n, _ptr(L), _ptr(R), w, h, C.byref(cfg),
                                     PS_RUN_UNCHECKED_CELL if unchecked_cell else 0,

@@ -141,7 +141,10 @@ ps_status ps_run_batch(ps_ctx* ctx, int n_frames, const uint8_t* left, const uin
     if (s != PS_OK) return s;
     s = ps_upload_batch(ctx, n_frames, left, right, width, height);
     if (s != PS_OK) return s;
+    // page-locked destinations are filled group by group during the run
+    ctx->engine->set_sink(disparity, disparity_valid, cost, dense, dense_valid);
     const ps_status run = ctx->engine->run_resident(*cfg, flags);
+    ctx->engine->clear_sink();
     if (run != PS_OK && run != PS_SEEDING_FAILED) return from_engine(ctx, run);
     s = from_engine(ctx, ctx->engine->download(disparity, disparity_valid, cost, dense,
                                                dense_valid, trace, frame_status));

@@ -294,6 +294,7 @@ ps_status Engine::upload(int frames, const uint8_t* left, const uint8_t* right, 
     if (s != PS_OK) return s;
     have_inputs_ = true;
     have_outputs_ = false;
+    streamed_ = false;
     return PS_OK;
 }
 
@@ -471,7 +472,11 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     }
     std::mutex done_m;
     std::condition_variable done_cv;
-    std::atomic<double> dt_ms_sum{0.0};
+    std::atomic<double> dt_ms_sum{0.0}, sweep_ms_sum{0.0}, pins_ms_sum{0.0};
+    auto add_ms = [](std::atomic<double>& acc, double x) {
+        double cur = acc.load();
+        while (!acc.compare_exchange_weak(cur, cur + x)) {}
+    };
 
     // (1) supports added since the group's last iteration -> pinned host staging
     auto fetch_delta = [&](FrameGroup& grp, bool counts) -> ps_status {
@@ -553,10 +558,14 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                     DelaunayWorkspace& w = ws_[worker];
                     // the reference's triangle order and rotation: pins and
                     // fitPlane rounding then match it bit for bit
+                    const double ts0 = now_ms();
                     t = delaunay_lex(hu_[f].data(), hv_[f].data(), ns, htri_[f], w);
+                    const double ts1 = now_ms();
                     if (t > 0)
                         mesh_pins(hu_[f].data(), hv_[f].data(), ns, htri_[f].data(), t, W, H,
                                   w.covered, hpin_[f]);
+                    add_ms(sweep_ms_sum, ts1 - ts0);
+                    add_ms(pins_ms_sum, now_ms() - ts1);
                     if (t < 0 || t > tri_cap) {
                         status_[f] = PS_ERROR;
                         t = 0;
@@ -569,8 +578,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                     }
                 }
                 g2.ntri[i] = t;
-                double cur = dt_ms_sum.load();
-                while (!dt_ms_sum.compare_exchange_weak(cur, cur + (now_ms() - t0))) {}
+                add_ms(dt_ms_sum, now_ms() - t0);
                 if (g2.pending.fetch_sub(1) == 1) {
                     std::lock_guard<std::mutex> lk(done_m);
                     done_cv.notify_all();
@@ -706,6 +714,20 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
             end_kernel(gs);
             std::swap(grp.S, grp.Snext);
         }
+        if (last && sink_.active) {
+            // streamed download of this group's final outputs (download())
+            const size_t b = size_t(f0) * P, cnt = size_t(n) * P;
+            if (sink_.disparity)
+                cudaMemcpyAsync(sink_.disparity + b, dDf + b, cnt * 4, cudaMemcpyDeviceToHost, gs);
+            if (sink_.disparity_valid)
+                cudaMemcpyAsync(sink_.disparity_valid + b, dDv + b, cnt, cudaMemcpyDeviceToHost, gs);
+            if (sink_.cost)
+                cudaMemcpyAsync(sink_.cost + b, dCf + b, cnt * 4, cudaMemcpyDeviceToHost, gs);
+            if (sink_.dense)
+                cudaMemcpyAsync(sink_.dense + b, dDense + b, cnt * 4, cudaMemcpyDeviceToHost, gs);
+            if (sink_.dense_valid)
+                cudaMemcpyAsync(sink_.dense_valid + b, dDenseV + b, cnt, cudaMemcpyDeviceToHost, gs);
+        }
         cudaEventRecord(grp.done_event, gs);
         grp.phase = FrameGroup::kDevice;
         return PS_OK;
@@ -804,6 +826,13 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         KernelStat& dt = stat("host_delaunay");  // ms = per-worker share of the work
         dt.launches += F * iters;
         dt.ms += host_dt_ms;
+        const double workers = double(std::max(1, pool_->size()));
+        KernelStat& sw = stat("host_sweep");  // of which: the lexicographic sweep
+        sw.launches += F * iters;
+        sw.ms += sweep_ms_sum.load() / workers;
+        KernelStat& pn = stat("host_pins");  // of which: hull-vertex pins
+        pn.launches += F * iters;
+        pn.ms += pins_ms_sum.load() / workers;
     }
     if (herr) return fail(PS_DEGENERATE_TRIANGLE, "collinear vertices in a triangle");
     for (int f = 0; f < F; ++f) {
@@ -834,6 +863,8 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         }
     }
     have_outputs_ = true;
+    streamed_ = sink_.active;
+    done_sink_ = sink_;
     for (int f = 0; f < F; ++f)
         if (status_[f] != PS_OK)
             return fail(ps_status(status_[f]), "only " + std::to_string(hS[f]) +
@@ -847,6 +878,15 @@ ps_status Engine::download(float* disparity, uint8_t* disparity_valid, float* co
     cudaSetDevice(device_);
     const size_t n = size_t(F_) * P_;
     ps_status s = PS_OK;
+    if (streamed_) {
+        // run_resident() already copied into the sink buffers; a different
+        // destination gets its own copy
+        if (disparity == done_sink_.disparity) disparity = nullptr;
+        if (disparity_valid == done_sink_.disparity_valid) disparity_valid = nullptr;
+        if (cost == done_sink_.cost) cost = nullptr;
+        if (dense == done_sink_.dense) dense = nullptr;
+        if (dense_valid == done_sink_.dense_valid) dense_valid = nullptr;
+    }
     if (disparity && s == PS_OK)
         s = check(cudaMemcpyAsync(disparity, dDf_.p, n * 4, cudaMemcpyDeviceToHost, st_), "D2H disparity");
     if (disparity_valid && s == PS_OK)
@@ -859,6 +899,13 @@ ps_status Engine::download(float* disparity, uint8_t* disparity_valid, float* co
         s = check(cudaMemcpyAsync(dense_valid, dDenseV_.p, n, cudaMemcpyDeviceToHost, st_), "D2H dense validity");
     if (s == PS_OK) s = sync("download");
     if (s != PS_OK) return s;
+    if (streamed_) {
+        if (!disparity) disparity = done_sink_.disparity;
+        if (!disparity_valid) disparity_valid = done_sink_.disparity_valid;
+        if (!cost) cost = done_sink_.cost;
+        if (!dense) dense = done_sink_.dense;
+        if (!dense_valid) dense_valid = done_sink_.dense_valid;
+    }
     for (int f = 0; f < F_; ++f) {
         if (frame_status) frame_status[f] = status_[f];
         if (status_[f] == PS_OK) continue;
@@ -872,6 +919,27 @@ ps_status Engine::download(float* disparity, uint8_t* disparity_valid, float* co
     }
     if (trace) std::copy(trace_.begin(), trace_.end(), trace);
     return PS_OK;
+}
+
+namespace {
+bool page_locked(const void* p) {
+    if (!p) return true;
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+}  // namespace
+
+void Engine::set_sink(float* disparity, uint8_t* disparity_valid, float* cost, float* dense,
+                      uint8_t* dense_valid) {
+    sink_ = Sink{disparity, disparity_valid, cost, dense, dense_valid, false};
+    sink_.active = (disparity || disparity_valid || cost || dense || dense_valid) &&
+                   page_locked(disparity) && page_locked(disparity_valid) && page_locked(cost) &&
+                   page_locked(dense) && page_locked(dense_valid);
+    if (!sink_.active) sink_ = Sink{};
 }
 
 ps_status Engine::supports(int frame, int* u, int* v, double* d, int capacity, int* count) {

@@ -75,6 +75,14 @@ public:
                            void* user = nullptr);
     ps_status download(float* disparity, uint8_t* disparity_valid, float* cost, float* dense,
                        uint8_t* dense_valid, ps_iter_stats* trace, int* frame_status);
+    // Streamed download: with a sink set, run_resident() copies each frame
+    // group's outputs to these (page-locked) host buffers on the group's
+    // stream as soon as its last iteration is launched, overlapping the D2H
+    // with the other groups' work; download() then only fixes up failed
+    // frames and copies the trace.  Pageable buffers are not streamed.
+    void set_sink(float* disparity, uint8_t* disparity_valid, float* cost, float* dense,
+                  uint8_t* dense_valid);
+    void clear_sink() { sink_ = Sink{}; }
     ps_status supports(int frame, int* u, int* v, double* d, int capacity, int* count);
 
     void set_profiling(bool on) { profiling_ = on; }
@@ -109,6 +117,18 @@ private:
         err_ = msg;
         return s;
     }
+
+    struct Sink {
+        float* disparity = nullptr;
+        uint8_t* disparity_valid = nullptr;
+        float* cost = nullptr;
+        float* dense = nullptr;
+        uint8_t* dense_valid = nullptr;
+        bool active = false;
+    };
+    Sink sink_;
+    Sink done_sink_;         // the sink the last run streamed into
+    bool streamed_ = false;  // the last run already copied its outputs
 
     int device_ = 0;
     cudaStream_t st_ = nullptr;

@@ -116,6 +116,33 @@ def test_batch_with_a_failed_frame(ctx, orc):
     assert res["disparity_valid"][1].sum() == 0
 
 
+def test_streamed_download_into_page_locked_buffers(ctx):
+    """ps_run_batch with page-locked outputs copies each frame group as it
+    finishes (Engine::set_sink); the result equals the end-of-run download,
+    including the zero/costHigh fill of a frame whose seeding failed."""
+    import torch
+
+    c = ps.BASELINE_CONFIGS[2]
+    cfg = ps.baseline_config(2)
+    n = 40  # > 32 frames: several frame groups
+    L, R = ps.synth_batch(n, c["width"], c["height"], c["n_planes"], c["max_disparity"],
+                          c["ground"], c["sigma"], seed=77)
+    L[5] = 128
+    R[5] = 128
+    shape = (n, c["height"], c["width"])
+    out = {k: torch.full(shape, 3, dtype=dt, pin_memory=True).numpy()
+           for k, dt in [("disparity", torch.float32), ("disparity_valid", torch.uint8),
+                         ("costs", torch.float32), ("dense", torch.float32),
+                         ("dense_valid", torch.uint8)]}
+    streamed = ctx.run_batch(L, R, cfg, unchecked_cell=True, raise_on_failure=False, out=out)
+    plain = ctx.run_batch(L, R, cfg, unchecked_cell=True, raise_on_failure=False)
+    assert streamed["status"][5] == 7 and (np.delete(streamed["status"], 5) == 0).all()
+    assert (streamed["status"] == plain["status"]).all()
+    for k in out:
+        assert np.array_equal(streamed[k].view(np.uint8), plain[k].view(np.uint8)), k
+    assert streamed["costs"][5].min() == cfg.costHigh and streamed["disparity_valid"][5].sum() == 0
+
+
 @pytest.mark.parametrize("w,h", [(16, 16), (17, 19), (37, 23), (64, 16), (255, 17)])
 def test_small_and_odd_sizes(ctx, orc, w, h):
     rng = np.random.default_rng(w * 100 + h)
