@@ -50,6 +50,11 @@ int delaunay_lex(const int* u, const int* v, int n, std::vector<int>& tris, Dela
 // Hull-vertex pinning (mesh.cpp:109-122) for this triangle list: pin_bits[t]
 // bit k set when corner k of triangle t is an uncovered vertex pixel whose
 // first incident triangle is t (pins.cpp).
+// The same pin bits for the triangulation delaunay_lex() just left in `ws`
+// (its triangle list, ntri triangles), visiting only hull vertices.
+void lex_hull_pins(const DelaunayWorkspace& ws, int ntri, int width, int height,
+                   std::vector<uint8_t>& pin_bits);
+
 void mesh_pins(const int* u, const int* v, int n, const int* tris, int nt, int width, int height,
                std::vector<uint8_t>& state, std::vector<uint8_t>& pin_bits);
 

@@ -214,4 +214,52 @@ int delaunay_lex(const int* u, const int* v, int n, std::vector<int>& tris,
     return s.ntri;
 }
 
+namespace {
+
+bool tie_accept(int xi, int yi, int xj, int yj) {
+    // edge i->j accepts pixels on it (mesh.cpp:80)
+    return (yj < yi) || (yj == yi && xj > xi);
+}
+
+}  // namespace
+
+// mesh_pins() for the triangulation delaunay_lex() just left in `ws`, from
+// its final half-edge state: only hull vertices can be uncovered by the tie
+// rule (an interior vertex pixel belongs to exactly one of the triangles
+// around it), so only their incident triangles are visited — a walk around
+// each hull vertex from its hull half-edge — instead of all T triangles.
+void lex_hull_pins(const DelaunayWorkspace& ws, int ntri, int width, int height,
+                   std::vector<uint8_t>& pin_bits) {
+    pin_bits.assign(ntri, 0);
+    if (ntri <= 0) return;
+    const LexTri* T = ws.lex.data();
+    auto V = [&](int e) { return T[e >> 2].v[e & 3]; };
+    auto N = [&](int e) { return T[e >> 2].n[e & 3]; };
+    const int* x = ws.px.data();
+    const int* y = ws.py.data();
+    int h = 0;  // the lexicographic minimum is a hull vertex
+    do {
+        bool covered = false;
+        int first = -1, corner = 0;
+        for (int g = ws.hedge[h];;) {  // g: half-edge h -> q, its triangle on the left
+            const int gin = lnext(lnext(g));  // r -> h
+            const int q = V(lnext(g)), r = V(gin);
+            if (tie_accept(x[r], y[r], x[h], y[h]) && tie_accept(x[h], y[h], x[q], y[q])) {
+                covered = true;
+                break;
+            }
+            if (first < 0 || (g >> 2) < first) {
+                first = g >> 2;
+                corner = g & 3;
+            }
+            const int tw = N(gin);
+            if (tw < 0) break;  // r -> h is the incoming hull edge
+            g = tw;
+        }
+        if (!covered && first >= 0 && x[h] >= 0 && x[h] < width && y[h] >= 0 && y[h] < height)
+            pin_bits[first] |= uint8_t(1u << corner);
+        h = ws.hnext[h];
+    } while (h != 0);
+}
+
 }  // namespace ps

@@ -561,9 +561,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                     const double ts0 = now_ms();
                     t = delaunay_lex(hu_[f].data(), hv_[f].data(), ns, htri_[f], w);
                     const double ts1 = now_ms();
-                    if (t > 0)
-                        mesh_pins(hu_[f].data(), hv_[f].data(), ns, htri_[f].data(), t, W, H,
-                                  w.covered, hpin_[f]);
+                    if (t > 0) lex_hull_pins(w, t, W, H, hpin_[f]);  // == mesh_pins()
                     add_ms(sweep_ms_sum, ts1 - ts0);
                     add_ms(pins_ms_sum, now_ms() - ts1);
                     if (t < 0 || t > tri_cap) {

@@ -179,3 +179,17 @@ def test_pipeline_support_sets_equal_reference(orc):
         want = orc.delaunay(u, v)
         assert canon(fast(u, v)) == canon(want), name
         assert np.array_equal(tri(u, v), want), name
+
+
+def test_hull_pins_equal_all_triangle_pins():
+    """The engine's hull-vertex pin walk (lex_hull_pins) equals mesh_pins over
+    every triangle (tests/cpp/test_pins.cpp, 3000 random and lattice sets)."""
+    import os
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run(["make", "-s", "-C", os.path.join(root, "tests", "cpp")], check=True)
+    out = subprocess.run([os.path.join(root, "tests", "cpp", "_build", "test_pins")],
+                         capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "mismatches 0" in out.stdout
