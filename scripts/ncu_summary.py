@@ -26,7 +26,7 @@ for r in rows:
 tot = sum(v[1] for v in agg.values())
 lines = [f"# ncu launch list ({tag})", "",
          f"Source: `{os.path.basename(launch_csv)}` — `ncu --metrics gpu__time_duration.sum --clock-control none` over "
-         "`python bench.py --steps 2 --warmup 1 --frames 64 --no-cpu-baseline` (cold-cache, serialised: compare shares).", "",
+         f"`{os.environ.get('NCU_CMD', 'python bench.py --steps 1 --warmup 3 --no-cpu-baseline')}` (cold-cache, serialised: compare shares).", "",
          "| kernel | launches | total us | share |", "|---|---:|---:|---:|"]
 for k, v in sorted(agg.items(), key=lambda x: -x[1][1]):
     lines.append(f"| `{k}` | {v[0]} | {v[1]:.1f} | {v[1] / tot * 100:.1f}% |")
@@ -47,11 +47,11 @@ traffic = {}
 for row in r[2:]:
     lines.append("| " + " | ".join(row[i].replace("|", "/")[:60] for i in idx) + " |")
     name = row[h.index("Kernel Name")]
-    rd = float(row[h.index("dram__bytes_read.sum")]); wr = float(row[h.index("dram__bytes_write.sum")])
-    unit = units[h.index("dram__bytes_read.sum")]
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    rd = float(row[h.index("dram__bytes_read.sum")]) * scale.get(units[h.index("dram__bytes_read.sum")], 1)
+    wr = float(row[h.index("dram__bytes_write.sum")]) * scale.get(units[h.index("dram__bytes_write.sum")], 1)
     key = "k_refine" if "k_refine" in name else ("k_raster" if "k_raster" in name else name[:40])
-    traffic.setdefault(key, []).append((rd + wr) * scale)
+    traffic.setdefault(key, []).append(rd + wr)
 open(os.path.join(out_dir, f"ncu_{tag}.md"), "w").write("\n".join(lines) + "\n")
 json.dump({k: sum(v) / len(v) for k, v in traffic.items()}, open(os.path.join(out_dir, "ncu_traffic.json"), "w"), indent=1)
 print("\n".join(lines))
