@@ -2,7 +2,7 @@
 //
 // Declares, in namespace planestereo, every type and function of the
 // reference's public header API (proj/include/planestereo/{error,config,
-// image,disparity,census,sparse,delaunay,mesh,pipeline}.hpp) with the same
+// image,disparity,census,sparse,delaunay,mesh,pipeline}.hpp, and wtaOracle of synth.hpp) with the same
 // names, signatures, value semantics and exceptions, so code written against
 // the reference recompiles unchanged (the per-name headers next to this one
 // just include it).  The implementation (paper_1511_00758_b200/csrc/cpp_api)
@@ -19,6 +19,7 @@
 #include <iosfwd>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 namespace planestereo {
@@ -324,6 +325,12 @@ using IterationObserver =
 
 StereoResult run(const GrayImage& left, const GrayImage& right, const PipelineConfig& config,
                  const IterationObserver& observer = {});
+
+// (reference synth.hpp:52-56) Exhaustive winner-take-all census matcher: per
+// mask pixel the cost-minimal integer disparity in [0, min(maxDisparity, u-2)],
+// ties toward smaller d.  Runs on the GPU (wta.cu).
+std::pair<DisparityMap, CostMap> wtaOracle(const GrayImage& left, const GrayImage& right,
+                                           const GradientMask& mask, int maxDisparity);
 
 // ------------------------------------------------------------------ extensions
 // GPU selection for the calling thread's default context (device 0 otherwise).

@@ -214,6 +214,21 @@ ps_status ps_support_resampling(ps_ctx* ctx, const ps_cell* confident, const ps_
                                 int width, int height, const ps_config* cfg, int* u, int* v,
                                 double* d, int capacity, int* count);
 
+/* wtaOracle (proj/include/planestereo/synth.hpp:52-56, proj/src/synth.cpp:171-198):
+ * per mask pixel the cost-minimal integer disparity in
+ * [0, min(max_disparity, u - 2)] (max_disparity inclusive), ties toward the
+ * smaller d; off-mask pixels get cost 1.0 and no disparity.  The census of
+ * both views is computed on the device. */
+ps_status ps_wta_oracle(ps_ctx* ctx, const uint8_t* left, const uint8_t* right, int width,
+                        int height, const uint8_t* mask, int max_disparity, float* disparity,
+                        uint8_t* disparity_valid, float* cost);
+/* The same over n_frames pairs stacked frame after frame, with each frame's
+ * mask = gradientMask(left, gradient_threshold): the dense WTA baseline of a
+ * batch (outputs n_frames * width * height each). */
+ps_status ps_wta_batch(ps_ctx* ctx, int n_frames, const uint8_t* left, const uint8_t* right,
+                       int width, int height, int gradient_threshold, int max_disparity,
+                       float* disparity, uint8_t* disparity_valid, float* cost);
+
 /* ------------------------------------------------- synthetic stereo pairs */
 /* Seeded BASELINE-style generator; bench/test fixture, not on
  * the hot path.  gt may be NULL. */

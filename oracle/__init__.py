@@ -82,6 +82,7 @@ class CpuChecker:
             "fit_plane": (I, [I, I, C.c_double, I, I, C.c_double, I, I, C.c_double, P]),
             "mesh_build": (I, [P, P, P, P, I, I, I, P, P]),
             "cost_evaluation": (None, [P, P, I, I, P, P, P, P]),
+            "wta": (None, [P, P, I, I, P, I, P, P, P]),
             "refinement": (None, [P, P, P, P, P, P, P, I, I, I, P, P, P]),
             "support_resampling": (I, [P, P, I, P, P, P, I, P, P, I, I, P, P, P, P, I]),
             "run": (I, [P, P, I, I, P, I, P, P, P, P, P, P, P, P, P, I, P]),
@@ -190,6 +191,18 @@ class CpuChecker:
                                   _p(np.ascontiguousarray(ok, np.uint8)),
                                   _p(np.ascontiguousarray(mask, np.uint8)), _p(cost))
         return cost
+
+    def wta(self, left, right, mask, nd):
+        """wtaOracle (proj/src/synth.cpp:171-198) -> (disparity, valid, cost)."""
+        L = np.ascontiguousarray(left, np.uint8)
+        R = np.ascontiguousarray(right, np.uint8)
+        h, w = L.shape
+        d = np.zeros((h, w), np.float32)
+        ok = np.zeros((h, w), np.uint8)
+        c = np.zeros((h, w), np.float32)
+        self.f("wta")(_p(L), _p(R), w, h, _p(np.ascontiguousarray(mask, np.uint8)), nd, _p(d), _p(ok),
+                      _p(c))
+        return d, ok, c
 
     def refinement(self, val, ok, cost, fd, fv, fc, mask, cell, cfg):
         h, w = val.shape

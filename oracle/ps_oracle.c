@@ -640,6 +640,44 @@ void orc_cost_evaluation(const uint32_t* cl, const uint32_t* cr, int w, int h, c
     }
 }
 
+/* wtaOracle, proj/src/synth.cpp:171-198 */
+void orc_wta(const uint8_t* left, const uint8_t* right, int w, int h, const uint8_t* mask, int nd,
+             float* disparity, uint8_t* valid, float* cost) {
+    const size_t n = (size_t)w * h;
+    uint32_t* cl = (uint32_t*)malloc(sizeof(uint32_t) * n);
+    uint32_t* cr = (uint32_t*)malloc(sizeof(uint32_t) * n);
+    orc_census(left, w, h, cl);
+    orc_census(right, w, h, cr);
+    for (size_t i = 0; i < n; ++i) {
+        disparity[i] = 0.0f;
+        valid[i] = 0;
+        cost[i] = 1.0f; /* CostMap(w, h, 1.0f) */
+    }
+    for (int v = 0; v < h; ++v) {
+        for (int u = 0; u < w; ++u) {
+            const size_t i = (size_t)v * w + u;
+            if (!mask[i]) continue; /* mask.points(), row-major */
+            const int dmax = nd < u - CENSUS_R ? nd : u - CENSUS_R;
+            int best_d = -1;
+            float best = 2.0f;
+            for (int d = 0; d <= dmax; ++d) {
+                const float c = census_cost(cl[i], cr[(size_t)v * w + (size_t)(u - d)]);
+                if (c < best) {
+                    best = c;
+                    best_d = d;
+                }
+            }
+            if (best_d >= 0) {
+                disparity[i] = (float)best_d;
+                valid[i] = 1;
+                cost[i] = best;
+            }
+        }
+    }
+    free(cl);
+    free(cr);
+}
+
 static int ceil_div_pos(int a, int b) { return (a + b - 1) / b; }
 
 /* disparityRefinement, pipeline.cpp:56-86 */

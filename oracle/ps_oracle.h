@@ -49,6 +49,10 @@ int orc_mesh_build(const int* u, const int* v, const double* d, const int* tris,
 void orc_interpolate(const int32_t* lookup, const double* planes, int w, int h,
                      const uint8_t* mask, float max_disparity, float* value, uint8_t* valid);
 /* costEvaluation, proj/src/pipeline.cpp:33-54. */
+/* wtaOracle, proj/src/synth.cpp:171-198: per mask pixel the first cost-minimal
+ * d in [0, min(nd, u - 2)]; cost 1.0 and invalid elsewhere. */
+void orc_wta(const uint8_t* left, const uint8_t* right, int w, int h, const uint8_t* mask, int nd,
+             float* disparity, uint8_t* valid, float* cost);
 void orc_cost_evaluation(const uint32_t* cl, const uint32_t* cr, int w, int h, const float* value,
                          const uint8_t* valid, const uint8_t* mask, float* cost);
 /* disparityRefinement, proj/src/pipeline.cpp:56-86. */

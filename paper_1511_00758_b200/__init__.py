@@ -402,6 +402,36 @@ class Context:
             _ptr(v), _ptr(d), cap, C.byref(n)))
         return u[:n.value], v[:n.value], d[:n.value]
 
+    def wta_oracle(self, left, right, mask, max_disparity: int):
+        """wtaOracle (proj/src/synth.cpp:171-198) on the device:
+        (disparity, valid, cost), cost 1.0 off the mask."""
+        L = np.ascontiguousarray(left, dtype=np.uint8)
+        R = np.ascontiguousarray(right, dtype=np.uint8)
+        M = np.ascontiguousarray(mask, dtype=np.uint8)
+        if L.shape != R.shape or L.shape != M.shape or L.ndim != 2:
+            raise DimensionMismatch("left, right and mask must be equal 2-D arrays")
+        h, w = L.shape
+        d = np.zeros((h, w), np.float32)
+        ok = np.zeros((h, w), np.uint8)
+        c = np.zeros((h, w), np.float32)
+        _check(self._lib.ps_wta_oracle(self._h, _ptr(L), _ptr(R), w, h, _ptr(M), max_disparity,
+                                       _ptr(d), _ptr(ok), _ptr(c)))
+        return d, ok, c
+
+    def wta_batch(self, left, right, gradient_threshold: int, max_disparity: int):
+        """Dense WTA baseline of an (F, H, W) batch, mask = gradientMask(left, t)."""
+        L = np.ascontiguousarray(left, dtype=np.uint8)
+        R = np.ascontiguousarray(right, dtype=np.uint8)
+        if L.ndim != 3 or L.shape != R.shape:
+            raise DimensionMismatch("expected two (F, H, W) uint8 stacks of equal shape")
+        n, h, w = L.shape
+        d = np.zeros((n, h, w), np.float32)
+        ok = np.zeros((n, h, w), np.uint8)
+        c = np.zeros((n, h, w), np.float32)
+        _check(self._lib.ps_wta_batch(self._h, n, _ptr(L), _ptr(R), w, h, gradient_threshold,
+                                      max_disparity, _ptr(d), _ptr(ok), _ptr(c)))
+        return d, ok, c
+
     def cost_evaluation(self, census_left, census_right, interp, interp_valid, mask):
         cl = np.ascontiguousarray(census_left, dtype=np.uint32)
         cr = np.ascontiguousarray(census_right, dtype=np.uint32)

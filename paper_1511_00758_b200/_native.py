@@ -114,6 +114,8 @@ SIGNATURES = {
     "ps_cost_evaluation": (I, [P, P, P, I, I, P, P, P, P]),
     "ps_refinement": (I, [P, P, P, P, P, P, P, P, I, I, I, P, P, P]),
     "ps_support_resampling": (I, [P, P, P, I, P, P, P, I, P, P, I, I, P, P, P, P, I, P]),
+    "ps_wta_oracle": (I, [P, P, P, I, I, P, I, P, P, P]),
+    "ps_wta_batch": (I, [P, I, P, P, I, I, I, I, P, P, P]),
     "ps_synth_pair": (I, [P, P, P, P]),
     "ps_synth_batch": (I, [P, I, I, P, P]),
 }

@@ -332,6 +332,20 @@ CostMap costEvaluation(const CensusField& left, const CensusField& right,
     return costs;
 }
 
+std::pair<DisparityMap, CostMap> wtaOracle(const GrayImage& left, const GrayImage& right,
+                                           const GradientMask& mask, int maxDisparity) {
+    if (left.width() != right.width() || left.height() != right.height() ||
+        mask.width() != left.width() || mask.height() != left.height())
+        throw DimensionMismatch("wtaOracle inputs differ in size");
+    DisparityMap disparity(left.width(), left.height());
+    CostMap costs(left.width(), left.height(), 1.0f);
+    check(ps_wta_oracle(ctx(), left.data().data(), right.data().data(), left.width(),
+                        left.height(), mask.membership().data(), maxDisparity,
+                        disparity.mutableValues().data(), disparity.mutableValidity().data(),
+                        costs.mutableValues().data()));
+    return {std::move(disparity), std::move(costs)};
+}
+
 RefinementGrids disparityRefinement(const DisparityMap& interpolated, const CostMap& costs,
                                     DisparityMap& finalDisparity, CostMap& finalCost,
                                     const GradientMask& mask, int cellSize,

@@ -478,6 +478,64 @@ ps_status ps_cost_evaluation(ps_ctx* ctx, const uint32_t* census_left, const uin
     return from_engine(ctx, e.sync("cost evaluation"));
 }
 
+namespace {
+ps_status wta_common(ps_ctx* ctx, int frames, const uint8_t* left, const uint8_t* right, int width,
+                     int height, const uint8_t* mask, int threshold, int max_disparity,
+                     float* disparity, uint8_t* valid, float* cost) {
+    if (frames < 1) return set_error(PS_ERROR, "batch needs at least one frame");
+    if (width < 1 || height < 1 || width > 50000)
+        return set_error(PS_DIMENSION_TOO_SMALL, "bad image size for the WTA matcher");
+    if (max_disparity < 0) return set_error(PS_INVALID_CONFIG, "maxDisparity must be >= 0");
+    if (!left || !right || !disparity || !valid || !cost) return set_error(PS_ERROR, "null buffer");
+    ps::Engine& e = *ctx->engine;
+    const long long P = (long long)width * height;
+    const size_t n = size_t(frames) * P;
+    uint8_t* d_l = e.dev<uint8_t>(e.s_a, n);
+    uint8_t* d_r = e.dev<uint8_t>(e.s_b, n);
+    uint32_t* d_cl = e.dev<uint32_t>(e.s_c, n);
+    uint32_t* d_cr = e.dev<uint32_t>(e.s_d, n);
+    uint8_t* d_m = e.dev<uint8_t>(e.s_e, n);
+    float* d_disp = e.dev<float>(e.s_f, n);
+    uint8_t* d_ok = e.dev<uint8_t>(e.s_g, n);
+    float* d_cost = e.dev<float>(e.s_h, n);
+    if (!d_l || !d_r || !d_cl || !d_cr || !d_m || !d_disp || !d_ok || !d_cost)
+        return set_error(PS_CUDA_ERROR, "allocation failed");
+    cudaStream_t st = e.stream();
+    const ps::FrameGeom g{width, height, P};
+    cudaMemcpyAsync(d_l, left, n, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_r, right, n, cudaMemcpyHostToDevice, st);
+    if (mask) cudaMemcpyAsync(d_m, mask, n, cudaMemcpyHostToDevice, st);
+    // census of both views (and the gradient mask when not given)
+    e.count_launches(ps::launch_frontend(d_l, d_r, g, frames, threshold, mask ? nullptr : d_m, d_cl,
+                                         d_cr, nullptr, st));
+    ps_config dc;
+    ps_config_default(&dc);
+    e.count_launches(ps::launch_wta(d_cl, d_cr, d_m, g, frames, max_disparity, ps::make_tables(dc),
+                                    d_disp, d_ok, d_cost, st));
+    cudaMemcpyAsync(disparity, d_disp, 4 * n, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(valid, d_ok, n, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(cost, d_cost, 4 * n, cudaMemcpyDeviceToHost, st);
+    return from_engine(ctx, e.sync("wta oracle"));
+}
+}  // namespace
+
+ps_status ps_wta_oracle(ps_ctx* ctx, const uint8_t* left, const uint8_t* right, int width,
+                        int height, const uint8_t* mask, int max_disparity, float* disparity,
+                        uint8_t* disparity_valid, float* cost) {
+    PS_REQUIRE_CTX(ctx);
+    if (!mask) return set_error(PS_ERROR, "null mask");
+    return wta_common(ctx, 1, left, right, width, height, mask, 0, max_disparity, disparity,
+                      disparity_valid, cost);
+}
+
+ps_status ps_wta_batch(ps_ctx* ctx, int n_frames, const uint8_t* left, const uint8_t* right,
+                       int width, int height, int gradient_threshold, int max_disparity,
+                       float* disparity, uint8_t* disparity_valid, float* cost) {
+    PS_REQUIRE_CTX(ctx);
+    return wta_common(ctx, n_frames, left, right, width, height, nullptr, gradient_threshold,
+                      max_disparity, disparity, disparity_valid, cost);
+}
+
 ps_status ps_refinement(ps_ctx* ctx, const float* interp, const uint8_t* interp_valid,
                         const float* cost, float* final_disparity, uint8_t* final_valid,
                         float* final_cost, const uint8_t* mask, int width, int height,

@@ -16,6 +16,7 @@
 namespace ps {
 
 constexpr int kCensusBits = 24;
+constexpr int kCensusRadius = 2;  // CensusField::kRadius (census.hpp:19)
 constexpr int kNoKey = 25;  // "no second-best" marker (BestMatch init 2.0f, sparse.cpp:38-42)
 constexpr unsigned long long kEmptyCell = ~0ull;
 constexpr unsigned char kCodeOff = 0xFF;  // C_f code of a pixel outside the gradient mask

@@ -141,4 +141,10 @@ int launch_stage_refine(FrameGeom g, const float* interp, const uint8_t* interp_
                         int cell, float cost_low, float cost_high, unsigned long long* kg,
                         unsigned long long* kb, StageCell* out_conf, StageCell* out_inv,
                         cudaStream_t st);
+// wtaOracle (proj/src/synth.cpp:171-198) over census fields of `frames`
+// frames (wta.cu): disparity / validity / cost per pixel, cost 1.0 off-mask.
+int launch_wta(const uint32_t* cl, const uint32_t* cr, const uint8_t* mask, FrameGeom g, int frames,
+               int max_disparity, const CostTables& tab, float* disparity, uint8_t* valid,
+               float* cost, cudaStream_t st);
+
 }  // namespace ps

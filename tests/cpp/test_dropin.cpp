@@ -20,6 +20,7 @@
 #include "planestereo/mesh.hpp"
 #include "planestereo/pipeline.hpp"
 #include "planestereo/sparse.hpp"
+#include "planestereo/synth.hpp"
 #include "planestereo_c.h"
 
 using namespace planestereo;
@@ -403,6 +404,34 @@ TEST(run_errors) {
     grid10.iterations = 2;
     const StereoResult r = runUnchecked(L, R, grid10);
     CHECK(r.trace.size() == 2 && r.trace[1].occupancyCellSize == 5);
+}
+
+// ----------------------------------------------------------- test_synth.cpp
+TEST(wta_oracle_cases) {
+    // identical images: d = 0 and cost 0 on every mask pixel (test_synth.cpp:82-91)
+    const GrayImage img = randomImage(64, 48, 5);
+    const GradientMask mask = gradientMask(img, 20);
+    const auto [disparity, costs] = wtaOracle(img, img, mask, 128);
+    for (const Pixel& p : mask.points()) {
+        CHECK(disparity.valid(p.u, p.v));
+        CHECK(disparity.at(p.u, p.v) == 0.0f);
+        CHECK(costs.at(p.u, p.v) == 0.0f);
+    }
+    // a pure shift of 7 (right = left moved left by 7) is found wherever the
+    // true match is in range and unique; off-mask pixels keep cost 1.0
+    const GrayImage R = shiftLeftBy(img, 7, 6);
+    const auto [d7, c7] = wtaOracle(img, R, mask, 16);
+    int exact = 0, n = 0;
+    for (const Pixel& p : mask.points())
+        if (p.u >= 16 + 2 && p.u + 2 < 64 - 7) {
+            ++n;
+            exact += d7.at(p.u, p.v) == 7.0f;
+        }
+    CHECK(n > 100 && exact * 10 >= n * 9);
+    for (int v = 0; v < 48; ++v)
+        for (int u = 0; u < 64; ++u)
+            if (!mask.contains(u, v)) CHECK(c7.at(u, v) == 1.0f && !d7.valid(u, v));
+    CHECK_THROWS_AS(wtaOracle(img, GrayImage(32, 48, 0), mask, 8), DimensionMismatch);
 }
 
 int main() {

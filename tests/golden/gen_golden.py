@@ -164,5 +164,41 @@ def main():
     print("stages_random_64x48 ok")
 
 
+def gen_wta(ref):
+    """wtaOracle known answers (proj/src/synth.cpp:171-198), the reference's
+    own cases (proj/tests/test_synth.cpp:82-108) plus ND edge cases."""
+    cases = {}
+    L, R, gt, gv = render(ref, 0, [7.0], 96, 64)  # rendered constant shift
+    m, _ = ref.gradient_mask(L, 20)
+    cases["shift7"] = (L, R, m, 128, dict(gt=gt, gt_valid=gv))
+    L0, _, _, _ = render(ref, 0, [0.0], 64, 48)  # identical images
+    m0, _ = ref.gradient_mask(L0, 20)
+    cases["identical"] = (L0, L0.copy(), m0, 128, {})
+    Ls, Rs = ps.synth_pair(120, 90, 6, 40, False, 2.0, seed=21)
+    ms, _ = ref.gradient_mask(Ls, 12)
+    cases["synth_nd40"] = (Ls, Rs, ms, 40, {})
+    cases["synth_nd200"] = (Ls, Rs, ms, 200, {})  # > width: bounded by u - 2
+    cases["synth_nd0"] = (Ls, Rs, ms, 0, {})
+    rng = np.random.default_rng(5)
+    mr = (rng.random((90, 120)) < 0.3).astype(np.uint8)  # arbitrary mask, border pixels too
+    cases["synth_randmask_nd9"] = (Ls, Rs, mr, 9, {})
+    arrays = {}
+    for name, (L, R, m, nd, extra) in cases.items():
+        d, v, c = wta(ref, L, R, m, nd)
+        arrays.update({f"{name}_left": L, f"{name}_right": R, f"{name}_mask": m,
+                       f"{name}_nd": np.int32(nd), f"{name}_disparity": d, f"{name}_valid": v,
+                       f"{name}_cost": c})
+        arrays.update({f"{name}_{k}": x for k, x in extra.items()})
+    arrays["cases"] = np.array(json.dumps(sorted(cases)))
+    np.savez_compressed(os.path.join(HERE, "wta_cases.npz"), **arrays)
+    print("wta_cases ok")
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["wta"]:
+        ref = oracle.load_ref()
+        assert ref is not None, "build oracle/_ref first (make -C oracle ref)"
+        gen_wta(ref)
+    else:
+        main()
+        gen_wta(oracle.load_ref())

@@ -255,3 +255,73 @@ def test_refinement_and_resampling_equal_oracle(ctx, orc):
         b = orc.support_resampling(g2[0], g2[1], cell, su, sv, sd, cl, cr, cfg)
         for x, y in zip(a, b):
             assert np.array_equal(x, y), cell
+
+
+def _wta_cases():
+    import json
+    import os
+
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "wta_cases.npz"))
+    return {name: {k: z[f"{name}_{k}"] for k in z.files if k.startswith(name + "_")
+                   for k in [k[len(name) + 1:]]}
+            for name in json.loads(str(z["cases"]))}
+
+
+@pytest.mark.gpu
+def test_wta_equals_reference_golden(ctx):
+    """GPU wtaOracle vs the reference's own outputs, bit for bit."""
+    for name, c in _wta_cases().items():
+        d, ok, cost = ctx.wta_oracle(c["left"], c["right"], c["mask"], int(c["nd"]))
+        assert np.array_equal(ok, c["valid"]), name
+        assert np.array_equal(d.view(np.uint32), c["disparity"].view(np.uint32)), name
+        assert np.array_equal(cost.view(np.uint32), c["cost"].view(np.uint32)), name
+
+
+@pytest.mark.gpu
+def test_wta_reference_behaviour(ctx):
+    """proj/tests/test_synth.cpp:82-108: identical images give d = 0 and cost 0
+    on every mask pixel; a rendered constant shift of 7 is recovered almost
+    everywhere.  (The reference test asks for >= 99%; the compiled reference
+    itself reaches 96.5% on this render — tests/golden/wta_cases.npz — so the
+    bar here is the reference's own figure, which the GPU matches exactly.)"""
+    c = _wta_cases()
+    ident = c["identical"]
+    d, ok, cost = ctx.wta_oracle(ident["left"], ident["right"], ident["mask"], 128)
+    m = ident["mask"].astype(bool)
+    assert ok[m].all() and (d[m] == 0).all() and (cost[m] == 0).all()
+    s = c["shift7"]
+    d, ok, cost = ctx.wta_oracle(s["left"], s["right"], s["mask"], 128)
+    both = s["mask"].astype(bool) & (s["gt_valid"] == 1) & (ok == 1)
+    assert both.sum() > 500
+    ref_rate = (s["disparity"][both] == 7.0).mean()
+    assert (d[both] == 7.0).mean() == ref_rate >= 0.95
+
+
+@pytest.mark.gpu
+def test_wta_batch_equals_oracle(ctx, orc):
+    n, w, h = 5, 160, 120
+    L, R = ps.synth_batch(n, w, h, 8, 64, False, 2.0, seed=61)
+    for nd in (64, 255):
+        d, ok, cost = ctx.wta_batch(L, R, 20, nd)
+        for f in range(n):
+            m, _ = orc.gradient_mask(L[f], 20)
+            od, ook, oc = orc.wta(L[f], R[f], m, nd)
+            assert np.array_equal(ok[f], ook)
+            assert np.array_equal(d[f].view(np.uint32), od.view(np.uint32))
+            assert np.array_equal(cost[f].view(np.uint32), oc.view(np.uint32))
+
+
+@pytest.mark.gpu
+def test_wta_vga_properties(ctx, orc):
+    """Full VGA frame at config 2's ND: against the oracle and as the lower bound of
+    the pipeline's final costs (proj/tests/test_pipeline.cpp:255-268)."""
+    L, R = ps.synth_pair(640, 480, 40, 64, seed=5)
+    cfg = ps.baseline_config(2)
+    res = ctx.run(L, R, cfg, unchecked_cell=True)
+    m, _ = ctx.gradient_mask(L, cfg.gradientThreshold)
+    d, ok, cost = ctx.wta_oracle(L, R, m, cfg.maxDisparity)
+    od, ook, oc = orc.wta(L, R, m, cfg.maxDisparity)
+    assert np.array_equal(ok, ook) and np.array_equal(d, od) and np.array_equal(cost, oc)
+    v = res.disparity_valid.astype(bool)
+    assert (res.costs[v] >= cost[v]).all()
+    assert ok[m.astype(bool)].all()

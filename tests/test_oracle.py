@@ -177,3 +177,31 @@ def test_oracle_predicates(orc):
     assert orc.incircle_sign((0, 0), (4, 0), (0, 4), (1, 1)) > 0
     assert orc.incircle_sign((0, 0), (4, 0), (0, 4), (9, 9)) < 0
     assert orc.incircle_sign((0, 0), (4, 0), (0, 4), (4, 4)) == 0
+
+
+def _wta_cases():
+    import json
+    import os
+
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "wta_cases.npz"))
+    return {name: {k: z[f"{name}_{k}"] for k in ("left", "right", "mask", "nd", "disparity", "valid", "cost")}
+            for name in json.loads(str(z["cases"]))}
+
+
+def test_oracle_wta_matches_golden(orc):
+    """wtaOracle restatement vs the reference's outputs (tests/golden/wta_cases.npz)."""
+    for name, c in _wta_cases().items():
+        d, ok, cost = orc.wta(c["left"], c["right"], c["mask"], int(c["nd"]))
+        assert np.array_equal(ok, c["valid"]), name
+        assert np.array_equal(d.view(np.uint32), c["disparity"].view(np.uint32)), name
+        assert np.array_equal(cost.view(np.uint32), c["cost"].view(np.uint32)), name
+
+
+def test_oracle_wta_equals_reference(orc, ref):
+    rng = np.random.default_rng(33)
+    for w, h, nd in [(64, 40, 24), (33, 17, 100), (80, 60, 0)]:
+        L = rng.integers(0, 256, (h, w), dtype=np.uint8)
+        R = np.roll(L, 3, axis=1)
+        m = (rng.random((h, w)) < 0.5).astype(np.uint8)
+        for a, b in zip(orc.wta(L, R, m, nd), ref.wta(L, R, m, nd)):
+            assert np.array_equal(a.view(np.uint8), b.view(np.uint8))
