@@ -67,7 +67,10 @@ typedef enum ps_status {
     PS_SEEDING_FAILED = 7,          /* SeedingFailed                       error.hpp:39 */
     PS_CUDA_ERROR = 8,              /* device failure (no reference analogue) */
     PS_NO_DEVICE = 9,               /* no sm_100 device / extension not usable */
-    PS_CAPACITY = 10                /* caller buffer too small (count written) */
+    PS_CAPACITY = 10,               /* caller buffer too small (count written) */
+    PS_NEGATIVE_DISPARITY = 11,     /* NegativeDisparity                   error.hpp:54 */
+    PS_EMPTY_CLOUD = 12,            /* EmptyCloud                          error.hpp:59 */
+    PS_NO_OVERLAP = 13              /* NoOverlap                           error.hpp:64 */
 } ps_status;
 
 /* Run flags. */
@@ -228,6 +231,44 @@ ps_status ps_wta_oracle(ps_ctx* ctx, const uint8_t* left, const uint8_t* right, 
 ps_status ps_wta_batch(ps_ctx* ctx, int n_frames, const uint8_t* left, const uint8_t* right,
                        int width, int height, int gradient_threshold, int max_disparity,
                        float* disparity, uint8_t* disparity_valid, float* cost);
+
+/* ------------------------------------------------------ output encoders */
+/* Rasters of the reference's io module (proj/src/io.cpp), computed on the
+ * device; the file containers (PNG/PFM/PLY headers) are the caller's.
+ *   KITTI 16-bit, writeKittiPng :349-368 — 2 bytes per pixel, row-major, the
+ *     PNG row bytes: big-endian raw = clamp(lround(d*256), 1, 65535), 0 =
+ *     invalid; PS_NEGATIVE_DISPARITY (message names the first one) if a valid
+ *     disparity is negative.
+ *   PFM, writePfm :311-329 — binary32 per pixel, rows bottom-up, invalid -1.0.
+ *   point cloud, exportPointCloud :395-454 — the vertex list: xyz (3 floats)
+ *     and intensity of each valid pixel with d >= min_disparity, row-major;
+ *     PS_EMPTY_CLOUD when there is none, PS_INVALID_CONFIG for a bad calib.
+ * The batch forms encode n_frames maps stacked frame after frame. */
+typedef struct ps_calib { /* CameraCalib, proj/include/planestereo/io.hpp:17-24 */
+    double focal;    /* pixels, > 0 */
+    double baseline; /* meters, > 0 */
+    double cx;
+    double cy;
+} ps_calib;
+ps_status ps_encode_kitti16(ps_ctx* ctx, const float* disparity, const uint8_t* valid, int width,
+                            int height, int n_frames, uint8_t* out);
+ps_status ps_encode_pfm(ps_ctx* ctx, const float* disparity, const uint8_t* valid, int width,
+                        int height, int n_frames, float* out);
+ps_status ps_point_cloud(ps_ctx* ctx, const float* disparity, const uint8_t* valid,
+                         const uint8_t* image, int width, int height, const ps_calib* calib,
+                         double min_disparity, float* xyz, uint8_t* intensity, int capacity,
+                         int* count);
+/* The same over the last run's results in device memory (no map D2H):
+ * which = PS_MAP_DISPARITY (the final disparity) or PS_MAP_DENSE (the dense
+ * interpolation); a frame whose seeding failed encodes as all-invalid.  The
+ * point cloud uses that frame's left image. */
+#define PS_MAP_DISPARITY 0
+#define PS_MAP_DENSE 1
+ps_status ps_download_kitti16(ps_ctx* ctx, int which, uint8_t* out);
+ps_status ps_download_pfm(ps_ctx* ctx, int which, float* out);
+ps_status ps_download_point_cloud(ps_ctx* ctx, int frame, int which, const ps_calib* calib,
+                                  double min_disparity, float* xyz, uint8_t* intensity,
+                                  int capacity, int* count);
 
 /* ------------------------------------------------- synthetic stereo pairs */
 /* Seeded BASELINE-style generator; bench/test fixture, not on

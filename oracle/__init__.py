@@ -63,6 +63,13 @@ def to_cfg(cfg) -> _Cfg:
                 g("perBinCap"), g("sparseAcceptCost"), g("uniquenessRatio"), g("threads"))
 
 
+class _Calib(C.Structure):
+    """ps_calib = CameraCalib (proj/include/planestereo/io.hpp:17-24)."""
+
+    _fields_ = [("focal", C.c_double), ("baseline", C.c_double), ("cx", C.c_double),
+                ("cy", C.c_double)]
+
+
 class CpuChecker:
     """numpy interface over a C library exporting <prefix>_* entry points."""
 
@@ -93,6 +100,12 @@ class CpuChecker:
             fn.restype = res
             fn.argtypes = args
         if prefix == "orc":
+            self.lib.orc_encode_kitti16.restype = C.c_longlong
+            self.lib.orc_encode_kitti16.argtypes = [P, P, I, I, P]
+            self.lib.orc_encode_pfm.restype = None
+            self.lib.orc_encode_pfm.argtypes = [P, P, I, I, P]
+            self.lib.orc_point_cloud.restype = I
+            self.lib.orc_point_cloud.argtypes = [P, P, P, I, I, P, C.c_double, P, P]
             self.lib.orc_interpolate.restype = None
             self.lib.orc_interpolate.argtypes = [P, P, I, I, P, C.c_float, P, P]
         if prefix == "ref":
@@ -191,6 +204,32 @@ class CpuChecker:
                                   _p(np.ascontiguousarray(ok, np.uint8)),
                                   _p(np.ascontiguousarray(mask, np.uint8)), _p(cost))
         return cost
+
+    # -- io.cpp encoders (restatement only: io.cpp needs libpng, absent here)
+    def encode_kitti16(self, d, valid):
+        d = np.ascontiguousarray(d, np.float32)
+        h, w = d.shape
+        out = np.zeros((h, 2 * w), np.uint8)
+        neg = self.lib.orc_encode_kitti16(_p(d), _p(np.ascontiguousarray(valid, np.uint8)), w, h, _p(out))
+        return out, int(neg)
+
+    def encode_pfm(self, d, valid):
+        d = np.ascontiguousarray(d, np.float32)
+        h, w = d.shape
+        out = np.zeros((h, w), np.float32)
+        self.lib.orc_encode_pfm(_p(d), _p(np.ascontiguousarray(valid, np.uint8)), w, h, _p(out))
+        return out
+
+    def point_cloud(self, d, valid, image, calib, min_disparity=0.5):
+        d = np.ascontiguousarray(d, np.float32)
+        h, w = d.shape
+        xyz = np.zeros((h * w, 3), np.float32)
+        inten = np.zeros(h * w, np.uint8)
+        c = _Calib(*[float(x) for x in calib])
+        n = self.lib.orc_point_cloud(_p(d), _p(np.ascontiguousarray(valid, np.uint8)),
+                                     _p(np.ascontiguousarray(image, np.uint8)), w, h, C.byref(c),
+                                     float(min_disparity), _p(xyz), _p(inten))
+        return (None, None) if n < 0 else (xyz[:n], inten[:n])
 
     def wta(self, left, right, mask, nd):
         """wtaOracle (proj/src/synth.cpp:171-198) -> (disparity, valid, cost)."""

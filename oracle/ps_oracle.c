@@ -678,6 +678,59 @@ void orc_wta(const uint8_t* left, const uint8_t* right, int w, int h, const uint
     free(cr);
 }
 
+/* writeKittiPng, proj/src/io.cpp:349-368 (the raster it hands to libpng) */
+long long orc_encode_kitti16(const float* d, const uint8_t* valid, int w, int h, uint8_t* out) {
+    memset(out, 0, (size_t)w * h * 2);
+    for (int v = 0; v < h; ++v) {
+        uint8_t* row = out + (size_t)v * w * 2;
+        for (int u = 0; u < w; ++u) {
+            const size_t i = (size_t)v * w + u;
+            if (!valid[i]) continue;
+            if (d[i] < 0.0f) return (long long)i; /* NegativeDisparity */
+            long raw = lround((double)d[i] * 256.0);
+            raw = raw < 1L ? 1L : (raw > 65535L ? 65535L : raw); /* raw 0 is reserved */
+            row[2 * u] = (uint8_t)(raw >> 8);
+            row[2 * u + 1] = (uint8_t)(raw & 0xff);
+        }
+    }
+    return -1;
+}
+
+/* writePfm, proj/src/io.cpp:311-329 */
+void orc_encode_pfm(const float* d, const uint8_t* valid, int w, int h, float* out) {
+    for (int r = 0; r < h; ++r) {
+        const int v = h - 1 - r;
+        for (int u = 0; u < w; ++u) {
+            const size_t i = (size_t)v * w + u;
+            out[(size_t)r * w + u] = valid[i] ? d[i] : -1.0f;
+        }
+    }
+}
+
+/* exportPointCloud, proj/src/io.cpp:395-454 (vertex list) */
+int orc_point_cloud(const float* d, const uint8_t* valid, const uint8_t* image, int w, int h,
+                    const ps_calib* calib, double min_disparity, float* xyz, uint8_t* intensity) {
+    if (!(calib->focal > 0.0) || !(calib->baseline > 0.0)) return -1; /* io.cpp:19-26 */
+    int n = 0;
+    for (int v = 0; v < h; ++v) {
+        for (int u = 0; u < w; ++u) {
+            const size_t i = (size_t)v * w + u;
+            if (!valid[i]) continue;
+            const double dd = d[i];
+            if (dd < min_disparity) continue;
+            const double z = calib->focal * calib->baseline / dd;
+            const double x = (u - calib->cx) * z / calib->focal;
+            const double y = (v - calib->cy) * z / calib->focal;
+            xyz[3 * n] = (float)x;
+            xyz[3 * n + 1] = (float)y;
+            xyz[3 * n + 2] = (float)z;
+            intensity[n] = image[i];
+            ++n;
+        }
+    }
+    return n;
+}
+
 static int ceil_div_pos(int a, int b) { return (a + b - 1) / b; }
 
 /* disparityRefinement, pipeline.cpp:56-86 */

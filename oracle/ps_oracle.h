@@ -53,6 +53,16 @@ void orc_interpolate(const int32_t* lookup, const double* planes, int w, int h,
  * d in [0, min(nd, u - 2)]; cost 1.0 and invalid elsewhere. */
 void orc_wta(const uint8_t* left, const uint8_t* right, int w, int h, const uint8_t* mask, int nd,
              float* disparity, uint8_t* valid, float* cost);
+/* Output encoders of proj/src/io.cpp (rasters only; the containers are text).
+ * writeKittiPng :349-368 -> 2 bytes/pixel big-endian, returns the index of
+ * the first negative valid disparity (row-major) or -1. */
+long long orc_encode_kitti16(const float* d, const uint8_t* valid, int w, int h, uint8_t* out);
+/* writePfm :311-329 -> rows bottom-up, invalid -1.0 */
+void orc_encode_pfm(const float* d, const uint8_t* valid, int w, int h, float* out);
+/* exportPointCloud :395-454 -> vertex count (xyz, intensity), -1 for a bad
+ * calibration (InvalidConfig); count 0 is the caller's EmptyCloud. */
+int orc_point_cloud(const float* d, const uint8_t* valid, const uint8_t* image, int w, int h,
+                    const ps_calib* calib, double min_disparity, float* xyz, uint8_t* intensity);
 void orc_cost_evaluation(const uint32_t* cl, const uint32_t* cr, int w, int h, const float* value,
                          const uint8_t* valid, const uint8_t* mask, float* cost);
 /* disparityRefinement, proj/src/pipeline.cpp:56-86. */

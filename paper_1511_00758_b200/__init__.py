@@ -58,6 +58,18 @@ class SeedingFailed(Error):
     pass
 
 
+class NegativeDisparity(Error):
+    pass
+
+
+class EmptyCloud(Error):
+    pass
+
+
+class NoOverlap(Error):
+    pass
+
+
 class CudaError(Error):
     pass
 
@@ -69,8 +81,16 @@ class NoDevice(Error):
 _STATUS = {
     1: Error, 2: InvalidConfig, 3: DimensionTooSmall, 4: DimensionMismatch,
     5: FewerThanThreePoints, 6: DegenerateTriangle, 7: SeedingFailed, 8: CudaError,
-    9: NoDevice, 10: Error,
+    9: NoDevice, 10: Error, 11: NegativeDisparity, 12: EmptyCloud, 13: NoOverlap,
 }
+
+
+def _maps(disparity, valid):
+    d = np.ascontiguousarray(disparity, dtype=np.float32)
+    v = np.ascontiguousarray(valid, dtype=np.uint8)
+    if d.shape != v.shape or d.ndim < 2:
+        raise DimensionMismatch("disparity and validity must be equal arrays of >= 2 dims")
+    return d, v
 
 
 def _check(status: int) -> None:
@@ -196,6 +216,7 @@ class Context:
                 observer(it, d, v, c)
             cb = _native.OBSERVER(_obs)
         flags = PS_RUN_UNCHECKED_CELL if unchecked_cell else 0
+        self._shape = (1, h, w)
         _check(self._lib.ps_run(self._h, _ptr(L), _ptr(R), w, h, C.byref(cfg), flags,
                                 _ptr(out.disparity), _ptr(out.disparity_valid), _ptr(out.costs),
                                 _ptr(out.dense), _ptr(out.dense_valid), trace, cb, None))
@@ -228,6 +249,7 @@ class Context:
                 raise ValueError(f"out[{key!r}] must be a C-contiguous {np.dtype(dt).name} array of shape {(n, h, w)}")
             res[key] = a
         res["status"] = np.zeros(n, np.int32)
+        self._shape = (n, h, w)
         trace = (PsIterStats * (n * config.iterations))()
         st = self._lib.ps_run_batch(self._h, n, _ptr(L), _ptr(R), w, h, C.byref(cfg),
                                     PS_RUN_UNCHECKED_CELL if unchecked_cell else 0,
@@ -243,9 +265,11 @@ class Context:
     def upload(self, left: np.ndarray, right: np.ndarray) -> None:
         n, h, w = left.shape
         _check(self._lib.ps_upload_batch(self._h, n, _ptr(left), _ptr(right), w, h))
+        self._shape = (n, h, w)
 
     def upload_ptr(self, n: int, left_ptr: int, right_ptr: int, w: int, h: int) -> None:
         _check(self._lib.ps_upload_batch(self._h, n, C.c_void_p(left_ptr), C.c_void_p(right_ptr), w, h))
+        self._shape = (n, h, w)
 
     def run_resident(self, config: PipelineConfig, unchecked_cell: bool = False) -> int:
         cfg = config.to_c()
@@ -432,6 +456,72 @@ class Context:
                                       max_disparity, _ptr(d), _ptr(ok), _ptr(c)))
         return d, ok, c
 
+    # ------------------------------------------------------------ encoders
+    def encode_kitti16(self, disparity, valid) -> np.ndarray:
+        """writeKittiPng's raster (proj/src/io.cpp:349-368): (..., H, 2W) uint8,
+        the PNG row bytes (big-endian raw = clamp(lround(d*256), 1, 65535), 0 invalid)."""
+        d, v = _maps(disparity, valid)
+        *lead, h, w = d.shape
+        n = int(np.prod(lead)) if lead else 1
+        out = np.zeros(tuple(lead) + (h, 2 * w), np.uint8)
+        _check(self._lib.ps_encode_kitti16(self._h, _ptr(d), _ptr(v), w, h, n, _ptr(out)))
+        return out
+
+    def encode_pfm(self, disparity, valid) -> np.ndarray:
+        """writePfm's raster (proj/src/io.cpp:311-329): rows bottom-up, invalid -1.0."""
+        d, v = _maps(disparity, valid)
+        *lead, h, w = d.shape
+        n = int(np.prod(lead)) if lead else 1
+        out = np.zeros(d.shape, np.float32)
+        _check(self._lib.ps_encode_pfm(self._h, _ptr(d), _ptr(v), w, h, n, _ptr(out)))
+        return out
+
+    def point_cloud(self, disparity, valid, image, calib, min_disparity: float = 0.5):
+        """exportPointCloud's vertices (proj/src/io.cpp:395-454): (xyz (N, 3) float32,
+        intensity (N,) uint8), row-major; calib = (focal, baseline, cx, cy)."""
+        d, v = _maps(disparity, valid)
+        img = _u8(image)
+        h, w = d.shape
+        c = _native.PsCalib(*[float(x) for x in calib])
+        cap = int(v.sum()) + 1
+        xyz = np.zeros((cap, 3), np.float32)
+        inten = np.zeros(cap, np.uint8)
+        n = C.c_int()
+        _check(self._lib.ps_point_cloud(self._h, _ptr(d), _ptr(v), _ptr(img), w, h, C.byref(c),
+                                        C.c_double(min_disparity), _ptr(xyz), _ptr(inten), cap,
+                                        C.byref(n)))
+        return xyz[:n.value], inten[:n.value]
+
+    def download_kitti16(self, which: int = 0) -> np.ndarray:
+        """KITTI raster of the last run's maps, encoded on the device (F, H, 2W)."""
+        f, h, w = self._resident_shape()
+        out = np.zeros((f, h, 2 * w), np.uint8)
+        _check(self._lib.ps_download_kitti16(self._h, which, _ptr(out)))
+        return out
+
+    def download_pfm(self, which: int = 0) -> np.ndarray:
+        f, h, w = self._resident_shape()
+        out = np.zeros((f, h, w), np.float32)
+        _check(self._lib.ps_download_pfm(self._h, which, _ptr(out)))
+        return out
+
+    def download_point_cloud(self, frame: int, calib, min_disparity: float = 0.5, which: int = 0):
+        f, h, w = self._resident_shape()
+        c = _native.PsCalib(*[float(x) for x in calib])
+        cap = h * w
+        xyz = np.zeros((cap, 3), np.float32)
+        inten = np.zeros(cap, np.uint8)
+        n = C.c_int()
+        _check(self._lib.ps_download_point_cloud(self._h, frame, which, C.byref(c),
+                                                 C.c_double(min_disparity), _ptr(xyz), _ptr(inten),
+                                                 cap, C.byref(n)))
+        return xyz[:n.value], inten[:n.value]
+
+    def _resident_shape(self):
+        if not getattr(self, "_shape", None):
+            raise Error("no batch uploaded through this Context")
+        return self._shape
+
     def cost_evaluation(self, census_left, census_right, interp, interp_valid, mask):
         cl = np.ascontiguousarray(census_left, dtype=np.uint32)
         cr = np.ascontiguousarray(census_right, dtype=np.uint32)
@@ -510,7 +600,8 @@ def baseline_config(idx: int) -> PipelineConfig:
 
 __all__ = [
     "Error", "InvalidConfig", "DimensionTooSmall", "DimensionMismatch", "FewerThanThreePoints",
-    "DegenerateTriangle", "SeedingFailed", "CudaError", "NoDevice", "PipelineConfig",
+    "DegenerateTriangle", "SeedingFailed", "NegativeDisparity", "EmptyCloud", "NoOverlap",
+    "CudaError", "NoDevice", "PipelineConfig",
     "IterationStats", "StereoResult", "Context", "delaunay_triangulate", "synth_pair",
     "synth_batch", "BASELINE_CONFIGS", "baseline_config", "PS_RUN_UNCHECKED_CELL",
 ]

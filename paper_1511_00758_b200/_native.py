@@ -76,6 +76,13 @@ class PsCell(C.Structure):
     ]
 
 
+class PsCalib(C.Structure):
+    """CameraCalib (proj/include/planestereo/io.hpp:17-24)."""
+
+    _fields_ = [("focal", C.c_double), ("baseline", C.c_double), ("cx", C.c_double),
+                ("cy", C.c_double)]
+
+
 OBSERVER = C.CFUNCTYPE(None, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int,
                        C.c_void_p)
 
@@ -116,6 +123,12 @@ SIGNATURES = {
     "ps_support_resampling": (I, [P, P, P, I, P, P, P, I, P, P, I, I, P, P, P, P, I, P]),
     "ps_wta_oracle": (I, [P, P, P, I, I, P, I, P, P, P]),
     "ps_wta_batch": (I, [P, I, P, P, I, I, I, I, P, P, P]),
+    "ps_encode_kitti16": (I, [P, P, P, I, I, I, P]),
+    "ps_encode_pfm": (I, [P, P, P, I, I, I, P]),
+    "ps_point_cloud": (I, [P, P, P, P, I, I, P, C.c_double, P, P, I, P]),
+    "ps_download_kitti16": (I, [P, I, P]),
+    "ps_download_pfm": (I, [P, I, P]),
+    "ps_download_point_cloud": (I, [P, I, I, P, C.c_double, P, P, I, P]),
     "ps_synth_pair": (I, [P, P, P, P]),
     "ps_synth_batch": (I, [P, I, I, P, P]),
 }

@@ -27,6 +27,9 @@ namespace {
         case PS_FEWER_THAN_THREE_POINTS: throw FewerThanThreePoints(msg);
         case PS_DEGENERATE_TRIANGLE: throw DegenerateTriangle(msg);
         case PS_SEEDING_FAILED: throw SeedingFailed(msg);
+        case PS_NEGATIVE_DISPARITY: throw NegativeDisparity(msg);
+        case PS_EMPTY_CLOUD: throw EmptyCloud(msg);
+        case PS_NO_OVERLAP: throw NoOverlap(msg);
         default: throw Error(msg);
     }
 }

@@ -536,6 +536,195 @@ ps_status ps_wta_batch(ps_ctx* ctx, int n_frames, const uint8_t* left, const uin
                       max_disparity, disparity, disparity_valid, cost);
 }
 
+namespace {
+// KITTI 16-bit raster of device maps into host `out` (2 bytes per pixel).
+ps_status kitti_device(ps_ctx* ctx, const float* d_disp, const uint8_t* d_valid, const int* d_ok,
+                       long long P, int frames, uint8_t* out) {
+    ps::Engine& e = *ctx->engine;
+    const size_t n = size_t(frames) * P;
+    uint16_t* d_out = e.dev<uint16_t>(e.s_j, n);
+    unsigned long long* d_neg = e.dev<unsigned long long>(e.s_i, 1);
+    if (!d_out || !d_neg) return set_error(PS_CUDA_ERROR, "allocation failed");
+    cudaStream_t st = e.stream();
+    cudaMemsetAsync(d_neg, 0xff, sizeof(unsigned long long), st);
+    e.count_launches(ps::launch_kitti16(d_disp, d_valid, d_ok, P, frames, d_out, d_neg, st));
+    unsigned long long neg = ~0ull;
+    cudaMemcpyAsync(&neg, d_neg, sizeof(neg), cudaMemcpyDeviceToHost, st);
+    ps_status s = from_engine(ctx, e.sync("kitti encode"));
+    if (s != PS_OK) return s;
+    if (neg != ~0ull) {  // writeKittiPng throws at the first negative valid disparity
+        float d = 0.0f;
+        cudaMemcpy(&d, d_disp + neg, sizeof(float), cudaMemcpyDeviceToHost);
+        return set_error(PS_NEGATIVE_DISPARITY, "cannot encode negative disparity " + std::to_string(d));
+    }
+    return from_engine(ctx, e.check(cudaMemcpy(out, d_out, 2 * n, cudaMemcpyDeviceToHost), "D2H kitti"));
+}
+
+ps_status pfm_device(ps_ctx* ctx, const float* d_disp, const uint8_t* d_valid, const int* d_ok,
+                     int W, int H, int frames, float* out) {
+    ps::Engine& e = *ctx->engine;
+    const size_t n = size_t(frames) * W * H;
+    float* d_out = e.dev<float>(e.s_j, n);
+    if (!d_out) return set_error(PS_CUDA_ERROR, "allocation failed");
+    cudaStream_t st = e.stream();
+    e.count_launches(ps::launch_pfm(d_disp, d_valid, d_ok, W, H, frames, d_out, st));
+    cudaMemcpyAsync(out, d_out, 4 * n, cudaMemcpyDeviceToHost, st);
+    return from_engine(ctx, e.sync("pfm encode"));
+}
+
+ps_status cloud_device(ps_ctx* ctx, const float* d_disp, const uint8_t* d_valid,
+                       const uint8_t* d_img, int W, int H, const ps_calib* calib, double min_d,
+                       float* xyz, uint8_t* intensity, int capacity, int* count) {
+    if (!calib) return set_error(PS_ERROR, "null calibration");
+    // CameraCalib::validate (proj/src/io.cpp:19-26)
+    if (!(calib->focal > 0.0))
+        return set_error(PS_INVALID_CONFIG, "calibration focal length must be positive");
+    if (!(calib->baseline > 0.0))
+        return set_error(PS_INVALID_CONFIG, "calibration baseline must be positive");
+    ps::Engine& e = *ctx->engine;
+    const long long P = (long long)W * H;
+    const int cap = std::max(capacity, 0);
+    float* d_xyz = e.dev<float>(e.s_h, size_t(std::max(cap, 1)) * 3);
+    uint8_t* d_int = e.dev<uint8_t>(e.s_g, size_t(std::max(cap, 1)));
+    int* d_chunk = e.dev<int>(e.s_f, size_t(P / 1024 + 2));
+    int* d_cnt = e.dev<int>(e.s_i, 1);
+    if (!d_xyz || !d_int || !d_chunk || !d_cnt) return set_error(PS_CUDA_ERROR, "allocation failed");
+    cudaStream_t st = e.stream();
+    e.count_launches(ps::launch_point_cloud(d_disp, d_valid, d_img, W, H, calib->focal,
+                                            calib->baseline, calib->cx, calib->cy, min_d, d_xyz,
+                                            d_int, cap, d_chunk, d_cnt, st));
+    int n = 0;
+    cudaMemcpyAsync(&n, d_cnt, sizeof(int), cudaMemcpyDeviceToHost, st);
+    ps_status s = from_engine(ctx, e.sync("point cloud"));
+    if (s != PS_OK) return s;
+    if (count) *count = n;
+    if (n == 0) return set_error(PS_EMPTY_CLOUD, "no valid pixels above the minimum disparity");
+    if (n > cap) return set_error(PS_CAPACITY, "point cloud buffer too small");
+    if (xyz) cudaMemcpyAsync(xyz, d_xyz, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost, st);
+    if (intensity) cudaMemcpyAsync(intensity, d_int, n, cudaMemcpyDeviceToHost, st);
+    return from_engine(ctx, e.sync("point cloud D2H"));
+}
+
+ps_status upload_map(ps_ctx* ctx, const float* disparity, const uint8_t* valid, size_t n,
+                     float** d_disp, uint8_t** d_valid) {
+    if (!disparity || !valid) return set_error(PS_ERROR, "null map");
+    ps::Engine& e = *ctx->engine;
+    *d_disp = e.dev<float>(e.s_a, n);
+    *d_valid = e.dev<uint8_t>(e.s_b, n);
+    if (!*d_disp || !*d_valid) return set_error(PS_CUDA_ERROR, "allocation failed");
+    cudaMemcpyAsync(*d_disp, disparity, 4 * n, cudaMemcpyHostToDevice, e.stream());
+    cudaMemcpyAsync(*d_valid, valid, n, cudaMemcpyHostToDevice, e.stream());
+    return PS_OK;
+}
+}  // namespace
+
+ps_status ps_encode_kitti16(ps_ctx* ctx, const float* disparity, const uint8_t* valid, int width,
+                            int height, int n_frames, uint8_t* out) {
+    PS_REQUIRE_CTX(ctx);
+    if (width < 1 || height < 1 || n_frames < 1 || !out) return set_error(PS_ERROR, "bad arguments");
+    float* dd;
+    uint8_t* dv;
+    ps_status s = upload_map(ctx, disparity, valid, size_t(n_frames) * width * height, &dd, &dv);
+    if (s != PS_OK) return s;
+    return kitti_device(ctx, dd, dv, nullptr, (long long)width * height, n_frames, out);
+}
+
+ps_status ps_encode_pfm(ps_ctx* ctx, const float* disparity, const uint8_t* valid, int width,
+                        int height, int n_frames, float* out) {
+    PS_REQUIRE_CTX(ctx);
+    if (width < 1 || height < 1 || n_frames < 1 || !out) return set_error(PS_ERROR, "bad arguments");
+    float* dd;
+    uint8_t* dv;
+    ps_status s = upload_map(ctx, disparity, valid, size_t(n_frames) * width * height, &dd, &dv);
+    if (s != PS_OK) return s;
+    return pfm_device(ctx, dd, dv, nullptr, width, height, n_frames, out);
+}
+
+ps_status ps_point_cloud(ps_ctx* ctx, const float* disparity, const uint8_t* valid,
+                         const uint8_t* image, int width, int height, const ps_calib* calib,
+                         double min_disparity, float* xyz, uint8_t* intensity, int capacity,
+                         int* count) {
+    PS_REQUIRE_CTX(ctx);
+    if (width < 1 || height < 1 || !image) return set_error(PS_ERROR, "bad arguments");
+    if (!calib) return set_error(PS_ERROR, "null calibration");
+    if (!(calib->focal > 0.0))
+        return set_error(PS_INVALID_CONFIG, "calibration focal length must be positive");
+    if (!(calib->baseline > 0.0))
+        return set_error(PS_INVALID_CONFIG, "calibration baseline must be positive");
+    const size_t n = size_t(width) * height;
+    float* dd;
+    uint8_t* dv;
+    ps_status s = upload_map(ctx, disparity, valid, n, &dd, &dv);
+    if (s != PS_OK) return s;
+    ps::Engine& e = *ctx->engine;
+    uint8_t* di = e.dev<uint8_t>(e.s_c, n);
+    if (!di) return set_error(PS_CUDA_ERROR, "allocation failed");
+    cudaMemcpyAsync(di, image, n, cudaMemcpyHostToDevice, e.stream());
+    return cloud_device(ctx, dd, dv, di, width, height, calib, min_disparity, xyz, intensity,
+                        capacity, count);
+}
+
+namespace {
+ps_status resident(ps_ctx* ctx, int which, ps::Engine::ResidentMaps& m, const float** d,
+                   const uint8_t** v) {
+    if (which != PS_MAP_DISPARITY && which != PS_MAP_DENSE)
+        return set_error(PS_ERROR, "which must be PS_MAP_DISPARITY or PS_MAP_DENSE");
+    ps_status s = from_engine(ctx, ctx->engine->resident_maps(m));
+    if (s != PS_OK) return s;
+    *d = which == PS_MAP_DENSE ? m.dense : m.disparity;
+    *v = which == PS_MAP_DENSE ? m.dense_valid : m.disparity_valid;
+    return PS_OK;
+}
+}  // namespace
+
+ps_status ps_download_kitti16(ps_ctx* ctx, int which, uint8_t* out) {
+    PS_REQUIRE_CTX(ctx);
+    if (!out) return set_error(PS_ERROR, "null output");
+    ps::Engine::ResidentMaps m;
+    const float* d;
+    const uint8_t* v;
+    ps_status s = resident(ctx, which, m, &d, &v);
+    if (s != PS_OK) return s;
+    return kitti_device(ctx, d, v, m.frame_ok, m.pixels, m.frames, out);
+}
+
+ps_status ps_download_pfm(ps_ctx* ctx, int which, float* out) {
+    PS_REQUIRE_CTX(ctx);
+    if (!out) return set_error(PS_ERROR, "null output");
+    ps::Engine::ResidentMaps m;
+    const float* d;
+    const uint8_t* v;
+    ps_status s = resident(ctx, which, m, &d, &v);
+    if (s != PS_OK) return s;
+    return pfm_device(ctx, d, v, m.frame_ok, m.width, m.height, m.frames, out);
+}
+
+ps_status ps_download_point_cloud(ps_ctx* ctx, int frame, int which, const ps_calib* calib,
+                                  double min_disparity, float* xyz, uint8_t* intensity,
+                                  int capacity, int* count) {
+    PS_REQUIRE_CTX(ctx);
+    ps::Engine::ResidentMaps m;
+    const float* d;
+    const uint8_t* v;
+    ps_status s = resident(ctx, which, m, &d, &v);
+    if (s != PS_OK) return s;
+    if (frame < 0 || frame >= m.frames) return set_error(PS_ERROR, "no such frame");
+    if (!calib) return set_error(PS_ERROR, "null calibration");
+    if (!(calib->focal > 0.0))
+        return set_error(PS_INVALID_CONFIG, "calibration focal length must be positive");
+    if (!(calib->baseline > 0.0))
+        return set_error(PS_INVALID_CONFIG, "calibration baseline must be positive");
+    int ok = 0;
+    cudaMemcpy(&ok, m.frame_ok + frame, sizeof(int), cudaMemcpyDeviceToHost);
+    if (!ok) {  // no result: an empty map
+        if (count) *count = 0;
+        return set_error(PS_EMPTY_CLOUD, "no valid pixels above the minimum disparity");
+    }
+    const size_t b = size_t(frame) * m.pixels;
+    return cloud_device(ctx, d + b, v + b, m.left + b, m.width, m.height, calib, min_disparity, xyz,
+                        intensity, capacity, count);
+}
+
 ps_status ps_refinement(ps_ctx* ctx, const float* interp, const uint8_t* interp_valid,
                         const float* cost, float* final_disparity, uint8_t* final_valid,
                         float* final_cost, const uint8_t* mask, int width, int height,

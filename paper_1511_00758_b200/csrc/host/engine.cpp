@@ -203,6 +203,7 @@ T* Engine::host(HostBuf& b, size_t count) {
     return static_cast<T*>(b.p);
 }
 
+template uint16_t* Engine::dev<uint16_t>(DevBuf&, size_t);
 template uint8_t* Engine::dev<uint8_t>(DevBuf&, size_t);
 template int* Engine::dev<int>(DevBuf&, size_t);
 template uint32_t* Engine::dev<uint32_t>(DevBuf&, size_t);
@@ -938,6 +939,21 @@ void Engine::set_sink(float* disparity, uint8_t* disparity_valid, float* cost, f
                    page_locked(disparity) && page_locked(disparity_valid) && page_locked(cost) &&
                    page_locked(dense) && page_locked(dense_valid);
     if (!sink_.active) sink_ = Sink{};
+}
+
+ps_status Engine::resident_maps(ResidentMaps& m) {
+    if (!have_outputs_) return fail(PS_ERROR, "no completed run to encode");
+    cudaSetDevice(device_);
+    int* ok = dev<int>(dFrameOk_, F_);
+    if (!ok) return fail(PS_CUDA_ERROR, "allocation failed");
+    std::vector<int> h(F_);
+    for (int f = 0; f < F_; ++f) h[f] = status_[f] == PS_OK ? 1 : 0;
+    ps_status s = check(cudaMemcpy(ok, h.data(), sizeof(int) * F_, cudaMemcpyHostToDevice), "H2D frame status");
+    if (s != PS_OK) return s;
+    m = ResidentMaps{static_cast<const float*>(dDf_.p), static_cast<const uint8_t*>(dDv_.p),
+                     static_cast<const float*>(dDense_.p), static_cast<const uint8_t*>(dDenseV_.p),
+                     static_cast<const uint8_t*>(dL_.p), ok, F_, W_, H_, P_};
+    return PS_OK;
 }
 
 ps_status Engine::supports(int frame, int* u, int* v, double* d, int capacity, int* count) {

@@ -84,6 +84,19 @@ public:
                   uint8_t* dense_valid);
     void clear_sink() { sink_ = Sink{}; }
     ps_status supports(int frame, int* u, int* v, double* d, int capacity, int* count);
+    // Device views of the last run's result maps, for the output encoders
+    // (capi.cpp); frame_ok[f] = 1 when frame f produced a result.
+    struct ResidentMaps {
+        const float* disparity;
+        const uint8_t* disparity_valid;
+        const float* dense;
+        const uint8_t* dense_valid;
+        const uint8_t* left;
+        const int* frame_ok;  // device, F entries
+        int frames, width, height;
+        long long pixels;
+    };
+    ps_status resident_maps(ResidentMaps& m);
 
     void set_profiling(bool on) { profiling_ = on; }
     // Upper bound on concurrent frame groups (streams); 1 serialises the
@@ -107,6 +120,7 @@ public:
 
     // Scratch for stage-API calls.
     DevBuf s_a, s_b, s_c, s_d, s_e, s_f, s_g, s_h, s_i, s_j;
+    DevBuf dFrameOk_;  // resident_maps()
 
 private:
     void begin_kernel(const char* name, double bytes, cudaStream_t s);

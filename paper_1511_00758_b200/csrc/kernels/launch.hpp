@@ -147,4 +147,17 @@ int launch_wta(const uint32_t* cl, const uint32_t* cr, const uint8_t* mask, Fram
                int max_disparity, const CostTables& tab, float* disparity, uint8_t* valid,
                float* cost, cudaStream_t st);
 
+// Output encoders (codecs.cu): KITTI 16-bit raster (big-endian words, 0 =
+// invalid; neg_first <- smallest index of a negative valid disparity), PFM
+// raster (bottom-up, -1 = invalid), and the ordered point-cloud vertex list.
+// frame_ok[f] == 0 marks a frame with no result (all invalid); may be null.
+int launch_kitti16(const float* d, const uint8_t* valid, const int* frame_ok, long long P, int frames,
+                   uint16_t* out, unsigned long long* neg_first, cudaStream_t st);
+int launch_pfm(const float* d, const uint8_t* valid, const int* frame_ok, int W, int H, int frames,
+               float* out, cudaStream_t st);
+int launch_point_cloud(const float* d, const uint8_t* valid, const uint8_t* image, int W, int H,
+                       double focal, double baseline, double cx, double cy, double min_d,
+                       float* xyz, uint8_t* intensity, int capacity, int* chunk_buf, int* count,
+                       cudaStream_t st);
+
 }  // namespace ps

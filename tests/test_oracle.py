@@ -205,3 +205,56 @@ def test_oracle_wta_equals_reference(orc, ref):
         m = (rng.random((h, w)) < 0.5).astype(np.uint8)
         for a, b in zip(orc.wta(L, R, m, nd), ref.wta(L, R, m, nd)):
             assert np.array_equal(a.view(np.uint8), b.view(np.uint8))
+
+
+def test_oracle_encoders_reference_known_answers(orc):
+    """The io.cpp encoder restatements against the reference's own known
+    answers (proj/tests/test_io.cpp:144-312); io.cpp itself cannot be compiled
+    here (it needs libpng), so these pin the restatement."""
+    # KITTI: raw = lround(d * 256), big-endian, raw 0 reserved (test_io.cpp:179-200)
+    d = np.zeros((16, 20), np.float32)
+    ok = np.zeros((16, 20), np.uint8)
+    for u, val in [(4, 2.0), (5, 0.5), (6, 63.75)]:
+        d[4, u], ok[4, u] = val, 1
+    raster, neg = orc.encode_kitti16(d, ok)
+    assert neg == -1
+    raw = raster[:, 0::2].astype(np.int32) << 8 | raster[:, 1::2]
+    assert raw[4, 4] == 512 and raw[4, 5] == 128 and raw[4, 6] == 16320
+    assert (raw > 0).sum() == 3
+    # round trip within the codec precision (test_io.cpp:202-216), clamp at both ends
+    rng = np.random.default_rng(31)
+    d = rng.uniform(0.01, 127.0, (19, 25)).astype(np.float32)
+    ok = (rng.random((19, 25)) < 0.75).astype(np.uint8)
+    d[0, 0], ok[0, 0] = 0.0, 1      # raw 0 -> clamped to 1
+    d[0, 1], ok[0, 1] = 300.0, 1    # raw 76800 -> clamped to 65535
+    raster, neg = orc.encode_kitti16(d, ok)
+    raw = raster[:, 0::2].astype(np.int32) << 8 | raster[:, 1::2]
+    assert neg == -1 and ((raw > 0) == (ok == 1)).all()
+    assert raw[0, 0] == 1 and raw[0, 1] == 65535
+    m = (ok == 1)
+    m[0, :2] = False
+    assert (np.abs(raw[m] / 256.0 - d[m]) <= 1.0 / 256.0).all()
+    # negative disparities cannot be encoded (test_io.cpp:218-224)
+    d = np.zeros((16, 16), np.float32)
+    ok = np.zeros((16, 16), np.uint8)
+    d[3, 3], ok[3, 3] = -1.0, 1
+    assert orc.encode_kitti16(d, ok)[1] == 3 * 16 + 3
+    # PFM: bottom-up rows, invalid -1, bit-exact round trip (test_io.cpp:144-159)
+    d = rng.uniform(0.01, 127.0, (17, 31)).astype(np.float32)
+    ok = (rng.random((17, 31)) < 0.75).astype(np.uint8)
+    pfm = orc.encode_pfm(d, ok)
+    back = pfm[::-1]
+    assert ((back > 0) == (ok == 1)).all() and np.array_equal(back[ok == 1], d[ok == 1])
+    assert (back[ok == 0] == -1.0).all()
+    # point cloud (test_io.cpp:232-274, 301-310)
+    img = np.full((32, 32), 200, np.uint8)
+    d = np.zeros((32, 32), np.float32)
+    ok = np.zeros((32, 32), np.uint8)
+    for (u, v, val) in [(16, 16, 25.0), (20, 16, 25.0), (4, 4, 0.2)]:
+        d[v, u], ok[v, u] = val, 1
+    xyz, inten = orc.point_cloud(d, ok, img, (100.0, 0.5, 16.0, 16.0))
+    assert len(xyz) == 2 and (inten == 200).all()
+    assert np.allclose(xyz[0], [0.0, 0.0, 2.0]) and np.allclose(xyz[1], [(20 - 16) * 2.0 / 100.0, 0.0, 2.0])
+    assert len(orc.point_cloud(np.zeros((16, 16), np.float32), np.zeros((16, 16), np.uint8),
+                               img[:16, :16], (100.0, 0.5, 8.0, 8.0))[0]) == 0
+    assert orc.point_cloud(d, ok, img, (0.0, 0.5, 0.0, 0.0))[0] is None
