@@ -270,6 +270,27 @@ ps_status ps_download_point_cloud(ps_ctx* ctx, int frame, int which, const ps_ca
                                   double min_disparity, float* xyz, uint8_t* intensity,
                                   int capacity, int* count);
 
+/* ------------------------------------------------------------ evaluation */
+/* accuracy (proj/include/planestereo/eval.hpp:15-29, proj/src/eval.cpp:19-70)
+ * of n_frames predictions against ground truth, on the device: per frame,
+ * over the pixels valid in both maps (and inside mask, when not NULL),
+ * evaluated[f], mean_abs_error[f] (the reference's row-major binary64 sum /
+ * evaluated) and fractions[f * n_thresholds + k] = #{err < thresholds[k]} /
+ * evaluated; n_thresholds <= 16.  PS_NO_OVERLAP (NoOverlap) if a frame has no
+ * jointly valid pixel — the other frames are still filled. */
+ps_status ps_accuracy(ps_ctx* ctx, int n_frames, const float* prediction,
+                      const uint8_t* prediction_valid, const float* ground_truth,
+                      const uint8_t* ground_truth_valid, const uint8_t* mask, int width,
+                      int height, const double* thresholds, int n_thresholds, double* fractions,
+                      long long* evaluated, double* mean_abs_error);
+/* The same for the last run's results in device memory (which = PS_MAP_*),
+ * ground truth given on the host for every frame of the batch; use_mask != 0
+ * restricts to the run's gradient mask (accuracy(prediction, gt, mask, ...)). */
+ps_status ps_download_accuracy(ps_ctx* ctx, int which, const float* ground_truth,
+                               const uint8_t* ground_truth_valid, int use_mask,
+                               const double* thresholds, int n_thresholds, double* fractions,
+                               long long* evaluated, double* mean_abs_error);
+
 /* ------------------------------------------------- synthetic stereo pairs */
 /* Seeded BASELINE-style generator; bench/test fixture, not on
  * the hot path.  gt may be NULL. */

@@ -90,6 +90,7 @@ class CpuChecker:
             "mesh_build": (I, [P, P, P, P, I, I, I, P, P]),
             "cost_evaluation": (None, [P, P, I, I, P, P, P, P]),
             "wta": (None, [P, P, I, I, P, I, P, P, P]),
+            "accuracy": (I, [P, P, P, P, P, I, I, P, I, P, P, P]),
             "refinement": (None, [P, P, P, P, P, P, P, I, I, I, P, P, P]),
             "support_resampling": (I, [P, P, I, P, P, P, I, P, P, I, I, P, P, P, P, I]),
             "run": (I, [P, P, I, I, P, I, P, P, P, P, P, P, P, P, P, I, P]),
@@ -230,6 +231,21 @@ class CpuChecker:
                                      _p(np.ascontiguousarray(image, np.uint8)), w, h, C.byref(c),
                                      float(min_disparity), _p(xyz), _p(inten))
         return (None, None) if n < 0 else (xyz[:n], inten[:n])
+
+    def accuracy(self, pred, pred_valid, gt, gt_valid, mask, thresholds):
+        """accuracy (proj/src/eval.cpp:19-70) -> (status, fractions, evaluated, meanAbsError)."""
+        pred = np.ascontiguousarray(pred, np.float32)
+        h, w = pred.shape
+        th = np.ascontiguousarray(thresholds, np.float64)
+        fr = np.zeros(len(th), np.float64)
+        ev = C.c_longlong()
+        mae = C.c_double()
+        st = self.f("accuracy")(_p(pred), _p(np.ascontiguousarray(pred_valid, np.uint8)),
+                                _p(np.ascontiguousarray(gt, np.float32)),
+                                _p(np.ascontiguousarray(gt_valid, np.uint8)),
+                                None if mask is None else _p(np.ascontiguousarray(mask, np.uint8)),
+                                w, h, _p(th), len(th), _p(fr), C.byref(ev), C.byref(mae))
+        return st, fr, ev.value, mae.value
 
     def wta(self, left, right, mask, nd):
         """wtaOracle (proj/src/synth.cpp:171-198) -> (disparity, valid, cost)."""

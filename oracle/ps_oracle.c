@@ -731,6 +731,36 @@ int orc_point_cloud(const float* d, const uint8_t* valid, const uint8_t* image, 
     return n;
 }
 
+/* accuracyImpl, proj/src/eval.cpp:19-59 */
+int orc_accuracy(const float* pred, const uint8_t* pred_valid, const float* gt,
+                 const uint8_t* gt_valid, const uint8_t* mask, int w, int h,
+                 const double* thresholds, int n_thr, double* fractions, long long* evaluated,
+                 double* mean_abs_error) {
+    long long n = 0;
+    long* hits = (long*)calloc(n_thr > 0 ? n_thr : 1, sizeof(long));
+    double err_sum = 0.0;
+    for (int v = 0; v < h; ++v) {
+        for (int u = 0; u < w; ++u) {
+            const size_t i = (size_t)v * w + u;
+            if (!pred_valid[i] || !gt_valid[i]) continue;
+            if (mask && !mask[i]) continue;
+            const double err = fabs((double)pred[i] - (double)gt[i]);
+            ++n;
+            err_sum += err;
+            for (int k = 0; k < n_thr; ++k) hits[k] += (err < thresholds[k]);
+        }
+    }
+    *evaluated = n;
+    if (n == 0) {
+        free(hits);
+        return PS_NO_OVERLAP;
+    }
+    *mean_abs_error = err_sum / (double)n;
+    for (int k = 0; k < n_thr; ++k) fractions[k] = (double)hits[k] / (double)n;
+    free(hits);
+    return PS_OK;
+}
+
 static int ceil_div_pos(int a, int b) { return (a + b - 1) / b; }
 
 /* disparityRefinement, pipeline.cpp:56-86 */

@@ -63,6 +63,12 @@ void orc_encode_pfm(const float* d, const uint8_t* valid, int w, int h, float* o
  * calibration (InvalidConfig); count 0 is the caller's EmptyCloud. */
 int orc_point_cloud(const float* d, const uint8_t* valid, const uint8_t* image, int w, int h,
                     const ps_calib* calib, double min_disparity, float* xyz, uint8_t* intensity);
+/* accuracy, proj/src/eval.cpp:19-59 (mask may be NULL): PS_NO_OVERLAP when
+ * no pixel is jointly valid. */
+int orc_accuracy(const float* pred, const uint8_t* pred_valid, const float* gt,
+                 const uint8_t* gt_valid, const uint8_t* mask, int w, int h,
+                 const double* thresholds, int n_thr, double* fractions, long long* evaluated,
+                 double* mean_abs_error);
 void orc_cost_evaluation(const uint32_t* cl, const uint32_t* cr, int w, int h, const float* value,
                          const uint8_t* valid, const uint8_t* mask, float* cost);
 /* disparityRefinement, proj/src/pipeline.cpp:56-86. */

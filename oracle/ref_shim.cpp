@@ -70,6 +70,7 @@ int statusOf(const std::exception& e) {
     if (dynamic_cast<const FewerThanThreePoints*>(&e)) return PS_FEWER_THAN_THREE_POINTS;
     if (dynamic_cast<const DegenerateTriangle*>(&e)) return PS_DEGENERATE_TRIANGLE;
     if (dynamic_cast<const SeedingFailed*>(&e)) return PS_SEEDING_FAILED;
+    if (dynamic_cast<const NoOverlap*>(&e)) return PS_NO_OVERLAP;
     return PS_ERROR;
 }
 
@@ -407,6 +408,31 @@ void ref_wta(const uint8_t* left, const uint8_t* right, int w, int h, const uint
     auto r = wtaOracle(toImage(left, w, h), toImage(right, w, h), toMask(mask, w, h), max_disparity);
     copyMap(r.first, disp, valid);
     std::memcpy(cost, r.second.values().data(), sizeof(float) * std::size_t(w) * h);
+}
+
+// accuracy (proj/src/eval.cpp:19-70); mask may be null (the maskless overload).
+int ref_accuracy(const float* pred, const uint8_t* pred_valid, const float* gt,
+                 const uint8_t* gt_valid, const uint8_t* mask, int w, int h,
+                 const double* thresholds, int n_thr, double* fractions, long long* evaluated,
+                 double* mean_abs_error) {
+    try {
+        DisparityMap p(w, h), g(w, h);
+        for (int v = 0; v < h; ++v)
+            for (int u = 0; u < w; ++u) {
+                const std::size_t i = std::size_t(v) * w + u;
+                if (pred_valid[i]) p.set(u, v, pred[i]);
+                if (gt_valid[i]) g.set(u, v, gt[i]);
+            }
+        const std::vector<double> th(thresholds, thresholds + n_thr);
+        const AccuracyReport r =
+            mask ? accuracy(p, g, toMask(mask, w, h), th) : accuracy(p, g, th);
+        for (int i = 0; i < n_thr; ++i) fractions[i] = r.fractions[i];
+        *evaluated = r.evaluated;
+        *mean_abs_error = r.meanAbsError;
+        return PS_OK;
+    } catch (const std::exception& e) {
+        return statusOf(e);
+    }
 }
 
 // The reference's own timing harness (proj/src/eval.cpp:144-177): pinned

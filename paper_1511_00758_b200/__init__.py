@@ -517,6 +517,48 @@ class Context:
                                                  cap, C.byref(n)))
         return xyz[:n.value], inten[:n.value]
 
+    # ---------------------------------------------------------- evaluation
+    def accuracy(self, prediction, prediction_valid, ground_truth, ground_truth_valid,
+                 mask=None, thresholds=(1.0, 2.0, 3.0)):
+        """planestereo::accuracy (proj/src/eval.cpp:19-70) on the device.
+        2-D maps -> (fractions, evaluated, meanAbsError); (F, H, W) stacks ->
+        arrays (F, T), (F,), (F,).  NoOverlap when a frame has no jointly valid pixel."""
+        d, v = _maps(prediction, prediction_valid)
+        g, gv = _maps(ground_truth, ground_truth_valid)
+        if g.shape != d.shape:
+            raise DimensionMismatch("prediction and ground truth dimensions differ")
+        m = None
+        if mask is not None:
+            m = np.ascontiguousarray(mask, np.uint8)
+            if m.shape != d.shape:
+                raise DimensionMismatch("mask dimensions differ from the disparity maps")
+        single = d.ndim == 2
+        *lead, h, w = d.shape
+        n = int(np.prod(lead)) if lead else 1
+        th = np.ascontiguousarray(thresholds, np.float64)
+        fr = np.zeros((n, len(th)), np.float64)
+        ev = np.zeros(n, np.int64)
+        mae = np.zeros(n, np.float64)
+        _check(self._lib.ps_accuracy(self._h, n, _ptr(d), _ptr(v), _ptr(g), _ptr(gv),
+                                     None if m is None else _ptr(m), w, h, _ptr(th), len(th),
+                                     _ptr(fr), _ptr(ev), _ptr(mae)))
+        return (fr[0], int(ev[0]), float(mae[0])) if single else (fr, ev, mae)
+
+    def download_accuracy(self, ground_truth, ground_truth_valid, use_mask: bool = True,
+                          thresholds=(1.0, 2.0, 3.0), which: int = 0):
+        """accuracy of the last run's maps (device-resident) against (F, H, W) ground truth."""
+        f, h, w = self._resident_shape()
+        g, gv = _maps(ground_truth, ground_truth_valid)
+        if g.shape != (f, h, w):
+            raise DimensionMismatch("ground truth must be (F, H, W) of the last batch")
+        th = np.ascontiguousarray(thresholds, np.float64)
+        fr = np.zeros((f, len(th)), np.float64)
+        ev = np.zeros(f, np.int64)
+        mae = np.zeros(f, np.float64)
+        _check(self._lib.ps_download_accuracy(self._h, which, _ptr(g), _ptr(gv), int(use_mask),
+                                              _ptr(th), len(th), _ptr(fr), _ptr(ev), _ptr(mae)))
+        return fr, ev, mae
+
     def _resident_shape(self):
         if not getattr(self, "_shape", None):
             raise Error("no batch uploaded through this Context")

@@ -129,6 +129,8 @@ SIGNATURES = {
     "ps_download_kitti16": (I, [P, I, P]),
     "ps_download_pfm": (I, [P, I, P]),
     "ps_download_point_cloud": (I, [P, I, I, P, C.c_double, P, P, I, P]),
+    "ps_accuracy": (I, [P, I, P, P, P, P, P, I, I, P, I, P, P, P]),
+    "ps_download_accuracy": (I, [P, I, P, P, I, P, I, P, P, P]),
     "ps_synth_pair": (I, [P, P, P, P]),
     "ps_synth_batch": (I, [P, I, I, P, P]),
 }

@@ -725,6 +725,111 @@ ps_status ps_download_point_cloud(ps_ctx* ctx, int frame, int which, const ps_ca
                         intensity, capacity, count);
 }
 
+namespace {
+ps_status accuracy_device(ps_ctx* ctx, int frames, const float* d_pred, const uint8_t* d_pv,
+                          const float* gt, const uint8_t* gt_valid, const uint8_t* d_mask,
+                          long long P, const double* thresholds, int n_thr, double* fractions,
+                          long long* evaluated, double* mean_abs_error) {
+    if (n_thr < 0 || n_thr > 16 || (n_thr > 0 && !thresholds))
+        return set_error(PS_ERROR, "0..16 thresholds");
+    if (!gt || !gt_valid) return set_error(PS_ERROR, "null ground truth");
+    ps::Engine& e = *ctx->engine;
+    const size_t n = size_t(frames) * P;
+    float* d_gt = e.dev<float>(e.s_c, n);
+    uint8_t* d_gv = e.dev<uint8_t>(e.s_d, n);
+    double* d_thr = e.dev<double>(e.s_e, 16);
+    unsigned long long* d_cnt = e.dev<unsigned long long>(e.s_f, size_t(frames) * (1 + n_thr));
+    double* d_sum = e.dev<double>(e.s_g, size_t(frames));
+    if (!d_gt || !d_gv || !d_thr || !d_cnt || !d_sum) return set_error(PS_CUDA_ERROR, "allocation failed");
+    cudaStream_t st = e.stream();
+    cudaMemcpyAsync(d_gt, gt, 4 * n, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_gv, gt_valid, n, cudaMemcpyHostToDevice, st);
+    if (n_thr > 0) cudaMemcpyAsync(d_thr, thresholds, sizeof(double) * n_thr, cudaMemcpyHostToDevice, st);
+    e.count_launches(ps::launch_accuracy(d_pred, d_pv, d_gt, d_gv, d_mask, P, frames, d_thr, n_thr,
+                                         d_cnt, d_sum, st));
+    std::vector<unsigned long long> cnt(size_t(frames) * (1 + n_thr));
+    std::vector<double> sum(frames);
+    cudaMemcpyAsync(cnt.data(), d_cnt, sizeof(unsigned long long) * cnt.size(), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(sum.data(), d_sum, sizeof(double) * frames, cudaMemcpyDeviceToHost, st);
+    ps_status s = from_engine(ctx, e.sync("accuracy"));
+    if (s != PS_OK) return s;
+    bool empty = false;
+    for (int f = 0; f < frames; ++f) {
+        const unsigned long long* c = cnt.data() + size_t(f) * (1 + n_thr);
+        const long long ev = (long long)c[0];
+        if (evaluated) evaluated[f] = ev;
+        if (ev == 0) {  // accuracyImpl throws NoOverlap (eval.cpp:50-52)
+            empty = true;
+            if (mean_abs_error) mean_abs_error[f] = 0.0;
+            for (int k = 0; k < n_thr && fractions; ++k) fractions[size_t(f) * n_thr + k] = 0.0;
+            continue;
+        }
+        if (mean_abs_error) mean_abs_error[f] = sum[f] / double(ev);
+        for (int k = 0; k < n_thr && fractions; ++k)
+            fractions[size_t(f) * n_thr + k] = double(c[1 + k]) / double(ev);
+    }
+    if (empty) return set_error(PS_NO_OVERLAP, "no jointly valid pixels to evaluate");
+    return PS_OK;
+}
+}  // namespace
+
+ps_status ps_accuracy(ps_ctx* ctx, int n_frames, const float* prediction,
+                      const uint8_t* prediction_valid, const float* ground_truth,
+                      const uint8_t* ground_truth_valid, const uint8_t* mask, int width,
+                      int height, const double* thresholds, int n_thresholds, double* fractions,
+                      long long* evaluated, double* mean_abs_error) {
+    PS_REQUIRE_CTX(ctx);
+    if (n_frames < 1 || width < 1 || height < 1) return set_error(PS_ERROR, "bad arguments");
+    const long long P = (long long)width * height;
+    const size_t n = size_t(n_frames) * P;
+    float* dd;
+    uint8_t* dv;
+    ps_status s = upload_map(ctx, prediction, prediction_valid, n, &dd, &dv);
+    if (s != PS_OK) return s;
+    ps::Engine& e = *ctx->engine;
+    uint8_t* dm = nullptr;
+    if (mask) {
+        dm = e.dev<uint8_t>(e.s_h, n);
+        if (!dm) return set_error(PS_CUDA_ERROR, "allocation failed");
+        cudaMemcpyAsync(dm, mask, n, cudaMemcpyHostToDevice, e.stream());
+    }
+    return accuracy_device(ctx, n_frames, dd, dv, ground_truth, ground_truth_valid, dm, P,
+                           thresholds, n_thresholds, fractions, evaluated, mean_abs_error);
+}
+
+ps_status ps_download_accuracy(ps_ctx* ctx, int which, const float* ground_truth,
+                               const uint8_t* ground_truth_valid, int use_mask,
+                               const double* thresholds, int n_thresholds, double* fractions,
+                               long long* evaluated, double* mean_abs_error) {
+    PS_REQUIRE_CTX(ctx);
+    ps::Engine::ResidentMaps m;
+    const float* d;
+    const uint8_t* v;
+    ps_status s = resident(ctx, which, m, &d, &v);
+    if (s != PS_OK) return s;
+    // a frame without a result has an all-invalid prediction: mask it out via
+    // its frame_ok entry by evaluating through a per-frame validity copy
+    ps::Engine& e = *ctx->engine;
+    std::vector<int> ok(m.frames);
+    cudaMemcpy(ok.data(), m.frame_ok, sizeof(int) * m.frames, cudaMemcpyDeviceToHost);
+    const uint8_t* pv = v;
+    bool any_failed = false;
+    for (int f = 0; f < m.frames; ++f) any_failed |= ok[f] == 0;
+    if (any_failed) {
+        uint8_t* copy = e.dev<uint8_t>(e.s_b, size_t(m.frames) * m.pixels);
+        if (!copy) return set_error(PS_CUDA_ERROR, "allocation failed");
+        for (int f = 0; f < m.frames; ++f) {
+            const size_t b = size_t(f) * m.pixels;
+            if (ok[f]) cudaMemcpyAsync(copy + b, v + b, m.pixels, cudaMemcpyDeviceToDevice, e.stream());
+            else cudaMemsetAsync(copy + b, 0, m.pixels, e.stream());
+        }
+        pv = copy;
+    }
+    return accuracy_device(ctx, m.frames, d, pv, ground_truth, ground_truth_valid,
+                           use_mask ? m.mask : nullptr, m.pixels, thresholds, n_thresholds,
+                           fractions, evaluated, mean_abs_error);
+}
+
 ps_status ps_refinement(ps_ctx* ctx, const float* interp, const uint8_t* interp_valid,
                         const float* cost, float* final_disparity, uint8_t* final_valid,
                         float* final_cost, const uint8_t* mask, int width, int height,

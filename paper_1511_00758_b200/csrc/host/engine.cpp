@@ -952,7 +952,8 @@ ps_status Engine::resident_maps(ResidentMaps& m) {
     if (s != PS_OK) return s;
     m = ResidentMaps{static_cast<const float*>(dDf_.p), static_cast<const uint8_t*>(dDv_.p),
                      static_cast<const float*>(dDense_.p), static_cast<const uint8_t*>(dDenseV_.p),
-                     static_cast<const uint8_t*>(dL_.p), ok, F_, W_, H_, P_};
+                     static_cast<const uint8_t*>(dL_.p), static_cast<const uint8_t*>(dMask_.p), ok,
+                     F_, W_, H_, P_};
     return PS_OK;
 }
 

@@ -92,6 +92,7 @@ public:
         const float* dense;
         const uint8_t* dense_valid;
         const uint8_t* left;
+        const uint8_t* mask;  // the run's gradient mask (Omega_I)
         const int* frame_ok;  // device, F entries
         int frames, width, height;
         long long pixels;

@@ -160,4 +160,12 @@ int launch_point_cloud(const float* d, const uint8_t* valid, const uint8_t* imag
                        float* xyz, uint8_t* intensity, int capacity, int* chunk_buf, int* count,
                        cudaStream_t st);
 
+// accuracy (proj/src/eval.cpp:19-70) over `frames` maps (accuracy.cu):
+// counts[f] = {evaluated, hits[0..n_thr)} (n_thr <= 16), err_sum[f] = the
+// row-major sequential binary64 error sum.  mask may be null.
+int launch_accuracy(const float* pred, const uint8_t* pred_valid, const float* gt,
+                    const uint8_t* gt_valid, const uint8_t* mask, long long P, int frames,
+                    const double* thresholds, int n_thr, unsigned long long* counts,
+                    double* err_sum, cudaStream_t st);
+
 }  // namespace ps

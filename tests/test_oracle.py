@@ -258,3 +258,20 @@ def test_oracle_encoders_reference_known_answers(orc):
     assert len(orc.point_cloud(np.zeros((16, 16), np.float32), np.zeros((16, 16), np.uint8),
                                img[:16, :16], (100.0, 0.5, 8.0, 8.0))[0]) == 0
     assert orc.point_cloud(d, ok, img, (0.0, 0.5, 0.0, 0.0))[0] is None
+
+
+def test_oracle_accuracy_equals_reference(orc, ref):
+    """accuracy restatement vs the compiled reference (proj/src/eval.cpp:19-70),
+    including the sequential binary64 error sum and NoOverlap."""
+    rng = np.random.default_rng(41)
+    for h, w in [(48, 64), (120, 160)]:
+        p = rng.uniform(0, 60, (h, w)).astype(np.float32)
+        pv = (rng.random((h, w)) < 0.8).astype(np.uint8)
+        g = (p + rng.normal(0, 2, (h, w))).astype(np.float32)
+        gv = (rng.random((h, w)) < 0.8).astype(np.uint8)
+        m = (rng.random((h, w)) < 0.6).astype(np.uint8)
+        for mm in (None, m):
+            a = orc.accuracy(p, pv, g, gv, mm, [0.5, 1.0, 2.0, 3.0])
+            b = ref.accuracy(p, pv, g, gv, mm, [0.5, 1.0, 2.0, 3.0])
+            assert a[0] == b[0] == 0 and np.array_equal(a[1], b[1]) and a[2] == b[2] and a[3] == b[3]
+    assert orc.accuracy(p, pv * 0, g, gv, None, [1.0])[0] == ref.accuracy(p, pv * 0, g, gv, None, [1.0])[0] == 13
