@@ -70,7 +70,8 @@ typedef enum ps_status {
     PS_CAPACITY = 10,               /* caller buffer too small (count written) */
     PS_NEGATIVE_DISPARITY = 11,     /* NegativeDisparity                   error.hpp:54 */
     PS_EMPTY_CLOUD = 12,            /* EmptyCloud                          error.hpp:59 */
-    PS_NO_OVERLAP = 13              /* NoOverlap                           error.hpp:64 */
+    PS_NO_OVERLAP = 13,             /* NoOverlap                           error.hpp:64 */
+    PS_INVALID_PLANE = 14           /* InvalidPlane                        error.hpp:69 */
 } ps_status;
 
 /* Run flags. */
@@ -307,6 +308,38 @@ ps_status ps_synth_pair(const ps_synth_params* params, uint8_t* left, uint8_t* r
 /* n_frames pairs with seeds params->seed + i, generated on `threads` host threads. */
 ps_status ps_synth_batch(const ps_synth_params* params, int n_frames, int threads, uint8_t* left,
                          uint8_t* right);
+
+/* The same generator on the device (bit-identical bytes, up to a 1-ulp
+ * difference of the device log/cos in the Gaussian noise, which in practice
+ * never changes a rounded byte): n_frames pairs with seeds params->seed + i,
+ * returned in host buffers (gt may be NULL). */
+ps_status ps_synth_batch_gpu(ps_ctx* ctx, const ps_synth_params* params, int n_frames,
+                             uint8_t* left, uint8_t* right, float* gt);
+/* ... or generated straight into the context's batch input buffers (as if
+ * ps_upload_batch had uploaded them): feeds ps_run_resident with no host
+ * generation and no host->device copy. */
+ps_status ps_synth_resident(ps_ctx* ctx, const ps_synth_params* params, int n_frames);
+
+/* renderScene (proj/include/planestereo/synth.hpp:13-50, proj/src/synth.cpp:
+ * 46-169) on the device: band-limited noise textures from mt19937(seed) and
+ * mt19937(seed+1), the left one forward-mapped into the right by the
+ * piecewise-planar ground truth (nearest wins; losers occluded, sources
+ * leaving the image invalid).  Regions must partition the image (PS_ERROR
+ * otherwise, with the reference's messages); a plane outside
+ * [0, max_disparity) inside its region is PS_INVALID_PLANE. */
+typedef struct ps_scene_region { /* SceneRegion: [u0,u1) x [v0,v1), d = a*u + b*v + c */
+    int u0;
+    int v0;
+    int u1;
+    int v1;
+    double a;
+    double b;
+    double c;
+} ps_scene_region;
+ps_status ps_render_scene(ps_ctx* ctx, int width, int height, float max_disparity, uint32_t seed,
+                          const ps_scene_region* regions, int n_regions, uint8_t* left,
+                          uint8_t* right, float* ground_truth, uint8_t* ground_truth_valid,
+                          uint8_t* occluded);
 
 #ifdef __cplusplus
 }

@@ -71,6 +71,7 @@ int statusOf(const std::exception& e) {
     if (dynamic_cast<const DegenerateTriangle*>(&e)) return PS_DEGENERATE_TRIANGLE;
     if (dynamic_cast<const SeedingFailed*>(&e)) return PS_SEEDING_FAILED;
     if (dynamic_cast<const NoOverlap*>(&e)) return PS_NO_OVERLAP;
+    if (dynamic_cast<const InvalidPlane*>(&e)) return PS_INVALID_PLANE;
     return PS_ERROR;
 }
 
@@ -396,6 +397,31 @@ int ref_render_scene(int kind, double p0, double p1, double p2, int w, int h, ui
         std::memcpy(left, r.left.data().data(), std::size_t(w) * h);
         std::memcpy(right, r.right.data().data(), std::size_t(w) * h);
         copyMap(r.groundTruth, gt, gt_valid);
+        return PS_OK;
+    } catch (const std::exception& e) {
+        return statusOf(e);
+    }
+}
+
+// renderScene over arbitrary regions (proj/src/synth.cpp:88-169), with the
+// occlusion map: the known answers for ps_render_scene.
+int ref_render_regions(int w, int h, float max_disparity, uint32_t seed, const int* box,
+                       const double* plane, int n, uint8_t* left, uint8_t* right, float* gt,
+                       uint8_t* gt_valid, uint8_t* occluded) {
+    try {
+        PlanarScene s;
+        s.width = w;
+        s.height = h;
+        s.maxDisparity = max_disparity;
+        s.seed = seed;
+        for (int k = 0; k < n; ++k)
+            s.regions.push_back({box[4 * k], box[4 * k + 1], box[4 * k + 2], box[4 * k + 3],
+                                 {plane[3 * k], plane[3 * k + 1], plane[3 * k + 2]}});
+        RenderedScene r = renderScene(s);
+        std::memcpy(left, r.left.data().data(), std::size_t(w) * h);
+        std::memcpy(right, r.right.data().data(), std::size_t(w) * h);
+        copyMap(r.groundTruth, gt, gt_valid);
+        std::memcpy(occluded, r.occlusion.data(), std::size_t(w) * h);
         return PS_OK;
     } catch (const std::exception& e) {
         return statusOf(e);

@@ -70,6 +70,10 @@ class NoOverlap(Error):
     pass
 
 
+class InvalidPlane(Error):
+    pass
+
+
 class CudaError(Error):
     pass
 
@@ -82,6 +86,7 @@ _STATUS = {
     1: Error, 2: InvalidConfig, 3: DimensionTooSmall, 4: DimensionMismatch,
     5: FewerThanThreePoints, 6: DegenerateTriangle, 7: SeedingFailed, 8: CudaError,
     9: NoDevice, 10: Error, 11: NegativeDisparity, 12: EmptyCloud, 13: NoOverlap,
+    14: InvalidPlane,
 }
 
 
@@ -559,6 +564,44 @@ class Context:
                                               _ptr(th), len(th), _ptr(fr), _ptr(ev), _ptr(mae)))
         return fr, ev, mae
 
+    # ------------------------------------------------ on-device generation
+    def synth_batch(self, n: int, width: int, height: int, n_planes: int, max_disparity: int,
+                    ground: bool = False, noise_sigma: float = 2.0, seed: int = 0,
+                    with_gt: bool = False):
+        """The BASELINE generator (synth_batch) run on the GPU: same bytes."""
+        p = _native.PsSynthParams(width, height, n_planes, max_disparity, 1 if ground else 0,
+                                  noise_sigma, seed)
+        L = np.zeros((n, height, width), np.uint8)
+        R = np.zeros((n, height, width), np.uint8)
+        gt = np.zeros((n, height, width), np.float32) if with_gt else None
+        _check(self._lib.ps_synth_batch_gpu(self._h, C.byref(p), n, _ptr(L), _ptr(R), _ptr(gt)))
+        return (L, R, gt) if with_gt else (L, R)
+
+    def synth_resident(self, n: int, width: int, height: int, n_planes: int, max_disparity: int,
+                       ground: bool = False, noise_sigma: float = 2.0, seed: int = 0) -> None:
+        """Generate the batch straight into the device input buffers (then run_resident)."""
+        p = _native.PsSynthParams(width, height, n_planes, max_disparity, 1 if ground else 0,
+                                  noise_sigma, seed)
+        _check(self._lib.ps_synth_resident(self._h, C.byref(p), n))
+        self._shape = (n, height, width)
+
+    def render_scene(self, width: int, height: int, regions, max_disparity: float = 128.0,
+                     seed: int = 1234):
+        """renderScene (proj/src/synth.cpp:88-169) on the GPU.  regions: sequence
+        of (u0, v0, u1, v1, a, b, c).  -> dict(left, right, gt, gt_valid, occluded)."""
+        regs = (_native.PsSceneRegion * max(1, len(regions)))()
+        for k, r in enumerate(regions):
+            regs[k] = _native.PsSceneRegion(int(r[0]), int(r[1]), int(r[2]), int(r[3]),
+                                            float(r[4]), float(r[5]), float(r[6]))
+        out = {k: np.zeros((height, width), dt) for k, dt in
+               [("left", np.uint8), ("right", np.uint8), ("gt", np.float32),
+                ("gt_valid", np.uint8), ("occluded", np.uint8)]}
+        _check(self._lib.ps_render_scene(self._h, width, height, float(max_disparity), seed, regs,
+                                         len(regions), _ptr(out["left"]), _ptr(out["right"]),
+                                         _ptr(out["gt"]), _ptr(out["gt_valid"]),
+                                         _ptr(out["occluded"])))
+        return out
+
     def _resident_shape(self):
         if not getattr(self, "_shape", None):
             raise Error("no batch uploaded through this Context")
@@ -643,6 +686,7 @@ def baseline_config(idx: int) -> PipelineConfig:
 __all__ = [
     "Error", "InvalidConfig", "DimensionTooSmall", "DimensionMismatch", "FewerThanThreePoints",
     "DegenerateTriangle", "SeedingFailed", "NegativeDisparity", "EmptyCloud", "NoOverlap",
+    "InvalidPlane",
     "CudaError", "NoDevice", "PipelineConfig",
     "IterationStats", "StereoResult", "Context", "delaunay_triangulate", "synth_pair",
     "synth_batch", "BASELINE_CONFIGS", "baseline_config", "PS_RUN_UNCHECKED_CELL",

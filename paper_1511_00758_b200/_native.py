@@ -76,6 +76,13 @@ class PsCell(C.Structure):
     ]
 
 
+class PsSceneRegion(C.Structure):
+    """SceneRegion (proj/include/planestereo/synth.hpp:13-20)."""
+
+    _fields_ = [("u0", C.c_int), ("v0", C.c_int), ("u1", C.c_int), ("v1", C.c_int),
+                ("a", C.c_double), ("b", C.c_double), ("c", C.c_double)]
+
+
 class PsCalib(C.Structure):
     """CameraCalib (proj/include/planestereo/io.hpp:17-24)."""
 
@@ -133,6 +140,9 @@ SIGNATURES = {
     "ps_download_accuracy": (I, [P, I, P, P, I, P, I, P, P, P]),
     "ps_synth_pair": (I, [P, P, P, P]),
     "ps_synth_batch": (I, [P, I, I, P, P]),
+    "ps_synth_batch_gpu": (I, [P, P, I, P, P, P]),
+    "ps_synth_resident": (I, [P, P, I]),
+    "ps_render_scene": (I, [P, I, I, F, C.c_uint32, P, I, P, P, P, P, P]),
 }
 
 _lib = None

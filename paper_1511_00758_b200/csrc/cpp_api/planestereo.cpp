@@ -30,6 +30,7 @@ namespace {
         case PS_NEGATIVE_DISPARITY: throw NegativeDisparity(msg);
         case PS_EMPTY_CLOUD: throw EmptyCloud(msg);
         case PS_NO_OVERLAP: throw NoOverlap(msg);
+        case PS_INVALID_PLANE: throw InvalidPlane(msg);
         default: throw Error(msg);
     }
 }

@@ -830,6 +830,139 @@ ps_status ps_download_accuracy(ps_ctx* ctx, int which, const float* ground_truth
                            fractions, evaluated, mean_abs_error);
 }
 
+namespace {
+// BASELINE generator on the device into (d_left, d_right) with frame stride P.
+ps_status synth_device(ps_ctx* ctx, const ps_synth_params* p, int n_frames, uint8_t* d_left,
+                       uint8_t* d_right, float** d_gt_out) {
+    ps::Engine& e = *ctx->engine;
+    const long long P = (long long)p->width * p->height;
+    const long long draws = ps::baseline_stream_draws(p->width, p->height, p->n_planes);
+    uint32_t* d_seeds = e.dev<uint32_t>(e.s_a, size_t(n_frames));
+    uint32_t* d_stream = e.dev<uint32_t>(e.s_b, size_t(n_frames) * draws);
+    float* d_disp = e.dev<float>(e.s_c, size_t(n_frames) * P);
+    unsigned long long* d_keys = e.dev<unsigned long long>(e.s_d, size_t(n_frames) * P);
+    if (!d_seeds || !d_stream || !d_disp || !d_keys) return set_error(PS_CUDA_ERROR, "allocation failed");
+    std::vector<uint32_t> seeds(n_frames);
+    for (int f = 0; f < n_frames; ++f) seeds[f] = p->seed + uint32_t(f);
+    cudaStream_t st = e.stream();
+    cudaMemcpyAsync(d_seeds, seeds.data(), sizeof(uint32_t) * n_frames, cudaMemcpyHostToDevice, st);
+    e.count_launches(ps::launch_mt_streams(d_seeds, n_frames, draws, draws, d_stream, st));
+    e.count_launches(ps::launch_synth_baseline(*p, n_frames, d_stream, draws, d_disp, d_keys,
+                                               d_left, d_right, P, st));
+    if (d_gt_out) *d_gt_out = d_disp;
+    return from_engine(ctx, e.sync("synth"));
+}
+
+ps_status check_synth(const ps_synth_params* p, int n_frames) {
+    if (!p || n_frames < 1) return set_error(PS_ERROR, "bad generator arguments");
+    if (p->width < 16 || p->height < 16) return set_error(PS_DIMENSION_TOO_SMALL, "image must be at least 16x16");
+    if (p->n_planes < 0 || p->n_planes > 4096) return set_error(PS_ERROR, "0..4096 planes");
+    return PS_OK;
+}
+}  // namespace
+
+ps_status ps_synth_batch_gpu(ps_ctx* ctx, const ps_synth_params* params, int n_frames,
+                             uint8_t* left, uint8_t* right, float* gt) {
+    PS_REQUIRE_CTX(ctx);
+    ps_status s = check_synth(params, n_frames);
+    if (s != PS_OK) return s;
+    if (!left || !right) return set_error(PS_ERROR, "null output");
+    ps::Engine& e = *ctx->engine;
+    const size_t n = size_t(n_frames) * params->width * params->height;
+    uint8_t* dl = e.dev<uint8_t>(e.s_e, n);
+    uint8_t* dr = e.dev<uint8_t>(e.s_f, n);
+    if (!dl || !dr) return set_error(PS_CUDA_ERROR, "allocation failed");
+    float* dg = nullptr;
+    s = synth_device(ctx, params, n_frames, dl, dr, &dg);
+    if (s != PS_OK) return s;
+    cudaStream_t st = e.stream();
+    cudaMemcpyAsync(left, dl, n, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(right, dr, n, cudaMemcpyDeviceToHost, st);
+    if (gt) cudaMemcpyAsync(gt, dg, 4 * n, cudaMemcpyDeviceToHost, st);
+    return from_engine(ctx, e.sync("synth D2H"));
+}
+
+ps_status ps_synth_resident(ps_ctx* ctx, const ps_synth_params* params, int n_frames) {
+    PS_REQUIRE_CTX(ctx);
+    ps_status s = check_synth(params, n_frames);
+    if (s != PS_OK) return s;
+    uint8_t *dl = nullptr, *dr = nullptr;
+    s = from_engine(ctx, ctx->engine->device_inputs(n_frames, params->width, params->height, &dl, &dr));
+    if (s != PS_OK) return s;
+    return synth_device(ctx, params, n_frames, dl, dr, nullptr);
+}
+
+ps_status ps_render_scene(ps_ctx* ctx, int width, int height, float max_disparity, uint32_t seed,
+                          const ps_scene_region* regions, int n_regions, uint8_t* left,
+                          uint8_t* right, float* ground_truth, uint8_t* ground_truth_valid,
+                          uint8_t* occluded) {
+    PS_REQUIRE_CTX(ctx);
+    if (width < 1 || height < 1 || (n_regions > 0 && !regions) || n_regions < 0)
+        return set_error(PS_ERROR, "bad scene arguments");
+    if (!left || !right || !ground_truth || !ground_truth_valid || !occluded)
+        return set_error(PS_ERROR, "null output");
+    const int w = width, h = height;
+    // region checks (proj/src/synth.cpp:94-110), on the host: regions are few
+    std::vector<uint8_t> covered(size_t(w) * h, 0);
+    for (int k = 0; k < n_regions; ++k) {
+        const ps_scene_region& r = regions[k];
+        if (r.u0 < 0 || r.v0 < 0 || r.u1 > w || r.v1 > h || r.u0 >= r.u1 || r.v0 >= r.v1)
+            return set_error(PS_ERROR, "scene region outside image bounds");
+        for (int v = r.v0; v < r.v1; ++v)
+            for (int u = r.u0; u < r.u1; ++u)
+                if (covered[size_t(v) * w + u]++) return set_error(PS_ERROR, "scene regions overlap");
+    }
+    for (uint8_t c : covered)
+        if (c != 1) return set_error(PS_ERROR, "scene regions must cover the image");
+    ps::Engine& e = *ctx->engine;
+    const long long P = (long long)w * h;
+    ps::SceneRegionDev* d_reg = e.dev<ps::SceneRegionDev>(e.s_a, size_t(std::max(1, n_regions)));
+    uint32_t* d_seeds = e.dev<uint32_t>(e.s_b, 2);
+    uint32_t* d_stream = e.dev<uint32_t>(e.s_c, size_t(2 * P));
+    int* d_ta = e.dev<int>(e.s_d, size_t(P));
+    int* d_tb = e.dev<int>(e.s_e, size_t(P));
+    int* d_mm = e.dev<int>(e.s_f, 4);
+    unsigned long long* d_keys = e.dev<unsigned long long>(e.s_g, size_t(P));
+    unsigned long long* d_bad = e.dev<unsigned long long>(e.s_h, 1);
+    uint8_t* d_out = e.dev<uint8_t>(e.s_i, size_t(4 * P));  // left, right, gt_valid, occluded
+    float* d_gt = e.dev<float>(e.s_j, size_t(P));
+    if (!d_reg || !d_seeds || !d_stream || !d_ta || !d_tb || !d_mm || !d_keys || !d_bad || !d_out || !d_gt)
+        return set_error(PS_CUDA_ERROR, "allocation failed");
+    std::vector<ps::SceneRegionDev> reg(n_regions);
+    for (int k = 0; k < n_regions; ++k)
+        reg[k] = {regions[k].u0, regions[k].v0, regions[k].u1, regions[k].v1, regions[k].a,
+                  regions[k].b, regions[k].c};
+    const uint32_t seeds[2] = {seed, seed + 1};
+    cudaStream_t st = e.stream();
+    if (n_regions > 0)
+        cudaMemcpyAsync(d_reg, reg.data(), sizeof(ps::SceneRegionDev) * n_regions, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_seeds, seeds, sizeof(seeds), cudaMemcpyHostToDevice, st);
+    e.count_launches(ps::launch_mt_streams(d_seeds, 2, P, P, d_stream, st));
+    e.count_launches(ps::launch_render_scene(w, h, max_disparity, d_reg, n_regions, d_stream,
+                                             d_stream + P, d_ta, d_tb, d_mm, d_keys, d_bad, d_out,
+                                             d_out + P, d_gt, d_out + 2 * P, d_out + 3 * P, st));
+    unsigned long long bad = 0;
+    cudaMemcpyAsync(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost, st);
+    ps_status s = from_engine(ctx, e.sync("render scene"));
+    if (s != PS_OK) return s;
+    if (bad != ~0ull) {  // renderScene throws InvalidPlane at the first offending pixel
+        const int k = int(bad >> 40);
+        const long long i = (long long)(bad & ((1ull << 40) - 1));
+        const int v = int(i / w), u = int(i - (long long)v * w);
+        const ps_scene_region& r = regions[k];
+        const double d = r.a * u + r.b * v + r.c;
+        return set_error(PS_INVALID_PLANE, "plane value " + std::to_string(d) + " at (" +
+                                               std::to_string(u) + "," + std::to_string(v) +
+                                               ") outside [0, " + std::to_string(max_disparity) + ")");
+    }
+    cudaMemcpyAsync(left, d_out, P, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(right, d_out + P, P, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(ground_truth_valid, d_out + 2 * P, P, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(occluded, d_out + 3 * P, P, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(ground_truth, d_gt, 4 * P, cudaMemcpyDeviceToHost, st);
+    return from_engine(ctx, e.sync("render scene D2H"));
+}
+
 ps_status ps_refinement(ps_ctx* ctx, const float* interp, const uint8_t* interp_valid,
                         const float* cost, float* final_disparity, uint8_t* final_valid,
                         float* final_cost, const uint8_t* mask, int width, int height,

@@ -211,6 +211,7 @@ template float* Engine::dev<float>(DevBuf&, size_t);
 template double* Engine::dev<double>(DevBuf&, size_t);
 template unsigned long long* Engine::dev<unsigned long long>(DevBuf&, size_t);
 template int2* Engine::dev<int2>(DevBuf&, size_t);
+template SceneRegionDev* Engine::dev<SceneRegionDev>(DevBuf&, size_t);
 template int* Engine::host<int>(HostBuf&, size_t);
 template uint8_t* Engine::host<uint8_t>(HostBuf&, size_t);
 
@@ -293,6 +294,28 @@ ps_status Engine::upload(int frames, const uint8_t* left, const uint8_t* right, 
     if (s != PS_OK) return s;
     s = check(cudaMemcpyAsync(dr, right, n, cudaMemcpyHostToDevice, st_), "H2D right");
     if (s != PS_OK) return s;
+    have_inputs_ = true;
+    have_outputs_ = false;
+    streamed_ = false;
+    return PS_OK;
+}
+
+ps_status Engine::device_inputs(int frames, int width, int height, uint8_t** left,
+                                uint8_t** right) {
+    if (width < 16 || height < 16)
+        return fail(PS_DIMENSION_TOO_SMALL, "image must be at least 16x16, got " +
+                                                std::to_string(width) + "x" +
+                                                std::to_string(height));
+    if (frames < 1) return fail(PS_ERROR, "batch needs at least one frame");
+    cudaSetDevice(device_);
+    F_ = frames;
+    W_ = width;
+    H_ = height;
+    P_ = (long long)width * height;
+    const size_t n = size_t(F_) * P_;
+    *left = dev<uint8_t>(dL_, n);
+    *right = dev<uint8_t>(dR_, n);
+    if (!*left || !*right) return fail(PS_CUDA_ERROR, "device allocation failed (images)");
     have_inputs_ = true;
     have_outputs_ = false;
     streamed_ = false;

@@ -71,6 +71,9 @@ public:
     std::string& error() { return err_; }
 
     ps_status upload(int frames, const uint8_t* left, const uint8_t* right, int width, int height);
+    // The batch input buffers themselves, for inputs generated on the device
+    // (ps_synth_resident); afterwards the batch counts as uploaded.
+    ps_status device_inputs(int frames, int width, int height, uint8_t** left, uint8_t** right);
     ps_status run_resident(const ps_config& cfg, unsigned flags, ps_observer_fn observer = nullptr,
                            void* user = nullptr);
     ps_status download(float* disparity, uint8_t* disparity_valid, float* cost, float* dense,

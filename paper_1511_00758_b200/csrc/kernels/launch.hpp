@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include "common.cuh"
+#include "planestereo_c.h"
 
 namespace ps {
 
@@ -167,5 +168,24 @@ int launch_accuracy(const float* pred, const uint8_t* pred_valid, const float* g
                     const uint8_t* gt_valid, const uint8_t* mask, long long P, int frames,
                     const double* thresholds, int n_thr, unsigned long long* counts,
                     double* err_sum, cudaStream_t st);
+
+// On-device scene generation (synth.cpp in kernels/): mt19937 output streams
+// (one CTA per seed), the BASELINE generator of host/synth.cpp (same bytes),
+// and the reference's renderScene (proj/src/synth.cpp:46-169).
+struct SceneRegionDev {  // SceneRegion, proj/include/planestereo/synth.hpp:13-20
+    int u0, v0, u1, v1;
+    double a, b, c;
+};
+int launch_mt_streams(const uint32_t* seeds, int streams, long long n, long long stride,
+                      uint32_t* out, cudaStream_t st);
+long long baseline_stream_draws(int w, int h, int n_planes);
+int launch_synth_baseline(const ps_synth_params& p, int frames, const uint32_t* stream,
+                          long long stride, float* disp, unsigned long long* keys, uint8_t* left,
+                          uint8_t* right, long long img_stride, cudaStream_t st);
+int launch_render_scene(int w, int h, float max_disp, const SceneRegionDev* regions,
+                        int n_regions, const uint32_t* stream_left, const uint32_t* stream_right,
+                        int* tmp_a, int* tmp_b, int* minmax, unsigned long long* keys,
+                        unsigned long long* bad, uint8_t* left, uint8_t* right, float* gt,
+                        uint8_t* gt_valid, uint8_t* occluded, cudaStream_t st);
 
 }  // namespace ps

@@ -194,11 +194,53 @@ def gen_wta(ref):
     print("wta_cases ok")
 
 
+def gen_render(ref):
+    """renderScene known answers (proj/src/synth.cpp:88-169) over region lists,
+    with the occlusion map and the reference's error statuses."""
+    fn = ref.lib.ref_render_regions
+    fn.restype = C.c_int
+    fn.argtypes = [C.c_int, C.c_int, C.c_float, C.c_uint32, C.c_void_p, C.c_void_p, C.c_int,
+                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    p = lambda a: a.ctypes.data_as(C.c_void_p)
+    cases = {
+        "flat7_96x64": (96, 64, 128.0, 1234, [(0, 0, 96, 64, 0.0, 0.0, 7.0)]),
+        "slanted_128x96": (128, 96, 128.0, 1234, [(0, 0, 128, 96, 0.08, 0.02, 6.0)]),
+        "steps_97x61": (97, 61, 64.0, 77, [(0, 0, 48, 61, 0.0, 0.0, 5.0), (48, 0, 97, 61, 0.0, 0.0, 17.0)]),
+        "quad_160x120": (160, 120, 96.0, 9, [(0, 0, 70, 50, 0.01, -0.02, 20.0),
+                                             (70, 0, 160, 50, -0.05, 0.0, 30.5),
+                                             (0, 50, 90, 120, 0.0, 0.1, 3.25),
+                                             (90, 50, 160, 120, 0.0, 0.0, 0.0)]),
+        "err_plane": (64, 48, 16.0, 1, [(0, 0, 64, 48, 0.3, 0.0, 0.5)]),
+        "err_overlap": (64, 48, 128.0, 1, [(0, 0, 40, 48, 0, 0, 3), (30, 0, 64, 48, 0, 0, 3)]),
+        "err_cover": (64, 48, 128.0, 1, [(0, 0, 40, 48, 0, 0, 3)]),
+        "err_bounds": (64, 48, 128.0, 1, [(0, 0, 65, 48, 0, 0, 3)]),
+    }
+    arrays = {}
+    for name, (w, h, md, seed, regs) in cases.items():
+        box = np.array([r[:4] for r in regs], np.int32)
+        pl = np.array([r[4:] for r in regs], np.float64)
+        L = np.zeros((h, w), np.uint8)
+        R = np.zeros((h, w), np.uint8)
+        g = np.zeros((h, w), np.float32)
+        gv = np.zeros((h, w), np.uint8)
+        oc = np.zeros((h, w), np.uint8)
+        st = fn(w, h, md, seed, p(box), p(pl), len(regs), p(L), p(R), p(g), p(gv), p(oc))
+        arrays.update({f"{name}_box": box, f"{name}_plane": pl, f"{name}_status": np.int32(st),
+                       f"{name}_geom": np.array([w, h, seed], np.int64), f"{name}_maxd": np.float32(md)})
+        if st == 0:
+            arrays.update({f"{name}_left": L, f"{name}_right": R, f"{name}_gt": g,
+                           f"{name}_gt_valid": gv, f"{name}_occluded": oc})
+        print(name, "status", st)
+    arrays["cases"] = np.array(json.dumps(sorted(cases)))
+    np.savez_compressed(os.path.join(HERE, "render_cases.npz"), **arrays)
+
+
 if __name__ == "__main__":
-    if sys.argv[1:] == ["wta"]:
+    if sys.argv[1:] in (["wta"], ["render"]):
         ref = oracle.load_ref()
         assert ref is not None, "build oracle/_ref first (make -C oracle ref)"
-        gen_wta(ref)
+        (gen_wta if sys.argv[1] == "wta" else gen_render)(ref)
     else:
         main()
         gen_wta(oracle.load_ref())
+        gen_render(oracle.load_ref())
