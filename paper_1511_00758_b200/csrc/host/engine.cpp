@@ -16,9 +16,12 @@
 #include <chrono>
 #include <cmath>
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <thread>
+
+#include <sched.h>
 
 #include "../kernels/launch.hpp"
 
@@ -123,12 +126,31 @@ bool trace_fixed_exact(float cost_high) {
     return x == std::floor(x);
 }
 
+// Host worker threads for the Delaunay tasks: PS_HOST_THREADS if set, else
+// the CPUs this process may run on (affinity / cpuset), shared evenly between
+// the ranks of a node (LOCAL_WORLD_SIZE, set by torchrun) so N GPUs' engines
+// do not oversubscribe the host.
+static int host_threads() {
+    if (const char* e = std::getenv("PS_HOST_THREADS")) {
+        const int n = std::atoi(e);
+        if (n > 0) return n;
+    }
+    int n = int(std::max(1u, std::thread::hardware_concurrency()));
+    cpu_set_t set;
+    CPU_ZERO(&set);
+    if (sched_getaffinity(0, sizeof(set), &set) == 0 && CPU_COUNT(&set) > 0) n = CPU_COUNT(&set);
+    if (const char* l = std::getenv("LOCAL_WORLD_SIZE")) {
+        const int k = std::atoi(l);
+        if (k > 1) n = std::max(1, n / k);
+    }
+    return n;
+}
+
 Engine::Engine(int device) : device_(device) {
     cudaSetDevice(device_);
     cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking);
     for (FrameGroup& g : groups_) cudaStreamCreateWithFlags(&g.st, cudaStreamNonBlocking);
-    const int hw = std::max(1u, std::thread::hardware_concurrency());
-    pool_ = new ThreadPool(hw);
+    pool_ = new ThreadPool(host_threads());
     ws_.resize(pool_->size());
 }
 
