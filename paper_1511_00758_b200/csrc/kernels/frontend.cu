@@ -141,27 +141,48 @@ __device__ __forceinline__ bool arc9(unsigned m16) {
     return (a & 0xffffu) != 0;
 }
 
-// Segment test at (u, v) (sparse.cpp:94-122); returns the score (> 0) or 0.
-__device__ __forceinline__ int corner_score(const uint8_t* __restrict__ L, int W, int u, int v,
-                                            int t) {
-    const int c = __ldg(L + (long long)v * W + u);
+// Segment test at (u, v) (sparse.cpp:94-122) on a shared-memory tile,
+// p(k) = s[base + off[k]]; returns the score (> 0, >= 9 for any accepted
+// corner) or 0.  The four compass pixels first, so a rejected pixel (the vast
+// majority) costs five shared loads.
+__device__ __forceinline__ int corner_score_s(const uint8_t* __restrict__ s, int base,
+                                              const int (&off)[16], int t) {
+    const int c = s[base];
     const int hi = c + t, lo = c - t;
-    int p[16];
-#pragma unroll
-    for (int k = 0; k < 16; ++k) p[k] = __ldg(L + (long long)(v + c_ring_v[k]) * W + (u + c_ring_u[k]));
-    const int nb = (p[0] > hi) + (p[4] > hi) + (p[8] > hi) + (p[12] > hi);
-    const int nd = (p[0] < lo) + (p[4] < lo) + (p[8] < lo) + (p[12] < lo);
+    const int p0 = s[base + off[0]], p4 = s[base + off[4]], p8 = s[base + off[8]],
+              p12 = s[base + off[12]];
+    const int nb = (p0 > hi) + (p4 > hi) + (p8 > hi) + (p12 > hi);
+    const int nd = (p0 < lo) + (p4 < lo) + (p8 < lo) + (p12 < lo);
     if (nb < 2 && nd < 2) return 0;
     unsigned bright = 0, dark = 0;
     int score = 0;
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
-        bright |= unsigned(p[k] > hi) << k;
-        dark |= unsigned(p[k] < lo) << k;
-        score += max(0, abs(p[k] - c) - t);
+        const int p = s[base + off[k]];
+        bright |= unsigned(p > hi) << k;
+        dark |= unsigned(p < lo) << k;
+        score += max(0, abs(p - c) - t);
     }
     if (!arc9(bright) && !arc9(dark)) return 0;
-    return score;  // >= 9 for any accepted corner
+    return score;
+}
+
+// Stage the bin [ulo, uhi) x [vlo, vhi) plus the 3-pixel ring halo into
+// shared memory (row stride sw) and set up the ring offsets.  Rows vlo-3 ..
+// vhi+2 and columns ulo-3 .. uhi+2 are inside the image (bin_range keeps a
+// 3-pixel margin).
+__device__ __forceinline__ void stage_bin(const uint8_t* __restrict__ L, int W, int ulo, int uhi,
+                                          int vlo, int vhi, uint8_t* __restrict__ s, int sw,
+                                          int (&off)[16]) {
+    const int tw = uhi - ulo + 6, th = vhi - vlo + 6;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int r = warp; r < th; r += nw) {
+        const uint8_t* src = L + (long long)(vlo - 3 + r) * W + (ulo - 3);
+        for (int c = lane; c < tw; c += 32) s[r * sw + c] = __ldg(src + c);
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) off[k] = c_ring_v[k] * sw + c_ring_u[k];
+    __syncthreads();
 }
 
 __device__ __forceinline__ unsigned long long corner_key(int score, int u, int v) {
@@ -201,6 +222,7 @@ __global__ void __launch_bounds__(256) k_corner_bins(const uint8_t* __restrict__
                                                      int* __restrict__ bin_count) {
     __shared__ unsigned long long lists[256][LK];
     __shared__ unsigned long long red[33];
+    extern __shared__ uint8_t s_tile[];
     const int f = blockIdx.y, bin = blockIdx.x;
     const int bu = bin % 12, bv = bin / 12;
     int ulo, uhi, vlo, vhi;
@@ -211,11 +233,23 @@ __global__ void __launch_bounds__(256) k_corner_bins(const uint8_t* __restrict__
 #pragma unroll
     for (int k = 0; k < LK; ++k) best[k] = kEmptyCell;
     const int bw = uhi - ulo, bh = vhi - vlo;
-    if (bw > 0 && bh > 0) {
+    if (bw > 0 && bh > 0) {  // block-uniform
+        const int sw = bw + 6;
+        int off[16];
+        stage_bin(L, g.width, ulo, uhi, vlo, vhi, s_tile, sw, off);
         const int n = bw * bh;
+        // (u, v) of pixel i = tid + 256 j, advanced without divisions
+        int cu = int(threadIdx.x) % bw, cv = int(threadIdx.x) / bw;
+        const int su = int(blockDim.x) % bw, sv = int(blockDim.x) / bw;
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
-            const int v = vlo + i / bw, u = ulo + i % bw;
-            const int s = corner_score(L, g.width, u, v, t);
+            const int u = ulo + cu, v = vlo + cv;
+            const int s = corner_score_s(s_tile, (cv + 3) * sw + cu + 3, off, t);
+            cu += su;
+            cv += sv;
+            if (cu >= bw) {
+                cu -= bw;
+                ++cv;
+            }
             if (s == 0) continue;
             unsigned long long key = corner_key(s, u, v);
             if (key >= best[LK - 1]) continue;
@@ -250,6 +284,7 @@ __global__ void __launch_bounds__(256) k_corner_bins_generic(
     unsigned long long* __restrict__ bin_keys, int* __restrict__ bin_count) {
     __shared__ unsigned long long red[33];
     __shared__ int n_keys;
+    extern __shared__ uint8_t s_tile[];
     const int f = blockIdx.y, bin = blockIdx.x;
     const int bu = bin % 12, bv = bin / 12;
     int ulo, uhi, vlo, vhi;
@@ -260,11 +295,22 @@ __global__ void __launch_bounds__(256) k_corner_bins_generic(
     if (threadIdx.x == 0) n_keys = 0;
     __syncthreads();
     const int bw = uhi - ulo, bh = vhi - vlo;
-    if (bw > 0 && bh > 0) {
+    if (bw > 0 && bh > 0) {  // block-uniform
+        const int sw = bw + 6;
+        int off[16];
+        stage_bin(L, g.width, ulo, uhi, vlo, vhi, s_tile, sw, off);
         const int n = bw * bh;
+        int cu = int(threadIdx.x) % bw, cv = int(threadIdx.x) / bw;
+        const int su = int(blockDim.x) % bw, sv = int(blockDim.x) / bw;
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
-            const int v = vlo + i / bw, u = ulo + i % bw;
-            const int s = corner_score(L, g.width, u, v, t);
+            const int u = ulo + cu, v = vlo + cv;
+            const int s = corner_score_s(s_tile, (cv + 3) * sw + cu + 3, off, t);
+            cu += su;
+            cv += sv;
+            if (cu >= bw) {
+                cu -= bw;
+                ++cv;
+            }
             if (s == 0) continue;
             sc[atomicAdd(&n_keys, 1)] = corner_key(s, u, v);
         }
@@ -366,13 +412,25 @@ int launch_candidates(const uint8_t* left, FrameGeom g, int frames, int corner_t
                       long long scratch_stride, int* cand_u, int* cand_v, float* cand_score,
                       int* cand_count, int cand_stride, cudaStream_t st) {
     dim3 grid(120, frames);
+    // bin tile + ring halo (bins are at most ceil(n/nb) + 1 wide, bin_range)
+    const size_t tile = size_t((g.width + 11) / 12 + 1 + 6) * size_t((g.height + 9) / 10 + 1 + 6);
+    static size_t configured[3] = {0, 0, 0};
+    auto allow = [&](const void* fn, int which, size_t static_bytes) {
+        if (tile + static_bytes > 48 * 1024 && tile > configured[which]) {
+            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(tile));
+            configured[which] = tile;
+        }
+    };
     if (cap <= 4) {
-        k_corner_bins<4><<<grid, 256, 0, st>>>(left, g, corner_threshold, cap, bin_keys, bin_count);
+        allow((const void*)k_corner_bins<4>, 0, 256 * 4 * 8 + 264);
+        k_corner_bins<4><<<grid, 256, tile, st>>>(left, g, corner_threshold, cap, bin_keys, bin_count);
     } else if (cap <= 8) {
-        k_corner_bins<8><<<grid, 256, 0, st>>>(left, g, corner_threshold, cap, bin_keys, bin_count);
+        allow((const void*)k_corner_bins<8>, 1, 256 * 8 * 8 + 264);
+        k_corner_bins<8><<<grid, 256, tile, st>>>(left, g, corner_threshold, cap, bin_keys, bin_count);
     } else {
-        k_corner_bins_generic<<<grid, 256, 0, st>>>(left, g, corner_threshold, cap, scratch,
-                                                    scratch_stride, bin_keys, bin_count);
+        allow((const void*)k_corner_bins_generic, 2, 272);
+        k_corner_bins_generic<<<grid, 256, tile, st>>>(left, g, corner_threshold, cap, scratch,
+                                                       scratch_stride, bin_keys, bin_count);
     }
     const int n = 120 * cap;
     int n_pow2 = 1;
