@@ -27,6 +27,8 @@
 // slot.  Algorithmic traffic P + 29*M bytes per frame.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "launch.hpp"
 
 namespace ps {
@@ -220,7 +222,7 @@ __device__ __forceinline__ void bar_wait(unsigned long long* bar, unsigned phase
         "{\n"
         ".reg .pred P1;\n"
         "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, 1000000;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
         "@!P1 bra WAIT_%=;\n"
         "}\n" :: "r"(smem_u32(bar)), "r"(phase) : "memory");
 }
@@ -234,7 +236,7 @@ struct BulkGeom {
     int r_tile;       // kTile % W
 };
 
-template <bool LAST, bool KEY32, int SPAN>
+template <bool LAST, bool KEY32, int SPAN, bool VEC>
 __global__ void __launch_bounds__(256, 4) k_refine_bulk(RefineArgs a, CostTables tab,
                                                         unsigned magic_cell31, unsigned magic_w,
                                                         BulkGeom bg) {
@@ -322,6 +324,145 @@ __global__ void __launch_bounds__(256, 4) k_refine_bulk(RefineArgs a, CostTables
         const int tb = f * P + off;  // first pixel of the tile within the batch
         unsigned long long* Cg_f = a.Cg + (long long)f * a.cell_stride;
         unsigned long long* Cb_f = a.Cb + (long long)f * a.cell_stride;
+        if constexpr (VEC) {
+            // 4 contiguous pixels per lane: p = warp*128 + 4*lane + j.  Vector
+            // stage loads; the pixels of a cell inside the lane are folded in
+            // order (first minimum wins) and each (cell, lane) segment issues
+            // one fire-and-forget atomicMin (RED) per grid.
+            const int p0 = warp * kWarpPx + 4 * lane;
+            const bool in = p0 < n_in;  // n_in % 16 == 0: all four or none
+            const float4 d4 = *reinterpret_cast<const float4*>(sm_dit + p0);
+            const uint4 cl4 = *reinterpret_cast<const uint4*>(sm_cl + p0);
+            const unsigned code4 = *reinterpret_cast<const unsigned*>(sm_code + p0);
+            const float dd[4] = {d4.x, d4.y, d4.z, d4.w};
+            const uint32_t cl[4] = {cl4.x, cl4.y, cl4.z, cl4.w};
+            const int r = r0 + p0;
+            const int dv = int(__umulhi(unsigned(r), magic_w));  // W >= 32
+            int uc[4], cellv[4];
+            uint32_t crv[4];
+            unsigned okm = 0;
+            {
+                int u = r - dv * W, v = v0 + dv;
+                int ccol = mdiv31(u, magic_cell31);
+                int rem = u - ccol * cellsz;
+                int crow = mdiv31(v, magic_cell31) * cols;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if (j > 0) {
+                        ++u;
+                        if (++rem == cellsz) {
+                            rem = 0;
+                            ++ccol;
+                        }
+                        if (u == W) {  // at most one row wrap in four pixels
+                            u = 0;
+                            ++v;
+                            ccol = 0;
+                            rem = 0;
+                            crow = mdiv31(v, magic_cell31) * cols;
+                        }
+                    }
+                    uc[j] = u;
+                    cellv[j] = crow + ccol;
+                    const unsigned c0 = (code4 >> (8 * j)) & 0xffu;
+                    const float d = dd[j];
+                    const int dr = lround_away(d);
+                    const bool ok = in && c0 != kCodeOff && d == d && dr >= 0 && u - dr >= 2;
+                    crv[j] = ok ? sm_cr[p0 + j - dr] : 0u;  // same-row cR(u - dr), staged
+                    okm |= unsigned(ok) << j;
+                }
+            }
+            (void)uc;
+            int seg = -1;
+            unsigned gk = 32, gi = 0, bk = 32, bi = 0;  // best (k, idx) of the segment per grid
+            auto seg_flush = [&]() {
+                if (gk < 32) atomicMin(Cg_f + seg, (unsigned long long)gk << 32 | gi);
+                if (bk < 32) atomicMin(Cb_f + seg, (unsigned long long)bk << 32 | bi);
+            };
+            float dense[4], cfo[4];
+            unsigned gkey[4], bkey[4];
+            unsigned dval = 0, dvo = 0, codes_new = code4;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int p = p0 + j;
+                const unsigned c0 = (code4 >> (8 * j)) & 0xffu;
+                const bool m = in && c0 != kCodeOff;
+                const float d = dd[j];
+                const int k = ((okm >> j) & 1u) ? __popc(cl[j] ^ crv[j]) : kCensusBits;
+                const bool upd = m && unsigned(k) < c0;  // cost[k] < C_f (pipeline.cpp:68-71)
+                if (upd) {
+                    codes_new = (codes_new & ~(0xffu << (8 * j))) | (unsigned(k) << (8 * j));
+                    a.Df[tb + p] = d;
+                }
+                const unsigned cc = (upd ? unsigned(k) : c0) & 31u;  // kCodeOff -> 31
+                if (LAST) {
+                    const bool valid = d == d;
+                    dense[j] = valid ? d : 0.0f;
+                    dval |= unsigned(valid) << (8 * j);
+                    cfo[j] = s_cout[cc];
+                    dvo |= unsigned(cc < code_high) << (8 * j);
+                }
+                const bool qg = m && ((tab.low_mask >> k) & 1u);
+                const bool qb = m && !qg && ((tab.high_mask >> k) & 1u);
+                tsum += in ? s_fix[cc] : 0ull;  // C_f * 2^36 (exact, see trace_fixed_exact)
+                tvalid += (in && cc < code_high) ? 1u : 0u;
+                const unsigned idx = unsigned(ib + p);
+                if constexpr (SPAN == 2) {
+                    // 32-bit keys (k << 27 | idx): their minimum is the first
+                    // (row-major) minimum; folded per segment after the loop
+                    gkey[j] = qg ? (unsigned(k) << kIdxBits | idx) : 0xffffffffu;
+                    bkey[j] = qb ? (unsigned(kCensusBits - k) << kIdxBits | idx) : 0xffffffffu;
+                } else {
+                    if (cellv[j] != seg) {
+                        if (seg >= 0) seg_flush();
+                        seg = cellv[j];
+                        gk = bk = 32;
+                    }
+                    if (qg && unsigned(k) < gk) {  // strict: the first (row-major) minimum
+                        gk = unsigned(k);
+                        gi = idx;
+                    }
+                    if (qb && unsigned(kCensusBits - k) < bk) {
+                        bk = unsigned(kCensusBits - k);
+                        bi = idx;
+                    }
+                }
+            }
+            if (in) {
+                if constexpr (SPAN == 2) {
+                    // at most one cell boundary inside the four pixels (host-
+                    // checked: cell >= 3 and the last cell of a row >= 3 wide)
+                    const bool b1 = cellv[1] != cellv[0], b2 = cellv[2] != cellv[0],
+                               b3 = cellv[3] != cellv[0];
+                    unsigned gA = gkey[0], bA = bkey[0], gB = 0xffffffffu, bB = 0xffffffffu;
+                    gA = min(gA, b1 ? 0xffffffffu : gkey[1]);
+                    bA = min(bA, b1 ? 0xffffffffu : bkey[1]);
+                    gB = min(gB, b1 ? gkey[1] : 0xffffffffu);
+                    bB = min(bB, b1 ? bkey[1] : 0xffffffffu);
+                    gA = min(gA, b2 ? 0xffffffffu : gkey[2]);
+                    bA = min(bA, b2 ? 0xffffffffu : bkey[2]);
+                    gB = min(gB, b2 ? gkey[2] : 0xffffffffu);
+                    bB = min(bB, b2 ? bkey[2] : 0xffffffffu);
+                    gA = min(gA, b3 ? 0xffffffffu : gkey[3]);
+                    bA = min(bA, b3 ? 0xffffffffu : bkey[3]);
+                    gB = min(gB, b3 ? gkey[3] : 0xffffffffu);
+                    bB = min(bB, b3 ? bkey[3] : 0xffffffffu);
+                    if (gA != 0xffffffffu) atomicMin(Cg_f + cellv[0], widen(gA));
+                    if (bA != 0xffffffffu) atomicMin(Cb_f + cellv[0], widen(bA));
+                    if (gB != 0xffffffffu) atomicMin(Cg_f + cellv[3], widen(gB));
+                    if (bB != 0xffffffffu) atomicMin(Cb_f + cellv[3], widen(bB));
+                } else {
+                    seg_flush();
+                }
+                if (codes_new != code4) *reinterpret_cast<unsigned*>(a.code + tb + p0) = codes_new;
+                if (LAST) {
+                    *reinterpret_cast<float4*>(a.dense + tb + p0) = make_float4(dense[0], dense[1], dense[2], dense[3]);
+                    *reinterpret_cast<unsigned*>(a.dense_valid + tb + p0) = dval;
+                    *reinterpret_cast<float4*>(a.Cf + tb + p0) = make_float4(cfo[0], cfo[1], cfo[2], cfo[3]);
+                    *reinterpret_cast<unsigned*>(a.Dv + tb + p0) = dvo;
+                }
+            }
+        } else {
         // slot geometry: lane l of slot q is pixel p = warp*128 + q*32 + l; the
         // slot's first pixel (row vrow, column ucol) is uniform, each lane adds
         // its lane index (W >= 32: at most one row wrap inside a slot).  The
@@ -404,6 +545,7 @@ __global__ void __launch_bounds__(256, 4) k_refine_bulk(RefineArgs a, CostTables
                     atomicMin(Cb_f + cells[q], (unsigned long long)(b >> 5) << 32 | (i0 + (b & 31u)));
             }
         }
+        }
         // release stage s: the last of the 8 warps to finish it refills it
         // (no CTA-wide barrier, so fast warps run ahead into the next stages)
         __syncwarp();
@@ -485,7 +627,7 @@ __global__ void k_fill_f32(float* __restrict__ p, long long n, float x) {
 namespace {
 // Persistent bulk-copy launch: as many CTAs per SM as registers and shared
 // memory allow (queried once per instantiation).
-template <bool LAST, int SPAN>
+template <bool LAST, int SPAN, bool VEC = false>
 int launch_bulk(const RefineArgs& a0, const CostTables& tab, unsigned magic_cell31, unsigned magic_w,
                 cudaStream_t st) {
     static int sms = 0;
@@ -502,13 +644,13 @@ int launch_bulk(const RefineArgs& a0, const CostTables& tab, unsigned magic_cell
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(k_refine_bulk<LAST, true, SPAN>,
+        cudaFuncSetAttribute(k_refine_bulk<LAST, true, SPAN, VEC>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(size_t(kStages) * (9 * kTile + 4 * (kTile + kMaxHalo))));
     }
     int& occ = per_sm[bg.halo / 4];
     if (occ == 0) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_refine_bulk<LAST, true, SPAN>, 256, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_refine_bulk<LAST, true, SPAN, VEC>, 256, smem);
         occ = std::max(1, occ);
     }
     // the kernel indexes the batch with 32-bit pixel offsets: launch per
@@ -537,7 +679,7 @@ int launch_bulk(const RefineArgs& a0, const CostTables& tab, unsigned magic_cell
         }
         bg.total_tiles = bg.tiles_per_frame * a.frames;
         const unsigned blocks = unsigned(std::min<long long>(bg.total_tiles, (long long)occ * sms));
-        k_refine_bulk<LAST, true, SPAN><<<blocks, 256, smem, st>>>(a, tab, magic_cell31, magic_w, bg);
+        k_refine_bulk<LAST, true, SPAN, VEC><<<blocks, 256, smem, st>>>(a, tab, magic_cell31, magic_w, bg);
         ++launches;
     }
     return launches;
@@ -556,6 +698,20 @@ int launch_refine(const RefineArgs& a, const CostTables& tab, bool last, cudaStr
         // exact 16-bit magic reciprocals for the row / cell divisions (mdiv)
         const unsigned magic_w = unsigned((0x100000000ull + a.g.width - 1) / a.g.width);
         const unsigned magic_cell = unsigned((0x80000000ull + a.cell - 1) / a.cell);  // 2^31 / cell
+        static const bool vec = [] {
+            const char* e = std::getenv("PS_K7_VEC");
+            return !e || std::atoi(e) != 0;
+        }();
+        if (vec) {
+            // at most one cell boundary in any four consecutive pixels
+            const int tail = a.g.width % a.cell;
+            const bool two = a.cell >= 3 && (tail == 0 || tail >= 3);
+            if (two)
+                return last ? launch_bulk<true, 2, true>(a, tab, magic_cell, magic_w, st)
+                            : launch_bulk<false, 2, true>(a, tab, magic_cell, magic_w, st);
+            return last ? launch_bulk<true, 1, true>(a, tab, magic_cell, magic_w, st)
+                        : launch_bulk<false, 1, true>(a, tab, magic_cell, magic_w, st);
+        }
         // longest run of equal cells inside a 32-pixel slot, rounded up to 2^n
         const int cols = (a.g.width + a.cell - 1) / a.cell;
         const int run = cols == 1 ? 32 : std::min(a.cell, 32);
