@@ -692,10 +692,12 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         // ---- K7 (+K9) refine (mesh.cpp:149-182, pipeline.cpp:33-86)
         unsigned long long* cg = dCg + size_t(f0) * cells_max;
         unsigned long long* cb = dCb + size_t(f0) * cells_max;
-        cudaMemset2DAsync(cg, sizeof(unsigned long long) * cells_max, 0xff,
-                          sizeof(unsigned long long) * cells, n, gs);
-        cudaMemset2DAsync(cb, sizeof(unsigned long long) * cells_max, 0xff,
-                          sizeof(unsigned long long) * cells, n, gs);
+        if (!last) {  // the last iteration's grids are never read (no resampling)
+            cudaMemset2DAsync(cg, sizeof(unsigned long long) * cells_max, 0xff,
+                              sizeof(unsigned long long) * cells, n, gs);
+            cudaMemset2DAsync(cb, sizeof(unsigned long long) * cells_max, 0xff,
+                              sizeof(unsigned long long) * cells, n, gs);
+        }
         const size_t fp = size_t(f0) * P;
         RefineArgs ra{};
         ra.g = g;

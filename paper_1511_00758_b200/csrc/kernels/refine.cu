@@ -402,12 +402,15 @@ __global__ void __launch_bounds__(256, 4) k_refine_bulk(RefineArgs a, CostTables
                     cfo[j] = s_cout[cc];
                     dvo |= unsigned(cc < code_high) << (8 * j);
                 }
-                const bool qg = m && ((tab.low_mask >> k) & 1u);
-                const bool qb = m && !qg && ((tab.high_mask >> k) & 1u);
                 tsum += in ? s_fix[cc] : 0ull;  // C_f * 2^36 (exact, see trace_fixed_exact)
                 tvalid += (in && cc < code_high) ? 1u : 0u;
+                // the grids feed only supportResampling, which the last
+                // iteration does not run (pipeline.cpp:168-171): skipped there
+                const bool qg = !LAST && m && ((tab.low_mask >> k) & 1u);
+                const bool qb = !LAST && m && !qg && ((tab.high_mask >> k) & 1u);
                 const unsigned idx = unsigned(ib + p);
-                if constexpr (SPAN == 2) {
+                if constexpr (LAST) {
+                } else if constexpr (SPAN == 2) {
                     // 32-bit keys (k << 27 | idx): their minimum is the first
                     // (row-major) minimum; folded per segment after the loop
                     gkey[j] = qg ? (unsigned(k) << kIdxBits | idx) : 0xffffffffu;
@@ -429,7 +432,8 @@ __global__ void __launch_bounds__(256, 4) k_refine_bulk(RefineArgs a, CostTables
                 }
             }
             if (in) {
-                if constexpr (SPAN == 2) {
+                if constexpr (LAST) {
+                } else if constexpr (SPAN == 2) {
                     // at most one cell boundary inside the four pixels (host-
                     // checked: cell >= 3 and the last cell of a row >= 3 wide)
                     const bool b1 = cellv[1] != cellv[0], b2 = cellv[2] != cellv[0],
