@@ -17,17 +17,15 @@
 // In the last iteration the same pass also writes the full-image dense
 // interpolation (mesh.cpp:166-182, K9).
 //
-// Layout: a warp owns a 128-pixel chunk of one frame; slot j of lane l is
-// pixel chunk + 32*j + l, so every load/store instruction of the warp covers
-// 32 consecutive pixels (coalesced), the four first-level loads of all slots
-// (mask, D_it, cL, C_f) are issued before any use (memory-level parallelism),
-// and pixels of one occupancy cell are contiguous lanes of a slot: the grid
-// keys of a cell are min-reduced across the warp (__match_any_sync +
-// __reduce_min_sync on the two key words) before ONE atomicMin per cell and
-// slot.  Algorithmic traffic P + 29*M bytes per frame.
+// Two kernels.  k_refine_bulk (the production path, below) streams tiles
+// through shared memory with bulk copies, each lane owning four contiguous
+// pixels; k_refine is the general fallback (frames whose width or
+// disparity range the bulk path does not cover, or P > 2^27): a warp owns a
+// 128-pixel chunk, slot j of lane l is pixel chunk + 32*j + l, and the keys of
+// a cell are min-reduced across the lanes of a slot before one atomicMin.
+// The C_f state is a byte code (CostTables): cost[k] < C_f <=> k < code.
+// Algorithmic traffic P + 29*M bytes per frame and iteration.
 #include <cuda_runtime.h>
-
-#include <cstdlib>
 
 #include "launch.hpp"
 
@@ -182,19 +180,20 @@ __global__ void __launch_bounds__(256) k_refine(RefineArgs a, CostTables tab, fl
 // gather cR(u - d)) into a shared-memory ring with cp.async.bulk + mbarrier
 // complete_tx, under an L2 evict-first policy (every byte is read once).  The
 // cR gather is then a shared-memory load.  Stage release: the last of the 8
-// warps to finish a stage refills it (no CTA-wide barrier).  Needs 16-B
-// aligned tiles (P % 16 == 0) and max_disp <= kMaxHalo.
+// warps to finish a stage refills it (no CTA-wide barrier).  Each lane owns
+// four contiguous pixels (LDS.128 stage loads, vector output stores); the
+// cell keys are folded inside the lane — SEG == 2: branch-free into at most
+// two segments (every cell >= 3 px wide, host-checked), SEG == 1: in order —
+// and each (cell, lane) segment issues one fire-and-forget atomicMin per
+// grid.  The last iteration writes the outputs and skips the grids (they feed
+// only supportResampling, which it does not run).  Needs 16-B aligned tiles
+// (P % 16 == 0), W >= 32 and max_disp <= kMaxHalo.
 constexpr int kTileSlots = 4;
 constexpr int kWarpPx = 32 * kTileSlots;
 constexpr int kWarps = 8;
 constexpr int kTile = kWarps * kWarpPx;  // 8 warps x 4 slots x 32 lanes = 1024 px
 constexpr int kStages = 4;
 constexpr int kMaxHalo = 1024;  // cR words staged left of the tile (>= max_disp)
-
-// n / d for 0 <= n, d < 2^16 with magic = ceil(2^32 / d) (exact in that range).
-__device__ __forceinline__ int mdiv(int n, unsigned magic, int d) {
-    return d == 1 ? n : int(__umulhi(unsigned(n), magic));
-}
 
 // n / d with magic31 = ceil(2^31 / d): exact whenever n * d < 2^31 (here
 // n < 2^16 and d < 2^15), including d = 1, so no special case.
@@ -236,7 +235,7 @@ struct BulkGeom {
     int r_tile;       // kTile % W
 };
 
-template <bool LAST, bool KEY32, int SPAN, bool VEC>
+template <bool LAST, int SEG>
 __global__ void __launch_bounds__(256, 4) k_refine_bulk(RefineArgs a, CostTables tab,
                                                         unsigned magic_cell31, unsigned magic_w,
                                                         BulkGeom bg) {
@@ -324,7 +323,7 @@ __global__ void __launch_bounds__(256, 4) k_refine_bulk(RefineArgs a, CostTables
         const int tb = f * P + off;  // first pixel of the tile within the batch
         unsigned long long* Cg_f = a.Cg + (long long)f * a.cell_stride;
         unsigned long long* Cb_f = a.Cb + (long long)f * a.cell_stride;
-        if constexpr (VEC) {
+        {
             // 4 contiguous pixels per lane: p = warp*128 + 4*lane + j.  Vector
             // stage loads; the pixels of a cell inside the lane are folded in
             // order (first minimum wins) and each (cell, lane) segment issues
@@ -410,7 +409,7 @@ __global__ void __launch_bounds__(256, 4) k_refine_bulk(RefineArgs a, CostTables
                 const bool qb = !LAST && m && !qg && ((tab.high_mask >> k) & 1u);
                 const unsigned idx = unsigned(ib + p);
                 if constexpr (LAST) {
-                } else if constexpr (SPAN == 2) {
+                } else if constexpr (SEG == 2) {
                     // 32-bit keys (k << 27 | idx): their minimum is the first
                     // (row-major) minimum; folded per segment after the loop
                     gkey[j] = qg ? (unsigned(k) << kIdxBits | idx) : 0xffffffffu;
@@ -433,7 +432,7 @@ __global__ void __launch_bounds__(256, 4) k_refine_bulk(RefineArgs a, CostTables
             }
             if (in) {
                 if constexpr (LAST) {
-                } else if constexpr (SPAN == 2) {
+                } else if constexpr (SEG == 2) {
                     // at most one cell boundary inside the four pixels (host-
                     // checked: cell >= 3 and the last cell of a row >= 3 wide)
                     const bool b1 = cellv[1] != cellv[0], b2 = cellv[2] != cellv[0],
@@ -466,89 +465,6 @@ __global__ void __launch_bounds__(256, 4) k_refine_bulk(RefineArgs a, CostTables
                     *reinterpret_cast<unsigned*>(a.Dv + tb + p0) = dvo;
                 }
             }
-        } else {
-        // slot geometry: lane l of slot q is pixel p = warp*128 + q*32 + l; the
-        // slot's first pixel (row vrow, column ucol) is uniform, each lane adds
-        // its lane index (W >= 32: at most one row wrap inside a slot).  The
-        // pixels of one occupancy cell are a run of consecutive lanes: run_end
-        // is the last lane of this lane's run, lead marks its first lane.
-        int cells[kTileSlots], run_end[kTileSlots];
-        uint32_t crv[kTileSlots];
-        unsigned okm = 0, leadm = 0;
-#pragma unroll
-        for (int q = 0; q < kTileSlots; ++q) {
-            const int r = r0 + warp * kWarpPx + q * 32;
-            const int dv = int(__umulhi(unsigned(r), magic_w));  // W >= 32
-            const int vrow = v0 + dv;
-            int u = r - dv * W + lane;
-            const bool wrap = u >= W;
-            u = wrap ? u - W : u;
-            const int crow0 = mdiv31(vrow, magic_cell31) * cols;
-            const int crow1 = mdiv31(vrow + 1, magic_cell31) * cols;
-            const int ccol = mdiv31(u, magic_cell31);
-            const int ubeg = ccol * cellsz;
-            cells[q] = (wrap ? crow1 : crow0) + ccol;
-            run_end[q] = lane + min(ubeg + cellsz, W) - u - 1;
-            leadm |= unsigned(lane == 0 || u == ubeg) << q;
-            const int p = warp * kWarpPx + q * 32 + lane;
-            const float d = sm_dit[p];
-            const int dr = lround_away(d);
-            const bool ok = p < n_in && sm_code[p] != kCodeOff && d == d && dr >= 0 && u - dr >= 2;
-            crv[q] = ok ? sm_cr[p - dr] : 0u;  // same-row cR(u - dr), staged
-            okm |= unsigned(ok) << q;
-        }
-#pragma unroll
-        for (int q = 0; q < kTileSlots; ++q) {
-            const int p = warp * kWarpPx + q * 32 + lane;
-            const bool in = p < n_in;
-            const unsigned c0 = sm_code[p];
-            const bool m = in && c0 != kCodeOff;
-            const float d = sm_dit[p];
-            const int k = ((okm >> q) & 1u) ? __popc(sm_cl[p] ^ crv[q]) : kCensusBits;
-            const bool upd = m && unsigned(k) < c0;  // cost[k] < C_f (pipeline.cpp:68-71)
-            if (upd) {
-                a.code[tb + p] = uint8_t(k);
-                a.Df[tb + p] = d;
-            }
-            const unsigned cc = (upd ? unsigned(k) : c0) & 31u;  // kCodeOff -> 31
-            if (LAST && in) {
-                const bool valid = d == d;
-                a.dense[tb + p] = valid ? d : 0.0f;
-                a.dense_valid[tb + p] = valid ? 1 : 0;
-                a.Cf[tb + p] = s_cout[cc];
-                a.Dv[tb + p] = cc < code_high ? 1 : 0;
-            }
-            const bool qg = m && ((tab.low_mask >> k) & 1u);
-            const bool qb = m && !qg && ((tab.high_mask >> k) & 1u);
-            tsum += in ? s_fix[cc] : 0ull;  // C_f * 2^36 (exact, see trace_fixed_exact); 0 off-mask
-            tvalid += (in && cc < code_high) ? 1u : 0u;
-            if (!KEY32) {
-                const int i = ib + p;
-                if (qg) atomicMin(Cg_f + cells[q], (unsigned long long)k << 32 | (unsigned long long)i);
-                if (qb) atomicMin(Cb_f + cells[q], (unsigned long long)(kCensusBits - k) << 32 | (unsigned long long)i);
-                continue;
-            }
-            if (__ballot_sync(0xffffffffu, qg | qb) == 0u) continue;
-            // both grid keys of the lane in one word, 16 bits each: (k << 5 | lane)
-            // for the confident grid, ((24 - k) << 5 | lane) for the invalid one;
-            // lanes grow with the pixel index, so the min is the reference's
-            // first-row-major winner.  Segmented min over the run: VIMNMX.U16x2.
-            unsigned key = (qg ? ((unsigned(k) << 5 | unsigned(lane)) << 16) : 0xffff0000u) |
-                           (qb ? (unsigned(kCensusBits - k) << 5 | unsigned(lane)) : 0xffffu);
-#pragma unroll
-            for (int o = 1; o < SPAN; o <<= 1) {
-                const unsigned other = __shfl_down_sync(0xffffffffu, key, o);
-                key = lane + o <= run_end[q] ? __vminu2(key, other) : key;
-            }
-            if ((leadm >> q) & 1u) {
-                const unsigned i0 = unsigned(ib + warp * kWarpPx + q * 32);  // pixel of lane 0
-                const unsigned g = key >> 16, b = key & 0xffffu;
-                if (g != 0xffffu)
-                    atomicMin(Cg_f + cells[q], (unsigned long long)(g >> 5) << 32 | (i0 + (g & 31u)));
-                if (b != 0xffffu)
-                    atomicMin(Cb_f + cells[q], (unsigned long long)(b >> 5) << 32 | (i0 + (b & 31u)));
-            }
-        }
         }
         // release stage s: the last of the 8 warps to finish it refills it
         // (no CTA-wide barrier, so fast warps run ahead into the next stages)
@@ -631,7 +547,7 @@ __global__ void k_fill_f32(float* __restrict__ p, long long n, float x) {
 namespace {
 // Persistent bulk-copy launch: as many CTAs per SM as registers and shared
 // memory allow (queried once per instantiation).
-template <bool LAST, int SPAN, bool VEC = false>
+template <bool LAST, int SEG>
 int launch_bulk(const RefineArgs& a0, const CostTables& tab, unsigned magic_cell31, unsigned magic_w,
                 cudaStream_t st) {
     static int sms = 0;
@@ -648,13 +564,13 @@ int launch_bulk(const RefineArgs& a0, const CostTables& tab, unsigned magic_cell
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(k_refine_bulk<LAST, true, SPAN, VEC>,
+        cudaFuncSetAttribute(k_refine_bulk<LAST, SEG>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(size_t(kStages) * (9 * kTile + 4 * (kTile + kMaxHalo))));
     }
     int& occ = per_sm[bg.halo / 4];
     if (occ == 0) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_refine_bulk<LAST, true, SPAN, VEC>, 256, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_refine_bulk<LAST, SEG>, 256, smem);
         occ = std::max(1, occ);
     }
     // the kernel indexes the batch with 32-bit pixel offsets: launch per
@@ -683,7 +599,7 @@ int launch_bulk(const RefineArgs& a0, const CostTables& tab, unsigned magic_cell
         }
         bg.total_tiles = bg.tiles_per_frame * a.frames;
         const unsigned blocks = unsigned(std::min<long long>(bg.total_tiles, (long long)occ * sms));
-        k_refine_bulk<LAST, true, SPAN, VEC><<<blocks, 256, smem, st>>>(a, tab, magic_cell31, magic_w, bg);
+        k_refine_bulk<LAST, SEG><<<blocks, 256, smem, st>>>(a, tab, magic_cell31, magic_w, bg);
         ++launches;
     }
     return launches;
@@ -702,39 +618,13 @@ int launch_refine(const RefineArgs& a, const CostTables& tab, bool last, cudaStr
         // exact 16-bit magic reciprocals for the row / cell divisions (mdiv)
         const unsigned magic_w = unsigned((0x100000000ull + a.g.width - 1) / a.g.width);
         const unsigned magic_cell = unsigned((0x80000000ull + a.cell - 1) / a.cell);  // 2^31 / cell
-        static const bool vec = [] {
-            const char* e = std::getenv("PS_K7_VEC");
-            return !e || std::atoi(e) != 0;
-        }();
-        if (vec) {
-            // at most one cell boundary in any four consecutive pixels
-            const int tail = a.g.width % a.cell;
-            const bool two = a.cell >= 3 && (tail == 0 || tail >= 3);
-            if (two)
-                return last ? launch_bulk<true, 2, true>(a, tab, magic_cell, magic_w, st)
-                            : launch_bulk<false, 2, true>(a, tab, magic_cell, magic_w, st);
-            return last ? launch_bulk<true, 1, true>(a, tab, magic_cell, magic_w, st)
-                        : launch_bulk<false, 1, true>(a, tab, magic_cell, magic_w, st);
-        }
-        // longest run of equal cells inside a 32-pixel slot, rounded up to 2^n
-        const int cols = (a.g.width + a.cell - 1) / a.cell;
-        const int run = cols == 1 ? 32 : std::min(a.cell, 32);
-        int span = 1;
-        while (span < run) span <<= 1;
-        switch (span * 2 + (last ? 1 : 0)) {
-            case 2: return launch_bulk<false, 1>(a, tab, magic_cell, magic_w, st);
-            case 3: return launch_bulk<true, 1>(a, tab, magic_cell, magic_w, st);
-            case 4: return launch_bulk<false, 2>(a, tab, magic_cell, magic_w, st);
-            case 5: return launch_bulk<true, 2>(a, tab, magic_cell, magic_w, st);
-            case 8: return launch_bulk<false, 4>(a, tab, magic_cell, magic_w, st);
-            case 9: return launch_bulk<true, 4>(a, tab, magic_cell, magic_w, st);
-            case 16: return launch_bulk<false, 8>(a, tab, magic_cell, magic_w, st);
-            case 17: return launch_bulk<true, 8>(a, tab, magic_cell, magic_w, st);
-            case 32: return launch_bulk<false, 16>(a, tab, magic_cell, magic_w, st);
-            case 33: return launch_bulk<true, 16>(a, tab, magic_cell, magic_w, st);
-            case 64: return launch_bulk<false, 32>(a, tab, magic_cell, magic_w, st);
-            default: return launch_bulk<true, 32>(a, tab, magic_cell, magic_w, st);
-        }
+        // at most one cell boundary in any four consecutive pixels
+        const int tail = a.g.width % a.cell;
+        if (a.cell >= 3 && (tail == 0 || tail >= 3))
+            return last ? launch_bulk<true, 2>(a, tab, magic_cell, magic_w, st)
+                        : launch_bulk<false, 2>(a, tab, magic_cell, magic_w, st);
+        return last ? launch_bulk<true, 1>(a, tab, magic_cell, magic_w, st)
+                    : launch_bulk<false, 1>(a, tab, magic_cell, magic_w, st);
     }
     if (last) {
         if (key32) k_refine<true, true><<<grid, 256, 0, st>>>(a, tab, inv_cell, inv_w);
