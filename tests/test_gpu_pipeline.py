@@ -268,3 +268,23 @@ def test_full_size_properties_1080p(ctx):
     assert (r.disparity[ok] >= 0).all() and (r.disparity[ok] < cfg.maxDisparity).all()
     r2 = ctx.run(L, R, cfg)
     assert np.array_equal(bits(r.costs), bits(r2.costs))
+
+
+def test_4k_frame_bit_exact(ctx, orc):
+    """Maximum-size frame (BASELINE config 4: 3840x2160, ND 256, grid 6) for two
+    iterations, bit for bit against the restatement: every output map and the
+    final support list (the restatement takes a few seconds here)."""
+    c = ps.BASELINE_CONFIGS[4]
+    cfg = ps.baseline_config(4)
+    cfg.iterations = 2
+    L, R = ps.synth_pair(c["width"], c["height"], c["n_planes"], c["max_disparity"], c["ground"],
+                         c["sigma"], seed=44)
+    r = ctx.run(L, R, cfg, unchecked_cell=True)
+    w = orc.run(L, R, cfg)  # validate() skipped: grid 6 is BASELINE's, not a power of two
+    assert w["status"] == 0
+    for k in ["disparity", "disparity_valid", "costs", "dense", "dense_valid"]:
+        assert np.array_equal(bits(getattr(r, k)), bits(w[k])), k
+    u, v, d = ctx.supports(0)
+    su, sv, sd = w["supports"]
+    assert np.array_equal(u, su) and np.array_equal(v, sv) and np.array_equal(bits(d), bits(sd))
+    assert [t.meanCost for t in r.trace] == [t["meanCost"] for t in w["trace"]]
