@@ -46,6 +46,9 @@ int delaunay(const int* u, const int* v, int n, std::vector<int>& tris, Delaunay
 // but cache-friendly, so only ~15% slower; the engine uses it because the
 // order decides hull-vertex pins and the rotation decides fitPlane rounding.
 int delaunay_lex(const int* u, const int* v, int n, std::vector<int>& tris, DelaunayWorkspace& ws);
+// The same into a caller buffer of capacity triangles (3 ints each); -3 when
+// the triangulation has more.
+int delaunay_lex(const int* u, const int* v, int n, int* tris, int capacity, DelaunayWorkspace& ws);
 
 // Hull-vertex pinning (mesh.cpp:109-122) for this triangle list: pin_bits[t]
 // bit k set when corner k of triangle t is an uncovered vertex pixel whose
@@ -54,6 +57,7 @@ int delaunay_lex(const int* u, const int* v, int n, std::vector<int>& tris, Dela
 // (its triangle list, ntri triangles), visiting only hull vertices.
 void lex_hull_pins(const DelaunayWorkspace& ws, int ntri, int width, int height,
                    std::vector<uint8_t>& pin_bits);
+void lex_hull_pins(const DelaunayWorkspace& ws, int ntri, int width, int height, uint8_t* pin_bits);
 
 void mesh_pins(const int* u, const int* v, int n, const int* tris, int nt, int width, int height,
                std::vector<uint8_t>& state, std::vector<uint8_t>& pin_bits);

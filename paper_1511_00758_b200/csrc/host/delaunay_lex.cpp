@@ -15,7 +15,9 @@
 // rounding depends on the vertex rotation (the plane offset is anchored at the
 // first vertex).  The engine therefore always triangulates with this sweep;
 // it is also the order of the public ps_delaunay().
+#include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "delaunay.hpp"
 
@@ -152,9 +154,34 @@ struct LexSweep {
 void lex_order(const int* u, const int* v, int n, DelaunayWorkspace& ws, int& minx, int& miny,
                int& m, int& spanx, int& spany);
 
+namespace {
+int lex_sweep(const int* u, const int* v, int n, DelaunayWorkspace& ws);
+}  // namespace
+
 int delaunay_lex(const int* u, const int* v, int n, std::vector<int>& tris,
                  DelaunayWorkspace& ws) {
     tris.clear();
+    const int nt = lex_sweep(u, v, n, ws);
+    if (nt <= 0) return nt;
+    tris.resize(3 * std::size_t(nt));
+    for (int t = 0; t < nt; ++t)
+        for (int k = 0; k < 3; ++k) tris[3 * t + k] = ws.kept[ws.lex[t].v[k]];
+    return nt;
+}
+
+int delaunay_lex(const int* u, const int* v, int n, int* tris, int capacity,
+                 DelaunayWorkspace& ws) {
+    const int nt = lex_sweep(u, v, n, ws);
+    if (nt <= 0) return nt;
+    if (nt > capacity) return -3;
+    for (int t = 0; t < nt; ++t)
+        for (int k = 0; k < 3; ++k) tris[3 * t + k] = ws.kept[ws.lex[t].v[k]];
+    return nt;
+}
+
+namespace {
+// The sweep itself: triangles left in ws.lex[0..ntri), vertex ids into ws.kept.
+int lex_sweep(const int* u, const int* v, int n, DelaunayWorkspace& ws) {
     constexpr int kLimit = 1 << 20;
     for (int i = 0; i < n; ++i)
         if (std::abs(u[i]) >= kLimit || std::abs(v[i]) >= kLimit) return -1;
@@ -208,11 +235,9 @@ int delaunay_lex(const int* u, const int* v, int n, std::vector<int>& tris,
     }
     for (int p = apex + 1; p < m; ++p)
         if (!s.insert(p)) return -2;
-    tris.resize(3 * std::size_t(s.ntri));
-    for (int t = 0; t < s.ntri; ++t)
-        for (int k = 0; k < 3; ++k) tris[3 * t + k] = ws.kept[ws.lex[t].v[k]];
     return s.ntri;
 }
+}  // namespace
 
 namespace {
 
@@ -230,8 +255,13 @@ bool tie_accept(int xi, int yi, int xj, int yj) {
 // each hull vertex from its hull half-edge — instead of all T triangles.
 void lex_hull_pins(const DelaunayWorkspace& ws, int ntri, int width, int height,
                    std::vector<uint8_t>& pin_bits) {
-    pin_bits.assign(ntri, 0);
+    pin_bits.assign(std::max(ntri, 0), 0);
+    if (ntri > 0) lex_hull_pins(ws, ntri, width, height, pin_bits.data());
+}
+
+void lex_hull_pins(const DelaunayWorkspace& ws, int ntri, int width, int height, uint8_t* pin_bits) {
     if (ntri <= 0) return;
+    std::memset(pin_bits, 0, std::size_t(ntri));
     const LexTri* T = ws.lex.data();
     auto V = [&](int e) { return T[e >> 2].v[e & 3]; };
     auto N = [&](int e) { return T[e >> 2].n[e & 3]; };

@@ -474,13 +474,9 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     double host_dt_ms = 0.0;
     hu_.resize(F);
     hv_.resize(F);
-    hd_.resize(F);
-    hpin_.resize(F);
-    htri_.resize(F);
     for (int f = 0; f < F; ++f) {
         hu_[f].clear();
         hv_[f].clear();
-        hd_[f].clear();
         if (hS[f] < 3) status_[f] = PS_SEEDING_FAILED;  // pipeline.cpp:151-154
     }
     trace_.assign(size_t(F) * iters, ps_iter_stats{});
@@ -545,13 +541,11 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
             total_new += k;
             max_new = std::max(max_new, k);
         }
+        // the Delaunay needs only the new supports' (u, v)
         const size_t npk = size_t(std::max<long long>(total_new, 1));
         int2* dPack = dev<int2>(grp.dPack, npk);
-        double* dPackD = dev<double>(grp.dPackD, npk);
         int2* hPack = reinterpret_cast<int2*>(host<uint8_t>(grp.hPack, npk * 8));
-        double* hPackD = reinterpret_cast<double*>(host<uint8_t>(grp.hPackD, npk * 8));
-        if (!dPack || !hPack || !dPackD || !hPackD)
-            return fail(PS_CUDA_ERROR, "allocation failed (support staging)");
+        if (!dPack || !hPack) return fail(PS_CUDA_ERROR, "allocation failed (support staging)");
         int* dSprev = static_cast<int*>(grp.dSprev.p);
         int* dPackOff = static_cast<int*>(grp.dPackOff.p);
         r = check(cudaMemcpyAsync(dSprev, hsp, sizeof(int) * n, cudaMemcpyHostToDevice, gs), "H2D Sprev");
@@ -562,14 +556,10 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         const int f0 = grp.f0;
         launches_ += launch_pack_new_supports(dSu + size_t(f0) * scap_, dSv + size_t(f0) * scap_,
                                               dSd + size_t(f0) * scap_, scap_, dSprev, grp.S,
-                                              dPackOff, n, max_new, dPack, dPackD, gs);
-        if (total_new > 0) {
+                                              dPackOff, n, max_new, dPack, nullptr, gs);
+        if (total_new > 0)
             r = check(cudaMemcpyAsync(hPack, dPack, sizeof(int2) * total_new, cudaMemcpyDeviceToHost, gs),
                       "D2H supports");
-            if (r == PS_OK)
-                r = check(cudaMemcpyAsync(hPackD, dPackD, sizeof(double) * total_new,
-                                          cudaMemcpyDeviceToHost, gs), "D2H support d");
-        }
         if (r == PS_OK) r = sync(gs, "support delta");
         return r;
     };
@@ -591,34 +581,35 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                 const int* hsp = static_cast<const int*>(g2.hSprev.p);
                 const int* hoff = static_cast<const int*>(g2.hPackOff.p);
                 const int2* hPack = static_cast<const int2*>(g2.hPack.p);
-                const double* hPackD = static_cast<const double*>(g2.hPackD.p);
                 const int k = hs[i] - hsp[i];
+                std::vector<int>& fu = hu_[f];
+                std::vector<int>& fv = hv_[f];
+                const size_t n0 = fu.size();
+                fu.resize(n0 + k);
+                fv.resize(n0 + k);
                 for (int j = 0; j < k; ++j) {
-                    hu_[f].push_back(hPack[hoff[i] + j].x);
-                    hv_[f].push_back(hPack[hoff[i] + j].y);
-                    hd_[f].push_back(hPackD[hoff[i] + j]);
+                    const int2 q = hPack[hoff[i] + j];
+                    fu[n0 + j] = q.x;
+                    fv[n0 + j] = q.y;
                 }
                 int t = 0;
                 if (status_[f] == PS_OK) {
-                    const int ns = int(hu_[f].size());
+                    const int ns = int(fu.size());
                     DelaunayWorkspace& w = ws_[worker];
-                    // the reference's triangle order and rotation: pins and
-                    // fitPlane rounding then match it bit for bit
+                    // the reference's triangle order and rotation (pins and
+                    // fitPlane rounding then match it bit for bit), written
+                    // straight into the group's pinned staging slot
+                    int* slot = static_cast<int*>(g2.hTri.p) + size_t(i) * tri_cap * 3;
                     const double ts0 = now_ms();
-                    t = delaunay_lex(hu_[f].data(), hv_[f].data(), ns, htri_[f], w);
+                    t = delaunay_lex(fu.data(), fv.data(), ns, slot, tri_cap, w);
                     const double ts1 = now_ms();
-                    if (t > 0) lex_hull_pins(w, t, W, H, hpin_[f]);  // == mesh_pins()
+                    if (t > 0)  // == mesh_pins()
+                        lex_hull_pins(w, t, W, H, static_cast<uint8_t*>(g2.hPin.p) + size_t(i) * tri_cap);
                     add_ms(sweep_ms_sum, ts1 - ts0);
                     add_ms(pins_ms_sum, now_ms() - ts1);
-                    if (t < 0 || t > tri_cap) {
+                    if (t < 0) {
                         status_[f] = PS_ERROR;
                         t = 0;
-                    }
-                    if (t > 0) {
-                        std::memcpy(static_cast<int*>(g2.hTri.p) + size_t(i) * tri_cap * 3,
-                                    htri_[f].data(), sizeof(int) * 3 * t);
-                        std::memcpy(static_cast<uint8_t*>(g2.hPin.p) + size_t(i) * tri_cap,
-                                    hpin_[f].data(), t);
                     }
                 }
                 g2.ntri[i] = t;

@@ -183,9 +183,7 @@ private:
     // pinned host staging
     HostBuf hS_, hTraceSum_, hTraceValid_, hMaskCount_;
     int scap_ = 0;
-    std::vector<std::vector<int>> hu_, hv_, htri_;
-    std::vector<std::vector<double>> hd_;
-    std::vector<std::vector<uint8_t>> hpin_;
+    std::vector<std::vector<int>> hu_, hv_;  // per frame support coordinates (host copy)
     std::vector<int> status_, final_count_;
     std::vector<ps_iter_stats> trace_;
 };

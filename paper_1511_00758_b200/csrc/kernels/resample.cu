@@ -102,7 +102,7 @@ __global__ void k_pack_new(const int* __restrict__ su, const int* __restrict__ s
     if (i >= n) return;
     const long long s = (long long)f * scap + S_prev[f] + i;
     out[off[f] + i] = make_int2(su[s], sv[s]);
-    out_d[off[f] + i] = sd[s];
+    if (out_d) out_d[off[f] + i] = sd[s];
 }
 
 }  // namespace
