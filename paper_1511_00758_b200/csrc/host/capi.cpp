@@ -139,7 +139,9 @@ ps_status ps_run_batch(ps_ctx* ctx, int n_frames, const uint8_t* left, const uin
     // run() checks the config before anything else (pipeline.cpp:133)
     ps_status s = ps_config_validate(cfg, flags);
     if (s != PS_OK) return s;
-    s = ps_upload_batch(ctx, n_frames, left, right, width, height);
+    if (!left || !right) return set_error(PS_ERROR, "null image");
+    // the images are copied inside the run, group by group, overlapping seeding
+    s = from_engine(ctx, ctx->engine->upload(n_frames, left, right, width, height, true));
     if (s != PS_OK) return s;
     // page-locked destinations are filled group by group during the run
     ctx->engine->set_sink(disparity, disparity_valid, cost, dense, dense_valid);

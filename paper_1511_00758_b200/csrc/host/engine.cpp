@@ -150,6 +150,7 @@ Engine::Engine(int device) : device_(device) {
     cudaSetDevice(device_);
     cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking);
     for (FrameGroup& g : groups_) cudaStreamCreateWithFlags(&g.st, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&start_event_, cudaEventDisableTiming);
     pool_ = new ThreadPool(host_threads());
     ws_.resize(pool_->size());
 }
@@ -183,6 +184,7 @@ Engine::~Engine() {
         cudaEventDestroy(p.b);
     }
     for (cudaEvent_t e : event_pool_) cudaEventDestroy(e);
+    if (start_event_) cudaEventDestroy(start_event_);
     if (st_) cudaStreamDestroy(st_);
     delete pool_;
 }
@@ -297,7 +299,7 @@ void Engine::resolve_timers() {
 }
 
 ps_status Engine::upload(int frames, const uint8_t* left, const uint8_t* right, int width,
-                         int height) {
+                         int height, bool deferred) {
     if (width < 16 || height < 16)
         return fail(PS_DIMENSION_TOO_SMALL, "image must be at least 16x16, got " +
                                                 std::to_string(width) + "x" +
@@ -312,6 +314,14 @@ ps_status Engine::upload(int frames, const uint8_t* left, const uint8_t* right, 
     uint8_t* dl = dev<uint8_t>(dL_, n);
     uint8_t* dr = dev<uint8_t>(dR_, n);
     if (!dl || !dr) return fail(PS_CUDA_ERROR, "device allocation failed (images)");
+    defer_left_ = deferred ? left : nullptr;
+    defer_right_ = deferred ? right : nullptr;
+    if (deferred) {
+        have_inputs_ = true;
+        have_outputs_ = false;
+        streamed_ = false;
+        return PS_OK;
+    }
     ps_status s = check(cudaMemcpyAsync(dl, left, n, cudaMemcpyHostToDevice, st_), "H2D left");
     if (s != PS_OK) return s;
     s = check(cudaMemcpyAsync(dr, right, n, cudaMemcpyHostToDevice, st_), "H2D right");
@@ -338,6 +348,7 @@ ps_status Engine::device_inputs(int frames, int width, int height, uint8_t** lef
     *left = dev<uint8_t>(dL_, n);
     *right = dev<uint8_t>(dR_, n);
     if (!*left || !*right) return fail(PS_CUDA_ERROR, "device allocation failed (images)");
+    defer_left_ = defer_right_ = nullptr;
     have_inputs_ = true;
     have_outputs_ = false;
     streamed_ = false;
@@ -412,7 +423,6 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     int* dRemV = dev<int>(dRemV_, size_t(F) * cells_max);
     int* dRemCount = dev<int>(dRemCount_, F);
     int* dConf = dev<int>(dConf_, F);
-    int* dChunk = dev<int>(dChunk_, size_t(F) * chunks + 1);
     unsigned long long* dTraceSum = dev<unsigned long long>(dTraceSum_, size_t(F) * iters);
     unsigned* dTraceValid = dev<uint32_t>(dTraceValid_, size_t(F) * iters);
     int* dErr = dev<int>(dErr_, 1);
@@ -424,7 +434,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     const void* must[] = {dMask, dMaskCount, dCL, dCR, dDf, dDv, dCf, dCode, dDense, dDenseV, dDit,
                           dSu, dSv, dSd, dS, dSnext, dTaken, dCg, dCb, dBinKeys, dBinCount,
                           dScratch, dCandU, dCandV, dCandCount, dOk, dDisp, dRemU, dRemV,
-                          dRemCount, dConf, dChunk, dTraceSum, dTraceValid, dErr, hS, hMaskCount,
+                          dRemCount, dConf, dTraceSum, dTraceValid, dErr, hS, hMaskCount,
                           hTraceSum, hTraceValid};
     for (const void* p : must)
         if (!p) return fail(PS_CUDA_ERROR, "allocation failed for a batch of " + std::to_string(F) +
@@ -433,41 +443,17 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
 
     const uint8_t* dL = static_cast<const uint8_t*>(dL_.p);
     const uint8_t* dR = static_cast<const uint8_t*>(dR_.p);
-    // ---- state init (pipeline.cpp:145-146: D_f invalid, C_f = costHigh everywhere)
-    cudaMemsetAsync(dMaskCount, 0, sizeof(int) * F, st_);
-    cudaMemsetAsync(dTaken, 0, sizeof(uint32_t) * F * words, st_);
-    cudaMemsetAsync(dTraceSum, 0, sizeof(unsigned long long) * F * iters, st_);
-    cudaMemsetAsync(dTraceValid, 0, sizeof(unsigned) * F * iters, st_);
-    cudaMemsetAsync(dDf, 0, sizeof(float) * F * P, st_);
-    cudaMemsetAsync(dErr, 0, sizeof(int), st_);
-
-    // ---- K1 frontend (image.cpp:43-60, census.cpp:10-41)
-    begin_kernel("frontend", 11.0 * double(P) * F, st_);
-    launches_ += launch_frontend(dL, dR, g, F, cfg.gradient_threshold, dMask, dCL, dCR, dMaskCount, st_,
-                                 dCode, tab.code_high);
-    end_kernel(st_);
-    // ---- K2 candidates (sparse.cpp:84-146)
-    begin_kernel("candidates", double(P) * F, st_);
-    launches_ += launch_candidates(dL, g, F, cfg.corner_threshold, cfg.per_bin_cap, dBinKeys,
-                                   dBinCount, dScratch, sc_stride, dCandU, dCandV, nullptr,
-                                   dCandCount, cand_stride, st_);
-    end_kernel(st_);
-    // ---- K3 seed match (sparse.cpp:148-195) + ordered compaction
-    begin_kernel("match_seed", 0.0, st_);
-    launches_ += launch_match(dCL, dCR, g, F, cfg.max_disparity, tab, dCandU, dCandV, dCandCount,
-                              cand_stride, cand_stride, dOk, dDisp, nullptr, st_);
-    end_kernel(st_);
-    begin_kernel("compact", 0.0, st_);
-    launches_ += launch_emit_matches(dCandU, dCandV, dCandCount, cand_stride, cand_stride, dOk,
-                                     dDisp, g, F, dTaken, dSu, dSv, dSd, scap_, nullptr, nullptr,
-                                     dS, dChunk, st_);
-    end_kernel(st_);
-    ps_status s = check(cudaMemcpyAsync(hS, dS, sizeof(int) * F, cudaMemcpyDeviceToHost, st_), "D2H S");
-    if (s == PS_OK)
-        s = check(cudaMemcpyAsync(hMaskCount, dMaskCount, sizeof(int) * F, cudaMemcpyDeviceToHost, st_),
-                  "D2H M");
-    if (s == PS_OK) s = sync("seeding");
-    if (s != PS_OK) return s;
+    // A deferred upload (ps_run_batch) is consumed by this run whatever
+    // happens: on an early return the batch no longer counts as uploaded.
+    struct DeferGuard {
+        Engine* e;
+        ~DeferGuard() {
+            if (e->defer_left_) e->have_inputs_ = false;
+            e->defer_left_ = e->defer_right_ = nullptr;
+        }
+    } defer_guard{this};
+    const uint8_t* upL = defer_left_;
+    const uint8_t* upR = defer_right_;
 
     status_.assign(F, PS_OK);
     final_count_.assign(F, 0);
@@ -477,17 +463,22 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     for (int f = 0; f < F; ++f) {
         hu_[f].clear();
         hv_[f].clear();
-        if (hS[f] < 3) status_[f] = PS_SEEDING_FAILED;  // pipeline.cpp:151-154
     }
     trace_.assign(size_t(F) * iters, ps_iter_stats{});
 
-    // ---- frame groups: a dataflow pipeline.  Per group, each iteration is
+    // ---- frame groups: a dataflow pipeline.  Per group: (H2D of a deferred
+    //   upload ->) seeding on the group's stream; then each iteration is
     //   delta D2H -> Delaunay tasks on the worker pool -> triangles H2D ->
     //   device stages on the group's stream -> (completion) -> next iteration.
     // The host loop below only moves data and launches; the workers
     // triangulate continuously while the device runs other groups' stages.
     const int G = std::max(1, std::min(std::min(kMaxGroups, max_groups_), (F + 31) / 32));
     const int tri_cap = int(std::min<long long>(2ll * scap_ + 8, 2ll * P + 8));  // T <= 2S per frame
+    cudaMemsetAsync(dErr, 0, sizeof(int), st_);
+    ps_status s = check(cudaEventRecord(start_event_, st_), "start event");
+    if (s != PS_OK) return s;
+    const long long scratch_per_frame =
+        cfg.per_bin_cap > 8 ? std::max<long long>(120 * sc_stride, n_pow2) : 0;
     for (int gi = 0; gi < G; ++gi) {
         FrameGroup& grp = groups_[gi];
         grp.f0 = int((long long)F * gi / G);
@@ -500,17 +491,77 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         grp.pending.store(0);
         int* hs = host<int>(grp.hS, grp.n);
         int* hsp = host<int>(grp.hSprev, grp.n);
+        int* gchunk = dev<int>(grp.dChunk, size_t(grp.n) * chunks + 1);
         if (!host<int>(grp.hPackOff, grp.n) || !host<int>(grp.hTriOff, grp.n + 1) ||
             !dev<int>(grp.dTriOff, grp.n + 1) || !dev<int>(grp.dPackOff, grp.n) ||
-            !dev<int>(grp.dSprev, grp.n) || !dev<int>(grp.dChunk, size_t(grp.n) * chunks + 1) ||
+            !dev<int>(grp.dSprev, grp.n) || !gchunk ||
             !host<int>(grp.hTri, size_t(grp.n) * tri_cap * 3) ||
-            !host<uint8_t>(grp.hPin, size_t(grp.n) * tri_cap) || !hs || !hsp)
+            !host<uint8_t>(grp.hPin, size_t(grp.n) * tri_cap) || !hs || !hsp) {
+            pool_->wait_idle();
             return fail(PS_CUDA_ERROR, "allocation failed (group staging)");
-        if (!grp.done_event) cudaEventCreateWithFlags(&grp.done_event, cudaEventDisableTiming);
-        for (int i = 0; i < grp.n; ++i) {
-            hs[i] = hS[grp.f0 + i];
-            hsp[i] = 0;
         }
+        if (!grp.done_event) cudaEventCreateWithFlags(&grp.done_event, cudaEventDisableTiming);
+
+        // ---- seeding of the group's frames on its own stream
+        cudaStream_t gs = grp.st;
+        const int f0 = grp.f0, n = grp.n;
+        const size_t fp = size_t(f0) * P;
+        s = check(cudaStreamWaitEvent(gs, start_event_, 0), "stream order");
+        if (s == PS_OK && upL)
+            s = check(cudaMemcpyAsync(static_cast<uint8_t*>(dL_.p) + fp, upL + fp, size_t(n) * P,
+                                      cudaMemcpyHostToDevice, gs), "H2D left");
+        if (s == PS_OK && upR)
+            s = check(cudaMemcpyAsync(static_cast<uint8_t*>(dR_.p) + fp, upR + fp, size_t(n) * P,
+                                      cudaMemcpyHostToDevice, gs), "H2D right");
+        if (s != PS_OK) {
+            pool_->wait_idle();
+            return s;
+        }
+        // state init (pipeline.cpp:145-146: D_f invalid, C_f = costHigh -> code)
+        cudaMemsetAsync(dMaskCount + f0, 0, sizeof(int) * n, gs);
+        cudaMemsetAsync(dTaken + size_t(f0) * words, 0, sizeof(uint32_t) * n * words, gs);
+        cudaMemsetAsync(dTraceSum + size_t(f0) * iters, 0, sizeof(unsigned long long) * n * iters, gs);
+        cudaMemsetAsync(dTraceValid + size_t(f0) * iters, 0, sizeof(unsigned) * n * iters, gs);
+        cudaMemsetAsync(dDf + fp, 0, sizeof(float) * n * P, gs);
+        // K1 frontend (image.cpp:43-60, census.cpp:10-41)
+        begin_kernel("frontend", 11.0 * double(P) * n, gs);
+        launches_ += launch_frontend(dL + fp, dR + fp, g, n, cfg.gradient_threshold, dMask + fp,
+                                     dCL + fp, dCR + fp, dMaskCount + f0, gs, dCode + fp,
+                                     tab.code_high);
+        end_kernel(gs);
+        // K2 candidates (sparse.cpp:84-146)
+        int* cu = dCandU + size_t(f0) * cand_stride;
+        int* cv = dCandV + size_t(f0) * cand_stride;
+        begin_kernel("candidates", double(P) * n, gs);
+        launches_ += launch_candidates(dL + fp, g, n, cfg.corner_threshold, cfg.per_bin_cap,
+                                       dBinKeys + size_t(f0) * 120 * cfg.per_bin_cap,
+                                       dBinCount + size_t(f0) * 120,
+                                       dScratch + size_t(f0) * scratch_per_frame, sc_stride, cu,
+                                       cv, nullptr, dCandCount + f0, cand_stride, gs);
+        end_kernel(gs);
+        // K3 seed match (sparse.cpp:148-195) + ordered compaction
+        uint8_t* ok = dOk + size_t(f0) * cand_stride;
+        int* disp = dDisp + size_t(f0) * cand_stride;
+        begin_kernel("match_seed", 0.0, gs);
+        launches_ += launch_match(dCL + fp, dCR + fp, g, n, cfg.max_disparity, tab, cu, cv,
+                                  dCandCount + f0, cand_stride, cand_stride, ok, disp, nullptr, gs);
+        end_kernel(gs);
+        begin_kernel("compact", 0.0, gs);
+        launches_ += launch_emit_matches(cu, cv, dCandCount + f0, cand_stride, cand_stride, ok, disp,
+                                         g, n, dTaken + size_t(f0) * words, dSu + size_t(f0) * scap_,
+                                         dSv + size_t(f0) * scap_, dSd + size_t(f0) * scap_, scap_,
+                                         nullptr, nullptr, grp.S, gchunk, gs);
+        end_kernel(gs);
+        s = check(cudaMemcpyAsync(hS + f0, grp.S, sizeof(int) * n, cudaMemcpyDeviceToHost, gs), "D2H S");
+        if (s == PS_OK)
+            s = check(cudaMemcpyAsync(hMaskCount + f0, dMaskCount + f0, sizeof(int) * n,
+                                      cudaMemcpyDeviceToHost, gs), "D2H M");
+        if (s == PS_OK) s = check(cudaEventRecord(grp.done_event, gs), "seed event");
+        if (s != PS_OK) {
+            pool_->wait_idle();
+            return s;
+        }
+        grp.phase = FrameGroup::kSeed;
     }
     std::mutex done_m;
     std::condition_variable done_cv;
@@ -771,16 +822,6 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     };
 
     // ---- the dataflow loop
-    for (int gi = 0; gi < G; ++gi) {
-        FrameGroup& grp = groups_[gi];
-        s = fetch_delta(grp, false);  // seeds: counts already on the host
-        if (s != PS_OK) {
-            pool_->wait_idle();
-            return s;
-        }
-        grp.it = 1;
-        submit_dt(grp);
-    }
     int done_groups = 0;
     while (done_groups < G) {
         bool progress = false;
@@ -793,12 +834,30 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                     return s;
                 }
                 progress = true;
-            } else if (grp.phase == FrameGroup::kDevice) {
+            } else if (grp.phase == FrameGroup::kDevice || grp.phase == FrameGroup::kSeed) {
                 const cudaError_t q = cudaEventQuery(grp.done_event);
                 if (q == cudaErrorNotReady) continue;
                 if (q != cudaSuccess) {
                     pool_->wait_idle();
                     return check(q, "device stages");
+                }
+                if (grp.phase == FrameGroup::kSeed) {  // seeds are in: first Delaunay
+                    int* hs = static_cast<int*>(grp.hS.p);
+                    int* hsp = static_cast<int*>(grp.hSprev.p);
+                    for (int i = 0; i < grp.n; ++i) {
+                        hs[i] = hS[grp.f0 + i];
+                        hsp[i] = 0;
+                        if (hs[i] < 3) status_[grp.f0 + i] = PS_SEEDING_FAILED;  // pipeline.cpp:151-154
+                    }
+                    s = fetch_delta(grp, false);
+                    if (s != PS_OK) {
+                        pool_->wait_idle();
+                        return s;
+                    }
+                    grp.it = 1;
+                    submit_dt(grp);
+                    progress = true;
+                    continue;
                 }
                 const double ms = now_ms() - grp.tic;
                 for (int i = 0; i < grp.n; ++i) trace_[size_t(grp.f0 + i) * iters + (grp.it - 1)].millis = ms;

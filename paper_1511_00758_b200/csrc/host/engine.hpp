@@ -42,7 +42,7 @@ struct KernelStat {
 
 // A contiguous range of frames with its own stream and per-iteration staging.
 struct FrameGroup {
-    enum Phase { kIdle, kHost, kDevice, kDone };
+    enum Phase { kIdle, kSeed, kHost, kDevice, kDone };
     int f0 = 0;
     int n = 0;
     int it = 0;                   // iteration being processed
@@ -70,7 +70,12 @@ public:
     cudaStream_t stream() const { return st_; }
     std::string& error() { return err_; }
 
-    ps_status upload(int frames, const uint8_t* left, const uint8_t* right, int width, int height);
+    // deferred = true (ps_run_batch only): the host images are copied by the
+    // next run_resident(), group by group on the group streams, so the first
+    // group's seeding overlaps the other groups' H2D; the caller keeps the
+    // buffers alive until that run returns.
+    ps_status upload(int frames, const uint8_t* left, const uint8_t* right, int width, int height,
+                     bool deferred = false);
     // The batch input buffers themselves, for inputs generated on the device
     // (ps_synth_resident); afterwards the batch counts as uploaded.
     ps_status device_inputs(int frames, int width, int height, uint8_t** left, uint8_t** right);
@@ -171,6 +176,9 @@ private:
     int F_ = 0, W_ = 0, H_ = 0;
     long long P_ = 0;
     bool have_inputs_ = false;
+    const uint8_t* defer_left_ = nullptr;  // upload(deferred): host images not yet copied
+    const uint8_t* defer_right_ = nullptr;
+    cudaEvent_t start_event_ = nullptr;  // st_ work the group streams wait on
     bool have_outputs_ = false;
     int iters_ = 0;
     float cost_high_ = 0.5f;
