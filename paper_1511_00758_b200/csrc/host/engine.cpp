@@ -151,6 +151,8 @@ Engine::Engine(int device) : device_(device) {
     cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking);
     for (FrameGroup& g : groups_) cudaStreamCreateWithFlags(&g.st, cudaStreamNonBlocking);
     cudaEventCreateWithFlags(&start_event_, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&chain_event_, cudaEventDisableTiming);
+    if (const char* e = std::getenv("PS_SERIAL_DEVICE")) serial_device_ = std::atoi(e) != 0;
     pool_ = new ThreadPool(host_threads());
     ws_.resize(pool_->size());
 }
@@ -185,6 +187,7 @@ Engine::~Engine() {
     }
     for (cudaEvent_t e : event_pool_) cudaEventDestroy(e);
     if (start_event_) cudaEventDestroy(start_event_);
+    if (chain_event_) cudaEventDestroy(chain_event_);
     if (st_) cudaStreamDestroy(st_);
     delete pool_;
 }
@@ -563,6 +566,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         }
         grp.phase = FrameGroup::kSeed;
     }
+    bool chained = false;  // chain_event_ recorded in this run
     std::mutex done_m;
     std::condition_variable done_cv;
     std::atomic<double> dt_ms_sum{0.0}, sweep_ms_sum{0.0}, pins_ms_sum{0.0};
@@ -722,6 +726,8 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
             final_count_[f0 + i] = hs[i];
         }
 
+        if (serial_device_ && chained) cudaStreamWaitEvent(gs, chain_event_, 0);
+
         // ---- K5/K6 mesh (mesh.cpp:44-123) -> interpolated disparity (mesh.cpp:149-182)
         float* lk = dDit + size_t(f0) * P;
         cudaMemsetAsync(lk, 0xff, sizeof(float) * n * P, gs);  // NaN: outside the hull
@@ -801,6 +807,10 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                                              scap_, grp.S, dConf + f0, grp.Snext, chunk, gs);
             end_kernel(gs);
             std::swap(grp.S, grp.Snext);
+        }
+        if (serial_device_) {
+            cudaEventRecord(chain_event_, gs);
+            chained = true;
         }
         if (last && sink_.active) {
             // streamed download of this group's final outputs (download())

@@ -179,6 +179,12 @@ private:
     const uint8_t* defer_left_ = nullptr;  // upload(deferred): host images not yet copied
     const uint8_t* defer_right_ = nullptr;
     cudaEvent_t start_event_ = nullptr;  // st_ work the group streams wait on
+    // Device stages of different groups run one after another (FIFO through
+    // chain_event_) rather than concurrently: the GPU is idle most of a pass
+    // (the host Delaunay bounds it), so nothing is lost, and every launch gets
+    // the whole GPU.  PS_SERIAL_DEVICE=0 lets groups overlap.
+    bool serial_device_ = true;
+    cudaEvent_t chain_event_ = nullptr;
     bool have_outputs_ = false;
     int iters_ = 0;
     float cost_high_ = 0.5f;
