@@ -303,6 +303,18 @@ def run_ours(args, rank, world, local_rank):
     h2d = 2 * frames * P
     d2h = frames * P * (4 + 1 + 4 + 4 + 1) + frames * cfg.iterations * C.sizeof(ps._native.PsIterStats)
 
+    # ---------------- single-frame latency through ps_run, wall clock
+    lat = []
+    for _ in range(5):
+        t0 = time.perf_counter()
+        ctx.run(L[0], R[0], cfg, unchecked_cell=True)
+        lat.append((time.perf_counter() - t0) * 1e3)
+    lat.sort()
+
+    # ---------------- Delaunay throughput (K4 is host work: points/s)
+    points_per_pass = sum(int(t.support_count) for t in trace)  # the e2e batch's trace
+    sweep = kstats_timed.get("host_sweep", {"ms": 0.0})
+
     # ---------------- roofline of the dominant graded kernel (K7 refine)
     peak, peak_src = measured_peak()
 
@@ -334,6 +346,7 @@ def run_ours(args, rank, world, local_rank):
         "roofline": {"kernel": "k_refine (K7 interpolate+cost+refine, fused K9 on the last iteration)",
                      "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if peak else None, "peak_source": peak_src,
+                     "frac_of_spec_8tbs": achieved / 8000.0,
                      "bytes_per_launch": per_launch_bytes, "ms_per_launch": per_launch_ms,
                      "launches_timed": kstats_timed.get("refine", {}).get("launches", 0),
                      "measured": "CUDA events on each launch's own stream, live over the timed region",
@@ -346,6 +359,15 @@ def run_ours(args, rank, world, local_rank):
                 "api": "ps_run_batch (C ABI) with pinned host buffers"},
         "clocks": clocks,
         "failed_frames": int((status != 0).sum()),
+        "delaunay": {"points_per_pass": points_per_pass,
+                     "points_per_s": points_per_pass / (ms / args.steps / 1e3),
+                     "sweep_ms_per_pass_per_worker": sweep["ms"] / args.steps,
+                     "sweep_ms_per_frame_iteration":
+                         sweep["ms"] / args.steps * ctx.host_threads() / (frames * cfg.iterations),
+                     "workers": ctx.host_threads(),
+                     "note": "host lexicographic sweep (reference order), one task per frame and iteration"},
+        "latency": {"ours_ms_min": lat[0], "ours_ms_median": lat[len(lat) // 2],
+                    "what": "one frame of the workload through ps_run (host buffers in and out), wall clock"},
     }
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -355,6 +377,12 @@ def run_ours(args, rank, world, local_rank):
         t0 = time.perf_counter()
         checker.run_batch(L[:n], R[:n], cfg, cores)
         dt = time.perf_counter() - t0
+        rl = []
+        for _ in range(3):  # eval.cpp:144-177 benchmark(): min over repeats, one thread
+            r0 = time.perf_counter()
+            checker.run(L[0], R[0], cfg)
+            rl.append((time.perf_counter() - r0) * 1e3)
+        line["latency"]["reference_ms_min"] = min(rl)
         line["cpu_baseline"] = {
             "value": n / dt, "unit": UNIT, "cores": cores, "kind": kind,
             "sample": f"{n} of the {frames} frames, one frame per host thread on {cores} threads "

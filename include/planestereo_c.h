@@ -146,6 +146,9 @@ ps_status ps_set_profiling(ps_ctx* ctx, int enabled);
 /* At most `groups` frame groups (CUDA streams) in flight; default 8.  With 1
  * the device stages run back to back, so kernel times are isolated. */
 ps_status ps_set_max_groups(ps_ctx* ctx, int groups);
+/* Host worker threads of the context's Delaunay pool (affinity CPUs / local
+ * ranks, or PS_HOST_THREADS). */
+ps_status ps_get_host_threads(ps_ctx* ctx, int* threads);
 ps_status ps_reset_kernel_stats(ps_ctx* ctx);
 ps_status ps_get_kernel_stats(ps_ctx* ctx, ps_kernel_stat* out, int capacity, int* count);
 /* Kernel launches issued by this context since creation. */

@@ -301,6 +301,11 @@ class Context:
     def set_max_groups(self, groups: int) -> None:
         _check(self._lib.ps_set_max_groups(self._h, groups))
 
+    def host_threads(self) -> int:
+        n = C.c_int()
+        _check(self._lib.ps_get_host_threads(self._h, C.byref(n)))
+        return n.value
+
     def reset_kernel_stats(self) -> None:
         _check(self._lib.ps_reset_kernel_stats(self._h))
 

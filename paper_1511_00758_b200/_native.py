@@ -113,6 +113,7 @@ SIGNATURES = {
     "ps_get_supports": (I, [P, I, P, P, P, I, P]),
     "ps_set_profiling": (I, [P, I]),
     "ps_set_max_groups": (I, [P, I]),
+    "ps_get_host_threads": (I, [P, P]),
     "ps_reset_kernel_stats": (I, [P]),
     "ps_get_kernel_stats": (I, [P, P, I, P]),
     "ps_launch_count": (C.c_longlong, [P]),

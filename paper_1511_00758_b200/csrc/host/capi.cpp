@@ -189,6 +189,13 @@ ps_status ps_set_max_groups(ps_ctx* ctx, int groups) {
     return PS_OK;
 }
 
+ps_status ps_get_host_threads(ps_ctx* ctx, int* threads) {
+    PS_REQUIRE_CTX(ctx);
+    if (!threads) return set_error(PS_ERROR, "null output");
+    *threads = ctx->engine->pool().size();
+    return PS_OK;
+}
+
 ps_status ps_reset_kernel_stats(ps_ctx* ctx) {
     PS_REQUIRE_CTX(ctx);
     ctx->engine->reset_stats();
