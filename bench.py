@@ -366,6 +366,8 @@ def run_ours(args, rank, world, local_rank):
                          sweep["ms"] / args.steps * ctx.host_threads() / (frames * cfg.iterations),
                      "workers": ctx.host_threads(),
                      "note": "host lexicographic sweep (reference order), one task per frame and iteration"},
+        "host_pipeline_ms_per_step": {k: v["ms"] / args.steps for k, v in kstats_timed.items()
+                                      if k.startswith("host_")},
         "latency": {"ours_ms_min": lat[0], "ours_ms_median": lat[len(lat) // 2],
                     "what": "one frame of the workload through ps_run (host buffers in and out), wall clock"},
     }

@@ -152,6 +152,7 @@ Engine::Engine(int device) : device_(device) {
     for (FrameGroup& g : groups_) cudaStreamCreateWithFlags(&g.st, cudaStreamNonBlocking);
     cudaEventCreateWithFlags(&start_event_, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&chain_event_, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&seed_event_, cudaEventDisableTiming);
     if (const char* e = std::getenv("PS_SERIAL_DEVICE")) serial_device_ = std::atoi(e) != 0;
     pool_ = new ThreadPool(host_threads());
     ws_.resize(pool_->size());
@@ -188,6 +189,7 @@ Engine::~Engine() {
     for (cudaEvent_t e : event_pool_) cudaEventDestroy(e);
     if (start_event_) cudaEventDestroy(start_event_);
     if (chain_event_) cudaEventDestroy(chain_event_);
+    if (seed_event_) cudaEventDestroy(seed_event_);
     if (st_) cudaStreamDestroy(st_);
     delete pool_;
 }
@@ -509,6 +511,8 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         cudaStream_t gs = grp.st;
         const int f0 = grp.f0, n = grp.n;
         const size_t fp = size_t(f0) * P;
+        // seeding in group order: group 0's seeds (and so the first host
+        // tasks) arrive after 1/G of the seeding time, not all of it
         s = check(cudaStreamWaitEvent(gs, start_event_, 0), "stream order");
         if (s == PS_OK && upL)
             s = check(cudaMemcpyAsync(static_cast<uint8_t*>(dL_.p) + fp, upL + fp, size_t(n) * P,
@@ -516,6 +520,8 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         if (s == PS_OK && upR)
             s = check(cudaMemcpyAsync(static_cast<uint8_t*>(dR_.p) + fp, upR + fp, size_t(n) * P,
                                       cudaMemcpyHostToDevice, gs), "H2D right");
+        if (s == PS_OK && gi > 0 && serial_device_)
+            s = check(cudaStreamWaitEvent(gs, seed_event_, 0), "seed order");
         if (s != PS_OK) {
             pool_->wait_idle();
             return s;
@@ -560,6 +566,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
             s = check(cudaMemcpyAsync(hMaskCount + f0, dMaskCount + f0, sizeof(int) * n,
                                       cudaMemcpyDeviceToHost, gs), "D2H M");
         if (s == PS_OK) s = check(cudaEventRecord(grp.done_event, gs), "seed event");
+        if (s == PS_OK && serial_device_) s = check(cudaEventRecord(seed_event_, gs), "seed chain");
         if (s != PS_OK) {
             pool_->wait_idle();
             return s;
@@ -570,6 +577,8 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     std::mutex done_m;
     std::condition_variable done_cv;
     std::atomic<double> dt_ms_sum{0.0}, sweep_ms_sum{0.0}, pins_ms_sum{0.0};
+    const double run_t0 = now_ms();
+    std::atomic<double> first_task{1e300}, last_task{0.0};  // pool occupancy (profiling)
     auto add_ms = [](std::atomic<double>& acc, double x) {
         double cur = acc.load();
         while (!acc.compare_exchange_weak(cur, cur + x)) {}
@@ -668,7 +677,10 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                     }
                 }
                 g2.ntri[i] = t;
-                add_ms(dt_ms_sum, now_ms() - t0);
+                const double t1 = now_ms();
+                add_ms(dt_ms_sum, t1 - t0);
+                for (double cur = first_task.load(); t0 < cur && !first_task.compare_exchange_weak(cur, t0);) {}
+                for (double cur = last_task.load(); t1 > cur && !last_task.compare_exchange_weak(cur, t1);) {}
                 if (g2.pending.fetch_sub(1) == 1) {
                     std::lock_guard<std::mutex> lk(done_m);
                     done_cv.notify_all();
@@ -939,6 +951,19 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         KernelStat& pn = stat("host_pins");  // of which: hull-vertex pins
         pn.launches += F * iters;
         pn.ms += pins_ms_sum.load() / workers;
+        // pool occupancy: before the first task, gaps between tasks, after the last
+        const double fa = first_task.load(), la = last_task.load(), end = now_ms();
+        if (la > 0.0) {
+            KernelStat& fill = stat("host_fill");
+            fill.launches += 1;
+            fill.ms += fa - run_t0;
+            KernelStat& gap = stat("host_gaps");  // per worker, between first and last task
+            gap.launches += 1;
+            gap.ms += (la - fa) - dt_ms_sum.load() / workers;
+            KernelStat& drain = stat("host_drain");
+            drain.launches += 1;
+            drain.ms += end - la;
+        }
     }
     if (herr) return fail(PS_DEGENERATE_TRIANGLE, "collinear vertices in a triangle");
     for (int f = 0; f < F; ++f) {

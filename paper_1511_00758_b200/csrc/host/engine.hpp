@@ -185,6 +185,7 @@ private:
     // the whole GPU.  PS_SERIAL_DEVICE=0 lets groups overlap.
     bool serial_device_ = true;
     cudaEvent_t chain_event_ = nullptr;
+    cudaEvent_t seed_event_ = nullptr;  // seeding runs group after group (group 0 first)
     bool have_outputs_ = false;
     int iters_ = 0;
     float cost_high_ = 0.5f;
