@@ -143,6 +143,30 @@ def test_streamed_download_into_page_locked_buffers(ctx):
     assert streamed["costs"][5].min() == cfg.costHigh and streamed["disparity_valid"][5].sum() == 0
 
 
+def test_schedules_agree(monkeypatch):
+    """Frame groups seeded and refined one after another (the default event
+    chain) or concurrently (PS_SERIAL_DEVICE=0), with 1 or 8 groups: the same
+    bits — results do not depend on the device schedule."""
+    c = ps.BASELINE_CONFIGS[2]
+    cfg = ps.baseline_config(2)
+    n = 70  # three frame groups of uneven size
+    L, R = ps.synth_batch(n, 160, 120, c["n_planes"], 40, False, 2.0, seed=31)
+    cfg.maxDisparity = 40
+    runs = []
+    for serial in ("1", "0"):
+        monkeypatch.setenv("PS_SERIAL_DEVICE", serial)
+        with ps.Context(0) as cx:
+            runs.append(cx.run_batch(L, R, cfg, unchecked_cell=True, raise_on_failure=False))
+            cx.set_max_groups(1)
+            runs.append(cx.run_batch(L, R, cfg, unchecked_cell=True, raise_on_failure=False))
+    for r in runs[1:]:
+        assert (r["status"] == runs[0]["status"]).all()
+        for k in ["disparity", "disparity_valid", "costs", "dense", "dense_valid"]:
+            assert np.array_equal(bits(r[k]), bits(runs[0][k])), k
+        assert [[t.meanCost for t in tr] for tr in r["trace"]] == \
+               [[t.meanCost for t in tr] for tr in runs[0]["trace"]]
+
+
 @pytest.mark.parametrize("w,h", [(16, 16), (17, 19), (37, 23), (64, 16), (255, 17)])
 def test_small_and_odd_sizes(ctx, orc, w, h):
     rng = np.random.default_rng(w * 100 + h)
