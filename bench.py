@@ -268,7 +268,7 @@ def run_ours(args, rank, world, local_rank):
     ctx.run_resident(cfg, unchecked_cell=True)
     kstats = ctx.kernel_stats()
     ctx.set_profiling(False)
-    ctx.set_max_groups(8)
+    ctx.set_max_groups(int(os.environ.get("PS_MAX_GROUPS", "8")))
     status = np.zeros(frames, np.int32)
     lib.ps_download_batch(ctx._h, None, None, None, None, None, None, status.ctypes.data_as(C.c_void_p))
     value = whole_job_value(frames, world, args.steps, ms)

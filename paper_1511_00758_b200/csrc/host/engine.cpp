@@ -16,6 +16,7 @@
 #include <chrono>
 #include <cmath>
 #include <condition_variable>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -149,11 +150,17 @@ static int host_threads() {
 Engine::Engine(int device) : device_(device) {
     cudaSetDevice(device_);
     cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking);
-    for (FrameGroup& g : groups_) cudaStreamCreateWithFlags(&g.st, cudaStreamNonBlocking);
+    // The groups' pipeline stages (small, latency-critical: they feed the host
+    // pool) run at high priority; the bulk seeding at low priority.
+    int prio_low = 0, prio_high = 0;
+    cudaDeviceGetStreamPriorityRange(&prio_low, &prio_high);
+    for (FrameGroup& g : groups_) cudaStreamCreateWithPriority(&g.st, cudaStreamNonBlocking, prio_high);
+    cudaStreamCreateWithPriority(&seed_st_, cudaStreamNonBlocking, prio_low);
     cudaEventCreateWithFlags(&start_event_, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&chain_event_, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&seed_event_, cudaEventDisableTiming);
     if (const char* e = std::getenv("PS_SERIAL_DEVICE")) serial_device_ = std::atoi(e) != 0;
+    if (const char* e = std::getenv("PS_MAX_GROUPS")) set_max_groups(std::atoi(e));
+    debug_timeline_ = std::getenv("PS_DEBUG_TIMELINE") != nullptr;
     pool_ = new ThreadPool(host_threads());
     ws_.resize(pool_->size());
 }
@@ -189,7 +196,7 @@ Engine::~Engine() {
     for (cudaEvent_t e : event_pool_) cudaEventDestroy(e);
     if (start_event_) cudaEventDestroy(start_event_);
     if (chain_event_) cudaEventDestroy(chain_event_);
-    if (seed_event_) cudaEventDestroy(seed_event_);
+    if (seed_st_) cudaStreamDestroy(seed_st_);
     if (st_) cudaStreamDestroy(st_);
     delete pool_;
 }
@@ -484,7 +491,11 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     if (s != PS_OK) return s;
     const long long scratch_per_frame =
         cfg.per_bin_cap > 8 ? std::max<long long>(120 * sc_stride, n_pow2) : 0;
-    for (int gi = 0; gi < G; ++gi) {
+    // Seeding of one group on its own stream.  Group 0 is launched before the
+    // dataflow loop, the others from inside it (one per loop turn), so the
+    // first host tasks do not wait for the launches of every group.
+    for (int gi = 0; gi < G; ++gi) groups_[gi].phase = FrameGroup::kIdle;
+    auto seed_group = [&](int gi) -> ps_status {
         FrameGroup& grp = groups_[gi];
         grp.f0 = int((long long)F * gi / G);
         grp.n = int((long long)F * (gi + 1) / G) - grp.f0;
@@ -502,30 +513,24 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
             !dev<int>(grp.dSprev, grp.n) || !gchunk ||
             !host<int>(grp.hTri, size_t(grp.n) * tri_cap * 3) ||
             !host<uint8_t>(grp.hPin, size_t(grp.n) * tri_cap) || !hs || !hsp) {
-            pool_->wait_idle();
             return fail(PS_CUDA_ERROR, "allocation failed (group staging)");
         }
         if (!grp.done_event) cudaEventCreateWithFlags(&grp.done_event, cudaEventDisableTiming);
 
-        // ---- seeding of the group's frames on its own stream
-        cudaStream_t gs = grp.st;
+        // ---- seeding of the group's frames on the (low-priority) seeding
+        // stream, in group order: group 0's seeds, and so the first host
+        // tasks, arrive after 1/G of the seeding time
+        cudaStream_t gs = seed_st_;
         const int f0 = grp.f0, n = grp.n;
         const size_t fp = size_t(f0) * P;
-        // seeding in group order: group 0's seeds (and so the first host
-        // tasks) arrive after 1/G of the seeding time, not all of it
-        s = check(cudaStreamWaitEvent(gs, start_event_, 0), "stream order");
+        ps_status s = gi == 0 ? check(cudaStreamWaitEvent(gs, start_event_, 0), "stream order") : PS_OK;
         if (s == PS_OK && upL)
             s = check(cudaMemcpyAsync(static_cast<uint8_t*>(dL_.p) + fp, upL + fp, size_t(n) * P,
                                       cudaMemcpyHostToDevice, gs), "H2D left");
         if (s == PS_OK && upR)
             s = check(cudaMemcpyAsync(static_cast<uint8_t*>(dR_.p) + fp, upR + fp, size_t(n) * P,
                                       cudaMemcpyHostToDevice, gs), "H2D right");
-        if (s == PS_OK && gi > 0 && serial_device_)
-            s = check(cudaStreamWaitEvent(gs, seed_event_, 0), "seed order");
-        if (s != PS_OK) {
-            pool_->wait_idle();
-            return s;
-        }
+        if (s != PS_OK) return s;
         // state init (pipeline.cpp:145-146: D_f invalid, C_f = costHigh -> code)
         cudaMemsetAsync(dMaskCount + f0, 0, sizeof(int) * n, gs);
         cudaMemsetAsync(dTaken + size_t(f0) * words, 0, sizeof(uint32_t) * n * words, gs);
@@ -566,19 +571,22 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
             s = check(cudaMemcpyAsync(hMaskCount + f0, dMaskCount + f0, sizeof(int) * n,
                                       cudaMemcpyDeviceToHost, gs), "D2H M");
         if (s == PS_OK) s = check(cudaEventRecord(grp.done_event, gs), "seed event");
-        if (s == PS_OK && serial_device_) s = check(cudaEventRecord(seed_event_, gs), "seed chain");
-        if (s != PS_OK) {
-            pool_->wait_idle();
-            return s;
-        }
+        // the group's own stream continues after its seeding
+        if (s == PS_OK) s = check(cudaStreamWaitEvent(grp.st, grp.done_event, 0), "group order");
+        if (s != PS_OK) return s;
         grp.phase = FrameGroup::kSeed;
-    }
+        return PS_OK;
+    };
+    const double run_t0 = now_ms();
+    s = seed_group(0);
+    if (s != PS_OK) return s;
+    int next_seed = 1;
     bool chained = false;  // chain_event_ recorded in this run
     std::mutex done_m;
     std::condition_variable done_cv;
     std::atomic<double> dt_ms_sum{0.0}, sweep_ms_sum{0.0}, pins_ms_sum{0.0};
-    const double run_t0 = now_ms();
     std::atomic<double> first_task{1e300}, last_task{0.0};  // pool occupancy (profiling)
+    std::vector<double> worker_end(pool_->size(), 0.0);     // PS_DEBUG_TIMELINE
     auto add_ms = [](std::atomic<double>& acc, double x) {
         double cur = acc.load();
         while (!acc.compare_exchange_weak(cur, cur + x)) {}
@@ -586,6 +594,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
 
     // (1) supports added since the group's last iteration -> pinned host staging
     auto fetch_delta = [&](FrameGroup& grp, bool counts) -> ps_status {
+        const double tfd0 = now_ms();
         const int n = grp.n;
         cudaStream_t gs = grp.st;
         int* hs = static_cast<int*>(grp.hS.p);
@@ -624,7 +633,11 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         if (total_new > 0)
             r = check(cudaMemcpyAsync(hPack, dPack, sizeof(int2) * total_new, cudaMemcpyDeviceToHost, gs),
                       "D2H supports");
+        const double tsync = now_ms();
         if (r == PS_OK) r = sync(gs, "support delta");
+        if (debug_timeline_)
+            std::fprintf(stderr, "[tl]   fetch_delta g%d it%d: launch %.3f ms, sync %.3f ms\n",
+                         int(&grp - groups_), grp.it, tsync - tfd0, now_ms() - tsync);
         return r;
     };
 
@@ -681,6 +694,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                 add_ms(dt_ms_sum, t1 - t0);
                 for (double cur = first_task.load(); t0 < cur && !first_task.compare_exchange_weak(cur, t0);) {}
                 for (double cur = last_task.load(); t1 > cur && !last_task.compare_exchange_weak(cur, t1);) {}
+                worker_end[worker] = t1;
                 if (g2.pending.fetch_sub(1) == 1) {
                     std::lock_guard<std::mutex> lk(done_m);
                     done_cv.notify_all();
@@ -847,6 +861,14 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     int done_groups = 0;
     while (done_groups < G) {
         bool progress = false;
+        if (next_seed < G) {
+            s = seed_group(next_seed++);
+            if (s != PS_OK) {
+                pool_->wait_idle();
+                return s;
+            }
+            progress = true;
+        }
         for (int gi = 0; gi < G; ++gi) {
             FrameGroup& grp = groups_[gi];
             if (grp.phase == FrameGroup::kHost && grp.pending.load() == 0) {
@@ -864,6 +886,8 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                     return check(q, "device stages");
                 }
                 if (grp.phase == FrameGroup::kSeed) {  // seeds are in: first Delaunay
+                    if (debug_timeline_)
+                        std::fprintf(stderr, "[tl] group %d seeds in at %.3f ms\n", gi, now_ms() - run_t0);
                     int* hs = static_cast<int*>(grp.hS.p);
                     int* hsp = static_cast<int*>(grp.hSprev.p);
                     for (int i = 0; i < grp.n; ++i) {
@@ -877,6 +901,8 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                         return s;
                     }
                     grp.it = 1;
+                    if (debug_timeline_)
+                        std::fprintf(stderr, "[tl] group %d first tasks at %.3f ms\n", gi, now_ms() - run_t0);
                     submit_dt(grp);
                     progress = true;
                     continue;
@@ -896,6 +922,9 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                     }
                     observer(grp.it, fd.data(), fv.data(), fc.data(), W, H, user);
                 }
+                if (debug_timeline_)
+                    std::fprintf(stderr, "[tl] group %d iteration %d device done at %.3f ms\n", gi, grp.it,
+                                 now_ms() - run_t0);
                 if (grp.it == iters) {
                     grp.phase = FrameGroup::kDone;
                     ++done_groups;
@@ -918,6 +947,13 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         }
     }
     host_dt_ms = dt_ms_sum.load() / std::max(1, pool_->size());
+    if (debug_timeline_) {
+        std::sort(worker_end.begin(), worker_end.end());
+        std::fprintf(stderr, "[tl] last task end at %.3f ms, loop end at %.3f ms; workers' last task ends (ms before the last):",
+                     last_task.load() - run_t0, now_ms() - run_t0);
+        for (double e : worker_end) std::fprintf(stderr, " %.2f", worker_end.back() - e);
+        std::fprintf(stderr, "\n");
+    }
 
     // ---- trace (pipeline.cpp:183-191)
     for (int gi = 0; gi < G; ++gi) {
@@ -933,7 +969,9 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     if (s == PS_OK) s = check(cudaMemcpyAsync(&herr, dErr, sizeof(int), cudaMemcpyDeviceToHost, st_), "D2H err");
     if (s == PS_OK) s = sync("pipeline");
     if (s != PS_OK) return s;
+    if (debug_timeline_) std::fprintf(stderr, "[tl] trace in at %.3f ms\n", now_ms() - run_t0);
     resolve_timers();
+    if (debug_timeline_) std::fprintf(stderr, "[tl] timers resolved at %.3f ms\n", now_ms() - run_t0);
     if (profiling_) {
         auto stat = [&](const char* name) -> KernelStat& {
             for (auto& k : stats_)

@@ -184,8 +184,9 @@ private:
     // (the host Delaunay bounds it), so nothing is lost, and every launch gets
     // the whole GPU.  PS_SERIAL_DEVICE=0 lets groups overlap.
     bool serial_device_ = true;
+    bool debug_timeline_ = false;  // PS_DEBUG_TIMELINE: group milestones on stderr
     cudaEvent_t chain_event_ = nullptr;
-    cudaEvent_t seed_event_ = nullptr;  // seeding runs group after group (group 0 first)
+    cudaStream_t seed_st_ = nullptr;  // seeding, group after group (group 0 first)
     bool have_outputs_ = false;
     int iters_ = 0;
     float cost_high_ = 0.5f;
