@@ -706,6 +706,9 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     // (3) triangles H2D + device stages of iteration grp.it on the group's stream
     auto launch_device = [&](FrameGroup& grp) -> ps_status {
         const int it = grp.it;
+        if (debug_timeline_)
+            std::fprintf(stderr, "[tl] group %d iteration %d host done at %.3f ms\n", int(&grp - groups_), it,
+                         now_ms() - run_t0);
         const bool last = it == iters;
         const int cell = cell_of[it - 1];
         const int cols = ceil_div(W, cell);
@@ -721,23 +724,24 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
             total_tri += grp.ntri[i];
         }
         hTriOff[n] = int(total_tri);
-        const size_t ntot = size_t(std::max<long long>(total_tri, 1));
-        int* dTri = dev<int>(grp.dTri, ntot * 3);
-        uint8_t* dPin = dev<uint8_t>(grp.dPin, ntot);
+        // one pitched copy per group: frame i's triangles at i * pitch
+        int max_nt = 1;
+        for (int i = 0; i < n; ++i) max_nt = std::max(max_nt, grp.ntri[i]);
+        const size_t pitch = size_t(max_nt);
+        int* dTri = dev<int>(grp.dTri, size_t(n) * pitch * 3);
+        uint8_t* dPin = dev<uint8_t>(grp.dPin, size_t(n) * pitch);
         int* dTriOff = static_cast<int*>(grp.dTriOff.p);
         if (!dTri || !dPin) return fail(PS_CUDA_ERROR, "allocation failed (triangles)");
         ps_status r = PS_OK;
-        for (int i = 0; i < n && r == PS_OK; ++i) {
-            if (grp.ntri[i] == 0) continue;
-            r = check(cudaMemcpyAsync(dTri + 3ll * hTriOff[i],
-                                      static_cast<int*>(grp.hTri.p) + size_t(i) * tri_cap * 3,
-                                      sizeof(int) * 3 * grp.ntri[i], cudaMemcpyHostToDevice, gs),
-                      "H2D triangles");
+        begin_kernel("h2d_triangles", 13.0 * double(pitch) * n, gs);
+        if (total_tri > 0) {
+            r = check(cudaMemcpy2DAsync(dTri, pitch * 12, grp.hTri.p, size_t(tri_cap) * 12, pitch * 12, n,
+                                        cudaMemcpyHostToDevice, gs), "H2D triangles");
             if (r == PS_OK)
-                r = check(cudaMemcpyAsync(dPin + hTriOff[i],
-                                          static_cast<uint8_t*>(grp.hPin.p) + size_t(i) * tri_cap,
-                                          grp.ntri[i], cudaMemcpyHostToDevice, gs), "H2D pins");
+                r = check(cudaMemcpy2DAsync(dPin, pitch, grp.hPin.p, size_t(tri_cap), pitch, n,
+                                            cudaMemcpyHostToDevice, gs), "H2D pins");
         }
+        end_kernel(gs);
         if (r == PS_OK)
             r = check(cudaMemcpyAsync(dTriOff, hTriOff, sizeof(int) * (n + 1), cudaMemcpyHostToDevice, gs),
                       "H2D triangle offsets");
@@ -757,10 +761,11 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         // ---- K5/K6 mesh (mesh.cpp:44-123) -> interpolated disparity (mesh.cpp:149-182)
         float* lk = dDit + size_t(f0) * P;
         cudaMemsetAsync(lk, 0xff, sizeof(float) * n * P, gs);  // NaN: outside the hull
-        begin_kernel("mesh", 4.0 * double(P) * n + 36.0 * double(total_tri), gs);
+        begin_kernel(it == 1 ? "mesh_it1" : it == 2 ? "mesh_it2" : "mesh_it3", 4.0 * double(P) * n + 36.0 * double(total_tri), gs);
         launches_ += launch_mesh_disparity(dTri, dTriOff, n, total_tri, dSu + size_t(f0) * scap_,
                                            dSv + size_t(f0) * scap_, dSd + size_t(f0) * scap_,
-                                           scap_, g, dPin, float(cfg.max_disparity), lk, dErr, gs);
+                                           scap_, g, dPin, float(cfg.max_disparity), lk, dErr, gs,
+                                           (long long)pitch);
         end_kernel(gs);
 
         // ---- K7 (+K9) refine (mesh.cpp:149-182, pipeline.cpp:33-86)
@@ -853,6 +858,9 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                 cudaMemcpyAsync(sink_.dense_valid + b, dDenseV + b, cnt, cudaMemcpyDeviceToHost, gs);
         }
         cudaEventRecord(grp.done_event, gs);
+        if (debug_timeline_)
+            std::fprintf(stderr, "[tl] group %d iteration %d launched at %.3f ms\n", int(&grp - groups_), it,
+                         now_ms() - run_t0);
         grp.phase = FrameGroup::kDevice;
         return PS_OK;
     };

@@ -60,11 +60,13 @@ int launch_mesh(const int* tris, const int* tri_off, int frames, long long total
 // Pipeline variant: rasterises the interpolated disparity itself
 // (interpolate(), mesh.cpp:149-182) instead of the triangle id: dit[px] =
 // binary32 plane value when 0 <= d < max_disp, NaN for invalid or outside the
-// hull.  dit must be preset to NaN (memset 0xff).
+// hull.  dit must be preset to NaN (memset 0xff).  tri_pitch > 0: frame f's
+// triangles (and pin bytes) sit at f * tri_pitch in the arrays (one pitched
+// copy per frame group) instead of flat at tri_off[f].
 int launch_mesh_disparity(const int* tris, const int* tri_off, int frames, long long total_tris,
                           const int* su, const int* sv, const double* sd, int scap, FrameGeom g,
                           const uint8_t* pin_bits, float max_disp, float* dit, int* err_flag,
-                          cudaStream_t st);
+                          cudaStream_t st, long long tri_pitch = 0);
 
 // K7 (+K9 when last) — fused interpolate / costEvaluation / disparityRefinement
 // with per-cell packed-key atomicMin grids and the trace reduction

@@ -8,11 +8,15 @@
 //   * the thread solves its plane in binary64 in the reference's source order
 //     with _rn intrinsics (no FMA);
 //   * small triangles (the vast majority after the first iteration: median
-//     2x area 3-15 px) are filled by their own thread, row by row,
-//     from the exact integer span [lo, hi] of each row with the top-left tie
-//     bias (mesh.cpp:75-106);
+//     2x area 3-15 px): the warp deals its 32 triangles' rows to
+//     its lanes, 32 rows at a time, each lane computing the exact integer
+//     span [lo, hi] of its row with the top-left tie bias (mesh.cpp:75-106),
+//     then deals the pixels of those spans, 32 at a time — every lane busy
+//     whatever the shapes of the 32 triangles;
 //   * large ones are handed to the whole warp, which computes 32 row spans at
-//     once (one per lane) and fills each row with coalesced stores.
+//     once (one per lane) and fills each row with coalesced stores; when the
+//     mean triangle of a launch covers >= 64 px (the first iteration's mesh)
+//     the launch runs one warp per triangle.
 // Pinning (mesh.cpp:109-122): an uncovered vertex pixel takes its first
 // incident triangle; which (triangle, corner) pairs pin is decided on the host
 // from the exact tie rule (pins.cpp) and passed as 3 bits per triangle, so the
@@ -48,56 +52,6 @@ __device__ __forceinline__ int frame_of(const int* __restrict__ tri_off, int fra
     return lo;
 }
 
-// Row-incremental form of one edge's constraint (mesh.cpp:88-99): per row the
-// exact ceil/floor quotient advances by a precomputed quotient/remainder step,
-// so a triangle pays two divisions per edge instead of one per edge and row.
-template <class Int>
-struct EdgeWalk {
-    int kind;  // 1: u >= q (A > 0), 2: u <= q (A < 0), 0: horizontal, row test K >= bias
-    Int q, r, qs, rs, B, K, dK, bias;
-
-    __device__ __forceinline__ void init(int xi, int yi, int xj, int yj, int v0) {
-        const Int A = Int(yi - yj);
-        bias = ((yj < yi) || (yj == yi && xj > xi)) ? 0 : 1;
-        const Int dx = Int(xj - xi);
-        K = dx * Int(v0 - yi) + Int(yj - yi) * Int(xi);  // edge value at (0, v0)
-        dK = dx;
-        if (A > 0) {  // lo(v) = ceil((bias - K) / A)
-            kind = 1;
-            B = A;
-            const Int N = bias - K;
-            q = ceil_div<Int>(N, B);
-            r = q * B - N;               // in [0, B)
-            qs = floor_div<Int>(-dx, B);  // N decreases by dx per row
-            rs = -dx - qs * B;           // in [0, B)
-        } else if (A < 0) {  // hi(v) = floor((K - bias) / -A)
-            kind = 2;
-            B = -A;
-            const Int M = K - bias;
-            q = floor_div<Int>(M, B);
-            r = M - q * B;  // in [0, B)
-            qs = floor_div<Int>(dx, B);
-            rs = dx - qs * B;
-        } else {
-            kind = 0;
-        }
-    }
-    __device__ __forceinline__ void step() {
-        if (kind == 1) {
-            const bool c = rs > r;
-            q += qs + (c ? 1 : 0);
-            r += (c ? B : 0) - rs;
-        } else if (kind == 2) {
-            r += rs;
-            const bool c = r >= B;
-            q += qs + (c ? 1 : 0);
-            r -= c ? B : 0;
-        } else {
-            K += dK;
-        }
-    }
-};
-
 // Exact covered span of row v (mesh.cpp:84-103); false if the row is empty.
 template <class Int>
 __device__ __forceinline__ bool row_span(const int* x, const int* y, int v, int W, Int& lo, Int& hi) {
@@ -118,6 +72,48 @@ __device__ __forceinline__ bool row_span(const int* x, const int* y, int v, int 
         }
     }
     return lo <= hi;
+}
+
+// floor(m / d) for d > 0 (C division truncates toward zero).
+template <class Int>
+__device__ __forceinline__ Int floor_div_pos(Int m, Int d) {
+    const Int q = m / d;
+    return (m - q * d < 0) ? q - 1 : q;
+}
+
+// Per-edge constants of the row-span rule (mesh.cpp:84-103) for edge i -> j:
+// the edge value at (u, v) is A*u + K(v) with K(v) = dx*v + C, and the pixel
+// is covered iff A*u + K >= bias.  With m(v) = K(v) - bias = dx*v + cb and
+// F = floor(m / |A|): A > 0 bounds u >= ceil((bias - K) / A) = -F, A < 0
+// bounds u <= floor((K - bias) / -A) = F, and A == 0 empties the row iff
+// m < 0 — one division per edge and row, no branches on the edge kind.
+template <class Int>
+struct EdgeConst {
+    Int a, dx, cb;
+    __device__ __forceinline__ void init(int xi, int yi, int xj, int yj) {
+        a = Int(yi - yj);
+        const Int bias = ((yj < yi) || (yj == yi && xj > xi)) ? 0 : 1;
+        dx = Int(xj - xi);
+        cb = Int(yj - yi) * Int(xi) - dx * Int(yi) - bias;
+    }
+};
+
+template <class Int>
+__device__ __forceinline__ bool row_span_const(const EdgeConst<Int>* e, int v, int W, Int& lo, Int& hi) {
+    lo = 0;
+    hi = W - 1;
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const Int a = e[i].a;
+        const Int m = e[i].dx * Int(v) + e[i].cb;
+        const Int d = a > 0 ? a : (a < 0 ? -a : Int(1));
+        const Int F = floor_div_pos<Int>(m, d);
+        if (a > 0) lo = max(lo, -F);
+        if (a < 0) hi = min(hi, F);
+        if (a == 0 && m < 0) ok = false;
+    }
+    return ok && lo <= hi;
 }
 
 // Output of the raster: the triangle id (DisparityMesh::lookup, the stage
@@ -149,22 +145,29 @@ __global__ void __launch_bounds__(kThreads) k_raster(
     const int* __restrict__ tris, const int* __restrict__ tri_off, int frames, long long total,
     const int* __restrict__ su, const int* __restrict__ sv, const double* __restrict__ sd, int scap,
     FrameGeom g, const uint8_t* __restrict__ pin_bits, double* __restrict__ planes, RasterOut out,
-    int* __restrict__ err) {
-    const long long t = (long long)blockIdx.x * kThreads + threadIdx.x;
+    int* __restrict__ err, long long tri_pitch, bool warp_per_tri) {
+    // one thread per triangle, or (large triangles, e.g. the first
+    // iteration's mesh) one warp per triangle: lane 0 owns it, the warp fills it
     const int lane = threadIdx.x & 31;
-    const bool active = t < total;
+    const long long gtid = (long long)blockIdx.x * kThreads + threadIdx.x;
+    const long long t = warp_per_tri ? gtid >> 5 : gtid;
+    const long long t_block = warp_per_tri ? (long long)blockIdx.x * (kThreads / 32)
+                                           : (long long)blockIdx.x * kThreads;
+    const bool active = t < total && (!warp_per_tri || lane == 0);
     const int W = g.width, H = g.height;
     int x[3] = {0, 0, 0}, y[3] = {0, 0, 0};
     int f = 0, vmin = 0, vmax = -1;
     double pa = 0.0, pb = 0.0, pc = 0.0;
-    bool big = false;
+    bool big = false, small = false;
     // frame of the block's first triangle (uniform), then a short local scan
-    const int fblk = frame_of(tri_off, frames, (long long)blockIdx.x * kThreads);
+    const int fblk = frame_of(tri_off, frames, t_block < total ? t_block : total - 1);
     if (active) {
         f = fblk;
         while (f + 1 < frames && __ldg(tri_off + f + 1) <= t) ++f;
         const long long sb = (long long)f * scap;
-        const int i0 = __ldg(tris + 3 * t), i1 = __ldg(tris + 3 * t + 1), i2 = __ldg(tris + 3 * t + 2);
+        // slot of the triangle in the (flat or per-frame pitched) input arrays
+        const long long ts = tri_pitch > 0 ? (long long)f * tri_pitch + (t - __ldg(tri_off + f)) : t;
+        const int i0 = __ldg(tris + 3 * ts), i1 = __ldg(tris + 3 * ts + 1), i2 = __ldg(tris + 3 * ts + 2);
         x[0] = __ldg(su + sb + i0); x[1] = __ldg(su + sb + i1); x[2] = __ldg(su + sb + i2);
         y[0] = __ldg(sv + sb + i0); y[1] = __ldg(sv + sb + i1); y[2] = __ldg(sv + sb + i2);
         // fitPlane, mesh.cpp:12-26 (integer det exact; doubles in source order)
@@ -196,7 +199,7 @@ __global__ void __launch_bounds__(kThreads) k_raster(
         }
         const long long fb = f * g.pixels;
         if (pin_bits) {
-            const unsigned bits = __ldg(pin_bits + t);
+            const unsigned bits = __ldg(pin_bits + ts);
 #pragma unroll
             for (int k = 0; k < 3; ++k)
                 if ((bits >> k) & 1u)
@@ -207,30 +210,78 @@ __global__ void __launch_bounds__(kThreads) k_raster(
         const int xmin = min(x[0], min(x[1], x[2])), xmax = max(x[0], max(x[1], x[2]));
         // warp-cooperative only when the bounding box is large (many pixels
         // or many rows); slivers and small triangles stay on their thread
-        big = (long long)(vmax - vmin + 1) * (xmax - xmin + 1) > 192 || (vmax - vmin) >= 32;
-        if (!big && vmin <= vmax) {
-            EdgeWalk<Int> e[3];
+        big = warp_per_tri || (long long)(vmax - vmin + 1) * (xmax - xmin + 1) > 192 || (vmax - vmin) >= 32;
+        small = !big && vmin <= vmax;
+    }
+    // Small triangles, flattened twice so that every lane stays busy: the
+    // warp's (triangle, row) pairs are dealt 32 at a time, one row per lane
+    // (exact span by row_span), then the pixels of those 32 spans are dealt
+    // 32 at a time (span found by binary search of the span prefix sums).
+    {
+        __shared__ EdgeConst<Int> s_e[3 * kThreads];
+        __shared__ double s_pa[kThreads], s_pb[kThreads], s_pc[kThreads];
+        __shared__ long long s_fb[kThreads], s_row[kThreads];
+        __shared__ int s_vmin[kThreads], s_tid[kThreads], s_rpre[kThreads];
+        __shared__ int s_pre[kThreads], s_lo[kThreads], s_k[kThreads], s_v[kThreads];
+        const int me = threadIdx.x, wb = me & ~31;
 #pragma unroll
-            for (int i = 0; i < 3; ++i) {
-                const int j = (i + 1) % 3;
-                e[i].init(x[i], y[i], x[j], y[j], vmin);
-            }
-            for (int v = vmin;; ++v) {
-                Int lo = 0, hi = W - 1;
-                bool empty = false;
+        for (int k = 0; k < 3; ++k) s_e[3 * me + k].init(x[k], y[k], x[(k + 1) % 3], y[(k + 1) % 3]);
+        s_pa[me] = pa;
+        s_pb[me] = pb;
+        s_pc[me] = pc;
+        s_fb[me] = (long long)f * g.pixels;
+        s_vmin[me] = vmin;
+        s_tid[me] = int32_t(t);
+        const int nrows = small ? vmax - vmin + 1 : 0;
+        int rincl = nrows;
 #pragma unroll
-                for (int i = 0; i < 3; ++i) {
-                    if (e[i].kind == 1) lo = max(lo, e[i].q);
-                    else if (e[i].kind == 2) hi = min(hi, e[i].q);
-                    else if (e[i].K < e[i].bias) empty = true;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y2 = __shfl_up_sync(0xffffffffu, rincl, o);
+            if (lane >= o) rincl += y2;
+        }
+        s_rpre[me] = rincl - nrows;
+        const int total_rows = __shfl_sync(0xffffffffu, rincl, 31);
+        __syncwarp();
+        for (int r0 = 0; r0 < total_rows; r0 += 32) {
+            const int r = r0 + lane;
+            int len = 0, lo32 = 0, k = wb, v = 0;
+            if (r < total_rows) {
+                int sp = 0;  // the last triangle whose row prefix is <= r
+#pragma unroll
+                for (int step = 16; step; step >>= 1)
+                    if (s_rpre[wb + sp + step] <= r) sp += step;
+                k = wb + sp;
+                v = s_vmin[k] + (r - s_rpre[k]);
+                Int lo, hi;
+                if (row_span_const<Int>(s_e + 3 * k, v, W, lo, hi)) {
+                    len = int(hi - lo) + 1;
+                    lo32 = int(lo);
                 }
-                if (!empty)
-                    for (int u = int(lo); u <= int(hi); ++u)
-                        put(out, fb, (long long)v * W + u, int32_t(t), pa, pb, pc, u, v);
-                if (v == vmax) break;
-#pragma unroll
-                for (int i = 0; i < 3; ++i) e[i].step();
             }
+            int incl = len;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y2 = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y2;
+            }
+            const int total_px = __shfl_sync(0xffffffffu, incl, 31);
+            s_pre[me] = incl - len;
+            s_lo[me] = lo32;
+            s_k[me] = k;
+            s_v[me] = v;
+            s_row[me] = s_fb[k] + (long long)v * W;
+            __syncwarp();
+            for (int j = lane; j < total_px; j += 32) {
+                int sp = 0;  // the last span whose pixel prefix is <= j
+#pragma unroll
+                for (int step = 16; step; step >>= 1)
+                    if (s_pre[wb + sp + step] <= j) sp += step;
+                const int q = wb + sp;
+                const int kt = s_k[q];
+                const int u = s_lo[q] + (j - s_pre[q]);
+                put(out, s_row[q], u, s_tid[kt], s_pa[kt], s_pb[kt], s_pc[kt], u, s_v[q]);
+            }
+            __syncwarp();
         }
     }
     // Large triangles: the whole warp, 32 rows at a time.
@@ -273,10 +324,14 @@ __global__ void __launch_bounds__(kThreads) k_raster(
 template <class Int>
 void launch_raster(const int* tris, const int* tri_off, int frames, long long total, const int* su,
                    const int* sv, const double* sd, int scap, FrameGeom g, const uint8_t* pin_bits,
-                   double* planes, RasterOut out, int* err, cudaStream_t st) {
-    const unsigned blocks = unsigned((total + kThreads - 1) / kThreads);
+                   double* planes, RasterOut out, int* err, cudaStream_t st, long long tri_pitch = 0) {
+    // warp per triangle when the mean triangle covers >= 64 px: a thread per
+    // triangle would leave too few warps, each looping over 32 large triangles
+    const bool warp_per_tri = double(g.pixels) * frames >= 64.0 * double(total);
+    const long long threads = warp_per_tri ? 32 * total : total;
+    const unsigned blocks = unsigned((threads + kThreads - 1) / kThreads);
     k_raster<Int><<<blocks, kThreads, 0, st>>>(tris, tri_off, frames, total, su, sv, sd, scap, g,
-                                               pin_bits, planes, out, err);
+                                               pin_bits, planes, out, err, tri_pitch, warp_per_tri);
 }
 
 }  // namespace
@@ -299,15 +354,15 @@ int launch_mesh(const int* tris, const int* tri_off, int frames, long long total
 int launch_mesh_disparity(const int* tris, const int* tri_off, int frames, long long total_tris,
                           const int* su, const int* sv, const double* sd, int scap, FrameGeom g,
                           const uint8_t* pin_bits, float max_disp, float* dit, int* err_flag,
-                          cudaStream_t st) {
+                          cudaStream_t st, long long tri_pitch) {
     if (total_tris <= 0) return 0;
     const RasterOut out{nullptr, dit, max_disp};
     if (g.width < (1 << 14) && g.height < (1 << 14))
         launch_raster<int>(tris, tri_off, frames, total_tris, su, sv, sd, scap, g, pin_bits,
-                           nullptr, out, err_flag, st);
+                           nullptr, out, err_flag, st, tri_pitch);
     else
         launch_raster<long long>(tris, tri_off, frames, total_tris, su, sv, sd, scap, g, pin_bits,
-                                 nullptr, out, err_flag, st);
+                                 nullptr, out, err_flag, st, tri_pitch);
     return 1;
 }
 
