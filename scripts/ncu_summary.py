@@ -53,5 +53,8 @@ for row in r[2:]:
     key = "k_refine" if "k_refine" in name else ("k_raster" if "k_raster" in name else name[:40])
     traffic.setdefault(key, []).append(rd + wr)
 open(os.path.join(out_dir, f"ncu_{tag}.md"), "w").write("\n".join(lines) + "\n")
-json.dump({k: sum(v) / len(v) for k, v in traffic.items()}, open(os.path.join(out_dir, "ncu_traffic.json"), "w"), indent=1)
+tpath = os.path.join(out_dir, "ncu_traffic.json")
+merged = json.load(open(tpath)) if os.path.exists(tpath) else {}
+merged.update({k: sum(v) / len(v) for k, v in traffic.items()})  # per launch, bytes
+json.dump(merged, open(tpath, "w"), indent=1)
 print("\n".join(lines))
