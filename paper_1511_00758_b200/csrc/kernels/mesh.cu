@@ -90,13 +90,32 @@ __device__ __forceinline__ Int floor_div_pos(Int m, Int d) {
 template <class Int>
 struct EdgeConst {
     Int a, dx, cb;
+    double rd;  // 1 / max(|a|, 1): floor(m / |a|) by one multiply (32-bit operands)
     __device__ __forceinline__ void init(int xi, int yi, int xj, int yj) {
         a = Int(yi - yj);
         const Int bias = ((yj < yi) || (yj == yi && xj > xi)) ? 0 : 1;
         dx = Int(xj - xi);
         cb = Int(yj - yi) * Int(xi) - dx * Int(yi) - bias;
+        const Int d = a > 0 ? a : (a < 0 ? -a : Int(1));
+        rd = __drcp_rn(double(d));
     }
 };
+
+// floor(m / d), d > 0.  For 32-bit operands (|m| < 2^31, d < 2^14) the double
+// product m * RN(1/d) is within 2^-21 of m / d, so its floor is off by at most
+// one, only next to an exact quotient; one remainder test corrects it.
+template <class Int>
+__device__ __forceinline__ Int floor_div_rcp(Int m, Int d, double rd) {
+    if constexpr (sizeof(Int) == 4) {
+        Int q = Int(floor(double(m) * rd));
+        const Int r = m - q * d;
+        q += (r >= d) ? 1 : 0;
+        q -= (r < 0) ? 1 : 0;
+        return q;
+    } else {
+        return floor_div_pos<Int>(m, d);
+    }
+}
 
 template <class Int>
 __device__ __forceinline__ bool row_span_const(const EdgeConst<Int>* e, int v, int W, Int& lo, Int& hi) {
@@ -108,7 +127,7 @@ __device__ __forceinline__ bool row_span_const(const EdgeConst<Int>* e, int v, i
         const Int a = e[i].a;
         const Int m = e[i].dx * Int(v) + e[i].cb;
         const Int d = a > 0 ? a : (a < 0 ? -a : Int(1));
-        const Int F = floor_div_pos<Int>(m, d);
+        const Int F = floor_div_rcp<Int>(m, d, e[i].rd);
         if (a > 0) lo = max(lo, -F);
         if (a < 0) hi = min(hi, F);
         if (a == 0 && m < 0) ok = false;
