@@ -46,6 +46,9 @@ def parse_args():
     p.add_argument("--frames", type=int, default=0, help="frames per GPU (default: the config's)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-frames", type=int, default=128)
+    p.add_argument("--configs", default="",
+                   help="comma list of BASELINE configs: print a markdown table of ours (ps_run_batch, "
+                        "pinned buffers, wall clock) vs the reference CPU arm instead of the JSON line")
     return p.parse_args()
 
 
@@ -397,12 +400,78 @@ def run_ours(args, rank, world, local_rank):
     del keep
 
 
+CONFIG_FRAMES = {0: 64, 1: 64, 2: 256, 3: 16, 4: 16}
+CONFIG_REF = {0: True, 1: True, 2: True, 3: True, 4: False}
+
+
+def run_configs_table(args):
+    """SURVEY 8(d) for every BASELINE config: ours (one batch through ps_run_batch with
+    pinned buffers, copies included; one frame through ps_run) beside the
+    reference CPU arm (one frame per host thread on all threads; one frame on
+    one thread).  Wall clock: the whole call is the unit of work; the device-
+    timed headline is the JSON line.  The reference legs are skipped where one
+    frame takes minutes (cfg4)."""
+    import numpy as np
+    import torch
+
+    import paper_1511_00758_b200 as ps
+
+    cfgs = [int(c) for c in args.configs.split(",")]
+    ctx = ps.Context(0)
+    threads = ctx.host_threads()
+    ref, _ = cpu_checker()
+    print("| config | shape | iterations | frames | ours frames/s (e2e) | ours Mpix/s | ours 1-frame ms "
+          "| reference frames/s (%d threads) | reference 1-frame ms | speed-up (throughput) |" % threads)
+    print("|---|---|---:|---:|---:|---:|---:|---:|---:|---:|")
+    for k in cfgs:
+        c = ps.BASELINE_CONFIGS[k]
+        cfg = ps.baseline_config(k)
+        n = CONFIG_FRAMES[k]
+        w, h = c["width"], c["height"]
+        L = torch.empty((n, h, w), dtype=torch.uint8, pin_memory=True).numpy()
+        R = torch.empty((n, h, w), dtype=torch.uint8, pin_memory=True).numpy()
+        ps.synth_batch(n, w, h, c["n_planes"], c["max_disparity"], c["ground"], c["sigma"], seed=4000 + k,
+                       left=L, right=R)
+        out = {key: torch.empty((n, h, w), dtype=dt, pin_memory=True).numpy()
+               for key, dt in [("disparity", torch.float32), ("disparity_valid", torch.uint8),
+                               ("costs", torch.float32), ("dense", torch.float32),
+                               ("dense_valid", torch.uint8)]}
+        ctx.run_batch(L, R, cfg, unchecked_cell=True, raise_on_failure=False, out=out)  # warm-up
+        t0 = time.perf_counter()
+        res = ctx.run_batch(L, R, cfg, unchecked_cell=True, raise_on_failure=False, out=out)
+        dt = time.perf_counter() - t0
+        ours = n / dt
+        lat = []
+        for _ in range(1 if k == 4 else 3):
+            t0 = time.perf_counter()
+            ctx.run(L[0], R[0], cfg, unchecked_cell=True)
+            lat.append((time.perf_counter() - t0) * 1e3)
+        rfps = rlat = None
+        if ref is not None and CONFIG_REF[k]:
+            m = min(n, threads)
+            t0 = time.perf_counter()
+            ref.run_batch(L[:m], R[:m], cfg, threads)
+            rfps = m / (time.perf_counter() - t0)
+            t0 = time.perf_counter()
+            ref.run(L[0], R[0], cfg)
+            rlat = (time.perf_counter() - t0) * 1e3
+        failed = int((np.asarray(res["status"]) != 0).sum())
+        print(f"| cfg{k} | {w}x{h}, ND {c['max_disparity']}, grid {c['cell']} | {c['iterations']} | {n}"
+              f"{' (' + str(failed) + ' failed)' if failed else ''} | {ours:.1f} | {ours * w * h / 1e6:.1f} "
+              f"| {min(lat):.1f} | {'%.2f' % rfps if rfps else 'not run'} | {'%.0f' % rlat if rlat else 'not run'} "
+              f"| {'%.1fx' % (ours / rfps) if rfps else '-'} |", flush=True)
+    ctx.close()
+
+
+
 def main():
     args = parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.impl == "reference":
+    if args.configs:
+        run_configs_table(args)
+    elif args.impl == "reference":
         run_reference_arm(args, rank, world)
     else:
         run_ours(args, rank, world, local_rank)

@@ -2,12 +2,12 @@
 the GPU pipeline (batched, several frames per run) against the C restatement,
 bit for bit on every output map, the support list and the trace.
 
-  python scripts/fuzz_parity.py [N] [seed]
+  python tests/tools/fuzz_parity.py [N] [seed]
 """
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 
 import numpy as np  # noqa: E402
 

@@ -1,6 +1,6 @@
 """Ad-hoc GPU parity probe: CUDA pipeline vs oracle on a few BASELINE shapes (prints diffs)."""
 import sys, time, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import paper_1511_00758_b200 as ps
 import oracle

@@ -1,6 +1,6 @@
 """GPU vs oracle over many BASELINE-style frames: counts every kind of difference."""
 import os, sys, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import paper_1511_00758_b200 as ps
 import oracle

@@ -1,6 +1,6 @@
 """Find frames whose final support list differs between GPU and oracle; print details."""
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import paper_1511_00758_b200 as ps
 import oracle
