@@ -645,11 +645,18 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     // sweep, or the reference-order sweep when the validity of a pinned hull
     // vertex depends on the triangle order (pins.cpp).  Each task writes its
     // triangles and pin bits into the group's pinned staging at a fixed slot.
+    std::vector<int> order;
     auto submit_dt = [&](FrameGroup& grp) {
         grp.pending.store(grp.n);
         grp.phase = FrameGroup::kHost;
         grp.tic = now_ms();
-        for (int i = 0; i < grp.n; ++i) {
+        // largest point sets first: the group's (and the pass's) last tasks
+        // are its smallest, so the workers run out of work more evenly
+        const int* cnt = static_cast<const int*>(grp.hS.p);
+        order.resize(grp.n);
+        for (int i = 0; i < grp.n; ++i) order[i] = i;
+        std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cnt[a] > cnt[b]; });
+        for (const int i : order) {
             pool_->submit([&, i, gp = &grp](int worker) {
                 FrameGroup& g2 = *gp;
                 const double t0 = now_ms();
