@@ -17,6 +17,7 @@
 #include <cmath>
 #include <condition_variable>
 #include <cstdio>
+#include <sys/resource.h>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -578,6 +579,13 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         return PS_OK;
     };
     const double run_t0 = now_ms();
+    auto thread_cpu_ms = [] {
+        rusage ru{};
+        getrusage(RUSAGE_THREAD, &ru);
+        return ru.ru_utime.tv_sec * 1e3 + ru.ru_utime.tv_usec * 1e-3 + ru.ru_stime.tv_sec * 1e3 +
+               ru.ru_stime.tv_usec * 1e-3;
+    };
+    const double cpu_t0 = debug_timeline_ ? thread_cpu_ms() : 0.0;
     s = seed_group(0);
     if (s != PS_OK) return s;
     int next_seed = 1;
@@ -984,7 +992,9 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     if (s == PS_OK) s = check(cudaMemcpyAsync(&herr, dErr, sizeof(int), cudaMemcpyDeviceToHost, st_), "D2H err");
     if (s == PS_OK) s = sync("pipeline");
     if (s != PS_OK) return s;
-    if (debug_timeline_) std::fprintf(stderr, "[tl] trace in at %.3f ms\n", now_ms() - run_t0);
+    if (debug_timeline_)
+        std::fprintf(stderr, "[tl] trace in at %.3f ms; main thread cpu %.3f ms\n", now_ms() - run_t0,
+                     thread_cpu_ms() - cpu_t0);
     resolve_timers();
     if (debug_timeline_) std::fprintf(stderr, "[tl] timers resolved at %.3f ms\n", now_ms() - run_t0);
     if (profiling_) {
