@@ -480,9 +480,11 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     trace_.assign(size_t(F) * iters, ps_iter_stats{});
 
     // ---- frame groups: a dataflow pipeline.  Per group: (H2D of a deferred
-    //   upload ->) seeding on the group's stream; then each iteration is
-    //   delta D2H -> Delaunay tasks on the worker pool -> triangles H2D ->
-    //   device stages on the group's stream -> (completion) -> next iteration.
+    //   upload ->) seeding on the low-priority seeding stream; then each
+    //   iteration is delta D2H -> Delaunay tasks on the worker pool ->
+    //   triangles H2D -> device stages on the group's (high-priority) stream,
+    //   chained after the previous group's stages -> (completion) -> next
+    //   iteration.
     // The host loop below only moves data and launches; the workers
     // triangulate continuously while the device runs other groups' stages.
     const int G = std::max(1, std::min(std::min(kMaxGroups, max_groups_), (F + 31) / 32));
@@ -492,9 +494,9 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     if (s != PS_OK) return s;
     const long long scratch_per_frame =
         cfg.per_bin_cap > 8 ? std::max<long long>(120 * sc_stride, n_pow2) : 0;
-    // Seeding of one group on its own stream.  Group 0 is launched before the
-    // dataflow loop, the others from inside it (one per loop turn), so the
-    // first host tasks do not wait for the launches of every group.
+    // Seeding of one group (on seed_st_, in group order).  Group 0 is launched
+    // before the dataflow loop, the others from inside it (one per loop turn),
+    // so the first host tasks do not wait for the launches of every group.
     for (int gi = 0; gi < G; ++gi) groups_[gi].phase = FrameGroup::kIdle;
     auto seed_group = [&](int gi) -> ps_status {
         FrameGroup& grp = groups_[gi];
