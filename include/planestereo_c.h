@@ -116,6 +116,19 @@ ps_status ps_run_batch(ps_ctx* ctx, int n_frames, const uint8_t* left, const uin
                        float* disparity, uint8_t* disparity_valid, float* cost, float* dense,
                        uint8_t* dense_valid, ps_iter_stats* trace, int* frame_status);
 
+/* The same batch sharded over n_ctx contexts — one per GPU of the box
+ * — from one process: contiguous blocks of
+ * ceil(n_frames / n_ctx) frames, each block run by ps_run_batch on its
+ * context from its own host thread.  Frames never interact, so no collective
+ * is involved.  Same arguments and per-frame outputs as ps_run_batch;
+ * returns the first context-level error (in context order), else the first
+ * non-OK frame status.  The contexts must be distinct. */
+ps_status ps_run_batch_multi(ps_ctx* const* ctxs, int n_ctx, int n_frames, const uint8_t* left,
+                             const uint8_t* right, int width, int height, const ps_config* cfg,
+                             unsigned flags, float* disparity, uint8_t* disparity_valid,
+                             float* cost, float* dense, uint8_t* dense_valid,
+                             ps_iter_stats* trace, int* frame_status);
+
 /* Device-resident variant used to time the pipeline with inputs already in
  * HBM: ps_upload_batch copies the pairs into ctx-owned device memory,
  * ps_run_resident runs the pipeline on them (no host copies of images or

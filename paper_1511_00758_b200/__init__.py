@@ -261,11 +261,7 @@ class Context:
                                     _ptr(res["disparity"]), _ptr(res["disparity_valid"]),
                                     _ptr(res["costs"]), _ptr(res["dense"]),
                                     _ptr(res["dense_valid"]), trace, _ptr(res["status"]))
-        if st != 0 and (raise_on_failure or st != 7):
-            _check(st)
-        res["trace"] = [[_stats(trace[f * config.iterations + i]) for i in range(config.iterations)]
-                        for f in range(n)]
-        return res
+        return _finish_batch(res, st, trace, n, config, raise_on_failure)
 
     def upload(self, left: np.ndarray, right: np.ndarray) -> None:
         n, h, w = left.shape
@@ -651,6 +647,45 @@ def synth_pair(width: int, height: int, n_planes: int, max_disparity: int, groun
     gt = np.zeros((height, width), np.float32) if with_gt else None
     _check(lib.ps_synth_pair(C.byref(p), _ptr(L), _ptr(R), _ptr(gt)))
     return (L, R, gt) if with_gt else (L, R)
+
+
+def _finish_batch(res, st, trace, n, config, raise_on_failure):
+    if st != 0 and (raise_on_failure or st != 7):
+        _check(st)
+    res["trace"] = [[_stats(trace[f * config.iterations + i]) for i in range(config.iterations)]
+                    for f in range(n)]
+    return res
+
+
+def run_batch_multi(contexts, left: np.ndarray, right: np.ndarray, config: PipelineConfig,
+                    unchecked_cell: bool = False, raise_on_failure: bool = True) -> dict:
+    """One (F, H, W) batch sharded over several contexts (one per GPU) from
+    this process: ps_run_batch_multi — contiguous frame blocks, one host
+    thread per context, no collective.  Same result dict as
+    Context.run_batch."""
+    L = np.ascontiguousarray(left, dtype=np.uint8)
+    R = np.ascontiguousarray(right, dtype=np.uint8)
+    if L.ndim != 3 or L.shape != R.shape:
+        raise DimensionMismatch("expected two (F, H, W) uint8 stacks of equal shape")
+    if not contexts:
+        raise ValueError("no contexts")
+    n, h, w = L.shape
+    cfg = config.to_c()
+    res = {"disparity": np.zeros((n, h, w), np.float32), "disparity_valid": np.zeros((n, h, w), np.uint8),
+           "costs": np.zeros((n, h, w), np.float32), "dense": np.zeros((n, h, w), np.float32),
+           "dense_valid": np.zeros((n, h, w), np.uint8), "status": np.zeros(n, np.int32)}
+    handles = (C.c_void_p * len(contexts))(*[cx._h for cx in contexts])
+    trace = (PsIterStats * (n * config.iterations))()
+    lib = contexts[0]._lib
+    st = lib.ps_run_batch_multi(handles, len(contexts), n, _ptr(L), _ptr(R), w, h, C.byref(cfg),
+                                PS_RUN_UNCHECKED_CELL if unchecked_cell else 0,
+                                _ptr(res["disparity"]), _ptr(res["disparity_valid"]), _ptr(res["costs"]),
+                                _ptr(res["dense"]), _ptr(res["dense_valid"]), trace, _ptr(res["status"]))
+    per = (n + len(contexts) - 1) // len(contexts)
+    for i, cx in enumerate(contexts):  # each context holds its own block
+        k = min(n, (i + 1) * per) - min(n, i * per)
+        cx._shape = (k, h, w) if k > 0 else None
+    return _finish_batch(res, st, trace, n, config, raise_on_failure)
 
 
 def synth_batch(n_frames: int, width: int, height: int, n_planes: int, max_disparity: int,

@@ -107,6 +107,7 @@ SIGNATURES = {
     "ps_config_validate": (I, [P, C.c_uint]),
     "ps_run": (I, [P, P, P, I, I, P, C.c_uint, P, P, P, P, P, P, OBSERVER, P]),
     "ps_run_batch": (I, [P, I, P, P, I, I, P, C.c_uint, P, P, P, P, P, P, P]),
+    "ps_run_batch_multi": (I, [P, I, I, P, P, I, I, P, C.c_uint, P, P, P, P, P, P, P]),
     "ps_upload_batch": (I, [P, I, P, P, I, I]),
     "ps_run_resident": (I, [P, P, C.c_uint]),
     "ps_download_batch": (I, [P, P, P, P, P, P, P, P]),

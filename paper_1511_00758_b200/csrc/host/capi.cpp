@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -153,6 +154,51 @@ ps_status ps_run_batch(ps_ctx* ctx, int n_frames, const uint8_t* left, const uin
     if (s != PS_OK) return s;
     if (run != PS_OK) g_last_error = ctx->engine->error();
     return run;
+}
+
+ps_status ps_run_batch_multi(ps_ctx* const* ctxs, int n_ctx, int n_frames, const uint8_t* left,
+                             const uint8_t* right, int width, int height, const ps_config* cfg,
+                             unsigned flags, float* disparity, uint8_t* disparity_valid,
+                             float* cost, float* dense, uint8_t* dense_valid,
+                             ps_iter_stats* trace, int* frame_status) {
+    if (!ctxs || n_ctx < 1) return set_error(PS_ERROR, "no contexts");
+    for (int i = 0; i < n_ctx; ++i) {
+        if (!ctxs[i]) return set_error(PS_ERROR, "null context");
+        for (int j = 0; j < i; ++j)
+            if (ctxs[j] == ctxs[i]) return set_error(PS_ERROR, "a context appears twice");
+    }
+    if (!cfg) return set_error(PS_ERROR, "null config");
+    if (!left || !right) return set_error(PS_ERROR, "null image");
+    ps_status s = ps_config_validate(cfg, flags);
+    if (s != PS_OK) return s;
+    if (n_frames < 1) return set_error(PS_ERROR, "batch needs at least one frame");
+    const long long P = (long long)width * height;
+    const int per = (n_frames + n_ctx - 1) / n_ctx;
+    std::vector<ps_status> st(n_ctx, PS_OK);
+    std::vector<std::string> msg(n_ctx);
+    std::vector<std::thread> th;
+    for (int i = 0; i < n_ctx; ++i) {
+        const int f0 = std::min(n_frames, i * per), n = std::min(n_frames, f0 + per) - f0;
+        if (n <= 0) continue;
+        th.emplace_back([&, i, f0, n] {
+            const size_t px = size_t(f0) * size_t(P);
+            st[i] = ps_run_batch(ctxs[i], n, left + px, right + px, width, height, cfg, flags,
+                                 disparity ? disparity + px : nullptr,
+                                 disparity_valid ? disparity_valid + px : nullptr,
+                                 cost ? cost + px : nullptr, dense ? dense + px : nullptr,
+                                 dense_valid ? dense_valid + px : nullptr,
+                                 trace ? trace + size_t(f0) * cfg->iterations : nullptr,
+                                 frame_status ? frame_status + f0 : nullptr);
+            if (st[i] != PS_OK) msg[i] = g_last_error;  // this thread's message
+        });
+    }
+    for (auto& t : th) t.join();
+    // context-level errors first, then frame statuses (ps_run_batch's precedence)
+    for (int i = 0; i < n_ctx; ++i)
+        if (st[i] != PS_OK && st[i] != PS_SEEDING_FAILED) return set_error(st[i], msg[i]);
+    for (int i = 0; i < n_ctx; ++i)
+        if (st[i] != PS_OK) return set_error(st[i], msg[i]);
+    return PS_OK;
 }
 
 ps_status ps_run(ps_ctx* ctx, const uint8_t* left, const uint8_t* right, int width, int height,

@@ -167,6 +167,29 @@ def test_schedules_agree(monkeypatch):
                [[t.meanCost for t in tr] for tr in runs[0]["trace"]]
 
 
+def test_run_batch_multi_equals_single_context(ctx):
+    """ps_run_batch_multi (frames sharded over contexts, one host thread each;
+    SURVEY 8(e)) gives the single-context bits, with a failed frame in the
+    second block.  Only one GPU is visible here, so both contexts sit on
+    device 0 — the sharding and offsets are what is under test."""
+    L, R = ps.synth_batch(11, 160, 120, 6, 40, False, 2.0, seed=61)
+    L[8] = 128
+    R[8] = 128
+    cfg = ps.PipelineConfig(iterations=2, maxDisparity=40, occupancyCellSize=8)
+    one = ctx.run_batch(L, R, cfg, raise_on_failure=False)
+    with ps.Context(0) as c1, ps.Context(0) as c2:
+        multi = ps.run_batch_multi([c1, c2], L, R, cfg, raise_on_failure=False)
+        with pytest.raises(ps.SeedingFailed):
+            ps.run_batch_multi([c1, c2], L, R, cfg)
+        with pytest.raises(ps.Error):
+            ps.run_batch_multi([c1, c1], L, R, cfg)
+    assert list(multi["status"]) == list(one["status"]) and multi["status"][8] == 7
+    for k in ["disparity", "disparity_valid", "costs", "dense", "dense_valid"]:
+        assert np.array_equal(bits(multi[k]), bits(one[k])), k
+    assert [[t.meanCost for t in tr] for tr in multi["trace"]] == \
+           [[t.meanCost for t in tr] for tr in one["trace"]]
+
+
 @pytest.mark.parametrize("w,h", [(16, 16), (17, 19), (37, 23), (64, 16), (255, 17)])
 def test_small_and_odd_sizes(ctx, orc, w, h):
     rng = np.random.default_rng(w * 100 + h)
