@@ -148,6 +148,18 @@ static int host_threads() {
     return n;
 }
 
+// One Delaunay worker pool per process, shared by every context (several
+// contexts in one process — ps_run_batch_multi — must not multiply the host
+// threads), with one workspace per worker: a worker runs one task at a time.
+static ThreadPool& shared_pool() {
+    static ThreadPool pool(host_threads());
+    return pool;
+}
+static std::vector<DelaunayWorkspace>& shared_workspaces() {
+    static std::vector<DelaunayWorkspace> ws(shared_pool().size());
+    return ws;
+}
+
 Engine::Engine(int device) : device_(device) {
     cudaSetDevice(device_);
     cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking);
@@ -162,8 +174,8 @@ Engine::Engine(int device) : device_(device) {
     if (const char* e = std::getenv("PS_SERIAL_DEVICE")) serial_device_ = std::atoi(e) != 0;
     if (const char* e = std::getenv("PS_MAX_GROUPS")) set_max_groups(std::atoi(e));
     debug_timeline_ = std::getenv("PS_DEBUG_TIMELINE") != nullptr;
-    pool_ = new ThreadPool(host_threads());
-    ws_.resize(pool_->size());
+    pool_ = &shared_pool();
+    ws_ = &shared_workspaces();
 }
 
 Engine::~Engine() {
@@ -199,7 +211,6 @@ Engine::~Engine() {
     if (chain_event_) cudaEventDestroy(chain_event_);
     if (seed_st_) cudaStreamDestroy(seed_st_);
     if (st_) cudaStreamDestroy(st_);
-    delete pool_;
 }
 
 template <class T>
@@ -594,6 +605,16 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     bool chained = false;  // chain_event_ recorded in this run
     std::mutex done_m;
     std::condition_variable done_cv;
+    // Before an early return: wait for this run's own host tasks (they hold
+    // references to this frame); the pool is shared with other contexts.
+    auto drain = [&] {
+        std::unique_lock<std::mutex> lk(done_m);
+        done_cv.wait(lk, [&] {
+            for (int gi = 0; gi < G; ++gi)
+                if (groups_[gi].pending.load() != 0) return false;
+            return true;
+        });
+    };
     std::atomic<double> dt_ms_sum{0.0}, sweep_ms_sum{0.0}, pins_ms_sum{0.0};
     std::atomic<double> first_task{1e300}, last_task{0.0};  // pool occupancy (profiling)
     std::vector<double> worker_end(pool_->size(), 0.0);     // PS_DEBUG_TIMELINE
@@ -689,7 +710,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                 int t = 0;
                 if (status_[f] == PS_OK) {
                     const int ns = int(fu.size());
-                    DelaunayWorkspace& w = ws_[worker];
+                    DelaunayWorkspace& w = (*ws_)[worker];
                     // the reference's triangle order and rotation (pins and
                     // fitPlane rounding then match it bit for bit), written
                     // straight into the group's pinned staging slot
@@ -889,7 +910,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         if (next_seed < G) {
             s = seed_group(next_seed++);
             if (s != PS_OK) {
-                pool_->wait_idle();
+                drain();
                 return s;
             }
             progress = true;
@@ -899,7 +920,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
             if (grp.phase == FrameGroup::kHost && grp.pending.load() == 0) {
                 s = launch_device(grp);
                 if (s != PS_OK) {
-                    pool_->wait_idle();
+                    drain();
                     return s;
                 }
                 progress = true;
@@ -907,7 +928,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                 const cudaError_t q = cudaEventQuery(grp.done_event);
                 if (q == cudaErrorNotReady) continue;
                 if (q != cudaSuccess) {
-                    pool_->wait_idle();
+                    drain();
                     return check(q, "device stages");
                 }
                 if (grp.phase == FrameGroup::kSeed) {  // seeds are in: first Delaunay
@@ -922,7 +943,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                     }
                     s = fetch_delta(grp, false);
                     if (s != PS_OK) {
-                        pool_->wait_idle();
+                        drain();
                         return s;
                     }
                     grp.it = 1;
@@ -956,7 +977,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                 } else {
                     s = fetch_delta(grp, true);
                     if (s != PS_OK) {
-                        pool_->wait_idle();
+                        drain();
                         return s;
                     }
                     grp.it += 1;

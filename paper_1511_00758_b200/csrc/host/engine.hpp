@@ -125,7 +125,7 @@ public:
     ps_status sync(cudaStream_t s, const char* what);
     void count_launches(int n) { launches_ += n; }
     ThreadPool& pool() { return *pool_; }
-    DelaunayWorkspace& workspace(int worker) { return ws_[worker]; }
+    DelaunayWorkspace& workspace(int worker) { return (*ws_)[worker]; }
 
     // Scratch for stage-API calls.
     DevBuf s_a, s_b, s_c, s_d, s_e, s_f, s_g, s_h, s_i, s_j;
@@ -156,8 +156,8 @@ private:
     int device_ = 0;
     cudaStream_t st_ = nullptr;
     std::string err_;
-    ThreadPool* pool_ = nullptr;
-    std::vector<DelaunayWorkspace> ws_;
+    ThreadPool* pool_ = nullptr;               // the process-wide pool (shared_pool)
+    std::vector<DelaunayWorkspace>* ws_ = nullptr;  // its per-worker workspaces
     bool profiling_ = false;
     int max_groups_ = kMaxGroups;
     long long launches_ = 0;
