@@ -2,7 +2,7 @@
 //
 // Declares, in namespace planestereo, every type and function of the
 // reference's public header API (proj/include/planestereo/{error,config,
-// image,disparity,census,sparse,delaunay,mesh,pipeline}.hpp, and wtaOracle of synth.hpp) with the same
+// image,disparity,census,sparse,delaunay,mesh,pipeline,synth}.hpp and accuracy() of eval.hpp) with the same
 // names, signatures, value semantics and exceptions, so code written against
 // the reference recompiles unchanged (the per-name headers next to this one
 // just include it).  The implementation (paper_1511_00758_b200/csrc/cpp_api)
@@ -331,6 +331,59 @@ StereoResult run(const GrayImage& left, const GrayImage& right, const PipelineCo
 // ties toward smaller d.  Runs on the GPU (wta.cu).
 std::pair<DisparityMap, CostMap> wtaOracle(const GrayImage& left, const GrayImage& right,
                                            const GradientMask& mask, int maxDisparity);
+
+// ------------------------------------------------------------------ eval
+// (reference eval.hpp:15-29) Fractions of the pixels valid in both maps (and
+// inside the mask) whose absolute error is strictly below each threshold, and
+// the mean absolute error (binary64, row-major sum).  Throws NoOverlap when
+// no pixel qualifies.  Runs on the GPU (accuracy.cu).  The table / CSV / JSON
+// writers and the timing harness of eval.hpp are not part of this build.
+struct AccuracyReport {
+    std::vector<double> thresholds;
+    std::vector<double> fractions;
+    long evaluated = 0;
+    double meanAbsError = 0.0;
+};
+AccuracyReport accuracy(const DisparityMap& prediction, const DisparityMap& groundTruth,
+                        const GradientMask& mask, const std::vector<double>& thresholds);
+AccuracyReport accuracy(const DisparityMap& prediction, const DisparityMap& groundTruth,
+                        const std::vector<double>& thresholds);
+
+// ------------------------------------------------------------------ synth
+// (reference synth.hpp:14-50) Piecewise-planar test scenes rendered on the GPU
+// (synth.cu: renderScene's texture, contrast stretch, forward warp with
+// occlusion), bit for bit the reference's images and ground truth.
+struct SceneRegion {  // [u0, u1) x [v0, v1) carrying one disparity plane
+    int u0 = 0;
+    int v0 = 0;
+    int u1 = 0;
+    int v1 = 0;
+    DisparityPlane plane;
+};
+
+struct PlanarScene {  // regions must partition the image
+    int width = 640;
+    int height = 480;
+    float maxDisparity = 128.0f;
+    std::uint32_t seed = 1234;
+    std::vector<SceneRegion> regions;
+
+    static PlanarScene flat(double d, int width = 640, int height = 480, std::uint32_t seed = 1234);
+    static PlanarScene slanted(double a, double b, double c, int width = 640, int height = 480,
+                               std::uint32_t seed = 1234);
+    static PlanarScene steps(double dLeft, double dRight, int width = 640, int height = 480,
+                             std::uint32_t seed = 1234);  // left half at dLeft, right at dRight
+};
+
+struct RenderedScene {
+    GrayImage left;
+    GrayImage right;
+    DisparityMap groundTruth;             // invalid where occluded or out of the right view
+    std::vector<std::uint8_t> occlusion;  // 1 where a nearer surface hides the pixel
+};
+
+// Throws InvalidPlane when a region's plane leaves [0, maxDisparity) inside it.
+RenderedScene renderScene(const PlanarScene& scene);
 
 // ------------------------------------------------------------------ extensions
 // GPU selection for the calling thread's default context (device 0 otherwise).

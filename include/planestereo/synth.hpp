@@ -1,4 +1,4 @@
-// synth.hpp — drop-in name for the reference header proj/include/planestereo/synth.hpp;
-// of it this build provides wtaOracle (GPU), declared in planestereo.hpp.
+// synth.hpp — drop-in name for the reference header proj/include/planestereo/synth.hpp
+// (PlanarScene, renderScene, wtaOracle; all on the GPU), declared in planestereo.hpp.
 #pragma once
 #include "planestereo/planestereo.hpp"

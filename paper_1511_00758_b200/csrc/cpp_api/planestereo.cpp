@@ -6,6 +6,7 @@
 // kernels.  Scalar geometry helpers (orient2d, inCircleSign, fitPlane) are
 // evaluated inline with the reference's exact arithmetic (delaunay.cpp:11-41,
 // mesh.cpp:12-26); DisparityMesh's planes and lookup come from the device.
+#include <algorithm>
 #include <cstdlib>
 #include <ostream>
 #include <string>
@@ -348,6 +349,90 @@ std::pair<DisparityMap, CostMap> wtaOracle(const GrayImage& left, const GrayImag
                         disparity.mutableValues().data(), disparity.mutableValidity().data(),
                         costs.mutableValues().data()));
     return {std::move(disparity), std::move(costs)};
+}
+
+namespace {
+AccuracyReport accuracy_impl(const DisparityMap& prediction, const DisparityMap& groundTruth,
+                             const GradientMask* mask, const std::vector<double>& thresholds) {
+    const int w = prediction.width(), h = prediction.height();
+    if (groundTruth.width() != w || groundTruth.height() != h ||
+        (mask && (mask->width() != w || mask->height() != h)))
+        throw DimensionMismatch("accuracy inputs differ in size");
+    AccuracyReport r;
+    r.thresholds = thresholds;
+    r.fractions.assign(thresholds.size(), 0.0);
+    long long evaluated = 0;
+    double mae = 0.0;
+    // the device kernel takes up to 16 thresholds per call; counts and the
+    // error sum do not depend on them
+    std::size_t k0 = 0;
+    do {
+        const int k = int(std::min<std::size_t>(16, thresholds.size() - k0));
+        check(ps_accuracy(ctx(), 1, prediction.values().data(), prediction.validity().data(),
+                          groundTruth.values().data(), groundTruth.validity().data(),
+                          mask ? mask->membership().data() : nullptr, w, h,
+                          k ? thresholds.data() + k0 : nullptr, k,
+                          k ? r.fractions.data() + k0 : nullptr, &evaluated, &mae));
+        k0 += std::size_t(k);
+    } while (k0 < thresholds.size());
+    r.evaluated = long(evaluated);
+    r.meanAbsError = mae;
+    return r;
+}
+}  // namespace
+
+AccuracyReport accuracy(const DisparityMap& prediction, const DisparityMap& groundTruth,
+                        const GradientMask& mask, const std::vector<double>& thresholds) {
+    return accuracy_impl(prediction, groundTruth, &mask, thresholds);
+}
+
+AccuracyReport accuracy(const DisparityMap& prediction, const DisparityMap& groundTruth,
+                        const std::vector<double>& thresholds) {
+    return accuracy_impl(prediction, groundTruth, nullptr, thresholds);
+}
+
+PlanarScene PlanarScene::flat(double d, int width, int height, std::uint32_t seed) {
+    return slanted(0.0, 0.0, d, width, height, seed);
+}
+
+PlanarScene PlanarScene::slanted(double a, double b, double c, int width, int height,
+                                 std::uint32_t seed) {
+    PlanarScene s;
+    s.width = width;
+    s.height = height;
+    s.seed = seed;
+    s.regions.push_back({0, 0, width, height, {a, b, c}});
+    return s;
+}
+
+PlanarScene PlanarScene::steps(double dLeft, double dRight, int width, int height,
+                               std::uint32_t seed) {
+    PlanarScene s;
+    s.width = width;
+    s.height = height;
+    s.seed = seed;
+    const int mid = width / 2;
+    s.regions.push_back({0, 0, mid, height, {0.0, 0.0, dLeft}});
+    s.regions.push_back({mid, 0, width, height, {0.0, 0.0, dRight}});
+    return s;
+}
+
+RenderedScene renderScene(const PlanarScene& scene) {
+    const int w = scene.width, h = scene.height;
+    std::vector<ps_scene_region> regs;
+    regs.reserve(scene.regions.size());
+    for (const SceneRegion& r : scene.regions)
+        regs.push_back({r.u0, r.v0, r.u1, r.v1, r.plane.a, r.plane.b, r.plane.c});
+    const std::size_t P = std::size_t(std::max(w, 0)) * std::size_t(std::max(h, 0));
+    std::vector<std::uint8_t> left(P), right(P), gtv(P), occ(P);
+    std::vector<float> gt(P);
+    check(ps_render_scene(ctx(), w, h, scene.maxDisparity, scene.seed, regs.data(), int(regs.size()),
+                          left.data(), right.data(), gt.data(), gtv.data(), occ.data()));
+    RenderedScene out{GrayImage(w, h, std::move(left)), GrayImage(w, h, std::move(right)),
+                      DisparityMap(w, h), std::move(occ)};
+    out.groundTruth.mutableValues() = std::move(gt);
+    out.groundTruth.mutableValidity() = std::move(gtv);
+    return out;
 }
 
 RefinementGrids disparityRefinement(const DisparityMap& interpolated, const CostMap& costs,
