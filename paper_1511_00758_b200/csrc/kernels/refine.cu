@@ -214,6 +214,8 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
         : "memory");
 }
 
+constexpr unsigned kSuspendNs = 20000;  // try_wait suspend-time hint (no spinning on issue slots)
+
 __device__ __forceinline__ void bar_wait(unsigned long long* bar, unsigned phase) {
     // try_wait with a suspend-time hint: the warp sleeps until the phase
     // completes instead of spinning on the issue slots
@@ -221,9 +223,9 @@ __device__ __forceinline__ void bar_wait(unsigned long long* bar, unsigned phase
         "{\n"
         ".reg .pred P1;\n"
         "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
         "@!P1 bra WAIT_%=;\n"
-        "}\n" :: "r"(smem_u32(bar)), "r"(phase) : "memory");
+        "}\n" :: "r"(smem_u32(bar)), "r"(phase), "r"(kSuspendNs) : "memory");
 }
 
 struct BulkGeom {
@@ -235,7 +237,7 @@ struct BulkGeom {
     int r_tile;       // kTile % W
 };
 
-template <bool LAST, int SEG>
+template <bool LAST, int SEG, bool WRAP>
 __global__ void __launch_bounds__(256, 4) k_refine_bulk(RefineArgs a, CostTables tab,
                                                         unsigned magic_cell31, unsigned magic_w,
                                                         BulkGeom bg) {
@@ -329,7 +331,8 @@ __global__ void __launch_bounds__(256, 4) k_refine_bulk(RefineArgs a, CostTables
             // order (first minimum wins) and each (cell, lane) segment issues
             // one fire-and-forget atomicMin (RED) per grid.
             const int p0 = warp * kWarpPx + 4 * lane;
-            const bool in = p0 < n_in;  // n_in % 16 == 0: all four or none
+            // n_in % 16 == 0: a lane's four pixels are all in the tile or none
+            if (p0 < n_in) {
             const float4 d4 = *reinterpret_cast<const float4*>(sm_dit + p0);
             const uint4 cl4 = *reinterpret_cast<const uint4*>(sm_cl + p0);
             const unsigned code4 = *reinterpret_cast<const unsigned*>(sm_code + p0);
@@ -353,7 +356,7 @@ __global__ void __launch_bounds__(256, 4) k_refine_bulk(RefineArgs a, CostTables
                             rem = 0;
                             ++ccol;
                         }
-                        if (u == W) {  // at most one row wrap in four pixels
+                        if (WRAP && u == W) {  // W % 4 != 0 only: at most one row wrap
                             u = 0;
                             ++v;
                             ccol = 0;
@@ -366,7 +369,8 @@ __global__ void __launch_bounds__(256, 4) k_refine_bulk(RefineArgs a, CostTables
                     const unsigned c0 = (code4 >> (8 * j)) & 0xffu;
                     const float d = dd[j];
                     const int dr = lround_away(d);
-                    const bool ok = in && c0 != kCodeOff && d == d && dr >= 0 && u - dr >= 2;
+                    // D_it is NaN or in [0, ND) (raster), so dr >= 0 for a number
+                    const bool ok = c0 != kCodeOff && d == d && u - dr >= 2;
                     crv[j] = ok ? sm_cr[p0 + j - dr] : 0u;  // same-row cR(u - dr), staged
                     okm |= unsigned(ok) << j;
                 }
@@ -385,7 +389,7 @@ __global__ void __launch_bounds__(256, 4) k_refine_bulk(RefineArgs a, CostTables
             for (int j = 0; j < 4; ++j) {
                 const int p = p0 + j;
                 const unsigned c0 = (code4 >> (8 * j)) & 0xffu;
-                const bool m = in && c0 != kCodeOff;
+                const bool m = c0 != kCodeOff;
                 const float d = dd[j];
                 const int k = ((okm >> j) & 1u) ? __popc(cl[j] ^ crv[j]) : kCensusBits;
                 const bool upd = m && unsigned(k) < c0;  // cost[k] < C_f (pipeline.cpp:68-71)
@@ -401,8 +405,8 @@ __global__ void __launch_bounds__(256, 4) k_refine_bulk(RefineArgs a, CostTables
                     cfo[j] = s_cout[cc];
                     dvo |= unsigned(cc < code_high) << (8 * j);
                 }
-                tsum += in ? s_fix[cc] : 0ull;  // C_f * 2^36 (exact, see trace_fixed_exact)
-                tvalid += (in && cc < code_high) ? 1u : 0u;
+                tsum += s_fix[cc];  // C_f * 2^36 (exact, see trace_fixed_exact)
+                tvalid += cc < code_high ? 1u : 0u;
                 // the grids feed only supportResampling, which the last
                 // iteration does not run (pipeline.cpp:168-171): skipped there
                 const bool qg = !LAST && m && ((tab.low_mask >> k) & 1u);
@@ -430,7 +434,7 @@ __global__ void __launch_bounds__(256, 4) k_refine_bulk(RefineArgs a, CostTables
                     }
                 }
             }
-            if (in) {
+            {
                 if constexpr (LAST) {
                 } else if constexpr (SEG == 2) {
                     // at most one cell boundary inside the four pixels (host-
@@ -465,6 +469,7 @@ __global__ void __launch_bounds__(256, 4) k_refine_bulk(RefineArgs a, CostTables
                     *reinterpret_cast<unsigned*>(a.Dv + tb + p0) = dvo;
                 }
             }
+            }  // p0 < n_in
         }
         // release stage s: the last of the 8 warps to finish it refills it
         // (no CTA-wide barrier, so fast warps run ahead into the next stages)
@@ -547,7 +552,7 @@ __global__ void k_fill_f32(float* __restrict__ p, long long n, float x) {
 namespace {
 // Persistent bulk-copy launch: as many CTAs per SM as registers and shared
 // memory allow (queried once per instantiation).
-template <bool LAST, int SEG>
+template <bool LAST, int SEG, bool WRAP>
 int launch_bulk(const RefineArgs& a0, const CostTables& tab, unsigned magic_cell31, unsigned magic_w,
                 cudaStream_t st) {
     static int sms = 0;
@@ -564,13 +569,13 @@ int launch_bulk(const RefineArgs& a0, const CostTables& tab, unsigned magic_cell
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(k_refine_bulk<LAST, SEG>,
+        cudaFuncSetAttribute(k_refine_bulk<LAST, SEG, WRAP>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(size_t(kStages) * (9 * kTile + 4 * (kTile + kMaxHalo))));
     }
     int& occ = per_sm[bg.halo / 4];
     if (occ == 0) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_refine_bulk<LAST, SEG>, 256, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_refine_bulk<LAST, SEG, WRAP>, 256, smem);
         occ = std::max(1, occ);
     }
     // the kernel indexes the batch with 32-bit pixel offsets: launch per
@@ -599,7 +604,7 @@ int launch_bulk(const RefineArgs& a0, const CostTables& tab, unsigned magic_cell
         }
         bg.total_tiles = bg.tiles_per_frame * a.frames;
         const unsigned blocks = unsigned(std::min<long long>(bg.total_tiles, (long long)occ * sms));
-        k_refine_bulk<LAST, SEG><<<blocks, 256, smem, st>>>(a, tab, magic_cell31, magic_w, bg);
+        k_refine_bulk<LAST, SEG, WRAP><<<blocks, 256, smem, st>>>(a, tab, magic_cell31, magic_w, bg);
         ++launches;
     }
     return launches;
@@ -620,11 +625,20 @@ int launch_refine(const RefineArgs& a, const CostTables& tab, bool last, cudaStr
         const unsigned magic_cell = unsigned((0x80000000ull + a.cell - 1) / a.cell);  // 2^31 / cell
         // at most one cell boundary in any four consecutive pixels
         const int tail = a.g.width % a.cell;
-        if (a.cell >= 3 && (tail == 0 || tail >= 3))
-            return last ? launch_bulk<true, 2>(a, tab, magic_cell, magic_w, st)
-                        : launch_bulk<false, 2>(a, tab, magic_cell, magic_w, st);
-        return last ? launch_bulk<true, 1>(a, tab, magic_cell, magic_w, st)
-                    : launch_bulk<false, 1>(a, tab, magic_cell, magic_w, st);
+        const bool seg2 = a.cell >= 3 && (tail == 0 || tail >= 3);
+        // a lane's four pixels cross a row end only when W % 4 != 0
+        if (a.g.width % 4 == 0) {
+            if (seg2)
+                return last ? launch_bulk<true, 2, false>(a, tab, magic_cell, magic_w, st)
+                            : launch_bulk<false, 2, false>(a, tab, magic_cell, magic_w, st);
+            return last ? launch_bulk<true, 1, false>(a, tab, magic_cell, magic_w, st)
+                        : launch_bulk<false, 1, false>(a, tab, magic_cell, magic_w, st);
+        }
+        if (seg2)
+            return last ? launch_bulk<true, 2, true>(a, tab, magic_cell, magic_w, st)
+                        : launch_bulk<false, 2, true>(a, tab, magic_cell, magic_w, st);
+        return last ? launch_bulk<true, 1, true>(a, tab, magic_cell, magic_w, st)
+                    : launch_bulk<false, 1, true>(a, tab, magic_cell, magic_w, st);
     }
     if (last) {
         if (key32) k_refine<true, true><<<grid, 256, 0, st>>>(a, tab, inv_cell, inv_w);
