@@ -61,6 +61,58 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+class NvmlClockSampler:
+    """SM clocks and clock-event (throttle) reasons sampled every 200 ms during the
+    timed region, in process through NVML: the nvidia-smi polling process it
+    replaces competed for the host cores the Delaunay workers run on."""
+
+    BITS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+            "sw_power_cap": 0x4}
+
+    def __init__(self, gpu: int):
+        import pynvml
+        self.nv = pynvml
+        pynvml.nvmlInit()
+        self.h = pynvml.nvmlDeviceGetHandleByIndex(gpu)
+        self.samples = []
+        self.stop_ev = threading.Event()
+
+    def start(self):
+        self.thread = threading.Thread(target=self._run, daemon=True)
+        self.thread.start()
+
+    def _run(self):
+        nv = self.nv
+        while not self.stop_ev.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                smax = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((sm, smax, rs))
+            except Exception:
+                pass
+            self.stop_ev.wait(0.2)
+
+    def stop(self):
+        self.stop_ev.set()
+        self.thread.join(timeout=5)
+        sm = [x[0] for x in self.samples]
+        reasons = sorted({n for _, _, r in self.samples for n, b in self.BITS.items() if r & b})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(x[1] for x in self.samples) if sm else None,
+                "reasons": reasons, "samples": len(sm), "via": "nvml"}
+
+
+def clock_sampler(gpu: int):
+    """NVML in process when available (PS_CLOCKS=smi forces the nvidia-smi poller)."""
+    if os.environ.get("PS_CLOCKS") != "smi":
+        try:
+            return NvmlClockSampler(gpu)
+        except Exception:
+            pass
+    return ClockSampler(gpu)
+
+
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
 
@@ -241,7 +293,7 @@ def run_ours(args, rank, world, local_rank):
         st = ctx.run_resident(cfg, unchecked_cell=True)
         if st not in (0, 7):
             raise RuntimeError(f"pipeline failed: {lib.ps_last_error(None)}")
-    sampler = ClockSampler(local_rank)
+    sampler = clock_sampler(local_rank)
     barrier()
     torch.cuda.synchronize()
     l0 = ctx.launch_count()
