@@ -46,6 +46,9 @@ def parse_args():
     p.add_argument("--frames", type=int, default=0, help="frames per GPU (default: the config's)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-frames", type=int, default=128)
+    p.add_argument("--ref-all", action="store_true",
+                   help="with --configs: also time the reference throughput leg of cfg4 "
+                        "(one frame per host thread, ~20 min)")
     p.add_argument("--configs", default="",
                    help="comma list of BASELINE configs: print a markdown table of ours (ps_run_batch, "
                         "pinned buffers, wall clock) vs the reference CPU arm instead of the JSON line")
@@ -499,14 +502,15 @@ def run_configs_table(args):
             ctx.run(L[0], R[0], cfg, unchecked_cell=True)
             lat.append((time.perf_counter() - t0) * 1e3)
         rfps = rlat = None
-        if ref is not None and CONFIG_REF[k]:
+        if ref is not None and (CONFIG_REF[k] or args.ref_all):
             m = min(n, threads)
             t0 = time.perf_counter()
             ref.run_batch(L[:m], R[:m], cfg, threads)
             rfps = m / (time.perf_counter() - t0)
-            t0 = time.perf_counter()
-            ref.run(L[0], R[0], cfg)
-            rlat = (time.perf_counter() - t0) * 1e3
+            if CONFIG_REF[k]:  # cfg4: one frame alone would take another ~18 min
+                t0 = time.perf_counter()
+                ref.run(L[0], R[0], cfg)
+                rlat = (time.perf_counter() - t0) * 1e3
         failed = int((np.asarray(res["status"]) != 0).sum())
         print(f"| cfg{k} | {w}x{h}, ND {c['max_disparity']}, grid {c['cell']} | {c['iterations']} | {n}"
               f"{' (' + str(failed) + ' failed)' if failed else ''} | {ours:.1f} | {ours * w * h / 1e6:.1f} "
