@@ -190,7 +190,8 @@ def test_run_batch_multi_equals_single_context(ctx):
            [[t.meanCost for t in tr] for tr in one["trace"]]
 
 
-@pytest.mark.parametrize("w,h", [(16, 16), (17, 19), (37, 23), (64, 16), (255, 17)])
+@pytest.mark.parametrize("w,h", [(16, 16), (17, 19), (37, 23), (64, 16), (255, 17),
+                                 (50, 48), (99, 64), (126, 96)])
 def test_small_and_odd_sizes(ctx, orc, w, h):
     rng = np.random.default_rng(w * 100 + h)
     L = rng.integers(0, 256, (h, w), dtype=np.uint8)
@@ -202,6 +203,20 @@ def test_small_and_odd_sizes(ctx, orc, w, h):
             ctx.run(L, R, cfg)
         return
     assert_frame_parity(result_dict(ctx.run(L, R, cfg)), want)
+
+
+@pytest.mark.parametrize("w,h,cell", [(254, 96, 5), (322, 120, 10), (333, 144, 2)])
+def test_bulk_refine_row_wrap(ctx, orc, w, h, cell):
+    """K7's bulk path when a lane's four pixels can cross a row end (W % 4 != 0,
+    P % 16 == 0): the row-wrap variant of k_refine_bulk."""
+    assert (w * h) % 16 == 0 and w % 4 != 0
+    L, R = ps.synth_pair(w, h, 6, 32, False, 2.0, seed=w + h)
+    cfg = ps.PipelineConfig(iterations=3, maxDisparity=32, occupancyCellSize=cell)
+    want = orc.run(L, R, cfg)
+    assert want["status"] == 0
+    r = ctx.run(L, R, cfg, unchecked_cell=True)
+    assert_frame_parity(result_dict(r), want)
+    assert [t.meanCost for t in r.trace] == [t["meanCost"] for t in want["trace"]]
 
 
 def test_random_configs_match_oracle(ctx, orc):
