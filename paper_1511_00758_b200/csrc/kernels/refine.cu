@@ -348,9 +348,14 @@ __global__ void __launch_bounds__(256, 4) k_refine_bulk(RefineArgs a, CostTables
                 int ccol = mdiv31(u, magic_cell31);
                 int rem = u - ccol * cellsz;
                 int crow = mdiv31(v, magic_cell31) * cols;
+                // SEG == 2 without row wraps: the cell steps by one at the
+                // first pixel with rem + j == cellsz (cells >= 3 px wide)
+                const int nb = cellsz - rem;
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    if (j > 0) {
+                    if (SEG == 2 && !WRAP) {
+                        u += j > 0 ? 1 : 0;
+                    } else if (j > 0) {
                         ++u;
                         if (++rem == cellsz) {
                             rem = 0;
@@ -365,11 +370,13 @@ __global__ void __launch_bounds__(256, 4) k_refine_bulk(RefineArgs a, CostTables
                         }
                     }
                     uc[j] = u;
-                    cellv[j] = crow + ccol;
+                    cellv[j] = crow + ccol + ((SEG == 2 && !WRAP && j >= nb) ? 1 : 0);
                     const unsigned c0 = (code4 >> (8 * j)) & 0xffu;
                     const float d = dd[j];
-                    const int dr = lround_away(d);
-                    // D_it is NaN or in [0, ND) (raster), so dr >= 0 for a number
+                    // lround (half away from zero) for d >= 0: trunc of d + 0.5
+                    // rounded toward zero is exact there; D_it is NaN or in
+                    // [0, ND) (raster), and a NaN (-> 0) is rejected below
+                    const int dr = __float2int_rz(__fadd_rz(d, 0.5f));
                     const bool ok = c0 != kCodeOff && d == d && u - dr >= 2;
                     crv[j] = ok ? sm_cr[p0 + j - dr] : 0u;  // same-row cR(u - dr), staged
                     okm |= unsigned(ok) << j;
