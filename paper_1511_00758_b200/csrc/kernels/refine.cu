@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(256, 4) k_refine_bulk(RefineArgs a, CostTables
             const uint32_t cl[4] = {cl4.x, cl4.y, cl4.z, cl4.w};
             const int r = r0 + p0;
             const int dv = int(__umulhi(unsigned(r), magic_w));  // W >= 32
-            int uc[4], cellv[4];
+            int cellv[4];
             uint32_t crv[4];
             unsigned okm = 0;
             {
@@ -369,7 +369,6 @@ __global__ void __launch_bounds__(256, 4) k_refine_bulk(RefineArgs a, CostTables
                             crow = mdiv31(v, magic_cell31) * cols;
                         }
                     }
-                    uc[j] = u;
                     cellv[j] = crow + ccol + ((SEG == 2 && !WRAP && j >= nb) ? 1 : 0);
                     const unsigned c0 = (code4 >> (8 * j)) & 0xffu;
                     const float d = dd[j];
@@ -382,7 +381,6 @@ __global__ void __launch_bounds__(256, 4) k_refine_bulk(RefineArgs a, CostTables
                     okm |= unsigned(ok) << j;
                 }
             }
-            (void)uc;
             int seg = -1;
             unsigned gk = 32, gi = 0, bk = 32, bi = 0;  // best (k, idx) of the segment per grid
             auto seg_flush = [&]() {
