@@ -304,6 +304,7 @@ __global__ void __launch_bounds__(kThreads) k_raster(
         }
     }
     // Large triangles: the whole warp, 32 rows at a time.
+    __shared__ int s_bpre[kThreads], s_blo[kThreads];
     unsigned bigs = __ballot_sync(0xffffffffu, big);
     while (bigs) {
         const int src = __ffs(bigs) - 1;
@@ -322,20 +323,34 @@ __global__ void __launch_bounds__(kThreads) k_raster(
         const double bb = __shfl_sync(0xffffffffu, pb, src);
         const double bc = __shfl_sync(0xffffffffu, pc, src);
         const long long fb = bf * g.pixels;
+        // 32 rows at a time, one per lane; then the pixels of those 32 spans
+        // are dealt 32 at a time (span by binary search of the prefix sums),
+        // so a long sliver (1-2 px per row) costs ~rows/32 steps, not ~rows
         for (int r0 = b0; r0 <= b1; r0 += 32) {
             const int v = r0 + lane;
             Int lo = 0, hi = -1;
             const bool ok = v <= b1 && row_span<Int>(bx, by, v, W, lo, hi);
-            unsigned rows = __ballot_sync(0xffffffffu, ok);
-            const int lo32 = int(lo), hi32 = int(hi);
-            while (rows) {
-                const int r = __ffs(rows) - 1;
-                rows &= rows - 1;
-                const int l = __shfl_sync(0xffffffffu, lo32, r);
-                const int h = __shfl_sync(0xffffffffu, hi32, r);
-                const long long rowb = (long long)(r0 + r) * W;
-                for (int u = l + lane; u <= h; u += 32) put(out, fb, rowb + u, bt, ba, bb, bc, u, r0 + r);
+            const int len = ok ? int(hi - lo) + 1 : 0;
+            int incl = len;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y2 = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y2;
             }
+            const int total_px = __shfl_sync(0xffffffffu, incl, 31);
+            s_bpre[threadIdx.x] = incl - len;
+            s_blo[threadIdx.x] = int(lo);
+            __syncwarp();
+            const int wb = threadIdx.x & ~31;
+            for (int j = lane; j < total_px; j += 32) {
+                int sp = 0;  // the last row whose pixel prefix is <= j
+#pragma unroll
+                for (int step = 16; step; step >>= 1)
+                    if (s_bpre[wb + sp + step] <= j) sp += step;
+                const int u = s_blo[wb + sp] + (j - s_bpre[wb + sp]);
+                put(out, fb, (long long)(r0 + sp) * W + u, bt, ba, bb, bc, u, r0 + sp);
+            }
+            __syncwarp();
         }
     }
 }
