@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(kThreads) k_raster(
         const int xmin = min(x[0], min(x[1], x[2])), xmax = max(x[0], max(x[1], x[2]));
         // warp-cooperative only when the bounding box is large (many pixels
         // or many rows); slivers and small triangles stay on their thread
-        big = warp_per_tri || (long long)(vmax - vmin + 1) * (xmax - xmin + 1) > 192 || (vmax - vmin) >= 32;
+        big = warp_per_tri || (long long)(vmax - vmin + 1) * (xmax - xmin + 1) > 512 || (vmax - vmin) >= 64;
         small = !big && vmin <= vmax;
     }
     // Small triangles, flattened twice so that every lane stays busy: the
