@@ -117,8 +117,8 @@ ps_status ps_run_batch(ps_ctx* ctx, int n_frames, const uint8_t* left, const uin
                        uint8_t* dense_valid, ps_iter_stats* trace, int* frame_status);
 
 /* The same batch sharded over n_ctx contexts — one per GPU of the box
- * — from one process: contiguous blocks of
- * ceil(n_frames / n_ctx) frames, each block run by ps_run_batch on its
+ * — from one process: an even split into contiguous blocks
+ * (sizes differ by at most one frame), each block run by ps_run_batch on its
  * context from its own host thread.  Frames never interact, so no collective
  * is involved.  Same arguments and per-frame outputs as ps_run_batch;
  * returns the first context-level error (in context order), else the first

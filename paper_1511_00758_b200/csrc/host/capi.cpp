@@ -173,12 +173,13 @@ ps_status ps_run_batch_multi(ps_ctx* const* ctxs, int n_ctx, int n_frames, const
     if (s != PS_OK) return s;
     if (n_frames < 1) return set_error(PS_ERROR, "batch needs at least one frame");
     const long long P = (long long)width * height;
-    const int per = (n_frames + n_ctx - 1) / n_ctx;
     std::vector<ps_status> st(n_ctx, PS_OK);
     std::vector<std::string> msg(n_ctx);
     std::vector<std::thread> th;
     for (int i = 0; i < n_ctx; ++i) {
-        const int f0 = std::min(n_frames, i * per), n = std::min(n_frames, f0 + per) - f0;
+        // even contiguous split: block sizes differ by at most one frame
+        const int f0 = int((long long)n_frames * i / n_ctx);
+        const int n = int((long long)n_frames * (i + 1) / n_ctx) - f0;
         if (n <= 0) continue;
         th.emplace_back([&, i, f0, n] {
             const size_t px = size_t(f0) * size_t(P);

@@ -185,7 +185,8 @@ Engine::~Engine() {
                       &dDense_, &dDenseV_, &dLookup_, &dSu_, &dSv_, &dSd_, &dS_, &dSnext_,
                       &dTaken_, &dCg_, &dCb_, &dBinKeys_, &dBinCount_, &dScratch_, &dCandU_,
                       &dCandV_, &dCandCount_, &dOk_, &dDisp_, &dRemU_, &dRemV_, &dRemCount_,
-                      &dConf_, &dChunk_, &dTraceSum_, &dTraceValid_, &dErr_, &s_a, &s_b, &s_c,
+                      &dConf_, &dChunk_, &dTraceSum_, &dTraceValid_, &dErr_, &dOkSeed_, &dDispSeed_,
+                      &dFrameOk_, &s_a, &s_b, &s_c,
                       &s_d, &s_e, &s_f, &s_g, &s_h, &s_i, &s_j};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
@@ -407,8 +408,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     }
     scap_ = int(std::min<long long>(P, bound));
     const int cand_stride = 120 * cfg.per_bin_cap;
-    const int mstride = std::max(cand_stride, cells_max);
-    const int chunks = ceil_div(mstride, 1024);
+    const int chunks = ceil_div(std::max(cand_stride, cells_max), 1024);
     const long long words = (P + 31) / 32;
     int n_pow2 = 1;
     while (n_pow2 < std::min<long long>(cand_stride, P)) n_pow2 <<= 1;
@@ -441,8 +441,12 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     int* dCandU = dev<int>(dCandU_, size_t(F) * cand_stride);
     int* dCandV = dev<int>(dCandV_, size_t(F) * cand_stride);
     int* dCandCount = dev<int>(dCandCount_, F);
-    uint8_t* dOk = dev<uint8_t>(dOk_, size_t(F) * mstride);
-    int* dDisp = dev<int>(dDisp_, size_t(F) * mstride);
+    // match scratch: seeding and resampling use disjoint buffers (frame groups
+    // seed on seed_st_ while earlier groups resample on their own streams)
+    uint8_t* dOk = dev<uint8_t>(dOk_, size_t(F) * cells_max);
+    int* dDisp = dev<int>(dDisp_, size_t(F) * cells_max);
+    uint8_t* dOkSeed = dev<uint8_t>(dOkSeed_, size_t(F) * cand_stride);
+    int* dDispSeed = dev<int>(dDispSeed_, size_t(F) * cand_stride);
     int* dRemU = dev<int>(dRemU_, size_t(F) * cells_max);
     int* dRemV = dev<int>(dRemV_, size_t(F) * cells_max);
     int* dRemCount = dev<int>(dRemCount_, F);
@@ -457,7 +461,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     unsigned* hTraceValid = reinterpret_cast<unsigned*>(host<uint8_t>(hTraceValid_, size_t(F) * iters * 4));
     const void* must[] = {dMask, dMaskCount, dCL, dCR, dDf, dDv, dCf, dCode, dDense, dDenseV, dDit,
                           dSu, dSv, dSd, dS, dSnext, dTaken, dCg, dCb, dBinKeys, dBinCount,
-                          dScratch, dCandU, dCandV, dCandCount, dOk, dDisp, dRemU, dRemV,
+                          dScratch, dCandU, dCandV, dCandCount, dOk, dDisp, dOkSeed, dDispSeed, dRemU, dRemV,
                           dRemCount, dConf, dTraceSum, dTraceValid, dErr, hS, hMaskCount,
                           hTraceSum, hTraceValid};
     for (const void* p : must)
@@ -568,8 +572,8 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                                        cv, nullptr, dCandCount + f0, cand_stride, gs);
         end_kernel(gs);
         // K3 seed match (sparse.cpp:148-195) + ordered compaction
-        uint8_t* ok = dOk + size_t(f0) * cand_stride;
-        int* disp = dDisp + size_t(f0) * cand_stride;
+        uint8_t* ok = dOkSeed + size_t(f0) * cand_stride;
+        int* disp = dDispSeed + size_t(f0) * cand_stride;
         begin_kernel("match_seed", 0.0, gs);
         launches_ += launch_match(dCL + fp, dCR + fp, g, n, cfg.max_disparity, tab, cu, cv,
                                   dCandCount + f0, cand_stride, cand_stride, ok, disp, nullptr, gs);
@@ -603,13 +607,11 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     if (s != PS_OK) return s;
     int next_seed = 1;
     bool chained = false;  // chain_event_ recorded in this run
-    std::mutex done_m;
-    std::condition_variable done_cv;
     // Before an early return: wait for this run's own host tasks (they hold
     // references to this frame); the pool is shared with other contexts.
     auto drain = [&] {
-        std::unique_lock<std::mutex> lk(done_m);
-        done_cv.wait(lk, [&] {
+        std::unique_lock<std::mutex> lk(done_m_);
+        done_cv_.wait(lk, [&] {
             for (int gi = 0; gi < G; ++gi)
                 if (groups_[gi].pending.load() != 0) return false;
             return true;
@@ -733,10 +735,11 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                 for (double cur = first_task.load(); t0 < cur && !first_task.compare_exchange_weak(cur, t0);) {}
                 for (double cur = last_task.load(); t1 > cur && !last_task.compare_exchange_weak(cur, t1);) {}
                 worker_end[worker] = t1;
-                if (g2.pending.fetch_sub(1) == 1) {
-                    std::lock_guard<std::mutex> lk(done_m);
-                    done_cv.notify_all();
-                }
+                // decrement and notify under the engine's lock: once the
+                // counter reads 0 the run may return, and this task touches
+                // nothing of it after the (engine-owned) mutex is released
+                std::lock_guard<std::mutex> lk(done_m_);
+                if (g2.pending.fetch_sub(1) == 1) done_cv_.notify_all();
             });
         }
     };
@@ -862,8 +865,8 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                                                  dRemV + size_t(f0) * cells_max, cells_max,
                                                  dRemCount + f0, chunk, gs);
             end_kernel(gs);
-            uint8_t* ok = dOk + size_t(f0) * mstride;
-            int* disp = dDisp + size_t(f0) * mstride;
+            uint8_t* ok = dOk + size_t(f0) * cells_max;
+            int* disp = dDisp + size_t(f0) * cells_max;
             begin_kernel("match_resample", 0.0, gs);
             launches_ += launch_match(dCL + fp, dCR + fp, g, n, cfg.max_disparity, tab,
                                       dRemU + size_t(f0) * cells_max, dRemV + size_t(f0) * cells_max,
@@ -988,8 +991,8 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         }
         if (!progress) {
             // wait for a Delaunay completion, or poll the device again shortly
-            std::unique_lock<std::mutex> lk(done_m);
-            done_cv.wait_for(lk, std::chrono::microseconds(200));
+            std::unique_lock<std::mutex> lk(done_m_);
+            done_cv_.wait_for(lk, std::chrono::microseconds(200));
         }
     }
     host_dt_ms = dt_ms_sum.load() / std::max(1, pool_->size());
@@ -1082,10 +1085,14 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     have_outputs_ = true;
     streamed_ = sink_.active;
     done_sink_ = sink_;
-    for (int f = 0; f < F; ++f)
+    for (int f = 0; f < F; ++f) {
+        if (status_[f] == PS_SEEDING_FAILED)
+            return fail(PS_SEEDING_FAILED, "only " + std::to_string(hS[f]) +
+                                               " seed matches survived; need at least 3");
         if (status_[f] != PS_OK)
-            return fail(ps_status(status_[f]), "only " + std::to_string(hS[f]) +
-                                                   " seed matches survived; need at least 3");
+            return fail(ps_status(status_[f]), "frame " + std::to_string(f) +
+                                                   ": triangulation failed (coordinates or capacity)");
+    }
     return PS_OK;
 }
 

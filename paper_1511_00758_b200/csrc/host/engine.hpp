@@ -10,7 +10,9 @@
 #pragma once
 
 #include <atomic>
+#include <condition_variable>
 #include <cstdint>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -171,6 +173,11 @@ private:
     int pending_stat_ = -1;
     cudaEvent_t pending_start_ = nullptr;
     FrameGroup groups_[kMaxGroups];
+    // Completion signal of the host Delaunay tasks.  Engine-owned (not a local
+    // of run_resident) so that a task finishing as the run returns never
+    // touches a destroyed mutex; tasks decrement their counter under it.
+    std::mutex done_m_;
+    std::condition_variable done_cv_;
 
     // batch shape
     int F_ = 0, W_ = 0, H_ = 0;
@@ -194,7 +201,7 @@ private:
     // device buffers (frame-strided)
     DevBuf dL_, dR_, dMask_, dMaskCount_, dCL_, dCR_, dDf_, dDv_, dCf_, dCode_, dDense_, dDenseV_,
         dLookup_, dSu_, dSv_, dSd_, dS_, dSnext_, dTaken_, dCg_, dCb_, dBinKeys_, dBinCount_,
-        dScratch_, dCandU_, dCandV_, dCandCount_, dOk_, dDisp_, dRemU_, dRemV_, dRemCount_,
+        dScratch_, dCandU_, dCandV_, dCandCount_, dOk_, dDisp_, dOkSeed_, dDispSeed_, dRemU_, dRemV_, dRemCount_,
         dConf_, dChunk_, dTraceSum_, dTraceValid_, dErr_;
     // pinned host staging
     HostBuf hS_, hTraceSum_, hTraceValid_, hMaskCount_;

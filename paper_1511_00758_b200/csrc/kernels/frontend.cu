@@ -414,12 +414,10 @@ int launch_candidates(const uint8_t* left, FrameGeom g, int frames, int corner_t
     dim3 grid(120, frames);
     // bin tile + ring halo (bins are at most ceil(n/nb) + 1 wide, bin_range)
     const size_t tile = size_t((g.width + 11) / 12 + 1 + 6) * size_t((g.height + 9) / 10 + 1 + 6);
-    static size_t configured[3] = {0, 0, 0};
-    auto allow = [&](const void* fn, int which, size_t static_bytes) {
-        if (tile + static_bytes > 48 * 1024 && tile > configured[which]) {
+    // per-device function attribute: set before every launch that needs it
+    auto allow = [&](const void* fn, int, size_t static_bytes) {
+        if (tile + static_bytes > 48 * 1024)
             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(tile));
-            configured[which] = tile;
-        }
     };
     if (cap <= 4) {
         allow((const void*)k_corner_bins<4>, 0, 256 * 4 * 8 + 264);

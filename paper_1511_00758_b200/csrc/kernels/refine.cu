@@ -27,6 +27,9 @@
 // Algorithmic traffic P + 29*M bytes per frame and iteration.
 #include <cuda_runtime.h>
 
+#include <map>
+#include <mutex>
+
 #include "launch.hpp"
 
 namespace ps {
@@ -560,8 +563,6 @@ namespace {
 template <bool LAST, int SEG, bool WRAP>
 int launch_bulk(const RefineArgs& a0, const CostTables& tab, unsigned magic_cell31, unsigned magic_w,
                 cudaStream_t st) {
-    static int sms = 0;
-    static int per_sm[kMaxHalo / 4 + 1] = {};
     BulkGeom bg{};
     const long long P = a0.g.pixels;
     bg.tiles_per_frame = int((P + kTile - 1) / kTile);
@@ -570,18 +571,28 @@ int launch_bulk(const RefineArgs& a0, const CostTables& tab, unsigned magic_cell
     bg.q_tile = kTile / a0.g.width;
     bg.r_tile = kTile % a0.g.width;
     const size_t smem = size_t(kStages) * bg.stage_bytes;
-    if (sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(k_refine_bulk<LAST, SEG, WRAP>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(size_t(kStages) * (9 * kTile + 4 * (kTile + kMaxHalo))));
-    }
-    int& occ = per_sm[bg.halo / 4];
-    if (occ == 0) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_refine_bulk<LAST, SEG, WRAP>, 256, smem);
-        occ = std::max(1, occ);
+    // The dynamic shared-memory opt-in is a per-device function attribute:
+    // set it on every launch (cheap), so each device of a multi-GPU process
+    // gets it.  SM count and occupancy are cached per device under a lock.
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaFuncSetAttribute(k_refine_bulk<LAST, SEG, WRAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(size_t(kStages) * (9 * kTile + 4 * (kTile + kMaxHalo))));
+    int sms = 0, occ = 0;
+    {
+        static std::mutex m;
+        static std::map<std::pair<int, int>, std::pair<int, int>> cache;  // (device, halo) -> (sms, occ)
+        std::lock_guard<std::mutex> lk(m);
+        auto it = cache.find({dev, bg.halo});
+        if (it == cache.end()) {
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_refine_bulk<LAST, SEG, WRAP>, 256, smem);
+            occ = std::max(1, occ);
+            cache[{dev, bg.halo}] = {sms, occ};
+        } else {
+            sms = it->second.first;
+            occ = it->second.second;
+        }
     }
     // the kernel indexes the batch with 32-bit pixel offsets: launch per
     // chunk of frames holding < 2^31 pixels

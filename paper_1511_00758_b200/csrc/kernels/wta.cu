@@ -70,11 +70,8 @@ int launch_wta(const uint32_t* cl, const uint32_t* cr, const uint8_t* mask, Fram
                float* cost, cudaStream_t st) {
     const int reach = std::min(max_disparity, g.width);
     const size_t smem = sizeof(uint32_t) * size_t(kWtaBlock + reach);
-    static int configured = 0;
-    if (smem > 48 * 1024 && smem > size_t(configured)) {
+    if (smem > 48 * 1024)  // per-device function attribute: set on every launch
         cudaFuncSetAttribute(k_wta, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        configured = int(smem);
-    }
     dim3 grid((g.width + kWtaBlock - 1) / kWtaBlock, g.height, frames);
     k_wta<<<grid, kWtaBlock, smem, st>>>(cl, cr, mask, g, max_disparity, tab, disparity, valid, cost);
     return 1;
