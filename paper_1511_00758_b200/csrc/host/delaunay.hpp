@@ -35,6 +35,11 @@ struct DelaunayWorkspace {
     std::vector<float> first;
 };
 
+// Lexicographic (u, v) order with coincident points removed, first
+// occurrence kept (delaunay.cpp:296-311): ws.kept[0..m) = original indices.
+void lex_order(const int* u, const int* v, int n, DelaunayWorkspace& ws, int& minx, int& miny,
+               int& m, int& spanx, int& spany);
+
 // Returns the number of triangles (index triples into the input written to
 // `tris`, 3 ints each, positively oriented: orient2d > 0), 0 for fewer than
 // three distinct points or a collinear set, -1 if a coordinate has

@@ -1,0 +1,208 @@
+// frame_mesh.cpp — see frame_mesh.hpp.
+#include "frame_mesh.hpp"
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+namespace ps {
+
+namespace {
+
+double now_ms() {
+    return std::chrono::duration<double, std::milli>(
+               std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+}
+
+inline int nxt(int e) { return (e % 3 == 2) ? e - 2 : e + 1; }
+inline int prv(int e) { return (e % 3 == 0) ? e + 2 : e - 1; }
+
+// fitPlane (proj/src/mesh.cpp:12-26), numerators in source order; this file is
+// built with -ffp-contract=off, so every step rounds like the reference's.
+struct Fit {
+    double A, B, C;
+    long long det;
+};
+
+inline Fit fit(const FrameMesh& fm, int i, int j, int k) {
+    const long long u1 = fm.u[i], u2 = fm.u[j], u3 = fm.u[k];
+    const long long w1 = fm.v[i], w2 = fm.v[j], w3 = fm.v[k];
+    const double d1 = fm.d[i], d2 = fm.d[j], d3 = fm.d[k];
+    Fit f;
+    f.det = u1 * (w2 - w3) + u2 * (w3 - w1) + u3 * (w1 - w2);
+    f.A = d1 * double(w2 - w3) + d2 * double(w3 - w1) + d3 * double(w1 - w2);
+    f.B = double(u1) * (d2 - d3) + double(u2) * (d3 - d1) + double(u3) * (d1 - d2);
+    f.C = d1 * double(u2 * w3 - u3 * w2) - d2 * double(u1 * w3 - u3 * w1) +
+          d3 * double(u1 * w2 - u2 * w1);
+    return f;
+}
+
+inline bool same_bits(const Fit& a, const Fit& b) {
+    return std::memcmp(&a.A, &b.A, 8) == 0 && std::memcmp(&a.B, &b.B, 8) == 0 &&
+           std::memcmp(&a.C, &b.C, 8) == 0;
+}
+
+// D_it at (u, v) as the raster stores it: binary32 bits, or NaN when invalid
+// (mesh.cpp:149-164: d = float(a*u + b*v + c), valid iff 0 <= d < ND).
+inline uint32_t dit_bits(const Fit& f, int u, int v, float nd) {
+    const double a = f.A / double(f.det), b = f.B / double(f.det), c = f.C / double(f.det);
+    const double s = (a * double(u) + b * double(v)) + c;
+    const float d = float(s);
+    if (!(d >= 0.0f && d < nd)) return 0x7fc00000u;
+    uint32_t bits;
+    std::memcpy(&bits, &d, 4);
+    return bits;
+}
+
+constexpr int kMaxQueries = 24;
+
+inline bool integral(double x) { return x == std::floor(x) && std::fabs(x) < 1e9; }
+
+inline bool tie_accept(int xi, int yi, int xj, int yj) {
+    return (yj < yi) || (yj == yi && xj > xi);  // mesh.cpp:80
+}
+
+int replay(FrameMesh& fm, int width, int height, int* tris, int cap, uint8_t* pins,
+           DelaunayWorkspace& ws, MeshStats& st) {
+    ++st.fallbacks;
+    const int n = int(fm.u.size());
+    const int t = delaunay_lex(fm.u.data(), fm.v.data(), n, tris, cap, ws);
+    if (t > 0) lex_hull_pins(ws, t, width, height, pins);
+    return t;
+}
+
+}  // namespace
+
+int mesh_iteration(FrameMesh& fm, int width, int height, float max_disparity, int* tris, int cap,
+                   uint8_t* pins, DelaunayWorkspace& ws, MeshStats& st) {
+    ++st.frames;
+    const int n = int(fm.u.size());
+    if (fm.lex_only) return replay(fm, width, height, tris, cap, pins, ws, st);
+    double t0 = now_ms();
+    if (!fm.dt.extend(fm.u.data(), fm.v.data(), n)) {
+        for (int i = 0; i < n; ++i)
+            if (std::abs(fm.u[i]) >= (1 << 20) || std::abs(fm.v[i]) >= (1 << 20)) return -1;
+        fm.lex_only = true;  // internal inconsistency: exact replay from now on
+        return replay(fm, width, height, tris, cap, pins, ws, st);
+    }
+    if (fm.dt.degenerate()) return 0;
+    const int nt = fm.dt.triangles();
+    if (nt > cap) return -3;
+    std::memcpy(tris, fm.dt.tri(), sizeof(int) * 3 * size_t(nt));
+    double t1 = now_ms();
+    st.dt_ms += t1 - t0;
+
+    // (2) rotation: fractional-vertex triangles fitted three ways
+    fm.q.clear();  // triangles whose rotation must come from the sweep
+    for (int t = 0; t < nt; ++t) {
+        const int i = tris[3 * t], j = tris[3 * t + 1], k = tris[3 * t + 2];
+        if (integral(fm.d[i]) && integral(fm.d[j]) && integral(fm.d[k])) continue;
+        ++st.rot_checked;
+        const Fit f0 = fit(fm, i, j, k), f1 = fit(fm, j, k, i), f2 = fit(fm, k, i, j);
+        if (!same_bits(f0, f1) || !same_bits(f0, f2)) fm.q.push_back(t);
+    }
+
+    bool have_order = false;
+    auto build_order = [&]() -> bool {
+        if (have_order) return true;
+        int minx, miny, m, spanx, spany;
+        lex_order(fm.u.data(), fm.v.data(), n, ws, minx, miny, m, spanx, spany);
+        fm.ranks.assign(ws.kept.begin(), ws.kept.begin() + m);
+        fm.rank_of.assign(n, -1);
+        fm.px.resize(m);
+        fm.py.resize(m);
+        for (int r = 0; r < m; ++r) {
+            fm.rank_of[fm.ranks[r]] = r;
+            fm.px[r] = fm.u[fm.ranks[r]];
+            fm.py[r] = fm.v[fm.ranks[r]];
+        }
+        fm.so.init(fm.px.data(), fm.py.data(), m);
+        have_order = true;
+        return true;
+    };
+
+    // Each order query replays a window of the sweep: past a handful the
+    // whole replay is cheaper (real meshes need 0-2 per frame-iteration).
+    if (int(fm.q.size()) > kMaxQueries) return replay(fm, width, height, tris, cap, pins, ws, st);
+    int queries = int(fm.q.size());
+    if (!fm.q.empty()) {
+        const double to = now_ms();
+        build_order();
+        const std::vector<int> rot = fm.q;
+        for (const int t : rot) {
+            int r3[3] = {fm.rank_of[tris[3 * t]], fm.rank_of[tris[3 * t + 1]], fm.rank_of[tris[3 * t + 2]]};
+            uint64_t b;
+            int s3[3];
+            if (!fm.so.resolve(r3, 1, &b, s3)) {
+                st.order_ms += now_ms() - to;
+                return replay(fm, width, height, tris, cap, pins, ws, st);
+            }
+            for (int k = 0; k < 3; ++k) tris[3 * t + k] = fm.ranks[s3[k]];
+            ++st.rotations;
+        }
+        st.order_ms += now_ms() - to;
+    }
+
+    // (3) pins: walk the hull; an uncovered vertex pixel whose incident planes
+    // disagree takes the incident triangle the sweep stored first
+    std::memset(pins, 0, size_t(nt));
+    const int* tv = fm.dt.tri();
+    const int* tn = fm.dt.nbr();
+    const int h0 = fm.dt.hull_start();
+    int guard = 0;
+    for (int h = h0; h >= 0;) {
+        if (++guard > n + 1) return replay(fm, width, height, tris, cap, pins, ws, st);
+        bool covered = false;
+        fm.inc.clear();
+        for (int g = fm.dt.hull_edge(h); g >= 0;) {  // g: h -> q, triangle on its left
+            const int q = tv[nxt(g)], r = tv[prv(g)];
+            if (tie_accept(fm.u[r], fm.v[r], fm.u[h], fm.v[h]) &&
+                tie_accept(fm.u[h], fm.v[h], fm.u[q], fm.v[q])) {
+                covered = true;
+                break;
+            }
+            fm.inc.push_back(g / 3);
+            g = tn[prv(g)];  // twin of r -> h: the next triangle around h
+            if (int(fm.inc.size()) > nt) return replay(fm, width, height, tris, cap, pins, ws, st);
+        }
+        const int hu = fm.u[h], hv = fm.v[h];
+        if (!covered && !fm.inc.empty() && hu >= 0 && hu < width && hv >= 0 && hv < height) {
+            uint32_t first = 0;
+            bool agree = true;
+            for (size_t i = 0; i < fm.inc.size(); ++i) {
+                const int t = fm.inc[i];
+                const uint32_t bits = dit_bits(fit(fm, tris[3 * t], tris[3 * t + 1], tris[3 * t + 2]), hu, hv, max_disparity);
+                if (i == 0) first = bits;
+                else if (bits != first) agree = false;
+            }
+            int pin_t = fm.inc[0];
+            if (!agree && ++queries > kMaxQueries) return replay(fm, width, height, tris, cap, pins, ws, st);
+            if (!agree) {
+                const double to = now_ms();
+                build_order();
+                const int cnt = int(fm.inc.size());
+                std::vector<int> r3(3 * size_t(cnt)), s3(3 * size_t(cnt));
+                fm.birth.resize(cnt);
+                for (int i = 0; i < cnt; ++i)
+                    for (int k = 0; k < 3; ++k) r3[3 * i + k] = fm.rank_of[tv[3 * fm.inc[i] + k]];
+                const bool ok = fm.so.resolve(r3.data(), cnt, fm.birth.data(), s3.data());
+                st.order_ms += now_ms() - to;
+                if (!ok) return replay(fm, width, height, tris, cap, pins, ws, st);
+                int best = 0;
+                for (int i = 1; i < cnt; ++i)
+                    if (fm.birth[i] < fm.birth[best]) best = i;
+                pin_t = fm.inc[best];
+                ++st.ambiguous;
+            }
+            for (int k = 0; k < 3; ++k)
+                if (tris[3 * pin_t + k] == h) pins[pin_t] |= uint8_t(1u << k);
+        }
+        h = fm.dt.hull_next(h);
+        if (h == h0) break;
+    }
+    st.check_ms += now_ms() - t1;
+    return nt;
+}
+
+}  // namespace ps

@@ -1,0 +1,67 @@
+// frame_mesh.hpp — one frame's mesh for one iteration, as the reference
+// builds it (planestereo::triangulate + DisparityMesh, proj/src/mesh.cpp:44-147),
+// without replaying the reference's lexicographic sweep when it can be avoided.
+//
+// What the raster consumes from the reference's mesh is (1) the triangle SET,
+// (2) each triangle's plane, fitted in the vertex rotation the sweep stored
+// (mesh.cpp:12-26 sums three products in source order), and (3) for each
+// hull vertex pixel the tie rule leaves uncovered, the FIRST incident
+// triangle in the sweep's output order (mesh.cpp:109-122).
+//
+//  (1) comes from IncDT: the previous iteration's triangulation plus this
+//      iteration's new supports (incdt.hpp).
+//  (2) matters only when the three rotations round differently; integer
+//      disparities (seeds, re-matched supports) are exact, so only triangles
+//      with a fractional vertex are fitted three ways, and the rare ones
+//      that differ get the sweep's rotation from SweepOrder.
+//  (3) matters only when the incident planes give different binary32 D_it
+//      bits at the vertex (a d = 0 hull vertex: ±1e-17); then SweepOrder
+//      orders the incident triangles as the sweep's slots.
+// Any inconsistency falls back to the exact replay (delaunay_lex).
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "delaunay.hpp"
+#include "incdt.hpp"
+#include "sweep_order.hpp"
+
+namespace ps {
+
+struct MeshStats {
+    long long frames = 0;      // frame-iterations meshed
+    long long fallbacks = 0;   // of which replayed with delaunay_lex
+    long long ambiguous = 0;   // hull-vertex pins resolved through SweepOrder
+    long long rotations = 0;   // triangles whose rotation SweepOrder decided
+    long long rot_checked = 0; // triangles fitted three ways
+    double dt_ms = 0, check_ms = 0, order_ms = 0;
+};
+
+struct FrameMesh {
+    IncDT dt;
+    std::vector<int> u, v;   // the frame's support list so far
+    std::vector<double> d;
+    bool lex_only = false;   // PS_DELAUNAY=lex: always replay
+    // scratch
+    std::vector<int> ranks, rank_of, px, py, inc, q, stored;
+    std::vector<uint64_t> birth;
+    std::vector<uint8_t> rot_bad;
+    SweepOrder so;
+    void reset() {
+        dt.reset();
+        u.clear();
+        v.clear();
+        d.clear();
+    }
+};
+
+// Meshes the frame's current support list (fm.u/v/d): writes up to `cap`
+// triangles (3 support indices each, in the rotation the raster must fit) to
+// `tris` and one pin byte per triangle (bit k: corner k is an uncovered
+// vertex pixel pinned to this triangle).  Returns the triangle count, 0 for
+// a degenerate set, -1 coordinate overflow, -2 internal error, -3 capacity.
+int mesh_iteration(FrameMesh& fm, int width, int height, float max_disparity, int* tris, int cap,
+                   uint8_t* pins, DelaunayWorkspace& ws, MeshStats& st);
+
+}  // namespace ps
