@@ -36,6 +36,57 @@ METRIC = "stereo frames/sec & Mpix/s at VGA, N iterations; achieved HBM GB/s vs 
 UNIT = "frames/s"
 
 
+# BASELINE.json configs (SURVEY 8(d) mapping); the same table as
+# paper_1511_00758_b200.BASELINE_CONFIGS (checked in the ours arm), repeated
+# here so the reference arm never imports the product package.
+CONFIGS = {
+    0: dict(width=640, height=480, frames=1, n_planes=12, max_disparity=64, ground=False,
+            sigma=2.0, iterations=2, cell=10),
+    1: dict(width=1242, height=375, frames=1, n_planes=24, max_disparity=128, ground=True,
+            sigma=2.0, iterations=4, cell=8),
+    2: dict(width=640, height=480, frames=256, n_planes=12, max_disparity=64, ground=False,
+            sigma=2.0, iterations=3, cell=10),
+    3: dict(width=1920, height=1080, frames=1, n_planes=40, max_disparity=256, ground=False,
+            sigma=4.0, iterations=4, cell=8),
+    4: dict(width=3840, height=2160, frames=64, n_planes=60, max_disparity=256, ground=False,
+            sigma=2.0, iterations=6, cell=6),
+}
+
+
+def config_fields(k: int) -> dict:
+    """PipelineConfig field dict (proj/include/planestereo/config.hpp:8-34 defaults)."""
+    c = CONFIGS[k]
+    return dict(iterations=c["iterations"], maxDisparity=c["max_disparity"], costLow=0.25,
+                costHigh=0.5, gradientThreshold=20, occupancyCellSize=c["cell"], cornerThreshold=20,
+                perBinCap=5, sparseAcceptCost=0.25, uniquenessRatio=0.9, threads=1)
+
+
+def config_line(args, frames: int, world: int) -> dict:
+    """The `config` object of both arms' JSON lines (identical by construction)."""
+    c = CONFIGS[args.config]
+    return {"workload": f"BASELINE config {args.config}: {frames} x {c['width']}x{c['height']} pairs per GPU, "
+                        f"{c['iterations']} iterations, grid {c['cell']}, ND {c['max_disparity']}",
+            "frames_per_gpu": frames, "parallelism": f"frame-sharded x{world} (no collective)",
+            "l2": "working set (census+state ~2.9 GB/batch) far larger than L2; no flush needed"}
+
+
+def host_info() -> dict:
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except AttributeError:
+        usable = os.cpu_count() or 1
+    return {"cpu_model": model, "nproc": os.cpu_count() or 1, "usable_cpus": usable}
+
+
 def parse_args():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -219,38 +270,76 @@ def make_inputs(ps, cfgd, frames, seed, pinned):
     return L, R, (tl, tr)
 
 
+def reference_inputs(ref, k: int, frames: int, seed: int):
+    """The seeded pairs, generated inside oracle/_ref (ref_synth_batch: the
+    repo's generator compiled into the checker), byte-identical to the ones
+    the ours arm generates through the product."""
+    import numpy as np
+
+    c = CONFIGS[k]
+    L = np.empty((frames, c["height"], c["width"]), np.uint8)
+    R = np.empty_like(L)
+    fn = ref.lib.ref_synth_batch
+    fn.restype = C.c_int
+    fn.argtypes = [C.c_int] * 4 + [C.c_int, C.c_float, C.c_uint, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
+    st = fn(c["width"], c["height"], c["n_planes"], c["max_disparity"], int(c["ground"]), c["sigma"],
+            seed, frames, os.cpu_count() or 8, L.ctypes.data, R.ctypes.data)
+    if st != 0:
+        raise RuntimeError(f"ref_synth_batch failed: {st}")
+    return L, R
+
+
+def reference_latency(ref, L, R, cfgd, repeats=5):
+    """The reference's own harness, benchmark(fn, repeats, pinToCore=true)
+    (proj/src/eval.cpp:144-177, via ref_benchmark_run): median ms, one thread."""
+    import oracle
+
+    fn = ref.lib.ref_benchmark_run
+    c = oracle.to_cfg(cfgd)
+    h, w = L.shape
+    return float(fn(L.ctypes.data, R.ctypes.data, w, h, C.byref(c), repeats))
+
+
 def run_reference_arm(args, rank, world):
+    """The reference's CPU path: oracle/_ref (the unmodified reference
+    sources compiled in place, driven by the staged run() loop) on all host
+    threads, one frame per thread.  Only oracle/_ref is loaded in this process."""
     if rank != 0:
         return
-    import paper_1511_00758_b200 as ps
+    import oracle
 
-    cfgd = ps.BASELINE_CONFIGS[args.config]
-    cfg = ps.baseline_config(args.config)
-    frames = args.frames or cfgd["frames"]
-    checker, kind = cpu_checker()
+    ref = oracle.load_ref()
+    if ref is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference)"}))
+        return
+    cfgd = config_fields(args.config)
+    c = CONFIGS[args.config]
+    frames = args.frames or c["frames"]
     cores = os.cpu_count() or 1
-    L, R, _ = make_inputs(ps, cfgd, frames, 1000, pinned=False)
+    L, R = reference_inputs(ref, args.config, frames, rank_seed(0, frames))
     for _ in range(args.warmup):
-        checker.run_batch(L, R, cfg, cores)
+        ref.run_batch(L, R, cfgd, cores)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        st = checker.run_batch(L, R, cfg, cores)["status"]
+        st = ref.run_batch(L, R, cfgd, cores)["status"]
     dt = time.perf_counter() - t0
     value = frames * args.steps / dt
-    P = cfgd["width"] * cfgd["height"]
+    P = c["width"] * c["height"]
+    lat = reference_latency(ref, L[0], R[0], cfgd) if c["width"] * c["height"] <= 2_100_000 else None
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8/u32/f32/f64",
-        "data": "synthetic (seeded BASELINE-style generator, SURVEY 8(d))",
-        "config": {"workload": f"BASELINE config {args.config}: {frames} x {cfgd['width']}x{cfgd['height']}"
-                               f" pairs, {cfg.iterations} iterations, grid {cfg.occupancyCellSize}, ND {cfg.maxDisparity}",
-                   "frames_per_step": frames},
+        "data": "synthetic (seeded BASELINE-style generator, SURVEY 8(d)); host memory",
+        "config": config_line(args, frames, world),
         "mpix_per_s": value * P / 1e6,
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
-                         "sample": f"all {frames} frames per step, one frame per host thread, "
-                                   f"{'oracle/_ref (reference sources)' if kind == 'reference' else 'oracle/ps_oracle.c'}"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": f"all {frames} frames per step, one frame per host thread on {cores} "
+                                   f"threads, oracle/_ref (reference sources, staged run())",
+                         **host_info()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "latency": {"reference_ms_median": lat,
+                    "what": "one frame, benchmark(fn, 5, pinToCore=true) (eval.cpp:144-177)"},
         "failed_frames": int((st != 0).sum()),
     }
     print(json.dumps(line), flush=True)
@@ -281,7 +370,9 @@ def run_ours(args, rank, world, local_rank):
         return float(t.item())
 
     cfgd = ps.BASELINE_CONFIGS[args.config]
+    assert cfgd == CONFIGS[args.config], "bench.CONFIGS out of sync with the package"
     cfg = ps.baseline_config(args.config)
+    assert {f: getattr(cfg, f) for f in cfg.__dataclass_fields__} == config_fields(args.config)
     frames = args.frames or cfgd["frames"]
     H, W = cfgd["height"], cfgd["width"]
     P = W * H
@@ -371,7 +462,9 @@ def run_ours(args, rank, world, local_rank):
 
     # ---------------- Delaunay throughput (K4 is host work: points/s)
     points_per_pass = sum(int(t.support_count) for t in trace)  # the e2e batch's trace
-    sweep = kstats_timed.get("host_sweep", {"ms": 0.0})
+    sweep = kstats_timed.get("host_mesh", {"ms": 0.0})
+    mesh_events = {k: kstats_timed.get(k, {}).get("launches", 0) // args.steps
+                   for k in ("host_replay", "host_order", "host_check")}
 
     # ---------------- roofline of the dominant graded kernel (K7 refine)
     peak, peak_src = measured_peak()
@@ -394,10 +487,8 @@ def run_ours(args, rank, world, local_rank):
         "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8/u32/f32/f64",
         "data": "synthetic (seeded BASELINE-style generator, SURVEY 8(d)); inputs resident in HBM",
-        "config": {"workload": f"BASELINE config {args.config}: {frames} x {W}x{H} pairs per GPU, "
-                               f"{cfg.iterations} iterations, grid {cfg.occupancyCellSize}, ND {cfg.maxDisparity}",
-                   "frames_per_gpu": frames, "parallelism": f"frame-sharded x{world} (no collective)",
-                   "l2": "working set (census+state ~2.9 GB/batch) far larger than L2; no flush needed"},
+        "config": config_line(args, frames, world),
+        "host": {**host_info(), "workers_per_rank": ctx.host_threads()},
         "mpix_per_s": value * P / 1e6,
         "wall_ms_per_step": wall_ms / args.steps,
         "gpu_launches": int(launches),
@@ -423,7 +514,13 @@ def run_ours(args, rank, world, local_rank):
                      "sweep_ms_per_frame_iteration":
                          sweep["ms"] / args.steps * ctx.host_threads() / (frames * cfg.iterations),
                      "workers": ctx.host_threads(),
-                     "note": "host lexicographic sweep (reference order), one task per frame and iteration"},
+                     "replayed_frame_iterations_per_pass": mesh_events["host_replay"],
+                     "order_queries_per_pass": mesh_events["host_order"],
+                     "planes_fitted_three_ways_per_pass": mesh_events["host_check"],
+                     "frame_iterations_per_pass": frames * cfg.iterations,
+                     "note": "host mesh per frame and iteration: incremental exact Delaunay (previous "
+                             "iteration + new supports), reference sweep order/rotation recovered only "
+                             "where the output depends on it (frame_mesh.hpp); replay = delaunay_lex"},
         "host_pipeline_ms_per_step": {k: v["ms"] / args.steps for k, v in kstats_timed.items()
                                       if k.startswith("host_")},
         "latency": {"ours_ms_min": lat[0], "ours_ms_median": lat[len(lat) // 2],
@@ -437,16 +534,15 @@ def run_ours(args, rank, world, local_rank):
         t0 = time.perf_counter()
         checker.run_batch(L[:n], R[:n], cfg, cores)
         dt = time.perf_counter() - t0
-        rl = []
-        for _ in range(3):  # eval.cpp:144-177 benchmark(): min over repeats, one thread
-            r0 = time.perf_counter()
-            checker.run(L[0], R[0], cfg)
-            rl.append((time.perf_counter() - r0) * 1e3)
-        line["latency"]["reference_ms_min"] = min(rl)
+        if kind == "reference":
+            line["latency"]["reference_ms_median"] = reference_latency(
+                checker, np.ascontiguousarray(L[0]), np.ascontiguousarray(R[0]), config_fields(args.config))
+            line["latency"]["reference_what"] = "benchmark(fn, 5, pinToCore=true) (eval.cpp:144-177), median"
         line["cpu_baseline"] = {
             "value": n / dt, "unit": UNIT, "cores": cores, "kind": kind,
             "sample": f"{n} of the {frames} frames, one frame per host thread on {cores} threads "
-                      f"({'oracle/_ref: reference sources' if kind == 'reference' else 'oracle/ps_oracle.c'})"}
+                      f"({'oracle/_ref: reference sources' if kind == 'reference' else 'oracle/ps_oracle.c'})",
+            **host_info()}
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()
@@ -520,8 +616,24 @@ def run_configs_table(args):
 
 
 
+def relaunch_under_torchrun(n: int) -> None:
+    """`python bench.py --gpus N` without a launcher: re-exec as N ranks under
+    torch.distributed.run (one process per GPU, rendezvous on 127.0.0.1)."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
 def main():
     args = parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and not args.configs:
+        relaunch_under_torchrun(args.gpus)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

@@ -474,4 +474,15 @@ double ref_benchmark_run(const uint8_t* left, const uint8_t* right, int w, int h
     return r.medianMs;
 }
 
+// Inputs for the reference arm: the repo's seeded generator (synth.cpp,
+// compiled into this library), frame f seeded with seed + f.
+ps_status ps_synth_batch(const ps_synth_params* p, int n_frames, int threads, uint8_t* left,
+                         uint8_t* right);
+int ref_synth_batch(int width, int height, int n_planes, int max_disparity, int ground,
+                    float sigma, unsigned seed, int n_frames, int threads, uint8_t* left,
+                    uint8_t* right) {
+    ps_synth_params p{width, height, n_planes, max_disparity, ground, sigma, seed};
+    return ps_synth_batch(&p, n_frames, threads, left, right);
+}
+
 }  // extern "C"

@@ -26,6 +26,7 @@
 #include <sched.h>
 
 #include "../kernels/launch.hpp"
+#include "frame_mesh.hpp"
 
 namespace ps {
 
@@ -486,12 +487,16 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     status_.assign(F, PS_OK);
     final_count_.assign(F, 0);
     double host_dt_ms = 0.0;
-    hu_.resize(F);
-    hv_.resize(F);
+    // per-frame mesh state, kept across the iterations of this run (the
+    // triangulation is extended, not rebuilt: frame_mesh.hpp)
+    const char* dt_mode = std::getenv("PS_DELAUNAY");
+    const bool lex_only = dt_mode && std::string(dt_mode) == "lex";
+    if (int(fmesh_.size()) < F) fmesh_.resize(F);
     for (int f = 0; f < F; ++f) {
-        hu_[f].clear();
-        hv_[f].clear();
+        fmesh_[f].reset();
+        fmesh_[f].lex_only = lex_only;
     }
+    std::vector<MeshStats> mstats(pool_->size());
     trace_.assign(size_t(F) * iters, ps_iter_stats{});
 
     // ---- frame groups: a dataflow pipeline.  Per group: (H2D of a deferred
@@ -617,7 +622,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
             return true;
         });
     };
-    std::atomic<double> dt_ms_sum{0.0}, sweep_ms_sum{0.0}, pins_ms_sum{0.0};
+    std::atomic<double> dt_ms_sum{0.0}, sweep_ms_sum{0.0};
     std::atomic<double> first_task{1e300}, last_task{0.0};  // pool occupancy (profiling)
     std::vector<double> worker_end(pool_->size(), 0.0);     // PS_DEBUG_TIMELINE
     auto add_ms = [](std::atomic<double>& acc, double x) {
@@ -647,11 +652,14 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
             total_new += k;
             max_new = std::max(max_new, k);
         }
-        // the Delaunay needs only the new supports' (u, v)
+        // the mesh needs the new supports' (u, v) and d (plane checks)
         const size_t npk = size_t(std::max<long long>(total_new, 1));
         int2* dPack = dev<int2>(grp.dPack, npk);
         int2* hPack = reinterpret_cast<int2*>(host<uint8_t>(grp.hPack, npk * 8));
-        if (!dPack || !hPack) return fail(PS_CUDA_ERROR, "allocation failed (support staging)");
+        double* dPackD = dev<double>(grp.dPackD, npk);
+        double* hPackD = reinterpret_cast<double*>(host<uint8_t>(grp.hPackD, npk * 8));
+        if (!dPack || !hPack || !dPackD || !hPackD)
+            return fail(PS_CUDA_ERROR, "allocation failed (support staging)");
         int* dSprev = static_cast<int*>(grp.dSprev.p);
         int* dPackOff = static_cast<int*>(grp.dPackOff.p);
         r = check(cudaMemcpyAsync(dSprev, hsp, sizeof(int) * n, cudaMemcpyHostToDevice, gs), "H2D Sprev");
@@ -662,10 +670,13 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         const int f0 = grp.f0;
         launches_ += launch_pack_new_supports(dSu + size_t(f0) * scap_, dSv + size_t(f0) * scap_,
                                               dSd + size_t(f0) * scap_, scap_, dSprev, grp.S,
-                                              dPackOff, n, max_new, dPack, nullptr, gs);
+                                              dPackOff, n, max_new, dPack, dPackD, gs);
         if (total_new > 0)
             r = check(cudaMemcpyAsync(hPack, dPack, sizeof(int2) * total_new, cudaMemcpyDeviceToHost, gs),
                       "D2H supports");
+        if (total_new > 0 && r == PS_OK)
+            r = check(cudaMemcpyAsync(hPackD, dPackD, sizeof(double) * total_new, cudaMemcpyDeviceToHost, gs),
+                      "D2H support disparities");
         const double tsync = now_ms();
         if (r == PS_OK) r = sync(gs, "support delta");
         if (debug_timeline_)
@@ -698,32 +709,26 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                 const int* hsp = static_cast<const int*>(g2.hSprev.p);
                 const int* hoff = static_cast<const int*>(g2.hPackOff.p);
                 const int2* hPack = static_cast<const int2*>(g2.hPack.p);
+                const double* hPackD = static_cast<const double*>(g2.hPackD.p);
                 const int k = hs[i] - hsp[i];
-                std::vector<int>& fu = hu_[f];
-                std::vector<int>& fv = hv_[f];
-                const size_t n0 = fu.size();
-                fu.resize(n0 + k);
-                fv.resize(n0 + k);
+                FrameMesh& fm = fmesh_[f];
                 for (int j = 0; j < k; ++j) {
                     const int2 q = hPack[hoff[i] + j];
-                    fu[n0 + j] = q.x;
-                    fv[n0 + j] = q.y;
+                    fm.u.push_back(q.x);
+                    fm.v.push_back(q.y);
+                    fm.d.push_back(hPackD[hoff[i] + j]);
                 }
                 int t = 0;
                 if (status_[f] == PS_OK) {
-                    const int ns = int(fu.size());
                     DelaunayWorkspace& w = (*ws_)[worker];
-                    // the reference's triangle order and rotation (pins and
-                    // fitPlane rounding then match it bit for bit), written
-                    // straight into the group's pinned staging slot
+                    // triangles (in the rotation the raster must fit) and pin
+                    // bits straight into the group's pinned staging slot
                     int* slot = static_cast<int*>(g2.hTri.p) + size_t(i) * tri_cap * 3;
+                    uint8_t* pins = static_cast<uint8_t*>(g2.hPin.p) + size_t(i) * tri_cap;
                     const double ts0 = now_ms();
-                    t = delaunay_lex(fu.data(), fv.data(), ns, slot, tri_cap, w);
-                    const double ts1 = now_ms();
-                    if (t > 0)  // == mesh_pins()
-                        lex_hull_pins(w, t, W, H, static_cast<uint8_t*>(g2.hPin.p) + size_t(i) * tri_cap);
-                    add_ms(sweep_ms_sum, ts1 - ts0);
-                    add_ms(pins_ms_sum, now_ms() - ts1);
+                    t = mesh_iteration(fm, W, H, float(cfg.max_disparity), slot, tri_cap, pins, w,
+                                       mstats[worker]);
+                    add_ms(sweep_ms_sum, now_ms() - ts0);
                     if (t < 0) {
                         status_[f] = PS_ERROR;
                         t = 0;
@@ -1034,12 +1039,33 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         dt.launches += F * iters;
         dt.ms += host_dt_ms;
         const double workers = double(std::max(1, pool_->size()));
-        KernelStat& sw = stat("host_sweep");  // of which: the lexicographic sweep
+        KernelStat& sw = stat("host_mesh");  // of which: mesh_iteration (per-worker share)
         sw.launches += F * iters;
         sw.ms += sweep_ms_sum.load() / workers;
-        KernelStat& pn = stat("host_pins");  // of which: hull-vertex pins
-        pn.launches += F * iters;
-        pn.ms += pins_ms_sum.load() / workers;
+        MeshStats tot;
+        for (const MeshStats& m : mstats) {
+            tot.frames += m.frames;
+            tot.fallbacks += m.fallbacks;
+            tot.ambiguous += m.ambiguous;
+            tot.rotations += m.rotations;
+            tot.rot_checked += m.rot_checked;
+            tot.dt_ms += m.dt_ms;
+            tot.check_ms += m.check_ms;
+            tot.order_ms += m.order_ms;
+        }
+        // launches = events: replays of the reference sweep, pins ordered by
+        // SweepOrder, rotations it decided, triangles fitted three ways
+        KernelStat& k1 = stat("host_dt");  // incremental Delaunay
+        k1.launches += int(tot.frames);
+        k1.ms += tot.dt_ms / workers;
+        KernelStat& k2 = stat("host_check");  // rotation + pin checks (incl. order)
+        k2.launches += int(tot.rot_checked);
+        k2.ms += tot.check_ms / workers;
+        KernelStat& k3 = stat("host_order");  // SweepOrder queries
+        k3.launches += int(tot.ambiguous + tot.rotations);
+        k3.ms += tot.order_ms / workers;
+        KernelStat& k4 = stat("host_replay");  // frame-iterations replayed (delaunay_lex)
+        k4.launches += int(tot.fallbacks);
         // pool occupancy: before the first task, gaps between tasks, after the last
         const double fa = first_task.load(), la = last_task.load(), end = now_ms();
         if (la > 0.0) {

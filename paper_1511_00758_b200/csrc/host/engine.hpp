@@ -20,6 +20,7 @@
 
 #include "../kernels/common.cuh"
 #include "delaunay.hpp"
+#include "frame_mesh.hpp"
 #include "planestereo_c.h"
 #include "thread_pool.hpp"
 
@@ -206,7 +207,7 @@ private:
     // pinned host staging
     HostBuf hS_, hTraceSum_, hTraceValid_, hMaskCount_;
     int scap_ = 0;
-    std::vector<std::vector<int>> hu_, hv_;  // per frame support coordinates (host copy)
+    std::vector<FrameMesh> fmesh_;  // per frame: support list (host copy) + mesh state
     std::vector<int> status_, final_count_;
     std::vector<ps_iter_stats> trace_;
 };
