@@ -1,6 +1,7 @@
 // frame_mesh.cpp — see frame_mesh.hpp.
 #include "frame_mesh.hpp"
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -15,8 +16,9 @@ double now_ms() {
         .count();
 }
 
-inline int nxt(int e) { return (e % 3 == 2) ? e - 2 : e + 1; }
-inline int prv(int e) { return (e % 3 == 0) ? e + 2 : e - 1; }
+// IncDT half-edges: e = 4t + k
+inline int nxt(int e) { return (e & 3) == 2 ? e - 2 : e + 1; }
+inline int prv(int e) { return (e & 3) == 0 ? e + 2 : e - 1; }
 
 // fitPlane (proj/src/mesh.cpp:12-26), numerators in source order; this file is
 // built with -ffp-contract=off, so every step rounds like the reference's.
@@ -57,6 +59,50 @@ inline uint32_t dit_bits(const Fit& f, int u, int v, float nd) {
 
 constexpr int kMaxQueries = 24;
 
+long long floor_div(long long a, long long b) {  // mesh.cpp:30-36
+    long long q = a / b;
+    if ((a % b != 0) && ((a < 0) != (b < 0))) --q;
+    return q;
+}
+
+// Whether the three rotations of a triangle whose fitted planes differ in
+// their binary64 bits still give the same binary32 D_it at every pixel the
+// triangle covers (the top-left rule of mesh.cpp:58-104) and at its vertex
+// pixels (pins): then the rotation the sweep stored cannot show in any output.
+bool rotations_equivalent(const FrameMesh& fm, int i, int j, int k, const Fit f[3], int width,
+                          int height, float nd) {
+    const int x[3] = {fm.u[i], fm.u[j], fm.u[k]}, y[3] = {fm.v[i], fm.v[j], fm.v[k]};
+    auto same_at = [&](int u, int v) {
+        const uint32_t b0 = dit_bits(f[0], u, v, nd);
+        return dit_bits(f[1], u, v, nd) == b0 && dit_bits(f[2], u, v, nd) == b0;
+    };
+    for (int q = 0; q < 3; ++q)
+        if (x[q] >= 0 && x[q] < width && y[q] >= 0 && y[q] < height && !same_at(x[q], y[q])) return false;
+    long long A[3], bias[3];
+    for (int a = 0; a < 3; ++a) {
+        const int b = (a + 1) % 3;
+        A[a] = y[a] - y[b];
+        bias[a] = ((y[b] < y[a]) || (y[b] == y[a] && x[b] > x[a])) ? 0 : 1;
+    }
+    const int vmin = std::max(0, std::min({y[0], y[1], y[2]}));
+    const int vmax = std::min(height - 1, std::max({y[0], y[1], y[2]}));
+    for (int v = vmin; v <= vmax; ++v) {
+        long long lo = 0, hi = width - 1;
+        bool empty = false;
+        for (int a = 0; a < 3 && !empty; ++a) {
+            const int b = (a + 1) % 3;
+            const long long K = (long long)(x[b] - x[a]) * (v - y[a]) + (long long)(y[b] - y[a]) * x[a];
+            if (A[a] > 0) lo = std::max(lo, -floor_div(K - bias[a], A[a]));
+            else if (A[a] < 0) hi = std::min(hi, floor_div(K - bias[a], -A[a]));
+            else if (K < bias[a]) empty = true;
+        }
+        if (empty) continue;
+        for (long long u = lo; u <= hi; ++u)
+            if (!same_at(int(u), v)) return false;
+    }
+    return true;
+}
+
 inline bool integral(double x) { return x == std::floor(x) && std::fabs(x) < 1e9; }
 
 inline bool tie_accept(int xi, int yi, int xj, int yj) {
@@ -89,7 +135,8 @@ int mesh_iteration(FrameMesh& fm, int width, int height, float max_disparity, in
     if (fm.dt.degenerate()) return 0;
     const int nt = fm.dt.triangles();
     if (nt > cap) return -3;
-    std::memcpy(tris, fm.dt.tri(), sizeof(int) * 3 * size_t(nt));
+    for (int t = 0; t < nt; ++t)
+        for (int k = 0; k < 3; ++k) tris[3 * t + k] = fm.dt.vert(t, k);
     double t1 = now_ms();
     st.dt_ms += t1 - t0;
 
@@ -99,8 +146,10 @@ int mesh_iteration(FrameMesh& fm, int width, int height, float max_disparity, in
         const int i = tris[3 * t], j = tris[3 * t + 1], k = tris[3 * t + 2];
         if (integral(fm.d[i]) && integral(fm.d[j]) && integral(fm.d[k])) continue;
         ++st.rot_checked;
-        const Fit f0 = fit(fm, i, j, k), f1 = fit(fm, j, k, i), f2 = fit(fm, k, i, j);
-        if (!same_bits(f0, f1) || !same_bits(f0, f2)) fm.q.push_back(t);
+        const Fit f3[3] = {fit(fm, i, j, k), fit(fm, j, k, i), fit(fm, k, i, j)};
+        if ((!same_bits(f3[0], f3[1]) || !same_bits(f3[0], f3[2])) &&
+            !rotations_equivalent(fm, i, j, k, f3, width, height, max_disparity))
+            fm.q.push_back(t);
     }
 
     bool have_order = false;
@@ -147,8 +196,7 @@ int mesh_iteration(FrameMesh& fm, int width, int height, float max_disparity, in
     // (3) pins: walk the hull; an uncovered vertex pixel whose incident planes
     // disagree takes the incident triangle the sweep stored first
     std::memset(pins, 0, size_t(nt));
-    const int* tv = fm.dt.tri();
-    const int* tn = fm.dt.nbr();
+    auto tv = [&](int e) { return fm.dt.vert(e >> 2, e & 3); };
     const int h0 = fm.dt.hull_start();
     int guard = 0;
     for (int h = h0; h >= 0;) {
@@ -156,14 +204,14 @@ int mesh_iteration(FrameMesh& fm, int width, int height, float max_disparity, in
         bool covered = false;
         fm.inc.clear();
         for (int g = fm.dt.hull_edge(h); g >= 0;) {  // g: h -> q, triangle on its left
-            const int q = tv[nxt(g)], r = tv[prv(g)];
+            const int q = tv(nxt(g)), r = tv(prv(g));
             if (tie_accept(fm.u[r], fm.v[r], fm.u[h], fm.v[h]) &&
                 tie_accept(fm.u[h], fm.v[h], fm.u[q], fm.v[q])) {
                 covered = true;
                 break;
             }
-            fm.inc.push_back(g / 3);
-            g = tn[prv(g)];  // twin of r -> h: the next triangle around h
+            fm.inc.push_back(g >> 2);
+            g = fm.dt.twin(prv(g));  // twin of r -> h: the next triangle around h
             if (int(fm.inc.size()) > nt) return replay(fm, width, height, tris, cap, pins, ws, st);
         }
         const int hu = fm.u[h], hv = fm.v[h];
@@ -185,7 +233,7 @@ int mesh_iteration(FrameMesh& fm, int width, int height, float max_disparity, in
                 std::vector<int> r3(3 * size_t(cnt)), s3(3 * size_t(cnt));
                 fm.birth.resize(cnt);
                 for (int i = 0; i < cnt; ++i)
-                    for (int k = 0; k < 3; ++k) r3[3 * i + k] = fm.rank_of[tv[3 * fm.inc[i] + k]];
+                    for (int k = 0; k < 3; ++k) r3[3 * i + k] = fm.rank_of[fm.dt.vert(fm.inc[i], k)];
                 const bool ok = fm.so.resolve(r3.data(), cnt, fm.birth.data(), s3.data());
                 st.order_ms += now_ms() - to;
                 if (!ok) return replay(fm, width, height, tris, cap, pins, ws, st);

@@ -1,8 +1,9 @@
 // incdt.cpp — see incdt.hpp.
 //
-// Half-edge e = 3t + k runs from tv[e] to tv[next(e)]; triangles are
-// counter-clockwise (orient > 0), tn[e] is the twin or -1 on the hull; a hull
-// edge a -> b (interior on its left) is hedge[a], with hnext[a] = b.
+// Half-edge e = 4t + k runs from V(e) to V(next(e)); triangles are 32-byte
+// records (vertices + twins: one cache line per flip side), counter-clockwise
+// (orient > 0); N(e) is the twin or -1 on the hull; a hull edge a -> b
+// (interior on its left) is hedge[a], with hnext[a] = b.
 #include "incdt.hpp"
 
 #include <algorithm>
@@ -11,15 +12,15 @@
 namespace ps {
 
 namespace {
-inline int nxt(int e) { return (e % 3 == 2) ? e - 2 : e + 1; }
-inline int prv(int e) { return (e % 3 == 0) ? e + 2 : e - 1; }
+inline int nxt(int e) { return (e & 3) == 2 ? e - 2 : e + 1; }
+inline int prv(int e) { return (e & 3) == 0 ? e + 2 : e - 1; }
 }  // namespace
 
 void IncDT::reset() {
     nv_ = 0;
     wide_ = false;
-    tv_.clear();
-    tn_.clear();
+    P_.clear();
+    T_.clear();
     hnext_.clear();
     hprev_.clear();
     hedge_.clear();
@@ -29,6 +30,7 @@ void IncDT::reset() {
     bucket_.clear();
     bw_ = bh_ = 0;
     last_ = 0;
+    lastp_ = -1;
     hull0_ = -1;
 }
 
@@ -36,9 +38,10 @@ void IncDT::reset() {
 // the lexicographically largest of the four points.
 bool IncDT::inside(int a, int b, int c, int d) {
     ++tests;
-    const long long adx = (long long)x_[a] - x_[d], ady = (long long)y_[a] - y_[d];
-    const long long bdx = (long long)x_[b] - x_[d], bdy = (long long)y_[b] - y_[d];
-    const long long cdx = (long long)x_[c] - x_[d], cdy = (long long)y_[c] - y_[d];
+    const Pt A = P_[a], B = P_[b], Cc = P_[c], D = P_[d];
+    const long long adx = (long long)A.x - D.x, ady = (long long)A.y - D.y;
+    const long long bdx = (long long)B.x - D.x, bdy = (long long)B.y - D.y;
+    const long long cdx = (long long)Cc.x - D.x, cdy = (long long)Cc.y - D.y;
     const long long aq = adx * adx + ady * ady;
     const long long bq = bdx * bdx + bdy * bdy;
     const long long cq = cdx * cdx + cdy * cdy;
@@ -54,7 +57,9 @@ bool IncDT::inside(int a, int b, int c, int d) {
         s = (det > 0) - (det < 0);
     }
     if (s != 0) return s > 0;
-    auto lex_less = [&](int p, int q) { return x_[p] < x_[q] || (x_[p] == x_[q] && y_[p] < y_[q]); };
+    auto lex_less = [&](int p, int q) {
+        return P_[p].x < P_[q].x || (P_[p].x == P_[q].x && P_[p].y < P_[q].y);
+    };
     int m = a;
     if (lex_less(m, b)) m = b;
     if (lex_less(m, c)) m = c;
@@ -66,16 +71,11 @@ bool IncDT::inside(int a, int b, int c, int d) {
 }
 
 int IncDT::add(int a, int b, int c, int na, int nb, int nc) {
-    const int e = int(tv_.size());
-    tv_.push_back(a);
-    tv_.push_back(b);
-    tv_.push_back(c);
-    tn_.push_back(na);
-    tn_.push_back(nb);
-    tn_.push_back(nc);
-    if (na >= 0) tn_[na] = e;
-    if (nb >= 0) tn_[nb] = e + 1;
-    if (nc >= 0) tn_[nc] = e + 2;
+    const int e = 4 * int(T_.size());
+    T_.push_back(Tri{{a, b, c}, {na, nb, nc}, {0, 0}});
+    if (na >= 0) N(na) = e;
+    if (nb >= 0) N(nb) = e + 1;
+    if (nc >= 0) N(nc) = e + 2;
     return e;
 }
 
@@ -85,18 +85,18 @@ void IncDT::legalize() {
     while (!stack_.empty()) {
         const int e = stack_.back();
         stack_.pop_back();
-        const int f = tn_[e];
+        const int f = N(e);
         if (f < 0) continue;
         const int e1 = nxt(e), e2 = nxt(e1);
         const int f1 = nxt(f), f2 = nxt(f1);
-        const int a = tv_[e], b = tv_[e1], c = tv_[e2], d = tv_[f2];
+        const int a = V(e), b = V(e1), c = V(e2), d = V(f2);
         if (!inside(a, b, c, d)) continue;
         ++flips;
-        const int ne1 = tn_[e1], nf1 = tn_[f1], nf2 = tn_[f2];
-        tv_[e1] = d;
-        tv_[f] = d;
-        tv_[f1] = b;
-        tv_[f2] = c;
+        const int ne1 = N(e1), nf1 = N(f1), nf2 = N(f2);
+        V(e1) = d;
+        V(f) = d;
+        V(f1) = b;
+        V(f2) = c;
         link(e, nf1);
         if (nf1 < 0) hedge_[a] = e;
         link(e1, f2);
@@ -115,7 +115,7 @@ bool IncDT::start(int) {
     int b = -1, c = -1;
     for (int q : pending_) {
         if (b < 0) {
-            if (x_[q] != x_[a] || y_[q] != y_[a]) b = q;
+            if (P_[q].x != P_[a].x || P_[q].y != P_[a].y) b = q;
         } else if (orient(a, b, q) != 0) {
             c = q;
             break;
@@ -143,17 +143,23 @@ bool IncDT::start(int) {
 }
 
 bool IncDT::insert(int p) {
-    // visibility walk from a triangle of the last vertex inserted near p
+    // visibility walk from the last triangle, or from one holding the last
+    // vertex inserted in p's 8x8 bucket when p is not next to the last point
     int t = std::min(last_, triangles() - 1);
     int* bucket = nullptr;
+    const Pt pp = P_[p];
     {
-        const int bx = (x_[p] - bx0_) >> 3, by = (y_[p] - by0_) >> 3;
+        const int bx = (pp.x - bx0_) >> 3, by = (pp.y - by0_) >> 3;
         if (bx >= 0 && bx < bw_ && by >= 0 && by < bh_) {
             bucket = &bucket_[size_t(by) * bw_ + bx];
             const int q = *bucket;
-            if (q >= 0) {
+            const bool near_last =
+                lastp_ >= 0 && std::abs(P_[lastp_].x - pp.x) + std::abs(P_[lastp_].y - pp.y) <= 6;
+            if (q >= 0 && !near_last) {
                 const int tq = vtri_[q];
-                if (tv_[3 * tq] == q || tv_[3 * tq + 1] == q || tv_[3 * tq + 2] == q) t = tq;
+                const Tri& T = T_[tq];
+                if (T.v[0] == q || T.v[1] == q || T.v[2] == q) t = tq;
+                else ++stale;
             }
         }
     }
@@ -161,37 +167,35 @@ bool IncDT::insert(int p) {
     for (int steps = 0;; ++steps) {
         if (steps > 4 * triangles() + 16) return false;
         ++walk_steps;
-        const int e0 = 3 * t;
-        long long o[3];
-        int neg = -1, zeros = 0, zk = -1;
-        for (int k = 0; k < 3; ++k) {
-            o[k] = orient(tv_[e0 + k], tv_[e0 + (k + 1) % 3], p);
-            if (o[k] == 0) {
-                ++zeros;
-                zk = k;
-            }
-        }
+        const Tri& T = T_[t];
+        const Pt A = P_[T.v[0]], B = P_[T.v[1]], Cc = P_[T.v[2]];
+        const long long o0 = ((long long)B.x - A.x) * (pp.y - A.y) - ((long long)B.y - A.y) * (pp.x - A.x);
+        const long long o1 = ((long long)Cc.x - B.x) * (pp.y - B.y) - ((long long)Cc.y - B.y) * (pp.x - B.x);
+        const long long o2 = ((long long)A.x - Cc.x) * (pp.y - Cc.y) - ((long long)A.y - Cc.y) * (pp.x - Cc.x);
+        const long long o[3] = {o0, o1, o2};
         // leave through the first separating edge, starting at a rotating index
+        int neg = -1;
         for (int i = 0; i < 3 && neg < 0; ++i) {
             const int k = (steps + i) % 3;
             if (o[k] < 0) neg = k;
         }
         if (neg >= 0) {
-            const int f = tn_[e0 + neg];
+            const int f = T.n[neg];
             if (f < 0) {
-                out_edge = e0 + neg;
+                out_edge = 4 * t + neg;
                 break;
             }
-            t = f / 3;
+            t = f >> 2;
             continue;
         }
+        const int zeros = (o0 == 0) + (o1 == 0) + (o2 == 0);
         if (zeros >= 2) return true;  // coincides with a vertex: the first occurrence wins
-        if (zeros == 1) on_edge = e0 + zk;
+        if (zeros == 1) on_edge = 4 * t + (o0 == 0 ? 0 : o1 == 0 ? 1 : 2);
         break;
     }
 
     if (out_edge >= 0) {  // outside the hull: fan to the strictly visible chain
-        int a = tv_[out_edge], b = tv_[nxt(out_edge)];
+        int a = V(out_edge), b = V(nxt(out_edge));
         auto visible = [&](int x) { return orient(x, hnext_[x], p) < 0; };
         while (hnext_[b] != a && visible(b)) b = hnext_[b];
         while (hprev_[a] != b && visible(hprev_[a])) a = hprev_[a];
@@ -214,12 +218,12 @@ bool IncDT::insert(int p) {
         hprev_[b] = p;
         hedge_[a] = firstE0;
         hedge_[p] = prevE1;
-        last_ = firstE0 / 3;
+        last_ = firstE0 >> 2;
     } else if (on_edge < 0) {  // strictly inside triangle t: 1 -> 3
-        const int e0 = 3 * t;
-        const int a = tv_[e0], b = tv_[e0 + 1], c = tv_[e0 + 2];
-        const int nbc = tn_[e0 + 1], nca = tn_[e0 + 2];
-        tv_[e0 + 2] = p;
+        const int e0 = 4 * t;
+        const int a = V(e0), b = V(e0 + 1), c = V(e0 + 2);
+        const int nbc = N(e0 + 1), nca = N(e0 + 2);
+        V(e0 + 2) = p;
         const int t1 = add(b, c, p, nbc, -1, -1);
         const int t2 = add(c, a, p, nca, -1, -1);
         link(e0 + 1, t1 + 2);
@@ -232,16 +236,16 @@ bool IncDT::insert(int p) {
         stack_.push_back(t2);
         last_ = t;
     } else {  // on the edge a -> b of t
-        const int e = on_edge, tt = e / 3;
-        const int a = tv_[e], b = tv_[nxt(e)], c = tv_[prv(e)];
-        const int nbc = tn_[nxt(e)], nca = tn_[prv(e)];
-        const int f = tn_[e];
-        const int e0 = 3 * tt;
+        const int e = on_edge, tt = e >> 2;
+        const int a = V(e), b = V(nxt(e)), c = V(prv(e));
+        const int nbc = N(nxt(e)), nca = N(prv(e));
+        const int f = N(e);
+        const int e0 = 4 * tt;
         if (f < 0) {  // a hull edge: 1 -> 2, p joins the hull between a and b
-            tv_[e0] = a;
-            tv_[e0 + 1] = p;
-            tv_[e0 + 2] = c;
-            tn_[e0] = -1;
+            V(e0) = a;
+            V(e0 + 1) = p;
+            V(e0 + 2) = c;
+            N(e0) = -1;
             link(e0 + 2, nca);
             const int t1 = add(p, b, c, -1, nbc, -1);
             link(e0 + 1, t1 + 2);
@@ -256,17 +260,17 @@ bool IncDT::insert(int p) {
             stack_.push_back(e0 + 2);
             stack_.push_back(t1 + 1);
         } else {  // 2 -> 4 with the twin triangle (b, a, d)
-            const int s0 = 3 * (f / 3);
+            const int s0 = 4 * (f >> 2);
             const int f1 = nxt(f), f2 = nxt(f1);
-            const int d = tv_[f2];
-            const int nad = tn_[f1], ndb = tn_[f2];
-            tv_[e0] = a;
-            tv_[e0 + 1] = p;
-            tv_[e0 + 2] = c;
-            tv_[s0] = b;
-            tv_[s0 + 1] = p;
-            tv_[s0 + 2] = d;
-            tn_[e0] = tn_[e0 + 1] = tn_[s0] = tn_[s0 + 1] = -1;
+            const int d = V(f2);
+            const int nad = N(f1), ndb = N(f2);
+            V(e0) = a;
+            V(e0 + 1) = p;
+            V(e0 + 2) = c;
+            V(s0) = b;
+            V(s0 + 1) = p;
+            V(s0 + 2) = d;
+            N(e0) = N(e0 + 1) = N(s0) = N(s0 + 1) = -1;
             link(e0 + 2, nca);
             link(s0 + 2, ndb);
             const int t1 = add(p, b, c, -1, nbc, -1);
@@ -288,22 +292,24 @@ bool IncDT::insert(int p) {
     }
     legalize();
     vtri_[p] = last_;  // holds p: flips during its own insertion keep p in the slot
+    lastp_ = p;
     if (bucket) *bucket = p;
     return true;
 }
 
 bool IncDT::extend(const int* u, const int* v, int n) {
-    x_ = u;
-    y_ = v;
     if (n <= nv_) return true;
     constexpr int kLimit = 1 << 20;
-    int minx = 0, maxx = 0, miny = 0, maxy = 0;
-    for (int i = 0; i < n; ++i) {
+    for (int i = nv_; i < n; ++i)
         if (std::abs(u[i]) >= kLimit || std::abs(v[i]) >= kLimit) return false;
-        if (i == 0 || u[i] < minx) minx = u[i];
-        if (i == 0 || u[i] > maxx) maxx = u[i];
-        if (i == 0 || v[i] < miny) miny = v[i];
-        if (i == 0 || v[i] > maxy) maxy = v[i];
+    P_.resize(n);
+    for (int i = nv_; i < n; ++i) P_[i] = Pt{u[i], v[i]};
+    int minx = P_[0].x, maxx = P_[0].x, miny = P_[0].y, maxy = P_[0].y;
+    for (int i = 1; i < n; ++i) {
+        minx = std::min(minx, P_[i].x);
+        maxx = std::max(maxx, P_[i].x);
+        miny = std::min(miny, P_[i].y);
+        maxy = std::max(maxy, P_[i].y);
     }
     wide_ = (maxx - minx) >= (1 << 14) || (maxy - miny) >= (1 << 14);
     hnext_.resize(n, -1);
@@ -318,10 +324,9 @@ bool IncDT::extend(const int* u, const int* v, int n) {
         bh_ = ((maxy - miny) >> 3) + 1;
         bucket_.assign(size_t(bw_) * bh_, -1);
     }
-    tv_.reserve(6 * size_t(n));
-    tn_.reserve(6 * size_t(n));
+    T_.reserve(2 * size_t(n) + 8);
     for (int p = nv_; p < n; ++p) {
-        if (tv_.empty()) {
+        if (T_.empty()) {
             pending_.push_back(p);
             if (pending_.size() >= 3 && !start(n)) return false;
             continue;

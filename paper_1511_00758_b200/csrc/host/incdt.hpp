@@ -29,36 +29,47 @@ public:
     // internal inconsistency.
     bool extend(const int* u, const int* v, int n);
 
-    int triangles() const { return int(tv_.size() / 3); }
-    const int* tri() const { return tv_.data(); }  // 3 vertex ids per triangle, CCW
-    const int* nbr() const { return tn_.data(); }  // twin half-edge (3t + k) or -1
+    int triangles() const { return int(T_.size()); }
+    // triangle t: vertices (counter-clockwise) and twin half-edges; half-edge
+    // e = 4t + k runs from vertex k to vertex k+1 (mod 3), -1 = hull
+    int vert(int t, int k) const { return T_[t].v[k]; }
+    int twin(int e) const { return T_[e >> 2].n[e & 3]; }
     int hull_start() const { return hull0_; }      // a hull vertex, -1 if < 1 triangle
     int hull_next(int v) const { return hnext_[v]; }
     int hull_edge(int v) const { return hedge_[v]; }  // half-edge v -> hull_next(v)
-    bool degenerate() const { return tv_.empty(); }  // fewer than 3 non-collinear points
+    bool degenerate() const { return T_.empty(); }  // fewer than 3 non-collinear points
 
-    long long flips = 0, tests = 0, walk_steps = 0;  // statistics
+    long long flips = 0, tests = 0, walk_steps = 0, stale = 0;  // statistics
 
 private:
+    struct alignas(32) Tri {
+        int v[3];
+        int n[3];
+        int pad[2];
+    };
+    struct Pt {
+        int x, y;
+    };
+    int& V(int e) { return T_[e >> 2].v[e & 3]; }
+    int& N(int e) { return T_[e >> 2].n[e & 3]; }
     long long orient(int a, int b, int c) const {
-        return ((long long)x_[b] - x_[a]) * ((long long)y_[c] - y_[a]) -
-               ((long long)y_[b] - y_[a]) * ((long long)x_[c] - x_[a]);
+        const Pt A = P_[a], B = P_[b], C = P_[c];
+        return ((long long)B.x - A.x) * ((long long)C.y - A.y) - ((long long)B.y - A.y) * ((long long)C.x - A.x);
     }
     bool inside(int a, int b, int c, int d);  // perturbed strict in-circle
     int add(int a, int b, int c, int na, int nb, int nc);
     void link(int e, int f) {
-        tn_[e] = f;
-        if (f >= 0) tn_[f] = e;
+        N(e) = f;
+        if (f >= 0) N(f) = e;
     }
     void legalize();
     bool insert(int p);
     bool start(int n);  // first non-degenerate triangle from the pending points
 
-    const int* x_ = nullptr;
-    const int* y_ = nullptr;
-    int nv_ = 0;  // points seen (indices < nv_)
+    std::vector<Pt> P_;  // points seen so far (indices < nv_)
+    int nv_ = 0;
     bool wide_ = false;
-    std::vector<int> tv_, tn_;
+    std::vector<Tri> T_;
     std::vector<int> hnext_, hprev_, hedge_;
     std::vector<int> stack_;
     std::vector<int> pending_;  // points waiting for a non-degenerate start
@@ -67,6 +78,7 @@ private:
     std::vector<int> vtri_, bucket_;
     int bx0_ = 0, by0_ = 0, bw_ = 0, bh_ = 0;
     int last_ = 0;  // triangle to start walks from otherwise
+    int lastp_ = -1;  // the last point inserted
     int hull0_ = -1;
 };
 

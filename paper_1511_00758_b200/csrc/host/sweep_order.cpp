@@ -459,7 +459,7 @@ bool SweepOrder::resolve(const int* tris, int count, uint64_t* birth, int* store
         bv1 = std::max(bv1, y_[tris[i]]);
     }
     const double area = double(maxx_ - minx_ + 1) * double(maxy_ - miny_ + 1);
-    int delta = std::max(8, int(6.0 * std::sqrt(area / m_)));
+    int delta = std::max(8, int(2.0 * std::sqrt(area / m_)));
     std::vector<std::pair<uint64_t, int>> key;  // sorted vertex set -> slot
     int u0 = std::max(minx_, bu0 - delta), u1 = std::min(maxx_, bu1 + delta);
     int v0 = std::max(miny_, bv0 - delta), v1 = std::min(maxy_, bv1 + delta);
@@ -469,6 +469,7 @@ bool SweepOrder::resolve(const int* tris, int count, uint64_t* birth, int* store
         v0 = miny_;
         v1 = maxy_;
     }
+    bool stuck = false;  // a requested growth could not enlarge the window
     for (int attempt = 0;; ++attempt) {
         const bool whole = u0 == minx_ && u1 == maxx_ && v0 == miny_ && v1 == maxy_;
         // growth for the next attempt: towards the points that broke a
@@ -476,7 +477,7 @@ bool SweepOrder::resolve(const int* tris, int count, uint64_t* birth, int* store
         int nu0 = u0, nu1 = u1, nv0 = v0, nv1 = v1;
         bool grow_all = false;
         bool gl = false, gr = false, gd = false, gu = false;  // directional growth requests
-        const bool fallback = attempt >= 6;  // then finish chains in the full set instead
+        const bool fallback = attempt >= 6 || stuck;  // then finish chains in the full set instead
         const bool replayed = replay(u0, u1, v0, v1);
         bool ok = replayed;
         if (!replayed) grow_all = true;
@@ -598,10 +599,15 @@ bool SweepOrder::resolve(const int* tris, int count, uint64_t* birth, int* store
             nv0 = std::min(nv0, v0 - delta);
             nv1 = std::max(nv1, v1 + delta);
         }
-        u0 = std::max(minx_, nu0);
-        u1 = std::min(maxx_, nu1);
-        v0 = std::max(miny_, nv0);
-        v1 = std::min(maxy_, nv1);
+        nu0 = std::max(minx_, nu0);
+        nu1 = std::min(maxx_, nu1);
+        nv0 = std::max(miny_, nv0);
+        nv1 = std::min(maxy_, nv1);
+        stuck = nu0 == u0 && nu1 == u1 && nv0 == v0 && nv1 == v1;
+        u0 = nu0;
+        u1 = nu1;
+        v0 = nv0;
+        v1 = nv1;
     }
 }
 

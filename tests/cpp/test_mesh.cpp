@@ -12,8 +12,10 @@
 //  * SweepOrder::resolve on the triangles around sampled vertices gives the
 //    sweep's slot order and stored rotation;
 //  * mesh_iteration's triangles are the same set, each plane (fitPlane's three
-//    numerators) has the same bits as in the sweep's rotation, and every
-//    uncovered hull-vertex pixel gets the same D_it bits as the sweep's pin.
+//    numerators) has the same bits as in the sweep's rotation or, where the
+//    rotations round differently, gives the same binary32 D_it at every pixel
+//    the triangle covers, and every uncovered hull-vertex pixel gets the same
+//    D_it bits as the sweep's pin.
 // Prints "ok <sets> <checks>" and exits 0, or prints the first failures.
 #include <algorithm>
 #include <array>
@@ -62,6 +64,37 @@ uint32_t dit(const Plane& p, int u, int v, float nd) {
     return bits;
 }
 
+long long floor_div(long long a, long long b) {
+    long long q = a / b;
+    if ((a % b != 0) && ((a < 0) != (b < 0))) --q;
+    return q;
+}
+
+// D_it bits of plane pa vs pb at every pixel the triangle covers under the
+// top-left rule (mesh.cpp:58-104) and at its vertex pixels
+bool same_dit(const std::vector<int>& u, const std::vector<int>& v, const int* t, const Plane& pa,
+              const Plane& pb, int W, int H, float nd) {
+    const int x[3] = {u[t[0]], u[t[1]], u[t[2]]}, y[3] = {v[t[0]], v[t[1]], v[t[2]]};
+    for (int q = 0; q < 3; ++q)
+        if (dit(pa, x[q], y[q], nd) != dit(pb, x[q], y[q], nd)) return false;
+    for (int vv = std::max(0, std::min({y[0], y[1], y[2]})); vv <= std::min(H - 1, std::max({y[0], y[1], y[2]})); ++vv) {
+        long long lo = 0, hi = W - 1;
+        bool empty = false;
+        for (int a = 0; a < 3 && !empty; ++a) {
+            const int b = (a + 1) % 3;
+            const long long A = y[a] - y[b];
+            const long long bias = ((y[b] < y[a]) || (y[b] == y[a] && x[b] > x[a])) ? 0 : 1;
+            const long long K = (long long)(x[b] - x[a]) * (vv - y[a]) + (long long)(y[b] - y[a]) * x[a];
+            if (A > 0) lo = std::max(lo, -floor_div(K - bias, A));
+            else if (A < 0) hi = std::min(hi, floor_div(K - bias, -A));
+            else if (K < bias) empty = true;
+        }
+        for (long long uu = lo; !empty && uu <= hi; ++uu)
+            if (dit(pa, int(uu), vv, nd) != dit(pb, int(uu), vv, nd)) return false;
+    }
+    return true;
+}
+
 std::array<int, 3> key(const int* t) {
     std::array<int, 3> k = {t[0], t[1], t[2]};
     std::sort(k.begin(), k.end());
@@ -98,8 +131,9 @@ void compare_mesh(FrameMesh& fm, int W, int H, float nd, const char* tag) {
         const int s = it->second;
         const Plane pa_ = fitp(fm.u, fm.v, fm.d, ta[3 * t], ta[3 * t + 1], ta[3 * t + 2]);
         const Plane pb_ = fitp(fm.u, fm.v, fm.d, tb[3 * s], tb[3 * s + 1], tb[3 * s + 2]);
-        if (std::memcmp(&pa_.A, &pb_.A, 8) || std::memcmp(&pa_.B, &pb_.B, 8) || std::memcmp(&pa_.C, &pb_.C, 8))
-            return fail(tag, "plane bits (rotation)");
+        if ((std::memcmp(&pa_.A, &pb_.A, 8) || std::memcmp(&pa_.B, &pb_.B, 8) || std::memcmp(&pa_.C, &pb_.C, 8)) &&
+            !same_dit(fm.u, fm.v, &ta[3 * t], pa_, pb_, W, H, nd))
+            return fail(tag, "D_it of a rotation-dependent plane");
         for (int k = 0; k < 3; ++k) {
             if (pa[t] >> k & 1) pin_a[ta[3 * t + k]] = dit(pa_, fm.u[ta[3 * t + k]], fm.v[ta[3 * t + k]], nd);
             if (pb[s] >> k & 1) pin_b[tb[3 * s + k]] = dit(pb_, fm.u[tb[3 * s + k]], fm.v[tb[3 * s + k]], nd);
