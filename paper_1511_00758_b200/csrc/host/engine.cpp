@@ -196,10 +196,11 @@ Engine::~Engine() {
         if (b->p) cudaFreeHost(b->p);
     for (FrameGroup& g : groups_) {
         for (DevBuf* b : {&g.dTri, &g.dTriOff, &g.dPlanes, &g.dPack, &g.dPackD, &g.dPackOff,
-                          &g.dSprev, &g.dChunk, &g.dPin})
+                          &g.dSprev, &g.dChunk, &g.dPin, &g.dCellCnt, &g.dCellStart, &g.dCellItems,
+                          &g.dDup, &g.dPinTri, &g.dTriCount, &g.dFlags, &g.dFix, &g.dColKey, &g.dColIdx, &g.dHull, &g.dHullTmp, &g.dHard})
             if (b->p) cudaFree(b->p);
         for (HostBuf* b : {&g.hS, &g.hSprev, &g.hPackOff, &g.hPack, &g.hPackD, &g.hTri, &g.hTriOff,
-                           &g.hPin})
+                           &g.hPin, &g.hTriCount, &g.hFlags, &g.hFix})
             if (b->p) cudaFreeHost(b->p);
         if (g.st) cudaStreamDestroy(g.st);
         if (g.done_event) cudaEventDestroy(g.done_event);
@@ -489,8 +490,14 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     double host_dt_ms = 0.0;
     // per-frame mesh state, kept across the iterations of this run (the
     // triangulation is extended, not rebuilt: frame_mesh.hpp)
+    // Mesh: on the device (kernels/star.cu) by default; PS_DELAUNAY=host runs
+    // the host incremental path (frame_mesh.cpp), =lex replays the reference
+    // sweep for every frame-iteration.  The device predicates are int64: the
+    // frame must span < 2^14 pixels.
     const char* dt_mode = std::getenv("PS_DELAUNAY");
     const bool lex_only = dt_mode && std::string(dt_mode) == "lex";
+    const bool device_dt = !(dt_mode && (std::string(dt_mode) == "host" || lex_only)) &&
+                           W < (1 << 14) && H < (1 << 14);
     if (int(fmesh_.size()) < F) fmesh_.resize(F);
     for (int f = 0; f < F; ++f) {
         fmesh_[f].reset();
@@ -509,6 +516,16 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     // triangulate continuously while the device runs other groups' stages.
     const int G = std::max(1, std::min(std::min(kMaxGroups, max_groups_), (F + 31) / 32));
     const int tri_cap = int(std::min<long long>(2ll * scap_ + 8, 2ll * P + 8));  // T <= 2S per frame
+    // device mesh grid of iteration `it` (1-based): ~1-3 supports per cell —
+    // seeds: <= 120 * cap over the frame; later: at most ~2 per cell of the
+    // previous iteration's occupancy grid (plus the older, sparser supports)
+    // ~1.3 supports per cell, so the 5x5 cells a star starts from hold ~30
+    // candidates (star_dt.cuh kLocalMax); est = expected supports per frame
+    auto star_gs = [&](double est) {
+        return std::max(2, int(std::sqrt(1.3 * double(P) / std::max(1.0, est)) + 0.5));
+    };
+    const long long star_cells_max = (long long)((W - 1) / 2 + 1) * ((H - 1) / 2 + 1);  // gs >= 2
+    const int star_budget = std::getenv("PS_STAR_BUDGET") ? std::atoi(std::getenv("PS_STAR_BUDGET")) : 0;
     cudaMemsetAsync(dErr, 0, sizeof(int), st_);
     ps_status s = check(cudaEventRecord(start_event_, st_), "start event");
     if (s != PS_OK) return s;
@@ -518,6 +535,55 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     // before the dataflow loop, the others from inside it (one per loop turn),
     // so the first host tasks do not wait for the launches of every group.
     for (int gi = 0; gi < G; ++gi) groups_[gi].phase = FrameGroup::kIdle;
+    // Device mesh of iteration `it` for the group's current supports (grp.S),
+    // then its triangle counts and flag records to the host (star.cu).
+    auto star_args = [&](FrameGroup& grp) {
+        StarArgs a{};
+        const size_t f0 = size_t(grp.f0);
+        a.su = dSu + f0 * scap_;
+        a.sv = dSv + f0 * scap_;
+        a.sd = dSd + f0 * scap_;
+        a.scap = scap_;
+        a.S = grp.S;
+        a.frames = grp.n;
+        a.W = W;
+        a.H = H;
+        a.max_disp = float(cfg.max_disparity);
+        a.gs = grp.gs;
+        a.gw = grp.gw;
+        a.gh = grp.gh;
+        a.cell_cnt = static_cast<int*>(grp.dCellCnt.p);
+        a.cell_start = static_cast<int*>(grp.dCellStart.p);
+        a.cell_items = static_cast<int*>(grp.dCellItems.p);
+        a.dup = static_cast<uint8_t*>(grp.dDup.p);
+        a.pin_tri = static_cast<int*>(grp.dPinTri.p);
+        a.tris = static_cast<int*>(grp.dTri.p);
+        a.pitch = tri_cap;
+        a.pins = static_cast<uint8_t*>(grp.dPin.p);
+        a.tri_count = static_cast<int*>(grp.dTriCount.p);
+        a.flags = static_cast<int*>(grp.dFlags.p);
+        a.col_key = static_cast<unsigned long long*>(grp.dColKey.p);
+        a.col_idx = static_cast<int*>(grp.dColIdx.p);
+        a.hull = static_cast<int*>(grp.dHull.p);
+        a.hull_tmp = static_cast<int*>(grp.dHullTmp.p);
+        a.hard = static_cast<int*>(grp.dHard.p);
+        a.budget = star_budget;
+        return a;
+    };
+    auto enqueue_mesh = [&](FrameGroup& grp, double est, int max_points) {
+        grp.gs = star_gs(est);
+        grp.gw = (W - 1) / grp.gs + 1;
+        grp.gh = (H - 1) / grp.gs + 1;
+        const StarArgs a = star_args(grp);
+        cudaStream_t gs = grp.st;
+        begin_kernel("star_mesh", 0.0, gs);
+        launches_ += launch_star_mesh(a, std::min(max_points, scap_), gs);
+        launches_ += launch_star_check(a, tri_cap, gs);
+        end_kernel(gs);
+        cudaMemcpyAsync(grp.hTriCount.p, grp.dTriCount.p, sizeof(int) * grp.n, cudaMemcpyDeviceToHost, gs);
+        cudaMemcpyAsync(grp.hFlags.p, grp.dFlags.p, sizeof(int) * size_t(grp.n) * kStarFlagInts,
+                        cudaMemcpyDeviceToHost, gs);
+    };
     auto seed_group = [&](int gi) -> ps_status {
         FrameGroup& grp = groups_[gi];
         grp.f0 = int((long long)F * gi / G);
@@ -539,6 +605,22 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
             return fail(PS_CUDA_ERROR, "allocation failed (group staging)");
         }
         if (!grp.done_event) cudaEventCreateWithFlags(&grp.done_event, cudaEventDisableTiming);
+        grp.fixes.assign(grp.n, {});
+        grp.replayed.assign(grp.n, 0);
+        if (device_dt) {
+            const size_t nn = size_t(grp.n);
+            if (!dev<int>(grp.dCellCnt, nn * star_cells_max) || !dev<int>(grp.dCellStart, nn * (star_cells_max + 1)) ||
+                !dev<int>(grp.dCellItems, nn * scap_) || !dev<uint8_t>(grp.dDup, nn * scap_) ||
+                !dev<int>(grp.dPinTri, nn * scap_ * 3) || !dev<int>(grp.dTriCount, nn) ||
+                !dev<int>(grp.dFlags, nn * kStarFlagInts) || !dev<int>(grp.dTri, nn * tri_cap * 3) ||
+                !dev<uint8_t>(grp.dPin, nn * tri_cap) || !host<int>(grp.hTriCount, nn) ||
+                !host<int>(grp.hFlags, nn * kStarFlagInts) || !host<int>(grp.hFix, nn * 6 * 96) ||
+                !dev<int>(grp.dFix, nn * 6 * 96) ||
+                !dev<unsigned long long>(grp.dColKey, nn * 2 * W) || !dev<int>(grp.dColIdx, nn * 2 * W) ||
+                !dev<int>(grp.dHull, nn * 2 * scap_) || !dev<int>(grp.dHullTmp, nn * 8 * (2 * size_t(W) + 2 * size_t(H) + 8)) ||
+                !dev<int>(grp.dHard, nn * scap_))
+                return fail(PS_CUDA_ERROR, "allocation failed (device mesh)");
+        }
 
         // ---- seeding of the group's frames on the (low-priority) seeding
         // stream, in group order: group 0's seeds, and so the first host
@@ -597,6 +679,11 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         // the group's own stream continues after its seeding
         if (s == PS_OK) s = check(cudaStreamWaitEvent(grp.st, grp.done_event, 0), "group order");
         if (s != PS_OK) return s;
+        if (device_dt) {  // the first iteration's mesh, on the group stream
+            enqueue_mesh(grp, 0.75 * cand_stride, cand_stride);  // ~75% of the candidates match
+            s = check(cudaEventRecord(grp.done_event, grp.st), "mesh event");
+            if (s != PS_OK) return s;
+        }
         grp.phase = FrameGroup::kSeed;
         return PS_OK;
     };
@@ -726,8 +813,25 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                     int* slot = static_cast<int*>(g2.hTri.p) + size_t(i) * tri_cap * 3;
                     uint8_t* pins = static_cast<uint8_t*>(g2.hPin.p) + size_t(i) * tri_cap;
                     const double ts0 = now_ms();
-                    t = mesh_iteration(fm, W, H, float(cfg.max_disparity), slot, tri_cap, pins, w,
-                                       mstats[worker]);
+                    if (device_dt) {
+                        // the device meshed the frame; resolve what it listed
+                        const int* fl = static_cast<const int*>(g2.hFlags.p) + size_t(i) * kStarFlagInts;
+                        t = static_cast<const int*>(g2.hTriCount.p)[i];
+                        bool rep = fl[0] != 0 || t > tri_cap;
+                        g2.fixes[i].clear();
+                        g2.replayed[i] = 0;
+                        if (!rep && (fl[1] > 0 || fl[3] > 0))
+                            rep = !resolve_device_flags(fm, fl, i, W, H, float(cfg.max_disparity),
+                                                        g2.fixes[i], w, mstats[worker]);
+                        if (rep) {
+                            g2.fixes[i].clear();
+                            g2.replayed[i] = 1;
+                            t = replay_mesh(fm, W, H, slot, tri_cap, pins, w, mstats[worker]);
+                        }
+                    } else {
+                        t = mesh_iteration(fm, W, H, float(cfg.max_disparity), slot, tri_cap, pins, w,
+                                           mstats[worker]);
+                    }
                     add_ms(sweep_ms_sum, now_ms() - ts0);
                     if (t < 0) {
                         status_[f] = PS_ERROR;
@@ -770,17 +874,45 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
             total_tri += grp.ntri[i];
         }
         hTriOff[n] = int(total_tri);
-        // one pitched copy per group: frame i's triangles at i * pitch
+        // frame i's triangles at i * pitch: one pitched copy per group from
+        // the host mesh, or the device mesh in place (+ host fixes / replays)
         int max_nt = 1;
         for (int i = 0; i < n; ++i) max_nt = std::max(max_nt, grp.ntri[i]);
-        const size_t pitch = size_t(max_nt);
+        const size_t pitch = device_dt ? size_t(tri_cap) : size_t(max_nt);
         int* dTri = dev<int>(grp.dTri, size_t(n) * pitch * 3);
         uint8_t* dPin = dev<uint8_t>(grp.dPin, size_t(n) * pitch);
         int* dTriOff = static_cast<int*>(grp.dTriOff.p);
         if (!dTri || !dPin) return fail(PS_CUDA_ERROR, "allocation failed (triangles)");
         ps_status r = PS_OK;
         begin_kernel("h2d_triangles", 13.0 * double(pitch) * n, gs);
-        if (total_tri > 0) {
+        if (device_dt) {
+            int n_fix = 0;
+            for (int i = 0; i < n; ++i) n_fix += int(grp.fixes[i].size() / 6);
+            int* hfix = host<int>(grp.hFix, size_t(std::max(n_fix, 1)) * 6);
+            int* dfix = dev<int>(grp.dFix, size_t(std::max(n_fix, 1)) * 6);
+            if (!hfix || !dfix) return fail(PS_CUDA_ERROR, "allocation failed (mesh fixes)");
+            size_t at = 0;
+            for (int i = 0; i < n; ++i) {
+                std::copy(grp.fixes[i].begin(), grp.fixes[i].end(), hfix + at);
+                at += grp.fixes[i].size();
+            }
+            if (n_fix > 0)
+                r = check(cudaMemcpyAsync(dfix, hfix, sizeof(int) * 6 * n_fix, cudaMemcpyHostToDevice, gs),
+                          "H2D mesh fixes");
+            const StarArgs a = star_args(grp);
+            launches_ += launch_star_finish(a, dfix, n_fix, tri_cap, gs);
+            // frames the host replayed: their triangles and pins replace the device's
+            for (int i = 0; i < n && r == PS_OK; ++i) {
+                if (!grp.replayed[i] || grp.ntri[i] <= 0) continue;
+                r = check(cudaMemcpyAsync(dTri + size_t(i) * pitch * 3,
+                                          static_cast<int*>(grp.hTri.p) + size_t(i) * tri_cap * 3,
+                                          size_t(grp.ntri[i]) * 12, cudaMemcpyHostToDevice, gs), "H2D replay");
+                if (r == PS_OK)
+                    r = check(cudaMemcpyAsync(dPin + size_t(i) * pitch,
+                                              static_cast<uint8_t*>(grp.hPin.p) + size_t(i) * tri_cap,
+                                              size_t(grp.ntri[i]), cudaMemcpyHostToDevice, gs), "H2D replay pins");
+            }
+        } else if (total_tri > 0) {
             r = check(cudaMemcpy2DAsync(dTri, pitch * 12, grp.hTri.p, size_t(tri_cap) * 12, pitch * 12, n,
                                         cudaMemcpyHostToDevice, gs), "H2D triangles");
             if (r == PS_OK)
@@ -884,6 +1016,16 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                                              scap_, grp.S, dConf + f0, grp.Snext, chunk, gs);
             end_kernel(gs);
             std::swap(grp.S, grp.Snext);
+            if (device_dt) {  // the next iteration's mesh, as soon as its supports exist
+                int max_s = 0;
+                double mean_s = 0.0;
+                for (int i = 0; i < n; ++i) {
+                    max_s = std::max(max_s, hs[i]);
+                    mean_s += hs[i];
+                }
+                // resampling adds at most 2 supports per cell (~1.5 measured)
+                enqueue_mesh(grp, mean_s / std::max(1, n) + 1.1 * cells, max_s + 2 * cells);
+            }
         }
         if (serial_device_) {
             cudaEventRecord(chain_event_, gs);

@@ -59,6 +59,12 @@ struct FrameGroup {
     DevBuf dTri, dTriOff, dPlanes, dPack, dPackD, dPackOff, dSprev, dChunk, dPin;
     HostBuf hS, hSprev, hPackOff, hPack, hPackD, hTri, hTriOff, hPin;
     std::vector<int> ntri;
+    // device mesh (kernels/star.cu): grid scratch, pin choices, flags, fixes
+    DevBuf dCellCnt, dCellStart, dCellItems, dDup, dPinTri, dTriCount, dFlags, dFix, dColKey, dColIdx, dHull, dHullTmp, dHard;
+    HostBuf hTriCount, hFlags, hFix;
+    std::vector<std::vector<int>> fixes;  // per frame: host fixes for the device mesh
+    std::vector<uint8_t> replayed;        // per frame: triangles came from the host replay
+    int gs = 0, gw = 0, gh = 0;           // grid of the mesh in flight
     double millis = 0.0;
 };
 

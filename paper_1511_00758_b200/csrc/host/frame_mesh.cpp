@@ -2,6 +2,7 @@
 #include "frame_mesh.hpp"
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -119,6 +120,125 @@ int replay(FrameMesh& fm, int width, int height, int* tris, int cap, uint8_t* pi
 }
 
 }  // namespace
+
+int replay_mesh(FrameMesh& fm, int width, int height, int* tris, int cap, uint8_t* pins,
+                DelaunayWorkspace& ws, MeshStats& st) {
+    return replay(fm, width, height, tris, cap, pins, ws, st);
+}
+
+bool resolve_device_flags(FrameMesh& fm, const int* flags, int frame, int width, int height,
+                          float max_disparity, std::vector<int>& fixes, DelaunayWorkspace& ws,
+                          MeshStats& st) {
+    ++st.frames;
+    const int n = int(fm.u.size());
+    const int n_sus = flags[1];
+    const int n_amb = flags[3];
+    const int* sus = flags + 8;  // kStarSuspectBase
+    const int* fan = flags + 8 + 4 * 64;  // kStarFanBase
+    bool have_order = false;
+    auto build_order = [&] {
+        if (have_order) return;
+        int minx, miny, m, spanx, spany;
+        lex_order(fm.u.data(), fm.v.data(), n, ws, minx, miny, m, spanx, spany);
+        fm.ranks.assign(ws.kept.begin(), ws.kept.begin() + m);
+        fm.rank_of.assign(n, -1);
+        fm.px.resize(m);
+        fm.py.resize(m);
+        for (int r = 0; r < m; ++r) {
+            fm.rank_of[fm.ranks[r]] = r;
+            fm.px[r] = fm.u[fm.ranks[r]];
+            fm.py[r] = fm.v[fm.ranks[r]];
+        }
+        fm.so.init(fm.px.data(), fm.py.data(), m);
+        have_order = true;
+    };
+    auto sorted3 = [](int a, int b, int c) {
+        if (a > b) std::swap(a, b);
+        if (b > c) std::swap(b, c);
+        if (a > b) std::swap(a, b);
+        return std::array<int, 3>{a, b, c};
+    };
+    int queries = 0;
+    // (2) rotation suspects: does any covered pixel see the difference?
+    std::vector<std::pair<std::array<int, 3>, std::array<int, 3>>> rotated;  // vertex set -> stored order
+    for (int q = 0; q < n_sus; ++q) {
+        const int t = sus[4 * q], i = sus[4 * q + 1], j = sus[4 * q + 2], k = sus[4 * q + 3];
+        if (i < 0 || j < 0 || k < 0 || i >= n || j >= n || k >= n) return false;
+        ++st.rot_checked;
+        const Fit f3[3] = {fit(fm, i, j, k), fit(fm, j, k, i), fit(fm, k, i, j)};
+        if (rotations_equivalent(fm, i, j, k, f3, width, height, max_disparity)) continue;
+        if (++queries > kMaxQueries) return false;
+        const double to = now_ms();
+        build_order();
+        int r3[3] = {fm.rank_of[i], fm.rank_of[j], fm.rank_of[k]};
+        uint64_t b;
+        int s3[3];
+        const bool ok = fm.so.resolve(r3, 1, &b, s3);
+        st.order_ms += now_ms() - to;
+        if (!ok) return false;
+        const int v0 = fm.ranks[s3[0]], v1 = fm.ranks[s3[1]], v2 = fm.ranks[s3[2]];
+        fixes.insert(fixes.end(), {frame, 0, t, v0, v1, v2});
+        rotated.push_back({sorted3(i, j, k), {v0, v1, v2}});
+        ++st.rotations;
+    }
+    // (3) ambiguous hull vertices: the incident triangle the sweep stored first
+    for (int a = 0, at = 0; a < n_amb; ++a) {
+        const int h = fan[at], cnt = fan[at + 1];
+        const int* tr = fan + at + 2;
+        at += 2 + 3 * cnt;
+        if (h < 0 || h >= n || cnt <= 0) return false;
+        std::vector<std::array<int, 3>> inc(cnt);
+        uint32_t first = 0;
+        bool agree = true;
+        for (int i = 0; i < cnt; ++i) {
+            int x = tr[3 * i], y = tr[3 * i + 1], z = tr[3 * i + 2];
+            // stored rotation: the host's fix, else the device's (smallest first)
+            std::array<int, 3> key = sorted3(x, y, z), order;
+            bool found = false;
+            for (const auto& rr : rotated)
+                if (rr.first == key) {
+                    order = rr.second;
+                    found = true;
+                }
+            if (!found) {
+                while (!(x < y && x < z)) {
+                    const int tmp = x;
+                    x = y;
+                    y = z;
+                    z = tmp;
+                }
+                order = {x, y, z};
+            }
+            inc[i] = order;
+            const uint32_t bits = dit_bits(fit(fm, order[0], order[1], order[2]), fm.u[h], fm.v[h], max_disparity);
+            if (i == 0) first = bits;
+            else if (bits != first) agree = false;
+        }
+        int pick = 0;
+        if (!agree) {
+            if (++queries > kMaxQueries) return false;
+            const double to = now_ms();
+            build_order();
+            std::vector<int> r3(3 * size_t(cnt)), s3(3 * size_t(cnt));
+            fm.birth.resize(cnt);
+            for (int i = 0; i < cnt; ++i) {
+                // counter-clockwise as the device wrote it (the set is what matters)
+                r3[3 * i] = fm.rank_of[tr[3 * i]];
+                r3[3 * i + 1] = fm.rank_of[tr[3 * i + 1]];
+                r3[3 * i + 2] = fm.rank_of[tr[3 * i + 2]];
+            }
+            const bool ok = fm.so.resolve(r3.data(), cnt, fm.birth.data(), s3.data());
+            st.order_ms += now_ms() - to;
+            if (!ok) return false;
+            for (int i = 1; i < cnt; ++i)
+                if (fm.birth[i] < fm.birth[pick]) pick = i;
+            ++st.ambiguous;
+        }
+        const auto s = sorted3(inc[pick][0], inc[pick][1], inc[pick][2]);
+        fixes.insert(fixes.end(), {frame, 1, h, s[0], s[1], s[2]});
+    }
+    return true;
+}
 
 int mesh_iteration(FrameMesh& fm, int width, int height, float max_disparity, int* tris, int cap,
                    uint8_t* pins, DelaunayWorkspace& ws, MeshStats& st) {

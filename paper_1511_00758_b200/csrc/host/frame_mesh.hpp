@@ -64,4 +64,19 @@ struct FrameMesh {
 int mesh_iteration(FrameMesh& fm, int width, int height, float max_disparity, int* tris, int cap,
                    uint8_t* pins, DelaunayWorkspace& ws, MeshStats& st);
 
+// Host side of the device mesh (kernels/star.cu): the frame's flag record
+// (kStarFlagInts ints: rotation suspects and ambiguous hull vertices, see
+// launch.hpp) is resolved into fixes appended to `fixes` as
+// {frame, 0, triangle, v0, v1, v2} (the sweep's stored rotation) and
+// {frame, 1, vertex, s0, s1, s2} (the pinned triangle's sorted vertex set).
+// Returns false when the frame should be replayed instead (query budget or
+// an inconsistency).
+bool resolve_device_flags(FrameMesh& fm, const int* flags, int frame, int width, int height,
+                          float max_disparity, std::vector<int>& fixes, DelaunayWorkspace& ws,
+                          MeshStats& st);
+
+// The exact replay (delaunay_lex + the sweep's pins) into caller buffers.
+int replay_mesh(FrameMesh& fm, int width, int height, int* tris, int cap, uint8_t* pins,
+                DelaunayWorkspace& ws, MeshStats& st);
+
 }  // namespace ps

@@ -110,6 +110,53 @@ int launch_resample_invalid(const unsigned long long* Cb, int cells_per_frame, i
 // S[f] = S[f] + a[f] + b[f]
 int launch_add_counts(int* S, const int* a, const int* b, int frames, cudaStream_t st);
 
+// K4 on the device (star.cu, star_dt.cuh): per-frame exact Delaunay of the
+// support lists of a frame group.  Arrays are frame-strided: supports and
+// per-support scratch by scap, cells by gw*gh (+1 for cell_start), triangles
+// and pin bytes by pitch, flags by kStarFlagInts.  Flags per frame: [0] fail
+// (the host replays the reference sweep for that frame), [1] rotation
+// suspects (4 ints each at kStarSuspectBase: triangle, v0, v1, v2), [2] ints
+// used and [3] count of the ambiguous hull vertices at kStarFanBase (vertex,
+// n, then n counter-clockwise triangles of 3 vertex ids).
+constexpr int kStarFlagInts = 2048;
+constexpr int kStarSuspectBase = 8;
+constexpr int kStarMaxSuspect = 64;
+constexpr int kStarFanBase = kStarSuspectBase + 4 * kStarMaxSuspect;
+struct StarArgs {
+    const int* su;
+    const int* sv;
+    const double* sd;
+    int scap;
+    const int* S;  // device support counts
+    int frames;
+    int W, H;
+    float max_disp;
+    int gs, gw, gh;  // grid cell size and dimensions (cells of gs x gs pixels)
+    int* cell_cnt;
+    int* cell_start;
+    int* cell_items;
+    uint8_t* dup;
+    int* pin_tri;  // per support: sorted vertex set of its pinned triangle or -1
+    int* tris;
+    long long pitch;  // triangle capacity per frame
+    uint8_t* pins;
+    int* tri_count;
+    int* flags;
+    unsigned long long* col_key;  // per frame 2 * W: column extremes as (v, index) keys
+    int* col_idx;                 // per frame 2 * W: their point indices (-1: empty column)
+    int* hull;                    // per frame 2 * scap: hull successor / predecessor per point
+    int* hull_tmp;                // per frame 8 * (2 * W + 2 * H + 8) ints: monotone-chain stacks
+    int* hard;                    // per frame scap: points deferred to a warp (count in flags[5])
+    int budget;                   // grid searches a thread may do before deferring its point
+};
+// grid + stars + triangle list + hull pins; then the rotation check; then
+// (after the host fixes: {frame, 0, tri, v0, v1, v2} rotation or {frame, 1,
+// vertex, s0, s1, s2} pin) the pin bits.
+int launch_star_mesh(const StarArgs& a, int max_points, cudaStream_t st);
+int launch_star_check(const StarArgs& a, long long max_tris, cudaStream_t st);
+int launch_star_finish(const StarArgs& a, const int* fixes, int n_fix, long long max_tris,
+                       cudaStream_t st);
+
 // Packs supports [S_prev[f], S_now[f]) of every frame into out (u,v pairs)
 // and out_d (disparities) at off[f].
 int launch_pack_new_supports(const int* su, const int* sv, const double* sd, int scap,
