@@ -64,3 +64,18 @@ def test_pipeline_support_lists(test_mesh_bin, orc, tmp_path, seed):
     out = subprocess.run([test_mesh_bin, path], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout + out.stderr
     assert out.stdout.startswith("ok ")
+
+
+def test_device_star_triangulation_on_cpu(test_mesh_bin, orc, tmp_path):
+    """The device Delaunay (kernels/star_dt.cuh: per-point stars from a grid,
+    convex hull from column extremes) compiled for the CPU: the same triangle
+    set as the reference-order sweep on 3,000 synthetic sets (lattices with
+    cocircular cells, random points, duplicates, collinear sets) and on every
+    iteration of a BASELINE config 2 frame."""
+    star = os.path.join(ROOT, "tests", "cpp", "_build", "test_star")
+    out = subprocess.run([star, "--synthetic", "3000"], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    path = str(tmp_path / "cfg2_9.sup")
+    _dump(path, orc, 640, 480, 12, 64, False, 2.0, 3, 10, 9)
+    out = subprocess.run([star, path], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
