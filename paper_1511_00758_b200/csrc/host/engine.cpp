@@ -514,7 +514,8 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     //   iteration.
     // The host loop below only moves data and launches; the workers
     // triangulate continuously while the device runs other groups' stages.
-    const int G = std::max(1, std::min(std::min(kMaxGroups, max_groups_), (F + 31) / 32));
+    // frame groups of >= 64 frames (measured on cfg2: 4 groups of 64 beat 8 of 32)
+    const int G = std::max(1, std::min(std::min(kMaxGroups, max_groups_), (F + 63) / 64));
     const int tri_cap = int(std::min<long long>(2ll * scap_ + 8, 2ll * P + 8));  // T <= 2S per frame
     // device mesh grid of iteration `it` (1-based): ~1-3 supports per cell —
     // seeds: <= 120 * cap over the frame; later: at most ~2 per cell of the
@@ -1194,6 +1195,9 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
             tot.dt_ms += m.dt_ms;
             tot.check_ms += m.check_ms;
             tot.order_ms += m.order_ms;
+            tot.rot_ms += m.rot_ms;
+            tot.pin_ms += m.pin_ms;
+            tot.init_ms += m.init_ms;
         }
         // launches = events: replays of the reference sweep, pins ordered by
         // SweepOrder, rotations it decided, triangles fitted three ways
@@ -1206,6 +1210,14 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         KernelStat& k3 = stat("host_order");  // SweepOrder queries
         k3.launches += int(tot.ambiguous + tot.rotations);
         k3.ms += tot.order_ms / workers;
+        KernelStat& k5 = stat("host_order_rot");  // of which: rotations decided
+        k5.launches += int(tot.rotations);
+        k5.ms += tot.rot_ms / workers;
+        KernelStat& k6 = stat("host_order_pin");  // of which: pins ordered
+        k6.launches += int(tot.ambiguous);
+        k6.ms += tot.pin_ms / workers;
+        KernelStat& k7 = stat("host_order_init");  // of which: SweepOrder::init (lex order, chains, buckets)
+        k7.ms += tot.init_ms / workers;
         KernelStat& k4 = stat("host_replay");  // frame-iterations replayed (delaunay_lex)
         k4.launches += int(tot.fallbacks);
         // pool occupancy: before the first task, gaps between tasks, after the last

@@ -138,6 +138,7 @@ bool resolve_device_flags(FrameMesh& fm, const int* flags, int frame, int width,
     bool have_order = false;
     auto build_order = [&] {
         if (have_order) return;
+        const double ti = now_ms();
         int minx, miny, m, spanx, spany;
         lex_order(fm.u.data(), fm.v.data(), n, ws, minx, miny, m, spanx, spany);
         fm.ranks.assign(ws.kept.begin(), ws.kept.begin() + m);
@@ -151,6 +152,7 @@ bool resolve_device_flags(FrameMesh& fm, const int* flags, int frame, int width,
         }
         fm.so.init(fm.px.data(), fm.py.data(), m);
         have_order = true;
+        st.init_ms += now_ms() - ti;
     };
     auto sorted3 = [](int a, int b, int c) {
         if (a > b) std::swap(a, b);
@@ -175,6 +177,7 @@ bool resolve_device_flags(FrameMesh& fm, const int* flags, int frame, int width,
         int s3[3];
         const bool ok = fm.so.resolve(r3, 1, &b, s3);
         st.order_ms += now_ms() - to;
+        st.rot_ms += now_ms() - to;
         if (!ok) return false;
         const int v0 = fm.ranks[s3[0]], v1 = fm.ranks[s3[1]], v2 = fm.ranks[s3[2]];
         fixes.insert(fixes.end(), {frame, 0, t, v0, v1, v2});
@@ -229,6 +232,7 @@ bool resolve_device_flags(FrameMesh& fm, const int* flags, int frame, int width,
             }
             const bool ok = fm.so.resolve(r3.data(), cnt, fm.birth.data(), s3.data());
             st.order_ms += now_ms() - to;
+            st.pin_ms += now_ms() - to;
             if (!ok) return false;
             for (int i = 1; i < cnt; ++i)
                 if (fm.birth[i] < fm.birth[pick]) pick = i;

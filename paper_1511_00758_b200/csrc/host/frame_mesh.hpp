@@ -36,6 +36,7 @@ struct MeshStats {
     long long rotations = 0;   // triangles whose rotation SweepOrder decided
     long long rot_checked = 0; // triangles fitted three ways
     double dt_ms = 0, check_ms = 0, order_ms = 0;
+    double rot_ms = 0, pin_ms = 0, init_ms = 0;  // of order_ms: rotations, pins, SweepOrder::init
 };
 
 struct FrameMesh {

@@ -349,7 +349,7 @@ bool SweepOrder::replay(int u0, int u1, int v0, int v1) {
     auto lnext = [](int e) { return (e & 3) == 2 ? e - 2 : e + 1; };
     auto add = [&](int a, int b, int c, int na, int nb, int nc, int birth, int fan) {
         const int e = 4 * int(rs_.size());
-        rs_.push_back(Slot{{a, b, c}, {na, nb, nc}, birth, fan, -1, -1});
+        rs_.push_back(Slot{{a, b, c}, {na, nb, nc}, birth, fan, -1, -1, a});
         if (na >= 0) N(na) = e;
         if (nb >= 0) N(nb) = e + 1;
         if (nc >= 0) N(nc) = e + 2;
@@ -469,7 +469,6 @@ bool SweepOrder::resolve(const int* tris, int count, uint64_t* birth, int* store
         v0 = miny_;
         v1 = maxy_;
     }
-    bool stuck = false;  // a requested growth could not enlarge the window
     for (int attempt = 0;; ++attempt) {
         const bool whole = u0 == minx_ && u1 == maxx_ && v0 == miny_ && v1 == maxy_;
         // growth for the next attempt: towards the points that broke a
@@ -477,7 +476,7 @@ bool SweepOrder::resolve(const int* tris, int count, uint64_t* birth, int* store
         int nu0 = u0, nu1 = u1, nv0 = v0, nv1 = v1;
         bool grow_all = false;
         bool gl = false, gr = false, gd = false, gu = false;  // directional growth requests
-        const bool fallback = attempt >= 6 || stuck;  // then finish chains in the full set instead
+        const bool fallback = attempt >= 8;  // then finish chains in the full set instead
         const bool replayed = replay(u0, u1, v0, v1);
         bool ok = replayed;
         if (!replayed) grow_all = true;
@@ -550,15 +549,10 @@ bool SweepOrder::resolve(const int* tris, int count, uint64_t* birth, int* store
             } else {
                 jq = fan_index(rrank_[origin], pb);
                 if (jq < 0 && !fallback) {
-                    // the window's hull edge into the origin is not the full
-                    // prefix's: grow the window across that edge
-                    const int o = rrank_[origin];
-                    int hpw = -1;  // the window's hull predecessor of o then: the slot's fan edge
-                    hpw = rrank_[b0[0]];  // contents (x_j.., p, o): b0[0] lies on that chain
-                    const long long nx = (long long)y_[o] - y_[hpw], ny = -((long long)x_[o] - x_[hpw]);
-                    const long long an = std::llabs(nx) + std::llabs(ny);
-                    if (5 * std::llabs(nx) >= an) (nx < 0 ? gl : gr) = true;
-                    if (5 * std::llabs(ny) >= an) (ny < 0 ? gd : gu) = true;
+                    // the window's visible chain from pb (it faces right, toward the
+                    // new point) is not the full prefix's: the window cut the
+                    // columns at the sweep front, so grow it vertically
+                    gd = gu = true;
                     ok = false;
                     continue;
                 }
@@ -592,18 +586,23 @@ bool SweepOrder::resolve(const int* tris, int count, uint64_t* birth, int* store
             if (gr) nu1 = std::max(nu1, u1 + gx);
             if (gd) nv0 = std::min(nv0, v0 - gy);
             if (gu) nv1 = std::max(nv1, v1 + gy);
-        } else if (grow_all || (nu0 == u0 && nu1 == u1 && nv0 == v0 && nv1 == v1)) {
+        }
+        auto clamp_new = [&] {
+            nu0 = std::max(minx_, nu0);
+            nu1 = std::min(maxx_, nu1);
+            nv0 = std::max(miny_, nv0);
+            nv1 = std::min(maxy_, nv1);
+        };
+        clamp_new();
+        // uniform growth when asked, or when no directed growth could enlarge the window
+        if (grow_all || (nu0 == u0 && nu1 == u1 && nv0 == v0 && nv1 == v1)) {
             delta *= 2;
             nu0 = std::min(nu0, u0 - delta);
             nu1 = std::max(nu1, u1 + delta);
             nv0 = std::min(nv0, v0 - delta);
             nv1 = std::max(nv1, v1 + delta);
+            clamp_new();
         }
-        nu0 = std::max(minx_, nu0);
-        nu1 = std::min(maxx_, nu1);
-        nv0 = std::max(miny_, nv0);
-        nv1 = std::min(maxy_, nv1);
-        stuck = nu0 == u0 && nu1 == u1 && nv0 == v0 && nv1 == v1;
         u0 = nu0;
         u1 = nu1;
         v0 = nv0;

@@ -101,6 +101,7 @@ private:
         int fan;    // fan position within the window's visible chain
         int hist;   // latest history entry, -1 if never eaten
         int eaten;  // window index of the last point that ate it
+        int x0;     // a fan slot's first hull vertex x_j at birth (window index)
     };
     struct Hist {
         int time;   // window index of the eating point
