@@ -197,7 +197,7 @@ Engine::~Engine() {
     for (FrameGroup& g : groups_) {
         for (DevBuf* b : {&g.dTri, &g.dTriOff, &g.dPlanes, &g.dPack, &g.dPackD, &g.dPackOff,
                           &g.dSprev, &g.dChunk, &g.dPin, &g.dCellCnt, &g.dCellStart, &g.dCellItems,
-                          &g.dDup, &g.dPinTri, &g.dTriCount, &g.dFlags, &g.dFix, &g.dColKey, &g.dColIdx, &g.dHull, &g.dHullTmp, &g.dHard})
+                          &g.dDup, &g.dPinTri, &g.dTriCount, &g.dFlags, &g.dFix, &g.dColKey, &g.dColIdx, &g.dHull, &g.dHullTmp, &g.dHard, &g.dHard2})
             if (b->p) cudaFree(b->p);
         for (HostBuf* b : {&g.hS, &g.hSprev, &g.hPackOff, &g.hPack, &g.hPackD, &g.hTri, &g.hTriOff,
                            &g.hPin, &g.hTriCount, &g.hFlags, &g.hFix})
@@ -568,6 +568,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         a.hull = static_cast<int*>(grp.dHull.p);
         a.hull_tmp = static_cast<int*>(grp.dHullTmp.p);
         a.hard = static_cast<int*>(grp.dHard.p);
+        a.hard2 = static_cast<int*>(grp.dHard2.p);
         a.budget = star_budget;
         return a;
     };
@@ -619,7 +620,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                 !dev<int>(grp.dFix, nn * 6 * 96) ||
                 !dev<unsigned long long>(grp.dColKey, nn * 2 * W) || !dev<int>(grp.dColIdx, nn * 2 * W) ||
                 !dev<int>(grp.dHull, nn * 2 * scap_) || !dev<int>(grp.dHullTmp, nn * 8 * (2 * size_t(W) + 2 * size_t(H) + 8)) ||
-                !dev<int>(grp.dHard, nn * scap_))
+                !dev<int>(grp.dHard, nn * scap_) || !dev<int>(grp.dHard2, nn * scap_))
                 return fail(PS_CUDA_ERROR, "allocation failed (device mesh)");
         }
 

@@ -146,7 +146,8 @@ struct StarArgs {
     int* col_idx;                 // per frame 2 * W: their point indices (-1: empty column)
     int* hull;                    // per frame 2 * scap: hull successor / predecessor per point
     int* hull_tmp;                // per frame 8 * (2 * W + 2 * H + 8) ints: monotone-chain stacks
-    int* hard;                    // per frame scap: points deferred to a warp (count in flags[5])
+    int* hard;                    // per frame scap: points pass 1 deferred (count in flags[5])
+    int* hard2;                   // per frame scap: points pass 1b deferred to warps (count in flags[6])
     int budget;                   // grid searches a thread may do before deferring its point
 };
 // grid + stars + triangle list + hull pins; then the rotation check; then

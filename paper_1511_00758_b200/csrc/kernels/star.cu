@@ -321,7 +321,8 @@ __device__ void star_clock(long long t0, int p) {
 }
 #endif
 
-__device__ __forceinline__ void star_body(const StarArgs& a, int f, int p);
+__device__ __forceinline__ void star_body(const StarArgs& a, int f, int p, int radius, int* cand, int cap,
+                                          int stride, int* defer_list, int defer_count_slot);
 
 __global__ void __launch_bounds__(kT) k_star(StarArgs a) {
     const int f = blockIdx.y;
@@ -330,13 +331,26 @@ __global__ void __launch_bounds__(kT) k_star(StarArgs a) {
     // threads take the points in grid order: neighbouring threads read the
     // same cells (cache locality) and do similar work (less divergence)
     const int p = a.cell_items[(long long)f * a.scap + t];
+    extern __shared__ int s_cand[];
 #ifdef PS_STAR_PROFILE
     const long long t0 = clock64();
-    star_body(a, f, p);
-    star_clock(t0, p);
-#else
-    star_body(a, f, p);
 #endif
+    star_body(a, f, p, 2, s_cand, star::kLocalMax, kT, a.hard, 5);
+#ifdef PS_STAR_PROFILE
+    star_clock(t0, p);
+#endif
+}
+
+// pass 1b: the points pass 1 deferred, with a 9x9-cell gather (about 100
+// candidates); what still needs the grid search goes to the warps
+constexpr int kWideT = 64;
+constexpr int kWideCap = 160;
+__global__ void __launch_bounds__(kWideT) k_star_wide(StarArgs a) {
+    const int f = blockIdx.y;
+    const int n = min(a.flags[(long long)f * kStarFlagInts + 5], a.scap);
+    extern __shared__ int s_cand[];
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
+        star_body(a, f, a.hard[(long long)f * a.scap + t], 4, s_cand, kWideCap, kWideT, a.hard2, 6);
 }
 
 // Hull-vertex bookkeeping shared by both passes: whether the vertex pixel is
@@ -403,7 +417,8 @@ __device__ void hull_outcome(const StarArgs& a, int f, int p, const HullCheck& h
 constexpr int kBudget = 8;   // grid searches a thread may do before handing p to a warp
 constexpr int kEmitBuf = 12;  // triangles a thread may hold before writing them
 
-__device__ __forceinline__ void star_body(const StarArgs& a, int f, int p) {
+__device__ __forceinline__ void star_body(const StarArgs& a, int f, int p, int radius, int* cand, int cap,
+                                          int stride, int* defer_list, int defer_count_slot) {
     const star::Grid g = make_grid(a, f);
     const long long sb = (long long)f * a.scap;
     const int* su = a.su + sb;
@@ -411,12 +426,12 @@ __device__ __forceinline__ void star_body(const StarArgs& a, int f, int p) {
     const double* sd = a.sd + sb;
     bool closed;
     // candidates in shared memory, the block's threads interleaved
-    extern __shared__ int s_cand[];
     star::Local L;
-    L.idx = s_cand + threadIdx.x;
-    L.dxy = s_cand + star::kLocalMax * kT + threadIdx.x;
-    L.stride = kT;
-    star::gather(g, p, 2, L);
+    L.idx = cand + threadIdx.x;
+    L.dxy = cand + cap * stride + threadIdx.x;
+    L.stride = stride;
+    L.cap = cap;
+    star::gather(g, p, radius, L);
     // the triangles this point writes (it is their smallest vertex), held
     // until the star is known to be complete within the search budget
     int buf[3 * kEmitBuf];
@@ -448,10 +463,10 @@ __device__ __forceinline__ void star_body(const StarArgs& a, int f, int p) {
         }, a.budget);
         defer = r2 == -4;
     }
-    if (defer) {  // too costly for one thread: a warp redoes this star (k_star_hard)
+    if (defer) {  // beyond this pass: a wider gather (k_star_wide), then a warp (k_star_hard)
         int* fl = a.flags + (long long)f * kStarFlagInts;
-        const int k = atomicAdd(fl + 5, 1);
-        if (k < a.scap) a.hard[sb + k] = p;
+        const int k = atomicAdd(fl + defer_count_slot, 1);
+        if (k < a.scap) defer_list[sb + k] = p;
         return;
     }
     if (nbuf > 0) {
@@ -638,7 +653,7 @@ __device__ int w_walk(const star::Grid& g, int p, bool& closed, F&& on_tri) {
 __global__ void k_star_hard(StarArgs a) {
     const int f = blockIdx.y;
     const int lane = threadIdx.x & 31;
-    const int nhard = min(a.flags[(long long)f * kStarFlagInts + 5], a.scap);
+    const int nhard = min(a.flags[(long long)f * kStarFlagInts + 6], a.scap);
     const int warps = gridDim.x * (blockDim.x >> 5);
     const star::Grid g = make_grid(a, f);
     const long long sb = (long long)f * a.scap;
@@ -647,7 +662,7 @@ __global__ void k_star_hard(StarArgs a) {
     const double* sd = a.sd + sb;
     int* tris = a.tris + 3 * (long long)f * a.pitch;
     for (int h = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); h < nhard; h += warps) {
-        const int p = a.hard[sb + h];
+        const int p = a.hard2[sb + h];
         bool closed;
         HullCheck hc;  // kept on the fly: one walk serves both purposes
         const int hu = su[p], hv = sv[p];
@@ -796,6 +811,12 @@ int launch_star_mesh(const StarArgs& a, int max_points, cudaStream_t st) {
     const int smem = 2 * star::kLocalMax * kT * int(sizeof(int));
     cudaFuncSetAttribute(k_star, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     k_star<<<dim3((max_points + kT - 1) / kT, a.frames), kT, smem, st>>>(a);
+    {
+        const int wsm = 2 * kWideCap * kWideT * int(sizeof(int));
+        cudaFuncSetAttribute(k_star_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, wsm);
+        // deferred points are a few percent: size the grid for 1/8 of them
+        k_star_wide<<<dim3((max_points / 8 + kWideT - 1) / kWideT + 1, a.frames), kWideT, wsm, st>>>(a);
+    }
     STAR_CHECK("k_star");
     k_star_hard<<<dim3(128, a.frames), 128, 0, st>>>(a); STAR_CHECK("k_star_hard");
 #ifdef PS_STAR_PROFILE

@@ -359,6 +359,7 @@ struct Local {
     int* idx = nullptr;    // point index
     int* dxy = nullptr;    // (dy << 16) | (dx & 0xffff), relative to p
     int stride = 1;
+    int cap = kLocalMax;   // capacity of idx / dxy
     PS_HD int id(int i) const { return idx[i * stride]; }
     PS_HD int dx(int i) const { return int(short(dxy[i * stride] & 0xffff)); }
     PS_HD int dy(int i) const { return dxy[i * stride] >> 16; }
@@ -380,7 +381,7 @@ PS_HD void gather(const Grid& g, int p, int radius, Local& L) {
             for (int i = g.cell_start[c]; i < g.cell_start[c + 1]; ++i) {
                 const int s = g.cell_items[i];
                 if (s == p || g.dup[s]) continue;
-                if (L.n == kLocalMax) {
+                if (L.n == L.cap) {
                     L.complete = false;
                     return;
                 }
