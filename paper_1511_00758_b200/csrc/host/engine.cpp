@@ -196,8 +196,8 @@ Engine::~Engine() {
         if (b->p) cudaFreeHost(b->p);
     for (FrameGroup& g : groups_) {
         for (DevBuf* b : {&g.dTri, &g.dTriOff, &g.dPlanes, &g.dPack, &g.dPackD, &g.dPackOff,
-                          &g.dSprev, &g.dChunk, &g.dPin, &g.dCellCnt, &g.dCellStart, &g.dCellItems,
-                          &g.dDup, &g.dPinTri, &g.dTriCount, &g.dFlags, &g.dFix, &g.dColKey, &g.dColIdx, &g.dHull, &g.dHullTmp, &g.dHard, &g.dHard2})
+                          &g.dSprev, &g.dChunk, &g.dPin, &g.dCellCnt, &g.dCellStart, &g.dCellItems, &g.dCellXY,
+                          &g.dDup, &g.dPinTri, &g.dTriCount, &g.dFlags, &g.dFix, &g.dColKey, &g.dColIdx, &g.dHull, &g.dHullTmp, &g.dHard})
             if (b->p) cudaFree(b->p);
         for (HostBuf* b : {&g.hS, &g.hSprev, &g.hPackOff, &g.hPack, &g.hPackD, &g.hTri, &g.hTriOff,
                            &g.hPin, &g.hTriCount, &g.hFlags, &g.hFix})
@@ -526,7 +526,6 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         return std::max(2, int(std::sqrt(1.3 * double(P) / std::max(1.0, est)) + 0.5));
     };
     const long long star_cells_max = (long long)((W - 1) / 2 + 1) * ((H - 1) / 2 + 1);  // gs >= 2
-    const int star_budget = std::getenv("PS_STAR_BUDGET") ? std::atoi(std::getenv("PS_STAR_BUDGET")) : 0;
     cudaMemsetAsync(dErr, 0, sizeof(int), st_);
     ps_status s = check(cudaEventRecord(start_event_, st_), "start event");
     if (s != PS_OK) return s;
@@ -556,6 +555,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         a.cell_cnt = static_cast<int*>(grp.dCellCnt.p);
         a.cell_start = static_cast<int*>(grp.dCellStart.p);
         a.cell_items = static_cast<int*>(grp.dCellItems.p);
+        a.cell_xy = static_cast<int*>(grp.dCellXY.p);
         a.dup = static_cast<uint8_t*>(grp.dDup.p);
         a.pin_tri = static_cast<int*>(grp.dPinTri.p);
         a.tris = static_cast<int*>(grp.dTri.p);
@@ -568,8 +568,6 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         a.hull = static_cast<int*>(grp.dHull.p);
         a.hull_tmp = static_cast<int*>(grp.dHullTmp.p);
         a.hard = static_cast<int*>(grp.dHard.p);
-        a.hard2 = static_cast<int*>(grp.dHard2.p);
-        a.budget = star_budget;
         return a;
     };
     auto enqueue_mesh = [&](FrameGroup& grp, double est, int max_points) {
@@ -612,7 +610,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         if (device_dt) {
             const size_t nn = size_t(grp.n);
             if (!dev<int>(grp.dCellCnt, nn * star_cells_max) || !dev<int>(grp.dCellStart, nn * (star_cells_max + 1)) ||
-                !dev<int>(grp.dCellItems, nn * scap_) || !dev<uint8_t>(grp.dDup, nn * scap_) ||
+                !dev<int>(grp.dCellItems, nn * scap_) || !dev<int>(grp.dCellXY, nn * scap_) || !dev<uint8_t>(grp.dDup, nn * scap_) ||
                 !dev<int>(grp.dPinTri, nn * scap_ * 3) || !dev<int>(grp.dTriCount, nn) ||
                 !dev<int>(grp.dFlags, nn * kStarFlagInts) || !dev<int>(grp.dTri, nn * tri_cap * 3) ||
                 !dev<uint8_t>(grp.dPin, nn * tri_cap) || !host<int>(grp.hTriCount, nn) ||
@@ -620,7 +618,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                 !dev<int>(grp.dFix, nn * 6 * 96) ||
                 !dev<unsigned long long>(grp.dColKey, nn * 2 * W) || !dev<int>(grp.dColIdx, nn * 2 * W) ||
                 !dev<int>(grp.dHull, nn * 2 * scap_) || !dev<int>(grp.dHullTmp, nn * 8 * (2 * size_t(W) + 2 * size_t(H) + 8)) ||
-                !dev<int>(grp.dHard, nn * scap_) || !dev<int>(grp.dHard2, nn * scap_))
+                !dev<int>(grp.dHard, nn * scap_))
                 return fail(PS_CUDA_ERROR, "allocation failed (device mesh)");
         }
 

@@ -60,7 +60,7 @@ struct FrameGroup {
     HostBuf hS, hSprev, hPackOff, hPack, hPackD, hTri, hTriOff, hPin;
     std::vector<int> ntri;
     // device mesh (kernels/star.cu): grid scratch, pin choices, flags, fixes
-    DevBuf dCellCnt, dCellStart, dCellItems, dDup, dPinTri, dTriCount, dFlags, dFix, dColKey, dColIdx, dHull, dHullTmp, dHard, dHard2;
+    DevBuf dCellCnt, dCellStart, dCellItems, dCellXY, dDup, dPinTri, dTriCount, dFlags, dFix, dColKey, dColIdx, dHull, dHullTmp, dHard;
     HostBuf hTriCount, hFlags, hFix;
     std::vector<std::vector<int>> fixes;  // per frame: host fixes for the device mesh
     std::vector<uint8_t> replayed;        // per frame: triangles came from the host replay

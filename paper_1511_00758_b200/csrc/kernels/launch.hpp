@@ -117,7 +117,8 @@ int launch_add_counts(int* S, const int* a, const int* b, int frames, cudaStream
 // (the host replays the reference sweep for that frame), [1] rotation
 // suspects (4 ints each at kStarSuspectBase: triangle, v0, v1, v2), [2] ints
 // used and [3] count of the ambiguous hull vertices at kStarFanBase (vertex,
-// n, then n counter-clockwise triangles of 3 vertex ids).
+// n, then n counter-clockwise triangles of 3 vertex ids), [4] collinear set,
+// [5] points deferred from pass 1 (k_star) to pass 2 (k_star_far).
 constexpr int kStarFlagInts = 2048;
 constexpr int kStarSuspectBase = 8;
 constexpr int kStarMaxSuspect = 64;
@@ -135,6 +136,7 @@ struct StarArgs {
     int* cell_cnt;
     int* cell_start;
     int* cell_items;
+    int* cell_xy;  // per cell_items position: (v << 16) | u of that point, -1 for a duplicate
     uint8_t* dup;
     int* pin_tri;  // per support: sorted vertex set of its pinned triangle or -1
     int* tris;
@@ -146,9 +148,7 @@ struct StarArgs {
     int* col_idx;                 // per frame 2 * W: their point indices (-1: empty column)
     int* hull;                    // per frame 2 * scap: hull successor / predecessor per point
     int* hull_tmp;                // per frame 8 * (2 * W + 2 * H + 8) ints: monotone-chain stacks
-    int* hard;                    // per frame scap: points pass 1 deferred (count in flags[5])
-    int* hard2;                   // per frame scap: points pass 1b deferred to warps (count in flags[6])
-    int budget;                   // grid searches a thread may do before deferring its point
+    int* hard;                    // per frame scap: points pass 1 deferred to pass 2 (count in flags[5])
 };
 // grid + stars + triangle list + hull pins; then the rotation check; then
 // (after the host fixes: {frame, 0, tri, v0, v1, v2} rotation or {frame, 1,

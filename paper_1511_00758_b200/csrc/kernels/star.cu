@@ -94,7 +94,7 @@ __device__ __forceinline__ star::Grid make_grid(const StarArgs& a, int f) {
     const int* hull = a.hull + 2 * sb;
     return star::Grid{a.su + sb, a.sv + sb, a.dup + sb, a.cell_start + cb, a.cell_items + sb, a.S[f],
                       0, 0, a.W - 1, a.H - 1, a.gs, a.gw, a.gh, cols, cols + a.W, hull, hull + a.scap,
-                      a.flags[(long long)f * kStarFlagInts + 4]};
+                      a.flags[(long long)f * kStarFlagInts + 4], 1.0 / a.gs};
 }
 
 __global__ void k_grid_count(StarArgs a) {
@@ -298,11 +298,29 @@ __global__ void k_grid_dup(StarArgs a) {
     pt[0] = pt[1] = pt[2] = -1;
 }
 
+// the points of each cell run packed for the tiled pass (duplicates -1)
+__global__ void k_grid_pack(StarArgs a) {
+    const int f = blockIdx.y;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= a.S[f]) return;
+    const long long sb = (long long)f * a.scap;
+    const int s = a.cell_items[sb + k];
+    a.cell_xy[sb + k] = a.dup[sb + s] ? -1 : (a.sv[sb + s] << 16) | a.su[sb + s];
+}
+
 __device__ __forceinline__ void set_fail(const StarArgs& a, int f) { atomicExch(a.flags + (long long)f * kStarFlagInts, 1); }
 
 #ifdef PS_STAR_PROFILE
 __device__ unsigned long long g_star_cycles, g_star_max, g_star_n, g_star_hist[24];
+// pass 2: [0] points [1] gather cycles [2] local steps [3] local cycles [4] row searches
+// [5] row cycles [6] rows visited [7] column searches [8] column cycles [9] nearest cycles [10] total cycles
+__device__ unsigned long long g_far[12];
+#define FAR_ADD(i, v) do { if ((threadIdx.x & 31) == 0) atomicAdd(&g_far[i], (unsigned long long)(v)); } while (0)
+#define FAR_CLOCK() clock64()
 __global__ void k_star_report() {
+    printf("k_star_far: %llu points, gather %llu cyc, local %llu steps %llu cyc, rows %llu searches %llu cyc %llu rows, cols %llu %llu cyc, nearest %llu cyc, total %llu cyc\n",
+           g_far[0], g_far[1], g_far[2], g_far[3], g_far[4], g_far[5], g_far[6], g_far[7], g_far[8], g_far[9], g_far[10]);
+    for (int i = 0; i < 12; ++i) g_far[i] = 0;
     printf("k_star: %llu points, mean %.0f cycles, max %llu cycles (point %llu)\n", g_star_n,
            double(g_star_cycles) / double(g_star_n > 0 ? g_star_n : 1), g_star_max >> 24, g_star_max & 0xffffff);
     for (int i = 0; i < 24; ++i)
@@ -319,39 +337,10 @@ __device__ void star_clock(long long t0, int p) {
     while (b < 23 && (1ull << (b + 1)) <= c) ++b;
     atomicAdd(&g_star_hist[b], 1ull);
 }
+#else
+#define FAR_ADD(i, v) do { } while (0)
+#define FAR_CLOCK() 0ll
 #endif
-
-__device__ __forceinline__ void star_body(const StarArgs& a, int f, int p, int radius, int* cand, int cap,
-                                          int stride, int* defer_list, int defer_count_slot);
-
-__global__ void __launch_bounds__(kT) k_star(StarArgs a) {
-    const int f = blockIdx.y;
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= a.S[f]) return;
-    // threads take the points in grid order: neighbouring threads read the
-    // same cells (cache locality) and do similar work (less divergence)
-    const int p = a.cell_items[(long long)f * a.scap + t];
-    extern __shared__ int s_cand[];
-#ifdef PS_STAR_PROFILE
-    const long long t0 = clock64();
-#endif
-    star_body(a, f, p, 2, s_cand, star::kLocalMax, kT, a.hard, 5);
-#ifdef PS_STAR_PROFILE
-    star_clock(t0, p);
-#endif
-}
-
-// pass 1b: the points pass 1 deferred, with a 9x9-cell gather (about 100
-// candidates); what still needs the grid search goes to the warps
-constexpr int kWideT = 64;
-constexpr int kWideCap = 160;
-__global__ void __launch_bounds__(kWideT) k_star_wide(StarArgs a) {
-    const int f = blockIdx.y;
-    const int n = min(a.flags[(long long)f * kStarFlagInts + 5], a.scap);
-    extern __shared__ int s_cand[];
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
-        star_body(a, f, a.hard[(long long)f * a.scap + t], 4, s_cand, kWideCap, kWideT, a.hard2, 6);
-}
 
 // Hull-vertex bookkeeping shared by both passes: whether the vertex pixel is
 // covered (tie rule), and whether the incident planes (smallest-first
@@ -414,179 +403,486 @@ __device__ void hull_outcome(const StarArgs& a, int f, int p, const HullCheck& h
     write_fan(w + 2);
 }
 
-constexpr int kBudget = 8;   // grid searches a thread may do before handing p to a warp
-constexpr int kEmitBuf = 12;  // triangles a thread may hold before writing them
+__device__ __forceinline__ int w_scan(int x) {  // inclusive prefix sum over the warp
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    return x;
+}
 
-__device__ __forceinline__ void star_body(const StarArgs& a, int f, int p, int radius, int* cand, int cap,
-                                          int stride, int* defer_list, int defer_count_slot) {
-    const star::Grid g = make_grid(a, f);
+constexpr int kStarTris = 16;  // triangles of one star a pass-1 thread may hold
+constexpr int kTileT = 128;
+constexpr int kTileCap = 1024;  // points of a tile's region (more: its points go to pass 2)
+constexpr int kRegionCells = star::kTileRegion * star::kTileRegion;
+static_assert(kRegionCells == 2 * kTileT, "two region cells per thread");
+
+__device__ __forceinline__ void defer_point(const StarArgs& a, int f, int p) {
+    const int k = atomicAdd(a.flags + (long long)f * kStarFlagInts + 5, 1);
+    if (k < a.scap) a.hard[(long long)f * a.scap + k] = p;
+}
+
+// the triangles of p's star that p writes (it is their smallest vertex)
+__device__ __forceinline__ void emit_star(const StarArgs& a, int f, int p, const int* tb, int nt) {
+    int ne = 0;
+    for (int j = 0; j < nt; ++j) ne += p < tb[2 * j] && p < tb[2 * j + 1];
+    if (ne == 0) return;
+    int slot = atomicAdd(a.tri_count + f, ne);
+    int* tris = a.tris + 3 * (long long)f * a.pitch;
+    for (int j = 0; j < nt; ++j)
+        if (p < tb[2 * j] && p < tb[2 * j + 1]) {
+            if (slot < a.pitch) {
+                tris[3 * (long long)slot] = p;
+                tris[3 * (long long)slot + 1] = tb[2 * j];
+                tris[3 * (long long)slot + 2] = tb[2 * j + 1];
+            }
+            ++slot;
+        }
+}
+
+// Pass 1, one block per tile of kTileCells^2 cells: the tile's region
+// (star_dt.cuh Tile: the tile plus a kTileHalo-cell halo) is staged in
+// shared memory, then one thread per point of the tile walks its star from
+// it (radius 2, else 4) into a buffer; the triangles it writes, its hull
+// bookkeeping and, rarely, its fan all come from that buffer.  A point whose
+// star needs a wider search (about 1% at BASELINE config 2's last iteration:
+// next to holes and along the hull) or has more than kStarTris triangles is
+// listed for pass 2.
+__global__ void __launch_bounds__(kTileT) k_star(StarArgs a) {
+    __shared__ int s_start[kRegionCells + 1];
+    __shared__ int s_xy[kTileCap], s_id[kTileCap];
+    __shared__ int s_warp[kTileT / 32];
+    __shared__ int s_list[kTileT], s_nlist;
+    const int f = blockIdx.y;
+    const int tw = (a.gw + star::kTileCells - 1) / star::kTileCells;
+    const int cx0 = (blockIdx.x % tw) * star::kTileCells - star::kTileHalo;
+    const int cy0 = (blockIdx.x / tw) * star::kTileCells - star::kTileHalo;
     const long long sb = (long long)f * a.scap;
-    const int* su = a.su + sb;
-    const int* sv = a.sv + sb;
-    const double* sd = a.sd + sb;
-    bool closed;
-    // candidates in shared memory, the block's threads interleaved
-    star::Local L;
-    L.idx = cand + threadIdx.x;
-    L.dxy = cand + cap * stride + threadIdx.x;
-    L.stride = stride;
-    L.cap = cap;
-    star::gather(g, p, radius, L);
-    // the triangles this point writes (it is their smallest vertex), held
-    // until the star is known to be complete within the search budget
-    int buf[3 * kEmitBuf];
-    int nbuf = 0;
-    bool overflow = false;
-    const int r = star::walk_star(g, L, p, closed, [&](int t0, int t1, int t2) {
-        if (t0 < t1 && t0 < t2) {
-            if (nbuf == kEmitBuf) {
-                overflow = true;
+    const int* cs = a.cell_start + (long long)f * (a.gw * a.gh + 1);
+    const int* cxy = a.cell_xy + sb;
+    const int* ci = a.cell_items + sb;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    // region cells 2t and 2t + 1: their non-duplicate points
+    int r0[2], r1[2], cnt[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int c = 2 * threadIdx.x + k;
+        const int gx = cx0 + c % star::kTileRegion, gy = cy0 + c / star::kTileRegion;
+        r0[k] = r1[k] = cnt[k] = 0;
+        if (gx >= 0 && gy >= 0 && gx < a.gw && gy < a.gh) {
+            r0[k] = cs[gy * a.gw + gx];
+            r1[k] = cs[gy * a.gw + gx + 1];
+            for (int i = r0[k]; i < r1[k]; ++i) cnt[k] += cxy[i] != -1;
+        }
+    }
+    const int mine = cnt[0] + cnt[1];
+    int incl = w_scan(mine);
+    if (lane == 31) s_warp[wid] = incl;
+    __syncthreads();
+    for (int w = 0; w < wid; ++w) incl += s_warp[w];
+    const int total = s_warp[0] + s_warp[1] + s_warp[2] + s_warp[3];
+    int at = incl - mine;
+    s_start[2 * threadIdx.x] = at;
+    s_start[2 * threadIdx.x + 1] = at + cnt[0];
+    if (threadIdx.x == 0) {
+        s_start[kRegionCells] = total;
+        s_nlist = 0;
+    }
+    if (total <= kTileCap) {
+        const int ox = cx0 * a.gs, oy = cy0 * a.gs;
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+            for (int i = r0[k]; i < r1[k]; ++i) {
+                const int w = cxy[i];
+                if (w == -1) continue;
+                s_xy[at] = (((w >> 16) - oy) << 16) | ((w & 0xffff) - ox);
+                s_id[at] = ci[i];
+                ++at;
+            }
+    }
+    __syncthreads();
+    const star::Grid g = make_grid(a, f);
+    const star::Tile T{s_start, s_xy, s_id, cx0, cy0};
+    // the tile's points: row y's entries from row_at[y], row_len[y] of them
+    int n_inner = 0;
+    int row_at[star::kTileCells], row_len[star::kTileCells];
+#pragma unroll
+    for (int y = 0; y < star::kTileCells; ++y) {
+        const int c = (star::kTileHalo + y) * star::kTileRegion + star::kTileHalo;
+        row_at[y] = s_start[c];
+        row_len[y] = s_start[c + star::kTileCells] - row_at[y];
+        n_inner += row_len[y];
+    }
+    // the region's entry i as p's walk state
+    auto point_at = [&](int i) {
+        star::TilePoint P;
+        const int w = s_xy[i];
+        P.p = s_id[i];
+        P.pxr = w & 0xffff;
+        P.pyr = w >> 16;
+        P.pcx = cx0 + P.pxr / a.gs;
+        P.pcy = cy0 + P.pyr / a.gs;
+        P.pu = cx0 * a.gs + P.pxr;
+        P.pv = cy0 * a.gs + P.pyr;
+        P.hprev = g.hprev[P.p];
+        P.hnext = g.hnext[P.p];
+        return P;
+    };
+    // phase 1: radius 2; the points needing more, and the hull vertices
+    // (their bookkeeping is heavy), are listed for phase 2 so a warp's
+    // threads stay on the common path together
+    for (int k = threadIdx.x; k < n_inner; k += kTileT) {
+        int y = 0, kk = k;
+        while (kk >= row_len[y]) kk -= row_len[y++];
+        const int i = row_at[y] + kk;
+        if (total > kTileCap) {  // an overfull region: the tile's points go to pass 2
+            // (entries were not written: find the kk-th non-duplicate point of the row)
+            const int gy = cy0 + star::kTileHalo + y;
+            int left = kk;
+            for (int gx = cx0 + star::kTileHalo; gx < cx0 + star::kTileHalo + star::kTileCells && gx < a.gw; ++gx)
+                for (int j = cs[gy * a.gw + gx]; j < cs[gy * a.gw + gx + 1]; ++j)
+                    if (cxy[j] != -1 && left-- == 0) defer_point(a, f, ci[j]);
+            continue;
+        }
+        const star::TilePoint P = point_at(i);
+        int tb[2 * kStarTris];  // (b, c) of each triangle (p, b, c), walk order
+        bool closed;
+        const int nt = star::tile_walk(g, T, P, 2, closed, tb, kStarTris);
+        if (nt == -4 || (nt > 0 && !closed)) {
+            const int at2 = atomicAdd(&s_nlist, 1);
+            if (at2 < kTileT) s_list[at2] = i;
+            else defer_point(a, f, P.p);
+            continue;
+        }
+        if (nt < 0) {
+            defer_point(a, f, P.p);
+            continue;
+        }
+        emit_star(a, f, P.p, tb, nt);
+    }
+    __syncthreads();
+    // phase 2: radius 4, hull bookkeeping
+    const int nl = min(s_nlist, kTileT);
+    for (int k = threadIdx.x; k < nl; k += kTileT) {
+        const star::TilePoint P = point_at(s_list[k]);
+        int tb[2 * kStarTris];
+        bool closed;
+        const int nt = star::tile_walk(g, T, P, 4, closed, tb, kStarTris);
+        if (nt < 0) {
+            defer_point(a, f, P.p);
+            continue;
+        }
+        emit_star(a, f, P.p, tb, nt);
+        if (closed || nt == 0) continue;
+        const long long sb2 = (long long)f * a.scap;
+        const int* su = a.su + sb2;
+        const int* sv = a.sv + sb2;
+        const double* sd = a.sd + sb2;
+        const int p = P.p;
+        HullCheck h;
+        for (int j = 0; j < nt; ++j) h.add(su, sv, sd, P.pu, P.pv, a.max_disp, p, tb[2 * j], tb[2 * j + 1]);
+        hull_outcome(a, f, p, h, [&](int* out) {
+            for (int j = 0; j < nt; ++j) {
+                out[3 * j] = p;
+                out[3 * j + 1] = tb[2 * j];
+                out[3 * j + 2] = tb[2 * j + 1];
+            }
+        });
+    }
+}
+
+// ---- pass 2: one warp per deferred point.  The warp gathers the 9x9 cells
+// around p into shared memory (about 100 points, three or four per lane);
+// each search is a lane-parallel scan of them under the pencil order
+// (star_dt.cuh Pencil) and a shuffle tournament, certified like pass 1's.
+// Only a winner whose circle leaves the gathered box continues on the grid:
+// the rows of its circle on the search side of p -> q, outside the box.
+
+constexpr int kFarT = 128;      // 4 warps per block
+constexpr int kFarR = 4;        // gather radius in cells
+constexpr int kFarCap = 256;    // gathered points per warp
+constexpr int kFarTris = 96;    // triangles of one star (more: the frame is replayed on the host)
+
+struct WLocal {
+    int n;
+    bool complete;
+    star::Box box;
+    int* idx;
+    int* dxy;  // (dy << 16) | (dx & 0xffff) relative to p; 0 for p and duplicates
+};
+
+
+__device__ void w_gather(const star::Grid& g, int p, WLocal& L) {
+    const int lane = threadIdx.x & 31;
+    const int px = star::cell_x(g, g.u[p]), py = star::cell_y(g, g.v[p]);
+    L.box = star::Box{max(px - kFarR, 0), max(py - kFarR, 0), min(px + kFarR, g.gw - 1), min(py + kFarR, g.gh - 1)};
+    const int bw = L.box.x1 - L.box.x0 + 1, cells = bw * (L.box.y1 - L.box.y0 + 1);
+    // lane l takes cells l, l + 32, l + 64 (<= 81)
+    int cnt[3], first[3];
+    int total = 0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const int c = lane + 32 * k;
+        cnt[k] = 0;
+        first[k] = 0;
+        if (c < cells) {
+            const int cell = (L.box.y0 + c / bw) * g.gw + L.box.x0 + c % bw;
+            first[k] = g.cell_start[cell];
+            cnt[k] = g.cell_start[cell + 1] - first[k];
+        }
+        total += cnt[k];
+    }
+    const int incl = w_scan(total);
+    L.n = __shfl_sync(0xffffffffu, incl, 31);
+    L.complete = L.n <= kFarCap && g.maxx - g.minx < 4096 && g.maxy - g.miny < 4096;
+    if (!L.complete) return;
+    int at = incl - total;
+    const int pu = g.u[p], pv = g.v[p];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+        for (int i = 0; i < cnt[k]; ++i, ++at) {
+            const int s = g.cell_items[first[k] + i];
+            L.idx[at] = s;
+            L.dxy[at] = g.dup[s] ? 0 : ((g.v[s] - pv) << 16) | ((g.u[s] - pu) & 0xffff);
+        }
+    __syncwarp();
+}
+
+// the shuffle tournament over (position, num, den) under the pencil order;
+// ties (cocircular) by the exact perturbed rule on the point indices
+__device__ __forceinline__ int w_tournament(const star::Grid& g, const WLocal& L, int p, int q, int side, int bi,
+                                            int bnum, int bden) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        const int on = __shfl_xor_sync(0xffffffffu, bnum, o);
+        const int od = __shfl_xor_sync(0xffffffffu, bden, o);
+        if (oi < 0 || oi == bi) continue;
+        bool take = bi < 0;
+        if (!take) {
+            const long long l = (long long)on * bden, r = (long long)bnum * od;
+            if (l == r) {
+                const int s = L.idx[oi], b = L.idx[bi];
+                take = side > 0 ? star::inside(g, p, q, b, s) : star::inside(g, p, b, q, s);
             } else {
-                buf[3 * nbuf] = t0;
-                buf[3 * nbuf + 1] = t1;
-                buf[3 * nbuf + 2] = t2;
-                ++nbuf;
+                take = side > 0 ? l < r : l > r;
             }
         }
-    }, a.budget);
-    if (r == -2) {
-        set_fail(a, f);
-        return;
+        if (take) {
+            bi = oi;
+            bnum = on;
+            bden = od;
+        }
     }
-    HullCheck h;
-    bool defer = r == -4 || overflow;
-    if (!defer && !closed && r > 0) {
-        // a hull vertex: the bookkeeping walk (within the same budget)
-        const int hu = su[p], hv = sv[p];
-        const int r2 = star::walk_star(g, L, p, closed, [&](int t0, int t1, int t2) {
-            h.add(su, sv, sd, hu, hv, a.max_disp, t0, t1, t2);
-        }, a.budget);
-        defer = r2 == -4;
-    }
-    if (defer) {  // beyond this pass: a wider gather (k_star_wide), then a warp (k_star_hard)
-        int* fl = a.flags + (long long)f * kStarFlagInts;
-        const int k = atomicAdd(fl + defer_count_slot, 1);
-        if (k < a.scap) defer_list[sb + k] = p;
-        return;
-    }
-    if (nbuf > 0) {
-        const int slot = atomicAdd(a.tri_count + f, nbuf);
-        int* tris = a.tris + 3 * (long long)f * a.pitch;
-        for (int i = 0; i < nbuf; ++i)
-            if (slot + i < a.pitch) {
-                tris[3 * (long long)(slot + i)] = buf[3 * i];
-                tris[3 * (long long)(slot + i) + 1] = buf[3 * i + 1];
-                tris[3 * (long long)(slot + i) + 2] = buf[3 * i + 2];
-            }
-    }
-    if (closed || r == 0) return;
-    hull_outcome(a, f, p, h, [&](int* out) {
-        int k = 0;
-        star::walk_star(g, L, p, closed, [&](int t0, int t1, int t2) {
-            if (k < h.n_inc) {
-                out[3 * k] = t0;
-                out[3 * k + 1] = t1;
-                out[3 * k + 2] = t2;
-            }
-            ++k;
-        });
-    });
+    return bi;
 }
 
-// ---- pass 2: one warp per deferred point.  The same searches with the
-// candidates of a box or a disc spread over the lanes, and the winner chosen
-// by a shuffle tournament under the perturbed in-circle order (a strict total
-// order on the candidates, so both lanes of a pair pick the same winner).
-
-__device__ __forceinline__ bool w_better(const star::Grid& g, int p, int q, int side, int a, int b) {
-    return side > 0 ? star::inside(g, p, q, a, b) : star::inside(g, p, a, q, b);
+// Local next neighbour over the warp: the winner if certified, -1 hull edge,
+// -3 otherwise with `start` = the local winner (or -1: none on that side).
+__device__ int w_next_local(const star::Grid& g, const WLocal& L, int p, int q, int side, int& start) {
+    start = -1;
+    if (star::hull_edge(g, p, q, side)) return -1;
+    if (!L.complete) return -3;
+    const int lane = threadIdx.x & 31;
+    const int qx = g.u[q] - g.u[p], qy = g.v[q] - g.v[p];
+    int bi = -1, bnum = 0, bden = 0;
+    for (int i = lane; i < L.n; i += 32) {
+        const int w = L.dxy[i];
+        const int sx = int(short(w & 0xffff)), sy = w >> 16;
+        const int den = qx * sy - qy * sx;
+        if (side > 0 ? den <= 0 : den >= 0) continue;
+        const int num = sx * (sx - qx) + sy * (sy - qy);
+        if (bi >= 0) {
+            const long long l = (long long)num * bden, r = (long long)bnum * den;
+            if (l == r) {
+                const int s = L.idx[i], b = L.idx[bi];
+                if (!(side > 0 ? star::inside(g, p, q, b, s) : star::inside(g, p, b, q, s))) continue;
+            } else if (side > 0 ? l > r : l < r) {
+                continue;
+            }
+        }
+        bi = i;
+        bnum = num;
+        bden = den;
+    }
+    bi = w_tournament(g, L, p, q, side, bi, bnum, bden);
+    if (bi < 0) return -3;
+    const int w = L.dxy[bi];
+    const double bx = int(short(w & 0xffff)), by = w >> 16;
+    const star::Box need = side > 0 ? star::circle_box_rel(g, p, double(qx), double(qy), bx, by)
+                                    : star::circle_box_rel(g, p, bx, by, double(qx), double(qy));
+    if (star::covers(L.box, need)) return L.idx[bi];
+    start = L.idx[bi];
+    return -3;
 }
 
-__device__ __forceinline__ int w_reduce(const star::Grid& g, int p, int q, int side, int best) {
+__device__ __forceinline__ bool w_better(const star::Grid& g, int p, int q, int side, int b, int s) {
+    return side > 0 ? star::inside(g, p, q, b, s) : star::inside(g, p, b, q, s);
+}
+
+// the tournament over point indices with their pencil keys (ties: inside())
+__device__ __forceinline__ int w_reduce(const star::Grid& g, int p, int q, int side, int best, star::Pencil k) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         const int other = __shfl_xor_sync(0xffffffffu, best, o);
-        if (other >= 0 && (best < 0 || w_better(g, p, q, side, best, other))) best = other;
+        const long long on = __shfl_xor_sync(0xffffffffu, k.num, o);
+        const long long od = __shfl_xor_sync(0xffffffffu, k.den, o);
+        if (other < 0 || other == best) continue;
+        bool take = best < 0;
+        if (!take) {
+            const int c = star::pencil_cmp(star::Pencil{on, od}, k, side);
+            take = c > 0 || (c == 0 && w_better(g, p, q, side, best, other));
+        }
+        if (take) {
+            best = other;
+            k = star::Pencil{on, od};
+        }
     }
     return best;
 }
 
-__device__ int w_next(const star::Grid& g, int p, int q, int side) {
-    // star_dt.cuh next_neighbour with the cells of each ring / row chord
-    // spread over the lanes and a tournament after each phase
-    if (star::hull_edge(g, p, q, side)) return -1;
+// The grid search from a first candidate `best` (one on the search side):
+// the cell rows of the search region (star_dt.cuh search_region) outward
+// from p's row, 32 rows at a time, one row per lane, each read over the
+// chord of the winner's circle at the start of its batch and only on the
+// search side of p -> q, the cells of `skip` excluded (already scanned).
+// A tournament after each batch; the region only shrinks as the winner
+// improves (circles through p and q form a pencil), so the rows read with
+// an older circle cover everything a newer one could need.
+__device__ __noinline__ int w_rows(const star::Grid& g, int p, int q, int side, int best, const star::Box& skip) {
     const int lane = threadIdx.x & 31;
-    int lbest = -1;
-    auto consider = [&](int s) {
-        if (s == p || s == q || g.dup[s]) return;
-        const long long o = star::orient(g, p, q, s);
-        if (side > 0 ? o <= 0 : o >= 0) return;
-        if (lbest < 0 || w_better(g, p, q, side, lbest, s)) lbest = s;
-    };
-    const int pcx = star::cell_x(g, g.u[p]), pcy = star::cell_y(g, g.v[p]);
-    const int qcx = star::cell_x(g, g.u[q]), qcy = star::cell_y(g, g.v[q]);
-    // rings 0..2 around p and q: a (2k+1)^2 square each, lanes over its cells
-    int best = -1;
-    for (int o = 0; o < 2; ++o) {
-        const int ox = o == 0 ? pcx : qcx, oy = o == 0 ? pcy : qcy;
-        for (int c = lane; c < 25; c += 32) {
-            const int cx = ox + c % 5 - 2, cy = oy + c / 5 - 2;
-            if (cx < 0 || cy < 0 || cx >= g.gw || cy >= g.gh) continue;
-            const int cell = cy * g.gw + cx;
-            for (int i = g.cell_start[cell]; i < g.cell_start[cell + 1]; ++i) consider(g.cell_items[i]);
-        }
-    }
-    best = w_reduce(g, p, q, side, lbest);
-    if (best < 0) {  // a far point from the column extremes
-        const int cols = g.maxx - g.minx + 1;
-        for (int i = lane; i < cols; i += 32) {
-            if (g.col_lo[i] >= 0) consider(g.col_lo[i]);
-            if (g.col_hi[i] >= 0) consider(g.col_hi[i]);
-        }
-        best = w_reduce(g, p, q, side, lbest);
-        if (best < 0) return -2;
-    }
-    lbest = best;
+    const long long qx = (long long)g.u[q] - g.u[p], qy = (long long)g.v[q] - g.v[p];
+    auto key = [&](int s) { return star::pencil(qx, qy, (long long)g.u[s] - g.u[p], (long long)g.v[s] - g.v[p]); };
+    star::Pencil bk = key(best);
     star::Disc d = side > 0 ? star::disc_of(g, p, q, best) : star::disc_of(g, p, best, q);
-    auto read = [&](int cx, int cy) {
-        return (cx >= pcx - 2 && cx <= pcx + 2 && cy >= pcy - 2 && cy <= pcy + 2) ||
-               (cx >= qcx - 2 && cx <= qcx + 2 && cy >= qcy - 2 && cy <= qcy + 2);
-    };
-    for (int t = 0;; ++t) {
-        bool any = false;
-        for (int sgn = 0; sgn < 2; ++sgn) {
-            if (t == 0 && sgn == 1) continue;
-            const int cy = sgn == 0 ? pcy + t : pcy - t;
-            if (cy < 0 || cy >= g.gh) continue;
-            const double ya = g.miny + double(cy) * g.gs, yb = ya + g.gs - 1;
+    star::Region reg = star::search_region(g, p, q, side, d);
+    const int pcy = star::cell_y(g, g.v[p]);
+    // batch b reads rows pcy + t for t in [-16 b - 15, -16 b] and [16 b + 1, 16 b + 16] (b = 0: pcy - 15 .. pcy + 16)
+    for (int b = 0;; ++b) {
+        const int t = lane < 16 ? -16 * b - lane : 16 * b + lane - 15;
+        const int cy = pcy + t;
+        int lbest = best;
+        star::Pencil lk = bk;
+        const double ya = g.miny + double(cy) * g.gs, yb = ya + g.gs - 1;
+        if (cy >= 0 && cy < g.gh && yb >= reg.y0 && ya <= reg.y1) {
             const double dy = d.cy < ya ? ya - d.cy : (d.cy > yb ? d.cy - yb : 0.0);
-            if (dy > d.r) continue;
-            any = true;
-            const double half = sqrt(d.r * d.r - dy * dy);
-            const int x0 = star::cell_x(g, d.cx - half), x1 = star::cell_x(g, d.cx + half);
-            for (int cx = x0 + lane; cx <= x1; cx += 32) {
-                if (read(cx, cy)) continue;
-                const int cell = cy * g.gw + cx;
-                for (int i = g.cell_start[cell]; i < g.cell_start[cell + 1]; ++i) consider(g.cell_items[i]);
-            }
-            // a tournament only when some lane found a better point
-            if (__any_sync(0xffffffffu, lbest != best)) {
-                const int nb = w_reduce(g, p, q, side, lbest);
-                if (nb != best) {
-                    best = nb;
-                    d = side > 0 ? star::disc_of(g, p, q, best) : star::disc_of(g, p, best, q);
+            if (dy <= d.r) {
+                const double half = sqrt(d.r * d.r - dy * dy);
+                int x0 = star::cell_x(g, d.cx - half > reg.x0 ? d.cx - half : reg.x0);
+                int x1 = star::cell_x(g, d.cx + half < reg.x1 ? d.cx + half : reg.x1);
+                if (star::clip_side(g, p, q, side, ya, yb, x0, x1)) {
+                    const bool in_rows = cy >= skip.y0 && cy <= skip.y1;
+                    star::row_runs(g, cy, x0, x1, in_rows ? skip.x0 : 1, in_rows ? skip.x1 : 0, 1, 0,
+                                   [&](int i0, int i1) {
+                                       for (int i = i0; i < i1; ++i) {
+                                           const int s = g.cell_items[i];
+                                           if (s == p || s == q || g.dup[s]) continue;
+                                           const star::Pencil ps = key(s);
+                                           if (side > 0 ? ps.den <= 0 : ps.den >= 0) continue;
+                                           const int c = star::pencil_cmp(ps, lk, side);
+                                           if (c < 0 || (c == 0 && !w_better(g, p, q, side, lbest, s))) continue;
+                                           lbest = s;
+                                           lk = ps;
+                                       }
+                                   });
                 }
-                lbest = best;
             }
         }
-        const double up = g.miny + double(pcy - t) * g.gs, dn = g.miny + double(pcy + t + 1) * g.gs - 1;
-        if (!any && (pcy - t < 0 || up - 1 < d.cy - d.r) && (pcy + t >= g.gh || dn + 1 > d.cy + d.r)) break;
-        if (pcy - t < 0 && pcy + t >= g.gh) break;
+        FAR_ADD(6, 1);
+        if (__any_sync(0xffffffffu, lbest != best)) {
+            const int nb = w_reduce(g, p, q, side, lbest, lk);
+            if (nb != best) {
+                best = nb;
+                bk = key(best);
+                d = side > 0 ? star::disc_of(g, p, q, best) : star::disc_of(g, p, best, q);
+                reg = star::search_region(g, p, q, side, d);
+            }
+        }
+        // done when the next batch's rows both ways lie outside the region
+        const int up = pcy - 16 * b - 16, dn = pcy + 16 * b + 17;  // nearest rows of batch b + 1
+        const bool up_out = up < 0 || g.miny + double(up + 1) * g.gs - 1 < reg.y0;
+        const bool dn_out = dn >= g.gh || g.miny + double(dn) * g.gs > reg.y1;
+        if (up_out && dn_out) break;
     }
     return best;
 }
 
-__device__ int w_nearest(const star::Grid& g, int p) {
+// No candidate in the gathered box on the search side: a first one from the
+// column extremes (nearest columns first), then w_rows.  -2 if none exists.
+__device__ int w_next_far(const star::Grid& g, int p, int q, int side, const star::Box& skip) {
+    const int lane = threadIdx.x & 31;
+    {  // the 5x5 cells around q: in a fan along the hull the next neighbour is next to q
+        const int qcx = star::cell_x(g, g.u[q]), qcy = star::cell_y(g, g.v[q]);
+        int found = -1;
+        if (lane < 25) {
+            const int cx = qcx + lane % 5 - 2, cy = qcy + lane / 5 - 2;
+            if (cx >= 0 && cy >= 0 && cx < g.gw && cy < g.gh) {
+                const int cell = cy * g.gw + cx;
+                for (int i = g.cell_start[cell]; i < g.cell_start[cell + 1] && found < 0; ++i) {
+                    const int s = g.cell_items[i];
+                    if (s == p || s == q || g.dup[s]) continue;
+                    const long long o = star::orient(g, p, q, s);
+                    if (side > 0 ? o > 0 : o < 0) found = s;
+                }
+            }
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, found >= 0);
+        if (m) return w_rows(g, p, q, side, __shfl_sync(0xffffffffu, found, __ffs(m) - 1), skip);
+    }
+    const int cols = g.maxx - g.minx + 1, c0 = g.u[p] - g.minx;
+    for (int base = 0; base < cols; base += 16) {
+        // lanes 0..15 columns c0 - base - k, lanes 16..31 c0 + base + k
+        const int k = base + (lane & 15);
+        const int i = lane < 16 ? c0 - k : c0 + k;
+        int found = -1;
+        if (i >= 0 && i < cols) {
+            for (int e = 0; e < 2 && found < 0; ++e) {
+                const int s = e == 0 ? g.col_lo[i] : g.col_hi[i];
+                if (s < 0 || s == p || s == q) continue;
+                const long long o = star::orient(g, p, q, s);
+                if (side > 0 ? o > 0 : o < 0) found = s;
+            }
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, found >= 0);
+        if (m) {
+            const int first = __shfl_sync(0xffffffffu, found, __ffs(m) - 1);
+            return w_rows(g, p, q, side, first, star::Box{1, 1, 0, 0});
+        }
+        if (base >= c0 && base >= cols - c0) break;
+    }
+    return -2;
+}
+
+__device__ int w_nearest_local(const star::Grid& g, const WLocal& L, int p) {
+    if (!L.complete) return -3;
+    const int lane = threadIdx.x & 31;
+    unsigned long long best = ~0ull;  // (d2 << 32) | index
+    for (int i = lane; i < L.n; i += 32) {
+        const int w = L.dxy[i];
+        const int sx = int(short(w & 0xffff)), sy = w >> 16;
+        const unsigned long long d2 = (unsigned long long)(sx * sx + sy * sy);
+        if (d2 == 0) continue;
+        const unsigned long long key = (d2 << 32) | unsigned(L.idx[i]);
+        best = key < best ? key : best;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long y = __shfl_xor_sync(0xffffffffu, best, o);
+        best = y < best ? y : best;
+    }
+    const long long px = g.u[p] - g.minx, py = g.v[p] - g.miny;
+    long long m = 1ll << 40;
+    if (L.box.x0 > 0) m = min(m, px - (long long)L.box.x0 * g.gs + 1);
+    if (L.box.y0 > 0) m = min(m, py - (long long)L.box.y0 * g.gs + 1);
+    if (L.box.x1 < g.gw - 1) m = min(m, (long long)(L.box.x1 + 1) * g.gs - px);
+    if (L.box.y1 < g.gh - 1) m = min(m, (long long)(L.box.y1 + 1) * g.gs - py);
+    if (best == ~0ull) return m >= (1ll << 40) ? -1 : -3;
+    return (long long)(best >> 32) < m * m ? int(best & 0xffffffffu) : -3;
+}
+
+__device__ __noinline__ int w_nearest(const star::Grid& g, int p) {
     const int lane = threadIdx.x & 31;
     const int px = star::cell_x(g, g.u[p]), py = star::cell_y(g, g.v[p]);
     unsigned long long best = ~0ull;  // (d2 << 32) | index
@@ -619,88 +915,121 @@ __device__ int w_nearest(const star::Grid& g, int p) {
     return best == ~0ull ? -1 : int(best & 0xffffffffu);
 }
 
-template <class F>
-__device__ int w_walk(const star::Grid& g, int p, bool& closed, F&& on_tri) {
+__device__ __noinline__ int w_step(const star::Grid& g, const WLocal& L, int p, int q, int side) {
+    int start;
+    long long t0 = FAR_CLOCK();
+    const int r = w_next_local(g, L, p, q, side, start);
+    FAR_ADD(2, 1);
+    FAR_ADD(3, FAR_CLOCK() - t0);
+    if (r != -3) return r;
+    t0 = FAR_CLOCK();
+    if (start >= 0) {
+        const int x = w_rows(g, p, q, side, start, L.box);
+        FAR_ADD(4, 1);
+        FAR_ADD(5, FAR_CLOCK() - t0);
+        return x;
+    }
+    const int x = w_next_far(g, p, q, side, L.complete ? L.box : star::Box{1, 1, 0, 0});
+    FAR_ADD(7, 1);
+    FAR_ADD(8, FAR_CLOCK() - t0);
+    return x;
+}
+
+// The star of p into tb ((b, c) per triangle (p, b, c): counter-clockwise
+// from p's nearest neighbour, then clockwise for a hull vertex).  Returns
+// the triangle count, -2 on a failed search or more than kFarTris.
+__device__ __noinline__ int w_walk(const star::Grid& g, const WLocal& L, int p, bool& closed, int* tb) {
+    const int lane = threadIdx.x & 31;
     closed = false;
     if (g.dup[p]) return 0;
-    const int q0 = w_nearest(g, p);
+    const long long t0 = FAR_CLOCK();
+    int q0 = w_nearest_local(g, L, p);
+    if (q0 == -3) q0 = w_nearest(g, p);
+    FAR_ADD(9, FAR_CLOCK() - t0);
     if (q0 < 0) return 0;
-    int count = 0, cur = q0;
-    for (int guard = 0; guard <= g.n; ++guard) {
-        const int r = w_next(g, p, cur, +1);
-        if (r == -2) return -2;
-        if (r < 0) break;
-        on_tri(p, cur, r);
-        ++count;
-        if (r == q0) {
-            closed = true;
-            return count;
+    int count = 0;
+    for (int dir = 0; dir < 2; ++dir) {
+        const int side = dir == 0 ? +1 : -1;
+        int cur = q0;
+        for (int guard = 0; guard <= g.n; ++guard) {
+            const int r = w_step(g, L, p, cur, side);
+            if (r == -2) return -2;
+            if (r < 0) break;
+            if (count == kFarTris) return -2;
+            if (lane == 0) {
+                tb[2 * count] = side > 0 ? cur : r;
+                tb[2 * count + 1] = side > 0 ? r : cur;
+            }
+            ++count;
+            if (side > 0 && r == q0) {
+                closed = true;
+                return count;
+            }
+            cur = r;
         }
-        cur = r;
-    }
-    cur = q0;
-    for (int guard = 0; guard <= g.n; ++guard) {
-        const int r = w_next(g, p, cur, -1);
-        if (r == -2) return -2;
-        if (r < 0) break;
-        on_tri(p, r, cur);
-        ++count;
-        cur = r;
     }
     return count;
 }
 
-__global__ void k_star_hard(StarArgs a) {
+__global__ void __launch_bounds__(kFarT) k_star_far(StarArgs a) {
+    __shared__ int s_idx[kFarT / 32][kFarCap], s_dxy[kFarT / 32][kFarCap];
+    __shared__ int s_tri[kFarT / 32][2 * kFarTris];  // (b, c) of each triangle (p, b, c), walk order
     const int f = blockIdx.y;
-    const int lane = threadIdx.x & 31;
-    const int nhard = min(a.flags[(long long)f * kStarFlagInts + 6], a.scap);
-    const int warps = gridDim.x * (blockDim.x >> 5);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int n = min(a.flags[(long long)f * kStarFlagInts + 5], a.scap);
+    const int warps = gridDim.x * (kFarT >> 5);
     const star::Grid g = make_grid(a, f);
     const long long sb = (long long)f * a.scap;
-    const int* su = a.su + sb;
-    const int* sv = a.sv + sb;
-    const double* sd = a.sd + sb;
     int* tris = a.tris + 3 * (long long)f * a.pitch;
-    for (int h = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); h < nhard; h += warps) {
-        const int p = a.hard2[sb + h];
+    WLocal L;
+    L.idx = s_idx[wid];
+    L.dxy = s_dxy[wid];
+    int* tb = s_tri[wid];
+    for (int h = blockIdx.x * (kFarT >> 5) + wid; h < n; h += warps) {
+        const int p = a.hard[sb + h];
+        __syncwarp();
+        const long long tg = FAR_CLOCK();
+        w_gather(g, p, L);
+        FAR_ADD(0, 1);
+        FAR_ADD(1, FAR_CLOCK() - tg);
         bool closed;
-        HullCheck hc;  // kept on the fly: one walk serves both purposes
-        const int hu = su[p], hv = sv[p];
-        const int r = w_walk(g, p, closed, [&](int t0, int t1, int t2) {
-            if (lane == 0 && t0 < t1 && t0 < t2) {
-                const int slot = atomicAdd(a.tri_count + f, 1);
-                if (slot < a.pitch) {
-                    tris[3 * (long long)slot] = t0;
-                    tris[3 * (long long)slot + 1] = t1;
-                    tris[3 * (long long)slot + 2] = t2;
-                }
-            }
-            hc.add(su, sv, sd, hu, hv, a.max_disp, t0, t1, t2);
-        });
-        if (r == -2) {
+        const int nt = w_walk(g, L, p, closed, tb);
+        FAR_ADD(10, FAR_CLOCK() - tg);
+        if (nt < 0) {  // a failed search, or more than kFarTris triangles
             if (lane == 0) set_fail(a, f);
             continue;
         }
-        if (closed || r == 0) continue;
-        // the fan, if needed, is written by a third walk (rare)
-        bool need_fan = !hc.covered && !(hc.agree && !hc.suspect) && hc.n_inc > 0 && hu >= 0 && hu < a.W &&
-                        hv >= 0 && hv < a.H;
-        int* fan = nullptr;
-        if (lane == 0) {
-            hull_outcome(a, f, p, hc, [&](int* out) { fan = out; });
-        }
-        if (need_fan) {
-            fan = (int*)__shfl_sync(0xffffffffu, (unsigned long long)fan, 0);
-            int k = 0;
-            w_walk(g, p, closed, [&](int t0, int t1, int t2) {
-                if (lane == 0 && fan && k < hc.n_inc) {
-                    fan[3 * k] = t0;
-                    fan[3 * k + 1] = t1;
-                    fan[3 * k + 2] = t2;
+        __syncwarp();
+        // the triangles p writes (it is their smallest vertex): one slot range
+        int ne = 0;
+        for (int i = lane; i < nt; i += 32) ne += p < tb[2 * i] && p < tb[2 * i + 1];
+        const int incl = w_scan(ne);
+        int slot = 0;
+        if (lane == 31 && incl > 0) slot = atomicAdd(a.tri_count + f, incl);
+        slot = __shfl_sync(0xffffffffu, slot, 31) + incl - ne;
+        for (int i = lane; i < nt; i += 32)
+            if (p < tb[2 * i] && p < tb[2 * i + 1]) {
+                if (slot < a.pitch) {
+                    tris[3 * (long long)slot] = p;
+                    tris[3 * (long long)slot + 1] = tb[2 * i];
+                    tris[3 * (long long)slot + 2] = tb[2 * i + 1];
                 }
-                ++k;
-            });
-        }
+                ++slot;
+            }
+        if (closed || nt == 0 || lane != 0) continue;
+        // a hull vertex: its bookkeeping (lane 0)
+        const int* su = a.su + sb;
+        const int* sv = a.sv + sb;
+        const double* sd = a.sd + sb;
+        HullCheck hc;
+        for (int i = 0; i < nt; ++i) hc.add(su, sv, sd, su[p], sv[p], a.max_disp, p, tb[2 * i], tb[2 * i + 1]);
+        hull_outcome(a, f, p, hc, [&](int* out) {
+            for (int i = 0; i < nt; ++i) {
+                out[3 * i] = p;
+                out[3 * i + 1] = tb[2 * i];
+                out[3 * i + 2] = tb[2 * i + 1];
+            }
+        });
     }
 }
 
@@ -800,6 +1129,7 @@ int launch_star_mesh(const StarArgs& a, int max_points, cudaStream_t st) {
     k_grid_scan<<<a.frames, 1024, 0, st>>>(a); STAR_CHECK("k_grid_scan");
     k_grid_fill<<<grid, 256, 0, st>>>(a); STAR_CHECK("k_grid_fill");
     k_grid_dup<<<grid, 256, 0, st>>>(a); STAR_CHECK("k_grid_dup");
+    k_grid_pack<<<grid, 256, 0, st>>>(a); STAR_CHECK("k_grid_pack");
     cudaMemsetAsync(a.col_key, 0xff, sizeof(unsigned long long) * 2 * a.W * a.frames, st);
     k_col_key<<<grid, 256, 0, st>>>(a); STAR_CHECK("k_col_key");
     k_col_decode<<<dim3((2 * a.W + 255) / 256, a.frames), 256, 0, st>>>(a);
@@ -808,17 +1138,14 @@ int launch_star_mesh(const StarArgs& a, int max_points, cudaStream_t st) {
         cudaFuncSetAttribute(k_hull, cudaFuncAttributeMaxDynamicSharedMemorySize, hsm);
         k_hull<<<a.frames, 256, hsm, st>>>(a);
     } STAR_CHECK("k_hull");
-    const int smem = 2 * star::kLocalMax * kT * int(sizeof(int));
-    cudaFuncSetAttribute(k_star, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k_star<<<dim3((max_points + kT - 1) / kT, a.frames), kT, smem, st>>>(a);
     {
-        const int wsm = 2 * kWideCap * kWideT * int(sizeof(int));
-        cudaFuncSetAttribute(k_star_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, wsm);
-        // deferred points are a few percent: size the grid for 1/8 of them
-        k_star_wide<<<dim3((max_points / 8 + kWideT - 1) / kWideT + 1, a.frames), kWideT, wsm, st>>>(a);
+        const int tiles = ((a.gw + star::kTileCells - 1) / star::kTileCells) * ((a.gh + star::kTileCells - 1) / star::kTileCells);
+        k_star<<<dim3(tiles, a.frames), kTileT, 0, st>>>(a);
     }
     STAR_CHECK("k_star");
-    k_star_hard<<<dim3(128, a.frames), 128, 0, st>>>(a); STAR_CHECK("k_star_hard");
+    // deferred points are a few percent: a warp each, the grid strided
+    k_star_far<<<dim3((max_points / 32 + 3) / 4 + 1, a.frames), kFarT, 0, st>>>(a);
+    STAR_CHECK("k_star_far");
 #ifdef PS_STAR_PROFILE
     k_star_report<<<1, 1, 0, st>>>();
 #endif

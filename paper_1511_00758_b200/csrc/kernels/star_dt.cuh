@@ -55,7 +55,8 @@ struct Grid {
     // them, delaunay.cpp:116-118), -1 off the hull (build_hull)
     const int* hnext;
     const int* hprev;
-    int flat;  // every point on one line: no triangle at all
+    int flat;    // every point on one line: no triangle at all
+    double igs;  // 1 / gs
 };
 
 PS_HD long long orient(const Grid& g, int a, int b, int c) {
@@ -93,12 +94,13 @@ struct Box {
     int x0, y0, x1, y1;  // cell index range, inclusive
 };
 
+// (the cell searches are conservative by a pixel: a product by 1 / gs does)
 PS_HD int cell_x(const Grid& g, double x) {
-    int c = int(floor((x - g.minx) / g.gs));
+    int c = int(floor((x - g.minx) * g.igs));
     return c < 0 ? 0 : (c >= g.gw ? g.gw - 1 : c);
 }
 PS_HD int cell_y(const Grid& g, double y) {
-    int c = int(floor((y - g.miny) / g.gs));
+    int c = int(floor((y - g.miny) * g.igs));
     return c < 0 ? 0 : (c >= g.gh ? g.gh - 1 : c);
 }
 
@@ -211,10 +213,52 @@ struct Disc {
 PS_HD Disc disc_of(const Grid& g, int a, int b, int c) {
     const double ax = g.u[a], ay = g.v[a];
     const double bx = g.u[b] - ax, by = g.v[b] - ay, cx = g.u[c] - ax, cy = g.v[c] - ay;
-    const double D = 2.0 * (bx * cy - by * cx);
+    const double iD = 0.5 / (bx * cy - by * cx);
     const double bq = bx * bx + by * by, cq = cx * cx + cy * cy;
-    const double ux = (cy * bq - by * cq) / D, uy = (bx * cq - cx * bq) / D;
+    const double ux = (cy * bq - by * cq) * iD, uy = (bx * cq - cx * bq) * iD;
     return Disc{ax + ux, ay + uy, sqrt(ux * ux + uy * uy) * (1.0 + 1e-9) + 1.0};
+}
+// Where a point beating the winner of a p -> q search can lie: inside the
+// winner's circle and strictly on the search side of p -> q.  When the
+// circle's centre is on the other side that part is the minor segment cut
+// by the chord pq, which lies within its sagitta h of the chord (for the
+// near-collinear triangles along the hull the circle is huge but h is
+// tiny); else the circle's bounding box.  Pixel coordinates, a margin kept.
+struct Region {
+    double x0, y0, x1, y1;
+};
+PS_HD Region search_region(const Grid& g, int p, int q, int side, const Disc& d) {
+    Region box{d.cx - d.r, d.cy - d.r, d.cx + d.r, d.cy + d.r};
+    // the points' bounding box: where the circle pokes out of it, only the
+    // part inside matters (the circle's extent across the box's bounds)
+    if (box.x0 < g.minx) box.x0 = g.minx;
+    if (box.x1 > g.maxx) box.x1 = g.maxx;
+    if (box.y0 < g.miny) box.y0 = g.miny;
+    if (box.y1 > g.maxy) box.y1 = g.maxy;
+    {
+        const double dx = d.cx < box.x0 ? box.x0 - d.cx : (d.cx > box.x1 ? d.cx - box.x1 : 0.0);
+        const double dy = d.cy < box.y0 ? box.y0 - d.cy : (d.cy > box.y1 ? d.cy - box.y1 : 0.0);
+        const double hy = sqrt(d.r * d.r > dx * dx ? d.r * d.r - dx * dx : 0.0) + 1.0;
+        const double hx = sqrt(d.r * d.r > dy * dy ? d.r * d.r - dy * dy : 0.0) + 1.0;
+        if (d.cy - hy > box.y0) box.y0 = d.cy - hy;
+        if (d.cy + hy < box.y1) box.y1 = d.cy + hy;
+        if (d.cx - hx > box.x0) box.x0 = d.cx - hx;
+        if (d.cx + hx < box.x1) box.x1 = d.cx + hx;
+    }
+    const double pu = g.u[p], pv = g.v[p], qu = g.u[q], qv = g.v[q];
+    const double ex = qu - pu, ey = qv - pv;
+    const double cs = ex * (d.cy - pv) - ey * (d.cx - pu);  // > 0: centre left of p -> q
+    if ((side > 0) == (cs > 0)) return box;
+    const double r0 = (d.r - 1.0) / (1.0 + 1e-9);  // disc_of's radius without its margin
+    const double a = 0.25 * (ex * ex + ey * ey);   // (half chord)^2
+    const double h = a / (r0 + sqrt(r0 * r0 > a ? r0 * r0 - a : 0.0)) + 2.0;
+    const double x0 = (pu < qu ? pu : qu) - h, x1 = (pu > qu ? pu : qu) + h;
+    const double y0 = (pv < qv ? pv : qv) - h, y1 = (pv > qv ? pv : qv) + h;
+    if (x0 > box.x0) box.x0 = x0;
+    if (x1 < box.x1) box.x1 = x1;
+    if (y0 > box.y0) box.y0 = y0;
+    if (y1 < box.y1) box.y1 = y1;
+    return box;
 }
 // squared distance from (x, y) to the pixel box of cell (cx, cy)
 PS_HD double cell_dist2(const Grid& g, int cx, int cy, double x, double y) {
@@ -223,6 +267,79 @@ PS_HD double cell_dist2(const Grid& g, int cx, int cy, double x, double y) {
     const double dx = x < x0 ? x0 - x : (x > x1 ? x - x1 : 0.0);
     const double dy = y < y0 ? y0 - y : (y > y1 ? y - y1 : 0.0);
     return dx * dx + dy * dy;
+}
+
+// The cells of row cy from x0 to x1 (inclusive) except the column ranges
+// [e0a, e0b] and [e1a, e1b] (empty when a > b), as runs of consecutive cells:
+// a run's points are consecutive in cell_items, so `f(i0, i1)` receives
+// item ranges — an empty stretch of a row costs one lookup, not one per cell.
+template <class F>
+PS_HD void row_runs(const Grid& g, int cy, int x0, int x1, int e0a, int e0b, int e1a, int e1b, F&& f) {
+    if (e0a > e0b || (e1a <= e1b && e1a < e0a)) {
+        const int ta = e0a, tb = e0b;
+        e0a = e1a;
+        e0b = e1b;
+        e1a = ta;
+        e1b = tb;
+    }
+    const int rb = cy * g.gw;
+    int cur = x0;
+    auto emit = [&](int a, int b) {
+        const int i0 = g.cell_start[rb + a], i1 = g.cell_start[rb + b + 1];
+        if (i0 < i1) f(i0, i1);
+    };
+    if (e0a <= e0b && e0b >= cur && e0a <= x1) {
+        if (e0a > cur) emit(cur, e0a - 1);
+        cur = e0b + 1 > cur ? e0b + 1 : cur;
+    }
+    if (e1a <= e1b && e1b >= cur && e1a <= x1 && cur <= x1) {
+        if (e1a > cur) emit(cur, e1a - 1);
+        cur = e1b + 1 > cur ? e1b + 1 : cur;
+    }
+    if (cur <= x1) emit(cur, x1);
+}
+
+// Clips the cell range [x0, x1] of the pixel-row band [ya, yb] to the cells
+// that can hold a point strictly on the search side of p -> q (left for
+// side > 0); false when none can.
+PS_HD bool clip_side(const Grid& g, int p, int q, int side, double ya, double yb, int& x0, int& x1) {
+    // side * (qx * (y - pv) - qy * (x - pu)) > 0, linear in x and y
+    const double sg = side > 0 ? 1.0 : -1.0, pu = g.u[p], pv = g.v[p];
+    const double qx = double(g.u[q]) - pu, qy = double(g.v[q]) - pv;
+    const double ax = -sg * qy;
+    const double b0 = sg * qx * (ya - pv) - ax * pu, b1 = sg * qx * (yb - pv) - ax * pu;
+    const double bm = b0 > b1 ? b0 : b1;
+    if (ax > 0) {
+        const int c = cell_x(g, -bm / ax - 1.0);
+        x0 = c > x0 ? c : x0;
+    } else if (ax < 0) {
+        const int c = cell_x(g, -bm / ax + 1.0);
+        x1 = c < x1 ? c : x1;
+    } else if (bm <= 0) {
+        return false;
+    }
+    return x0 <= x1;
+}
+
+// The pencil of circles through p and q: relative to p, the circle through
+// p, q and s has its centre at q / 2 + t(s) * perp(q), perp(q) = (-qy, qx),
+// with t(s) = num(s) / (2 den(s)), num = |s|^2 - q.s, den = cross(q, s) (> 0
+// left of p -> q).  A point s on the search side lies inside the circle of
+// the current winner b exactly when t(s) < t(b) (left) or t(s) > t(b)
+// (right); compared as num(s) * den(b) vs num(b) * den(s) — both dens share
+// the side's sign — which is exact in int64 for offsets below 2^14.  Equal
+// products: cocircular (the exact rule of inside() decides).
+struct Pencil {
+    long long num, den;
+};
+PS_HD Pencil pencil(long long qx, long long qy, long long sx, long long sy) {
+    return Pencil{sx * (sx - qx) + sy * (sy - qy), qx * sy - qy * sx};
+}
+// +1: s beats b (strictly inside b's circle), -1: b stays, 0: cocircular
+PS_HD int pencil_cmp(const Pencil& s, const Pencil& b, int side) {
+    const long long l = s.num * b.den, r = b.num * s.den;
+    if (l == r) return 0;
+    return (side > 0 ? l < r : l > r) ? 1 : -1;
 }
 
 // Next star neighbour of p after q: counter-clockwise (side > 0: r left of
@@ -239,14 +356,19 @@ PS_HD int next_neighbour(const Grid& g, int p, int q, int side) {
     if (hull_edge(g, p, q, side)) return -1;
     int r = -1;
     Disc d{0.0, 0.0, 0.0};
+    const long long qx = (long long)g.u[q] - g.u[p], qy = (long long)g.v[q] - g.v[p];
+    Pencil rb{0, 0};
     auto consider = [&](int s) {
         if (s == p || s == q || g.dup[s]) return;
-        const long long o = orient(g, p, q, s);
-        if (side > 0 ? o <= 0 : o >= 0) return;
-        if (r < 0 || (side > 0 ? inside(g, p, q, r, s) : inside(g, p, r, q, s))) {
-            r = s;
-            d = side > 0 ? disc_of(g, p, q, r) : disc_of(g, p, r, q);
+        const Pencil ps = pencil(qx, qy, (long long)g.u[s] - g.u[p], (long long)g.v[s] - g.v[p]);
+        if (side > 0 ? ps.den <= 0 : ps.den >= 0) return;
+        if (r >= 0) {
+            const int c = pencil_cmp(ps, rb, side);
+            if (c < 0 || (c == 0 && !(side > 0 ? inside(g, p, q, r, s) : inside(g, p, r, q, s)))) return;
         }
+        r = s;
+        rb = ps;
+        d = side > 0 ? disc_of(g, p, q, r) : disc_of(g, p, r, q);
     };
     // rings around p and around q until a candidate appears: the next
     // neighbour is next to p, or — in a long thin hull triangle — next to q
@@ -273,42 +395,45 @@ PS_HD int next_neighbour(const Grid& g, int p, int q, int side) {
         // nothing nearby: a far point on that side (a long thin triangle
         // along the hull); any one starts the circle search, and one exists
         // among the column extremes (they include every hull vertex)
-        const int cols = g.maxx - g.minx + 1;
-        for (int i = 0; i < cols && r < 0; ++i)
-            for (int e = 0; e < 2 && r < 0; ++e) {
-                const int w = e == 0 ? g.col_lo[i] : g.col_hi[i];
+        // (columns outward from p's: a near one keeps the first circle small)
+        const int cols = g.maxx - g.minx + 1, c0 = g.u[p] - g.minx;
+        for (int k2 = 0; r < 0 && (c0 - k2 >= 0 || c0 + k2 < cols); ++k2)
+            for (int e = 0; e < 4 && r < 0; ++e) {
+                const int i = e < 2 ? c0 - k2 : c0 + k2;
+                if (i < 0 || i >= cols || (k2 == 0 && e >= 2)) continue;
+                const int w = (e & 1) == 0 ? g.col_lo[i] : g.col_hi[i];
                 if (w >= 0) consider(w);
             }
         if (r < 0) return -2;
     }
     const int done = k - 1;  // rings 0..done around both cells are read
-    auto read = [&](int cx, int cy) {
-        return (cx >= pcx - done && cx <= pcx + done && cy >= pcy - done && cy <= pcy + done) ||
-               (cx >= qcx - done && cx <= qcx + done && cy >= qcy - done && cy <= qcy + done);
-    };
     const int py = pcy;
     for (int t = 0;; ++t) {
-        bool any = false;
+        const Region reg = search_region(g, p, q, side, d);
         for (int sgn = 0; sgn < 2; ++sgn) {
             if (t == 0 && sgn == 1) continue;
             const int cy = sgn == 0 ? py + t : py - t;
             if (cy < 0 || cy >= g.gh) continue;
             const double ya = g.miny + double(cy) * g.gs, yb = ya + g.gs - 1;
+            if (yb < reg.y0 || ya > reg.y1) continue;
             const double dy = d.cy < ya ? ya - d.cy : (d.cy > yb ? d.cy - yb : 0.0);
             if (dy > d.r) continue;
-            any = true;
             const double half = sqrt(d.r * d.r - dy * dy);
-            const int x0 = cell_x(g, d.cx - half), x1 = cell_x(g, d.cx + half);
-            for (int cx = x0; cx <= x1; ++cx) {
-                if (read(cx, cy)) continue;
-                const int c = cy * g.gw + cx;
-                for (int i = g.cell_start[c]; i < g.cell_start[c + 1]; ++i) consider(g.cell_items[i]);
-            }
+            int x0 = cell_x(g, d.cx - half > reg.x0 ? d.cx - half : reg.x0);
+            int x1 = cell_x(g, d.cx + half < reg.x1 ? d.cx + half : reg.x1);
+            if (!clip_side(g, p, q, side, ya, yb, x0, x1)) continue;
+            const bool rp = cy >= pcy - done && cy <= pcy + done, rq = cy >= qcy - done && cy <= qcy + done;
+            row_runs(g, cy, x0, x1, rp ? pcx - done : 1, rp ? pcx + done : 0, rq ? qcx - done : 1,
+                     rq ? qcx + done : 0, [&](int i0, int i1) {
+                         for (int i = i0; i < i1; ++i) consider(g.cell_items[i]);
+                     });
         }
-    // stop once both rows lie beyond the circle's vertical extent
-        const double up = g.miny + double(py - t) * g.gs, dn = g.miny + double(py + t + 1) * g.gs - 1;
-        if (!any && (py - t < 0 || up - 1 < d.cy - d.r) && (py + t >= g.gh || dn + 1 > d.cy + d.r)) break;
-        if (py - t < 0 && py + t >= g.gh) break;
+        // stop once the next rows both ways lie outside the region (it only
+        // shrinks as the winner improves: circles through p, q form a pencil)
+        const Region now = search_region(g, p, q, side, d);
+        const bool up = py - t <= 0 || g.miny + double(py - t) * g.gs - 1 < now.y0;
+        const bool dn = py + t >= g.gh - 1 || g.miny + double(py + t + 1) * g.gs > now.y1;
+        if (up && dn) break;
     }
     return r;
 }
@@ -368,7 +493,7 @@ struct Local {
 PS_HD void gather(const Grid& g, int p, int radius, Local& L) {
     L.n = 0;
     if (g.maxx - g.minx >= 4096 || g.maxy - g.miny >= 4096 || radius * g.gs >= 16000) {
-        L.complete = false;  // incircle_rel's exactness bound / 16-bit offsets
+        L.complete = false;  // next_local's int32 bound / 16-bit offsets
         return;
     }
     const int px = cell_x(g, g.u[p]), py = cell_y(g, g.v[p]);
@@ -392,20 +517,12 @@ PS_HD void gather(const Grid& g, int p, int radius, Local& L) {
         }
 }
 
-// s inside the circle through p (origin) and the counter-clockwise a, b:
-// the lifted 3x3 determinant relative to p, exact in binary64 while the
-// coordinates differ by < 2^12 (|det| < 2^52); 0 = cocircular -> exact rule.
-PS_HD double incircle_rel(double ax, double ay, double bx, double by, double sx, double sy) {
-    const double aq = ax * ax + ay * ay, bq = bx * bx + by * by, sq = sx * sx + sy * sy;
-    return ax * (by * sq - sy * bq) - ay * (bx * sq - sx * bq) + aq * (bx * sy - sx * by);
-}
-
 // The cells whose points could lie within the circle through p, q, r
 // (relative coordinates; r, q counter-clockwise after p for side > 0).
 PS_HD Box circle_box_rel(const Grid& g, int p, double qx, double qy, double rx, double ry) {
-    const double D = 2.0 * (qx * ry - qy * rx);
+    const double iD = 0.5 / (qx * ry - qy * rx);
     const double qq = qx * qx + qy * qy, rr = rx * rx + ry * ry;
-    const double ux = (ry * qq - qy * rr) / D, uy = (qx * rr - rx * qq) / D;
+    const double ux = (ry * qq - qy * rr) * iD, uy = (qx * rr - rx * qq) * iD;
     const double rad = sqrt(ux * ux + uy * uy) * (1.0 + 1e-9) + 1.0;
     const double cx = g.u[p] + ux, cy = g.v[p] + uy;
     return Box{cell_x(g, cx - rad), cell_y(g, cy - rad), cell_x(g, cx + rad), cell_y(g, cy + rad)};
@@ -413,36 +530,36 @@ PS_HD Box circle_box_rel(const Grid& g, int p, double qx, double qy, double rx, 
 
 // Local next neighbour: -1 hull edge, -3 not certified (use the grid search).
 PS_HD int next_local(const Grid& g, const Local& L, int p, int q, int side) {
-    const long long qx = g.u[q] - g.u[p], qy = g.v[q] - g.v[p];
-    int best = -1;
     if (hull_edge(g, p, q, side)) return -1;
     if (!L.complete) return -3;
-    int bx = 0, by = 0;
+    // relative offsets below 2^12 (gather): every product below fits int32
+    const int qx = g.u[q] - g.u[p], qy = g.v[q] - g.v[p];
+    int bi = -1;
+    int bnum = 0, bden = 0;
     for (int i = 0; i < L.n; ++i) {
-        const int s = L.id(i);
-        if (s == q) continue;
-        const int sx = L.dx(i), sy = L.dy(i);
-        const long long o = qx * sy - qy * sx;  // orient(p, q, s)
-        if (side > 0 ? o <= 0 : o >= 0) continue;
-        if (best < 0) {
-            best = s;
-            bx = sx;
-            by = sy;
-            continue;
+        const int w = L.dxy[i * L.stride];
+        const int sx = int(short(w & 0xffff)), sy = w >> 16;
+        const int den = qx * sy - qy * sx;  // orient(p, q, s); q itself gives 0
+        if (side > 0 ? den <= 0 : den >= 0) continue;
+        const int num = sx * (sx - qx) + sy * (sy - qy);
+        if (bi >= 0) {
+            const long long l = (long long)num * bden, r = (long long)bnum * den;
+            if (l == r) {  // cocircular: the exact perturbed rule
+                const int s = L.id(i), b = L.id(bi);
+                if (!(side > 0 ? inside(g, p, q, b, s) : inside(g, p, b, q, s))) continue;
+            } else if (side > 0 ? l > r : l < r) {
+                continue;
+            }
         }
-        const double det = side > 0 ? incircle_rel(double(qx), double(qy), double(bx), double(by), double(sx), double(sy))
-                                    : incircle_rel(double(bx), double(by), double(qx), double(qy), double(sx), double(sy));
-        const bool in = det != 0.0 ? det < 0.0 : (side > 0 ? inside(g, p, q, best, s) : inside(g, p, best, q, s));
-        if (in) {
-            best = s;
-            bx = sx;
-            by = sy;
-        }
+        bi = i;
+        bnum = num;
+        bden = den;
     }
-    if (best >= 0) {
-        const Box need = side > 0 ? circle_box_rel(g, p, double(qx), double(qy), double(bx), double(by))
-                                  : circle_box_rel(g, p, double(bx), double(by), double(qx), double(qy));
-        return covers(L.box, need) ? best : -3;
+    if (bi >= 0) {
+        const double bx = L.dx(bi), by = L.dy(bi);
+        const Box need = side > 0 ? circle_box_rel(g, p, double(qx), double(qy), bx, by)
+                                  : circle_box_rel(g, p, bx, by, double(qx), double(qy));
+        return covers(L.box, need) ? L.id(bi) : -3;
     }
     return -3;  // not a hull edge: the neighbour lies beyond the gathered cells
 }
@@ -472,6 +589,176 @@ PS_HD int nearest_local(const Grid& g, const Local& L, int p) {
     if (L.box.y1 < g.gh - 1) lower((long long)(L.box.y1 + 1) * g.gs - py);
     if (best < 0) return m >= (1ll << 40) ? -1 : -3;
     return bd < m * m ? best : -3;
+}
+
+// inside() for a cocircular quadruple given by offsets from p: triangle
+// (p, a, b) counter-clockwise, d the fourth point (all distinct); the same
+// lifting of the lexicographically largest point.
+PS_HD bool inside_tie_rel(int ax, int ay, int bx, int by, int dx, int dy) {
+    // lexicographic maximum of p = (0, 0), a, b, d
+    int mx = 0, my = 0, m = 0;
+    auto take = [&](int x, int y, int k) {
+        if (x > mx || (x == mx && y > my)) {
+            mx = x;
+            my = y;
+            m = k;
+        }
+    };
+    take(ax, ay, 1);
+    take(bx, by, 2);
+    take(dx, dy, 3);
+    auto orient_rel = [](long long x0, long long y0, long long x1, long long y1, long long x2, long long y2) {
+        return (x1 - x0) * (y2 - y0) - (y1 - y0) * (x2 - x0);
+    };
+    if (m == 3) return false;
+    if (m == 0) return orient_rel(ax, ay, bx, by, dx, dy) > 0;
+    if (m == 1) return orient_rel(bx, by, 0, 0, dx, dy) > 0;
+    return orient_rel(0, 0, ax, ay, dx, dy) > 0;
+}
+
+// ---- the tiled fast path (star.cu k_star): a block holds the points of a
+// tile of cells plus a halo of kTileHalo cells in shared memory, compacted
+// per cell (duplicates dropped) with coordinates relative to the region's
+// pixel origin; a point's searches read the rows of its (2R+1)^2-cell box
+// there as runs of consecutive entries.  Same certificates as Local.
+constexpr int kTileCells = 8;  // tile width in cells
+constexpr int kTileHalo = 4;   // halo (the largest search radius)
+constexpr int kTileRegion = kTileCells + 2 * kTileHalo;
+
+struct Tile {
+    const int* start;  // kTileRegion^2 + 1 offsets into xy / id, region cells row-major
+    const int* xy;     // (y << 16) | x relative to the region's pixel origin
+    const int* id;     // point index
+    int cx0, cy0;      // grid cell of region cell (0, 0) (may lie outside the grid)
+};
+
+// The point of p's walk state: its grid cell, region-relative pixel, absolute pixel.
+struct TilePoint {
+    int p, pcx, pcy, pxr, pyr, pu, pv;
+    int hprev, hnext;  // hull neighbours (-1 off the hull)
+};
+
+// Rows of p's box of radius R (grid cells, clipped to the grid) in region
+// coordinates: calls f(i0, i1) per row.
+template <class F>
+PS_HD void tile_box(const Grid& g, const Tile& T, const TilePoint& P, int R, Box& box, F&& f) {
+    box = Box{P.pcx - R < 0 ? 0 : P.pcx - R, P.pcy - R < 0 ? 0 : P.pcy - R,
+              P.pcx + R >= g.gw ? g.gw - 1 : P.pcx + R, P.pcy + R >= g.gh ? g.gh - 1 : P.pcy + R};
+    const int x0 = box.x0 - T.cx0, x1 = box.x1 - T.cx0;
+    for (int y = box.y0 - T.cy0; y <= box.y1 - T.cy0; ++y) {
+        const int i0 = T.start[y * kTileRegion + x0], i1 = T.start[y * kTileRegion + x1 + 1];
+        if (i0 < i1) f(i0, i1);
+    }
+}
+
+// Nearest other point within the box, certified when every point outside
+// is strictly farther; -1 no other point in the set, -3 not certified.
+// (bx, by): its offset from p.
+PS_HD int tile_nearest(const Grid& g, const Tile& T, const TilePoint& P, int R, int& bx, int& by) {
+    int best = -1;
+    int bd = 0;
+    Box box;
+    tile_box(g, T, P, R, box, [&](int i0, int i1) {
+        for (int i = i0; i < i1; ++i) {
+            const int w = T.xy[i];
+            const int sx = (w & 0xffff) - P.pxr, sy = (w >> 16) - P.pyr;
+            const int d2 = sx * sx + sy * sy;
+            if (d2 == 0) continue;  // p itself (duplicates are not in the region)
+            if (best >= 0 && (d2 > bd || (d2 == bd && T.id[i] > best))) continue;
+            best = T.id[i];
+            bd = d2;
+            bx = sx;
+            by = sy;
+        }
+    });
+    const long long px = P.pu - g.minx, py = P.pv - g.miny;
+    long long m = 1ll << 40;
+    auto lower = [&](long long x) { m = x < m ? x : m; };
+    if (box.x0 > 0) lower(px - (long long)box.x0 * g.gs + 1);
+    if (box.y0 > 0) lower(py - (long long)box.y0 * g.gs + 1);
+    if (box.x1 < g.gw - 1) lower((long long)(box.x1 + 1) * g.gs - px);
+    if (box.y1 < g.gh - 1) lower((long long)(box.y1 + 1) * g.gs - py);
+    if (best < 0) return m >= (1ll << 40) ? -1 : -3;
+    return (long long)bd < m * m ? best : -3;
+}
+
+// Next neighbour of p after q (offset (qx, qy)) within the box: -1 hull
+// edge, -3 not certified; (bx, by): the winner's offset.
+PS_HD int tile_next(const Grid& g, const Tile& T, const TilePoint& P, int R, int q, int qx, int qy, int side,
+                    int& bx, int& by) {
+    if (g.flat || (side > 0 ? P.hprev == q : P.hnext == q)) return -1;
+    int bi = -1, bnum = 0, bden = 0;
+    Box box;
+    tile_box(g, T, P, R, box, [&](int i0, int i1) {
+        for (int i = i0; i < i1; ++i) {
+            const int w = T.xy[i];
+            const int sx = (w & 0xffff) - P.pxr, sy = (w >> 16) - P.pyr;
+            const int den = qx * sy - qy * sx;  // orient(p, q, s); p and q give 0
+            if (side > 0 ? den <= 0 : den >= 0) continue;
+            const int num = sx * (sx - qx) + sy * (sy - qy);
+            if (bi >= 0) {
+                const long long l = (long long)num * bden, r = (long long)bnum * den;
+                if (l == r) {  // cocircular
+                    if (!(side > 0 ? inside_tie_rel(qx, qy, bx, by, sx, sy) : inside_tie_rel(bx, by, qx, qy, sx, sy)))
+                        continue;
+                } else if (side > 0 ? l > r : l < r) {
+                    continue;
+                }
+            }
+            bi = i;
+            bnum = num;
+            bden = den;
+            bx = sx;
+            by = sy;
+        }
+    });
+    if (bi < 0) return -3;
+    // the winner's circle must lie within the box
+    const double qxd = qx, qyd = qy, rx = side > 0 ? bx : qx, ry = side > 0 ? by : qy;
+    const double ax = side > 0 ? qxd : bx, ay = side > 0 ? qyd : by;
+    const double iD = 0.5 / (ax * ry - ay * rx);
+    const double aa = ax * ax + ay * ay, rr = rx * rx + ry * ry;
+    const double ux = (ry * aa - ay * rr) * iD, uy = (ax * rr - rx * aa) * iD;
+    const double rad = sqrt(ux * ux + uy * uy) * (1.0 + 1e-9) + 1.0;
+    const double cx = P.pu + ux, cy = P.pv + uy;
+    const Box need{cell_x(g, cx - rad), cell_y(g, cy - rad), cell_x(g, cx + rad), cell_y(g, cy + rad)};
+    return covers(box, need) ? T.id[bi] : -3;
+}
+
+// p's star from the region with search radius R, into tb ((b, c) per
+// triangle (p, b, c), counter-clockwise from the nearest neighbour, then
+// clockwise for a hull vertex).  Returns the triangle count, -4 when a
+// search is not certified within the box, -5 for more than `cap` triangles.
+PS_HD int tile_walk(const Grid& g, const Tile& T, const TilePoint& P, int R, bool& closed, int* tb, int cap) {
+    closed = false;
+    int qx = 0, qy = 0;
+    const int q0 = tile_nearest(g, T, P, R, qx, qy);
+    if (q0 == -3) return -4;
+    if (q0 < 0) return 0;
+    const int q0x = qx, q0y = qy;
+    int count = 0;
+    for (int dir = 0; dir < 2; ++dir) {
+        const int side = dir == 0 ? 1 : -1;
+        int cur = q0, cx = q0x, cy = q0y;
+        for (int guard = 0; guard <= g.n; ++guard) {
+            int rx = 0, ry = 0;
+            const int r = tile_next(g, T, P, R, cur, cx, cy, side, rx, ry);
+            if (r == -3) return -4;
+            if (r < 0) break;
+            if (count == cap) return -5;
+            tb[2 * count] = side > 0 ? cur : r;
+            tb[2 * count + 1] = side > 0 ? r : cur;
+            ++count;
+            if (side > 0 && r == q0) {
+                closed = true;
+                return count;
+            }
+            cur = r;
+            cx = rx;
+            cy = ry;
+        }
+    }
+    return count;
 }
 
 // Walks the star of p and calls on_tri(a, b, c) for each incident triangle,

@@ -2,7 +2,7 @@
 // run on the CPU, against the reference-order sweep's triangle set
 // (delaunay_lex, array-for-array equal to the compiled reference).
 //
-//   test_star [--synthetic N] [FILE.sup ...]
+//   test_star [--no-local | --tiled] [--synthetic N] [FILE.sup ...]
 // Prints "ok <sets> <triangles>" and exits 0, or the first failures.
 #include <algorithm>
 #include <array>
@@ -21,6 +21,8 @@ using namespace ps;
 namespace {
 
 int failures = 0;
+int radius = 2;  // gather radius of the local pass (--no-local: every search on the grid)
+bool tiled = false;  // --tiled: the device's tiled pass 1
 long long sets = 0, tris_checked = 0;
 
 void fail(const char* tag, const char* what) {
@@ -65,15 +67,69 @@ std::vector<std::array<int, 3>> star_triangles(const std::vector<int>& u, const 
     }
     std::vector<int> hn(n, -1), hp(n, -1), c1(n + 2 * (maxx - minx + 1) + 8), c2(c1.size());
     star::Grid g{u.data(), v.data(), dup.data(), start.data(), items.data(), n, minx, miny, maxx, maxy,
-                 gs, gw, gh, lo.data(), hi.data(), hn.data(), hp.data(), 0};
+                 gs, gw, gh, lo.data(), hi.data(), hn.data(), hp.data(), 0, 1.0 / gs};
     g.flat = star::build_hull(g, c1.data(), c2.data(), hn.data(), hp.data());
     star::Local L;
     int lidx[star::kLocalMax], ldxy[star::kLocalMax];
     L.idx = lidx;
     L.dxy = ldxy;
+    if (tiled) {
+        // the device's pass 1 (star.cu k_star): tiles of cells with a halo in
+        // "shared memory", radius 2 then 4, the grid search for the rest
+        const int tw = (gw + star::kTileCells - 1) / star::kTileCells, th = (gh + star::kTileCells - 1) / star::kTileCells;
+        constexpr int RC = star::kTileRegion * star::kTileRegion;
+        std::vector<int> rs(RC + 1), rxy, rid;
+        for (int ty = 0; ty < th; ++ty)
+            for (int tx = 0; tx < tw; ++tx) {
+                const int cx0 = tx * star::kTileCells - star::kTileHalo, cy0 = ty * star::kTileCells - star::kTileHalo;
+                rxy.clear();
+                rid.clear();
+                for (int c = 0; c < RC; ++c) {
+                    rs[c] = int(rxy.size());
+                    const int gx = cx0 + c % star::kTileRegion, gy = cy0 + c / star::kTileRegion;
+                    if (gx < 0 || gy < 0 || gx >= gw || gy >= gh) continue;
+                    for (int k = start[size_t(gy) * gw + gx]; k < start[size_t(gy) * gw + gx + 1]; ++k) {
+                        const int s = items[k];
+                        if (dup[s]) continue;
+                        rxy.push_back(((v[s] - (miny + cy0 * gs)) << 16) | (u[s] - (minx + cx0 * gs)));
+                        rid.push_back(s);
+                    }
+                }
+                rs[RC] = int(rxy.size());
+                const star::Tile T{rs.data(), rxy.data(), rid.data(), cx0, cy0};
+                for (int ry = star::kTileHalo; ry < star::kTileHalo + star::kTileCells; ++ry)
+                    for (int rx = star::kTileHalo; rx < star::kTileHalo + star::kTileCells; ++rx) {
+                        const int c = ry * star::kTileRegion + rx;
+                        for (int i = rs[c]; i < rs[c + 1]; ++i) {
+                            const int p = rid[i];
+                            const star::TilePoint P{p, cx0 + rx, cy0 + ry, rxy[i] & 0xffff, rxy[i] >> 16, u[p], v[p], hp[p], hn[p]};
+                            int tb[2 * 16];
+                            bool closed;
+                            int k = star::tile_walk(g, T, P, 2, closed, tb, 16);
+                            if (k == -4) k = star::tile_walk(g, T, P, 4, closed, tb, 16);
+                            if (k >= 0) {
+                                for (int j = 0; j < k; ++j)
+                                    if (p < tb[2 * j] && p < tb[2 * j + 1]) out.push_back({p, tb[2 * j], tb[2 * j + 1]});
+                                continue;
+                            }
+                            star::Local none;
+                            none.complete = false;
+                            k = star::walk_star(g, none, p, closed, [&](int a, int b, int c2) {
+                                if (a < b && a < c2) out.push_back({a, b, c2});
+                            });
+                            if (k == -2) {
+                                ok = false;
+                                return out;
+                            }
+                        }
+                    }
+            }
+        return out;
+    }
     for (int p = 0; p < n; ++p) {
         bool closed;
-        star::gather(g, p, 2, L);
+        star::gather(g, p, radius, L);
+        if (radius < 0) L.complete = false;
         const int k = star::walk_star(g, L, p, closed, [&](int a, int b, int c) {
             if (a < b && a < c) out.push_back({a, b, c});
         });
@@ -169,6 +225,12 @@ void from_file(const char* path) {
 
 int main(int argc, char** argv) {
     int a = 1;
+    if (argc > 1 && (std::strcmp(argv[1], "--no-local") == 0 || std::strcmp(argv[1], "--tiled") == 0)) {
+        if (argv[1][2] == 'n') radius = -1;
+        else tiled = true;
+        ++argv;
+        --argc;
+    }
     if (argc == 1) synthetic(3000);
     if (argc > 2 && std::strcmp(argv[1], "--synthetic") == 0) {
         synthetic(std::atoi(argv[2]));

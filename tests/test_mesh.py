@@ -71,11 +71,14 @@ def test_device_star_triangulation_on_cpu(test_mesh_bin, orc, tmp_path):
     convex hull from column extremes) compiled for the CPU: the same triangle
     set as the reference-order sweep on 3,000 synthetic sets (lattices with
     cocircular cells, random points, duplicates, collinear sets) and on every
-    iteration of a BASELINE config 2 frame."""
+    iteration of a BASELINE config 2 frame — for each of its search paths."""
     star = os.path.join(ROOT, "tests", "cpp", "_build", "test_star")
-    out = subprocess.run([star, "--synthetic", "3000"], capture_output=True, text=True, timeout=600)
-    assert out.returncode == 0, out.stdout + out.stderr
     path = str(tmp_path / "cfg2_9.sup")
     _dump(path, orc, 640, 480, 12, 64, False, 2.0, 3, 10, 9)
-    out = subprocess.run([star, path], capture_output=True, text=True, timeout=600)
-    assert out.returncode == 0, out.stdout + out.stderr
+    # the per-point local pass, the grid search alone (pass 2's search), and
+    # the tiled pass 1 of the device (radius 2, then 4, then the grid)
+    for mode in ([], ["--no-local"], ["--tiled"]):
+        out = subprocess.run([star] + mode + ["--synthetic", "3000"], capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, " ".join(mode) + out.stdout + out.stderr
+        out = subprocess.run([star] + mode + [path], capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, " ".join(mode) + out.stdout + out.stderr
