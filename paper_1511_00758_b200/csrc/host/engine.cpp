@@ -160,6 +160,11 @@ static std::vector<DelaunayWorkspace>& shared_workspaces() {
     static std::vector<DelaunayWorkspace> ws(shared_pool().size());
     return ws;
 }
+// order-query scratch per worker (queries of one frame run on several workers)
+static std::vector<SweepOrder::Scratch>& shared_order_scratch() {
+    static std::vector<SweepOrder::Scratch> s(shared_pool().size());
+    return s;
+}
 
 Engine::Engine(int device) : device_(device) {
     cudaSetDevice(device_);
@@ -525,6 +530,10 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     auto star_gs = [&](double est) {
         return std::max(2, int(std::sqrt(1.3 * double(P) / std::max(1.0, est)) + 0.5));
     };
+    const StarFlagLayout flay = star_flag_layout(scap_);
+    // fewer frames than host workers: a frame's order queries spread over the
+    // idle workers, so a larger query budget still beats the serial replay
+    const int budget_scale = std::max(1, int(pool_->size()) / std::max(1, F));
     const long long star_cells_max = (long long)((W - 1) / 2 + 1) * ((H - 1) / 2 + 1);  // gs >= 2
     cudaMemsetAsync(dErr, 0, sizeof(int), st_);
     ps_status s = check(cudaEventRecord(start_event_, st_), "start event");
@@ -563,6 +572,9 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         a.pins = static_cast<uint8_t*>(grp.dPin.p);
         a.tri_count = static_cast<int*>(grp.dTriCount.p);
         a.flags = static_cast<int*>(grp.dFlags.p);
+        a.flag_ints = flay.ints;
+        a.max_suspect = flay.max_suspect;
+        a.fan_base = flay.fan_base;
         a.col_key = static_cast<unsigned long long*>(grp.dColKey.p);
         a.col_idx = static_cast<int*>(grp.dColIdx.p);
         a.hull = static_cast<int*>(grp.dHull.p);
@@ -581,7 +593,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         launches_ += launch_star_check(a, tri_cap, gs);
         end_kernel(gs);
         cudaMemcpyAsync(grp.hTriCount.p, grp.dTriCount.p, sizeof(int) * grp.n, cudaMemcpyDeviceToHost, gs);
-        cudaMemcpyAsync(grp.hFlags.p, grp.dFlags.p, sizeof(int) * size_t(grp.n) * kStarFlagInts,
+        cudaMemcpyAsync(grp.hFlags.p, grp.dFlags.p, sizeof(int) * size_t(grp.n) * flay.ints,
                         cudaMemcpyDeviceToHost, gs);
     };
     auto seed_group = [&](int gi) -> ps_status {
@@ -612,9 +624,9 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
             if (!dev<int>(grp.dCellCnt, nn * star_cells_max) || !dev<int>(grp.dCellStart, nn * (star_cells_max + 1)) ||
                 !dev<int>(grp.dCellItems, nn * scap_) || !dev<int>(grp.dCellXY, nn * scap_) || !dev<uint8_t>(grp.dDup, nn * scap_) ||
                 !dev<int>(grp.dPinTri, nn * scap_ * 3) || !dev<int>(grp.dTriCount, nn) ||
-                !dev<int>(grp.dFlags, nn * kStarFlagInts) || !dev<int>(grp.dTri, nn * tri_cap * 3) ||
+                !dev<int>(grp.dFlags, nn * flay.ints) || !dev<int>(grp.dTri, nn * tri_cap * 3) ||
                 !dev<uint8_t>(grp.dPin, nn * tri_cap) || !host<int>(grp.hTriCount, nn) ||
-                !host<int>(grp.hFlags, nn * kStarFlagInts) || !host<int>(grp.hFix, nn * 6 * 96) ||
+                !host<int>(grp.hFlags, nn * flay.ints) || !host<int>(grp.hFix, nn * 6 * 96) ||
                 !dev<int>(grp.dFix, nn * 6 * 96) ||
                 !dev<unsigned long long>(grp.dColKey, nn * 2 * W) || !dev<int>(grp.dColIdx, nn * 2 * W) ||
                 !dev<int>(grp.dHull, nn * 2 * scap_) || !dev<int>(grp.dHullTmp, nn * 8 * (2 * size_t(W) + 2 * size_t(H) + 8)) ||
@@ -815,14 +827,25 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                     const double ts0 = now_ms();
                     if (device_dt) {
                         // the device meshed the frame; resolve what it listed
-                        const int* fl = static_cast<const int*>(g2.hFlags.p) + size_t(i) * kStarFlagInts;
+                        const int* fl = static_cast<const int*>(g2.hFlags.p) + size_t(i) * flay.ints;
                         t = static_cast<const int*>(g2.hTriCount.p)[i];
                         bool rep = fl[0] != 0 || t > tri_cap;
+                        if (rep) {
+                            ++mstats[worker].fb_device;
+                            const int why = t > tri_cap ? 16 : fl[6];
+                            for (int b = 0; b < 5; ++b) mstats[worker].fb_why[b] += (why >> b) & 1;
+                        }
                         g2.fixes[i].clear();
                         g2.replayed[i] = 0;
-                        if (!rep && (fl[1] > 0 || fl[3] > 0))
-                            rep = !resolve_device_flags(fm, fl, i, W, H, float(cfg.max_disparity),
-                                                        g2.fixes[i], w, mstats[worker]);
+                        if (!rep && (fl[1] > 0 || fl[3] > 0)) {
+                            // order queries of the frame on idle workers too
+                            const ParallelQueries par = [&, worker](int nq, const std::function<void(int, SweepOrder::Scratch&)>& fn) {
+                                auto& scr = shared_order_scratch();
+                                pool_->help_run(worker, nq, [&](int q, int w) { fn(q, scr[w]); });
+                            };
+                            rep = !resolve_device_flags(fm, fl, flay, i, W, H, float(cfg.max_disparity),
+                                                        g2.fixes[i], w, mstats[worker], &par, budget_scale);
+                        }
                         if (rep) {
                             g2.fixes[i].clear();
                             g2.replayed[i] = 1;
@@ -1188,6 +1211,11 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         for (const MeshStats& m : mstats) {
             tot.frames += m.frames;
             tot.fallbacks += m.fallbacks;
+            tot.fb_device += m.fb_device;
+            for (int b = 0; b < 5; ++b) tot.fb_why[b] += m.fb_why[b];
+            tot.fb_queries += m.fb_queries;
+            tot.fb_resolve += m.fb_resolve;
+            tot.replay_ms += m.replay_ms;
             tot.ambiguous += m.ambiguous;
             tot.rotations += m.rotations;
             tot.rot_checked += m.rot_checked;
@@ -1219,6 +1247,16 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         k7.ms += tot.init_ms / workers;
         KernelStat& k4 = stat("host_replay");  // frame-iterations replayed (delaunay_lex)
         k4.launches += int(tot.fallbacks);
+        k4.ms += tot.replay_ms / workers;
+        // of which, by cause
+        stat("host_replay_device").launches += int(tot.fb_device);    // star overflow / capacity
+        stat("host_replay_dev_fan").launches += int(tot.fb_why[0]);
+        stat("host_replay_dev_search").launches += int(tot.fb_why[1]);
+        stat("host_replay_dev_degree").launches += int(tot.fb_why[2]);
+        stat("host_replay_dev_suspects").launches += int(tot.fb_why[3]);
+        stat("host_replay_dev_capacity").launches += int(tot.fb_why[4]);
+        stat("host_replay_queries").launches += int(tot.fb_queries);  // order-query budget
+        stat("host_replay_resolve").launches += int(tot.fb_resolve);  // window not certified
         // pool occupancy: before the first task, gaps between tasks, after the last
         const double fa = first_task.load(), la = last_task.load(), end = now_ms();
         if (la > 0.0) {

@@ -5,6 +5,7 @@
 #include <array>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 namespace ps {
@@ -58,7 +59,19 @@ inline uint32_t dit_bits(const Fit& f, int u, int v, float nd) {
     return bits;
 }
 
-constexpr int kMaxQueries = 24;
+// Order-query budget per frame-iteration.  Each query replays windows of
+// the sweep; past the budget the whole replay is cheaper.  Measured (one
+// host core): VGA ~20 k supports, query ~0.05 ms vs replay 3-8 ms; 1080p
+// 465 k, 45 ms vs 1.4 s; 4K 5.8 M, ~170 ms vs ~30 s: the ratio grows slowly
+// with the point count.  PS_MAX_QUERIES overrides it (probing).
+int max_queries(int n) {
+    static const int env = [] {
+        const char* e = std::getenv("PS_MAX_QUERIES");
+        return e ? std::atoi(e) : -1;
+    }();
+    if (env >= 0) return env;
+    return 32 + n / 32768;
+}
 
 long long floor_div(long long a, long long b) {  // mesh.cpp:30-36
     long long q = a / b;
@@ -113,9 +126,11 @@ inline bool tie_accept(int xi, int yi, int xj, int yj) {
 int replay(FrameMesh& fm, int width, int height, int* tris, int cap, uint8_t* pins,
            DelaunayWorkspace& ws, MeshStats& st) {
     ++st.fallbacks;
+    const double t0 = now_ms();
     const int n = int(fm.u.size());
     const int t = delaunay_lex(fm.u.data(), fm.v.data(), n, tris, cap, ws);
     if (t > 0) lex_hull_pins(ws, t, width, height, pins);
+    st.replay_ms += now_ms() - t0;
     return t;
 }
 
@@ -126,15 +141,16 @@ int replay_mesh(FrameMesh& fm, int width, int height, int* tris, int cap, uint8_
     return replay(fm, width, height, tris, cap, pins, ws, st);
 }
 
-bool resolve_device_flags(FrameMesh& fm, const int* flags, int frame, int width, int height,
+bool resolve_device_flags(FrameMesh& fm, const int* flags, const StarFlagLayout& layout, int frame, int width, int height,
                           float max_disparity, std::vector<int>& fixes, DelaunayWorkspace& ws,
-                          MeshStats& st) {
+                          MeshStats& st, const ParallelQueries* par, int budget_scale) {
     ++st.frames;
     const int n = int(fm.u.size());
+    const int budget = max_queries(n) * std::max(1, budget_scale);
     const int n_sus = flags[1];
     const int n_amb = flags[3];
-    const int* sus = flags + 8;  // kStarSuspectBase
-    const int* fan = flags + 8 + 4 * 64;  // kStarFanBase
+    const int* sus = flags + kStarSuspectBase;
+    const int* fan = flags + layout.fan_base;
     bool have_order = false;
     auto build_order = [&] {
         if (have_order) return;
@@ -161,28 +177,53 @@ bool resolve_device_flags(FrameMesh& fm, const int* flags, int frame, int width,
         return std::array<int, 3>{a, b, c};
     };
     int queries = 0;
-    // (2) rotation suspects: does any covered pixel see the difference?
+    // (2) rotation suspects: does any covered pixel see the difference?  The
+    // suspects that need the sweep's rotation are collected first, their
+    // order queries run (possibly on several host threads: each query is
+    // independent given the frame's SweepOrder), then the fixes are written
+    // in suspect order, so the result does not depend on the schedule.
     std::vector<std::pair<std::array<int, 3>, std::array<int, 3>>> rotated;  // vertex set -> stored order
+    std::vector<std::array<int, 4>> need;  // (triangle, i, j, k)
     for (int q = 0; q < n_sus; ++q) {
         const int t = sus[4 * q], i = sus[4 * q + 1], j = sus[4 * q + 2], k = sus[4 * q + 3];
         if (i < 0 || j < 0 || k < 0 || i >= n || j >= n || k >= n) return false;
         ++st.rot_checked;
         const Fit f3[3] = {fit(fm, i, j, k), fit(fm, j, k, i), fit(fm, k, i, j)};
         if (rotations_equivalent(fm, i, j, k, f3, width, height, max_disparity)) continue;
-        if (++queries > kMaxQueries) return false;
+        need.push_back({t, i, j, k});
+    }
+    queries = int(need.size());
+    if (queries > budget) {
+        ++st.fb_queries;
+        return false;
+    }
+    if (!need.empty()) {
         const double to = now_ms();
         build_order();
-        int r3[3] = {fm.rank_of[i], fm.rank_of[j], fm.rank_of[k]};
-        uint64_t b;
-        int s3[3];
-        const bool ok = fm.so.resolve(r3, 1, &b, s3);
+        std::vector<std::array<int, 3>> s3(need.size());
+        std::vector<uint8_t> okq(need.size(), 0);
+        auto one = [&](int q, SweepOrder::Scratch& S) {
+            int r3[3] = {fm.rank_of[need[q][1]], fm.rank_of[need[q][2]], fm.rank_of[need[q][3]]};
+            uint64_t b;
+            okq[q] = fm.so.resolve(r3, 1, &b, s3[q].data(), S) ? 1 : 0;
+        };
+        if (par && need.size() > 1) {
+            (*par)(int(need.size()), one);
+        } else {
+            for (int q = 0; q < int(need.size()); ++q) one(q, fm.so.scratch());
+        }
         st.order_ms += now_ms() - to;
         st.rot_ms += now_ms() - to;
-        if (!ok) return false;
-        const int v0 = fm.ranks[s3[0]], v1 = fm.ranks[s3[1]], v2 = fm.ranks[s3[2]];
-        fixes.insert(fixes.end(), {frame, 0, t, v0, v1, v2});
-        rotated.push_back({sorted3(i, j, k), {v0, v1, v2}});
-        ++st.rotations;
+        for (size_t q = 0; q < need.size(); ++q) {
+            if (!okq[q]) {
+                ++st.fb_resolve;
+                return false;
+            }
+            const int v0 = fm.ranks[s3[q][0]], v1 = fm.ranks[s3[q][1]], v2 = fm.ranks[s3[q][2]];
+            fixes.insert(fixes.end(), {frame, 0, need[q][0], v0, v1, v2});
+            rotated.push_back({sorted3(need[q][1], need[q][2], need[q][3]), {v0, v1, v2}});
+            ++st.rotations;
+        }
     }
     // (3) ambiguous hull vertices: the incident triangle the sweep stored first
     for (int a = 0, at = 0; a < n_amb; ++a) {
@@ -219,7 +260,10 @@ bool resolve_device_flags(FrameMesh& fm, const int* flags, int frame, int width,
         }
         int pick = 0;
         if (!agree) {
-            if (++queries > kMaxQueries) return false;
+            if (++queries > budget) {
+                ++st.fb_queries;
+                return false;
+            }
             const double to = now_ms();
             build_order();
             std::vector<int> r3(3 * size_t(cnt)), s3(3 * size_t(cnt));
@@ -233,7 +277,10 @@ bool resolve_device_flags(FrameMesh& fm, const int* flags, int frame, int width,
             const bool ok = fm.so.resolve(r3.data(), cnt, fm.birth.data(), s3.data());
             st.order_ms += now_ms() - to;
             st.pin_ms += now_ms() - to;
-            if (!ok) return false;
+            if (!ok) {
+                ++st.fb_resolve;
+                return false;
+            }
             for (int i = 1; i < cnt; ++i)
                 if (fm.birth[i] < fm.birth[pick]) pick = i;
             ++st.ambiguous;
@@ -297,7 +344,7 @@ int mesh_iteration(FrameMesh& fm, int width, int height, float max_disparity, in
 
     // Each order query replays a window of the sweep: past a handful the
     // whole replay is cheaper (real meshes need 0-2 per frame-iteration).
-    if (int(fm.q.size()) > kMaxQueries) return replay(fm, width, height, tris, cap, pins, ws, st);
+    if (int(fm.q.size()) > max_queries(n)) return replay(fm, width, height, tris, cap, pins, ws, st);
     int queries = int(fm.q.size());
     if (!fm.q.empty()) {
         const double to = now_ms();
@@ -349,7 +396,7 @@ int mesh_iteration(FrameMesh& fm, int width, int height, float max_disparity, in
                 else if (bits != first) agree = false;
             }
             int pin_t = fm.inc[0];
-            if (!agree && ++queries > kMaxQueries) return replay(fm, width, height, tris, cap, pins, ws, st);
+            if (!agree && ++queries > max_queries(n)) return replay(fm, width, height, tris, cap, pins, ws, st);
             if (!agree) {
                 const double to = now_ms();
                 build_order();

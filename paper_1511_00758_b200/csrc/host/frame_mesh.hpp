@@ -21,8 +21,10 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <vector>
 
+#include "../kernels/star_layout.hpp"
 #include "delaunay.hpp"
 #include "incdt.hpp"
 #include "sweep_order.hpp"
@@ -32,6 +34,11 @@ namespace ps {
 struct MeshStats {
     long long frames = 0;      // frame-iterations meshed
     long long fallbacks = 0;   // of which replayed with delaunay_lex
+    long long fb_device = 0;   //   because the device mesh flagged the frame (star overflow, capacity)
+    long long fb_why[5] = {0, 0, 0, 0, 0};  // device causes: fan, search, degree, suspects, capacity
+    long long fb_queries = 0;  //   because the order-query budget ran out
+    long long fb_resolve = 0;  //   because SweepOrder could not certify a window
+    double replay_ms = 0;      // time in delaunay_lex replays
     long long ambiguous = 0;   // hull-vertex pins resolved through SweepOrder
     long long rotations = 0;   // triangles whose rotation SweepOrder decided
     long long rot_checked = 0; // triangles fitted three ways
@@ -66,15 +73,20 @@ int mesh_iteration(FrameMesh& fm, int width, int height, float max_disparity, in
                    uint8_t* pins, DelaunayWorkspace& ws, MeshStats& st);
 
 // Host side of the device mesh (kernels/star.cu): the frame's flag record
-// (kStarFlagInts ints: rotation suspects and ambiguous hull vertices, see
+// (layout.ints ints: rotation suspects and ambiguous hull vertices, see
 // launch.hpp) is resolved into fixes appended to `fixes` as
 // {frame, 0, triangle, v0, v1, v2} (the sweep's stored rotation) and
 // {frame, 1, vertex, s0, s1, s2} (the pinned triangle's sorted vertex set).
 // Returns false when the frame should be replayed instead (query budget or
 // an inconsistency).
-bool resolve_device_flags(FrameMesh& fm, const int* flags, int frame, int width, int height,
+// par (optional) runs fn(i, scratch) for i in [0, n) on any threads, each
+// concurrent call with its own scratch; budget_scale multiplies the order-
+// query budget (queries that run in parallel cost less latency than the
+// serial replay they avoid).
+using ParallelQueries = std::function<void(int, const std::function<void(int, SweepOrder::Scratch&)>&)>;
+bool resolve_device_flags(FrameMesh& fm, const int* flags, const StarFlagLayout& layout, int frame, int width, int height,
                           float max_disparity, std::vector<int>& fixes, DelaunayWorkspace& ws,
-                          MeshStats& st);
+                          MeshStats& st, const ParallelQueries* par = nullptr, int budget_scale = 1);
 
 // The exact replay (delaunay_lex + the sweep's pins) into caller buffers.
 int replay_mesh(FrameMesh& fm, int width, int height, int* tris, int cap, uint8_t* pins,

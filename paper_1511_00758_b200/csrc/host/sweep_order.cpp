@@ -4,8 +4,14 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 
 namespace ps {
+
+SweepOrder::Scratch& SweepOrder::own() {
+    if (!own_) own_ = std::make_unique<Scratch>();
+    return *own_;
+}
 
 void SweepOrder::init(const int* px, const int* py, int m) {
     x_ = px;
@@ -91,7 +97,7 @@ int SweepOrder::incircle(int a, int b, int c, int d) const {
 
 // Counter-clockwise predecessor of o on hull(Q<p): the lower chain runs left
 // to right, the upper chain right to left, and they meet at rank 0 and p - 1.
-int SweepOrder::hull_prev(int o, int p) {
+int SweepOrder::hull_prev(int o, int p) const {
     if (o >= p) return -1;
     const bool onL = popL_[o] >= p, onU = popU_[o] >= p;
     if (onL && o != 0) return belowL_[o];
@@ -102,7 +108,7 @@ int SweepOrder::hull_prev(int o, int p) {
     return -1;
 }
 
-int SweepOrder::fan_index(int o, int p) {
+int SweepOrder::fan_index(int o, int p) const {
     const int h = hull_prev(o, p);
     if (h < 0 || orient(h, o, p) >= 0) return -1;  // hull edge h->o not strictly visible
     int count = 0;
@@ -115,7 +121,7 @@ int SweepOrder::fan_index(int o, int p) {
 }
 
 bool SweepOrder::disk_clear(int a, int b, int c, int p, int& u0, int& u1, int& v0, int& v1,
-                            int grow) {
+                            int grow) const {
     const double ax = x_[a], ay = y_[a];
     const double bxx = x_[b] - ax, byy = y_[b] - ay;
     const double cxx = x_[c] - ax, cyy = y_[c] - ay;
@@ -171,7 +177,7 @@ bool SweepOrder::disk_clear(int a, int b, int c, int p, int& u0, int& u1, int& v
     return clear;
 }
 
-bool SweepOrder::window_triangle(int o, int p, int out[3]) {
+bool SweepOrder::window_triangle(int o, int p, int out[3], Scratch& S) const {
     const int R0 = 2 * bs_;
     int u0 = std::min(x_[o], x_[p]) - R0, u1 = std::min(std::max(x_[o], x_[p]) + R0, x_[p]);
     int v0 = std::min(y_[o], y_[p]) - R0, v1 = std::max(y_[o], y_[p]) + R0;
@@ -184,9 +190,9 @@ bool SweepOrder::window_triangle(int o, int p, int out[3]) {
     clamp_box();
     for (int attempt = 0; attempt < 24; ++attempt) {
         // prefix points (rank < p) in the box
-        wu_.clear();
-        wv_.clear();
-        wrank_.clear();
+        S.wu_.clear();
+        S.wv_.clear();
+        S.wrank_.clear();
         int io = -1;
         const int bx0 = (u0 - minx_) / bs_, bx1 = (u1 - minx_) / bs_;
         const int by0 = (v0 - miny_) / bs_, by1 = (v1 - miny_) / bs_;
@@ -197,23 +203,23 @@ bool SweepOrder::window_triangle(int o, int p, int out[3]) {
                     const int r = bitems_[i];
                     if (r >= p) break;
                     if (x_[r] < u0 || x_[r] > u1 || y_[r] < v0 || y_[r] > v1) continue;
-                    if (r == o) io = int(wrank_.size());
-                    wu_.push_back(x_[r]);
-                    wv_.push_back(y_[r]);
-                    wrank_.push_back(r);
+                    if (r == o) io = int(S.wrank_.size());
+                    S.wu_.push_back(x_[r]);
+                    S.wv_.push_back(y_[r]);
+                    S.wrank_.push_back(r);
                 }
             }
-        ++windows;
-        window_points += (long long)wrank_.size();
+        ++S.windows;
+        S.window_points += (long long)S.wrank_.size();
         int sigma[3] = {-1, -1, -1};
-        const int nw = int(wrank_.size());
+        const int nw = int(S.wrank_.size());
         if (io >= 0 && nw >= 3) {
-            const int nt = delaunay(wu_.data(), wv_.data(), nw, wtris_, ws_);
+            const int nt = delaunay(S.wu_.data(), S.wv_.data(), nw, S.wtris_, S.ws_);
             for (int t = 0; t < nt && sigma[0] < 0; ++t) {
-                const int* tr = &wtris_[3 * size_t(t)];
+                const int* tr = &S.wtris_[3 * size_t(t)];
                 for (int k = 0; k < 3; ++k) {
                     if (tr[k] != io) continue;
-                    const int a = wrank_[tr[(k + 1) % 3]], b = wrank_[tr[(k + 2) % 3]];
+                    const int a = S.wrank_[tr[(k + 1) % 3]], b = S.wrank_[tr[(k + 2) % 3]];
                     if (orient(o, a, p) > 0 && orient(o, p, b) > 0) {
                         sigma[0] = o;
                         sigma[1] = a;
@@ -246,7 +252,7 @@ bool SweepOrder::window_triangle(int o, int p, int out[3]) {
     return false;
 }
 
-bool SweepOrder::query(int a, int b, int c, uint64_t& birth, int stored[3]) {
+bool SweepOrder::query(int a, int b, int c, uint64_t& birth, int stored[3], Scratch& S) const {
     if (apex_ < 0) return false;
     struct Step {
         int o, t, p;
@@ -278,7 +284,7 @@ bool SweepOrder::query(int a, int b, int c, uint64_t& birth, int stored[3]) {
             break;
         }
         int sigma[3];
-        if (!window_triangle(o, p, sigma)) return false;
+        if (!window_triangle(o, p, sigma, S)) return false;
         chain.push_back({o, t, p});
         T[0] = sigma[0];
         T[1] = sigma[1];
@@ -313,8 +319,8 @@ namespace ps {
 // The reference sweep (delaunay.cpp:50-284) over the window's points in rank
 // order, recording for every slot the contents it had before each time it
 // was eaten (a Lawson flip on the side not holding the new point).
-bool SweepOrder::replay(int u0, int u1, int v0, int v1) {
-    rrank_.clear();
+bool SweepOrder::replay(int u0, int u1, int v0, int v1, Scratch& S) const {
+    S.rrank_.clear();
     const int bx0 = std::max(0, (u0 - minx_) / bs_), bx1 = std::min(bw_ - 1, (u1 - minx_) / bs_);
     const int by0 = std::max(0, (v0 - miny_) / bs_), by1 = std::min(bh_ - 1, (v1 - miny_) / bs_);
     for (int by = by0; by <= by1; ++by)
@@ -322,53 +328,53 @@ bool SweepOrder::replay(int u0, int u1, int v0, int v1) {
             const size_t b = size_t(by) * bw_ + bx;
             for (int i = bstart_[b]; i < bstart_[b + 1]; ++i) {
                 const int r = bitems_[i];
-                if (x_[r] >= u0 && x_[r] <= u1 && y_[r] >= v0 && y_[r] <= v1) rrank_.push_back(r);
+                if (x_[r] >= u0 && x_[r] <= u1 && y_[r] >= v0 && y_[r] <= v1) S.rrank_.push_back(r);
             }
         }
-    std::sort(rrank_.begin(), rrank_.end());
-    const int n = int(rrank_.size());
-    ++replays;
-    replay_points += n;
-    rs_.clear();
-    rh_.clear();
-    rapex_ = -1;
+    std::sort(S.rrank_.begin(), S.rrank_.end());
+    const int n = int(S.rrank_.size());
+    ++S.replays;
+    S.replay_points += n;
+    S.rs_.clear();
+    S.rh_.clear();
+    S.rapex_ = -1;
     if (n < 3) return false;
-    const int* R = rrank_.data();
+    const int* R = S.rrank_.data();
     auto ori = [&](int a, int b, int c) { return orient(R[a], R[b], R[c]); };
     int k = 2;
     while (k < n && ori(0, 1, k) == 0) ++k;
     if (k == n) return false;
-    rapex_ = k;
-    rhn_.assign(n, -1);
-    rhp_.assign(n, -1);
-    rhe_.assign(n, -1);
-    rstack_.clear();
-    rs_.reserve(2 * size_t(n));
-    auto V = [&](int e) -> int& { return rs_[e >> 2].v[e & 3]; };
-    auto N = [&](int e) -> int& { return rs_[e >> 2].n[e & 3]; };
+    S.rapex_ = k;
+    S.rhn_.assign(n, -1);
+    S.rhp_.assign(n, -1);
+    S.rhe_.assign(n, -1);
+    S.rstack_.clear();
+    S.rs_.reserve(2 * size_t(n));
+    auto V = [&](int e) -> int& { return S.rs_[e >> 2].v[e & 3]; };
+    auto N = [&](int e) -> int& { return S.rs_[e >> 2].n[e & 3]; };
     auto lnext = [](int e) { return (e & 3) == 2 ? e - 2 : e + 1; };
     auto add = [&](int a, int b, int c, int na, int nb, int nc, int birth, int fan) {
-        const int e = 4 * int(rs_.size());
-        rs_.push_back(Slot{{a, b, c}, {na, nb, nc}, birth, fan, -1, -1, a});
+        const int e = 4 * int(S.rs_.size());
+        S.rs_.push_back(Scratch::Slot{{a, b, c}, {na, nb, nc}, birth, fan, -1, -1, a});
         if (na >= 0) N(na) = e;
         if (nb >= 0) N(nb) = e + 1;
         if (nc >= 0) N(nc) = e + 2;
         return e;
     };
     auto hull = [&](int a, int b) {
-        rhn_[a] = b;
-        rhp_[b] = a;
+        S.rhn_[a] = b;
+        S.rhp_[b] = a;
     };
     const int apex = k;
     if (ori(0, 1, apex) > 0) {
         int prevE1 = -1;
         for (int j = 0; j + 1 < k; ++j) {
             const int e = add(j, j + 1, apex, -1, -1, prevE1, apex, j);
-            if (j == 0) rhe_[apex] = e + 2;
-            rhe_[j] = e;
+            if (j == 0) S.rhe_[apex] = e + 2;
+            S.rhe_[j] = e;
             prevE1 = e + 1;
         }
-        rhe_[k - 1] = prevE1;
+        S.rhe_[k - 1] = prevE1;
         for (int j = 0; j + 1 < k; ++j) hull(j, j + 1);
         hull(k - 1, apex);
         hull(apex, 0);
@@ -376,56 +382,56 @@ bool SweepOrder::replay(int u0, int u1, int v0, int v1) {
         int prevE2 = -1;
         for (int j = 0; j + 1 < k; ++j) {
             const int e = add(j + 1, j, apex, -1, prevE2, -1, apex, j);
-            if (j == 0) rhe_[0] = e + 1;
-            rhe_[j + 1] = e;
+            if (j == 0) S.rhe_[0] = e + 1;
+            S.rhe_[j + 1] = e;
             prevE2 = e + 2;
         }
-        rhe_[apex] = prevE2;
+        S.rhe_[apex] = prevE2;
         for (int j = 0; j + 1 < k; ++j) hull(j + 1, j);
         hull(0, apex);
         hull(apex, k - 1);
     }
-    auto visible = [&](int a, int p) { return ori(a, rhn_[a], p) < 0; };
+    auto visible = [&](int a, int p) { return ori(a, S.rhn_[a], p) < 0; };
     for (int p = apex + 1; p < n; ++p) {
         const int q = p - 1;
         int a, b;
         if (visible(q, p)) {
             a = q;
-            b = rhn_[q];
-        } else if (visible(rhp_[q], p)) {
-            a = rhp_[q];
+            b = S.rhn_[q];
+        } else if (visible(S.rhp_[q], p)) {
+            a = S.rhp_[q];
             b = q;
         } else {
             return false;
         }
-        while (rhn_[b] != a && visible(b, p)) b = rhn_[b];
-        while (rhp_[a] != b && visible(rhp_[a], p)) a = rhp_[a];
+        while (S.rhn_[b] != a && visible(b, p)) b = S.rhn_[b];
+        while (S.rhp_[a] != b && visible(S.rhp_[a], p)) a = S.rhp_[a];
         int prevE1 = -1, firstE0 = -1, j = 0;
         for (int xv = a; xv != b; ++j) {
-            const int xn = rhn_[xv];
-            const int e = add(xv, p, xn, prevE1, -1, rhe_[xv], p, j);
+            const int xn = S.rhn_[xv];
+            const int e = add(xv, p, xn, prevE1, -1, S.rhe_[xv], p, j);
             if (firstE0 < 0) firstE0 = e;
             prevE1 = e + 1;
-            rstack_.push_back(e + 2);
+            S.rstack_.push_back(e + 2);
             xv = xn;
         }
         hull(a, p);
         hull(p, b);
-        rhe_[a] = firstE0;
-        rhe_[p] = prevE1;
-        while (!rstack_.empty()) {
-            const int e = rstack_.back();
-            rstack_.pop_back();
+        S.rhe_[a] = firstE0;
+        S.rhe_[p] = prevE1;
+        while (!S.rstack_.empty()) {
+            const int e = S.rstack_.back();
+            S.rstack_.pop_back();
             const int f = N(e);
             if (f < 0) continue;
             const int e1 = lnext(e), e2 = lnext(e1);
             const int f1 = lnext(f), f2 = lnext(f1);
             const int va = V(e), vb = V(e1), vc = V(e2), vd = V(f2);
             if (incircle(R[va], R[vb], R[vc], R[vd]) <= 0) continue;
-            Slot& F = rs_[f >> 2];
+            Scratch::Slot& F = S.rs_[f >> 2];
             if (F.eaten != p) {  // first time this insertion eats the slot
-                rh_.push_back(Hist{p, {F.v[0], F.v[1], F.v[2]}, F.hist});
-                F.hist = int(rh_.size()) - 1;
+                S.rh_.push_back(Scratch::Hist{p, {F.v[0], F.v[1], F.v[2]}, F.hist});
+                F.hist = int(S.rh_.size()) - 1;
                 F.eaten = p;
             }
             const int ne1 = N(e1), nf1 = N(f1), nf2 = N(f2);
@@ -434,23 +440,29 @@ bool SweepOrder::replay(int u0, int u1, int v0, int v1) {
             V(f1) = vb;
             V(f2) = vc;
             N(e) = nf1;
-            if (nf1 >= 0) N(nf1) = e; else rhe_[va] = e;
+            if (nf1 >= 0) N(nf1) = e; else S.rhe_[va] = e;
             N(e1) = f2;
             N(f2) = e1;
             N(f) = nf2;
-            if (nf2 >= 0) N(nf2) = f; else rhe_[vd] = f;
+            if (nf2 >= 0) N(nf2) = f; else S.rhe_[vd] = f;
             N(f1) = ne1;
-            if (ne1 >= 0) N(ne1) = f1; else rhe_[vb] = f1;
-            rstack_.push_back(e);
-            rstack_.push_back(f);
+            if (ne1 >= 0) N(ne1) = f1; else S.rhe_[vb] = f1;
+            S.rstack_.push_back(e);
+            S.rstack_.push_back(f);
         }
     }
     return true;
 }
 
-bool SweepOrder::resolve(const int* tris, int count, uint64_t* birth, int* stored) {
+bool SweepOrder::resolve(const int* tris, int count, uint64_t* birth, int* stored, Scratch& S) const {
     if (apex_ < 0) return false;
     if (count <= 0) return true;
+    static const bool chains = std::getenv("PS_ORDER_CHAINS") != nullptr;
+    if (chains) {
+        for (int t = 0; t < count; ++t)
+            if (!query(tris[3 * t], tris[3 * t + 1], tris[3 * t + 2], birth[t], stored + 3 * t, S)) return false;
+        return true;
+    }
     int bu0 = INT_MAX, bu1 = INT_MIN, bv0 = INT_MAX, bv1 = INT_MIN;
     for (int i = 0; i < 3 * count; ++i) {
         bu0 = std::min(bu0, x_[tris[i]]);
@@ -477,14 +489,14 @@ bool SweepOrder::resolve(const int* tris, int count, uint64_t* birth, int* store
         bool grow_all = false;
         bool gl = false, gr = false, gd = false, gu = false;  // directional growth requests
         const bool fallback = attempt >= 8;  // then finish chains in the full set instead
-        const bool replayed = replay(u0, u1, v0, v1);
+        const bool replayed = replay(u0, u1, v0, v1, S);
         bool ok = replayed;
         if (!replayed) grow_all = true;
-        const int n = int(rrank_.size());
+        const int n = int(S.rrank_.size());
         if (replayed) {
             key.clear();
-            for (size_t s = 0; s < rs_.size(); ++s) {
-                int a = rrank_[rs_[s].v[0]], b = rrank_[rs_[s].v[1]], c = rrank_[rs_[s].v[2]];
+            for (size_t s = 0; s < S.rs_.size(); ++s) {
+                int a = S.rrank_[S.rs_[s].v[0]], b = S.rrank_[S.rs_[s].v[1]], c = S.rrank_[S.rs_[s].v[2]];
                 if (a > b) std::swap(a, b);
                 if (b > c) std::swap(b, c);
                 if (a > b) std::swap(a, b);
@@ -501,8 +513,8 @@ bool SweepOrder::resolve(const int* tris, int count, uint64_t* birth, int* store
             auto it = std::lower_bound(key.begin(), key.end(), std::make_pair(kq, -1));
             int slot = -1;
             for (; it != key.end() && it->first == kq; ++it) {
-                const Slot& S = rs_[it->second];
-                int sa = rrank_[S.v[0]], sb = rrank_[S.v[1]], sc = rrank_[S.v[2]];
+                const Scratch::Slot& SL = S.rs_[it->second];
+                int sa = S.rrank_[SL.v[0]], sb = S.rrank_[SL.v[1]], sc = S.rrank_[SL.v[2]];
                 if (sa > sb) std::swap(sa, sb);
                 if (sb > sc) std::swap(sb, sc);
                 if (sa > sb) std::swap(sa, sb);
@@ -513,14 +525,14 @@ bool SweepOrder::resolve(const int* tris, int count, uint64_t* birth, int* store
                 grow_all = true;
                 break;
             }
-            const Slot& S = rs_[slot];
+            const Scratch::Slot& SL = S.rs_[slot];
             // every eaten state must be a triangle of the full prefix DT
-            int origin = S.v[2];
+            int origin = SL.v[2];
             bool certified = true;
-            for (int h = S.hist; h >= 0; h = rh_[h].prev) {
-                const Hist& H = rh_[h];
+            for (int h = SL.hist; h >= 0; h = S.rh_[h].prev) {
+                const Scratch::Hist& H = S.rh_[h];
                 int cu0 = u0, cu1 = u1, cv0 = v0, cv1 = v1;
-                if (!whole && !disk_clear(rrank_[H.v[0]], rrank_[H.v[1]], rrank_[H.v[2]], rrank_[H.time],
+                if (!whole && !disk_clear(S.rrank_[H.v[0]], S.rrank_[H.v[1]], S.rrank_[H.v[2]], S.rrank_[H.time],
                                           cu0, cu1, cv0, cv1, 2 * bs_)) {
                     ok = certified = false;
                     nu0 = std::min(nu0, cu0);
@@ -531,23 +543,23 @@ bool SweepOrder::resolve(const int* tris, int count, uint64_t* birth, int* store
                 origin = H.v[2];  // after the loop: the contents at the end of its birth
             }
             if (!certified) continue;  // collect every offender of this attempt
-            const int pb = rrank_[S.birth];
+            const int pb = S.rrank_[SL.birth];
             // contents at the end of the birth insertion, in the window's rotation
-            int b0[3] = {S.v[0], S.v[1], S.v[2]};
-            for (int h = S.hist; h >= 0; h = rh_[h].prev)
-                for (int q = 0; q < 3; ++q) b0[q] = rh_[h].v[q];
+            int b0[3] = {SL.v[0], SL.v[1], SL.v[2]};
+            for (int h = SL.hist; h >= 0; h = S.rh_[h].prev)
+                for (int q = 0; q < 3; ++q) b0[q] = S.rh_[h].v[q];
             uint64_t bkey;
             int shift = 0;  // window rotation -> the sweep's rotation
-            const bool lead = S.birth == rapex_;
+            const bool lead = SL.birth == S.rapex_;
             int jq = -1;
             if (whole) {
-                jq = S.fan;
+                jq = SL.fan;
             } else if (lead) {
-                bool same = rapex_ == apex_ && pb == apex_;
-                for (int i = 0; i <= rapex_ && same; ++i) same = rrank_[i] == i;
-                if (same) jq = S.fan;
+                bool same = S.rapex_ == apex_ && pb == apex_;
+                for (int i = 0; i <= S.rapex_ && same; ++i) same = S.rrank_[i] == i;
+                if (same) jq = SL.fan;
             } else {
-                jq = fan_index(rrank_[origin], pb);
+                jq = fan_index(S.rrank_[origin], pb);
                 if (jq < 0 && !fallback) {
                     // the window's visible chain from pb (it faces right, toward the
                     // new point) is not the full prefix's: the window cut the
@@ -562,9 +574,9 @@ bool SweepOrder::resolve(const int* tris, int count, uint64_t* birth, int* store
             } else {
                 // born from a hull vertex of the window that is not one of the
                 // full prefix's: follow the rest of the chain in the full set
-                const int tb[3] = {rrank_[b0[0]], rrank_[b0[1]], rrank_[b0[2]]};
+                const int tb[3] = {S.rrank_[b0[0]], S.rrank_[b0[1]], S.rrank_[b0[2]]};
                 int qs[3];
-                if (!query(tb[0], tb[1], tb[2], bkey, qs)) return false;
+                if (!query(tb[0], tb[1], tb[2], bkey, qs, S)) return false;
                 int pos = -1;
                 for (int q = 0; q < 3; ++q)
                     if (qs[q] == tb[0]) pos = q;
@@ -572,7 +584,7 @@ bool SweepOrder::resolve(const int* tris, int count, uint64_t* birth, int* store
                 shift = pos;  // qs[(i + shift) % 3] == tb[i]
             }
             int fin[3];
-            for (int q = 0; q < 3; ++q) fin[(q + shift) % 3] = rrank_[S.v[q]];
+            for (int q = 0; q < 3; ++q) fin[(q + shift) % 3] = S.rrank_[SL.v[q]];
             birth[t] = bkey;
             stored[3 * t] = fin[0];
             stored[3 * t + 1] = fin[1];

@@ -31,6 +31,7 @@
 #pragma once
 
 #include <cstdint>
+#include <memory>
 #include <vector>
 
 #include "delaunay.hpp"
@@ -39,6 +40,10 @@ namespace ps {
 
 class SweepOrder {
 public:
+    // Mutable state of one query (window points, replay slots and history):
+    // queries on the same SweepOrder may run concurrently, one Scratch each.
+    struct Scratch;
+
     // px/py: the lexicographically sorted, deduplicated points (ranks 0..m-1).
     void init(const int* px, const int* py, int m);
     // Triangle with ranks (a, b, c), counter-clockwise (orient > 0), of the
@@ -46,7 +51,8 @@ public:
     // the slot the sweep leaves it in (ordered like the slot indices), and
     // stored[0..2] = its ranks in the sweep's stored rotation.  Returns false
     // if the chain could not be followed (the caller then replays the sweep).
-    bool query(int a, int b, int c, uint64_t& birth, int stored[3]);
+    bool query(int a, int b, int c, uint64_t& birth, int stored[3]) { return query(a, b, c, birth, stored, own()); }
+    bool query(int a, int b, int c, uint64_t& birth, int stored[3], Scratch& S) const;
 
     // The same for a group of final triangles (ranks, counter-clockwise, 3 per
     // triangle) by replaying the sweep on the points of a window around them
@@ -55,12 +61,14 @@ public:
     // in its closed circumdisk) and every fan birth checked against the full
     // hull; the window doubles until all certify.  Returns false only when
     // even the whole set fails (an inconsistency: the caller replays).
-    bool resolve(const int* tris, int count, uint64_t* birth, int* stored);
+    bool resolve(const int* tris, int count, uint64_t* birth, int* stored) {
+        return resolve(tris, count, birth, stored, own());
+    }
+    bool resolve(const int* tris, int count, uint64_t* birth, int* stored, Scratch& S) const;
 
-    long long window_points = 0;  // statistics: points triangulated in windows
-    int windows = 0;
-    long long replay_points = 0;  // statistics: points replayed by resolve()
-    int replays = 0;
+    // the scratch of the single-threaded entry points (and their statistics)
+    Scratch& scratch() { return own(); }
+    const Scratch& stats() { return own(); }
 
 private:
     long long orient(int a, int b, int c) const {
@@ -68,14 +76,14 @@ private:
                ((long long)y_[b] - y_[a]) * ((long long)x_[c] - x_[a]);
     }
     int incircle(int a, int b, int c, int d) const;  // exact sign
-    int hull_prev(int o, int p);                     // CCW predecessor of o on hull(Q<p), -1 if none
-    int fan_index(int o, int p);                     // j with o = x_{j+1} on p's visible chain, else -1
-    bool window_triangle(int o, int p, int out[3]);  // sigma (ranks, CCW)
+    int hull_prev(int o, int p) const;                     // CCW predecessor of o on hull(Q<p), -1 if none
+    int fan_index(int o, int p) const;                     // j with o = x_{j+1} on p's visible chain, else -1
+    bool window_triangle(int o, int p, int out[3], Scratch& S) const;  // sigma (ranks, CCW)
     // true if no point of rank < p outside the box [u0,u1]x[v0,v1] lies in the
     // closed circumdisk of the CCW triangle (a, b, c); grows the box to cover
     // the offenders otherwise
-    bool disk_clear(int a, int b, int c, int p, int& u0, int& u1, int& v0, int& v1, int grow);
-    bool replay(int u0, int u1, int v0, int v1);  // lex sweep of the window's points, with slot history
+    bool disk_clear(int a, int b, int c, int p, int& u0, int& u1, int& v0, int& v1, int grow) const;
+    bool replay(int u0, int u1, int v0, int v1, Scratch& S) const;  // lex sweep of the window's points, with slot history
 
     const int* x_ = nullptr;
     const int* y_ = nullptr;
@@ -91,8 +99,12 @@ private:
     // bucket grid of ranks (increasing within a bucket)
     int bs_ = 16, bw_ = 0, bh_ = 0;
     std::vector<int> bstart_, bitems_;
-    // window scratch
-    std::vector<int> wu_, wv_, wrank_, wtris_;
+    Scratch& own();
+    std::unique_ptr<Scratch> own_;
+};
+
+struct SweepOrder::Scratch {
+    std::vector<int> wu_, wv_, wrank_, wtris_;  // window points
     // replay state (window ranks; slot = 4 * index, half-edge = 4 * slot + k)
     struct Slot {
         int v[3];
@@ -113,6 +125,8 @@ private:
     std::vector<int> rrank_, rhn_, rhp_, rhe_, rstack_;
     int rapex_ = -1;
     DelaunayWorkspace ws_;
+    long long window_points = 0, replay_points = 0;  // statistics
+    int windows = 0, replays = 0;
 };
 
 }  // namespace ps

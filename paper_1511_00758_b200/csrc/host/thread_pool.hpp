@@ -8,9 +8,12 @@
 // n items and returns when all are done.
 #pragma once
 
+#include <algorithm>
+#include <atomic>
 #include <condition_variable>
 #include <deque>
 #include <functional>
+#include <memory>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -54,6 +57,39 @@ public:
         if (n <= 0) return;
         for (int i = 0; i < n; ++i) submit([&fn, i](int w) { fn(i, w); });
         wait_idle();
+    }
+
+    // Runs fn(item, worker) for item in [0, n) from inside a task running on
+    // `self`: the caller works through the items itself while up to n - 1
+    // helper tasks (queued behind earlier tasks) take items in parallel when
+    // a worker is free.  Returns when every item has finished; a helper that
+    // starts after that finds no item and returns without touching fn.
+    void help_run(int self, int n, const std::function<void(int, int)>& fn) {
+        if (n <= 0) return;
+        struct State {
+            std::atomic<int> next{0};
+            int done = 0;
+            std::mutex m;
+            std::condition_variable cv;
+        };
+        auto st = std::make_shared<State>();
+        // fn is alive while an item is unclaimed (the caller waits for all)
+        auto work = [st, n](int w, const std::function<void(int, int)>* f) {
+            for (int i; (i = st->next.fetch_add(1)) < n;) {
+                (*f)(i, w);
+                std::lock_guard<std::mutex> lk(st->m);
+                if (++st->done == n) st->cv.notify_all();
+            }
+        };
+        const int helpers = std::min(n - 1, size() - 1);
+        const std::function<void(int, int)>* fp = &fn;
+        for (int h = 0; h < helpers; ++h)
+            submit([st, n, work, fp](int w) {
+                if (st->next.load() < n) work(w, fp);
+            });
+        work(self, fp);
+        std::unique_lock<std::mutex> lk(st->m);
+        st->cv.wait(lk, [&] { return st->done == n; });
     }
 
 private:

@@ -23,93 +23,210 @@ namespace ps {
 
 namespace {
 
-constexpr int kTileW = 128;  // 32 threads x 4 px
-constexpr int kTileH = 8;
-constexpr int kHalo = 2;
-constexpr int kSmW = kTileW + 2 * kHalo;
-constexpr int kSmH = kTileH + 2 * kHalo;
+// K1 layout.  A block covers a 128 x 32 tile of the frame.  Shared memory
+// holds the tile plus a 2-px halo as 32-bit words in a column-INTERLEAVED
+// order: word (r, j) packs the bytes of tile columns j-2, j+30, j+62 and j+94
+// (byte q = column j-2+32q) of tile row r-2.  Lane c of a warp then owns the
+// four pixels c, c+32, c+64, c+96 of a row, and the 5x5 census window of all
+// four is the 5x5 block of words (rows r-2..r+2, words c..c+4): one aligned
+// 32-bit shared load per neighbour and no byte extraction.  The 24 census
+// comparisons run four pixels per instruction group (SWAR, below), the
+// outputs of a lane are warp-contiguous per q (coalesced 128-B census stores).
+constexpr int kK1W = 128;             // tile columns (4 x 32)
+constexpr int kK1H = 32;              // tile rows (8 warps x 4 rows)
+constexpr int kK1Rows = kK1H + 4;     // staged rows (2-px halo above and below)
+constexpr int kK1Words = 36;          // interleaved words per staged row (32 + halo)
+constexpr int kK1RowsPerWarp = kK1H / 8;
 
-__device__ __forceinline__ uint32_t census_at(const uint8_t (*s)[kSmW], int x, int y) {
-    // Bit k = k-th neighbour of the 5x5 window in row-major order, centre
-    // skipped, set when strictly darker than the centre (census.cpp:22-35).
-    const uint8_t c = s[y][x];
-    uint32_t desc = 0;
-    int bit = 0;
-#pragma unroll
-    for (int dv = -2; dv <= 2; ++dv) {
-#pragma unroll
-        for (int du = -2; du <= 2; ++du) {
-            if (dv == 0 && du == 0) continue;
-            desc |= uint32_t(s[y + dv][x + du] < c) << bit;
-            ++bit;
-        }
-    }
-    return desc;
+// Byte-wise a < b flags in bit 7 of each byte (SWAR, no carries across
+// bytes): d7 = [a_lo7 < b_lo7] from (b & 0x7f) + (~a & 0x7f); then
+// a < b <=> (!a7 & b7) | (a7 == b7 & d7).  na = ~a & 0x7f7f7f7f and
+// cb = b & 0x7f7f7f7f are computed once per word.
+__device__ __forceinline__ uint32_t lt_flags(uint32_t a, uint32_t na, uint32_t b, uint32_t cb) {
+    const uint32_t d = cb + na;
+    uint32_t t;
+    // f(a, b, d) = (~a & b) | (~(a ^ b) & d): truth table over (a, b, d) = (0xF0, 0xCC, 0xAA)
+    asm("lop3.b32 %0, %1, %2, %3, 0x8e;" : "=r"(t) : "r"(a), "r"(b), "r"(d));
+    return t;
 }
 
-__global__ void __launch_bounds__(256) k_frontend(const uint8_t* __restrict__ left,
+// Census of the four interleaved pixels of the centre word w[2][2] of a 5x5
+// word window: three accumulators hold bits 0-7, 8-15, 16-23 of the four
+// descriptors, byte q for pixel q (bit k = k-th neighbour in row-major order,
+// centre skipped, set when strictly darker: census.cpp:22-35).  Each
+// comparison shifts its accumulator right by one and ORs its flags into bit 7,
+// so after eight the first is in bit 0.
+__device__ __forceinline__ void census4(const uint32_t (&w)[5][5], const uint32_t (&nw)[5][5],
+                                        uint32_t& a0, uint32_t& a1, uint32_t& a2) {
+    const uint32_t b = w[2][2], cb = b & 0x7f7f7f7fu;
+    uint32_t acc[3] = {0u, 0u, 0u};
+    int k = 0;
+#pragma unroll
+    for (int dv = 0; dv < 5; ++dv) {
+#pragma unroll
+        for (int du = 0; du < 5; ++du) {
+            if (dv == 2 && du == 2) continue;
+            const uint32_t t = lt_flags(w[dv][du], nw[dv][du], b, cb);
+            acc[k >> 3] = (acc[k >> 3] >> 1) | (t & 0x80808080u);
+            ++k;
+        }
+    }
+    a0 = acc[0];
+    a1 = acc[1];
+    a2 = acc[2];
+}
+
+// descriptor of interleaved pixel q from the three accumulators
+__device__ __forceinline__ uint32_t census_of(uint32_t a0, uint32_t a1, uint32_t a2, int q) {
+    const uint32_t lo = __byte_perm(a0, a1, uint32_t(q) | uint32_t(4 + q) << 4);
+    return __byte_perm(lo, a2, 0x0010u | uint32_t(4 + q) << 8) & 0x00ffffffu;
+}
+
+// Stage rows [v0-2, v0+kK1H+2) x columns [u0-2, u0+130) of both images into
+// the interleaved words (zeros outside the image; those bytes only feed
+// border pixels, whose census and mask are 0).  All of a thread's global
+// loads are issued before the first shared store (one latency per block).
+constexpr int kK1Src = kK1Rows * 34;               // 4-column source words per image
+constexpr int kK1SrcIt = (kK1Src + 255) / 256;     // per thread
+
+__device__ __forceinline__ uint32_t k1_load(const uint8_t* __restrict__ img, int W, int H, int u0, int v0,
+                                            bool aligned, int i) {
+    const int r = i / 34, k = i - r * 34;
+    const int gv = v0 - 2 + r, gu = u0 - 4 + 4 * k;
+    uint32_t x = 0;
+    if (i < kK1Src && gv >= 0 && gv < H) {
+        const uint8_t* row = img + (long long)gv * W;
+        if (aligned && gu >= 0 && gu + 3 < W) {
+            x = __ldg(reinterpret_cast<const uint32_t*>(row + gu));
+        } else {
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+                if (gu + b >= 0 && gu + b < W) x |= uint32_t(__ldg(row + gu + b)) << (8 * b);
+        }
+    }
+    return x;
+}
+
+__device__ __forceinline__ void k1_store(uint32_t (*sw)[kK1Words], int i, uint32_t x) {
+    if (i >= kK1Src) return;
+    uint8_t* sb = reinterpret_cast<uint8_t*>(&sw[0][0]);
+    const int r = i / 34, k = i - r * 34;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        const int xc = 4 * k - 4 + b;  // tile column, -4 .. 131
+        if (xc < -2 || xc > 129) continue;
+        const uint8_t byte = uint8_t(x >> (8 * b));
+        // word j = xc + 2 - 32 q for every q with 0 <= j < 36 (one or two)
+        const int q0 = xc + 2 >= kK1Words ? (xc + 2 - kK1Words) / 32 + 1 : 0;
+        const int j0 = xc + 2 - 32 * q0;
+        sb[(r * kK1Words + j0) * 4 + q0] = byte;
+        if (j0 >= 32 && q0 < 3) sb[(r * kK1Words + j0 - 32) * 4 + q0 + 1] = byte;
+    }
+}
+
+__global__ void __launch_bounds__(256, 4) k_frontend(const uint8_t* __restrict__ left,
                                                   const uint8_t* __restrict__ right, FrameGeom g,
                                                   int thr, uint8_t* __restrict__ mask,
                                                   uint32_t* __restrict__ cl,
                                                   uint32_t* __restrict__ cr,
                                                   int* __restrict__ mask_count,
                                                   uint8_t* __restrict__ code, uint8_t code_high) {
-    __shared__ uint8_t sl[kSmH][kSmW];
-    __shared__ uint8_t sr[kSmH][kSmW];
+    __shared__ uint32_t sl[kK1Rows][kK1Words];
+    __shared__ uint32_t sr[kK1Rows][kK1Words];
     __shared__ int warp_cnt[8];
     const int f = blockIdx.z;
     const int W = g.width, H = g.height;
-    const int u0 = blockIdx.x * kTileW - kHalo;
-    const int v0 = blockIdx.y * kTileH - kHalo;
+    const int u0 = blockIdx.x * kK1W;
+    const int v0 = blockIdx.y * kK1H;
+    const bool aligned = (W & 3) == 0 && (g.pixels & 3) == 0;
     const uint8_t* L = left + f * g.pixels;
     const uint8_t* R = right ? right + f * g.pixels : nullptr;
-    const int tid = threadIdx.y * 32 + threadIdx.x;
-    for (int i = tid; i < kSmH * kSmW; i += 256) {
-        const int y = i / kSmW, x = i % kSmW;
-        const int gu = u0 + x, gv = v0 + y;
-        const bool in = gu >= 0 && gu < W && gv >= 0 && gv < H;
-        sl[y][x] = in ? __ldg(L + (long long)gv * W + gu) : 0;
-        if (R) sr[y][x] = in ? __ldg(R + (long long)gv * W + gu) : 0;
+    {
+        const int tid = threadIdx.y * 32 + threadIdx.x;
+        uint32_t xl[kK1SrcIt], xr[kK1SrcIt];
+#pragma unroll
+        for (int it = 0; it < kK1SrcIt; ++it) {
+            xl[it] = k1_load(L, W, H, u0, v0, aligned, tid + 256 * it);
+            xr[it] = R ? k1_load(R, W, H, u0, v0, aligned, tid + 256 * it) : 0u;
+        }
+#pragma unroll
+        for (int it = 0; it < kK1SrcIt; ++it) {
+            k1_store(sl, tid + 256 * it, xl[it]);
+            if (R) k1_store(sr, tid + 256 * it, xr[it]);
+        }
     }
     __syncthreads();
 
-    const int v = blockIdx.y * kTileH + threadIdx.y;
-    const int ub = blockIdx.x * kTileW + threadIdx.x * 4;
-    int cnt = 0;
-    if (v < H) {
-        uint32_t dl[4], dr[4];
-        uint8_t mk[4];
+    const int c = threadIdx.x, wy = threadIdx.y;
+    // gradient threshold in 16-bit lanes: grad in [0, 510]
+    const int tc = thr < 0 ? 0 : (thr > 511 ? 511 : thr);
+    const uint32_t tbias = uint32_t(0x8000 - tc) * 0x00010001u;
+    // interior test per pixel (u in [2, W-2)) of the lane's four columns
+    uint32_t colok = 0;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int u = ub + j;
-            const int x = threadIdx.x * 4 + j + kHalo, y = threadIdx.y + kHalo;
-            const bool interior = u >= 2 && u < W - 2 && v >= 2 && v < H - 2;
-            dl[j] = interior ? census_at(sl, x, y) : 0u;
-            dr[j] = (interior && R) ? census_at(sr, x, y) : 0u;
-            int gm = 0;
-            if (interior) {
-                gm = abs(int(sl[y][x + 1]) - int(sl[y][x - 1])) +
-                     abs(int(sl[y + 1][x]) - int(sl[y - 1][x]));
+    for (int q = 0; q < 4; ++q) {
+        const int u = u0 + c + 32 * q;
+        colok |= uint32_t(u >= 2 && u < W - 2) << q;
+    }
+    int cnt = 0;
+    const int y0 = wy * kK1RowsPerWarp;  // first tile row of this warp
+    // one view at a time (half the live window registers): L with the
+    // gradient mask and code, then R
+#pragma unroll 1
+    for (int view = 0; view < (R ? 2 : 1); ++view) {
+        const uint32_t(*sw)[kK1Words] = view ? sr : sl;
+        uint32_t* cen = view ? cr : cl;
+        uint32_t w[5][5], nw[5][5];
+#pragma unroll
+        for (int dv = 0; dv < 4; ++dv)
+#pragma unroll
+            for (int du = 0; du < 5; ++du) {
+                w[dv + 1][du] = sw[y0 + dv][c + du];
+                nw[dv + 1][du] = ~w[dv + 1][du] & 0x7f7f7f7fu;
             }
-            mk[j] = (interior && gm >= thr) ? 1 : 0;
-            cnt += mk[j];
-        }
-        const long long base = f * g.pixels + (long long)v * W + ub;
-        const bool vec = (ub + 3 < W) && ((base & 3) == 0);
-        if (vec) {
-            if (cl) *reinterpret_cast<uint4*>(cl + base) = make_uint4(dl[0], dl[1], dl[2], dl[3]);
-            if (cr && R) *reinterpret_cast<uint4*>(cr + base) = make_uint4(dr[0], dr[1], dr[2], dr[3]);
-            if (mask) *reinterpret_cast<uchar4*>(mask + base) = make_uchar4(mk[0], mk[1], mk[2], mk[3]);
-            if (code)
-                *reinterpret_cast<uchar4*>(code + base) =
-                    make_uchar4(mk[0] ? code_high : kCodeOff, mk[1] ? code_high : kCodeOff,
-                                mk[2] ? code_high : kCodeOff, mk[3] ? code_high : kCodeOff);
-        } else {
-            for (int j = 0; j < 4 && ub + j < W; ++j) {
-                if (cl) cl[base + j] = dl[j];
-                if (cr && R) cr[base + j] = dr[j];
-                if (mask) mask[base + j] = mk[j];
-                if (code) code[base + j] = mk[j] ? code_high : kCodeOff;
+#pragma unroll
+        for (int i = 0; i < kK1RowsPerWarp; ++i) {
+            // slide the window one row down: staged rows y0+i .. y0+i+4
+#pragma unroll
+            for (int dv = 0; dv < 4; ++dv)
+#pragma unroll
+                for (int du = 0; du < 5; ++du) {
+                    w[dv][du] = w[dv + 1][du];
+                    nw[dv][du] = nw[dv + 1][du];
+                }
+#pragma unroll
+            for (int du = 0; du < 5; ++du) {
+                w[4][du] = sw[y0 + i + 4][c + du];
+                nw[4][du] = ~w[4][du] & 0x7f7f7f7fu;
+            }
+            const int v = v0 + y0 + i;
+            if (v >= H) break;  // warp-uniform
+            const bool row_in = v >= 2 && v < H - 2;
+            const uint32_t ok = row_in ? colok : 0u;
+            const long long base = f * g.pixels + (long long)v * W + u0 + c;
+            if (cen) {
+                uint32_t a0, a1, a2;
+                census4(w, nw, a0, a1, a2);
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (u0 + c + 32 * q < W) cen[base + 32 * q] = ((ok >> q) & 1u) ? census_of(a0, a1, a2, q) : 0u;
+            }
+            if (view == 0 && (mask || code || mask_count)) {
+                // |L(u+1)-L(u-1)| + |L(v+1)-L(v-1)| >= threshold (image.cpp:43-60), 16-bit lanes
+                const uint32_t gh = __vabsdiffu4(w[2][3], w[2][1]);
+                const uint32_t gv = __vabsdiffu4(w[3][2], w[1][2]);
+                const uint32_t ge = (gh & 0x00ff00ffu) + (gv & 0x00ff00ffu) + tbias;                // pixels 0, 2
+                const uint32_t go = ((gh >> 8) & 0x00ff00ffu) + ((gv >> 8) & 0x00ff00ffu) + tbias;  // 1, 3
+                const uint32_t mk =
+                    (((ge >> 15) & 1u) | ((go >> 14) & 2u) | ((ge >> 29) & 4u) | ((go >> 28) & 8u)) & ok;
+                cnt += __popc(mk);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (u0 + c + 32 * q >= W) continue;
+                    const bool m = (mk >> q) & 1u;
+                    if (mask) mask[base + 32 * q] = m ? 1 : 0;
+                    if (code) code[base + 32 * q] = m ? code_high : kCodeOff;
+                }
             }
         }
     }
@@ -117,7 +234,7 @@ __global__ void __launch_bounds__(256) k_frontend(const uint8_t* __restrict__ le
         cnt = __reduce_add_sync(0xffffffffu, cnt);
         if (threadIdx.x == 0) warp_cnt[threadIdx.y] = cnt;
         __syncthreads();
-        if (tid == 0) {
+        if (threadIdx.x == 0 && threadIdx.y == 0) {
             int s = 0;
             for (int i = 0; i < 8; ++i) s += warp_cnt[i];
             if (s) atomicAdd(mask_count + f, s);
@@ -396,7 +513,7 @@ __global__ void __launch_bounds__(1024) k_candidate_sort(
 int launch_frontend(const uint8_t* left, const uint8_t* right, FrameGeom g, int frames,
                     int grad_threshold, uint8_t* mask, uint32_t* cl, uint32_t* cr,
                     int* mask_count, cudaStream_t st, uint8_t* code, int code_high) {
-    dim3 grid((g.width + kTileW - 1) / kTileW, (g.height + kTileH - 1) / kTileH, frames);
+    dim3 grid((g.width + kK1W - 1) / kK1W, (g.height + kK1H - 1) / kK1H, frames);
     k_frontend<<<grid, dim3(32, 8), 0, st>>>(left, right, g, grad_threshold, mask, cl, cr,
                                              mask_count, code, uint8_t(code_high));
     return 1;

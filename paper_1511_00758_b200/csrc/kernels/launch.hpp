@@ -8,6 +8,7 @@
 
 #include "common.cuh"
 #include "planestereo_c.h"
+#include "star_layout.hpp"
 
 namespace ps {
 
@@ -113,16 +114,12 @@ int launch_add_counts(int* S, const int* a, const int* b, int frames, cudaStream
 // K4 on the device (star.cu, star_dt.cuh): per-frame exact Delaunay of the
 // support lists of a frame group.  Arrays are frame-strided: supports and
 // per-support scratch by scap, cells by gw*gh (+1 for cell_start), triangles
-// and pin bytes by pitch, flags by kStarFlagInts.  Flags per frame: [0] fail
+// and pin bytes by pitch, flags by flag_ints.  Flags per frame: [0] fail
 // (the host replays the reference sweep for that frame), [1] rotation
 // suspects (4 ints each at kStarSuspectBase: triangle, v0, v1, v2), [2] ints
 // used and [3] count of the ambiguous hull vertices at kStarFanBase (vertex,
 // n, then n counter-clockwise triangles of 3 vertex ids), [4] collinear set,
 // [5] points deferred from pass 1 (k_star) to pass 2 (k_star_far).
-constexpr int kStarFlagInts = 2048;
-constexpr int kStarSuspectBase = 8;
-constexpr int kStarMaxSuspect = 64;
-constexpr int kStarFanBase = kStarSuspectBase + 4 * kStarMaxSuspect;
 struct StarArgs {
     const int* su;
     const int* sv;
@@ -144,6 +141,7 @@ struct StarArgs {
     uint8_t* pins;
     int* tri_count;
     int* flags;
+    int flag_ints, max_suspect, fan_base;  // star_flag_layout(scap)
     unsigned long long* col_key;  // per frame 2 * W: column extremes as (v, index) keys
     int* col_idx;                 // per frame 2 * W: their point indices (-1: empty column)
     int* hull;                    // per frame 2 * scap: hull successor / predecessor per point

@@ -94,7 +94,7 @@ __device__ __forceinline__ star::Grid make_grid(const StarArgs& a, int f) {
     const int* hull = a.hull + 2 * sb;
     return star::Grid{a.su + sb, a.sv + sb, a.dup + sb, a.cell_start + cb, a.cell_items + sb, a.S[f],
                       0, 0, a.W - 1, a.H - 1, a.gs, a.gw, a.gh, cols, cols + a.W, hull, hull + a.scap,
-                      a.flags[(long long)f * kStarFlagInts + 4], 1.0 / a.gs};
+                      a.flags[(long long)f * a.flag_ints + 4], 1.0 / a.gs};
 }
 
 __global__ void k_grid_count(StarArgs a) {
@@ -203,7 +203,7 @@ __global__ void k_hull(StarArgs a) {
         }
     int* hnext = a.hull + 2 * sb;
     int* hprev = hnext + a.scap;
-    int* flat = a.flags + (long long)f * kStarFlagInts + 4;
+    int* flat = a.flags + (long long)f * a.flag_ints + 4;
     if (c0 < 0) {
         *flat = 1;
         return;
@@ -308,7 +308,12 @@ __global__ void k_grid_pack(StarArgs a) {
     a.cell_xy[sb + k] = a.dup[sb + s] ? -1 : (a.sv[sb + s] << 16) | a.su[sb + s];
 }
 
-__device__ __forceinline__ void set_fail(const StarArgs& a, int f) { atomicExch(a.flags + (long long)f * kStarFlagInts, 1); }
+// flags[0] = 1 sends the frame to the host replay; flags[6] ORs the causes
+// (1 fan record full, 2 search failed, 4 star above kFarTris, 8 suspects full)
+__device__ __forceinline__ void set_fail(const StarArgs& a, int f, int why) {
+    atomicExch(a.flags + (long long)f * a.flag_ints, 1);
+    atomicOr(a.flags + (long long)f * a.flag_ints + 6, why);
+}
 
 #ifdef PS_STAR_PROFILE
 __device__ unsigned long long g_star_cycles, g_star_max, g_star_n, g_star_hist[24];
@@ -389,15 +394,15 @@ __device__ void hull_outcome(const StarArgs& a, int f, int p, const HullCheck& h
         pt[2] = s2;
         return;
     }
-    int* fl = a.flags + (long long)f * kStarFlagInts;
+    int* fl = a.flags + (long long)f * a.flag_ints;
     const int need = 2 + 3 * h.n_inc;
     const int at = atomicAdd(fl + 2, need);
-    if (kStarFanBase + at + need > kStarFlagInts) {
-        set_fail(a, f);
+    if (a.fan_base + at + need > a.flag_ints) {
+        set_fail(a, f, 1);
         return;
     }
     atomicAdd(fl + 3, 1);
-    int* w = fl + kStarFanBase + at;
+    int* w = fl + a.fan_base + at;
     w[0] = p;
     w[1] = h.n_inc;
     write_fan(w + 2);
@@ -420,7 +425,7 @@ constexpr int kRegionCells = star::kTileRegion * star::kTileRegion;
 static_assert(kRegionCells == 2 * kTileT, "two region cells per thread");
 
 __device__ __forceinline__ void defer_point(const StarArgs& a, int f, int p) {
-    const int k = atomicAdd(a.flags + (long long)f * kStarFlagInts + 5, 1);
+    const int k = atomicAdd(a.flags + (long long)f * a.flag_ints + 5, 1);
     if (k < a.scap) a.hard[(long long)f * a.scap + k] = p;
 }
 
@@ -603,7 +608,7 @@ __global__ void __launch_bounds__(kTileT) k_star(StarArgs a) {
 constexpr int kFarT = 128;      // 4 warps per block
 constexpr int kFarR = 4;        // gather radius in cells
 constexpr int kFarCap = 256;    // gathered points per warp
-constexpr int kFarTris = 96;    // triangles of one star (more: the frame is replayed on the host)
+constexpr int kFarTris = 640;   // triangles of one star (more: the frame is replayed on the host)
 
 struct WLocal {
     int n;
@@ -937,7 +942,7 @@ __device__ __noinline__ int w_step(const star::Grid& g, const WLocal& L, int p, 
 
 // The star of p into tb ((b, c) per triangle (p, b, c): counter-clockwise
 // from p's nearest neighbour, then clockwise for a hull vertex).  Returns
-// the triangle count, -2 on a failed search or more than kFarTris.
+// the triangle count, -2 on a failed search, -4 past kFarTris triangles.
 __device__ __noinline__ int w_walk(const star::Grid& g, const WLocal& L, int p, bool& closed, int* tb) {
     const int lane = threadIdx.x & 31;
     closed = false;
@@ -955,7 +960,7 @@ __device__ __noinline__ int w_walk(const star::Grid& g, const WLocal& L, int p, 
             const int r = w_step(g, L, p, cur, side);
             if (r == -2) return -2;
             if (r < 0) break;
-            if (count == kFarTris) return -2;
+            if (count == kFarTris) return -4;
             if (lane == 0) {
                 tb[2 * count] = side > 0 ? cur : r;
                 tb[2 * count + 1] = side > 0 ? r : cur;
@@ -976,7 +981,7 @@ __global__ void __launch_bounds__(kFarT) k_star_far(StarArgs a) {
     __shared__ int s_tri[kFarT / 32][2 * kFarTris];  // (b, c) of each triangle (p, b, c), walk order
     const int f = blockIdx.y;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int n = min(a.flags[(long long)f * kStarFlagInts + 5], a.scap);
+    const int n = min(a.flags[(long long)f * a.flag_ints + 5], a.scap);
     const int warps = gridDim.x * (kFarT >> 5);
     const star::Grid g = make_grid(a, f);
     const long long sb = (long long)f * a.scap;
@@ -996,7 +1001,7 @@ __global__ void __launch_bounds__(kFarT) k_star_far(StarArgs a) {
         const int nt = w_walk(g, L, p, closed, tb);
         FAR_ADD(10, FAR_CLOCK() - tg);
         if (nt < 0) {  // a failed search, or more than kFarTris triangles
-            if (lane == 0) set_fail(a, f);
+            if (lane == 0) set_fail(a, f, nt == -4 ? 4 : 2);
             continue;
         }
         __syncwarp();
@@ -1051,10 +1056,10 @@ __global__ void k_tri_check(StarArgs a) {
     if (d1 == floor(d1) && d2 == floor(d2) && d3 == floor(d3)) return;
     const Fit f0 = fit3(su, sv, sd, i, j, k), f1 = fit3(su, sv, sd, j, k, i), f2 = fit3(su, sv, sd, k, i, j);
     if (same_bits(f0, f1) && same_bits(f0, f2)) return;
-    int* fl = a.flags + (long long)f * kStarFlagInts;
+    int* fl = a.flags + (long long)f * a.flag_ints;
     const int s = atomicAdd(fl + 1, 1);
-    if (s >= kStarMaxSuspect) {
-        set_fail(a, f);
+    if (s >= a.max_suspect) {
+        set_fail(a, f, 8);
         return;
     }
     int* w = fl + kStarSuspectBase + 4 * s;
@@ -1122,7 +1127,7 @@ int launch_star_mesh(const StarArgs& a, int max_points, cudaStream_t st) {
     const long long cells = (long long)a.gw * a.gh;
     cudaMemsetAsync(a.cell_cnt, 0, sizeof(int) * cells * a.frames, st);
     cudaMemsetAsync(a.tri_count, 0, sizeof(int) * a.frames, st);
-    cudaMemset2DAsync(a.flags, sizeof(int) * kStarFlagInts, 0, sizeof(int) * kStarFanBase, a.frames, st);
+    cudaMemset2DAsync(a.flags, sizeof(int) * a.flag_ints, 0, sizeof(int) * a.fan_base, a.frames, st);
     if (max_points <= 0) return 0;
     const dim3 grid((max_points + 255) / 256, a.frames);
     k_grid_count<<<grid, 256, 0, st>>>(a); STAR_CHECK("k_grid_count");

@@ -116,7 +116,7 @@ void compare_mesh(FrameMesh& fm, int W, int H, float nd, const char* tag) {
     const int na = mesh_iteration(fm, W, H, nd, ta.data(), cap, pa.data(), wa, st);
     if (std::getenv("TEST_MESH_VERBOSE"))
         std::printf("  stats: rot_checked %lld rotations %lld ambiguous %lld fallbacks %lld order %.1f ms replays %d pts %lld windows %d\n",
-                    st.rot_checked, st.rotations, st.ambiguous, st.fallbacks, st.order_ms, fm.so.replays, fm.so.replay_points, fm.so.windows);
+                    st.rot_checked, st.rotations, st.ambiguous, st.fallbacks, st.order_ms, fm.so.stats().replays, fm.so.stats().replay_points, fm.so.stats().windows);
     const int nb = delaunay_lex(fm.u.data(), fm.v.data(), n, tb.data(), cap, wb);
     if (nb > 0) lex_hull_pins(wb, nb, W, H, pb.data());
     ++sets;
