@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libplanestereo_b200.so")
+# PS_LIB_PATH: an instrumented build of the same sources (profiling probes)
+LIB_PATH = os.environ.get("PS_LIB_PATH") or os.path.join(_HERE, "libplanestereo_b200.so")
 
 
 class PsConfig(C.Structure):

@@ -173,11 +173,17 @@ Engine::Engine(int device) : device_(device) {
     // pool) run at high priority; the bulk seeding at low priority.
     int prio_low = 0, prio_high = 0;
     cudaDeviceGetStreamPriorityRange(&prio_low, &prio_high);
-    for (FrameGroup& g : groups_) cudaStreamCreateWithPriority(&g.st, cudaStreamNonBlocking, prio_high);
+    for (FrameGroup& g : groups_) {
+        cudaStreamCreateWithPriority(&g.st, cudaStreamNonBlocking, prio_high);
+        cudaStreamCreateWithPriority(&g.mst, cudaStreamNonBlocking, prio_low);
+        cudaEventCreateWithFlags(&g.mesh_in, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&g.mesh_out, cudaEventDisableTiming);
+    }
     cudaStreamCreateWithPriority(&seed_st_, cudaStreamNonBlocking, prio_low);
     cudaEventCreateWithFlags(&start_event_, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&chain_event_, cudaEventDisableTiming);
     if (const char* e = std::getenv("PS_SERIAL_DEVICE")) serial_device_ = std::atoi(e) != 0;
+    if (const char* e = std::getenv("PS_MIN_GROUP")) min_group_ = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("PS_MAX_GROUPS")) set_max_groups(std::atoi(e));
     debug_timeline_ = std::getenv("PS_DEBUG_TIMELINE") != nullptr;
     pool_ = &shared_pool();
@@ -208,6 +214,9 @@ Engine::~Engine() {
                            &g.hPin, &g.hTriCount, &g.hFlags, &g.hFix})
             if (b->p) cudaFreeHost(b->p);
         if (g.st) cudaStreamDestroy(g.st);
+        if (g.mst) cudaStreamDestroy(g.mst);
+        if (g.mesh_in) cudaEventDestroy(g.mesh_in);
+        if (g.mesh_out) cudaEventDestroy(g.mesh_out);
         if (g.done_event) cudaEventDestroy(g.done_event);
     }
     for (auto& p : pending_) {
@@ -520,7 +529,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     // The host loop below only moves data and launches; the workers
     // triangulate continuously while the device runs other groups' stages.
     // frame groups of >= 64 frames (measured on cfg2: 4 groups of 64 beat 8 of 32)
-    const int G = std::max(1, std::min(std::min(kMaxGroups, max_groups_), (F + 63) / 64));
+    const int G = std::max(1, std::min(std::min(kMaxGroups, max_groups_), (F + min_group_ - 1) / min_group_));
     const int tri_cap = int(std::min<long long>(2ll * scap_ + 8, 2ll * P + 8));  // T <= 2S per frame
     // device mesh grid of iteration `it` (1-based): ~1-3 supports per cell —
     // seeds: <= 120 * cap over the frame; later: at most ~2 per cell of the
@@ -587,14 +596,20 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         grp.gw = (W - 1) / grp.gs + 1;
         grp.gh = (H - 1) / grp.gs + 1;
         const StarArgs a = star_args(grp);
-        cudaStream_t gs = grp.st;
-        begin_kernel("star_mesh", 0.0, gs);
-        launches_ += launch_star_mesh(a, std::min(max_points, scap_), gs);
-        launches_ += launch_star_check(a, tri_cap, gs);
-        end_kernel(gs);
-        cudaMemcpyAsync(grp.hTriCount.p, grp.dTriCount.p, sizeof(int) * grp.n, cudaMemcpyDeviceToHost, gs);
+        // on the group's mesh stream: after the supports exist (st), and st
+        // continues (raster of the next iteration, completion event) after it
+        cudaStream_t ms = grp.mst;
+        cudaEventRecord(grp.mesh_in, grp.st);
+        cudaStreamWaitEvent(ms, grp.mesh_in, 0);
+        begin_kernel("star_mesh", 0.0, ms);
+        launches_ += launch_star_mesh(a, std::min(max_points, scap_), ms);
+        launches_ += launch_star_check(a, tri_cap, ms);
+        end_kernel(ms);
+        cudaMemcpyAsync(grp.hTriCount.p, grp.dTriCount.p, sizeof(int) * grp.n, cudaMemcpyDeviceToHost, ms);
         cudaMemcpyAsync(grp.hFlags.p, grp.dFlags.p, sizeof(int) * size_t(grp.n) * flay.ints,
-                        cudaMemcpyDeviceToHost, gs);
+                        cudaMemcpyDeviceToHost, ms);
+        cudaEventRecord(grp.mesh_out, ms);
+        cudaStreamWaitEvent(grp.st, grp.mesh_out, 0);
     };
     auto seed_group = [&](int gi) -> ps_status {
         FrameGroup& grp = groups_[gi];
@@ -1039,6 +1054,10 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                                              scap_, grp.S, dConf + f0, grp.Snext, chunk, gs);
             end_kernel(gs);
             std::swap(grp.S, grp.Snext);
+            if (serial_device_) {  // the next group's pixel stages may start; the mesh runs beside them
+                cudaEventRecord(chain_event_, gs);
+                chained = true;
+            }
             if (device_dt) {  // the next iteration's mesh, as soon as its supports exist
                 int max_s = 0;
                 double mean_s = 0.0;
@@ -1050,7 +1069,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                 enqueue_mesh(grp, mean_s / std::max(1, n) + 1.1 * cells, max_s + 2 * cells);
             }
         }
-        if (serial_device_) {
+        if (serial_device_ && last) {
             cudaEventRecord(chain_event_, gs);
             chained = true;
         }

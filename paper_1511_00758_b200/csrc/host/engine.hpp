@@ -54,6 +54,10 @@ struct FrameGroup {
     cudaEvent_t done_event = nullptr;
     double tic = 0.0;
     cudaStream_t st = nullptr;
+    // the device mesh runs on its own low-priority stream (kernels/star.cu:
+    // latency-bound, small grids), ordered after / before st by two events
+    cudaStream_t mst = nullptr;
+    cudaEvent_t mesh_in = nullptr, mesh_out = nullptr;
     int* S = nullptr;      // device support counts of the group's frames (current)
     int* Snext = nullptr;  // device support counts (next)
     DevBuf dTri, dTriOff, dPlanes, dPack, dPackD, dPackOff, dSprev, dChunk, dPin;
@@ -198,6 +202,7 @@ private:
     // (the host Delaunay bounds it), so nothing is lost, and every launch gets
     // the whole GPU.  PS_SERIAL_DEVICE=0 lets groups overlap.
     bool serial_device_ = true;
+    int min_group_ = 64;  // frames per group at least (PS_MIN_GROUP)
     bool debug_timeline_ = false;  // PS_DEBUG_TIMELINE: group milestones on stderr
     cudaEvent_t chain_event_ = nullptr;
     cudaStream_t seed_st_ = nullptr;  // seeding, group after group (group 0 first)

@@ -42,8 +42,11 @@ constexpr int kK1RowsPerWarp = kK1H / 8;
 // bytes): d7 = [a_lo7 < b_lo7] from (b & 0x7f) + (~a & 0x7f); then
 // a < b <=> (!a7 & b7) | (a7 == b7 & d7).  na = ~a & 0x7f7f7f7f and
 // cb = b & 0x7f7f7f7f are computed once per word.
-__device__ __forceinline__ uint32_t lt_flags(uint32_t a, uint32_t na, uint32_t b, uint32_t cb) {
-    const uint32_t d = cb + na;
+__device__ __forceinline__ uint32_t lt_flags(uint32_t a, uint32_t na, uint32_t b, uint32_t cb, uint32_t one) {
+    // the add as an IMAD by a runtime 1: it issues on the FMA pipe, the LOP3s
+    // on the ALU pipe
+    uint32_t d;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(na), "r"(one), "r"(cb));
     uint32_t t;
     // f(a, b, d) = (~a & b) | (~(a ^ b) & d): truth table over (a, b, d) = (0xF0, 0xCC, 0xAA)
     asm("lop3.b32 %0, %1, %2, %3, 0x8e;" : "=r"(t) : "r"(a), "r"(b), "r"(d));
@@ -55,8 +58,9 @@ __device__ __forceinline__ uint32_t lt_flags(uint32_t a, uint32_t na, uint32_t b
 // descriptors, byte q for pixel q (bit k = k-th neighbour in row-major order,
 // centre skipped, set when strictly darker: census.cpp:22-35).  Each
 // comparison shifts its accumulator right by one and ORs its flags into bit 7,
-// so after eight the first is in bit 0.
-__device__ __forceinline__ void census4(const uint32_t (&w)[5][5], const uint32_t (&nw)[5][5],
+// so after eight the first is in bit 0.  Per comparison and four pixels: two
+// ALU-pipe LOP3s and two FMA-pipe IMADs (the two pipes issue in parallel).
+__device__ __forceinline__ void census4(const uint32_t (&w)[5][5], const uint32_t (&nw)[5][5], uint32_t one,
                                         uint32_t& a0, uint32_t& a1, uint32_t& a2) {
     const uint32_t b = w[2][2], cb = b & 0x7f7f7f7fu;
     uint32_t acc[3] = {0u, 0u, 0u};
@@ -66,8 +70,10 @@ __device__ __forceinline__ void census4(const uint32_t (&w)[5][5], const uint32_
 #pragma unroll
         for (int du = 0; du < 5; ++du) {
             if (dv == 2 && du == 2) continue;
-            const uint32_t t = lt_flags(w[dv][du], nw[dv][du], b, cb);
-            acc[k >> 3] = (acc[k >> 3] >> 1) | (t & 0x80808080u);
+            const uint32_t t = lt_flags(w[dv][du], nw[dv][du], b, cb, one);
+            // acc >> 1 as the high word of acc * 2^31 (FMA pipe; no carries
+            // cross bytes: a byte holds at most 7 flags before this shift)
+            acc[k >> 3] = __umulhi(acc[k >> 3], 0x80000000u) | (t & 0x80808080u);
             ++k;
         }
     }
@@ -84,44 +90,33 @@ __device__ __forceinline__ uint32_t census_of(uint32_t a0, uint32_t a1, uint32_t
 
 // Stage rows [v0-2, v0+kK1H+2) x columns [u0-2, u0+130) of both images into
 // the interleaved words (zeros outside the image; those bytes only feed
-// border pixels, whose census and mask are 0).  All of a thread's global
-// loads are issued before the first shared store (one latency per block).
-constexpr int kK1Src = kK1Rows * 34;               // 4-column source words per image
-constexpr int kK1SrcIt = (kK1Src + 255) / 256;     // per thread
+// border pixels, whose census and mask are 0).  Thread i builds word
+// (r, j) = i from its four bytes (columns j-2+32q: for each q the warp's
+// lanes read consecutive bytes); all of a thread's loads are issued before
+// its first shared store.
+constexpr int kK1Src = kK1Rows * kK1Words;          // interleaved words per image
+constexpr int kK1SrcIt = (kK1Src + 255) / 256;      // per thread
 
-__device__ __forceinline__ uint32_t k1_load(const uint8_t* __restrict__ img, int W, int H, int u0, int v0,
-                                            bool aligned, int i) {
-    const int r = i / 34, k = i - r * 34;
-    const int gv = v0 - 2 + r, gu = u0 - 4 + 4 * k;
+__device__ __forceinline__ uint32_t k1_word(const uint8_t* __restrict__ img, int W, int H, int u0, int v0,
+                                            int i) {
+    const int r = i / kK1Words, j = i - r * kK1Words;
+    const int gv = v0 - 2 + r, gu = u0 + j - 2;
     uint32_t x = 0;
     if (i < kK1Src && gv >= 0 && gv < H) {
         const uint8_t* row = img + (long long)gv * W;
-        if (aligned && gu >= 0 && gu + 3 < W) {
-            x = __ldg(reinterpret_cast<const uint32_t*>(row + gu));
+        if (gu >= 0 && gu + 96 < W) {  // all four columns inside (most words)
+            const uint8_t* q = row + gu;
+            x = __byte_perm(__byte_perm(uint32_t(__ldg(q)), uint32_t(__ldg(q + 32)), 0x0040u),
+                            __byte_perm(uint32_t(__ldg(q + 64)), uint32_t(__ldg(q + 96)), 0x0040u), 0x5410u);
         } else {
 #pragma unroll
-            for (int b = 0; b < 4; ++b)
-                if (gu + b >= 0 && gu + b < W) x |= uint32_t(__ldg(row + gu + b)) << (8 * b);
+            for (int q = 0; q < 4; ++q) {
+                const int u = gu + 32 * q;
+                if (u >= 0 && u < W) x |= uint32_t(__ldg(row + u)) << (8 * q);
+            }
         }
     }
     return x;
-}
-
-__device__ __forceinline__ void k1_store(uint32_t (*sw)[kK1Words], int i, uint32_t x) {
-    if (i >= kK1Src) return;
-    uint8_t* sb = reinterpret_cast<uint8_t*>(&sw[0][0]);
-    const int r = i / 34, k = i - r * 34;
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-        const int xc = 4 * k - 4 + b;  // tile column, -4 .. 131
-        if (xc < -2 || xc > 129) continue;
-        const uint8_t byte = uint8_t(x >> (8 * b));
-        // word j = xc + 2 - 32 q for every q with 0 <= j < 36 (one or two)
-        const int q0 = xc + 2 >= kK1Words ? (xc + 2 - kK1Words) / 32 + 1 : 0;
-        const int j0 = xc + 2 - 32 * q0;
-        sb[(r * kK1Words + j0) * 4 + q0] = byte;
-        if (j0 >= 32 && q0 < 3) sb[(r * kK1Words + j0 - 32) * 4 + q0 + 1] = byte;
-    }
 }
 
 __global__ void __launch_bounds__(256, 4) k_frontend(const uint8_t* __restrict__ left,
@@ -138,7 +133,6 @@ __global__ void __launch_bounds__(256, 4) k_frontend(const uint8_t* __restrict__
     const int W = g.width, H = g.height;
     const int u0 = blockIdx.x * kK1W;
     const int v0 = blockIdx.y * kK1H;
-    const bool aligned = (W & 3) == 0 && (g.pixels & 3) == 0;
     const uint8_t* L = left + f * g.pixels;
     const uint8_t* R = right ? right + f * g.pixels : nullptr;
     {
@@ -146,18 +140,24 @@ __global__ void __launch_bounds__(256, 4) k_frontend(const uint8_t* __restrict__
         uint32_t xl[kK1SrcIt], xr[kK1SrcIt];
 #pragma unroll
         for (int it = 0; it < kK1SrcIt; ++it) {
-            xl[it] = k1_load(L, W, H, u0, v0, aligned, tid + 256 * it);
-            xr[it] = R ? k1_load(R, W, H, u0, v0, aligned, tid + 256 * it) : 0u;
+            xl[it] = k1_word(L, W, H, u0, v0, tid + 256 * it);
+            xr[it] = R ? k1_word(R, W, H, u0, v0, tid + 256 * it) : 0u;
         }
+        uint32_t* fl = &sl[0][0];
+        uint32_t* fr = &sr[0][0];
 #pragma unroll
         for (int it = 0; it < kK1SrcIt; ++it) {
-            k1_store(sl, tid + 256 * it, xl[it]);
-            if (R) k1_store(sr, tid + 256 * it, xr[it]);
+            const int i = tid + 256 * it;
+            if (i < kK1Src) {
+                fl[i] = xl[it];
+                if (R) fr[i] = xr[it];
+            }
         }
     }
     __syncthreads();
 
     const int c = threadIdx.x, wy = threadIdx.y;
+    const uint32_t one = W != 0 ? 1u : 0u;  // 1, opaque to the compiler (see lt_flags)
     // gradient threshold in 16-bit lanes: grad in [0, 510]
     const int tc = thr < 0 ? 0 : (thr > 511 ? 511 : thr);
     const uint32_t tbias = uint32_t(0x8000 - tc) * 0x00010001u;
@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(256, 4) k_frontend(const uint8_t* __restrict__
             const long long base = f * g.pixels + (long long)v * W + u0 + c;
             if (cen) {
                 uint32_t a0, a1, a2;
-                census4(w, nw, a0, a1, a2);
+                census4(w, nw, one, a0, a1, a2);
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
                     if (u0 + c + 32 * q < W) cen[base + 32 * q] = ((ok >> q) & 1u) ? census_of(a0, a1, a2, q) : 0u;
