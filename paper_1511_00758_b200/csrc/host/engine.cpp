@@ -169,13 +169,18 @@ static std::vector<SweepOrder::Scratch>& shared_order_scratch() {
 Engine::Engine(int device) : device_(device) {
     cudaSetDevice(device_);
     cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking);
-    // The groups' pipeline stages (small, latency-critical: they feed the host
-    // pool) run at high priority; the bulk seeding at low priority.
+    // The groups' pixel stages (small, latency-critical: they feed the host
+    // pool) run at the highest priority, the bulk seeding at the lowest, and
+    // the groups' meshes in between, earlier groups first: the first group's
+    // mesh finishes (and its host work starts) while later meshes still run,
+    // instead of all of them finishing together and leaving the host the tail.
     int prio_low = 0, prio_high = 0;
     cudaDeviceGetStreamPriorityRange(&prio_low, &prio_high);
-    for (FrameGroup& g : groups_) {
+    for (int gi = 0; gi < kMaxGroups; ++gi) {
+        FrameGroup& g = groups_[gi];
+        const int mesh_prio = std::min(prio_low, prio_high + 1 + gi);  // numerically lower = higher
         cudaStreamCreateWithPriority(&g.st, cudaStreamNonBlocking, prio_high);
-        cudaStreamCreateWithPriority(&g.mst, cudaStreamNonBlocking, prio_low);
+        cudaStreamCreateWithPriority(&g.mst, cudaStreamNonBlocking, mesh_prio);
         cudaEventCreateWithFlags(&g.mesh_in, cudaEventDisableTiming);
         cudaEventCreateWithFlags(&g.mesh_out, cudaEventDisableTiming);
     }

@@ -253,6 +253,15 @@ bool SweepOrder::window_triangle(int o, int p, int out[3], Scratch& S) const {
 }
 
 bool SweepOrder::query(int a, int b, int c, uint64_t& birth, int stored[3], Scratch& S) const {
+    bool more = false;
+    return query_steps(a, b, c, birth, stored, S, -1, more);
+}
+
+// query() following at most max_steps sigma steps (-1: no limit); `more` is
+// set when the chain needs more (the result is then not written).
+bool SweepOrder::query_steps(int a, int b, int c, uint64_t& birth, int stored[3], Scratch& S, int max_steps,
+                             bool& more) const {
+    more = false;
     if (apex_ < 0) return false;
     struct Step {
         int o, t, p;
@@ -282,6 +291,10 @@ bool SweepOrder::query(int a, int b, int c, uint64_t& birth, int stored[3], Scra
             base[2] = o;
             birth = (uint64_t(uint32_t(p)) << 32) | uint32_t(j);
             break;
+        }
+        if (max_steps >= 0 && int(chain.size()) >= max_steps) {
+            more = true;
+            return false;
         }
         int sigma[3];
         if (!window_triangle(o, p, sigma, S)) return false;
@@ -457,12 +470,36 @@ bool SweepOrder::replay(int u0, int u1, int v0, int v1, Scratch& S) const {
 bool SweepOrder::resolve(const int* tris, int count, uint64_t* birth, int* stored, Scratch& S) const {
     if (apex_ < 0) return false;
     if (count <= 0) return true;
-    static const bool chains = std::getenv("PS_ORDER_CHAINS") != nullptr;
-    if (chains) {
-        for (int t = 0; t < count; ++t)
-            if (!query(tris[3 * t], tris[3 * t + 1], tris[3 * t + 2], birth[t], stored + 3 * t, S)) return false;
+    // Triangles left in a fan slot of their lexicographic maximum need no
+    // window (query's first step, from the precomputed hull chains); only the
+    // rest are resolved by window replays.
+    std::vector<int> rest;
+    for (int t = 0; t < count; ++t) {
+        bool more = false;
+        if (query_steps(tris[3 * t], tris[3 * t + 1], tris[3 * t + 2], birth[t], stored + 3 * t, S, 0, more))
+            continue;
+        if (!more) return false;
+        rest.push_back(t);
+    }
+    ++S.fast_calls;
+    S.fast_hits += count - int(rest.size());
+    if (rest.empty()) return true;
+    if (int(rest.size()) < count) {
+        std::vector<int> sub(3 * rest.size()), ss(3 * rest.size());
+        std::vector<uint64_t> sb(rest.size());
+        for (size_t i = 0; i < rest.size(); ++i)
+            for (int q = 0; q < 3; ++q) sub[3 * i + q] = tris[3 * rest[i] + q];
+        if (!resolve_windows(sub.data(), int(rest.size()), sb.data(), ss.data(), S)) return false;
+        for (size_t i = 0; i < rest.size(); ++i) {
+            birth[rest[i]] = sb[i];
+            for (int q = 0; q < 3; ++q) stored[3 * rest[i] + q] = ss[3 * i + q];
+        }
         return true;
     }
+    return resolve_windows(tris, count, birth, stored, S);
+}
+
+bool SweepOrder::resolve_windows(const int* tris, int count, uint64_t* birth, int* stored, Scratch& S) const {
     int bu0 = INT_MAX, bu1 = INT_MIN, bv0 = INT_MAX, bv1 = INT_MIN;
     for (int i = 0; i < 3 * count; ++i) {
         bu0 = std::min(bu0, x_[tris[i]]);
@@ -474,13 +511,15 @@ bool SweepOrder::resolve(const int* tris, int count, uint64_t* birth, int* store
     int delta = std::max(8, int(2.0 * std::sqrt(area / m_)));
     std::vector<std::pair<uint64_t, int>> key;  // sorted vertex set -> slot
     int u0 = std::max(minx_, bu0 - delta), u1 = std::min(maxx_, bu1 + delta);
-    int v0 = std::max(miny_, bv0 - delta), v1 = std::min(maxy_, bv1 + delta);
-    // Near the last columns the sweep's slots are column-tall fans eaten
-    // point after point down the column: start with the full height there.
-    if (bu0 + delta >= maxx_) {
-        v0 = miny_;
-        v1 = maxy_;
-    }
+    int v0, v1;
+    // The sweep's slots are column-tall fans eaten point after point down the
+    // column, so a window that cuts the columns is (nearly always) grown to
+    // the full height anyway, one doubling per attempt (measured on BASELINE
+    // config 2: 5-6 attempts, the last one full-height): start there.
+    (void)bv0;
+    (void)bv1;
+    v0 = miny_;
+    v1 = maxy_;
     for (int attempt = 0;; ++attempt) {
         const bool whole = u0 == minx_ && u1 == maxx_ && v0 == miny_ && v1 == maxy_;
         // growth for the next attempt: towards the points that broke a

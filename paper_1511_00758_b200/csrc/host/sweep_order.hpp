@@ -53,6 +53,8 @@ public:
     // if the chain could not be followed (the caller then replays the sweep).
     bool query(int a, int b, int c, uint64_t& birth, int stored[3]) { return query(a, b, c, birth, stored, own()); }
     bool query(int a, int b, int c, uint64_t& birth, int stored[3], Scratch& S) const;
+    bool query_steps(int a, int b, int c, uint64_t& birth, int stored[3], Scratch& S, int max_steps,
+                     bool& more) const;
 
     // The same for a group of final triangles (ranks, counter-clockwise, 3 per
     // triangle) by replaying the sweep on the points of a window around them
@@ -83,7 +85,8 @@ private:
     // closed circumdisk of the CCW triangle (a, b, c); grows the box to cover
     // the offenders otherwise
     bool disk_clear(int a, int b, int c, int p, int& u0, int& u1, int& v0, int& v1, int grow) const;
-    bool replay(int u0, int u1, int v0, int v1, Scratch& S) const;  // lex sweep of the window's points, with slot history
+    bool replay(int u0, int u1, int v0, int v1, Scratch& S) const;
+    bool resolve_windows(const int* tris, int count, uint64_t* birth, int* stored, Scratch& S) const;  // lex sweep of the window's points, with slot history
 
     const int* x_ = nullptr;
     const int* y_ = nullptr;
@@ -127,6 +130,7 @@ struct SweepOrder::Scratch {
     DelaunayWorkspace ws_;
     long long window_points = 0, replay_points = 0;  // statistics
     int windows = 0, replays = 0;
+    long long fast_calls = 0, fast_hits = 0;  // resolve() calls, triangles answered without a window
 };
 
 }  // namespace ps
