@@ -174,14 +174,21 @@ __global__ void k_col_decode(StarArgs a) {
 
 // The convex hull boundary of each frame, as star_dt.cuh build_hull (the
 // same chains, the same candidates in the same order): the block loads the
-// column extremes and their rows into shared memory, then one thread runs
-// the monotone chains with (u, v, index) stack entries (no dependent global
-// loads per step); flags[4] = 1 for a collinear set.
-__global__ void k_hull(StarArgs a) {
+// column extremes and their rows into shared memory, then thread 0 runs the
+// lower monotone chain and thread 1 the upper one, each over (u, v, index)
+// stack entries in shared memory when they fit (no dependent global loads
+// per step); flags[4] = 1 for a collinear set.
+__host__ __device__ inline int hull_stack_entries(int W, int H) { return 2 * W + 2 * H + 8; }
+inline size_t hull_smem_bytes(int W, int H, bool stacks) {
+    return size_t(4) * W * sizeof(int) + (stacks ? size_t(2) * hull_stack_entries(W, H) * sizeof(int2) : 0) + 16;
+}
+
+__global__ void k_hull(StarArgs a, int stacks_in_smem) {
     const int f = blockIdx.x;
     extern __shared__ int sm[];
     int* s_idx = sm;             // 2W: col_lo then col_hi
     int* s_v = sm + 2 * a.W;     // their rows
+    __shared__ int s_n[2], s_c[2];
     const long long sb = (long long)f * a.scap;
     const int* cols = a.col_idx + 2ll * f * a.W;
     for (int c = threadIdx.x; c < 2 * a.W; c += blockDim.x) {
@@ -190,80 +197,101 @@ __global__ void k_hull(StarArgs a) {
         s_v[c] = i >= 0 ? a.sv[sb + i] : 0;
     }
     __syncthreads();
-    if (threadIdx.x != 0) return;
-    const star::Grid g = make_grid(a, f);
-    const long long ncand = 2ll * a.W + 2ll * a.H + 8;  // column extremes + two whole columns
-    int4* lo = reinterpret_cast<int4*>(a.hull_tmp) + 2 * ncand * f;
-    int4* hi = lo + ncand;
-    int c0 = -1, c1 = -1;
-    for (int i = 0; i < a.W; ++i)
-        if (s_idx[i] >= 0) {
-            if (c0 < 0) c0 = i;
-            c1 = i;
-        }
+    const long long ncand = hull_stack_entries(a.W, a.H);  // column extremes + two whole columns
+    int2* stk = stacks_in_smem ? reinterpret_cast<int2*>(sm + 4 * a.W)
+                               : reinterpret_cast<int2*>(a.hull_tmp) + 2 * ncand * f;
+    int2* lo = stk;  // entries ((v << 16) | u, index)
+    int2* hi = stk + ncand;
     int* hnext = a.hull + 2 * sb;
     int* hprev = hnext + a.scap;
     int* flat = a.flags + (long long)f * a.flag_ints + 4;
-    if (c0 < 0) {
+    if (threadIdx.x < 2) {
+        const star::Grid g = make_grid(a, f);
+        const bool upper = threadIdx.x == 1;
+        int2* st = upper ? hi : lo;
+        int c0 = -1, c1 = -1;
+        for (int i = 0; i < a.W; ++i)
+            if (s_idx[i] >= 0) {
+                if (c0 < 0) c0 = i;
+                c1 = i;
+            }
+        if (!upper) s_c[0] = c0;
+        int n = 0;
+        if (c0 >= 0) {
+            auto cross = [](int2 o, int2 b, int x, int y) {
+                const int ox = o.x & 0xffff, oy = o.x >> 16, bx = b.x & 0xffff, by = b.x >> 16;
+                return (long long)(bx - ox) * (y - oy) - (long long)(by - oy) * (x - ox);
+            };
+            // lower chain: pop on a right turn; upper: on a left turn
+            auto push = [&](int x, int y, int idx) {
+                if (upper) {
+                    while (n >= 2 && cross(st[n - 2], st[n - 1], x, y) > 0) --n;
+                } else {
+                    while (n >= 2 && cross(st[n - 2], st[n - 1], x, y) < 0) --n;
+                }
+                st[n++] = make_int2((y << 16) | x, idx);
+            };
+            auto whole_column = [&](int x) {  // every point of column x by v (star_dt.cuh)
+                const int cx = x / g.gs;
+                for (int cy = 0; cy < g.gh; ++cy) {
+                    const int c = cy * g.gw + cx;
+                    int last = -2147483647;
+                    for (;;) {
+                        int best = -1, bv = 0;
+                        for (int k = g.cell_start[c]; k < g.cell_start[c + 1]; ++k) {
+                            const int s2 = g.cell_items[k];
+                            if (g.u[s2] != x || g.dup[s2]) continue;
+                            const int vs = g.v[s2];
+                            if (vs <= last) continue;
+                            if (best < 0 || vs < bv) {
+                                best = s2;
+                                bv = vs;
+                            }
+                        }
+                        if (best < 0) break;
+                        push(x, bv, best);
+                        last = bv;
+                    }
+                }
+            };
+            whole_column(c0);
+            for (int i = c0 + 1; i < c1; ++i) {
+                const int pa = s_idx[i], pb = s_idx[a.W + i];
+                if (pa < 0) continue;
+                push(i, s_v[i], pa);
+                if (pb != pa) push(i, s_v[a.W + i], pb);
+            }
+            if (c1 != c0) whole_column(c1);
+        }
+        s_n[threadIdx.x] = n;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    if (s_c[0] < 0) {
         *flat = 1;
         return;
     }
-    int nl = 0, nh = 0;
-    auto cross = [](int4 o, int4 b, int x, int y) {
-        return (long long)(b.x - o.x) * (y - o.y) - (long long)(b.y - o.y) * (x - o.x);
+    const int nl = s_n[0], nh = s_n[1];
+    auto cross = [](int2 o, int2 b, int2 c) {
+        const int ox = o.x & 0xffff, oy = o.x >> 16, bx = b.x & 0xffff, by = b.x >> 16;
+        const int x = c.x & 0xffff, y = c.x >> 16;
+        return (long long)(bx - ox) * (y - oy) - (long long)(by - oy) * (x - ox);
     };
-    auto push = [&](int x, int y, int idx) {
-        while (nl >= 2 && cross(lo[nl - 2], lo[nl - 1], x, y) < 0) --nl;
-        lo[nl++] = make_int4(x, y, idx, 0);
-        while (nh >= 2 && cross(hi[nh - 2], hi[nh - 1], x, y) > 0) --nh;
-        hi[nh++] = make_int4(x, y, idx, 0);
-    };
-    auto whole_column = [&](int x) {  // every point of column x by v (star_dt.cuh)
-        const int cx = x / g.gs;
-        for (int cy = 0; cy < g.gh; ++cy) {
-            const int c = cy * g.gw + cx;
-            int last = -2147483647;
-            for (;;) {
-                int best = -1, bv = 0;
-                for (int k = g.cell_start[c]; k < g.cell_start[c + 1]; ++k) {
-                    const int s = g.cell_items[k];
-                    if (g.u[s] != x || g.dup[s]) continue;
-                    const int vs = g.v[s];
-                    if (vs <= last) continue;
-                    if (best < 0 || vs < bv) {
-                        best = s;
-                        bv = vs;
-                    }
-                }
-                if (best < 0) break;
-                push(x, bv, best);
-                last = bv;
-            }
-        }
-    };
-    whole_column(c0);
-    for (int i = c0 + 1; i < c1; ++i) {
-        const int pa = s_idx[i], pb = s_idx[a.W + i];
-        if (pa < 0) continue;
-        push(i, s_v[i], pa);
-        if (pb != pa) push(i, s_v[a.W + i], pb);
-    }
-    if (c1 != c0) whole_column(c1);
     bool is_flat = nl < 2;
     if (!is_flat) {
         is_flat = true;
-        for (int i = 1; i + 1 < nh && is_flat; ++i) is_flat = cross(hi[0], hi[nh - 1], hi[i].x, hi[i].y) == 0;
-        for (int i = 1; i + 1 < nl && is_flat; ++i) is_flat = cross(lo[0], lo[nl - 1], lo[i].x, lo[i].y) == 0;
+        for (int i = 1; i + 1 < nh && is_flat; ++i) is_flat = cross(hi[0], hi[nh - 1], hi[i]) == 0;
+        for (int i = 1; i + 1 < nl && is_flat; ++i) is_flat = cross(lo[0], lo[nl - 1], lo[i]) == 0;
     }
     *flat = is_flat ? 1 : 0;
     if (is_flat) return;
     for (int i = 0; i + 1 < nl; ++i) {
-        hnext[lo[i].z] = lo[i + 1].z;
-        hprev[lo[i + 1].z] = lo[i].z;
+        hnext[lo[i].y] = lo[i + 1].y;
+        hprev[lo[i + 1].y] = lo[i].y;
     }
     for (int i = nh - 1; i > 0; --i) {
-        hnext[hi[i].z] = hi[i - 1].z;
-        hprev[hi[i - 1].z] = hi[i].z;
+        hnext[hi[i].y] = hi[i - 1].y;
+        hprev[hi[i - 1].y] = hi[i].y;
     }
 }
 
@@ -320,7 +348,11 @@ __device__ unsigned long long g_star_cycles, g_star_max, g_star_n, g_star_hist[2
 // pass 2: [0] points [1] gather cycles [2] local steps [3] local cycles [4] row searches
 // [5] row cycles [6] rows visited [7] column searches [8] column cycles [9] nearest cycles [10] total cycles
 __device__ unsigned long long g_far[12];
-#define FAR_ADD(i, v) do { if ((threadIdx.x & 31) == 0) atomicAdd(&g_far[i], (unsigned long long)(v)); } while (0)
+__device__ unsigned long long g_far_pt[1 << 16][12];  // per warp slot: this point's counters
+__device__ __forceinline__ int far_slot() {
+    return int(((blockIdx.y * gridDim.x + blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5)) & 0xffff);
+}
+#define FAR_ADD(i, v) do { if ((threadIdx.x & 31) == 0) { atomicAdd(&g_far[i], (unsigned long long)(v)); g_far_pt[far_slot()][i] += (unsigned long long)(v); } } while (0)
 #define FAR_CLOCK() clock64()
 __global__ void k_star_report() {
     printf("k_star_far: %llu points, gather %llu cyc, local %llu steps %llu cyc, rows %llu searches %llu cyc %llu rows, cols %llu %llu cyc, nearest %llu cyc, total %llu cyc\n",
@@ -611,6 +643,7 @@ constexpr int kFarCap = 256;    // gathered points per warp
 constexpr int kFarTris = 640;   // triangles of one star (more: the frame is replayed on the host)
 
 struct WLocal {
+    const unsigned long long* ckey;  // the frame's column-extreme keys (k_col_key): lo [0, W), hi [W, 2W)
     int n;
     bool complete;
     star::Box box;
@@ -770,6 +803,11 @@ __device__ __noinline__ int w_rows(const star::Grid& g, int p, int q, int side, 
         const int cy = pcy + t;
         int lbest = best;
         star::Pencil lk = bk;
+        // this lane's row: the item range of its cells over the chord (one
+        // contiguous range: a row's cells are consecutive in cell_items);
+        // the skip box's cells are filtered per point below
+        int i0 = 0, cnt = 0;
+        bool in_rows = false;
         const double ya = g.miny + double(cy) * g.gs, yb = ya + g.gs - 1;
         if (cy >= 0 && cy < g.gh && yb >= reg.y0 && ya <= reg.y1) {
             const double dy = d.cy < ya ? ya - d.cy : (d.cy > yb ? d.cy - yb : 0.0);
@@ -778,22 +816,41 @@ __device__ __noinline__ int w_rows(const star::Grid& g, int p, int q, int side, 
                 int x0 = star::cell_x(g, d.cx - half > reg.x0 ? d.cx - half : reg.x0);
                 int x1 = star::cell_x(g, d.cx + half < reg.x1 ? d.cx + half : reg.x1);
                 if (star::clip_side(g, p, q, side, ya, yb, x0, x1)) {
-                    const bool in_rows = cy >= skip.y0 && cy <= skip.y1;
-                    star::row_runs(g, cy, x0, x1, in_rows ? skip.x0 : 1, in_rows ? skip.x1 : 0, 1, 0,
-                                   [&](int i0, int i1) {
-                                       for (int i = i0; i < i1; ++i) {
-                                           const int s = g.cell_items[i];
-                                           if (s == p || s == q || g.dup[s]) continue;
-                                           const star::Pencil ps = key(s);
-                                           if (side > 0 ? ps.den <= 0 : ps.den >= 0) continue;
-                                           const int c = star::pencil_cmp(ps, lk, side);
-                                           if (c < 0 || (c == 0 && !w_better(g, p, q, side, lbest, s))) continue;
-                                           lbest = s;
-                                           lk = ps;
-                                       }
-                                   });
+                    in_rows = cy >= skip.y0 && cy <= skip.y1 && skip.x0 <= skip.x1;
+                    i0 = g.cell_start[cy * g.gw + x0];
+                    cnt = g.cell_start[cy * g.gw + x1 + 1] - i0;
                 }
             }
+        }
+        // the batch's points over the whole warp (a wide, flat region -- the
+        // thin segment along a hull edge -- is one long row: one lane per
+        // row would walk it alone)
+        const int incl = w_scan(cnt);
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        for (int base = 0; base < total; base += 32) {
+            const int k = base + lane;
+            int owner = 0;  // the lane whose range holds item k: #lanes with incl <= k
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const int v = __shfl_sync(0xffffffffu, incl, owner + step - 1);
+                if (v <= k) owner += step;
+            }
+            const int oi0 = __shfl_sync(0xffffffffu, i0, owner & 31);
+            const int oex = __shfl_sync(0xffffffffu, incl - cnt, owner & 31);
+            const bool orows = __shfl_sync(0xffffffffu, in_rows, owner & 31);
+            if (k >= total) continue;
+            const int s = g.cell_items[oi0 + (k - oex)];
+            if (s == p || s == q || g.dup[s]) continue;
+            if (orows) {
+                const int cx = (g.u[s] - g.minx) / g.gs;  // the cell k_grid_fill put it in
+                if (cx >= skip.x0 && cx <= skip.x1) continue;
+            }
+            const star::Pencil ps = key(s);
+            if (side > 0 ? ps.den <= 0 : ps.den >= 0) continue;
+            const int c = star::pencil_cmp(ps, lk, side);
+            if (c < 0 || (c == 0 && !w_better(g, p, q, side, lbest, s))) continue;
+            lbest = s;
+            lk = ps;
         }
         FAR_ADD(6, 1);
         if (__any_sync(0xffffffffu, lbest != best)) {
@@ -816,7 +873,8 @@ __device__ __noinline__ int w_rows(const star::Grid& g, int p, int q, int side, 
 
 // No candidate in the gathered box on the search side: a first one from the
 // column extremes (nearest columns first), then w_rows.  -2 if none exists.
-__device__ int w_next_far(const star::Grid& g, int p, int q, int side, const star::Box& skip) {
+__device__ int w_next_far(const star::Grid& g, const unsigned long long* ckey, int p, int q, int side,
+                           const star::Box& skip) {
     const int lane = threadIdx.x & 31;
     {  // the 5x5 cells around q: in a fan along the hull the next neighbour is next to q
         const int qcx = star::cell_x(g, g.u[q]), qcy = star::cell_y(g, g.v[q]);
@@ -836,26 +894,51 @@ __device__ int w_next_far(const star::Grid& g, int p, int q, int side, const sta
         const unsigned m = __ballot_sync(0xffffffffu, found >= 0);
         if (m) return w_rows(g, p, q, side, __shfl_sync(0xffffffffu, found, __ffs(m) - 1), skip);
     }
+    // Column extremes nearest first: lanes 0..15 take columns c0 - k, lanes
+    // 16..31 c0 + k, four rounds of 16 per side per pass with all their
+    // (v, index) keys loaded up front (one memory round trip per 64 columns
+    // a side; the keys hold the row, so no dependent coordinate loads).  The
+    // seed is the first hit in round order, then lane order, low extreme
+    // first -- the same seed as a one-round-at-a-time scan.
     const int cols = g.maxx - g.minx + 1, c0 = g.u[p] - g.minx;
-    for (int base = 0; base < cols; base += 16) {
-        // lanes 0..15 columns c0 - base - k, lanes 16..31 c0 + base + k
-        const int k = base + (lane & 15);
-        const int i = lane < 16 ? c0 - k : c0 + k;
-        int found = -1;
-        if (i >= 0 && i < cols) {
-            for (int e = 0; e < 2 && found < 0; ++e) {
-                const int s = e == 0 ? g.col_lo[i] : g.col_hi[i];
-                if (s < 0 || s == p || s == q) continue;
-                const long long o = star::orient(g, p, q, s);
-                if (side > 0 ? o > 0 : o < 0) found = s;
+    const int pu = g.u[p], pv = g.v[p];
+    const long long qx = g.u[q] - pu, qy = g.v[q] - pv;
+    for (int base = 0; base < cols; base += 64) {
+        unsigned long long kk[4][2];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int k = base + 16 * r + (lane & 15);
+            const int i = lane < 16 ? c0 - k : c0 + k;
+            const bool in = i >= 0 && i < cols;
+            kk[r][0] = in ? ckey[i] : ~0ull;
+            kk[r][1] = in ? ckey[cols + i] : ~0ull;
+        }
+        int found = -1, fr = 4;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int k = base + 16 * r + (lane & 15);
+            const int i = lane < 16 ? c0 - k : c0 + k;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const unsigned long long key = kk[r][e];
+                if (found >= 0 || key == ~0ull) continue;
+                const int s = int(key & 0xffffffffu);
+                if (s == p || s == q) continue;
+                const int sv = e == 0 ? g.miny + int(key >> 32) : g.maxy - int(key >> 32);
+                const long long o = qx * (sv - pv) - qy * (g.minx + i - pu);
+                if (side > 0 ? o > 0 : o < 0) {
+                    found = s;
+                    fr = r;
+                }
             }
         }
-        const unsigned m = __ballot_sync(0xffffffffu, found >= 0);
-        if (m) {
+        const int mr = __reduce_min_sync(0xffffffffu, fr);
+        if (mr < 4) {
+            const unsigned m = __ballot_sync(0xffffffffu, fr == mr);
             const int first = __shfl_sync(0xffffffffu, found, __ffs(m) - 1);
             return w_rows(g, p, q, side, first, star::Box{1, 1, 0, 0});
         }
-        if (base >= c0 && base >= cols - c0) break;
+        if (base + 48 >= c0 && base + 48 >= cols - c0) break;
     }
     return -2;
 }
@@ -934,7 +1017,7 @@ __device__ __noinline__ int w_step(const star::Grid& g, const WLocal& L, int p, 
         FAR_ADD(5, FAR_CLOCK() - t0);
         return x;
     }
-    const int x = w_next_far(g, p, q, side, L.complete ? L.box : star::Box{1, 1, 0, 0});
+    const int x = w_next_far(g, L.ckey, p, q, side, L.complete ? L.box : star::Box{1, 1, 0, 0});
     FAR_ADD(7, 1);
     FAR_ADD(8, FAR_CLOCK() - t0);
     return x;
@@ -987,12 +1070,17 @@ __global__ void __launch_bounds__(kFarT) k_star_far(StarArgs a) {
     const long long sb = (long long)f * a.scap;
     int* tris = a.tris + 3 * (long long)f * a.pitch;
     WLocal L;
+    L.ckey = a.col_key + 2ll * f * a.W;
     L.idx = s_idx[wid];
     L.dxy = s_dxy[wid];
     int* tb = s_tri[wid];
     for (int h = blockIdx.x * (kFarT >> 5) + wid; h < n; h += warps) {
         const int p = a.hard[sb + h];
         __syncwarp();
+#ifdef PS_STAR_PROFILE
+        if (lane == 0)
+            for (int i = 0; i < 12; ++i) g_far_pt[far_slot()][i] = 0;
+#endif
         const long long tg = FAR_CLOCK();
         w_gather(g, p, L);
         FAR_ADD(0, 1);
@@ -1000,6 +1088,24 @@ __global__ void __launch_bounds__(kFarT) k_star_far(StarArgs a) {
         bool closed;
         const int nt = w_walk(g, L, p, closed, tb);
         FAR_ADD(10, FAR_CLOCK() - tg);
+#ifdef PS_STAR_PROFILE
+        {
+            const long long cyc = FAR_CLOCK() - tg;
+            if (lane == 0) {
+                atomicMax(&g_star_max, ((unsigned long long)cyc << 24) | (unsigned long long)(p & 0xffffff));
+                int b = 0;
+                while (b < 23 && (1ll << (b + 1)) <= cyc) ++b;
+                atomicAdd(&g_star_hist[b], 1ull);
+                if (cyc > 2000000 && atomicAdd(&g_far[11], 1ull) < 40) {
+                    const unsigned long long* c = g_far_pt[far_slot()];
+                    printf("slow far point f %d p %d (%d,%d) cycles %lld nt %d closed %d gathered %d complete %d hull %d/%d | "
+                           "local %llu/%llu cyc rows %llu/%llu cyc (%llu rows) cols %llu/%llu cyc nearest %llu\n",
+                           f, p, g.u[p], g.v[p], cyc, nt, int(closed), L.n, int(L.complete), g.hnext[p], g.hprev[p],
+                           c[2], c[3], c[4], c[5], c[6], c[7], c[8], c[9]);
+                }
+            }
+        }
+#endif
         if (nt < 0) {  // a failed search, or more than kFarTris triangles
             if (lane == 0) set_fail(a, f, nt == -4 ? 4 : 2);
             continue;
@@ -1139,9 +1245,11 @@ int launch_star_mesh(const StarArgs& a, int max_points, cudaStream_t st) {
     k_col_key<<<grid, 256, 0, st>>>(a); STAR_CHECK("k_col_key");
     k_col_decode<<<dim3((2 * a.W + 255) / 256, a.frames), 256, 0, st>>>(a);
     {
-        const int hsm = 4 * a.W * int(sizeof(int));
+        // the chains' stacks in shared memory up to 160 KB (VGA: 46 KB)
+        const bool stacks = hull_smem_bytes(a.W, a.H, true) <= 160 * 1024;
+        const int hsm = int(hull_smem_bytes(a.W, a.H, stacks));
         cudaFuncSetAttribute(k_hull, cudaFuncAttributeMaxDynamicSharedMemorySize, hsm);
-        k_hull<<<a.frames, 256, hsm, st>>>(a);
+        k_hull<<<a.frames, 256, hsm, st>>>(a, stacks ? 1 : 0);
     } STAR_CHECK("k_hull");
     {
         const int tiles = ((a.gw + star::kTileCells - 1) / star::kTileCells) * ((a.gh + star::kTileCells - 1) / star::kTileCells);
