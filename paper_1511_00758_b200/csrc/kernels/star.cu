@@ -178,44 +178,114 @@ __global__ void k_col_decode(StarArgs a) {
 // lower monotone chain and thread 1 the upper one, each over (u, v, index)
 // stack entries in shared memory when they fit (no dependent global loads
 // per step); flags[4] = 1 for a collinear set.
+__device__ __forceinline__ int w_scan(int x) {  // inclusive prefix sum over the warp
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    return x;
+}
+
 __host__ __device__ inline int hull_stack_entries(int W, int H) { return 2 * W + 2 * H + 8; }
 inline size_t hull_smem_bytes(int W, int H, bool stacks) {
-    return size_t(4) * W * sizeof(int) + (stacks ? size_t(2) * hull_stack_entries(W, H) * sizeof(int2) : 0) + 16;
+    return size_t(4) * W * sizeof(int) + size_t(2) * H * sizeof(int2) +
+           (stacks ? size_t(2) * hull_stack_entries(W, H) * sizeof(int2) : 0) + 16;
 }
 
 __global__ void k_hull(StarArgs a, int stacks_in_smem) {
     const int f = blockIdx.x;
     extern __shared__ int sm[];
-    int* s_idx = sm;             // 2W: col_lo then col_hi
-    int* s_v = sm + 2 * a.W;     // their rows
-    __shared__ int s_n[2], s_c[2];
+    int* s_idx = sm;                                        // 2W: col_lo then col_hi
+    int* s_v = sm + 2 * a.W;                                // their rows
+    int2* s_col = reinterpret_cast<int2*>(sm + 4 * a.W);    // 2H: the first / last column's points (v, index)
+    __shared__ int s_n[2], s_c[2], s_cnt[2];
     const long long sb = (long long)f * a.scap;
     const int* cols = a.col_idx + 2ll * f * a.W;
+    if (threadIdx.x == 0) {
+        s_c[0] = 0x7fffffff;
+        s_c[1] = -1;
+        s_cnt[0] = s_cnt[1] = 0;
+    }
+    __syncthreads();
+    int lo_c = 0x7fffffff, hi_c = -1;
     for (int c = threadIdx.x; c < 2 * a.W; c += blockDim.x) {
         const int i = cols[c];
         s_idx[c] = i;
         s_v[c] = i >= 0 ? a.sv[sb + i] : 0;
+        if (c < a.W && i >= 0) {
+            lo_c = min(lo_c, c);
+            hi_c = max(hi_c, c);
+        }
     }
+    atomicMin(&s_c[0], lo_c);
+    atomicMax(&s_c[1], hi_c);
     __syncthreads();
+    const int c0 = s_c[0] == 0x7fffffff ? -1 : s_c[0], c1 = s_c[1];
+    const star::Grid g = make_grid(a, f);
+    // every point of the first and last columns, by v (star_dt.cuh build_hull):
+    // a thread per cell of the column collects its points, sorted within the
+    // cell (a column's cells are in v order), then a scan places the cells
+    if (c0 >= 0) {
+        for (int e = 0; e < (c1 != c0 ? 2 : 1); ++e) {
+            const int x = e == 0 ? c0 : c1, cx = x / g.gs;
+            // pass 1: counts; pass 2: positions (cells in order, block-strided)
+            for (int base = 0; base < g.gh; base += blockDim.x) {
+                const int cy = base + threadIdx.x;
+                int n = 0;
+                int start = 0, stop = 0;
+                if (cy < g.gh) {
+                    start = g.cell_start[cy * g.gw + cx];
+                    stop = g.cell_start[cy * g.gw + cx + 1];
+                    for (int k = start; k < stop; ++k) {
+                        const int s2 = g.cell_items[k];
+                        n += g.u[s2] == x && !g.dup[s2];
+                    }
+                }
+                // block-wide exclusive scan of n (in cell order)
+                __shared__ int s_warp[32];
+                const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+                int incl = w_scan(n);
+                if (lane == 31) s_warp[w] = incl;
+                __syncthreads();
+                if (w == 0) {
+                    int t = lane < int(blockDim.x >> 5) ? s_warp[lane] : 0;
+                    t = w_scan(t);
+                    s_warp[lane] = t;
+                }
+                __syncthreads();
+                const int off = s_cnt[e] + (w > 0 ? s_warp[w - 1] : 0) + incl - n;
+                int2* out = s_col + e * a.H + off;
+                int m = 0;
+                for (int k = start; k < stop; ++k) {
+                    const int s2 = g.cell_items[k];
+                    if (g.u[s2] != x || g.dup[s2]) continue;
+                    // insertion by v
+                    const int vs = g.v[s2];
+                    int j = m++;
+                    while (j > 0 && out[j - 1].x > vs) {
+                        out[j] = out[j - 1];
+                        --j;
+                    }
+                    out[j] = make_int2(vs, s2);
+                }
+                __syncthreads();
+                if (threadIdx.x == 0) s_cnt[e] += s_warp[(blockDim.x >> 5) - 1];
+                __syncthreads();
+            }
+        }
+    }
     const long long ncand = hull_stack_entries(a.W, a.H);  // column extremes + two whole columns
-    int2* stk = stacks_in_smem ? reinterpret_cast<int2*>(sm + 4 * a.W)
-                               : reinterpret_cast<int2*>(a.hull_tmp) + 2 * ncand * f;
+    int2* stk = stacks_in_smem ? s_col + 2 * a.H : reinterpret_cast<int2*>(a.hull_tmp) + 2 * ncand * f;
     int2* lo = stk;  // entries ((v << 16) | u, index)
     int2* hi = stk + ncand;
     int* hnext = a.hull + 2 * sb;
     int* hprev = hnext + a.scap;
     int* flat = a.flags + (long long)f * a.flag_ints + 4;
     if (threadIdx.x < 2) {
-        const star::Grid g = make_grid(a, f);
         const bool upper = threadIdx.x == 1;
         int2* st = upper ? hi : lo;
-        int c0 = -1, c1 = -1;
-        for (int i = 0; i < a.W; ++i)
-            if (s_idx[i] >= 0) {
-                if (c0 < 0) c0 = i;
-                c1 = i;
-            }
-        if (!upper) s_c[0] = c0;
         int n = 0;
         if (c0 >= 0) {
             auto cross = [](int2 o, int2 b, int x, int y) {
@@ -231,43 +301,21 @@ __global__ void k_hull(StarArgs a, int stacks_in_smem) {
                 }
                 st[n++] = make_int2((y << 16) | x, idx);
             };
-            auto whole_column = [&](int x) {  // every point of column x by v (star_dt.cuh)
-                const int cx = x / g.gs;
-                for (int cy = 0; cy < g.gh; ++cy) {
-                    const int c = cy * g.gw + cx;
-                    int last = -2147483647;
-                    for (;;) {
-                        int best = -1, bv = 0;
-                        for (int k = g.cell_start[c]; k < g.cell_start[c + 1]; ++k) {
-                            const int s2 = g.cell_items[k];
-                            if (g.u[s2] != x || g.dup[s2]) continue;
-                            const int vs = g.v[s2];
-                            if (vs <= last) continue;
-                            if (best < 0 || vs < bv) {
-                                best = s2;
-                                bv = vs;
-                            }
-                        }
-                        if (best < 0) break;
-                        push(x, bv, best);
-                        last = bv;
-                    }
-                }
-            };
-            whole_column(c0);
+            for (int k = 0; k < s_cnt[0]; ++k) push(c0, s_col[k].x, s_col[k].y);
             for (int i = c0 + 1; i < c1; ++i) {
                 const int pa = s_idx[i], pb = s_idx[a.W + i];
                 if (pa < 0) continue;
                 push(i, s_v[i], pa);
                 if (pb != pa) push(i, s_v[a.W + i], pb);
             }
-            if (c1 != c0) whole_column(c1);
+            if (c1 != c0)
+                for (int k = 0; k < s_cnt[1]; ++k) push(c1, s_col[a.H + k].x, s_col[a.H + k].y);
         }
         s_n[threadIdx.x] = n;
     }
     __syncthreads();
     if (threadIdx.x != 0) return;
-    if (s_c[0] < 0) {
+    if (c0 < 0) {
         *flat = 1;
         return;
     }
@@ -440,15 +488,6 @@ __device__ void hull_outcome(const StarArgs& a, int f, int p, const HullCheck& h
     write_fan(w + 2);
 }
 
-__device__ __forceinline__ int w_scan(int x) {  // inclusive prefix sum over the warp
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    return x;
-}
 
 constexpr int kStarTris = 16;  // triangles of one star a pass-1 thread may hold
 constexpr int kTileT = 128;
