@@ -37,44 +37,53 @@ void SweepOrder::init(const int* px, const int* py, int m) {
     // Andrew's monotone chains (collinear points kept, as the sweep's strict
     // visibility keeps them on the hull): lower pops on a right turn, upper
     // on a left turn.
-    belowL_.assign(m, -1);
-    belowU_.assign(m, -1);
-    popL_.assign(m, INT_MAX);
-    popU_.assign(m, INT_MAX);
-    std::vector<int> st;
-    st.reserve(m);
+    // Both chains in one pass over the points (they are independent), raw
+    // stacks; every entry of below*/pop* is written exactly once.
+    belowL_.resize(m);
+    belowU_.resize(m);
+    popL_.resize(m);
+    popU_.resize(m);
+    stk_.resize(2 * size_t(m));
+    int* sL = stk_.data();
+    int* sU = sL + m;
+    int nL = 0, nU = 0;
+    const int* X = px;
+    const int* Y = py;
+    auto ori = [X, Y](int a, int b, int c) {
+        return ((long long)X[b] - X[a]) * ((long long)Y[c] - Y[a]) - ((long long)Y[b] - Y[a]) * ((long long)X[c] - X[a]);
+    };
     for (int r = 0; r < m; ++r) {
-        while (st.size() >= 2 && orient(st[st.size() - 2], st.back(), r) < 0) {
-            popL_[st.back()] = r;
-            st.pop_back();
-        }
-        belowL_[r] = st.empty() ? -1 : st.back();
-        st.push_back(r);
-    }
-    st.clear();
-    for (int r = 0; r < m; ++r) {
-        while (st.size() >= 2 && orient(st[st.size() - 2], st.back(), r) > 0) {
-            popU_[st.back()] = r;
-            st.pop_back();
-        }
-        belowU_[r] = st.empty() ? -1 : st.back();
-        st.push_back(r);
+        popL_[r] = popU_[r] = INT_MAX;
+        while (nL >= 2 && ori(sL[nL - 2], sL[nL - 1], r) < 0) popL_[sL[--nL]] = r;
+        belowL_[r] = nL ? sL[nL - 1] : -1;
+        sL[nL++] = r;
+        while (nU >= 2 && ori(sU[nU - 2], sU[nU - 1], r) > 0) popU_[sU[--nU]] = r;
+        belowU_[r] = nU ? sU[nU - 1] : -1;
+        sU[nU++] = r;
     }
 
-    // bucket grid: ranks are increasing within a bucket (filled in rank order)
+    // bucket grid: ranks are increasing within a bucket (filled in rank
+    // order); power-of-two buckets, so the cell of a point is two shifts
     const int span = std::max(maxx_ - minx_, maxy_ - miny_) + 1;
     bs_ = 16;
-    while (bs_ < span / 512) bs_ *= 2;
+    int sh = 4;
+    while (bs_ < span / 512) {
+        bs_ *= 2;
+        ++sh;
+    }
     bw_ = (maxx_ - minx_) / bs_ + 1;
     bh_ = (maxy_ - miny_) / bs_ + 1;
     bstart_.assign(size_t(bw_) * bh_ + 1, 0);
-    for (int r = 0; r < m; ++r)
-        ++bstart_[size_t((py[r] - miny_) / bs_) * bw_ + (px[r] - minx_) / bs_ + 1];
+    bcell_.resize(m);
+    for (int r = 0; r < m; ++r) {
+        const int c = ((py[r] - miny_) >> sh) * bw_ + ((px[r] - minx_) >> sh);
+        bcell_[r] = c;
+        ++bstart_[size_t(c) + 1];
+    }
     for (size_t i = 1; i < bstart_.size(); ++i) bstart_[i] += bstart_[i - 1];
     bitems_.resize(m);
-    std::vector<int> fill(bstart_.begin(), bstart_.end() - 1);
-    for (int r = 0; r < m; ++r)
-        bitems_[fill[size_t((py[r] - miny_) / bs_) * bw_ + (px[r] - minx_) / bs_]++] = r;
+    bfill_.assign(bstart_.begin(), bstart_.end() - 1);
+    for (int r = 0; r < m; ++r) bitems_[bfill_[bcell_[r]]++] = r;
 }
 
 int SweepOrder::incircle(int a, int b, int c, int d) const {
@@ -332,7 +341,7 @@ namespace ps {
 // The reference sweep (delaunay.cpp:50-284) over the window's points in rank
 // order, recording for every slot the contents it had before each time it
 // was eaten (a Lawson flip on the side not holding the new point).
-bool SweepOrder::replay(int u0, int u1, int v0, int v1, Scratch& S) const {
+bool SweepOrder::replay(int u0, int u1, int v0, int v1, int last, Scratch& S) const {
     S.rrank_.clear();
     const int bx0 = std::max(0, (u0 - minx_) / bs_), bx1 = std::min(bw_ - 1, (u1 - minx_) / bs_);
     const int by0 = std::max(0, (v0 - miny_) / bs_), by1 = std::min(bh_ - 1, (v1 - miny_) / bs_);
@@ -341,6 +350,7 @@ bool SweepOrder::replay(int u0, int u1, int v0, int v1, Scratch& S) const {
             const size_t b = size_t(by) * bw_ + bx;
             for (int i = bstart_[b]; i < bstart_[b + 1]; ++i) {
                 const int r = bitems_[i];
+                if (r > last) break;  // ranks increase within a bucket
                 if (x_[r] >= u0 && x_[r] <= u1 && y_[r] >= v0 && y_[r] <= v1) S.rrank_.push_back(r);
             }
         }
@@ -501,6 +511,12 @@ bool SweepOrder::resolve(const int* tris, int count, uint64_t* birth, int* store
 
 bool SweepOrder::resolve_windows(const int* tris, int count, uint64_t* birth, int* stored, Scratch& S) const {
     int bu0 = INT_MAX, bu1 = INT_MIN, bv0 = INT_MAX, bv1 = INT_MIN;
+    // Only points up to the last vertex of the triangles matter: a final
+    // triangle's slot is not touched after its last vertex is inserted, so
+    // the window's sweep stops there (and its right edge is that column).
+    int last = 0;
+    for (int i = 0; i < 3 * count; ++i) last = std::max(last, tris[i]);
+    const int xcap = x_[last];
     for (int i = 0; i < 3 * count; ++i) {
         bu0 = std::min(bu0, x_[tris[i]]);
         bu1 = std::max(bu1, x_[tris[i]]);
@@ -510,7 +526,7 @@ bool SweepOrder::resolve_windows(const int* tris, int count, uint64_t* birth, in
     const double area = double(maxx_ - minx_ + 1) * double(maxy_ - miny_ + 1);
     int delta = std::max(8, int(2.0 * std::sqrt(area / m_)));
     std::vector<std::pair<uint64_t, int>> key;  // sorted vertex set -> slot
-    int u0 = std::max(minx_, bu0 - delta), u1 = std::min(maxx_, bu1 + delta);
+    int u0 = std::max(minx_, bu0 - delta), u1 = std::min(xcap, bu1 + delta);
     int v0, v1;
     // The sweep's slots are column-tall fans eaten point after point down the
     // column, so a window that cuts the columns is (nearly always) grown to
@@ -521,18 +537,22 @@ bool SweepOrder::resolve_windows(const int* tris, int count, uint64_t* birth, in
     v0 = miny_;
     v1 = maxy_;
     for (int attempt = 0;; ++attempt) {
-        const bool whole = u0 == minx_ && u1 == maxx_ && v0 == miny_ && v1 == maxy_;
+        // the window holds every point up to `last`: nothing to certify
+        const bool whole = u0 <= minx_ && u1 >= xcap && v0 <= miny_ && v1 >= maxy_;
         // growth for the next attempt: towards the points that broke a
         // certificate, or uniformly when the window itself was too small
         int nu0 = u0, nu1 = u1, nv0 = v0, nv1 = v1;
         bool grow_all = false;
         bool gl = false, gr = false, gd = false, gu = false;  // directional growth requests
         const bool fallback = attempt >= 8;  // then finish chains in the full set instead
-        const bool replayed = replay(u0, u1, v0, v1, S);
+        const bool replayed = replay(u0, u1, v0, v1, last, S);
         bool ok = replayed;
         if (!replayed) grow_all = true;
         const int n = int(S.rrank_.size());
-        if (replayed) {
+        // the query triangles' slots: a linear scan for a few triangles, a
+        // sorted key table for many
+        const bool table = count > 8;
+        if (replayed && table) {
             key.clear();
             for (size_t s = 0; s < S.rs_.size(); ++s) {
                 int a = S.rrank_[S.rs_[s].v[0]], b = S.rrank_[S.rs_[s].v[1]], c = S.rrank_[S.rs_[s].v[2]];
@@ -548,16 +568,33 @@ bool SweepOrder::resolve_windows(const int* tris, int count, uint64_t* birth, in
             if (a > b) std::swap(a, b);
             if (b > c) std::swap(b, c);
             if (a > b) std::swap(a, b);
-            const uint64_t kq = (uint64_t(uint32_t(a)) << 42) ^ (uint64_t(uint32_t(b)) << 21) ^ uint64_t(uint32_t(c));
-            auto it = std::lower_bound(key.begin(), key.end(), std::make_pair(kq, -1));
             int slot = -1;
-            for (; it != key.end() && it->first == kq; ++it) {
-                const Scratch::Slot& SL = S.rs_[it->second];
-                int sa = S.rrank_[SL.v[0]], sb = S.rrank_[SL.v[1]], sc = S.rrank_[SL.v[2]];
-                if (sa > sb) std::swap(sa, sb);
-                if (sb > sc) std::swap(sb, sc);
-                if (sa > sb) std::swap(sa, sb);
-                if (sa == a && sb == b && sc == c) slot = it->second;
+            if (table) {
+                const uint64_t kq = (uint64_t(uint32_t(a)) << 42) ^ (uint64_t(uint32_t(b)) << 21) ^ uint64_t(uint32_t(c));
+                auto it = std::lower_bound(key.begin(), key.end(), std::make_pair(kq, -1));
+                for (; it != key.end() && it->first == kq; ++it) {
+                    const Scratch::Slot& SL = S.rs_[it->second];
+                    int sa = S.rrank_[SL.v[0]], sb = S.rrank_[SL.v[1]], sc = S.rrank_[SL.v[2]];
+                    if (sa > sb) std::swap(sa, sb);
+                    if (sb > sc) std::swap(sb, sc);
+                    if (sa > sb) std::swap(sa, sb);
+                    if (sa == a && sb == b && sc == c) slot = it->second;
+                }
+            } else {
+                // window indices of the three ranks (rrank_ is sorted)
+                const auto wi = [&](int r) {
+                    const auto it = std::lower_bound(S.rrank_.begin(), S.rrank_.end(), r);
+                    return it != S.rrank_.end() && *it == r ? int(it - S.rrank_.begin()) : -1;
+                };
+                const int ia = wi(a), ib = wi(b), ic = wi(c);
+                if (ia >= 0 && ib >= 0 && ic >= 0)
+                    for (size_t q = 0; q < S.rs_.size() && slot < 0; ++q) {
+                        const int* v = S.rs_[q].v;
+                        const bool has_a = v[0] == ia || v[1] == ia || v[2] == ia;
+                        const bool has_b = v[0] == ib || v[1] == ib || v[2] == ib;
+                        const bool has_c = v[0] == ic || v[1] == ic || v[2] == ic;
+                        if (has_a && has_b && has_c) slot = int(q);
+                    }
             }
             if (slot < 0) {  // not a triangle of DT(window): the window is too small
                 ok = false;
@@ -630,7 +667,7 @@ bool SweepOrder::resolve_windows(const int* tris, int count, uint64_t* birth, in
             stored[3 * t + 2] = fin[2];
         }
         if (ok) return true;
-        if (whole || n >= m_) return false;
+        if (whole) return false;
         if (!grow_all && (gl || gr || gd || gu)) {
             const int gx = std::max(delta, (u1 - u0 + 1) / 2), gy = std::max(delta, (v1 - v0 + 1) / 2);
             if (gl) nu0 = std::min(nu0, u0 - gx);
@@ -640,7 +677,7 @@ bool SweepOrder::resolve_windows(const int* tris, int count, uint64_t* birth, in
         }
         auto clamp_new = [&] {
             nu0 = std::max(minx_, nu0);
-            nu1 = std::min(maxx_, nu1);
+            nu1 = std::min(xcap, nu1);
             nv0 = std::max(miny_, nv0);
             nv1 = std::min(maxy_, nv1);
         };

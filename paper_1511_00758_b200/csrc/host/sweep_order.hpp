@@ -85,7 +85,7 @@ private:
     // closed circumdisk of the CCW triangle (a, b, c); grows the box to cover
     // the offenders otherwise
     bool disk_clear(int a, int b, int c, int p, int& u0, int& u1, int& v0, int& v1, int grow) const;
-    bool replay(int u0, int u1, int v0, int v1, Scratch& S) const;
+    bool replay(int u0, int u1, int v0, int v1, int last, Scratch& S) const;  // ranks <= last only
     bool resolve_windows(const int* tris, int count, uint64_t* birth, int* stored, Scratch& S) const;  // lex sweep of the window's points, with slot history
 
     const int* x_ = nullptr;
@@ -102,6 +102,7 @@ private:
     // bucket grid of ranks (increasing within a bucket)
     int bs_ = 16, bw_ = 0, bh_ = 0;
     std::vector<int> bstart_, bitems_;
+    std::vector<int> stk_, bcell_, bfill_;  // init scratch
     Scratch& own();
     std::unique_ptr<Scratch> own_;
 };
