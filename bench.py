@@ -96,6 +96,10 @@ def parse_args():
     p.add_argument("--config", type=int, default=2, help="BASELINE.json config index")
     p.add_argument("--frames", type=int, default=0, help="frames per GPU (default: the config's)")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--inflight", type=int, default=2,
+                   help="batches in flight per GPU: that many contexts on the GPU, one host thread "
+                        "each, steps dealt round-robin (double buffering: one batch's host tail and "
+                        "output copies overlap the next batch's device work)")
     p.add_argument("--cpu-sample-frames", type=int, default=128)
     p.add_argument("--ref-all", action="store_true",
                    help="with --configs: also time the reference throughput leg of cfg4 "
@@ -377,41 +381,82 @@ def run_ours(args, rank, world, local_rank):
     H, W = cfgd["height"], cfgd["width"]
     P = W * H
     L, R, keep = make_inputs(ps, cfgd, frames, rank_seed(rank, frames), pinned=True)
-    ctx = ps.Context(local_rank)
-    stream = torch.cuda.ExternalStream(ctx.stream_handle())
+    inflight = max(1, args.inflight)
+    ctxs = [ps.Context(local_rank) for _ in range(inflight)]
+    ctx = ctxs[0]
+    stream = torch.cuda.current_stream()
     lib = ps._native.load()
 
+    def run_steps(fn):
+        """Steps dealt round-robin to the contexts, one host thread each (the
+        C calls release the GIL); returns when every step has finished."""
+        if inflight == 1:
+            for k in range(args.steps):
+                fn(0, k)
+            return
+        errs = []
+
+        def worker(i):
+            try:
+                for k in range(i, args.steps, inflight):
+                    fn(i, k)
+            except Exception as e:  # noqa: BLE001
+                errs.append(e)
+
+        ts = [threading.Thread(target=worker, args=(i,)) for i in range(inflight)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        if errs:
+            raise errs[0]
+
+    def merged_stats():
+        out = {}
+        for c in ctxs:
+            for k, v in c.kernel_stats().items():
+                o = out.setdefault(k, {"launches": 0, "ms": 0.0, "bytes": 0.0})
+                o["launches"] += v["launches"]
+                o["ms"] += v["ms"]
+                o["bytes"] += v.get("bytes", 0.0)
+        return out
+
     # ---------------- value: inputs resident in HBM, full pipeline per step
-    ctx.upload_ptr(frames, L.ctypes.data, R.ctypes.data, W, H)
-    for _ in range(max(3, args.warmup)):
-        st = ctx.run_resident(cfg, unchecked_cell=True)
-        if st not in (0, 7):
-            raise RuntimeError(f"pipeline failed: {lib.ps_last_error(None)}")
+    for c in ctxs:
+        c.upload_ptr(frames, L.ctypes.data, R.ctypes.data, W, H)
+        for _ in range(max(3, args.warmup)):
+            st = c.run_resident(cfg, unchecked_cell=True)
+            if st not in (0, 7):
+                raise RuntimeError(f"pipeline failed: {lib.ps_last_error(None)}")
     sampler = clock_sampler(local_rank)
     barrier()
     torch.cuda.synchronize()
-    l0 = ctx.launch_count()
+    l0 = sum(c.launch_count() for c in ctxs)
     # per-kernel CUDA events, recorded by the engine on the stream each kernel
     # is launched on, live over the timed region (the roofline below)
-    ctx.set_profiling(True)
-    ctx.reset_kernel_stats()
+    for c in ctxs:
+        c.set_profiling(True)
+        c.reset_kernel_stats()
     sampler.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     w0 = time.perf_counter()
-    for _ in range(args.steps):
-        ctx.run_resident(cfg, unchecked_cell=True)
+    run_steps(lambda i, k: ctxs[i].run_resident(cfg, unchecked_cell=True))
+    torch.cuda.synchronize()  # every context's streams (device-wide)
     e1.record(stream)
     torch.cuda.synchronize()
     wall_ms = (time.perf_counter() - w0) * 1e3
     barrier()
     clocks = sampler.stop()
     ms = max_over_ranks(e0.elapsed_time(e1))
-    launches = ctx.launch_count() - l0
-    kstats_timed = ctx.kernel_stats()
+    launches = sum(c.launch_count() for c in ctxs) - l0
+    kstats_timed = merged_stats()
+    for c in ctxs:
+        c.set_profiling(False)
     # Also one extra pass (outside the timed region) with the frame groups
     # serialised on one stream: each kernel's event time is then its isolated
     # launch duration (in the timed pass kernels of different groups overlap).
+    ctx.set_profiling(True)
     ctx.set_max_groups(1)
     ctx.reset_kernel_stats()
     ctx.run_resident(cfg, unchecked_cell=True)
@@ -423,28 +468,33 @@ def run_ours(args, rank, world, local_rank):
     value = whole_job_value(frames, world, args.steps, ms)
 
     # ---------------- e2e: public C-ABI call with host buffers (pinned), copies inside
-    outs = [torch.empty(frames * P * 4, dtype=torch.uint8, pin_memory=True),
-            torch.empty(frames * P, dtype=torch.uint8, pin_memory=True),
-            torch.empty(frames * P * 4, dtype=torch.uint8, pin_memory=True),
-            torch.empty(frames * P * 4, dtype=torch.uint8, pin_memory=True),
-            torch.empty(frames * P, dtype=torch.uint8, pin_memory=True)]
-    trace = (ps._native.PsIterStats * (frames * cfg.iterations))()
+    def out_set():
+        return [torch.empty(frames * P * 4, dtype=torch.uint8, pin_memory=True),
+                torch.empty(frames * P, dtype=torch.uint8, pin_memory=True),
+                torch.empty(frames * P * 4, dtype=torch.uint8, pin_memory=True),
+                torch.empty(frames * P * 4, dtype=torch.uint8, pin_memory=True),
+                torch.empty(frames * P, dtype=torch.uint8, pin_memory=True)]
+
+    outs = [out_set() for _ in ctxs]
+    traces = [(ps._native.PsIterStats * (frames * cfg.iterations))() for _ in ctxs]
+    trace = traces[0]
     cfgc = cfg.to_c()
-    st_arr = np.zeros(frames, np.int32)
+    st_arrs = [np.zeros(frames, np.int32) for _ in ctxs]
 
-    def e2e_call():
-        return lib.ps_run_batch(ctx._h, frames, C.c_void_p(L.ctypes.data), C.c_void_p(R.ctypes.data),
+    def e2e_call(i, k=0):
+        return lib.ps_run_batch(ctxs[i]._h, frames, C.c_void_p(L.ctypes.data), C.c_void_p(R.ctypes.data),
                                 W, H, C.byref(cfgc), ps.PS_RUN_UNCHECKED_CELL,
-                                *[C.c_void_p(o.data_ptr()) for o in outs], trace,
-                                st_arr.ctypes.data_as(C.c_void_p))
+                                *[C.c_void_p(o.data_ptr()) for o in outs[i]], traces[i],
+                                st_arrs[i].ctypes.data_as(C.c_void_p))
 
-    e2e_call()
+    for i in range(inflight):
+        e2e_call(i)
     barrier()
     torch.cuda.synchronize()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record(stream)
-    for _ in range(args.steps):
-        e2e_call()
+    run_steps(e2e_call)
+    torch.cuda.synchronize()
     f1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = max_over_ranks(f0.elapsed_time(f1))
@@ -505,7 +555,12 @@ def run_ours(args, rank, world, local_rank):
                      "traffic": traffic_from_profiles("k_refine")},
         "kernels_isolated_pass": kernels,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "api": "ps_run_batch (C ABI) with pinned host buffers"},
+                "api": "ps_run_batch (C ABI) with pinned host buffers",
+                "inflight": inflight},
+        "inflight": {"batches": inflight,
+                     "how": "one context per in-flight batch on the same GPU, one host thread each, steps "
+                            "dealt round-robin; the timed region runs from before the first step to "
+                            "after the last step of every context (device-wide synchronize)"},
         "clocks": clocks,
         "failed_frames": int((status != 0).sum()),
         "delaunay": {"points_per_pass": points_per_pass,
@@ -545,7 +600,8 @@ def run_ours(args, rank, world, local_rank):
             **host_info()}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    ctx.close()
+    for c in ctxs:
+        c.close()
     if dist is not None:
         dist.destroy_process_group()
     del keep

@@ -176,10 +176,16 @@ Engine::Engine(int device) : device_(device) {
     // instead of all of them finishing together and leaving the host the tail.
     int prio_low = 0, prio_high = 0;
     cudaDeviceGetStreamPriorityRange(&prio_low, &prio_high);
+    // PS_GROUP_PRIO=1: both streams of a group at the group's own priority,
+    // earlier groups first (the device drains group 0, then 1, ...: groups
+    // finish staggered and their output copies overlap later groups' work)
+    const char* gp = std::getenv("PS_GROUP_PRIO");
+    group_prio_ = gp ? std::atoi(gp) != 0 : group_prio_;
     for (int gi = 0; gi < kMaxGroups; ++gi) {
         FrameGroup& g = groups_[gi];
-        const int mesh_prio = std::min(prio_low, prio_high + 1 + gi);  // numerically lower = higher
-        cudaStreamCreateWithPriority(&g.st, cudaStreamNonBlocking, prio_high);
+        const int by_group = std::min(prio_low, prio_high + gi);  // numerically lower = higher
+        const int mesh_prio = group_prio_ ? by_group : std::min(prio_low, prio_high + 1 + gi);
+        cudaStreamCreateWithPriority(&g.st, cudaStreamNonBlocking, group_prio_ ? by_group : prio_high);
         cudaStreamCreateWithPriority(&g.mst, cudaStreamNonBlocking, mesh_prio);
         cudaEventCreateWithFlags(&g.mesh_in, cudaEventDisableTiming);
         cudaEventCreateWithFlags(&g.mesh_out, cudaEventDisableTiming);
