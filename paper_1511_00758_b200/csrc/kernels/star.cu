@@ -191,7 +191,7 @@ __device__ __forceinline__ int w_scan(int x) {  // inclusive prefix sum over the
 __host__ __device__ inline int hull_stack_entries(int W, int H) { return 2 * W + 2 * H + 8; }
 inline size_t hull_smem_bytes(int W, int H, bool stacks) {
     return size_t(4) * W * sizeof(int) + size_t(2) * H * sizeof(int2) +
-           (stacks ? size_t(2) * hull_stack_entries(W, H) * sizeof(int2) : 0) + 16;
+           (stacks ? size_t(3) * hull_stack_entries(W, H) * sizeof(int2) : 0) + 16;
 }
 
 __global__ void k_hull(StarArgs a, int stacks_in_smem) {
@@ -277,41 +277,100 @@ __global__ void k_hull(StarArgs a, int stacks_in_smem) {
         }
     }
     const long long ncand = hull_stack_entries(a.W, a.H);  // column extremes + two whole columns
-    int2* stk = stacks_in_smem ? s_col + 2 * a.H : reinterpret_cast<int2*>(a.hull_tmp) + 2 * ncand * f;
+    int2* stk = stacks_in_smem ? s_col + 2 * a.H : reinterpret_cast<int2*>(a.hull_tmp) + 4 * ncand * f;
     int2* lo = stk;  // entries ((v << 16) | u, index)
     int2* hi = stk + ncand;
+    int2* cand = stk + 2 * ncand;  // the candidates in chain order
     int* hnext = a.hull + 2 * sb;
     int* hprev = hnext + a.scap;
     int* flat = a.flags + (long long)f * a.flag_ints + 4;
-    if (threadIdx.x < 2) {
-        const bool upper = threadIdx.x == 1;
-        int2* st = upper ? hi : lo;
-        int n = 0;
-        if (c0 >= 0) {
-            auto cross = [](int2 o, int2 b, int x, int y) {
-                const int ox = o.x & 0xffff, oy = o.x >> 16, bx = b.x & 0xffff, by = b.x >> 16;
-                return (long long)(bx - ox) * (y - oy) - (long long)(by - oy) * (x - ox);
-            };
-            // lower chain: pop on a right turn; upper: on a left turn
-            auto push = [&](int x, int y, int idx) {
-                if (upper) {
-                    while (n >= 2 && cross(st[n - 2], st[n - 1], x, y) > 0) --n;
-                } else {
-                    while (n >= 2 && cross(st[n - 2], st[n - 1], x, y) < 0) --n;
-                }
-                st[n++] = make_int2((y << 16) | x, idx);
-            };
-            for (int k = 0; k < s_cnt[0]; ++k) push(c0, s_col[k].x, s_col[k].y);
-            for (int i = c0 + 1; i < c1; ++i) {
-                const int pa = s_idx[i], pb = s_idx[a.W + i];
-                if (pa < 0) continue;
-                push(i, s_v[i], pa);
-                if (pb != pa) push(i, s_v[a.W + i], pb);
+    // (1) the candidates in the chains' order: the first column by v, each
+    // middle column's low then high extreme (one if they coincide), the last
+    // column by v; middle columns placed by a block scan of their counts
+    __shared__ int s_base;
+    int n_c = 0;
+    if (c0 >= 0) {
+        const int n0 = s_cnt[0];
+        for (int k = threadIdx.x; k < n0; k += blockDim.x)
+            cand[k] = make_int2((s_col[k].x << 16) | c0, s_col[k].y);
+        if (threadIdx.x == 0) s_base = n0;
+        __syncthreads();
+        __shared__ int s_wsum[32];
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+        for (int base = c0 + 1; base < c1; base += blockDim.x) {
+            const int i = base + threadIdx.x;
+            int pa = -1, pb = -1, cnt = 0;
+            if (i < c1) {
+                pa = s_idx[i];
+                pb = s_idx[a.W + i];
+                cnt = pa < 0 ? 0 : (pb != pa ? 2 : 1);
             }
-            if (c1 != c0)
-                for (int k = 0; k < s_cnt[1]; ++k) push(c1, s_col[a.H + k].x, s_col[a.H + k].y);
+            const int incl = w_scan(cnt);
+            if (lane == 31) s_wsum[w] = incl;
+            __syncthreads();
+            if (w == 0) {
+                int t = lane < nw ? s_wsum[lane] : 0;
+                t = w_scan(t);
+                s_wsum[lane] = t;
+            }
+            __syncthreads();
+            const int at = s_base + (w > 0 ? s_wsum[w - 1] : 0) + incl - cnt;
+            if (cnt >= 1) cand[at] = make_int2((s_v[i] << 16) | i, pa);
+            if (cnt == 2) cand[at + 1] = make_int2((s_v[a.W + i] << 16) | i, pb);
+            __syncthreads();
+            if (threadIdx.x == 0) s_base += s_wsum[nw - 1];
+            __syncthreads();
         }
-        s_n[threadIdx.x] = n;
+        const int n1 = c1 != c0 ? s_cnt[1] : 0;
+        const int b1 = s_base;
+        for (int k = threadIdx.x; k < n1; k += blockDim.x)
+            cand[b1 + k] = make_int2((s_col[a.H + k].x << 16) | c1, s_col[a.H + k].y);
+        n_c = b1 + n1;
+    }
+    __syncthreads();
+    // (2) Andrew's chains, chunk-parallel: warp 0 the lower chain, warp 1 the
+    // upper; each lane runs the chain over its chunk of the candidates (in
+    // place), then lane 0 runs it over the concatenated chunk chains.  A
+    // candidate a chunk pops lies strictly inside a segment of two other
+    // candidates, so it is off the whole set's chain too: the result is the
+    // chain of all candidates.
+    if (threadIdx.x < 64 && n_c > 0) {
+        const int lane = threadIdx.x & 31;
+        const bool upper = threadIdx.x >= 32;
+        int2* st = upper ? hi : lo;
+        auto cross = [](int2 o, int2 b, int2 c) {
+            const int ox = o.x & 0xffff, oy = o.x >> 16, bx = b.x & 0xffff, by = b.x >> 16;
+            const int x = c.x & 0xffff, y = c.x >> 16;
+            return (long long)(bx - ox) * (y - oy) - (long long)(by - oy) * (x - ox);
+        };
+        auto pops = [upper](long long c) { return upper ? c > 0 : c < 0; };  // lower: right turn
+        const int k0 = int((long long)n_c * lane / 32), k1 = int((long long)n_c * (lane + 1) / 32);
+        int n = 0;
+        for (int k = k0; k < k1; ++k) {
+            const int2 e = cand[k];
+            while (n >= 2 && pops(cross(st[k0 + n - 2], st[k0 + n - 1], e))) --n;
+            st[k0 + n++] = e;
+        }
+        const int my_len = n;
+        __syncwarp();
+        // chunk chain lengths through shared memory
+        __shared__ int s_len[2][32];
+        s_len[upper ? 1 : 0][lane] = my_len;
+        __syncwarp();
+        if (lane == 0) {
+            int m = 0;
+            for (int l = 0; l < 32; ++l) {
+                const int l0 = int((long long)n_c * l / 32), ln = s_len[upper ? 1 : 0][l];
+                for (int k = 0; k < ln; ++k) {
+                    const int2 e = st[l0 + k];  // read position >= write position m
+                    while (m >= 2 && pops(cross(st[m - 2], st[m - 1], e))) --m;
+                    st[m++] = e;
+                }
+            }
+            s_n[upper ? 1 : 0] = m;
+        }
+    } else if (threadIdx.x < 2) {
+        s_n[threadIdx.x] = 0;
     }
     __syncthreads();
     if (threadIdx.x != 0) return;
