@@ -140,8 +140,9 @@ def test_schedules_agree(monkeypatch):
     L, R = ps.synth_batch(n, 160, 120, c["n_planes"], 40, False, 2.0, seed=31)
     cfg.maxDisparity = 40
     runs = []
-    for serial in ("1", "0"):
+    for serial, prio in (("1", "0"), ("0", "0"), ("0", "1")):
         monkeypatch.setenv("PS_SERIAL_DEVICE", serial)
+        monkeypatch.setenv("PS_GROUP_PRIO", prio)
         with ps.Context(0) as cx:
             runs.append(cx.run_batch(L, R, cfg, unchecked_cell=True, raise_on_failure=False))
             cx.set_max_groups(1)
@@ -152,6 +153,35 @@ def test_schedules_agree(monkeypatch):
             assert np.array_equal(bits(r[k]), bits(runs[0][k])), k
         assert [[t.meanCost for t in tr] for tr in r["trace"]] == \
                [[t.meanCost for t in tr] for tr in runs[0]["trace"]]
+
+
+def test_concurrent_batches_agree(ctx):
+    """Two batches in flight on one GPU (two contexts, one host thread each,
+    sharing the host worker pool and the device: bench.py --inflight 2) give
+    the bits of each batch run alone -- the reference's threaded == sequential
+    guard (proj/tests/test_pipeline.cpp:75-84,282-291) for the engine."""
+    import threading
+
+    c = ps.BASELINE_CONFIGS[2]
+    cfg = ps.baseline_config(2)
+    batches = [ps.synth_batch(40, 320, 240, c["n_planes"], 48, False, 2.0, seed=s) for s in (71, 72)]
+    cfg.maxDisparity = 48
+    alone = [ctx.run_batch(L, R, cfg, unchecked_cell=True, raise_on_failure=False) for L, R in batches]
+    got = [None, None]
+    with ps.Context(0) as c1, ps.Context(0) as c2:
+        def work(i, cx):
+            for _ in range(2):
+                got[i] = cx.run_batch(*batches[i], cfg, unchecked_cell=True, raise_on_failure=False)
+
+        ts = [threading.Thread(target=work, args=(0, c1)), threading.Thread(target=work, args=(1, c2))]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+    for a, g in zip(alone, got):
+        assert (a["status"] == g["status"]).all()
+        for k in ["disparity", "disparity_valid", "costs", "dense", "dense_valid"]:
+            assert np.array_equal(bits(a[k]), bits(g[k])), k
 
 
 def test_run_batch_multi_equals_single_context(ctx):
