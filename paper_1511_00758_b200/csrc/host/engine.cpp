@@ -219,7 +219,7 @@ Engine::~Engine() {
     for (FrameGroup& g : groups_) {
         for (DevBuf* b : {&g.dTri, &g.dTriOff, &g.dPlanes, &g.dPack, &g.dPackD, &g.dPackOff,
                           &g.dSprev, &g.dChunk, &g.dPin, &g.dCellCnt, &g.dCellStart, &g.dCellItems, &g.dCellXY,
-                          &g.dDup, &g.dPinTri, &g.dTriCount, &g.dFlags, &g.dFix, &g.dColKey, &g.dColIdx, &g.dHull, &g.dHullTmp, &g.dHard})
+                          &g.dDup, &g.dPinTri, &g.dTriCount, &g.dFlags, &g.dFix, &g.dColKey, &g.dColIdx, &g.dHull, &g.dHullTmp, &g.dHard, &g.dRing})
             if (b->p) cudaFree(b->p);
         for (HostBuf* b : {&g.hS, &g.hSprev, &g.hPackOff, &g.hPack, &g.hPackD, &g.hTri, &g.hTriOff,
                            &g.hPin, &g.hTriCount, &g.hFlags, &g.hFix})
@@ -600,6 +600,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         a.hull = static_cast<int*>(grp.dHull.p);
         a.hull_tmp = static_cast<int*>(grp.dHullTmp.p);
         a.hard = static_cast<int*>(grp.dHard.p);
+        a.ring = static_cast<int*>(grp.dRing.p);
         return a;
     };
     auto enqueue_mesh = [&](FrameGroup& grp, double est, int max_points) {
@@ -658,6 +659,15 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                 !dev<int>(grp.dHull, nn * 2 * scap_) || !dev<int>(grp.dHullTmp, nn * 8 * (2 * size_t(W) + 2 * size_t(H) + 8)) ||
                 !dev<int>(grp.dHard, nn * scap_))
                 return fail(PS_CUDA_ERROR, "allocation failed (device mesh)");
+            // pass-1 stars for pass 2 (a lookup instead of a search per step),
+            // kept when they fit in 2 GB per group
+            if (nn * size_t(scap_) * kRingInts * sizeof(int) <= (size_t(2) << 30)) {
+                if (!dev<int>(grp.dRing, nn * size_t(scap_) * kRingInts))
+                    return fail(PS_CUDA_ERROR, "allocation failed (device mesh stars)");
+            } else if (grp.dRing.p) {
+                cudaFree(grp.dRing.p);
+                grp.dRing = DevBuf{};
+            }
         }
 
         // ---- seeding of the group's frames on the (low-priority) seeding

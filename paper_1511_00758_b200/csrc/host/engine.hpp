@@ -64,7 +64,7 @@ struct FrameGroup {
     HostBuf hS, hSprev, hPackOff, hPack, hPackD, hTri, hTriOff, hPin;
     std::vector<int> ntri;
     // device mesh (kernels/star.cu): grid scratch, pin choices, flags, fixes
-    DevBuf dCellCnt, dCellStart, dCellItems, dCellXY, dDup, dPinTri, dTriCount, dFlags, dFix, dColKey, dColIdx, dHull, dHullTmp, dHard;
+    DevBuf dCellCnt, dCellStart, dCellItems, dCellXY, dDup, dPinTri, dTriCount, dFlags, dFix, dColKey, dColIdx, dHull, dHullTmp, dHard, dRing;
     HostBuf hTriCount, hFlags, hFix;
     std::vector<std::vector<int>> fixes;  // per frame: host fixes for the device mesh
     std::vector<uint8_t> replayed;        // per frame: triangles came from the host replay

@@ -428,6 +428,7 @@ __global__ void k_grid_dup(StarArgs a) {
     }
     a.dup[sb + i] = d;
     a.hull[2 * sb + i] = -1;
+    if (a.ring) a.ring[(sb + i) * kRingInts] = -1;
     a.hull[2 * sb + a.scap + i] = -1;
     int* pt = a.pin_tri + 3 * (sb + i);
     pt[0] = pt[1] = pt[2] = -1;
@@ -455,7 +456,8 @@ __device__ unsigned long long g_star_cycles, g_star_max, g_star_n, g_star_hist[2
 // pass 2: [0] points [1] gather cycles [2] local steps [3] local cycles [4] row searches
 // [5] row cycles [6] rows visited [7] column searches [8] column cycles [9] nearest cycles [10] total cycles
 __device__ unsigned long long g_far[12];
-__device__ unsigned long long g_far_pt[1 << 16][12];  // per warp slot: this point's counters
+__device__ unsigned long long g_far_pt[1 << 16][16];  // per warp slot: this point's counters
+#define FAR_PT(i, v) do { if ((threadIdx.x & 31) == 0) g_far_pt[far_slot()][i] += (unsigned long long)(v); } while (0)
 __device__ __forceinline__ int far_slot() {
     return int(((blockIdx.y * gridDim.x + blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5)) & 0xffff);
 }
@@ -483,6 +485,7 @@ __device__ void star_clock(long long t0, int p) {
 }
 #else
 #define FAR_ADD(i, v) do { } while (0)
+#define FAR_PT(i, v) do { } while (0)
 #define FAR_CLOCK() 0ll
 #endif
 
@@ -557,6 +560,15 @@ static_assert(kRegionCells == 2 * kTileT, "two region cells per thread");
 __device__ __forceinline__ void defer_point(const StarArgs& a, int f, int p) {
     const int k = atomicAdd(a.flags + (long long)f * a.flag_ints + 5, 1);
     if (k < a.scap) a.hard[(long long)f * a.scap + k] = p;
+}
+
+// p's pass-1 star kept for pass 2: a deferred point walking past p reads
+// its next neighbour here instead of searching
+__device__ __forceinline__ void keep_star(const StarArgs& a, int f, int p, const int* tb, int nt) {
+    if (!a.ring || nt > (kRingInts - 1) / 2) return;
+    int* rg = a.ring + ((long long)f * a.scap + p) * kRingInts;
+    for (int j = 0; j < 2 * nt; ++j) rg[1 + j] = tb[j];
+    rg[0] = nt;
 }
 
 // the triangles of p's star that p writes (it is their smallest vertex)
@@ -696,6 +708,7 @@ __global__ void __launch_bounds__(kTileT) k_star(StarArgs a) {
             continue;
         }
         emit_star(a, f, P.p, tb, nt);
+        keep_star(a, f, P.p, tb, nt);
     }
     __syncthreads();
     // phase 2: radius 4, hull bookkeeping
@@ -710,6 +723,7 @@ __global__ void __launch_bounds__(kTileT) k_star(StarArgs a) {
             continue;
         }
         emit_star(a, f, P.p, tb, nt);
+        keep_star(a, f, P.p, tb, nt);
         if (closed || nt == 0) continue;
         const long long sb2 = (long long)f * a.scap;
         const int* su = a.su + sb2;
@@ -742,6 +756,7 @@ constexpr int kFarTris = 640;   // triangles of one star (more: the frame is rep
 
 struct WLocal {
     const unsigned long long* ckey;  // the frame's column-extreme keys (k_col_key): lo [0, W), hi [W, 2W)
+    const int* ring;                 // the frame's pass-1 stars (StarArgs::ring), nullptr: none
     int n;
     bool complete;
     star::Box box;
@@ -974,23 +989,42 @@ __device__ __noinline__ int w_rows(const star::Grid& g, int p, int q, int side, 
 __device__ int w_next_far(const star::Grid& g, const unsigned long long* ckey, int p, int q, int side,
                            const star::Box& skip) {
     const int lane = threadIdx.x & 31;
-    {  // the 5x5 cells around q: in a fan along the hull the next neighbour is next to q
+    {  // the 5x5 cells around q: in a fan along the hull the next neighbour is
+       // next to q.  The seed is the best of them in the pencil order (not
+       // just any point on the search side): along a sliver fan its circle is
+       // then the thin one through the true neighbour, and the row search
+       // below reads a few rows instead of the disc of a far seed.
         const int qcx = star::cell_x(g, g.u[q]), qcy = star::cell_y(g, g.v[q]);
-        int found = -1;
+        const long long qx = (long long)g.u[q] - g.u[p], qy = (long long)g.v[q] - g.v[p];
+        int lbest = -1;
+        star::Pencil lk{0, 0};
         if (lane < 25) {
             const int cx = qcx + lane % 5 - 2, cy = qcy + lane / 5 - 2;
             if (cx >= 0 && cy >= 0 && cx < g.gw && cy < g.gh) {
                 const int cell = cy * g.gw + cx;
-                for (int i = g.cell_start[cell]; i < g.cell_start[cell + 1] && found < 0; ++i) {
-                    const int s = g.cell_items[i];
-                    if (s == p || s == q || g.dup[s]) continue;
-                    const long long o = star::orient(g, p, q, s);
-                    if (side > 0 ? o > 0 : o < 0) found = s;
+                for (int i = g.cell_start[cell]; i < g.cell_start[cell + 1]; ++i) {
+                    const int s2 = g.cell_items[i];
+                    if (s2 == p || s2 == q || g.dup[s2]) continue;
+                    const star::Pencil ps =
+                        star::pencil(qx, qy, (long long)g.u[s2] - g.u[p], (long long)g.v[s2] - g.v[p]);
+                    if (side > 0 ? ps.den <= 0 : ps.den >= 0) continue;
+                    if (lbest >= 0) {
+                        const int c = star::pencil_cmp(ps, lk, side);
+                        if (c < 0 || (c == 0 && !w_better(g, p, q, side, lbest, s2))) continue;
+                    }
+                    lbest = s2;
+                    lk = ps;
                 }
             }
         }
-        const unsigned m = __ballot_sync(0xffffffffu, found >= 0);
-        if (m) return w_rows(g, p, q, side, __shfl_sync(0xffffffffu, found, __ffs(m) - 1), skip);
+        if (__any_sync(0xffffffffu, lbest >= 0)) {
+            const int seed = w_reduce(g, p, q, side, lbest, lk);
+            FAR_PT(11, 1);
+            const long long tr = FAR_CLOCK();
+            const int r = w_rows(g, p, q, side, seed, skip);
+            FAR_PT(12, FAR_CLOCK() - tr);
+            return r;
+        }
     }
     // Column extremes nearest first: lanes 0..15 take columns c0 - k, lanes
     // 16..31 c0 + k, four rounds of 16 per side per pass with all their
@@ -1031,10 +1065,14 @@ __device__ int w_next_far(const star::Grid& g, const unsigned long long* ckey, i
             }
         }
         const int mr = __reduce_min_sync(0xffffffffu, fr);
+        FAR_PT(13, 1);
         if (mr < 4) {
             const unsigned m = __ballot_sync(0xffffffffu, fr == mr);
             const int first = __shfl_sync(0xffffffffu, found, __ffs(m) - 1);
-            return w_rows(g, p, q, side, first, star::Box{1, 1, 0, 0});
+            const long long tr = FAR_CLOCK();
+            const int r = w_rows(g, p, q, side, first, star::Box{1, 1, 0, 0});
+            FAR_PT(14, FAR_CLOCK() - tr);
+            return r;
         }
         if (base + 48 >= c0 && base + 48 >= cols - c0) break;
     }
@@ -1102,6 +1140,23 @@ __device__ __noinline__ int w_nearest(const star::Grid& g, int p) {
 }
 
 __device__ __noinline__ int w_step(const star::Grid& g, const WLocal& L, int p, int q, int side) {
+    if (L.ring) {
+        // q's star from pass 1 holds the triangle after p -> q: (q, r, p)
+        // counter-clockwise for side > 0, (q, p, r) for side < 0
+        const int* rg = L.ring + (long long)q * kRingInts;
+        const int n = rg[0];
+        if (n > 0) {
+            const int lane = threadIdx.x & 31;
+            int r = -1;
+            if (lane < n) {
+                const int b = rg[1 + 2 * lane], c = rg[2 + 2 * lane];
+                if (side > 0 ? c == p : b == p) r = side > 0 ? b : c;
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, r >= 0);
+            FAR_ADD(9, 0);
+            if (m) return __shfl_sync(0xffffffffu, r, __ffs(m) - 1);
+        }
+    }
     int start;
     long long t0 = FAR_CLOCK();
     const int r = w_next_local(g, L, p, q, side, start);
@@ -1169,6 +1224,7 @@ __global__ void __launch_bounds__(kFarT) k_star_far(StarArgs a) {
     int* tris = a.tris + 3 * (long long)f * a.pitch;
     WLocal L;
     L.ckey = a.col_key + 2ll * f * a.W;
+    L.ring = a.ring ? a.ring + (long long)f * a.scap * kRingInts : nullptr;
     L.idx = s_idx[wid];
     L.dxy = s_dxy[wid];
     int* tb = s_tri[wid];
@@ -1177,7 +1233,7 @@ __global__ void __launch_bounds__(kFarT) k_star_far(StarArgs a) {
         __syncwarp();
 #ifdef PS_STAR_PROFILE
         if (lane == 0)
-            for (int i = 0; i < 12; ++i) g_far_pt[far_slot()][i] = 0;
+            for (int i = 0; i < 16; ++i) g_far_pt[far_slot()][i] = 0;
 #endif
         const long long tg = FAR_CLOCK();
         w_gather(g, p, L);
@@ -1197,9 +1253,9 @@ __global__ void __launch_bounds__(kFarT) k_star_far(StarArgs a) {
                 if (cyc > 2000000 && atomicAdd(&g_far[11], 1ull) < 40) {
                     const unsigned long long* c = g_far_pt[far_slot()];
                     printf("slow far point f %d p %d (%d,%d) cycles %lld nt %d closed %d gathered %d complete %d hull %d/%d | "
-                           "local %llu/%llu cyc rows %llu/%llu cyc (%llu rows) cols %llu/%llu cyc nearest %llu\n",
+                           "local %llu/%llu cyc rows %llu/%llu cyc (%llu rows) cols %llu/%llu cyc nearest %llu | qfound %llu rows %llu cyc; col rounds %llu rows %llu cyc\n",
                            f, p, g.u[p], g.v[p], cyc, nt, int(closed), L.n, int(L.complete), g.hnext[p], g.hprev[p],
-                           c[2], c[3], c[4], c[5], c[6], c[7], c[8], c[9]);
+                           c[2], c[3], c[4], c[5], c[6], c[7], c[8], c[9], c[11], c[12], c[13], c[14]);
                 }
             }
         }

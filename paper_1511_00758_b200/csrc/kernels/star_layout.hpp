@@ -9,6 +9,8 @@ namespace ps {
 // ambiguous hull vertices grow with the point count, and a record that
 // overflows sends the frame to the (costly, ~n x column height) replay.
 constexpr int kStarSuspectBase = 8;
+// pass-1 stars kept for pass 2 (kernels/star.cu): count + 16 (b, c) pairs
+constexpr int kRingInts = 33;
 struct StarFlagLayout {
     int max_suspect;  // rotation suspects per frame
     int fan_base;     // first int of the hull-vertex fans
