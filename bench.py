@@ -96,7 +96,7 @@ def parse_args():
     p.add_argument("--config", type=int, default=2, help="BASELINE.json config index")
     p.add_argument("--frames", type=int, default=0, help="frames per GPU (default: the config's)")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--inflight", type=int, default=2,
+    p.add_argument("--inflight", type=int, default=3,
                    help="batches in flight per GPU: that many contexts on the GPU, one host thread "
                         "each, steps dealt round-robin (double buffering: one batch's host tail and "
                         "output copies overlap the next batch's device work)")

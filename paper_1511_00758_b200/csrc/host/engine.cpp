@@ -195,6 +195,7 @@ Engine::Engine(int device) : device_(device) {
     cudaEventCreateWithFlags(&chain_event_, cudaEventDisableTiming);
     if (const char* e = std::getenv("PS_SERIAL_DEVICE")) serial_device_ = std::atoi(e) != 0;
     if (const char* e = std::getenv("PS_MIN_GROUP")) min_group_ = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("PS_HOST_FIRST")) host_first_ = std::atoi(e) != 0;
     if (const char* e = std::getenv("PS_MAX_GROUPS")) set_max_groups(std::atoi(e));
     debug_timeline_ = std::getenv("PS_DEBUG_TIMELINE") != nullptr;
     pool_ = &shared_pool();
@@ -551,6 +552,10 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         return std::max(2, int(std::sqrt(1.3 * double(P) / std::max(1.0, est)) + 0.5));
     };
     const StarFlagLayout flay = star_flag_layout(scap_);
+    // the first iteration's mesh (the seeds only) on the host: the device's
+    // mesh kernels are latency-bound at that size and the device is the
+    // busier side (PS_HOST_FIRST=0: device for every iteration)
+    const bool host_first = device_dt && host_first_;
     // fewer frames than host workers: a frame's order queries spread over the
     // idle workers, so a larger query budget still beats the serial replay
     const int budget_scale = std::max(1, int(pool_->size()) / std::max(1, F));
@@ -727,7 +732,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         // the group's own stream continues after its seeding
         if (s == PS_OK) s = check(cudaStreamWaitEvent(grp.st, grp.done_event, 0), "group order");
         if (s != PS_OK) return s;
-        if (device_dt) {  // the first iteration's mesh, on the group stream
+        if (device_dt && !host_first) {  // the first iteration's mesh, on the group stream
             enqueue_mesh(grp, 0.75 * cand_stride, cand_stride);  // ~75% of the candidates match
             s = check(cudaEventRecord(grp.done_event, grp.st), "mesh event");
             if (s != PS_OK) return s;
@@ -861,7 +866,14 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                     int* slot = static_cast<int*>(g2.hTri.p) + size_t(i) * tri_cap * 3;
                     uint8_t* pins = static_cast<uint8_t*>(g2.hPin.p) + size_t(i) * tri_cap;
                     const double ts0 = now_ms();
-                    if (device_dt) {
+                    if (device_dt && host_first && g2.it == 1) {
+                        // the seeds (<= 120 x perBinCap points): the reference sweep
+                        // itself, exact order and pins, cheaper than a device mesh
+                        g2.fixes[i].clear();
+                        g2.replayed[i] = 1;
+                        t = replay_mesh(fm, W, H, slot, tri_cap, pins, w, mstats[worker]);
+                        ++mstats[worker].first_iter;
+                    } else if (device_dt) {
                         // the device meshed the frame; resolve what it listed
                         const int* fl = static_cast<const int*>(g2.hFlags.p) + size_t(i) * flay.ints;
                         t = static_cast<const int*>(g2.hTriCount.p)[i];
@@ -958,8 +970,10 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
             if (n_fix > 0)
                 r = check(cudaMemcpyAsync(dfix, hfix, sizeof(int) * 6 * n_fix, cudaMemcpyHostToDevice, gs),
                           "H2D mesh fixes");
-            const StarArgs a = star_args(grp);
-            launches_ += launch_star_finish(a, dfix, n_fix, tri_cap, gs);
+            if (!(host_first && it == 1)) {
+                const StarArgs a = star_args(grp);
+                launches_ += launch_star_finish(a, dfix, n_fix, tri_cap, gs);
+            }
             // frames the host replayed: their triangles and pins replace the device's
             for (int i = 0; i < n && r == PS_OK; ++i) {
                 if (!grp.replayed[i] || grp.ntri[i] <= 0) continue;
@@ -1251,6 +1265,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         for (const MeshStats& m : mstats) {
             tot.frames += m.frames;
             tot.fallbacks += m.fallbacks;
+            tot.first_iter += m.first_iter;
             tot.fb_device += m.fb_device;
             for (int b = 0; b < 5; ++b) tot.fb_why[b] += m.fb_why[b];
             tot.fb_queries += m.fb_queries;
@@ -1286,7 +1301,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         KernelStat& k7 = stat("host_order_init");  // of which: SweepOrder::init (lex order, chains, buckets)
         k7.ms += tot.init_ms / workers;
         KernelStat& k4 = stat("host_replay");  // frame-iterations replayed (delaunay_lex)
-        k4.launches += int(tot.fallbacks);
+        k4.launches += int(tot.fallbacks - tot.first_iter);  // first-iteration host meshes are not fallbacks
         k4.ms += tot.replay_ms / workers;
         // of which, by cause
         stat("host_replay_device").launches += int(tot.fb_device);    // star overflow / capacity

@@ -204,6 +204,7 @@ private:
     bool serial_device_ = true;
     int min_group_ = 64;  // frames per group at least (PS_MIN_GROUP)
     bool group_prio_ = false;  // PS_GROUP_PRIO
+    bool host_first_ = true;   // PS_HOST_FIRST: first-iteration mesh on the host
     bool debug_timeline_ = false;  // PS_DEBUG_TIMELINE: group milestones on stderr
     cudaEvent_t chain_event_ = nullptr;
     cudaStream_t seed_st_ = nullptr;  // seeding, group after group (group 0 first)

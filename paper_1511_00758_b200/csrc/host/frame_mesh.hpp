@@ -34,6 +34,7 @@ namespace ps {
 struct MeshStats {
     long long frames = 0;      // frame-iterations meshed
     long long fallbacks = 0;   // of which replayed with delaunay_lex
+    long long first_iter = 0;  //   of which first-iteration meshes (by design, not a fallback)
     long long fb_device = 0;   //   because the device mesh flagged the frame (star overflow, capacity)
     long long fb_why[5] = {0, 0, 0, 0, 0};  // device causes: fan, search, degree, suspects, capacity
     long long fb_queries = 0;  //   because the order-query budget ran out
