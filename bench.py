@@ -500,7 +500,10 @@ def run_ours(args, rank, world, local_rank):
     e2e_ms = max_over_ranks(f0.elapsed_time(f1))
     e2e_value = whole_job_value(frames, world, args.steps, e2e_ms)
     h2d = 2 * frames * P
-    d2h = frames * P * (4 + 1 + 4 + 4 + 1) + frames * cfg.iterations * C.sizeof(ps._native.PsIterStats)
+    # D_f 4 B + dense 4 B + dense validity 1 B per pixel, and C_f / validity as
+    # one code byte (expanded on the host: engine wire_codes; PS_WIRE_CODES=0: 5 B)
+    wire = os.environ.get("PS_WIRE_CODES", "1") != "0"
+    d2h = frames * P * (4 + 4 + 1 + (1 if wire else 5)) + frames * cfg.iterations * C.sizeof(ps._native.PsIterStats)
 
     # ---------------- single-frame latency through ps_run, wall clock
     lat = []

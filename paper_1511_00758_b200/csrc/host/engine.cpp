@@ -196,6 +196,7 @@ Engine::Engine(int device) : device_(device) {
     if (const char* e = std::getenv("PS_SERIAL_DEVICE")) serial_device_ = std::atoi(e) != 0;
     if (const char* e = std::getenv("PS_MIN_GROUP")) min_group_ = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("PS_HOST_FIRST")) host_first_ = std::atoi(e) != 0;
+    if (const char* e = std::getenv("PS_WIRE_CODES")) wire_codes_ = std::atoi(e) != 0;
     if (const char* e = std::getenv("PS_MAX_GROUPS")) set_max_groups(std::atoi(e));
     debug_timeline_ = std::getenv("PS_DEBUG_TIMELINE") != nullptr;
     pool_ = &shared_pool();
@@ -552,6 +553,31 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         return std::max(2, int(std::sqrt(1.3 * double(P) / std::max(1.0, est)) + 0.5));
     };
     const StarFlagLayout flay = star_flag_layout(scap_);
+    // C_f and validity over PCIe as the byte codes (expand(): C_f = cost[c]
+    // for c < code_high, else costHigh; valid = c < code_high -- K7's own
+    // expansion, refine.cu)
+    const bool wire_codes = wire_codes_ && sink_.active && (sink_.cost || sink_.disparity_valid);
+    uint8_t* hCodes = wire_codes ? host<uint8_t>(hCodeStage_, size_t(F) * P) : nullptr;
+    if (wire_codes && !hCodes) return fail(PS_CUDA_ERROR, "allocation failed (code staging)");
+    float code_lut[256];
+    for (int c = 0; c < 256; ++c) code_lut[c] = c < tab.code_high ? tab.cost[c] : tab.cost_high;
+    const Sink wsink = sink_;
+    auto expand = [&, code_lut_p = &code_lut](int f0, int n) {
+        // a task per 4 frames; the run waits for them before it returns
+        for (int a = 0; a < n; a += 4) {
+            const int fa = f0 + a, fn = std::min(4, n - a);
+            expand_pending_.fetch_add(1);
+            pool_->submit([this, fa, fn, P, hCodes, wsink, lut = *code_lut_p, ch = tab.code_high](int) {
+                const size_t b = size_t(fa) * P, e = b + size_t(fn) * P;
+                if (wsink.cost)
+                    for (size_t i = b; i < e; ++i) wsink.cost[i] = lut[hCodes[i]];
+                if (wsink.disparity_valid)
+                    for (size_t i = b; i < e; ++i) wsink.disparity_valid[i] = hCodes[i] < ch ? 1 : 0;
+                std::lock_guard<std::mutex> lk(done_m_);
+                if (expand_pending_.fetch_sub(1) == 1) done_cv_.notify_all();
+            });
+        }
+    };
     // the first iteration's mesh (the seeds only) on the host: the device's
     // mesh kernels are latency-bound at that size and the device is the
     // busier side (PS_HOST_FIRST=0: device for every iteration)
@@ -759,7 +785,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         done_cv_.wait(lk, [&] {
             for (int gi = 0; gi < G; ++gi)
                 if (groups_[gi].pending.load() != 0) return false;
-            return true;
+            return expand_pending_.load() == 0;
         });
     };
     std::atomic<double> dt_ms_sum{0.0}, sweep_ms_sum{0.0};
@@ -1113,10 +1139,14 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
             const size_t b = size_t(f0) * P, cnt = size_t(n) * P;
             if (sink_.disparity)
                 cudaMemcpyAsync(sink_.disparity + b, dDf + b, cnt * 4, cudaMemcpyDeviceToHost, gs);
-            if (sink_.disparity_valid)
-                cudaMemcpyAsync(sink_.disparity_valid + b, dDv + b, cnt, cudaMemcpyDeviceToHost, gs);
-            if (sink_.cost)
-                cudaMemcpyAsync(sink_.cost + b, dCf + b, cnt * 4, cudaMemcpyDeviceToHost, gs);
+            if (wire_codes) {  // one code byte per pixel; expanded on the host when the group is done
+                cudaMemcpyAsync(hCodes + b, dCode + b, cnt, cudaMemcpyDeviceToHost, gs);
+            } else {
+                if (sink_.disparity_valid)
+                    cudaMemcpyAsync(sink_.disparity_valid + b, dDv + b, cnt, cudaMemcpyDeviceToHost, gs);
+                if (sink_.cost)
+                    cudaMemcpyAsync(sink_.cost + b, dCf + b, cnt * 4, cudaMemcpyDeviceToHost, gs);
+            }
             if (sink_.dense)
                 cudaMemcpyAsync(sink_.dense + b, dDense + b, cnt * 4, cudaMemcpyDeviceToHost, gs);
             if (sink_.dense_valid)
@@ -1201,6 +1231,7 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                 if (grp.it == iters) {
                     grp.phase = FrameGroup::kDone;
                     ++done_groups;
+                    if (wire_codes) expand(grp.f0, grp.n);  // its codes are in hCodes
                 } else {
                     s = fetch_delta(grp, true);
                     if (s != PS_OK) {
@@ -1218,6 +1249,10 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
             std::unique_lock<std::mutex> lk(done_m_);
             done_cv_.wait_for(lk, std::chrono::microseconds(200));
         }
+    }
+    {  // the host expansion of the streamed codes
+        std::unique_lock<std::mutex> lk(done_m_);
+        done_cv_.wait(lk, [&] { return expand_pending_.load() == 0; });
     }
     host_dt_ms = dt_ms_sum.load() / std::max(1, pool_->size());
     if (debug_timeline_) {

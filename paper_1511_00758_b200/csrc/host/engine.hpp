@@ -164,6 +164,11 @@ private:
     };
     Sink sink_;
     Sink done_sink_;         // the sink the last run streamed into
+    // C_f / validity streamed as their byte codes (1 B/px over PCIe instead of
+    // 5) and expanded on the host pool (PS_WIRE_CODES=0: copy the expanded maps)
+    bool wire_codes_ = true;
+    HostBuf hCodeStage_;
+    std::atomic<int> expand_pending_{0};
     bool streamed_ = false;  // the last run already copied its outputs
 
     int device_ = 0;
