@@ -21,6 +21,7 @@
 // then replays the reference sweep for that frame (exact fallback).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 
 #include "launch.hpp"
@@ -1411,7 +1412,13 @@ int launch_star_mesh(const StarArgs& a, int max_points, cudaStream_t st) {
     }
     STAR_CHECK("k_star");
     // deferred points are a few percent: a warp each, the grid strided
-    k_star_far<<<dim3((max_points / 32 + 3) / 4 + 1, a.frames), kFarT, 0, st>>>(a);
+    // (the grid strides over the deferred list: ~1-8% of the points, so a
+    // warp per 32 points would leave most blocks empty; a warp per ~1k points
+    // of the frame, at least 48 blocks, keeps a point per warp at VGA)
+    {
+        const int per_frame = std::min((max_points / 32 + 3) / 4 + 1, std::max(48, max_points / 1024));
+        k_star_far<<<dim3(per_frame, a.frames), kFarT, 0, st>>>(a);
+    }
     STAR_CHECK("k_star_far");
 #ifdef PS_STAR_PROFILE
     k_star_report<<<1, 1, 0, st>>>();
