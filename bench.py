@@ -96,7 +96,7 @@ def parse_args():
     p.add_argument("--config", type=int, default=2, help="BASELINE.json config index")
     p.add_argument("--frames", type=int, default=0, help="frames per GPU (default: the config's)")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--inflight", type=int, default=3,
+    p.add_argument("--inflight", type=int, default=0,
                    help="batches in flight per GPU: that many contexts on the GPU, one host thread "
                         "each, steps dealt round-robin (double buffering: one batch's host tail and "
                         "output copies overlap the next batch's device work)")
@@ -381,7 +381,7 @@ def run_ours(args, rank, world, local_rank):
     H, W = cfgd["height"], cfgd["width"]
     P = W * H
     L, R, keep = make_inputs(ps, cfgd, frames, rank_seed(rank, frames), pinned=True)
-    inflight = max(1, args.inflight)
+    inflight = args.inflight if args.inflight > 0 else (3 if world < 4 else 2)
     ctxs = [ps.Context(local_rank) for _ in range(inflight)]
     ctx = ctxs[0]
     stream = torch.cuda.current_stream()

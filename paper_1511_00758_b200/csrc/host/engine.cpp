@@ -549,8 +549,12 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     // previous iteration's occupancy grid (plus the older, sparser supports)
     // ~1.3 supports per cell, so the 5x5 cells a star starts from hold ~30
     // candidates (star_dt.cuh kLocalMax); est = expected supports per frame
+    static const double star_density = [] {  // supports per grid cell (PS_STAR_DENSITY: probing)
+        const char* e = std::getenv("PS_STAR_DENSITY");
+        return e ? std::atof(e) : 1.3;
+    }();
     auto star_gs = [&](double est) {
-        return std::max(2, int(std::sqrt(1.3 * double(P) / std::max(1.0, est)) + 0.5));
+        return std::max(2, int(std::sqrt(star_density * double(P) / std::max(1.0, est)) + 0.5));
     };
     const StarFlagLayout flay = star_flag_layout(scap_);
     // C_f and validity over PCIe as the byte codes (expand(): C_f = cost[c]
