@@ -598,7 +598,7 @@ __device__ __forceinline__ void emit_star(const StarArgs& a, int f, int p, const
 // star needs a wider search (about 1% at BASELINE config 2's last iteration:
 // next to holes and along the hull) or has more than kStarTris triangles is
 // listed for pass 2.
-__global__ void __launch_bounds__(kTileT) k_star(StarArgs a) {
+__global__ void __launch_bounds__(kTileT, 8) k_star(StarArgs a) {
     __shared__ int s_start[kRegionCells + 1];
     __shared__ int s_xy[kTileCap], s_id[kTileCap];
     __shared__ int s_warp[kTileT / 32];
