@@ -161,17 +161,22 @@ __global__ void __launch_bounds__(256, 4) k_frontend(const uint8_t* __restrict__
     // gradient threshold in 16-bit lanes: grad in [0, 510]
     const int tc = thr < 0 ? 0 : (thr > 511 ? 511 : thr);
     const uint32_t tbias = uint32_t(0x8000 - tc) * 0x00010001u;
-    // interior test per pixel (u in [2, W-2)) of the lane's four columns
-    uint32_t colok = 0;
+    // interior test per pixel (u in [2, W-2)) and in-frame test (u < W) of the
+    // lane's four columns
+    uint32_t colok = 0, colin = 0;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const int u = u0 + c + 32 * q;
         colok |= uint32_t(u >= 2 && u < W - 2) << q;
+        colin |= uint32_t(u < W) << q;
     }
     int cnt = 0;
     const int y0 = wy * kK1RowsPerWarp;  // first tile row of this warp
+    const long long fb = f * g.pixels + u0 + c;
+    const bool want_mask = mask || code || mask_count;
     // one view at a time (half the live window registers): L with the
-    // gradient mask and code, then R
+    // gradient mask and code, then R; the rows fully unrolled (a row past the
+    // frame only stores nothing), so the window slides by renaming
 #pragma unroll 1
     for (int view = 0; view < (R ? 2 : 1); ++view) {
         const uint32_t(*sw)[kK1Words] = view ? sr : sl;
@@ -200,18 +205,19 @@ __global__ void __launch_bounds__(256, 4) k_frontend(const uint8_t* __restrict__
                 nw[4][du] = ~w[4][du] & 0x7f7f7f7fu;
             }
             const int v = v0 + y0 + i;
-            if (v >= H) break;  // warp-uniform
-            const bool row_in = v >= 2 && v < H - 2;
-            const uint32_t ok = row_in ? colok : 0u;
-            const long long base = f * g.pixels + (long long)v * W + u0 + c;
-            if (cen) {
+            const bool row_ok = v < H;  // warp-uniform
+            const uint32_t ok = (v >= 2 && v < H - 2) ? colok : 0u;
+            const uint32_t st = row_ok ? colin : 0u;
+            const long long rb = fb + (long long)v * W;
+            if (cen && st) {
                 uint32_t a0, a1, a2;
                 census4(w, nw, one, a0, a1, a2);
+                uint32_t* crow = cen + rb;
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
-                    if (u0 + c + 32 * q < W) cen[base + 32 * q] = ((ok >> q) & 1u) ? census_of(a0, a1, a2, q) : 0u;
+                    if ((st >> q) & 1u) crow[32 * q] = ((ok >> q) & 1u) ? census_of(a0, a1, a2, q) : 0u;
             }
-            if (view == 0 && (mask || code || mask_count)) {
+            if (view == 0 && want_mask && st) {
                 // |L(u+1)-L(u-1)| + |L(v+1)-L(v-1)| >= threshold (image.cpp:43-60), 16-bit lanes
                 const uint32_t gh = __vabsdiffu4(w[2][3], w[2][1]);
                 const uint32_t gv = __vabsdiffu4(w[3][2], w[1][2]);
@@ -220,12 +226,14 @@ __global__ void __launch_bounds__(256, 4) k_frontend(const uint8_t* __restrict__
                 const uint32_t mk =
                     (((ge >> 15) & 1u) | ((go >> 14) & 2u) | ((ge >> 29) & 4u) | ((go >> 28) & 8u)) & ok;
                 cnt += __popc(mk);
+                uint8_t* mrow = mask ? mask + rb : nullptr;
+                uint8_t* crow8 = code ? code + rb : nullptr;
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    if (u0 + c + 32 * q >= W) continue;
+                    if (!((st >> q) & 1u)) continue;
                     const bool m = (mk >> q) & 1u;
-                    if (mask) mask[base + 32 * q] = m ? 1 : 0;
-                    if (code) code[base + 32 * q] = m ? code_high : kCodeOff;
+                    if (mrow) mrow[32 * q] = m ? 1 : 0;
+                    if (crow8) crow8[32 * q] = m ? code_high : kCodeOff;
                 }
             }
         }
