@@ -548,7 +548,6 @@ bool SweepOrder::resolve_windows(const int* tris, int count, uint64_t* birth, in
         const bool replayed = replay(u0, u1, v0, v1, last, S);
         bool ok = replayed;
         if (!replayed) grow_all = true;
-        const int n = int(S.rrank_.size());
         // the query triangles' slots: a linear scan for a few triangles, a
         // sorted key table for many
         const bool table = count > 8;

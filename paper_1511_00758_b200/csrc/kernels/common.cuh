@@ -11,9 +11,29 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 namespace ps {
+
+// Device-side bounds checks of the checked build (make CHECKED=1, or
+// -DPS_CHECKED): a failing check prints its site and traps, so the launch
+// fails and the run returns PS_CUDA_ERROR.  The stand-in for
+// compute-sanitizer, which this GPU pool does not allow.
+#ifdef PS_CHECKED
+#define PS_CHECK(cond)                                                                             \
+    do {                                                                                           \
+        if (!(cond)) {                                                                             \
+            printf("PS_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__,   \
+                   int(blockIdx.x), int(threadIdx.x));                                             \
+            __trap();                                                                              \
+        }                                                                                          \
+    } while (0)
+#else
+#define PS_CHECK(cond) \
+    do {               \
+    } while (0)
+#endif
 
 constexpr int kCensusBits = 24;
 constexpr int kCensusRadius = 2;  // CensusField::kRadius (census.hpp:19)

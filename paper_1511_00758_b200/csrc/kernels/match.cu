@@ -111,6 +111,7 @@ struct MatchEmitOp {
         const long long o = (long long)f * cand_stride + i;
         const long long s = (long long)f * scap + pos;
         const int u = cand_u[o], v = cand_v[o];
+        PS_CHECK(pos >= 0 && pos < scap && u >= 0 && u < g.width && v >= 0 && v < g.height);
         su[s] = u;
         sv[s] = v;
         sd[s] = double(disp[o]);  // SupportPoint{u, v, double(match.disparity)}, sparse.cpp:187

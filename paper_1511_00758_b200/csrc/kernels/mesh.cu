@@ -148,6 +148,7 @@ struct RasterOut {
 
 __device__ __forceinline__ void put(const RasterOut& o, long long frame_base, long long idx,
                                     int32_t t, double a, double b, double c, int u, int v) {
+    PS_CHECK(u >= 0 && v >= 0 && idx >= 0 && frame_base >= 0);
     if (o.lookup) {
         o.lookup[frame_base + idx] = t;
     } else {
@@ -174,6 +175,7 @@ __global__ void __launch_bounds__(kThreads) k_raster(
                                            : (long long)blockIdx.x * kThreads;
     const bool active = t < total && (!warp_per_tri || lane == 0);
     const int W = g.width, H = g.height;
+    PS_CHECK(total > 0 && frames > 0);
     int x[3] = {0, 0, 0}, y[3] = {0, 0, 0};
     int f = 0, vmin = 0, vmax = -1;
     double pa = 0.0, pb = 0.0, pc = 0.0;

@@ -274,6 +274,8 @@ __global__ void __launch_bounds__(256, 4) k_refine_bulk(RefineArgs a, CostTables
         const unsigned n = unsigned(min(kTile, P - off));
         const int h = min(off, H);  // halo inside this frame (rows never reach back further)
         const int base = f * P + off;
+        PS_CHECK(off >= 0 && off < P && h >= 0 && h <= H && base - h >= 0);
+        PS_CHECK(9 * kTile + 4 * (H + int(n)) <= bg.stage_bytes);
         unsigned char* st = stage_ptr(s);
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n"
                      :: "r"(smem_u32(&bars[s])), "r"(n * 13u + 4u * unsigned(h)) : "memory");
@@ -380,6 +382,7 @@ __global__ void __launch_bounds__(256, 4) k_refine_bulk(RefineArgs a, CostTables
                     // [0, ND) (raster), and a NaN (-> 0) is rejected below
                     const int dr = __float2int_rz(__fadd_rz(d, 0.5f));
                     const bool ok = c0 != kCodeOff && d == d && u - dr >= 2;
+                    PS_CHECK(!ok || (p0 + j - dr >= -H && p0 + j - dr < kTile));
                     crv[j] = ok ? sm_cr[p0 + j - dr] : 0u;  // same-row cR(u - dr), staged
                     okm |= unsigned(ok) << j;
                 }
@@ -387,6 +390,7 @@ __global__ void __launch_bounds__(256, 4) k_refine_bulk(RefineArgs a, CostTables
             int seg = -1;
             unsigned gk = 32, gi = 0, bk = 32, bi = 0;  // best (k, idx) of the segment per grid
             auto seg_flush = [&]() {
+                PS_CHECK((gk == 32 && bk == 32) || (seg >= 0 && seg < a.cells_per_frame));
                 if (gk < 32) atomicMin(Cg_f + seg, (unsigned long long)gk << 32 | gi);
                 if (bk < 32) atomicMin(Cb_f + seg, (unsigned long long)bk << 32 | bi);
             };

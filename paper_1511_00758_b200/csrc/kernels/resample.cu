@@ -58,6 +58,7 @@ struct ConfidentOp {
         float d;
         winner(f, c, u, v, d);
         const long long s = (long long)f * scap + pos;
+        PS_CHECK(pos >= 0 && pos < scap && u >= 0 && u < g.width && v >= 0 && v < g.height);
         su[s] = u;
         sv[s] = v;
         sd[s] = double(d);
@@ -81,6 +82,7 @@ struct InvalidOp {
     __device__ void emit(int f, int c, int pos) const {
         const long long idx = (long long)(Cb[(long long)f * stride + c] & 0xffffffffull);
         const int v = int(idx / g.width);
+        PS_CHECK(pos >= 0 && pos < rstride && v >= 0 && v < g.height);
         ru[(long long)f * rstride + pos] = int(idx - (long long)v * g.width);
         rv[(long long)f * rstride + pos] = v;
     }

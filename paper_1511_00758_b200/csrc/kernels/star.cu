@@ -409,7 +409,9 @@ __global__ void k_grid_fill(StarArgs a) {
     if (i >= a.S[f]) return;
     const long long sb = (long long)f * a.scap;
     const int cell = (a.sv[sb + i] / a.gs) * a.gw + a.su[sb + i] / a.gs;
+    PS_CHECK(cell >= 0 && cell < a.gw * a.gh);
     const int pos = atomicAdd(a.cell_cnt + (long long)f * a.gw * a.gh + cell, 1);
+    PS_CHECK(pos >= 0 && pos < a.S[f]);
     a.cell_items[sb + pos] = i;
 }
 
@@ -578,6 +580,7 @@ __device__ __forceinline__ void emit_star(const StarArgs& a, int f, int p, const
     for (int j = 0; j < nt; ++j) ne += p < tb[2 * j] && p < tb[2 * j + 1];
     if (ne == 0) return;
     int slot = atomicAdd(a.tri_count + f, ne);
+    PS_CHECK(nt >= 0 && nt <= kStarTris && p >= 0 && p < a.S[f]);
     int* tris = a.tris + 3 * (long long)f * a.pitch;
     for (int j = 0; j < nt; ++j)
         if (p < tb[2 * j] && p < tb[2 * j + 1]) {

@@ -1,4 +1,5 @@
-"""Small pipeline batches for compute-sanitizer (racecheck / synccheck / memcheck / initcheck).
+"""Small pipeline batches for compute-sanitizer (racecheck / synccheck / memcheck / initcheck)
+or for the bounds-checked build (PS_LIB_PATH=.../libplanestereo_b200_checked.so).
 
 Runs every device stage of the pipeline (K1 front end, K2 corners + sort, K3
 match + compaction, the device mesh of kernels/star.cu, the raster, K7 bulk
@@ -23,6 +24,10 @@ import paper_1511_00758_b200 as ps
 def main(mode: str) -> int:
     if mode == "tiny":
         shapes = [(64, 48, 1, 16, 4, 2)]
+    elif mode == "baseline":
+        # BASELINE config 2 geometry (VGA, ND 64, grid 10, 3 iterations), a
+        # 70-frame batch (two frame groups), and cfg1's KITTI shape
+        shapes = [(640, 480, 70, 64, 10, 3), (1242, 375, 3, 128, 8, 4)]
     else:
         # (W, H, frames, ND, cell, iterations): a multi-group batch is not
         # needed for the kernels' own races; 8 frames exercise the grid loops
