@@ -12,6 +12,9 @@
 #include "engine.hpp"
 
 #include <algorithm>
+#ifdef __SSE2__
+#include <emmintrin.h>
+#endif
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -119,6 +122,29 @@ CostTables make_tables(const ps_config& c) {
     t.fixed[t.code_high] = (unsigned long long)std::ldexp(double(c.cost_high), 36);
     t.cost_high = c.cost_high;
     return t;
+}
+
+// C_f from its byte code: cost[c] = float(c) / 24.0f (make_tables) for
+// c < code_high, else costHigh -- 16 codes per step with SSE2 (divps is
+// correctly rounded, so the values are make_tables' bit for bit).
+static void expand_costs(const uint8_t* __restrict__ in, float* __restrict__ out, size_t n, int ch, float chigh) {
+    size_t i = 0;
+#ifdef __SSE2__
+    const __m128 d24 = _mm_set1_ps(float(kCensusBits)), hi = _mm_set1_ps(chigh);
+    const __m128i chv = _mm_set1_epi32(ch), zero = _mm_setzero_si128();
+    for (; i + 16 <= n; i += 16) {
+        const __m128i v = _mm_loadu_si128(reinterpret_cast<const __m128i*>(in + i));
+        const __m128i lo16 = _mm_unpacklo_epi8(v, zero), hi16 = _mm_unpackhi_epi8(v, zero);
+        const __m128i q[4] = {_mm_unpacklo_epi16(lo16, zero), _mm_unpackhi_epi16(lo16, zero),
+                              _mm_unpacklo_epi16(hi16, zero), _mm_unpackhi_epi16(hi16, zero)};
+        for (int k = 0; k < 4; ++k) {
+            const __m128 x = _mm_div_ps(_mm_cvtepi32_ps(q[k]), d24);
+            const __m128 m = _mm_castsi128_ps(_mm_cmplt_epi32(q[k], chv));
+            _mm_storeu_ps(out + i + 4 * k, _mm_or_ps(_mm_and_ps(m, x), _mm_andnot_ps(m, hi)));
+        }
+    }
+#endif
+    for (; i < n; ++i) out[i] = int(in[i]) < ch ? float(in[i]) / float(kCensusBits) : chigh;
 }
 
 // C_f values are k/24 floats or costHigh; their 2^-36 fixed-point sum is exact
@@ -563,20 +589,22 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     const bool wire_codes = wire_codes_ && sink_.active && (sink_.cost || sink_.disparity_valid);
     uint8_t* hCodes = wire_codes ? host<uint8_t>(hCodeStage_, size_t(F) * P) : nullptr;
     if (wire_codes && !hCodes) return fail(PS_CUDA_ERROR, "allocation failed (code staging)");
-    float code_lut[256];
-    for (int c = 0; c < 256; ++c) code_lut[c] = c < tab.code_high ? tab.cost[c] : tab.cost_high;
     const Sink wsink = sink_;
-    auto expand = [&, code_lut_p = &code_lut](int f0, int n) {
+    auto expand = [&](int f0, int n) {
         // a task per 4 frames; the run waits for them before it returns
         for (int a = 0; a < n; a += 4) {
             const int fa = f0 + a, fn = std::min(4, n - a);
             expand_pending_.fetch_add(1);
-            pool_->submit([this, fa, fn, P, hCodes, wsink, lut = *code_lut_p, ch = tab.code_high](int) {
-                const size_t b = size_t(fa) * P, e = b + size_t(fn) * P;
-                if (wsink.cost)
-                    for (size_t i = b; i < e; ++i) wsink.cost[i] = lut[hCodes[i]];
-                if (wsink.disparity_valid)
-                    for (size_t i = b; i < e; ++i) wsink.disparity_valid[i] = hCodes[i] < ch ? 1 : 0;
+            pool_->submit([this, fa, fn, P, hCodes, wsink, ch = tab.code_high, chigh = tab.cost_high](int) {
+                const size_t b = size_t(fa) * P, n = size_t(fn) * P;
+                const uint8_t* __restrict__ in = hCodes + b;
+                // cost[c] = float(c) / 24.0f (make_tables, census.hpp:45-47):
+                // a correctly rounded division, so the loop vectorises
+                if (wsink.cost) expand_costs(in, wsink.cost + b, n, ch, chigh);
+                if (wsink.disparity_valid) {
+                    uint8_t* __restrict__ out = wsink.disparity_valid + b;
+                    for (size_t i = 0; i < n; ++i) out[i] = in[i] < ch ? 1 : 0;
+                }
                 std::lock_guard<std::mutex> lk(done_m_);
                 if (expand_pending_.fetch_sub(1) == 1) done_cv_.notify_all();
             });
