@@ -1033,7 +1033,15 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
                 launches_ += launch_star_finish(a, dfix, n_fix, tri_cap, gs);
             }
             // frames the host replayed: their triangles and pins replace the device's
-            for (int i = 0; i < n && r == PS_OK; ++i) {
+            // (the first iteration on the host: every frame, one pitched copy each)
+            if (host_first && it == 1 && r == PS_OK && max_nt > 0) {
+                r = check(cudaMemcpy2DAsync(dTri, pitch * 12, grp.hTri.p, size_t(tri_cap) * 12, size_t(max_nt) * 12, n,
+                                            cudaMemcpyHostToDevice, gs), "H2D first-iteration triangles");
+                if (r == PS_OK)
+                    r = check(cudaMemcpy2DAsync(dPin, pitch, grp.hPin.p, size_t(tri_cap), size_t(max_nt), n,
+                                                cudaMemcpyHostToDevice, gs), "H2D first-iteration pins");
+            }
+            for (int i = 0; i < n && r == PS_OK && !(host_first && it == 1); ++i) {
                 if (!grp.replayed[i] || grp.ntri[i] <= 0) continue;
                 r = check(cudaMemcpyAsync(dTri + size_t(i) * pitch * 3,
                                           static_cast<int*>(grp.hTri.p) + size_t(i) * tri_cap * 3,
