@@ -85,3 +85,21 @@ def test_reference_arm_under_torchrun_two_ranks():
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["cpu_baseline"]["kind"] in ("reference", "port")
     assert line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libps_ref.so"))
+                    and not os.path.exists(os.path.join(ROOT, "oracle", "_build", "libps_oracle.so")),
+                    reason="CPU checker not built")
+def test_bench_gpus_flag_launches_ranks_itself():
+    """`python bench.py --gpus 2` without a launcher re-executes itself under
+    torch.distributed.run with two ranks (one process per GPU): the line
+    reports n_gpus 2, printed by rank 0 only."""
+    cmd = [sys.executable, "bench.py", "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "0",
+           "--frames", "2", "--config", "0"]
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["impl"] == "reference"
