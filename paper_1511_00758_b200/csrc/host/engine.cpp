@@ -664,6 +664,11 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
         a.hull_tmp = static_cast<int*>(grp.dHullTmp.p);
         a.hard = static_cast<int*>(grp.dHard.p);
         a.ring = static_cast<int*>(grp.dRing.p);
+        static const int phase2 = [] {
+            const char* e = std::getenv("PS_STAR_PHASE2");
+            return e ? std::atoi(e) : 1;
+        }();
+        a.phase2 = phase2;
         return a;
     };
     auto enqueue_mesh = [&](FrameGroup& grp, double est, int max_points) {

@@ -147,6 +147,7 @@ struct StarArgs {
     int* hull;                    // per frame 2 * scap: hull successor / predecessor per point
     int* hull_tmp;                // per frame 8 * (2 * W + 2 * H + 8) ints: monotone-chain stacks
     int* hard;                    // per frame scap: points pass 1 deferred to pass 2 (count in flags[5])
+    int phase2;                   // k_star's own radius-4 phase (1), else such points go to pass 2
     int* ring;                    // per support kRingInts ints: its pass-1 star (count, then the (b, c)
                                   // of each triangle (p, b, c)); count -1: none; nullptr: not kept
 };

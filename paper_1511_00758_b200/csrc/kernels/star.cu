@@ -702,9 +702,15 @@ __global__ void __launch_bounds__(kTileT, 8) k_star(StarArgs a) {
         bool closed;
         const int nt = star::tile_walk(g, T, P, 2, closed, tb, kStarTris);
         if (nt == -4 || (nt > 0 && !closed)) {
-            const int at2 = atomicAdd(&s_nlist, 1);
-            if (at2 < kTileT) s_list[at2] = i;
-            else defer_point(a, f, P.p);
+            // radius 4 / hull bookkeeping: in this block (phase 2, a thread per
+            // point) or, PS_STAR_PHASE2=0, in pass 2 (a warp per point)
+            if (a.phase2) {
+                const int at2 = atomicAdd(&s_nlist, 1);
+                if (at2 < kTileT) s_list[at2] = i;
+                else defer_point(a, f, P.p);
+            } else {
+                defer_point(a, f, P.p);
+            }
             continue;
         }
         if (nt < 0) {
