@@ -547,6 +547,9 @@ int launch_candidates(const uint8_t* left, FrameGeom g, int frames, int corner_t
     if (cap <= 4) {
         allow((const void*)k_corner_bins<4>, 0, 256 * 4 * 8 + 264);
         k_corner_bins<4><<<grid, 256, tile, st>>>(left, g, corner_threshold, cap, bin_keys, bin_count);
+    } else if (cap == 5) {  // the default perBinCap (config.hpp): a top-5 per thread
+        allow((const void*)k_corner_bins<5>, 0, 256 * 5 * 8 + 264);
+        k_corner_bins<5><<<grid, 256, tile, st>>>(left, g, corner_threshold, cap, bin_keys, bin_count);
     } else if (cap <= 8) {
         allow((const void*)k_corner_bins<8>, 1, 256 * 8 * 8 + 264);
         k_corner_bins<8><<<grid, 256, tile, st>>>(left, g, corner_threshold, cap, bin_keys, bin_count);
