@@ -241,7 +241,7 @@ Engine::~Engine() {
                       &s_d, &s_e, &s_f, &s_g, &s_h, &s_i, &s_j};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
-    HostBuf* hbufs[] = {&hS_, &hTraceSum_, &hTraceValid_, &hMaskCount_};
+    HostBuf* hbufs[] = {&hS_, &hTraceSum_, &hTraceValid_, &hMaskCount_, &hCodeStage_};
     for (HostBuf* b : hbufs)
         if (b->p) cudaFreeHost(b->p);
     for (FrameGroup& g : groups_) {
@@ -550,7 +550,8 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
     const char* dt_mode = std::getenv("PS_DELAUNAY");
     const bool lex_only = dt_mode && std::string(dt_mode) == "lex";
     const bool device_dt = !(dt_mode && (std::string(dt_mode) == "host" || lex_only)) &&
-                           W < (1 << 14) && H < (1 << 14);
+                           W < (1 << 14) && H < (1 << 14) &&
+                           16ll * W + 16ll * H + 16 <= 200 * 1024;  // k_hull's column extremes in shared memory
     if (int(fmesh_.size()) < F) fmesh_.resize(F);
     for (int f = 0; f < F; ++f) {
         fmesh_[f].reset();
