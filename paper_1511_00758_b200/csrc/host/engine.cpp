@@ -670,6 +670,16 @@ ps_status Engine::run_resident(const ps_config& cfg, unsigned flags, ps_observer
             return e ? std::atoi(e) : 1;
         }();
         a.phase2 = phase2;
+        static const int near = [] {
+            const char* e = std::getenv("PS_STAR_NEAR");
+            return e ? std::atoi(e) : 1;
+        }();
+        a.near = near;
+        static const int hull_late = [] {
+            const char* e = std::getenv("PS_STAR_HULL_LATE");
+            return e ? std::atoi(e) : 0;
+        }();
+        a.hull_late = hull_late;
         return a;
     };
     auto enqueue_mesh = [&](FrameGroup& grp, double est, int max_points) {

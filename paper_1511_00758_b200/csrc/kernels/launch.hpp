@@ -148,6 +148,8 @@ struct StarArgs {
     int* hull_tmp;                // per frame 8 * (2 * W + 2 * H + 8) ints: monotone-chain stacks
     int* hard;                    // per frame scap: points pass 1 deferred to pass 2 (count in flags[5])
     int phase2;                   // k_star's own radius-4 phase (1), else such points go to pass 2
+    int hull_late;                // k_star's hull vertices in phase 2 (1) or where pass 1 finds them (0)
+    int near;                     // k_star's radius-2 steps scan the point's near set first (1) or the box rows (0)
     int* ring;                    // per support kRingInts ints: its pass-1 star (count, then the (b, c)
                                   // of each triangle (p, b, c)); count -1: none; nullptr: not kept
 };

@@ -593,6 +593,32 @@ __device__ __forceinline__ void emit_star(const StarArgs& a, int f, int p, const
         }
 }
 
+// a star's outcome: deferred to pass 2 (nt < 0), else its triangles, its
+// ring entry and, for a hull vertex, the hull bookkeeping
+__device__ __noinline__ void finish_star(const StarArgs& a, int f, int p, int pu, int pv, const int* tb, int nt,
+                                         bool closed) {
+    if (nt < 0) {
+        defer_point(a, f, p);
+        return;
+    }
+    emit_star(a, f, p, tb, nt);
+    keep_star(a, f, p, tb, nt);
+    if (closed || nt == 0) return;
+    const long long sb = (long long)f * a.scap;
+    const int* su = a.su + sb;
+    const int* sv = a.sv + sb;
+    const double* sd = a.sd + sb;
+    HullCheck h;
+    for (int j = 0; j < nt; ++j) h.add(su, sv, sd, pu, pv, a.max_disp, p, tb[2 * j], tb[2 * j + 1]);
+    hull_outcome(a, f, p, h, [&](int* out) {
+        for (int j = 0; j < nt; ++j) {
+            out[3 * j] = p;
+            out[3 * j + 1] = tb[2 * j];
+            out[3 * j + 2] = tb[2 * j + 1];
+        }
+    });
+}
+
 // Pass 1, one block per tile of kTileCells^2 cells: the tile's region
 // (star_dt.cuh Tile: the tile plus a kTileHalo-cell halo) is staged in
 // shared memory, then one thread per point of the tile walks its star from
@@ -606,6 +632,7 @@ __global__ void __launch_bounds__(kTileT, 8) k_star(StarArgs a) {
     __shared__ int s_xy[kTileCap], s_id[kTileCap];
     __shared__ int s_warp[kTileT / 32];
     __shared__ int s_list[kTileT], s_nlist;
+    __shared__ int s_near[star::kNearCap * kTileT];  // each thread's near set (star_dt.cuh), strided
     const int f = blockIdx.y;
     const int tw = (a.gw + star::kTileCells - 1) / star::kTileCells;
     const int cx0 = (blockIdx.x % tw) * star::kTileCells - star::kTileHalo;
@@ -700,8 +727,15 @@ __global__ void __launch_bounds__(kTileT, 8) k_star(StarArgs a) {
         const star::TilePoint P = point_at(i);
         int tb[2 * kStarTris];  // (b, c) of each triangle (p, b, c), walk order
         bool closed;
-        const int nt = star::tile_walk(g, T, P, 2, closed, tb, kStarTris);
-        if (nt == -4 || (nt > 0 && !closed)) {
+        star::Near N{s_near + threadIdx.x, kTileT, -1, 0};
+        if (a.near && !star::near_build(g, T, P, N)) N.n = -1;
+        const int nt = star::tile_walk_near(g, T, P, N, closed, tb, kStarTris);
+        if (nt == -4 && a.phase2 == 2) {  // radius 4 right away (PS_STAR_PHASE2=2)
+            const int nt4 = star::tile_walk(g, T, P, 4, closed, tb, kStarTris);
+            finish_star(a, f, P.p, P.pu, P.pv, tb, nt4, closed);
+            continue;
+        }
+        if (nt == -4 || (a.hull_late && nt > 0 && !closed)) {
             // radius 4 / hull bookkeeping: in this block (phase 2, a thread per
             // point) or, PS_STAR_PHASE2=0, in pass 2 (a warp per point)
             if (a.phase2) {
@@ -713,12 +747,7 @@ __global__ void __launch_bounds__(kTileT, 8) k_star(StarArgs a) {
             }
             continue;
         }
-        if (nt < 0) {
-            defer_point(a, f, P.p);
-            continue;
-        }
-        emit_star(a, f, P.p, tb, nt);
-        keep_star(a, f, P.p, tb, nt);
+        finish_star(a, f, P.p, P.pu, P.pv, tb, nt, closed);
     }
     __syncthreads();
     // phase 2: radius 4, hull bookkeeping
@@ -728,27 +757,7 @@ __global__ void __launch_bounds__(kTileT, 8) k_star(StarArgs a) {
         int tb[2 * kStarTris];
         bool closed;
         const int nt = star::tile_walk(g, T, P, 4, closed, tb, kStarTris);
-        if (nt < 0) {
-            defer_point(a, f, P.p);
-            continue;
-        }
-        emit_star(a, f, P.p, tb, nt);
-        keep_star(a, f, P.p, tb, nt);
-        if (closed || nt == 0) continue;
-        const long long sb2 = (long long)f * a.scap;
-        const int* su = a.su + sb2;
-        const int* sv = a.sv + sb2;
-        const double* sd = a.sd + sb2;
-        const int p = P.p;
-        HullCheck h;
-        for (int j = 0; j < nt; ++j) h.add(su, sv, sd, P.pu, P.pv, a.max_disp, p, tb[2 * j], tb[2 * j + 1]);
-        hull_outcome(a, f, p, h, [&](int* out) {
-            for (int j = 0; j < nt; ++j) {
-                out[3 * j] = p;
-                out[3 * j + 1] = tb[2 * j];
-                out[3 * j + 2] = tb[2 * j + 1];
-            }
-        });
+        finish_star(a, f, P.p, P.pu, P.pv, tb, nt, closed);
     }
 }
 

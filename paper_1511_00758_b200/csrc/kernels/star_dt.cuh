@@ -761,6 +761,162 @@ PS_HD int tile_walk(const Grid& g, const Tile& T, const TilePoint& P, int R, boo
     return count;
 }
 
+// ---- pass 1's common case: the near set.  The points of p's radius-2 box
+// at squared distance below t2 <= (2 gs)^2 from p -- all of the set's points
+// that close lie in that box -- are listed once per point (at most
+// kNearCap, packed (x + 128) | (y + 128) << 8 | region index << 16, at
+// list[j * stride]); each step then scans that short list instead of the box
+// rows.  A winner over the list is the winner over the set when the circle
+// through p, q and it has squared diameter below t2: a point beating it lies
+// in (or on) that circle, so within the diameter of p, so in the list.  The
+// certificate is exact integer arithmetic; a step it does not certify falls
+// back to tile_next over the box.
+constexpr int kNearCap = 32;
+
+struct Near {
+    int* list;
+    int stride, n, t2;
+};
+
+// Builds p's near set: t2 the largest of 4, 3, 2, 1 gs^2 whose set fits
+// kNearCap.  False (use the box) when none fits or the offsets would not
+// pack (gs > 60).
+PS_HD bool near_build(const Grid& g, const Tile& T, const TilePoint& P, Near& N) {
+    if (g.gs > 60) return false;
+    const int s2 = g.gs * g.gs;
+    int c1 = 0, c2 = 0, c3 = 0, n = 0;
+    Box box;
+    tile_box(g, T, P, 2, box, [&](int i0, int i1) {
+        for (int i = i0; i < i1; ++i) {
+            const int w = T.xy[i];
+            const int sx = (w & 0xffff) - P.pxr, sy = (w >> 16) - P.pyr;
+            const int d2 = sx * sx + sy * sy;
+            if (d2 == 0 || d2 >= 4 * s2) continue;  // p itself (duplicates are not in the region)
+            c1 += d2 < s2;
+            c2 += d2 < 2 * s2;
+            c3 += d2 < 3 * s2;
+            if (n < kNearCap) N.list[n * N.stride] = (sx + 128) | ((sy + 128) << 8) | (i << 16);
+            ++n;
+        }
+    });
+    if (n <= kNearCap) {
+        N.n = n;
+        N.t2 = 4 * s2;
+        return true;
+    }
+    const int t2 = c3 <= kNearCap ? 3 * s2 : c2 <= kNearCap ? 2 * s2 : c1 <= kNearCap ? s2 : 0;
+    if (t2 == 0) return false;
+    n = 0;
+    tile_box(g, T, P, 2, box, [&](int i0, int i1) {
+        for (int i = i0; i < i1; ++i) {
+            const int w = T.xy[i];
+            const int sx = (w & 0xffff) - P.pxr, sy = (w >> 16) - P.pyr;
+            const int d2 = sx * sx + sy * sy;
+            if (d2 == 0 || d2 >= t2) continue;
+            N.list[n * N.stride] = (sx + 128) | ((sy + 128) << 8) | (i << 16);
+            ++n;
+        }
+    });
+    N.n = n;
+    N.t2 = t2;
+    return true;
+}
+
+// Nearest other point from the near set, certified when closer than sqrt(t2).
+PS_HD int near_nearest(const Tile& T, const Near& N, int& bx, int& by) {
+    int best = -1, bd = 0;
+    for (int j = 0; j < N.n; ++j) {
+        const int w = N.list[j * N.stride];
+        const int sx = (w & 0xff) - 128, sy = ((w >> 8) & 0xff) - 128;
+        const int d2 = sx * sx + sy * sy;
+        if (best >= 0 && d2 > bd) continue;
+        const int id = T.id[w >> 16];
+        if (best >= 0 && d2 == bd && id > best) continue;
+        best = id;
+        bd = d2;
+        bx = sx;
+        by = sy;
+    }
+    return best >= 0 && bd < N.t2 ? best : -3;
+}
+
+// tile_next over the near set: the winner's id, or -1 hull edge, -3 not
+// certified (the caller then searches the box).
+PS_HD int near_next(const Grid& g, const Tile& T, const TilePoint& P, const Near& N, int q, int qx, int qy, int side,
+                    int& bx, int& by) {
+    if (g.flat || (side > 0 ? P.hprev == q : P.hnext == q)) return -1;
+    int bw = -1, bnum = 0, bden = 0;
+    for (int j = 0; j < N.n; ++j) {
+        const int w = N.list[j * N.stride];
+        const int sx = (w & 0xff) - 128, sy = ((w >> 8) & 0xff) - 128;
+        const int den = qx * sy - qy * sx;
+        if (side > 0 ? den <= 0 : den >= 0) continue;
+        const int num = sx * (sx - qx) + sy * (sy - qy);
+        if (bw >= 0) {
+            const long long l = (long long)num * bden, r = (long long)bnum * den;
+            if (l == r) {
+                if (!(side > 0 ? inside_tie_rel(qx, qy, bx, by, sx, sy) : inside_tie_rel(bx, by, qx, qy, sx, sy)))
+                    continue;
+            } else if (side > 0 ? l > r : l < r) {
+                continue;
+            }
+        }
+        bw = w;
+        bnum = num;
+        bden = den;
+        bx = sx;
+        by = sy;
+    }
+    if (bw < 0) return -3;
+    // circle through p (the origin), a and b (counter-clockwise): centre
+    // (nx, ny) / (2 cr), squared diameter (nx^2 + ny^2) / cr^2
+    const long long ax = side > 0 ? qx : bx, ay = side > 0 ? qy : by;
+    const long long cx = side > 0 ? bx : qx, cy = side > 0 ? by : qy;
+    const long long aa = ax * ax + ay * ay, cc = cx * cx + cy * cy, cr = ax * cy - ay * cx;
+    const long long nx = cy * aa - ay * cc, ny = ax * cc - cx * aa;
+    return nx * nx + ny * ny < (long long)N.t2 * cr * cr ? T.id[bw >> 16] : -3;
+}
+
+// tile_walk at radius 2 through the near set (N.n < 0: no near set).
+PS_HD int tile_walk_near(const Grid& g, const Tile& T, const TilePoint& P, const Near& N, bool& closed, int* tb,
+                         int cap) {
+    if (N.n < 0) return tile_walk(g, T, P, 2, closed, tb, cap);
+    closed = false;
+    int qx = 0, qy = 0;
+    int q0 = near_nearest(T, N, qx, qy);
+    if (q0 == -3) q0 = tile_nearest(g, T, P, 2, qx, qy);
+    if (q0 == -3) return -4;
+    if (q0 < 0) return 0;
+    const int q0x = qx, q0y = qy;
+    int count = 0;
+    for (int dir = 0; dir < 2; ++dir) {
+        const int side = dir == 0 ? 1 : -1;
+        int cur = q0, cx = q0x, cy = q0y;
+        for (int guard = 0; guard <= g.n; ++guard) {
+            int rx = 0, ry = 0;
+            int r = near_next(g, T, P, N, cur, cx, cy, side, rx, ry);
+#ifdef PS_NEAR_STATS
+            PS_NEAR_STATS(r == -3);
+#endif
+            if (r == -3) r = tile_next(g, T, P, 2, cur, cx, cy, side, rx, ry);
+            if (r == -3) return -4;
+            if (r < 0) break;
+            if (count == cap) return -5;
+            tb[2 * count] = side > 0 ? cur : r;
+            tb[2 * count + 1] = side > 0 ? r : cur;
+            ++count;
+            if (side > 0 && r == q0) {
+                closed = true;
+                return count;
+            }
+            cur = r;
+            cx = rx;
+            cy = ry;
+        }
+    }
+    return count;
+}
+
 // Walks the star of p and calls on_tri(a, b, c) for each incident triangle,
 // counter-clockwise (a = p).  Returns the triangle count (0: p is not a
 // vertex or the set is collinear around it), -2 if a search failed, or -4

@@ -4,6 +4,8 @@
 //
 //   test_star [--no-local | --tiled] [--synthetic N] [FILE.sup ...]
 // Prints "ok <sets> <triangles>" and exits 0, or the first failures.
+static long long g_near_steps = 0, g_near_miss = 0, g_near_none = 0;
+#define PS_NEAR_STATS(miss) (++g_near_steps, g_near_miss += (miss))
 #include <algorithm>
 #include <array>
 #include <cmath>
@@ -105,7 +107,13 @@ std::vector<std::array<int, 3>> star_triangles(const std::vector<int>& u, const 
                             const star::TilePoint P{p, cx0 + rx, cy0 + ry, rxy[i] & 0xffff, rxy[i] >> 16, u[p], v[p], hp[p], hn[p]};
                             int tb[2 * 16];
                             bool closed;
-                            int k = star::tile_walk(g, T, P, 2, closed, tb, 16);
+                            int nl[star::kNearCap];
+                            star::Near N{nl, 1, -1, 0};
+                            if (!star::near_build(g, T, P, N)) {
+                                N.n = -1;
+                                ++g_near_none;
+                            }
+                            int k = star::tile_walk_near(g, T, P, N, closed, tb, 16);
                             if (k == -4) k = star::tile_walk(g, T, P, 4, closed, tb, 16);
                             if (k >= 0) {
                                 for (int j = 0; j < k; ++j)
@@ -241,6 +249,9 @@ int main(int argc, char** argv) {
         std::printf("%d failures (%lld sets)\n", failures, sets);
         return 1;
     }
+    if (g_near_steps)
+        std::printf("near set: %lld steps, %lld not certified, %lld points without one\n", g_near_steps, g_near_miss,
+                    g_near_none);
     std::printf("ok %lld %lld\n", sets, tris_checked);
     return 0;
 }
