@@ -627,7 +627,10 @@ __device__ __noinline__ void finish_star(const StarArgs& a, int f, int p, int pu
 // star needs a wider search (about 1% at BASELINE config 2's last iteration:
 // next to holes and along the hull) or has more than kStarTris triangles is
 // listed for pass 2.
-__global__ void __launch_bounds__(kTileT, 8) k_star(StarArgs a) {
+#ifndef PS_KSTAR_MINB
+#define PS_KSTAR_MINB 6  // resident blocks per SM (80 registers; 8 / 64: +7% time)
+#endif
+__global__ void __launch_bounds__(kTileT, PS_KSTAR_MINB) k_star(StarArgs a) {
     __shared__ int s_start[kRegionCells + 1];
     __shared__ int s_xy[kTileCap], s_id[kTileCap];
     __shared__ int s_warp[kTileT / 32];
