@@ -132,6 +132,16 @@ static void expand_costs(const uint8_t* __restrict__ in, float* __restrict__ out
 #ifdef __SSE2__
     const __m128 d24 = _mm_set1_ps(float(kCensusBits)), hi = _mm_set1_ps(chigh);
     const __m128i chv = _mm_set1_epi32(ch), zero = _mm_setzero_si128();
+    // scalar head up to a 16-byte boundary of the output, then non-temporal
+    // stores: the map is written once and read by the caller much later, so
+    // the lines need not be fetched for ownership (a quarter less host memory
+    // traffic beside the DMA writes of the other outputs)
+    static const bool nt = [] {  // PS_EXPAND_NT=0: ordinary stores (A/B probe)
+        const char* e = std::getenv("PS_EXPAND_NT");
+        return !e || std::atoi(e) != 0;
+    }();
+    for (; i < n && (reinterpret_cast<uintptr_t>(out + i) & 15u) != 0; ++i)
+        out[i] = int(in[i]) < ch ? float(in[i]) / float(kCensusBits) : chigh;
     for (; i + 16 <= n; i += 16) {
         const __m128i v = _mm_loadu_si128(reinterpret_cast<const __m128i*>(in + i));
         const __m128i lo16 = _mm_unpacklo_epi8(v, zero), hi16 = _mm_unpackhi_epi8(v, zero);
@@ -140,9 +150,14 @@ static void expand_costs(const uint8_t* __restrict__ in, float* __restrict__ out
         for (int k = 0; k < 4; ++k) {
             const __m128 x = _mm_div_ps(_mm_cvtepi32_ps(q[k]), d24);
             const __m128 m = _mm_castsi128_ps(_mm_cmplt_epi32(q[k], chv));
-            _mm_storeu_ps(out + i + 4 * k, _mm_or_ps(_mm_and_ps(m, x), _mm_andnot_ps(m, hi)));
+            const __m128 y = _mm_or_ps(_mm_and_ps(m, x), _mm_andnot_ps(m, hi));
+            if (nt)
+                _mm_stream_ps(out + i + 4 * k, y);
+            else
+                _mm_store_ps(out + i + 4 * k, y);
         }
     }
+    _mm_sfence();
 #endif
     for (; i < n; ++i) out[i] = int(in[i]) < ch ? float(in[i]) / float(kCensusBits) : chigh;
 }
